@@ -1,0 +1,138 @@
+/*
+ * visloc_b200 — C ABI of the B200-native LO-RANSAC PnP hot path.
+ *
+ * Drop-in boundary for the reference package `visloc` (pure Python/numpy,
+ * /root/reference/pkg/src/visloc).  The reference has no native FFI: its
+ * "operator API" is the set of module-level functions listed below, and a
+ * drop-in is installed by rebinding them.  Each entry point
+ * cites the reference function it replaces.
+ *
+ * Conventions
+ *  - Every call returns an int status (VL_OK == 0).  Non-convergence of the
+ *    estimator is NOT an error: it is reported in-band (converged = 0),
+ *    exactly like PoseEstimate.converged (posest.py:278-289).
+ *  - Large arrays are caller-owned DEVICE pointers (C-contiguous, fp64,
+ *    row-major AoS exactly like the reference's numpy arrays: px (n,2),
+ *    X (n,3), w (n)).  Small per-query metadata is passed in host memory.
+ *  - All work is stream-ordered on the caller's cudaStream_t (passed as
+ *    void*); calls that return host-visible scalars synchronise that stream.
+ *  - A context is bound to one device and is not thread-safe; use one
+ *    context per host thread / per GPU (one process per GPU is the model).
+ *  - Workspace is library-owned and grows only in vl_reserve / on the first
+ *    call that needs more; steady-state calls do not allocate.
+ */
+#ifndef VISLOC_B200_H
+#define VISLOC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  VL_OK = 0,
+  VL_ERR_INVALID = 1,          /* bad argument -> ValueError */
+  VL_ERR_CUDA = 2,             /* CUDA runtime error */
+  VL_ERR_OOM = 3,              /* device allocation failed */
+  VL_ERR_UNDERCONSTRAINED = 4, /* n < 3 -> UnderConstrainedError (posest.py:232-234) */
+  VL_ERR_SINGULAR = 5          /* refine with < 3 points (refine.py:185-186) */
+};
+
+typedef struct vl_ctx vl_ctx;
+
+/* Pinhole intrinsics (geometry.py:44-76); width/height are not needed on device. */
+typedef struct { double fx, fy, cx, cy; } vl_intrinsics;
+
+/* numpy PCG64 bit-generator state (numpy 2.3.5 `bit_generator.state`):
+ * 128-bit state and increment split in 64-bit halves + the uint32 buffer. */
+typedef struct {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;
+  uint32_t has_uint32, uinteger;
+} vl_pcg64_state;
+
+/* RansacConfig (posest.py:69-90).  cauchy_scale <= 0 means "None -> tau". */
+typedef struct {
+  int64_t max_iterations;
+  int32_t batch_size;
+  int32_t max_scoring;
+  double miss_probability;
+  double reproj_threshold;
+  double cauchy_scale;
+  int32_t lm_max_iters;
+  int32_t _pad;
+} vl_ransac_config;
+
+/* Batched ransac_pnp (posest.py:223-299): Q independent queries whose
+ * matches are concatenated; query i owns rows [offsets[i], offsets[i+1]). */
+typedef struct {
+  int32_t num_queries;
+  int32_t _pad;
+  const int64_t* offsets;      /* HOST [Q+1] */
+  const vl_intrinsics* intr;   /* HOST [Q] */
+  const vl_pcg64_state* rng;   /* HOST [Q] initial generator state (default_rng(seed)) */
+  const double* px;            /* DEVICE [N,2] query pixels */
+  const double* X;             /* DEVICE [N,3] world points */
+  const double* w;             /* DEVICE [N]  confidence weights (> 0) */
+  vl_ransac_config cfg;
+} vl_ransac_args;
+
+/* PoseEstimate (posest.py:93-103), one row per query; all DEVICE pointers. */
+typedef struct {
+  double* q;                /* [Q,4] scalar-first unit quaternion, w >= 0 */
+  double* t;                /* [Q,3] */
+  uint8_t* inlier_flags;    /* [N]   */
+  int64_t* inlier_count;    /* [Q]   */
+  double* score;            /* [Q]   fp64 MSAC cost of the final pose (inf on failure) */
+  int64_t* iterations;      /* [Q]   minimal samples drawn */
+  int32_t* converged;       /* [Q]   */
+  int64_t* stats;           /* [Q,4] optional (may be NULL): lo_calls, hypotheses, evals, rounds */
+} vl_ransac_out;
+
+/* ---- context ---------------------------------------------------------- */
+int vl_create(int device, vl_ctx** out);
+int vl_destroy(vl_ctx* ctx);
+const char* vl_last_error(vl_ctx* ctx);
+/* Pre-size the workspace (optional). */
+int vl_reserve(vl_ctx* ctx, int32_t max_queries, int64_t max_n_per_query, int32_t batch_size);
+/* Number of kernel launches issued by this context since creation. */
+int64_t vl_launch_count(vl_ctx* ctx);
+
+/* numpy SeedSequence(seed) -> PCG64 state (np.random.default_rng(seed),
+ * posest.py:243).  Host-only helper, no device work. */
+int vl_pcg64_seed(uint64_t seed, vl_pcg64_state* out);
+
+/* ---- hot path ---------------------------------------------------------- */
+/* replaces visloc.posest.ransac_pnp (posest.py:223) — batched over queries */
+int vl_ransac_pnp(vl_ctx* ctx, const vl_ransac_args* args, const vl_ransac_out* out, void* stream);
+
+/* replaces visloc.posest.msac_score (posest.py:160).  pose q[4], t[3] HOST;
+ * arrays DEVICE; cost -> *cost_out (HOST), flags -> DEVICE (may be NULL). */
+int vl_msac_score(vl_ctx* ctx, const double* q, const double* t, const double* px,
+                  const double* X, const double* w, int64_t n, vl_intrinsics intr, double tau,
+                  double* cost_out, uint8_t* flags, void* stream);
+
+/* replaces visloc.refine.refine_pose (refine.py:164).  loss: 0 truncated
+ * (TruncatedLoss(scale)), 1 Cauchy (CauchyLoss(scale)).  q_io/t_io HOST
+ * in/out; trace HOST [max_iters+1] (may be NULL). */
+int vl_refine_pose(vl_ctx* ctx, double* q_io, double* t_io, const double* px, const double* X,
+                   const double* w, int64_t n, vl_intrinsics intr, int32_t loss, double scale,
+                   int32_t max_iters, double gradient_tol, double cost_tol, int32_t* converged,
+                   int32_t* iterations, double* trace, int32_t* trace_len, void* stream);
+
+/* replaces visloc.p3p.p3p_solve_batch (p3p.py:57).  bearings/points DEVICE
+ * [B,3,3]; outputs DEVICE R [4B,3,3], t [4B,3], sample [4B]; *m_out HOST. */
+int vl_p3p_solve_batch(vl_ctx* ctx, const double* bearings, const double* points, int32_t B,
+                       double* R, double* t, int64_t* sample, int32_t* m_out, void* stream);
+
+/* Reproduce numpy's `rng.choice(n, 3, replace=False)` stream on device
+ * (posest.py:252): `count` samples from state `st` (HOST), written to DEVICE
+ * out [count,3] (int32; n < 2^31 on the path); the advanced generator state
+ * is written back to *st (HOST), matching numpy's `bit_generator.state`. */
+int vl_sample_minimal_sets(vl_ctx* ctx, vl_pcg64_state* st, int64_t n, int32_t count,
+                           int32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VISLOC_B200_H */

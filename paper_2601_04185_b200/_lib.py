@@ -1,0 +1,189 @@
+"""ctypes binding of the sm_100a C ABI (include/visloc_b200.h).
+
+The shared library is built in-tree by ``_build.py`` (``__graft_entry__.build``)
+and is the only compute path of this package: there is no CPU fallback.  If
+the library or a CUDA device is missing every hot-path call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libvisloc_b200.so"
+
+VL_OK = 0
+VL_ERR_INVALID = 1
+VL_ERR_CUDA = 2
+VL_ERR_OOM = 3
+VL_ERR_UNDERCONSTRAINED = 4
+VL_ERR_SINGULAR = 5
+
+
+class Intrinsics(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double)]
+
+
+class PCG64State(C.Structure):
+    _fields_ = [("state_hi", C.c_uint64), ("state_lo", C.c_uint64), ("inc_hi", C.c_uint64),
+                ("inc_lo", C.c_uint64), ("has_uint32", C.c_uint32), ("uinteger", C.c_uint32)]
+
+
+class RansacConfigC(C.Structure):
+    _fields_ = [("max_iterations", C.c_int64), ("batch_size", C.c_int32), ("max_scoring", C.c_int32),
+                ("miss_probability", C.c_double), ("reproj_threshold", C.c_double),
+                ("cauchy_scale", C.c_double), ("lm_max_iters", C.c_int32), ("_pad", C.c_int32)]
+
+
+class RansacArgs(C.Structure):
+    _fields_ = [("num_queries", C.c_int32), ("_pad", C.c_int32),
+                ("offsets", C.POINTER(C.c_int64)), ("intr", C.POINTER(Intrinsics)),
+                ("rng", C.POINTER(PCG64State)), ("px", C.c_void_p), ("X", C.c_void_p),
+                ("w", C.c_void_p), ("cfg", RansacConfigC)]
+
+
+class RansacOut(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("t", C.c_void_p), ("inlier_flags", C.c_void_p),
+                ("inlier_count", C.c_void_p), ("score", C.c_void_p), ("iterations", C.c_void_p),
+                ("converged", C.c_void_p), ("stats", C.c_void_p)]
+
+
+class VislocError(RuntimeError):
+    pass
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib():
+    """Load the shared library (once); raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not _LIB_PATH.exists():
+            raise VislocError(
+                f"{_LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a). "
+                "There is no CPU fallback.")
+        L = C.CDLL(str(_LIB_PATH))
+        vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        dp = C.POINTER(C.c_double)
+        ip = C.POINTER(C.c_int32)
+        L.vl_create.argtypes = [C.c_int, C.POINTER(vp)]
+        L.vl_destroy.argtypes = [vp]
+        L.vl_last_error.argtypes = [vp]
+        L.vl_last_error.restype = C.c_char_p
+        L.vl_launch_count.argtypes = [vp]
+        L.vl_launch_count.restype = i64
+        L.vl_reserve.argtypes = [vp, i32, i64, i32]
+        L.vl_pcg64_seed.argtypes = [C.c_uint64, C.POINTER(PCG64State)]
+        L.vl_ransac_pnp.argtypes = [vp, C.POINTER(RansacArgs), C.POINTER(RansacOut), vp]
+        L.vl_msac_score.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, dbl, dp, vp, vp]
+        L.vl_refine_pose.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, i32, dbl, i32, dbl, dbl,
+                                     ip, ip, dp, ip, vp]
+        L.vl_p3p_solve_batch.argtypes = [vp, vp, vp, i32, vp, vp, vp, ip, vp]
+        L.vl_sample_minimal_sets.argtypes = [vp, C.POINTER(PCG64State), i64, i32, vp, vp]
+        for name in ("vl_create", "vl_destroy", "vl_reserve", "vl_pcg64_seed", "vl_ransac_pnp",
+                     "vl_msac_score", "vl_refine_pose", "vl_p3p_solve_batch", "vl_sample_minimal_sets"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+        return L
+
+
+EXPORTED_SYMBOLS = (
+    "vl_create", "vl_destroy", "vl_last_error", "vl_reserve", "vl_launch_count", "vl_pcg64_seed",
+    "vl_ransac_pnp", "vl_msac_score", "vl_refine_pose", "vl_p3p_solve_batch",
+    "vl_sample_minimal_sets",
+)
+
+
+class Context:
+    """One C-ABI context per CUDA device (workspace lives here)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.handle = C.c_void_p()
+        rc = lib().vl_create(device, C.byref(self.handle))
+        if rc != VL_OK:
+            raise VislocError(f"vl_create(device={device}) failed with status {rc} "
+                              "(a B200 / sm_100 GPU is required)")
+
+    def check(self, rc: int, what: str):
+        if rc == VL_OK:
+            return
+        msg = lib().vl_last_error(self.handle).decode(errors="replace")
+        if rc == VL_ERR_INVALID:
+            raise ValueError(f"{what}: {msg}")
+        if rc == VL_ERR_UNDERCONSTRAINED:
+            from .posest import UnderConstrainedError
+            raise UnderConstrainedError(msg)
+        if rc == VL_ERR_SINGULAR:
+            raise ValueError(msg)
+        raise VislocError(f"{what} failed ({rc}): {msg}")
+
+    def launches(self) -> int:
+        return int(lib().vl_launch_count(self.handle))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().vl_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_contexts: dict[int, Context] = {}
+
+
+def context(device: int | None = None) -> Context:
+    import torch
+    if not torch.cuda.is_available():
+        raise VislocError("CUDA device not available: the visloc_b200 hot path runs only on the GPU")
+    if device is None:
+        device = torch.cuda.current_device()
+    ctx = _contexts.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        _contexts[device] = ctx
+    return ctx
+
+
+def pcg64_state(seed: int) -> PCG64State:
+    """numpy ``default_rng(seed)`` generator state (C implementation for 0 <= seed < 2^64)."""
+    st = PCG64State()
+    if 0 <= int(seed) < 2 ** 64:
+        rc = lib().vl_pcg64_seed(C.c_uint64(int(seed)), C.byref(st))
+        if rc != VL_OK:
+            raise ValueError(f"bad seed {seed}")
+        return st
+    # arbitrary-precision seeds: numpy's own SeedSequence (host-side seeding only)
+    s = np.random.PCG64(int(seed)).state
+    return state_from_numpy(s)
+
+
+def state_from_numpy(s: dict) -> PCG64State:
+    st = PCG64State()
+    v, inc = int(s["state"]["state"]), int(s["state"]["inc"])
+    m64 = (1 << 64) - 1
+    st.state_hi, st.state_lo = v >> 64, v & m64
+    st.inc_hi, st.inc_lo = inc >> 64, inc & m64
+    st.has_uint32 = int(s["has_uint32"])
+    st.uinteger = int(s["uinteger"])
+    return st
+
+
+def state_to_dict(st: PCG64State) -> dict:
+    return {"state": (int(st.state_hi) << 64) | int(st.state_lo),
+            "inc": (int(st.inc_hi) << 64) | int(st.inc_lo),
+            "has_uint32": int(st.has_uint32), "uinteger": int(st.uinteger)}
+
+
+def stream_ptr():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)

@@ -1,0 +1,432 @@
+// C ABI (include/visloc_b200.h): context, workspace, and the host-side round
+// loop of the batched estimator.  No CPU compute fallback exists: every
+// entry point either launches sm_100a kernels or fails with a status code.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/visloc_b200.h"
+#include "vl_internal.h"
+
+using namespace vl;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct vl_ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+  int64_t launches = 0;
+  DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, P32, hsrc, items, item_count,
+      partial, sub_px, sub_X, sub_w, sub32, comp_px, comp_X, comp_w;
+  DevBuf scratch;  // small standalone-call scratch
+  void* h_pinned = nullptr;
+  size_t h_pinned_cap = 0;
+};
+
+static int fail(vl_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define VL_CUDA(ctx, expr)                                                                   \
+  do {                                                                                       \
+    cudaError_t e__ = (expr);                                                                \
+    if (e__ != cudaSuccess)                                                                  \
+      return fail(ctx, e__ == cudaErrorMemoryAllocation ? VL_ERR_OOM : VL_ERR_CUDA,          \
+                  std::string(#expr) + ": " + cudaGetErrorString(e__));                     \
+  } while (0)
+
+static int ensure(vl_ctx* c, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return VL_OK;
+  if (b.p) {
+    cudaError_t e = cudaFree(b.p);
+    if (e != cudaSuccess) return fail(c, VL_ERR_CUDA, std::string("cudaFree: ") + cudaGetErrorString(e));
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  size_t nb = bytes + bytes / 8;
+  cudaError_t e = cudaMalloc(&b.p, nb);
+  if (e != cudaSuccess) {
+    b.p = nullptr;
+    return fail(c, VL_ERR_OOM, "cudaMalloc(" + std::to_string(nb) + "): " + cudaGetErrorString(e));
+  }
+  b.cap = nb;
+  return VL_OK;
+}
+
+static int ensure_host(vl_ctx* c, size_t bytes) {
+  if (c->h_pinned_cap >= bytes) return VL_OK;
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  c->h_pinned = nullptr;
+  c->h_pinned_cap = 0;
+  cudaError_t e = cudaMallocHost(&c->h_pinned, bytes);
+  if (e != cudaSuccess) return fail(c, VL_ERR_OOM, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
+  c->h_pinned_cap = bytes;
+  return VL_OK;
+}
+
+static int check_launch(vl_ctx* c) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, VL_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return VL_OK;
+}
+
+static GenState gen_from(const vl_pcg64_state& s) {
+  GenState g;
+  g.state = ((u128)s.state_hi << 64) | s.state_lo;
+  g.inc = ((u128)s.inc_hi << 64) | s.inc_lo;
+  g.has0 = s.has_uint32;
+  g.uint0 = s.uinteger;
+  return g;
+}
+
+static vl_pcg64_state state_from(const GenState& g) {
+  vl_pcg64_state s;
+  s.state_hi = (uint64_t)(g.state >> 64);
+  s.state_lo = (uint64_t)g.state;
+  s.inc_hi = (uint64_t)(g.inc >> 64);
+  s.inc_lo = (uint64_t)g.inc;
+  s.has_uint32 = g.has0;
+  s.uinteger = g.uint0;
+  return s;
+}
+
+// Generator state after `pos` 32-bit words were consumed (numpy semantics,
+// including the stale `uinteger` value numpy reports).
+static GenState advance_words(const GenState& g, uint64_t pos) {
+  if (pos == 0) return g;
+  GenState r = g;
+  uint64_t k = pos;
+  if (g.has0) k -= 1;  // the buffered word
+  const uint64_t m = k >> 1;
+  if ((k & 1) == 0) {
+    r.state = pcg_advance(g.state, g.inc, m);
+    r.has0 = 0;
+    if (m > 0) r.uint0 = (uint32_t)(pcg_out(r.state) >> 32);
+  } else {
+    r.state = pcg_advance(g.state, g.inc, m + 1);
+    r.has0 = 1;
+    r.uint0 = (uint32_t)(pcg_out(r.state) >> 32);
+  }
+  return r;
+}
+
+extern "C" {
+
+int vl_create(int device, vl_ctx** out) {
+  if (!out) return VL_ERR_INVALID;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return VL_ERR_CUDA;
+  if (device < 0 || device >= ndev) return VL_ERR_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return VL_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return VL_ERR_CUDA;
+  if (prop.major != 10) return VL_ERR_CUDA;  // sm_100a build only
+  vl_ctx* c = new vl_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  *out = c;
+  return VL_OK;
+}
+
+int vl_destroy(vl_ctx* c) {
+  if (!c) return VL_OK;
+  cudaSetDevice(c->device);
+  DevBuf* bufs[] = {&c->qs,      &c->active, &c->next_active, &c->active_count, &c->samples, &c->slots,
+                    &c->slot_cnt, &c->P32,   &c->hsrc,        &c->items,        &c->item_count,
+                    &c->partial, &c->sub_px, &c->sub_X,       &c->sub_w,        &c->sub32,   &c->comp_px,
+                    &c->comp_X,  &c->comp_w, &c->scratch};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  delete c;
+  return VL_OK;
+}
+
+const char* vl_last_error(vl_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t vl_launch_count(vl_ctx* c) { return c ? c->launches : -1; }
+
+int vl_pcg64_seed(uint64_t seed, vl_pcg64_state* out) {
+  if (!out) return VL_ERR_INVALID;
+  *out = state_from(seed_pcg64(seed));
+  return VL_OK;
+}
+
+int vl_reserve(vl_ctx* c, int32_t max_queries, int64_t max_n_per_query, int32_t batch_size) {
+  if (!c || max_queries <= 0 || max_n_per_query < 3 || batch_size <= 0) return VL_ERR_INVALID;
+  cudaSetDevice(c->device);
+  const int64_t Qc = max_queries, B = batch_size, H = 4 * B;
+  const int64_t nsub = std::min<int64_t>(max_n_per_query, 10000);
+  const int64_t ns = (nsub + kScoreChunk - 1) / kScoreChunk;
+  int rc = VL_OK;
+  rc |= ensure(c, c->samples, Qc * B * 3 * sizeof(int));
+  rc |= ensure(c, c->slots, Qc * B * 48 * sizeof(double));
+  rc |= ensure(c, c->slot_cnt, Qc * B * sizeof(int));
+  rc |= ensure(c, c->P32, Qc * 12 * H * sizeof(float));
+  rc |= ensure(c, c->hsrc, Qc * H * sizeof(int));
+  rc |= ensure(c, c->partial, Qc * ns * H * sizeof(float));
+  return rc ? VL_ERR_OOM : VL_OK;
+}
+
+int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, void* stream) {
+  if (!c || !a || !o) return fail(c, VL_ERR_INVALID, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const vl_ransac_config& cfg = a->cfg;
+  if (!(cfg.reproj_threshold > 0)) return fail(c, VL_ERR_INVALID, "reproj_threshold must be positive");
+  if (!(cfg.miss_probability > 0 && cfg.miss_probability < 1))
+    return fail(c, VL_ERR_INVALID, "miss_probability must be in (0, 1)");
+  if (cfg.batch_size <= 0 || cfg.batch_size > cfg.max_iterations)
+    return fail(c, VL_ERR_INVALID, "batch_size must be in [1, max_iterations]");
+  if (cfg.max_scoring <= 0 || cfg.lm_max_iters < 0) return fail(c, VL_ERR_INVALID, "bad config");
+  const double cauchy = cfg.cauchy_scale > 0 ? cfg.cauchy_scale : cfg.reproj_threshold;
+  const int Q = a->num_queries;
+  if (Q <= 0) return fail(c, VL_ERR_INVALID, "num_queries must be positive");
+  if (!a->offsets || !a->intr || !a->rng || !a->px || !a->X || !a->w)
+    return fail(c, VL_ERR_INVALID, "null input array");
+  for (int q = 0; q < Q; ++q) {
+    const int64_t n = a->offsets[q + 1] - a->offsets[q];
+    if (n < 3) return fail(c, VL_ERR_UNDERCONSTRAINED, "need >= 3 matches, got " + std::to_string(n));
+    if (n > 0x7FFFFFFF) return fail(c, VL_ERR_INVALID, "more than 2^31-1 matches in one query");
+  }
+  VL_CUDA(c, cudaSetDevice(c->device));
+  RansacParams p;
+  p.max_iterations = cfg.max_iterations;
+  p.batch_size = cfg.batch_size;
+  p.lm_max_iters = cfg.lm_max_iters;
+  p.eta = cfg.miss_probability;
+  p.tau = cfg.reproj_threshold;
+  p.cauchy = cauchy;
+  const int64_t B = cfg.batch_size;
+  const int64_t HCAP = 4 * B;
+  // chunk the query set so the per-round workspace stays bounded (~6 GB)
+  const int64_t per_q = B * (3 * 4 + 48 * 8 + 4) + HCAP * (12 * 4 + 4) + HCAP * 4 * 20;
+  int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, (int64_t)6e9 / per_q));
+  Qc = std::min<int64_t>(Qc, 4096);
+  Inputs in{a->px, a->X, a->w};
+  Outputs out{o->q, o->t, o->inlier_flags, o->inlier_count, o->score, o->iterations, o->converged, o->stats};
+  std::vector<QState> hq;
+  for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
+    const int Qn = (int)std::min<int64_t>(Qc, Q - q0);
+    hq.assign(Qn, QState());
+    int64_t nsub_tot = 0, ncomp = 0;
+    int max_split = 1;
+    for (int i = 0; i < Qn; ++i) {
+      const int64_t gq = q0 + i;
+      QState& S = hq[i];
+      std::memset(&S, 0, sizeof(QState));
+      const int64_t n = a->offsets[gq + 1] - a->offsets[gq];
+      S.gen = gen_from(a->rng[gq]);
+      S.off = a->offsets[gq];
+      S.coff = ncomp;
+      S.n = (int)n;
+      S.stride = (int)((n + cfg.max_scoring - 1) / cfg.max_scoring);
+      S.nsub = (int)((n + S.stride - 1) / S.stride);
+      S.nsplit = (S.nsub + kScoreChunk - 1) / kScoreChunk;
+      S.sub_off = nsub_tot;
+      S.in = Intr{a->intr[gq].fx, a->intr[gq].fy, a->intr[gq].cx, a->intr[gq].cy};
+      S.active = 1;
+      S.best_cost = INFINITY;
+      S.best.q[0] = 1.0;
+      nsub_tot += S.nsub;
+      ncomp += n;
+      max_split = std::max(max_split, S.nsplit);
+    }
+    const int64_t ntile = (HCAP + kScoreTileHyps - 1) / kScoreTileHyps;
+    const int64_t item_cap = (int64_t)Qn * ntile * max_split;
+    int rc = VL_OK;
+    if ((rc = ensure(c, c->qs, Qn * sizeof(QState))) ||
+        (rc = ensure(c, c->active, Qn * sizeof(int))) ||
+        (rc = ensure(c, c->active_count, 2 * sizeof(int))) ||
+        (rc = ensure(c, c->samples, Qn * B * 3 * sizeof(int))) ||
+        (rc = ensure(c, c->slots, Qn * B * 48 * sizeof(double))) ||
+        (rc = ensure(c, c->slot_cnt, Qn * B * sizeof(int))) ||
+        (rc = ensure(c, c->P32, Qn * 12 * HCAP * sizeof(float))) ||
+        (rc = ensure(c, c->hsrc, Qn * HCAP * sizeof(int))) ||
+        (rc = ensure(c, c->items, item_cap * sizeof(ScoreItem))) ||
+        (rc = ensure(c, c->item_count, 2 * sizeof(int))) ||
+        (rc = ensure(c, c->partial, (size_t)Qn * max_split * HCAP * sizeof(float))) ||
+        (rc = ensure(c, c->sub_px, nsub_tot * 2 * sizeof(double))) ||
+        (rc = ensure(c, c->sub_X, nsub_tot * 3 * sizeof(double))) ||
+        (rc = ensure(c, c->sub_w, nsub_tot * sizeof(double))) ||
+        (rc = ensure(c, c->sub32, nsub_tot * 2 * sizeof(float4))) ||
+        (rc = ensure(c, c->comp_px, ncomp * 2 * sizeof(double))) ||
+        (rc = ensure(c, c->comp_X, ncomp * 3 * sizeof(double))) ||
+        (rc = ensure(c, c->comp_w, ncomp * sizeof(double))))
+      return rc;
+    const size_t host_bytes = Qn * sizeof(QState) + Qn * sizeof(int) + 64;
+    if ((rc = ensure_host(c, host_bytes))) return rc;
+    char* hp = (char*)c->h_pinned;
+    QState* h_qs = (QState*)hp;
+    int* h_active = (int*)(hp + Qn * sizeof(QState));
+    int* h_count = (int*)(hp + Qn * sizeof(QState) + Qn * sizeof(int));
+    // the pinned staging buffer is reused across chunks: previous copies finished at the last sync
+    std::memcpy(h_qs, hq.data(), Qn * sizeof(QState));
+    for (int i = 0; i < Qn; ++i) h_active[i] = i;
+    Work wk;
+    wk.qs = (QState*)c->qs.p;
+    wk.active_list = (int*)c->active.p;
+    wk.active_count = (int*)c->active_count.p;
+    wk.next_active = nullptr;
+    wk.samples = (int*)c->samples.p;
+    wk.slots = (double*)c->slots.p;
+    wk.slot_cnt = (int*)c->slot_cnt.p;
+    wk.P32 = (float*)c->P32.p;
+    wk.hsrc = (int*)c->hsrc.p;
+    wk.items = (ScoreItem*)c->items.p;
+    wk.item_count = (int*)c->item_count.p;
+    wk.partial = (float*)c->partial.p;
+    wk.sub_px = (double*)c->sub_px.p;
+    wk.sub_X = (double*)c->sub_X.p;
+    wk.sub_w = (double*)c->sub_w.p;
+    wk.sub32 = (float4*)c->sub32.p;
+    wk.comp_px = (double*)c->comp_px.p;
+    wk.comp_X = (double*)c->comp_X.p;
+    wk.comp_w = (double*)c->comp_w.p;
+    wk.B = (int)B;
+    wk.HCAP = (int)HCAP;
+    wk.NSPLIT = max_split;
+    wk.item_cap = item_cap;
+    VL_CUDA(c, cudaMemcpyAsync(wk.qs, h_qs, Qn * sizeof(QState), cudaMemcpyHostToDevice, st));
+    VL_CUDA(c, cudaMemcpyAsync(wk.active_list, h_active, Qn * sizeof(int), cudaMemcpyHostToDevice, st));
+    VL_CUDA(c, cudaMemsetAsync(wk.item_count, 0, sizeof(int), st));
+    c->launches += launch_prep(wk, in, Qn, st);
+    if ((rc = check_launch(c))) return rc;
+    int nactive = Qn;
+    int guard = 0;
+    const int64_t max_rounds = (cfg.max_iterations + B - 1) / B + 1;
+    while (nactive > 0) {
+      c->launches += launch_round(wk, in, p, nactive, c->num_sms, st);
+      if ((rc = check_launch(c))) return rc;
+      VL_CUDA(c, cudaMemcpyAsync(h_count, wk.active_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+      VL_CUDA(c, cudaStreamSynchronize(st));
+      nactive = *h_count;
+      if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
+    }
+    c->launches += launch_final(wk, in, out, p, Qn, (int)q0, st);
+    if ((rc = check_launch(c))) return rc;
+    if (q0 + Qc < Q) VL_CUDA(c, cudaStreamSynchronize(st));  // staging buffer reuse
+  }
+  return VL_OK;
+}
+
+static Pose pose_from_host(const double* q, const double* t) {
+  Pose p;
+  for (int i = 0; i < 4; ++i) p.q[i] = q[i];
+  for (int i = 0; i < 3; ++i) p.t[i] = t[i];
+  return p;
+}
+
+int vl_msac_score(vl_ctx* c, const double* q, const double* t, const double* px, const double* X,
+                  const double* w, int64_t n, vl_intrinsics intr, double tau, double* cost_out,
+                  uint8_t* flags, void* stream) {
+  if (!c || !q || !t || !cost_out || n < 0) return fail(c, VL_ERR_INVALID, "bad argument");
+  if (n > 0x7FFFFFFF) return fail(c, VL_ERR_INVALID, "n too large");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if ((rc = ensure(c, c->scratch, 4096))) return rc;
+  if ((rc = ensure_host(c, 4096))) return rc;
+  double* dred = (double*)c->scratch.p;
+  c->launches += launch_msac(pose_from_host(q, t), px, X, w, (int)n, Intr{intr.fx, intr.fy, intr.cx, intr.cy},
+                             tau, dred, flags, st);
+  if ((rc = check_launch(c))) return rc;
+  double* h = (double*)c->h_pinned;
+  VL_CUDA(c, cudaMemcpyAsync(h, dred, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  VL_CUDA(c, cudaStreamSynchronize(st));
+  *cost_out = h[0];
+  return VL_OK;
+}
+
+int vl_refine_pose(vl_ctx* c, double* q_io, double* t_io, const double* px, const double* X, const double* w,
+                   int64_t n, vl_intrinsics intr, int32_t loss, double scale, int32_t max_iters,
+                   double gradient_tol, double cost_tol, int32_t* converged, int32_t* iterations,
+                   double* trace, int32_t* trace_len, void* stream) {
+  if (!c || !q_io || !t_io || max_iters < 0 || (loss != 0 && loss != 1))
+    return fail(c, VL_ERR_INVALID, "bad argument");
+  if (!(scale > 0)) return fail(c, VL_ERR_INVALID, "scale must be positive");
+  if (n < 3) return fail(c, VL_ERR_SINGULAR, "refinement needs >= 3 matches, got " + std::to_string(n));
+  if (n > 0x7FFFFFFF) return fail(c, VL_ERR_INVALID, "n too large");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t trace_bytes = (size_t)(max_iters + 1) * sizeof(double);
+  const size_t need = 256 + trace_bytes;
+  int rc;
+  if ((rc = ensure(c, c->scratch, need))) return rc;
+  if ((rc = ensure_host(c, need))) return rc;
+  char* base = (char*)c->scratch.p;
+  Pose* dpose = (Pose*)base;
+  int* dinfo = (int*)(base + 128);
+  double* dtrace = (double*)(base + 256);
+  c->launches += launch_refine(pose_from_host(q_io, t_io), px, X, w, (int)n,
+                               Intr{intr.fx, intr.fy, intr.cx, intr.cy}, loss, scale, max_iters, gradient_tol,
+                               cost_tol, dpose, dinfo, dtrace, st);
+  if ((rc = check_launch(c))) return rc;
+  char* h = (char*)c->h_pinned;
+  VL_CUDA(c, cudaMemcpyAsync(h, base, need, cudaMemcpyDeviceToHost, st));
+  VL_CUDA(c, cudaStreamSynchronize(st));
+  const Pose* hp = (const Pose*)h;
+  const int* hi = (const int*)(h + 128);
+  for (int i = 0; i < 4; ++i) q_io[i] = hp->q[i];
+  for (int i = 0; i < 3; ++i) t_io[i] = hp->t[i];
+  if (converged) *converged = hi[0];
+  if (iterations) *iterations = hi[1];
+  if (trace_len) *trace_len = hi[2];
+  if (trace) std::memcpy(trace, h + 256, (size_t)hi[2] * sizeof(double));
+  return VL_OK;
+}
+
+int vl_p3p_solve_batch(vl_ctx* c, const double* bearings, const double* points, int32_t B, double* R,
+                       double* t, int64_t* sample, int32_t* m_out, void* stream) {
+  if (!c || B < 0 || !m_out) return fail(c, VL_ERR_INVALID, "bad argument");
+  *m_out = 0;
+  if (B == 0) return VL_OK;
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if ((rc = ensure(c, c->slots, (size_t)B * 48 * sizeof(double)))) return rc;
+  if ((rc = ensure(c, c->slot_cnt, (size_t)B * sizeof(int) + 16))) return rc;
+  if ((rc = ensure_host(c, 64))) return rc;
+  int* dm = (int*)c->slot_cnt.p + B;
+  c->launches += launch_p3p_batch(bearings, points, B, (double*)c->slots.p, (int*)c->slot_cnt.p, R, t, sample,
+                                  dm, st);
+  if ((rc = check_launch(c))) return rc;
+  int* h = (int*)c->h_pinned;
+  VL_CUDA(c, cudaMemcpyAsync(h, dm, sizeof(int), cudaMemcpyDeviceToHost, st));
+  VL_CUDA(c, cudaStreamSynchronize(st));
+  *m_out = *h;
+  return VL_OK;
+}
+
+int vl_sample_minimal_sets(vl_ctx* c, vl_pcg64_state* stt, int64_t n, int32_t count, int32_t* out,
+                           void* stream) {
+  if (!c || !stt || count < 0) return fail(c, VL_ERR_INVALID, "bad argument");
+  if (n < 3 || n > 0xFFFFFFFFll) return fail(c, VL_ERR_INVALID, "population must be in [3, 2^32)");
+  if (count == 0) return VL_OK;
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if ((rc = ensure(c, c->scratch, 64))) return rc;
+  if ((rc = ensure_host(c, 64))) return rc;
+  const GenState g = gen_from(*stt);
+  uint64_t* dpos = (uint64_t*)c->scratch.p;
+  c->launches += launch_sample(g, 0, n, count, out, dpos, st);
+  if ((rc = check_launch(c))) return rc;
+  uint64_t* h = (uint64_t*)c->h_pinned;
+  VL_CUDA(c, cudaMemcpyAsync(h, dpos, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  VL_CUDA(c, cudaStreamSynchronize(st));
+  *stt = state_from(advance_words(g, *h));
+  return VL_OK;
+}
+
+}  // extern "C"

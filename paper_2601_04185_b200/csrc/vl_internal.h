@@ -1,0 +1,108 @@
+// Internal declarations shared by the kernel translation units and the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "vl_common.cuh"
+#include "vl_rng.cuh"
+
+namespace vl {
+
+// Scoring tile geometry (vl_score.cu).
+constexpr int kScoreThreads = 128;
+constexpr int kScoreHypPerThread = 4;
+constexpr int kScoreTileHyps = kScoreThreads * kScoreHypPerThread;  // 512
+constexpr int kScoreChunk = 512;  // correspondences per split (fixed => launch-independent sums)
+
+// Per-query device state of the batched estimator.
+struct __align__(16) QState {
+  GenState gen;        // initial generator state
+  int64_t off;         // first row in px/X/w (absolute)
+  int64_t coff;        // first row in the chunk-relative compaction buffer
+  int64_t sub_off;     // first row in the scoring-subset arrays
+  int n, nsub, stride, nsplit;
+  Intr in;
+  // dynamic
+  uint64_t rng_pos;    // uint32 words consumed so far
+  int64_t iters;       // minimal samples drawn
+  int batch_n;         // samples in the current round
+  int active;
+  int has_best;
+  int nh;              // hypotheses in the current round
+  double best_cost;
+  Pose best;
+  int64_t lo_calls, hyps, evals, rounds;
+};
+
+struct ScoreItem {
+  int q, tile, split, pad;
+};
+
+struct RansacParams {
+  int64_t max_iterations;
+  int batch_size;
+  int lm_max_iters;
+  double eta;
+  double tau;
+  double cauchy;
+};
+
+// Device workspace view for one chunk of queries.
+struct Work {
+  QState* qs;
+  int* active_list;
+  int* active_count;     // device scalar
+  int* next_active;      // [Qc]
+  int* samples;          // [Qc][B][3]
+  double* slots;         // [Qc][B][4][12]
+  int* slot_cnt;         // [Qc][B]
+  float* P32;            // [Qc][12][HCAP]
+  int* hsrc;             // [Qc][HCAP]
+  ScoreItem* items;      // [item_cap]
+  int* item_count;       // device scalar
+  float* partial;        // [Qc][NSPLIT][HCAP]
+  double* sub_px;        // [Nsub][2]
+  double* sub_X;         // [Nsub][3]
+  double* sub_w;         // [Nsub]
+  float4* sub32;         // [Nsub][2]
+  double* comp_px;       // [N][2]
+  double* comp_X;        // [N][3]
+  double* comp_w;        // [N]
+  int B, HCAP, NSPLIT;
+  int64_t item_cap;
+};
+
+struct Inputs {
+  const double* px;
+  const double* X;
+  const double* w;
+};
+
+struct Outputs {
+  double* q;
+  double* t;
+  uint8_t* flags;
+  int64_t* inlier_count;
+  double* score;
+  int64_t* iterations;
+  int32_t* converged;
+  int64_t* stats;
+};
+
+// ---- launchers (return number of kernels launched) -------------------------
+int launch_prep(const Work& wk, const Inputs& in, int Q, cudaStream_t st);
+int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
+                 cudaStream_t st);
+int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
+                 int q_base, cudaStream_t st);
+
+int launch_msac(const Pose& pose, const double* px, const double* X, const double* w, int n, Intr in,
+                double tau, double* red_out, uint8_t* flags, cudaStream_t st);
+int launch_refine(const Pose& start, const double* px, const double* X, const double* w, int n, Intr in,
+                  int kind, double scale, int max_iters, double gtol, double ctol, Pose* pose_out,
+                  int* info_out, double* trace, cudaStream_t st);
+int launch_p3p_batch(const double* f, const double* P, int B, double* slots, int* cnt, double* R_out,
+                     double* t_out, int64_t* idx_out, int* m_out, cudaStream_t st);
+int launch_sample(const GenState& g, uint64_t pos0, int64_t n, int count, int* out, uint64_t* pos_out,
+                  cudaStream_t st);
+
+}  // namespace vl

@@ -1,0 +1,314 @@
+// CTA-cooperative fp64 passes over a point set: MSAC classification and the
+// Levenberg-Marquardt / IRLS pose refinement.
+//
+//  * msac_pass  == posest._errors_sq + msac_score (posest.py:137-175): fp64,
+//    behind-camera -> +inf error, cost sum w min(e2, tau^2), flags e2 < tau^2.
+//    The per-point arithmetic is issued without FMA contraction in the
+//    reference's operation order so flags agree bit-for-bit away from ties.
+//  * lm_refine  == refine.refine_pose (refine.py:164-230) with TruncatedLoss
+//    or CauchyLoss (:43-77), residuals (:90-100), analytic Jacobian
+//    (:103-132), robust cost (:135-149), apply_delta (:80-87), and the exact
+//    damping schedule.  One fused pass evaluates cost + gradient + the 21
+//    unique entries of J^T W J at every candidate, so an accepted step
+//    already carries the next iteration's normal equations (the reference
+//    recomputes them at the same pose, so the values are identical).
+//  Reductions are deterministic (fixed warp-shuffle tree + ordered warp sum).
+#pragma once
+#include "vl_common.cuh"
+
+namespace vl {
+
+enum LossKind { kTruncated = 0, kCauchy = 1 };
+constexpr int kRed = 28;  // cost, g[6], H upper triangle [21]
+
+template <int NT>
+struct LMShared {
+  double R[9], t[3];
+  Pose cur, cand;
+  double red[kRed];
+  double scratch[(NT / 32) * kRed];
+  int flag;
+  int ibuf[NT / 32];
+};
+
+// Load rotation matrix + translation of `p` into shared memory (thread 0).
+template <int NT>
+__device__ __forceinline__ void set_eval_pose(LMShared<NT>& sm, const Pose& p) {
+  if (threadIdx.x == 0) {
+    q2R(p.q, sm.R);
+    sm.t[0] = p.t[0];
+    sm.t[1] = p.t[1];
+    sm.t[2] = p.t[2];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void cam_point(const double* R, const double* t, const double* X,
+                                          double& x, double& y, double& z) {
+  // X @ R.T + t, no contraction
+  x = dadd(dadd(dadd(dmul(X[0], R[0]), dmul(X[1], R[1])), dmul(X[2], R[2])), t[0]);
+  y = dadd(dadd(dadd(dmul(X[0], R[3]), dmul(X[1], R[4])), dmul(X[2], R[5])), t[1]);
+  z = dadd(dadd(dadd(dmul(X[0], R[6]), dmul(X[1], R[7])), dmul(X[2], R[8])), t[2]);
+}
+
+// MSAC pass with the pose currently in sm.R / sm.t.  Writes flags (if not
+// null), returns cost and inlier count in sm.red[0], sm.red[1].
+template <int NT>
+__device__ void msac_pass(LMShared<NT>& sm, const PointSet& ps, const Intr& in, double tau,
+                          uint8_t* flags) {
+  const double t2 = dmul(tau, tau);
+  double acc[2] = {0.0, 0.0};
+  for (int i = threadIdx.x; i < ps.n; i += NT) {
+    const double X[3] = {ps.X[3 * i], ps.X[3 * i + 1], ps.X[3 * i + 2]};
+    double x, y, z;
+    cam_point(sm.R, sm.t, X, x, y, z);
+    const bool front = z > 0;
+    const double zs = front ? z : 1.0;
+    double du = dmul(in.fx, x);
+    du = __ddiv_rn(du, zs);
+    du = dadd(du, dsub(in.cx, ps.px[2 * i]));
+    double dv = dmul(in.fy, y);
+    dv = __ddiv_rn(dv, zs);
+    dv = dadd(dv, dsub(in.cy, ps.px[2 * i + 1]));
+    double e2 = dmul(du, du);
+    e2 = dadd(e2, dmul(dv, dv));
+    if (!front) e2 = CUDART_INF;
+    acc[0] = acc[0] + dmul(ps.w[i], fmin(e2, t2));
+    const bool inl = e2 < t2;
+    acc[1] += inl ? 1.0 : 0.0;
+    if (flags) flags[i] = inl ? 1 : 0;
+  }
+  double* out = sm.red;
+  block_sum<NT, 2>(acc, sm.scratch, out);
+}
+
+// Fused robust-cost (+ gradient + normal matrix) pass at the pose in sm.R/t.
+// Result: sm.red[0] = cost (inf for Cauchy with a point behind the camera),
+// sm.red[1..6] = g (without the factor 2), sm.red[7..27] = H upper (no 2).
+template <int NT, bool GRAD>
+__device__ void lm_pass(LMShared<NT>& sm, const PointSet& ps, const Intr& in, int kind,
+                        double scale) {
+  const double s2 = dmul(scale, scale);
+  double acc[kRed];
+#pragma unroll
+  for (int k = 0; k < kRed; ++k) acc[k] = 0.0;
+  double behind = 0.0;
+  for (int i = threadIdx.x; i < ps.n; i += NT) {
+    const double X[3] = {ps.X[3 * i], ps.X[3 * i + 1], ps.X[3 * i + 2]};
+    const double w = ps.w[i];
+    double x, y, z;
+    cam_point(sm.R, sm.t, X, x, y, z);
+    if (!(z > 0)) {
+      behind = 1.0;
+      if (kind == kTruncated) acc[0] += dmul(w, s2);
+      continue;
+    }
+    const double u = dadd(__ddiv_rn(dmul(in.fx, x), z), in.cx);
+    const double v = dadd(__ddiv_rn(dmul(in.fy, y), z), in.cy);
+    const double ru = dsub(u, ps.px[2 * i]);
+    const double rv = dsub(v, ps.px[2 * i + 1]);
+    const double e2 = dadd(dmul(ru, ru), dmul(rv, rv));
+    double rho, wt;
+    if (kind == kTruncated) {
+      rho = fmin(e2, s2);
+      wt = (e2 < s2) ? 1.0 : 0.0;
+    } else {
+      const double r = __ddiv_rn(e2, s2);
+      rho = dmul(dmul(0.5, s2), log1p(r));
+      wt = __ddiv_rn(0.5, dadd(1.0, r));
+    }
+    acc[0] += dmul(w, rho);
+    if (GRAD) {
+      const double wr = dmul(w, wt);
+      if (wr != 0.0) {
+        const double p00 = in.fx / z, p02 = -in.fx * x / (z * z);
+        const double p11 = in.fy / z, p12 = -in.fy * y / (z * z);
+        double J0[6], J1[6];
+        J0[0] = p02 * y;
+        J0[1] = p00 * z + p02 * (-x);
+        J0[2] = p00 * (-y);
+        J0[3] = p00;
+        J0[4] = 0.0;
+        J0[5] = p02;
+        J1[0] = p11 * (-z) + p12 * y;
+        J1[1] = p12 * (-x);
+        J1[2] = p11 * x;
+        J1[3] = 0.0;
+        J1[4] = p11;
+        J1[5] = p12;
+#pragma unroll
+        for (int a = 0; a < 6; ++a) acc[1 + a] += wr * (J0[a] * ru + J1[a] * rv);
+        int k = 7;
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+          for (int b = a; b < 6; ++b) acc[k++] += wr * (J0[a] * J0[b] + J1[a] * J1[b]);
+      }
+    }
+  }
+  if (GRAD) {
+    block_sum<NT, kRed>(acc, sm.scratch, sm.red);
+  } else {
+    double a1[1] = {acc[0]};
+    block_sum<NT, 1>(a1, sm.scratch, sm.red);
+  }
+  // any-behind flag (deterministic OR)
+  const int anyb = __syncthreads_or(behind != 0.0);
+  if (kind == kCauchy && anyb) {
+    if (threadIdx.x == 0) sm.red[0] = CUDART_INF;
+  }
+  __syncthreads();
+}
+
+// 6x6 LU with partial pivoting (np.linalg.solve / LAPACK gesv semantics:
+// fails only on an exactly zero pivot).
+__device__ __forceinline__ bool solve6(double (&A)[36], double (&b)[6]) {
+  for (int k = 0; k < 6; ++k) {
+    int p = k;
+    double pv = fabs(A[6 * k + k]);
+    for (int i = k + 1; i < 6; ++i) {
+      const double v = fabs(A[6 * i + k]);
+      if (v > pv) {
+        pv = v;
+        p = i;
+      }
+    }
+    if (A[6 * p + k] == 0.0) return false;
+    if (p != k) {
+      for (int j = 0; j < 6; ++j) {
+        const double tmp = A[6 * k + j];
+        A[6 * k + j] = A[6 * p + j];
+        A[6 * p + j] = tmp;
+      }
+      const double tb = b[k];
+      b[k] = b[p];
+      b[p] = tb;
+    }
+    const double inv = A[6 * k + k];
+    for (int i = k + 1; i < 6; ++i) {
+      const double f = A[6 * i + k] / inv;
+      for (int j = k + 1; j < 6; ++j) A[6 * i + j] -= f * A[6 * k + j];
+      b[i] -= f * b[k];
+    }
+  }
+  for (int i = 5; i >= 0; --i) {
+    double s = b[i];
+    for (int j = i + 1; j < 6; ++j) s -= A[6 * i + j] * b[j];
+    b[i] = s / A[6 * i + i];
+  }
+  return true;
+}
+
+struct LMResult {
+  int converged;
+  int iterations;
+  double cost;
+};
+
+// Levenberg-Marquardt refinement of `start` (all threads pass the same
+// value).  Result pose in sm.cur.  trace (global, optional): accepted costs.
+template <int NT>
+__device__ LMResult lm_refine(LMShared<NT>& sm, const PointSet& ps, const Intr& in,
+                              const Pose& start, int kind, double scale, int max_iters,
+                              double gtol, double ctol, double* trace, int* trace_len) {
+  if (threadIdx.x == 0) sm.cur = start;
+  __syncthreads();
+  set_eval_pose(sm, sm.cur);
+  lm_pass<NT, true>(sm, ps, in, kind, scale);
+  double cost = sm.red[0];
+  double g[6], Hu[21];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) g[a] = 2.0 * sm.red[1 + a];
+#pragma unroll
+  for (int k = 0; k < 21; ++k) Hu[k] = 2.0 * sm.red[7 + k];
+  int ntr = 0;
+  if (trace && threadIdx.x == 0) trace[0] = cost;
+  ntr = 1;
+  double lam = 1e-6;
+  int conv = 0;
+  int it = 0;
+  for (it = 1; it <= max_iters; ++it) {
+    double gn = 0.0;
+#pragma unroll
+    for (int a = 0; a < 6; ++a) gn += g[a] * g[a];
+    if (sqrt(gn) < gtol) {
+      conv = 1;
+      break;
+    }
+    double dg[6];
+    {
+      int k = 0;
+      for (int a = 0; a < 6; ++a)
+        for (int b = a; b < 6; ++b, ++k)
+          if (a == b) dg[a] = fmax(Hu[k], 1e-12);
+    }
+    bool accepted = false;
+    double cc = 0.0;
+    for (int trial = 0; trial < 25; ++trial) {
+      if (threadIdx.x == 0) {
+        double A[36], bb[6];
+        int k = 0;
+        for (int a = 0; a < 6; ++a)
+          for (int b = a; b < 6; ++b, ++k) {
+            A[6 * a + b] = Hu[k];
+            A[6 * b + a] = Hu[k];
+          }
+        for (int a = 0; a < 6; ++a) {
+          A[7 * a] = A[7 * a] + lam * dg[a];
+          bb[a] = -g[a];
+        }
+        const bool ok = solve6(A, bb);
+        sm.flag = ok ? 1 : 0;
+        if (ok) {
+          apply_delta(sm.cur, bb, sm.cand);
+          q2R(sm.cand.q, sm.R);
+          sm.t[0] = sm.cand.t[0];
+          sm.t[1] = sm.cand.t[1];
+          sm.t[2] = sm.cand.t[2];
+        }
+      }
+      __syncthreads();
+      if (!sm.flag) {
+        lam *= 10.0;
+        __syncthreads();
+        continue;
+      }
+      lm_pass<NT, true>(sm, ps, in, kind, scale);
+      cc = sm.red[0];
+      if (cc <= cost) {
+        accepted = true;
+        break;
+      }
+      lam *= 10.0;
+      if (lam > 1e14) break;
+    }
+    if (!accepted) break;
+    lam = fmax(lam / 3.0, 1e-12);
+    const double drop = cost - cc;
+    cost = cc;
+#pragma unroll
+    for (int a = 0; a < 6; ++a) g[a] = 2.0 * sm.red[1 + a];
+#pragma unroll
+    for (int k = 0; k < 21; ++k) Hu[k] = 2.0 * sm.red[7 + k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sm.cur = sm.cand;
+      if (trace) trace[ntr] = cost;
+    }
+    ++ntr;
+    __syncthreads();
+    if (drop < ctol * fmax(cost, 1e-300)) {
+      conv = 1;
+      break;
+    }
+  }
+  if (it > max_iters) it = max_iters;
+  if (trace_len && threadIdx.x == 0) *trace_len = ntr;
+  LMResult r;
+  r.converged = conv;
+  r.iterations = it;
+  r.cost = cost;
+  return r;
+}
+
+}  // namespace vl

@@ -1,0 +1,549 @@
+// Batched, device-resident LO-RANSAC driver kernels (all but scoring).
+//
+// One "round" = one batch of `batch_size` minimal samples for every active
+// query (posest.py:250-276):
+//   k_sample   CTA/query : numpy-exact minimal sets (posest.py:252)
+//   k_p3p      thread/sample : P3P solutions into per-sample slots (p3p.py:57)
+//   k_compact  CTA/query : ordered hypothesis list + fp32 K[R|t] tiles,
+//                          appends scoring work items
+//   k_score    persistent grid (vl_score.cu): fp32 MSAC costs (posest.py:178)
+//   k_scan     CTA/query : ordered first-better scan with LM local
+//                          optimisation + adaptive stop (posest.py:257-276)
+//   k_active   1 CTA     : compacts the active-query list for the next round
+// After the last round k_final (CTA/query) classifies the full set and runs
+// the Cauchy refinement (posest.py:284-299).
+#include <climits>
+#include "vl_internal.h"
+#include "vl_lm.cuh"
+#include "vl_p3p.cuh"
+
+namespace vl {
+
+// ------------------------------------------------------------------ prep
+__global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in) {
+  QState& S = wk.qs[blockIdx.x];
+  const int64_t off = S.off, so = S.sub_off;
+  const int stride = S.stride, nsub = S.nsub;
+  const double cx = S.in.cx, cy = S.in.cy;
+  for (int i = threadIdx.x; i < nsub; i += blockDim.x) {
+    const int64_t src = off + (int64_t)i * stride;
+    const double pu = in.px[2 * src], pv = in.px[2 * src + 1];
+    const double X = in.X[3 * src], Y = in.X[3 * src + 1], Z = in.X[3 * src + 2];
+    const double w = in.w[src];
+    const int64_t d = so + i;
+    wk.sub_px[2 * d] = pu;
+    wk.sub_px[2 * d + 1] = pv;
+    wk.sub_X[3 * d] = X;
+    wk.sub_X[3 * d + 1] = Y;
+    wk.sub_X[3 * d + 2] = Z;
+    wk.sub_w[d] = w;
+    // fp32 scoring record: X32, Y32, Z32, f32(cx - u), f32(cy - v), w32
+    wk.sub32[2 * d] = make_float4((float)X, (float)Y, (float)Z, (float)(cx - pu));
+    wk.sub32[2 * d + 1] = make_float4((float)(cy - pv), (float)w, 0.f, 0.f);
+  }
+}
+
+int launch_prep(const Work& wk, const Inputs& in, int Q, cudaStream_t st) {
+  k_prep<<<Q, 256, 0, st>>>(wk, in);
+  return 1;
+}
+
+// ------------------------------------------------------------------ sampling
+// Speculative parallel generation: sample i assumes no Lemire rejection
+// happened in samples [i0, i); the first sample that would reject is redone
+// exactly by one thread and speculation restarts after it.
+template <int NT>
+__device__ void sample_batch(const GenState& g, uint64_t& pos, int64_t n, int bn, int* out) {
+  __shared__ int s_first;
+  __shared__ unsigned long long s_pos;
+  const int D = draws_per_sample(n);
+  int i0 = 0;
+  while (i0 < bn) {
+    if (threadIdx.x == 0) s_first = INT_MAX;
+    __syncthreads();
+    for (int i = i0 + threadIdx.x; i < bn; i += NT) {
+      WordReader rd;
+      rd.init(g, pos + (uint64_t)D * (uint64_t)(i - i0));
+      int64_t v[3];
+      if (choice3(rd, (uint32_t)n, false, v, nullptr)) {
+        out[3 * i] = (int)v[0];
+        out[3 * i + 1] = (int)v[1];
+        out[3 * i + 2] = (int)v[2];
+      } else {
+        atomicMin(&s_first, i);
+      }
+    }
+    __syncthreads();
+    const int r = s_first;
+    if (r == INT_MAX) {
+      pos += (uint64_t)D * (uint64_t)(bn - i0);
+      break;
+    }
+    if (threadIdx.x == 0) {
+      const uint64_t p = pos + (uint64_t)D * (uint64_t)(r - i0);
+      WordReader rd;
+      rd.init(g, p);
+      int64_t v[3];
+      int used = 0;
+      choice3(rd, (uint32_t)n, true, v, &used);
+      out[3 * r] = (int)v[0];
+      out[3 * r + 1] = (int)v[1];
+      out[3 * r + 2] = (int)v[2];
+      s_pos = p + (uint64_t)used;
+    }
+    __syncthreads();
+    pos = s_pos;
+    i0 = r + 1;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sample(Work wk, RansacParams p) {
+  const int q = wk.active_list[blockIdx.x];
+  QState& S = wk.qs[q];
+  const int64_t rem = p.max_iterations - S.iters;
+  const int bn = (int)(rem < p.batch_size ? rem : p.batch_size);
+  uint64_t pos = S.rng_pos;
+  sample_batch<256>(S.gen, pos, S.n, bn, wk.samples + (int64_t)q * wk.B * 3);
+  if (threadIdx.x == 0) {
+    S.rng_pos = pos;
+    S.batch_n = bn;
+    S.iters += bn;
+    S.rounds += 1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sample_one(GenState g, uint64_t pos0, int64_t n, int count,
+                                                    int* out, uint64_t* pos_out) {
+  uint64_t pos = pos0;
+  sample_batch<256>(g, pos, n, count, out);
+  if (threadIdx.x == 0) *pos_out = pos;
+}
+
+int launch_sample(const GenState& g, uint64_t pos0, int64_t n, int count, int* out, uint64_t* pos_out,
+                  cudaStream_t st) {
+  k_sample_one<<<1, 256, 0, st>>>(g, pos0, n, count, out, pos_out);
+  return 1;
+}
+
+// ------------------------------------------------------------------ P3P
+__device__ __forceinline__ void bearing(const double* px, const Intr& in, double* f) {
+  const double b0 = (px[0] - in.cx) / in.fx, b1 = (px[1] - in.cy) / in.fy;
+  const double nr = sqrt(dadd(dadd(dmul(b0, b0), dmul(b1, b1)), 1.0));
+  f[0] = b0 / nr;
+  f[1] = b1 / nr;
+  f[2] = 1.0 / nr;
+}
+
+__global__ void __launch_bounds__(128) k_p3p(Work wk, Inputs in) {
+  const int q = wk.active_list[blockIdx.x];
+  const QState& S = wk.qs[q];
+  const int s = blockIdx.y * blockDim.x + threadIdx.x;
+  if (s >= S.batch_n) return;
+  const int* smp = wk.samples + ((int64_t)q * wk.B + s) * 3;
+  double f[9], P[9];
+  for (int k = 0; k < 3; ++k) {
+    const int64_t r = S.off + smp[k];
+    bearing(in.px + 2 * r, S.in, f + 3 * k);
+    P[3 * k] = in.X[3 * r];
+    P[3 * k + 1] = in.X[3 * r + 1];
+    P[3 * k + 2] = in.X[3 * r + 2];
+  }
+  double Rs[36], ts[12];
+  const int c = p3p_solve_one(f, P, Rs, ts);
+  double* slot = wk.slots + ((int64_t)q * wk.B + s) * (4 * 12);
+  for (int k = 0; k < c; ++k) {
+    for (int i = 0; i < 9; ++i) slot[12 * k + i] = Rs[9 * k + i];
+    for (int i = 0; i < 3; ++i) slot[12 * k + 9 + i] = ts[3 * k + i];
+  }
+  wk.slot_cnt[(int64_t)q * wk.B + s] = c;
+}
+
+__global__ void __launch_bounds__(128) k_p3p_batch(const double* f, const double* P, int B, double* slots,
+                                                   int* cnt) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= B) return;
+  double Rs[36], ts[12];
+  const int c = p3p_solve_one(f + 9 * s, P + 9 * s, Rs, ts);
+  double* slot = slots + (int64_t)s * 48;
+  for (int k = 0; k < c; ++k) {
+    for (int i = 0; i < 9; ++i) slot[12 * k + i] = Rs[9 * k + i];
+    for (int i = 0; i < 3; ++i) slot[12 * k + 9 + i] = ts[3 * k + i];
+  }
+  cnt[s] = c;
+}
+
+// ------------------------------------------------------------------ compaction
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  int base = 0, tot = 0;
+  for (int w = 0; w < NT / 32; ++w) {
+    const int t = warp_tot[w];
+    if (w < wid) base += t;
+    tot += t;
+  }
+  __syncthreads();
+  total = tot;
+  return base + x - v;
+}
+
+// ordered gather of the per-sample solution slots (standalone p3p_solve_batch)
+__global__ void __launch_bounds__(1024) k_p3p_gather(const double* slots, const int* cnt, int B, double* R_out,
+                                                    double* t_out, int64_t* idx_out, int* m_out) {
+  __shared__ int warp_tot[32];
+  int running = 0;
+  for (int base = 0; base < B; base += 1024) {
+    const int s = base + threadIdx.x;
+    const int c = s < B ? cnt[s] : 0;
+    int total;
+    const int ex = block_excl_scan<1024>(c, warp_tot, total);
+    for (int k = 0; k < c; ++k) {
+      const int m = running + ex + k;
+      const double* sl = slots + (int64_t)s * 48 + 12 * k;
+      for (int i = 0; i < 9; ++i) R_out[9 * (int64_t)m + i] = sl[i];
+      for (int i = 0; i < 3; ++i) t_out[3 * (int64_t)m + i] = sl[9 + i];
+      idx_out[m] = s;
+    }
+    running += total;
+  }
+  if (threadIdx.x == 0) *m_out = running;
+}
+
+int launch_p3p_batch(const double* f, const double* P, int B, double* slots, int* cnt, double* R_out,
+                     double* t_out, int64_t* idx_out, int* m_out, cudaStream_t st) {
+  if (B <= 0) return 0;
+  k_p3p_batch<<<(B + 127) / 128, 128, 0, st>>>(f, P, B, slots, cnt);
+  k_p3p_gather<<<1, 1024, 0, st>>>(slots, cnt, B, R_out, t_out, idx_out, m_out);
+  return 2;
+}
+
+__global__ void __launch_bounds__(1024) k_compact(Work wk) {
+  __shared__ int warp_tot[32];
+  __shared__ int s_item0;
+  const int q = wk.active_list[blockIdx.x];
+  QState& S = wk.qs[q];
+  const int bn = S.batch_n;
+  const double fx = S.in.fx, fy = S.in.fy;
+  int running = 0;
+  for (int base = 0; base < bn; base += 1024) {
+    const int s = base + threadIdx.x;
+    const int c = s < bn ? wk.slot_cnt[(int64_t)q * wk.B + s] : 0;
+    int total;
+    const int ex = block_excl_scan<1024>(c, warp_tot, total);
+    for (int k = 0; k < c; ++k) {
+      const int h = running + ex + k;
+      wk.hsrc[(int64_t)q * wk.HCAP + h] = s * 4 + k;
+      const double* sl = wk.slots + ((int64_t)q * wk.B + s) * 48 + 12 * k;
+      float* P = wk.P32 + (int64_t)q * 12 * wk.HCAP + h;
+      const int64_t cs = wk.HCAP;
+      P[0 * cs] = (float)(fx * sl[0]);
+      P[1 * cs] = (float)(fx * sl[1]);
+      P[2 * cs] = (float)(fx * sl[2]);
+      P[3 * cs] = (float)(fx * sl[9]);
+      P[4 * cs] = (float)(fy * sl[3]);
+      P[5 * cs] = (float)(fy * sl[4]);
+      P[6 * cs] = (float)(fy * sl[5]);
+      P[7 * cs] = (float)(fy * sl[10]);
+      P[8 * cs] = (float)sl[6];
+      P[9 * cs] = (float)sl[7];
+      P[10 * cs] = (float)sl[8];
+      P[11 * cs] = (float)sl[11];
+    }
+    running += total;
+  }
+  const int nh = running;
+  const int ntile = (nh + kScoreTileHyps - 1) / kScoreTileHyps;
+  const int nitems = ntile * S.nsplit;
+  if (threadIdx.x == 0) {
+    S.nh = nh;
+    S.hyps += nh;
+    S.evals += (int64_t)nh * S.nsub;
+    s_item0 = nitems > 0 ? atomicAdd(wk.item_count, nitems) : 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nitems; i += 1024) {
+    ScoreItem it;
+    it.q = q;
+    it.tile = i / S.nsplit;
+    it.split = i % S.nsplit;
+    it.pad = 0;
+    const int64_t pos = (int64_t)s_item0 + i;
+    if (pos < wk.item_cap) wk.items[pos] = it;
+  }
+}
+
+// ------------------------------------------------------------------ scan + LO + stop
+__device__ __forceinline__ int64_t required_iters_dev(double eps, double eta, int64_t cap) {
+  eps = fmin(fmax(eps, 0.0), 1.0);
+  if (eps <= 0.0) return cap;
+  if (eps >= 1.0) return 1;
+  const double den = log1p(-pow(eps, 3.0));
+  if (den == 0.0) return cap;
+  const double nn = ceil(log(eta) / den);
+  double v = fmax(nn, 1.0);
+  if (v > (double)cap) return cap;
+  return (int64_t)v;
+}
+
+constexpr int kScanThreads = 256;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan(Work wk, RansacParams p) {
+  extern __shared__ float costs[];
+  __shared__ LMShared<kScanThreads> sm;
+  __shared__ Pose s_start;
+  const int q = wk.active_list[blockIdx.x];
+  QState& S = wk.qs[q];
+  const int nh = S.nh, NS = S.nsplit;
+  const float* part = wk.partial + (int64_t)q * wk.NSPLIT * wk.HCAP;
+  for (int h = threadIdx.x; h < nh; h += kScanThreads) {
+    float c = 0.f;
+    for (int s = 0; s < NS; ++s) c += part[(int64_t)s * wk.HCAP + h];
+    costs[h] = c;
+  }
+  __syncthreads();
+  const Intr in = S.in;
+  const PointSet sub{wk.sub_px + 2 * S.sub_off, wk.sub_X + 3 * S.sub_off, wk.sub_w + S.sub_off, S.nsub};
+  double best_cost = S.best_cost;
+  int has_best = S.has_best;
+  Pose best = S.best;
+  int64_t lo_calls = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int h0 = 0;
+  while (h0 < nh) {
+    int found = INT_MAX;
+    for (int base = h0; base < nh; base += kScanThreads) {
+      const int i = base + threadIdx.x;
+      const bool pred = i < nh && (double)costs[i] < best_cost;
+      const unsigned bal = __ballot_sync(0xffffffffu, pred);
+      if (lane == 0) sm.ibuf[wid] = bal ? base + wid * 32 + __ffs(bal) - 1 : INT_MAX;
+      __syncthreads();
+      int f = INT_MAX;
+      for (int w = 0; w < kScanThreads / 32; ++w) f = min(f, sm.ibuf[w]);
+      __syncthreads();
+      if (f != INT_MAX) {
+        found = f;
+        break;
+      }
+    }
+    if (found == INT_MAX) break;
+    best_cost = (double)costs[found];
+    has_best = 1;
+    if (threadIdx.x == 0) {
+      const int src = wk.hsrc[(int64_t)q * wk.HCAP + found];
+      const double* sl = wk.slots + ((int64_t)q * wk.B + (src >> 2)) * 48 + 12 * (src & 3);
+      pose_from_Rt(sl, sl + 9, s_start);
+    }
+    __syncthreads();
+    const Pose start = s_start;
+    lm_refine<kScanThreads>(sm, sub, in, start, kTruncated, p.tau, p.lm_max_iters, 1e-10, 1e-12, nullptr,
+                            nullptr);
+    const Pose lo = sm.cur;
+    set_eval_pose(sm, lo);
+    msac_pass<kScanThreads>(sm, sub, in, p.tau, nullptr);
+    const double lo_cost = sm.red[0];
+    if (lo_cost < best_cost) {
+      best_cost = lo_cost;
+      best = lo;
+    } else {
+      best = start;
+    }
+    ++lo_calls;
+    h0 = found + 1;
+    __syncthreads();
+  }
+  int active = 1;
+  if (has_best) {
+    set_eval_pose(sm, best);
+    msac_pass<kScanThreads>(sm, sub, in, p.tau, nullptr);
+    const int64_t cnt = (int64_t)sm.red[1];
+    const int64_t need = required_iters_dev((double)cnt / (double)S.nsub, p.eta, p.max_iterations);
+    if (S.iters >= need) active = 0;
+  }
+  if (S.iters >= p.max_iterations) active = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.best_cost = best_cost;
+    S.has_best = has_best;
+    S.best = best;
+    S.lo_calls += lo_calls;
+    S.active = active;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_active(Work wk, int nactive) {
+  __shared__ int warp_tot[32];
+  int running = 0;
+  for (int base = 0; base < nactive; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int q = i < nactive ? wk.active_list[i] : -1;
+    const int a = (q >= 0 && wk.qs[q].active) ? 1 : 0;
+    int total;
+    const int ex = block_excl_scan<1024>(a, warp_tot, total);
+    if (a) wk.active_list[running + ex] = q;  // in place: write index <= read index
+    running += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *wk.active_count = running;
+    *wk.item_count = 0;
+  }
+}
+
+int launch_score(const Work& wk, float tau2, int num_sms, cudaStream_t st);  // vl_score.cu
+
+int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
+                 cudaStream_t st) {
+  int n = 0;
+  k_sample<<<nactive, 256, 0, st>>>(wk, p);
+  ++n;
+  dim3 gp(nactive, (wk.B + 127) / 128);
+  k_p3p<<<gp, 128, 0, st>>>(wk, in);
+  ++n;
+  k_compact<<<nactive, 1024, 0, st>>>(wk);
+  ++n;
+  n += launch_score(wk, (float)(p.tau * p.tau), num_sms, st);
+  const size_t smem = (size_t)wk.HCAP * sizeof(float);
+  k_scan<<<nactive, kScanThreads, smem, st>>>(wk, p);
+  ++n;
+  k_active<<<1, 1024, 0, st>>>(wk, nactive);
+  ++n;
+  return n;
+}
+
+// ------------------------------------------------------------------ final stage
+constexpr int kFinalThreads = 512;
+
+__global__ void __launch_bounds__(kFinalThreads) k_final(Work wk, Inputs in, Outputs out, RansacParams p,
+                                                         int q_base) {
+  __shared__ LMShared<kFinalThreads> sm;
+  __shared__ int warp_tot[32];
+  const int q = blockIdx.x;
+  const QState& S = wk.qs[q];
+  const int64_t gq = q_base + q;
+  const int n = S.n;
+  uint8_t* flags = out.flags + S.off;
+  const PointSet full{in.px + 2 * S.off, in.X + 3 * S.off, in.w + S.off, n};
+  const Intr cin = S.in;
+  auto write_small = [&](const Pose& ps, int64_t cnt, double score, int conv) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 4; ++i) out.q[4 * gq + i] = ps.q[i];
+      for (int i = 0; i < 3; ++i) out.t[3 * gq + i] = ps.t[i];
+      out.inlier_count[gq] = cnt;
+      out.score[gq] = score;
+      out.iterations[gq] = S.iters;
+      out.converged[gq] = conv;
+      if (out.stats) {
+        out.stats[4 * gq + 0] = S.lo_calls;
+        out.stats[4 * gq + 1] = S.hyps;
+        out.stats[4 * gq + 2] = S.evals;
+        out.stats[4 * gq + 3] = S.rounds;
+      }
+    }
+  };
+  if (!S.has_best) {
+    for (int i = threadIdx.x; i < n; i += kFinalThreads) flags[i] = 0;
+    Pose id;
+    id.q[0] = 1;
+    id.q[1] = id.q[2] = id.q[3] = 0;
+    id.t[0] = id.t[1] = id.t[2] = 0;
+    write_small(id, 0, CUDART_INF, 0);
+    return;
+  }
+  const Pose best = S.best;
+  set_eval_pose(sm, best);
+  msac_pass<kFinalThreads>(sm, full, cin, p.tau, flags);
+  const double cost_full = sm.red[0];
+  const int64_t cnt_full = (int64_t)sm.red[1];
+  if (cnt_full < 3) {
+    write_small(best, cnt_full, cost_full, 0);
+    return;
+  }
+  // ordered compaction of the full-set inliers (X[flags_full], posest.py:291-294)
+  __syncthreads();
+  double* cpx = wk.comp_px + 2 * S.coff;
+  double* cX = wk.comp_X + 3 * S.coff;
+  double* cw = wk.comp_w + S.coff;
+  int running = 0;
+  for (int base = 0; base < n; base += kFinalThreads) {
+    const int i = base + threadIdx.x;
+    const int f = (i < n && flags[i]) ? 1 : 0;
+    int total;
+    const int ex = block_excl_scan<kFinalThreads>(f, warp_tot, total);
+    if (f) {
+      const int d = running + ex;
+      cpx[2 * d] = full.px[2 * i];
+      cpx[2 * d + 1] = full.px[2 * i + 1];
+      cX[3 * d] = full.X[3 * i];
+      cX[3 * d + 1] = full.X[3 * i + 1];
+      cX[3 * d + 2] = full.X[3 * i + 2];
+      cw[d] = full.w[i];
+    }
+    running += total;
+  }
+  __threadfence_block();
+  __syncthreads();
+  const PointSet inl{cpx, cX, cw, running};
+  lm_refine<kFinalThreads>(sm, inl, cin, best, kCauchy, p.cauchy, p.lm_max_iters, 1e-10, 1e-12, nullptr,
+                           nullptr);
+  const Pose fin = sm.cur;
+  set_eval_pose(sm, fin);
+  msac_pass<kFinalThreads>(sm, full, cin, p.tau, flags);
+  write_small(fin, (int64_t)sm.red[1], sm.red[0], 1);
+}
+
+int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
+                 int q_base, cudaStream_t st) {
+  k_final<<<Q, kFinalThreads, 0, st>>>(wk, in, out, p, q_base);
+  return 1;
+}
+
+// ------------------------------------------------------------------ standalone msac / refine
+__global__ void __launch_bounds__(512) k_msac(Pose pose, PointSet ps, Intr in, double tau, double* red_out,
+                                              uint8_t* flags) {
+  __shared__ LMShared<512> sm;
+  set_eval_pose(sm, pose);
+  msac_pass<512>(sm, ps, in, tau, flags);
+  if (threadIdx.x == 0) {
+    red_out[0] = sm.red[0];
+    red_out[1] = sm.red[1];
+  }
+}
+
+int launch_msac(const Pose& pose, const double* px, const double* X, const double* w, int n, Intr in,
+                double tau, double* red_out, uint8_t* flags, cudaStream_t st) {
+  k_msac<<<1, 512, 0, st>>>(pose, PointSet{px, X, w, n}, in, tau, red_out, flags);
+  return 1;
+}
+
+__global__ void __launch_bounds__(512) k_refine(Pose start, PointSet ps, Intr in, int kind, double scale,
+                                                int max_iters, double gtol, double ctol, Pose* pose_out,
+                                                int* info_out, double* trace) {
+  __shared__ LMShared<512> sm;
+  int tl = 0;
+  LMResult r = lm_refine<512>(sm, ps, in, start, kind, scale, max_iters, gtol, ctol, trace, &tl);
+  if (threadIdx.x == 0) {
+    *pose_out = sm.cur;
+    info_out[0] = r.converged;
+    info_out[1] = r.iterations;
+    info_out[2] = tl;
+  }
+}
+
+int launch_refine(const Pose& start, const double* px, const double* X, const double* w, int n, Intr in,
+                  int kind, double scale, int max_iters, double gtol, double ctol, Pose* pose_out,
+                  int* info_out, double* trace, cudaStream_t st) {
+  k_refine<<<1, 512, 0, st>>>(start, PointSet{px, X, w, n}, in, kind, scale, max_iters, gtol, ctol,
+                              pose_out, info_out, trace);
+  return 1;
+}
+
+}  // namespace vl

@@ -1,0 +1,267 @@
+"""Confidence-weighted LO-RANSAC PnP — drop-in for ``visloc.posest``.
+
+Same public surface as ``pkg/src/visloc/posest.py``: ``Match2D3D`` (:55-66),
+``RansacConfig`` (:69-90), ``PoseEstimate`` (:93-103),
+``UnderConstrainedError`` (:51-52), ``required_iterations`` (:106-120),
+``msac_score`` (:160-175) and ``ransac_pnp`` (:223-299), plus the additive
+``ransac_pnp_batch`` / ``ransac_pnp_device`` for many queries per launch.
+
+Every estimator call runs on the GPU through the sm_100a C ABI
+(``vl_ransac_pnp`` / ``vl_msac_score``); the host only packs arrays, moves
+them to HBM and unpacks results.  Identical inputs and config (seed
+included) reproduce the reference's minimal sample sets exactly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .geometry import CameraIntrinsics, Pose
+
+__all__ = [
+    "Match2D3D", "PoseEstimate", "RansacConfig", "UnderConstrainedError", "msac_score",
+    "ransac_pnp", "ransac_pnp_batch", "ransac_pnp_device", "required_iterations",
+]
+
+
+class UnderConstrainedError(ValueError):
+    """Fewer correspondences than the minimal sample size."""
+
+
+@dataclass(frozen=True)
+class Match2D3D:
+    query_px: np.ndarray
+    world_point: np.ndarray
+    weight: float
+    entry_id: str = ""
+
+    def __post_init__(self):
+        if not self.weight > 0:
+            raise ValueError(f"match weight must be positive, got {self.weight}")
+
+
+@dataclass(frozen=True)
+class RansacConfig:
+    max_iterations: int = 100_000
+    batch_size: int = 1_000
+    miss_probability: float = 1e-4
+    reproj_threshold: float = 12.0
+    max_scoring: int = 10_000
+    cauchy_scale: float | None = None
+    lm_max_iters: int = 100
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.reproj_threshold <= 0:
+            raise ValueError("reproj_threshold must be positive")
+        if not 0 < self.miss_probability < 1:
+            raise ValueError("miss_probability must be in (0, 1)")
+        if self.batch_size > self.max_iterations:
+            raise ValueError("batch_size must not exceed max_iterations")
+
+    @property
+    def cauchy(self) -> float:
+        return self.reproj_threshold if self.cauchy_scale is None else self.cauchy_scale
+
+
+@dataclass
+class PoseEstimate:
+    pose: Pose
+    inlier_count: int
+    inlier_flags: np.ndarray
+    score: float
+    iterations: int
+    converged: bool
+    stats: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def __post_init__(self):
+        self.inlier_flags = np.asarray(self.inlier_flags, dtype=bool)
+
+
+def required_iterations(inlier_ratio: float, miss_probability: float, sample_size: int = 3,
+                        max_iterations: int = 100_000) -> int:
+    """Adaptive bound ceil(ln eta / ln(1 - eps^m)), clamped (posest.py:106-120)."""
+    eps = min(max(inlier_ratio, 0.0), 1.0)
+    if eps <= 0.0:
+        return max_iterations
+    if eps >= 1.0:
+        return 1
+    den = math.log1p(-(eps ** sample_size))
+    if den == 0.0:
+        return max_iterations
+    return int(min(max(math.ceil(math.log(miss_probability) / den), 1), max_iterations))
+
+
+# ----------------------------------------------------------------- helpers
+def _host_arrays(matches):
+    """Match list or (px, X, w) triple -> fp64 numpy (n,2), (n,3), (n,) (posest.py:123-134)."""
+    if isinstance(matches, tuple) and len(matches) == 3:
+        px, X, w = matches
+        if hasattr(px, "detach"):  # torch tensors
+            px, X, w = (a.detach().cpu().numpy() for a in (px, X, w))
+        return (np.ascontiguousarray(np.asarray(px, dtype=np.float64).reshape(-1, 2)),
+                np.ascontiguousarray(np.asarray(X, dtype=np.float64).reshape(-1, 3)),
+                np.ascontiguousarray(np.asarray(w, dtype=np.float64).reshape(-1)))
+    px = np.array([m.query_px for m in matches], dtype=np.float64).reshape(-1, 2)
+    X = np.array([m.world_point for m in matches], dtype=np.float64).reshape(-1, 3)
+    w = np.array([m.weight for m in matches], dtype=np.float64).reshape(-1)
+    return px, X, w
+
+
+def _intr_c(intr) -> _lib.Intrinsics:
+    return _lib.Intrinsics(float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy))
+
+
+def _cfg_c(cfg: RansacConfig) -> _lib.RansacConfigC:
+    c = _lib.RansacConfigC()
+    c.max_iterations = int(cfg.max_iterations)
+    c.batch_size = int(cfg.batch_size)
+    c.max_scoring = int(cfg.max_scoring)
+    c.miss_probability = float(cfg.miss_probability)
+    c.reproj_threshold = float(cfg.reproj_threshold)
+    c.cauchy_scale = float(cfg.cauchy) if cfg.cauchy_scale is not None else -1.0
+    c.lm_max_iters = int(cfg.lm_max_iters)
+    return c
+
+
+def _to_device(a: np.ndarray):
+    import torch
+    _lib.context()  # fails loudly (VislocError) without a CUDA device / built library
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if t.numel() == 0:
+        return t.cuda()
+    return t.pin_memory().cuda(non_blocking=True)
+
+
+# ----------------------------------------------------------------- device entry
+def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, out=None):
+    """Batched estimator on device-resident inputs (the HBM-resident hot path).
+
+    ``px`` (N,2), ``X`` (N,3), ``w`` (N,) are fp64 CUDA tensors holding Q
+    queries back to back; ``offsets`` (Q+1,) int64 host array; ``intrinsics``
+    a list of Q intrinsics; ``seeds`` Q seeds (each query behaves exactly like
+    ``ransac_pnp`` with ``RansacConfig(seed=seeds[i])``).  Returns a dict of
+    CUDA tensors (q, t, flags, count, score, iterations, converged, stats).
+    """
+    import torch
+    offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    Q = offsets.shape[0] - 1
+    if Q <= 0:
+        raise ValueError("need at least one query")
+    for i in range(Q):
+        if offsets[i + 1] - offsets[i] < 3:
+            raise UnderConstrainedError(f"need >= 3 matches, got {offsets[i + 1] - offsets[i]}")
+    dev = px.device
+    N = int(offsets[-1])
+    for a, shape in ((px, (N, 2)), (X, (N, 3)), (w, (N,))):
+        if not (a.is_cuda and a.dtype == torch.float64 and a.is_contiguous() and tuple(a.shape) == shape):
+            raise ValueError(f"expected contiguous fp64 CUDA tensor of shape {shape}")
+    ctx = _lib.context(dev.index)
+    if out is None:
+        out = {
+            "q": torch.empty((Q, 4), dtype=torch.float64, device=dev),
+            "t": torch.empty((Q, 3), dtype=torch.float64, device=dev),
+            "flags": torch.empty((N,), dtype=torch.uint8, device=dev),
+            "count": torch.empty((Q,), dtype=torch.int64, device=dev),
+            "score": torch.empty((Q,), dtype=torch.float64, device=dev),
+            "iterations": torch.empty((Q,), dtype=torch.int64, device=dev),
+            "converged": torch.empty((Q,), dtype=torch.int32, device=dev),
+            "stats": torch.empty((Q, 4), dtype=torch.int64, device=dev),
+        }
+    intr_arr = (_lib.Intrinsics * Q)(*[_intr_c(i) for i in intrinsics])
+    rng_arr = (_lib.PCG64State * Q)(*[_lib.pcg64_state(int(s)) for s in seeds])
+    args = _lib.RansacArgs()
+    args.num_queries = Q
+    args.offsets = offsets.ctypes.data_as(C.POINTER(C.c_int64))
+    args.intr = intr_arr
+    args.rng = rng_arr
+    args.px, args.X, args.w = px.data_ptr(), X.data_ptr(), w.data_ptr()
+    args.cfg = _cfg_c(cfg)
+    o = _lib.RansacOut()
+    o.q, o.t, o.inlier_flags = out["q"].data_ptr(), out["t"].data_ptr(), out["flags"].data_ptr()
+    o.inlier_count, o.score = out["count"].data_ptr(), out["score"].data_ptr()
+    o.iterations, o.converged = out["iterations"].data_ptr(), out["converged"].data_ptr()
+    o.stats = out["stats"].data_ptr()
+    with torch.cuda.device(dev):
+        rc = _lib.lib().vl_ransac_pnp(ctx.handle, C.byref(args), C.byref(o), _lib.stream_ptr())
+    ctx.check(rc, "vl_ransac_pnp")
+    return out
+
+
+def _estimates_from(out, offsets) -> list[PoseEstimate]:
+    q = out["q"].cpu().numpy()
+    t = out["t"].cpu().numpy()
+    flags = out["flags"].cpu().numpy().astype(bool)
+    cnt = out["count"].cpu().numpy()
+    score = out["score"].cpu().numpy()
+    iters = out["iterations"].cpu().numpy()
+    conv = out["converged"].cpu().numpy()
+    stats = out["stats"].cpu().numpy()
+    res = []
+    for i in range(q.shape[0]):
+        a, b = int(offsets[i]), int(offsets[i + 1])
+        res.append(PoseEstimate(
+            pose=Pose(q[i], t[i]), inlier_count=int(cnt[i]), inlier_flags=flags[a:b],
+            score=float(score[i]), iterations=int(iters[i]), converged=bool(conv[i]),
+            stats={"lo_calls": int(stats[i, 0]), "hypotheses": int(stats[i, 1]),
+                   "evals": int(stats[i, 2]), "rounds": int(stats[i, 3])}))
+    return res
+
+
+def ransac_pnp_batch(queries, intrinsics, cfg: RansacConfig, seeds=None) -> list[PoseEstimate]:
+    """Estimate many independent queries in one device-resident run.
+
+    ``queries``: list of match sets (as ``ransac_pnp`` accepts);
+    ``intrinsics``: one ``CameraIntrinsics`` or one per query; ``seeds``:
+    per-query seeds (default ``cfg.seed`` for every query).
+    """
+    arrs = [_host_arrays(m) for m in queries]
+    Q = len(arrs)
+    if Q == 0:
+        return []
+    if isinstance(intrinsics, CameraIntrinsics) or not isinstance(intrinsics, (list, tuple)):
+        intrinsics = [intrinsics] * Q
+    if seeds is None:
+        seeds = [cfg.seed] * Q
+    offsets = np.zeros(Q + 1, dtype=np.int64)
+    offsets[1:] = np.cumsum([a[0].shape[0] for a in arrs])
+    for i in range(Q):
+        if offsets[i + 1] - offsets[i] < 3:
+            raise UnderConstrainedError(f"need >= 3 matches, got {offsets[i + 1] - offsets[i]}")
+    px = _to_device(np.concatenate([a[0] for a in arrs]))
+    X = _to_device(np.concatenate([a[1] for a in arrs]))
+    w = _to_device(np.concatenate([a[2] for a in arrs]))
+    out = ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg)
+    return _estimates_from(out, offsets)
+
+
+def ransac_pnp(matches, intr: CameraIntrinsics, cfg: RansacConfig) -> PoseEstimate:
+    """Estimate a camera-from-world pose from weighted 2D-3D matches (posest.py:223)."""
+    px, X, w = _host_arrays(matches)
+    if px.shape[0] < 3:
+        raise UnderConstrainedError(f"need >= 3 matches, got {px.shape[0]}")
+    return ransac_pnp_batch([(px, X, w)], [intr], cfg, seeds=[cfg.seed])[0]
+
+
+def msac_score(pose: Pose, matches, intr: CameraIntrinsics, tau: float):
+    """Weighted MSAC cost and inlier flags (posest.py:160-175), fp64 on the GPU."""
+    import torch
+    px, X, w = _host_arrays(matches)
+    n = px.shape[0]
+    ctx = _lib.context()
+    dpx, dX, dw = _to_device(px), _to_device(X), _to_device(w)
+    flags = torch.empty((max(n, 1),), dtype=torch.uint8, device=dpx.device)
+    q = np.ascontiguousarray(pose.q, dtype=np.float64)
+    t = np.ascontiguousarray(pose.t, dtype=np.float64)
+    cost = C.c_double()
+    dp = C.POINTER(C.c_double)
+    rc = _lib.lib().vl_msac_score(ctx.handle, q.ctypes.data_as(dp), t.ctypes.data_as(dp),
+                                  dpx.data_ptr(), dX.data_ptr(), dw.data_ptr(), n, _intr_c(intr),
+                                  float(tau), C.byref(cost), flags.data_ptr(), _lib.stream_ptr())
+    ctx.check(rc, "vl_msac_score")
+    return float(cost.value), flags[:n].cpu().numpy().astype(bool)

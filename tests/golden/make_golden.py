@@ -1,0 +1,137 @@
+"""Generate golden vectors by running the REAL reference (``/root/reference``).
+
+Run in the build container only (the reference does not exist on the GPU
+box):  ``python tests/golden/make_golden.py``.  Writes small ``.npz``
+fixtures next to this script; they pin the oracle (``tests/test_oracle_golden.py``)
+and the GPU path (``tests/test_gpu_*.py``).  numpy version is recorded
+because the minimal-sample sets come from numpy's PCG64 stream.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+sys.path.insert(0, str(REF))
+
+from visloc.geometry import CameraIntrinsics, Pose, rotvec_to_quat  # noqa: E402
+from visloc.p3p import p3p_solve_batch  # noqa: E402
+from visloc.posest import (RansacConfig, _bearings, _score_hypotheses, msac_score,  # noqa: E402
+                           ransac_pnp)
+from visloc.refine import CauchyLoss, TruncatedLoss, refine_pose  # noqa: E402
+
+sys.path.insert(0, str(OUT.parent))
+from synth_inputs import INTR_A, GT_A, matches_a, refine_problem  # noqa: E402
+
+
+def rng_vectors():
+    cases = [(0, 2000), (5, 3), (5, 4), (7, 50), (11, 23_000), (12345, 200_000), (2**40 + 3, 50_000),
+             (99, 2**31 - 1)]
+    seeds, ns, samples, states = [], [], [], []
+    for seed, n in cases:
+        g = np.random.default_rng(seed)
+        s = np.stack([g.choice(n, size=3, replace=False) for _ in range(2000)])
+        st = g.bit_generator.state
+        seeds.append(seed)
+        ns.append(n)
+        samples.append(s)
+        states.append([st["state"]["state"] >> 64, st["state"]["state"] & (2**64 - 1),
+                       st["state"]["inc"] >> 64, st["state"]["inc"] & (2**64 - 1),
+                       st["has_uint32"], st["uinteger"]])
+    np.savez_compressed(OUT / "rng.npz", seeds=np.array(seeds, dtype=np.uint64), n=np.array(ns),
+                        samples=np.stack(samples), states=np.array(states, dtype=np.uint64),
+                        numpy_version=np.array(np.__version__))
+
+
+def p3p_vectors():
+    px, X, w, _ = matches_a(4000, 0.5, 1.0, seed=21)
+    b = _bearings(px, INTR_A)
+    rng = np.random.default_rng(3)
+    smp = np.stack([rng.choice(4000, 3, replace=False) for _ in range(3000)])
+    R, t, idx = p3p_solve_batch(b[smp], X[smp])
+    np.savez_compressed(OUT / "p3p.npz", bearings=b[smp], points=X[smp], R=R, t=t, idx=idx)
+    return R, t, px, X, w
+
+
+def score_vectors(R, t, px, X, w):
+    sub = slice(0, 4000, 2)
+    costs = _score_hypotheses(R[:600], t[:600], X[sub], px[sub], w[sub], INTR_A, 12.0)
+    np.savez_compressed(OUT / "score.npz", R=R[:600], t=t[:600], px=px[sub], X=X[sub], w=w[sub],
+                        costs=costs, tau=12.0)
+
+
+def msac_vectors():
+    px, X, w, _ = matches_a(3000, 0.4, 2.0, seed=8)
+    out = {"px": px, "X": X, "w": w}
+    rng = np.random.default_rng(1)
+    qs, ts, costs, flags = [], [], [], []
+    for k in range(6):
+        dq = rotvec_to_quat(rng.normal(size=3) * 0.01 * k)
+        pose = Pose(dq, np.zeros(3)).compose(GT_A) if k else GT_A
+        pose = Pose(pose.q, pose.t + rng.normal(size=3) * 0.01 * k)
+        c, f = msac_score(pose, (px, X, w), INTR_A, 12.0)
+        qs.append(pose.q)
+        ts.append(pose.t)
+        costs.append(c)
+        flags.append(f)
+    out.update(q=np.array(qs), t=np.array(ts), costs=np.array(costs), flags=np.array(flags))
+    np.savez_compressed(OUT / "msac.npz", **out)
+
+
+def refine_vectors():
+    recs = {}
+    for k, (kind, n, noise, outl) in enumerate([("trunc", 300, 1.0, 0.3), ("trunc", 2000, 0.5, 0.5),
+                                               ("cauchy", 500, 1.0, 0.25), ("cauchy", 3000, 0.3, 0.0)]):
+        start, X, px, w = refine_problem(np.random.default_rng(100 + k), n, noise, outl)
+        loss = TruncatedLoss(12.0) if kind == "trunc" else CauchyLoss(12.0)
+        r = refine_pose(start, X, px, w, loss, INTR_A, max_iters=100)
+        recs[f"c{k}"] = dict(kind=kind, start_q=start.q, start_t=start.t, X=X, px=px, w=w, q=r.pose.q,
+                             t=r.pose.t, iters=r.iterations, conv=r.converged, trace=np.array(r.cost_trace))
+    flat = {}
+    for key, d in recs.items():
+        for k2, v in d.items():
+            flat[f"{key}_{k2}"] = np.asarray(v)
+    flat["cases"] = np.array(list(recs))
+    np.savez_compressed(OUT / "refine.npz", **flat)
+
+
+def ransac_vectors():
+    cases = [
+        # (n, outlier_frac, sigma, data seed, ransac seed, max_iterations, eta)
+        (2000, 0.0, 0.0, 0, 5, 100_000, 1e-4),
+        (2000, 0.5, 0.0, 3, 5, 100_000, 1e-4),
+        (1500, 0.4, 0.5, 4, 9, 100_000, 1e-4),
+        (3000, 0.3, 1.0, 9, 3, 100_000, 1e-4),
+        (800, 0.3, 0.0, 6, 1, 100_000, 1e-4),
+        (2000, 0.7, 1.0, 12, 7, 3000, 1e-300),
+        (23_000, 0.2, 0.0, 7, 2, 100_000, 1e-4),
+        (12_000, 0.6, 1.0, 13, 17, 2000, 1e-300),
+    ]
+    flat = {"cases": np.array(cases, dtype=np.float64)}
+    for k, (n, of, sg, ds, rs, mi, eta) in enumerate(cases):
+        px, X, w, _ = matches_a(int(n), of, sg, seed=int(ds))
+        cfg = RansacConfig(seed=int(rs), max_iterations=int(mi), miss_probability=eta)
+        e = ransac_pnp((px, X, w), INTR_A, cfg)
+        flat[f"r{k}_q"] = e.pose.q
+        flat[f"r{k}_t"] = e.pose.t
+        flat[f"r{k}_flags"] = np.packbits(e.inlier_flags)
+        flat[f"r{k}_score"] = np.array(e.score)
+        flat[f"r{k}_iters"] = np.array(e.iterations)
+        flat[f"r{k}_conv"] = np.array(e.converged)
+        flat[f"r{k}_count"] = np.array(e.inlier_count)
+    np.savez_compressed(OUT / "ransac.npz", **flat)
+
+
+if __name__ == "__main__":
+    rng_vectors()
+    R, t, px, X, w = p3p_vectors()
+    score_vectors(R, t, px, X, w)
+    msac_vectors()
+    refine_vectors()
+    ransac_vectors()
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)

@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path (through the C ABI) against golden vectors and the oracle.
+
+Bars (BASELINE.json north_star): identical minimal sets; inlier masks
+bit-exact except points within 1e-6 px of the threshold; final pose within
+0.01 deg rotation and 1e-4 relative translation.  P3P solutions to 1e-9,
+fp32 costs to 1e-5 relative, fp64 MSAC costs to 1e-12 relative.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import geometry as og
+from oracle.posest import Config, errors_sq, msac, ransac
+from synth_inputs import batch_a, matches_a
+
+pytestmark = pytest.mark.gpu
+
+INTR_T = (700.0, 700.0, 350.0, 350.0)
+TAU = 12.0
+
+
+@pytest.fixture(scope="module")
+def vl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_04185_b200 as vl
+    return vl
+
+
+@pytest.fixture(scope="module")
+def intr(vl):
+    return vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
+
+
+def _near_threshold(q, t, px, X, tol=1e-6):
+    """Points whose reprojection error lies within `tol` px of tau under pose (q,t)."""
+    e2 = errors_sq(og.q2R(q), t, X, px, INTR_T)
+    e = np.sqrt(e2)
+    return np.abs(e - TAU) < tol
+
+
+def _check_mask(flags, ref_flags, q, t, px, X, tol=1e-6):
+    diff = flags != ref_flags
+    if diff.any():
+        amb = _near_threshold(q, t, px, X, tol)
+        assert not (diff & ~amb).any(), f"{int((diff & ~amb).sum())} mask differences away from tau"
+
+
+def _check_pose(q, t, q_ref, t_ref):
+    rot = og.rot_err_deg(q, q_ref)
+    assert rot < 0.01, rot
+    rel = np.linalg.norm(t - t_ref) / max(np.linalg.norm(t_ref), 1e-12)
+    assert rel < 1e-4, rel
+
+
+# ----------------------------------------------------------------------- sampling
+def test_sampler_matches_numpy_golden(vl, golden):
+    from paper_2601_04185_b200.p3p import sample_minimal_sets
+    g = golden("rng")
+    for k, (seed, n) in enumerate(zip(g["seeds"], g["n"])):
+        s, st = sample_minimal_sets(int(seed), int(n), g["samples"].shape[1])
+        assert np.array_equal(s, g["samples"][k]), (seed, n)
+        ref = g["states"][k]
+        assert st["state"]["state"] == (int(ref[0]) << 64) | int(ref[1])
+        assert st["has_uint32"] == int(ref[4]) and st["uinteger"] == int(ref[5])
+
+
+def test_sampler_chained_batches_match_numpy(vl):
+    from paper_2601_04185_b200.p3p import sample_minimal_sets
+    for seed, n in [(3, 200_000), (4, 3), (8, 17)]:
+        g = np.random.default_rng(seed)
+        state = seed
+        for _ in range(5):
+            ref = np.stack([g.choice(n, 3, replace=False) for _ in range(777)])
+            got, state = sample_minimal_sets(state, n, 777)
+            assert np.array_equal(got, ref)
+        assert state["state"]["state"] == g.bit_generator.state["state"]["state"]
+
+
+# ----------------------------------------------------------------------- p3p
+def test_p3p_matches_reference_golden(vl, golden):
+    from paper_2601_04185_b200.p3p import p3p_solve_batch
+    g = golden("p3p")
+    R, t, idx = p3p_solve_batch(g["bearings"], g["points"])
+    assert np.array_equal(idx, g["idx"])
+    assert np.abs(R - g["R"]).max() < 1e-9
+    assert (np.abs(t - g["t"]).max() / np.abs(g["t"]).max()) < 1e-9
+
+
+def test_p3p_degenerate_and_scalar(vl):
+    from paper_2601_04185_b200.p3p import p3p_solve, p3p_solve_batch
+    P = np.array([[0, 0, 2.0], [1, 0, 2.0], [2, 0, 2.0]])
+    f = P / np.linalg.norm(P, axis=1, keepdims=True)
+    assert p3p_solve(f, P) == []
+    R, t, idx = p3p_solve_batch(np.zeros((0, 3, 3)), np.zeros((0, 3, 3)))
+    assert R.shape == (0, 3, 3)
+
+
+# ----------------------------------------------------------------------- msac / refine
+def test_msac_matches_reference_golden(vl, intr, golden):
+    g = golden("msac")
+    for k in range(g["q"].shape[0]):
+        pose = vl.Pose(g["q"][k], g["t"][k])
+        c, f = vl.msac_score(pose, (g["px"], g["X"], g["w"]), intr, TAU)
+        assert math.isclose(c, float(g["costs"][k]), rel_tol=1e-12)
+        _check_mask(f, g["flags"][k], g["q"][k], g["t"][k], g["px"], g["X"])
+
+
+def test_msac_kats(vl, intr):
+    pose = vl.Pose.identity()
+    xw = np.array([[0.0, 0.0, 2.0], [0.0, 0.0, 3.0]])
+    px = np.array([[350.0, 350.0], [360.0, 350.0]])
+    c, f = vl.msac_score(pose, (px, xw, np.ones(2)), intr, 5.0)
+    assert c == pytest.approx(25.0) and list(f) == [True, False]
+    c, f = vl.msac_score(pose, (np.array([[350.0, 350.0]]), np.array([[0, 0, -2.0]]), np.ones(1)),
+                         intr, 10.0)
+    assert c == pytest.approx(100.0) and not f[0]
+
+
+def test_refine_matches_reference_golden(vl, intr, golden):
+    from paper_2601_04185_b200.refine import CauchyLoss, TruncatedLoss, refine_pose
+    g = golden("refine")
+    for key in g["cases"]:
+        loss = TruncatedLoss(12.0) if str(g[f"{key}_kind"]) == "trunc" else CauchyLoss(12.0)
+        r = refine_pose(vl.Pose(g[f"{key}_start_q"], g[f"{key}_start_t"]), g[f"{key}_X"], g[f"{key}_px"],
+                        g[f"{key}_w"], loss, intr)
+        assert og.rot_err_deg(r.pose.q, g[f"{key}_q"]) < 1e-7
+        assert np.linalg.norm(r.pose.t - g[f"{key}_t"]) < 1e-8 * max(1, np.linalg.norm(g[f"{key}_t"]))
+        tr = np.array(r.cost_trace)
+        ref = g[f"{key}_trace"]
+        assert np.all(np.diff(tr) <= 0)
+        assert math.isclose(tr[-1], ref[-1], rel_tol=1e-9, abs_tol=1e-9)
+        assert r.converged == bool(g[f"{key}_conv"])
+        assert abs(r.iterations - int(g[f"{key}_iters"])) <= 1
+
+
+# ----------------------------------------------------------------------- ransac
+def test_ransac_matches_reference_golden(vl, intr, golden):
+    g = golden("ransac")
+    for k, (n, of, sg, ds, rs, mi, eta) in enumerate(g["cases"]):
+        px, X, w, _ = matches_a(int(n), of, sg, seed=int(ds))
+        cfg = vl.RansacConfig(seed=int(rs), max_iterations=int(mi), miss_probability=eta)
+        e = vl.ransac_pnp((px, X, w), intr, cfg)
+        assert e.converged == bool(g[f"r{k}_conv"]), k
+        assert e.iterations == int(g[f"r{k}_iters"]), k
+        _check_pose(e.pose.q, e.pose.t, g[f"r{k}_q"], g[f"r{k}_t"])
+        ref_flags = np.unpackbits(g[f"r{k}_flags"])[: int(n)].astype(bool)
+        _check_mask(e.inlier_flags, ref_flags, g[f"r{k}_q"], g[f"r{k}_t"], px, X)
+        assert math.isclose(e.score, float(g[f"r{k}_score"]), rel_tol=1e-6)
+
+
+def test_ransac_reference_behaviours(vl, intr):
+    """Ports of pkg/tests/test_posest.py:95-175 (same data, same assertions)."""
+    q_gt, R_gt, t_gt = og.canon(og.rotvec2q(np.array([0.05, -0.1, 0.2]))), None, np.array([0.1, 0.2, 0.3])
+    gt = vl.Pose(q_gt, t_gt)
+    px, X, w, _ = matches_a(2000)
+    e = vl.ransac_pnp((px, X, w), intr, vl.RansacConfig(seed=5))
+    pe = vl.pose_error(e.pose, gt)
+    assert e.converged and pe.rotation_error_deg < 1e-6 and pe.translation_error_m < 1e-6
+    assert e.iterations == 1000 and e.inlier_count == 2000
+    px, X, w, out = matches_a(2000, outlier_frac=0.5, seed=3)
+    e = vl.ransac_pnp((px, X, w), intr, vl.RansacConfig(seed=5))
+    assert np.array_equal(e.inlier_flags, ~out)
+    with pytest.raises(vl.UnderConstrainedError):
+        vl.ransac_pnp(matches_a(2)[:3], intr, vl.RansacConfig(seed=0))
+    px1 = np.tile(np.array([[350.0, 350.0]]), (5, 1))
+    xw1 = np.tile(np.array([[0.0, 0.0, 2.0]]), (5, 1))
+    e = vl.ransac_pnp((px1, xw1, np.ones(5)), intr, vl.RansacConfig(seed=0, max_iterations=2000))
+    assert not e.converged and e.iterations == 2000
+    px, X, w, _ = matches_a(1500, outlier_frac=0.4, sigma=0.5, seed=4)
+    a = vl.ransac_pnp((px, X, w), intr, vl.RansacConfig(seed=9))
+    b = vl.ransac_pnp((px, X, w), intr, vl.RansacConfig(seed=9))
+    assert np.array_equal(a.pose.q, b.pose.q) and np.array_equal(a.pose.t, b.pose.t)
+    assert a.score == b.score and np.array_equal(a.inlier_flags, b.inlier_flags)
+    matches = [vl.Match2D3D(px[i], X[i], float(w[i]), "e") for i in range(50)]
+    assert vl.ransac_pnp(matches, intr, vl.RansacConfig(seed=1)).converged
+
+
+def test_batch_equals_single_and_oracle(vl, intr):
+    pxs, Xs, ws = batch_a(6, 1500, 0.5, 1.0, seed0=40)
+    cfg = vl.RansacConfig(seed=0, max_iterations=4000, miss_probability=1e-300)
+    seeds = [11 * i + 1 for i in range(6)]
+    res = vl.ransac_pnp_batch(list(zip(pxs, Xs, ws)), intr, cfg, seeds=seeds)
+    for i in range(6):
+        single = vl.ransac_pnp((pxs[i], Xs[i], ws[i]), intr,
+                               vl.RansacConfig(seed=seeds[i], max_iterations=4000, miss_probability=1e-300))
+        assert np.array_equal(res[i].pose.q, single.pose.q) and np.array_equal(res[i].inlier_flags,
+                                                                               single.inlier_flags)
+        o = ransac(pxs[i], Xs[i], ws[i], INTR_T, Config(seed=seeds[i], max_iterations=4000,
+                                                         miss_probability=1e-300))
+        assert res[i].iterations == o.iterations
+        _check_pose(res[i].pose.q, res[i].pose.t, o.q, o.t)
+        _check_mask(res[i].inlier_flags, o.inlier_flags, o.q, o.t, pxs[i], Xs[i])
