@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 LO-RANSAC PnP hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c4] [--impl ours|reference]
+
+One *step* = one complete batched ``ransac_pnp`` over the workload's
+queries (sampling, P3P, fp32 scoring, LO, adaptive stop, final Cauchy
+refinement) with inputs resident in HBM.  Default workload is BASELINE
+config C3 ("Aachen-style batch": 1000 queries x 50k correspondences per GPU,
+30% inliers, sigma 1 px) in fixed-iteration mode (10k minimal samples per
+query, eta = 1e-300) so every query does the same, BASELINE-named amount of
+work.  Queries shard across GPUs with no collective (weak scaling: 1000
+queries per GPU).  ``value`` = hypothesis x correspondence evaluations / s
+over the whole job; ``e2e`` = the same through the host-buffer API
+(H2D of the packed matches + D2H of poses/masks inside the timed region).
+
+``--impl reference`` times the CPU reference arm: the oracle port of the
+reference algorithm (``oracle/``, bit-identical to visloc on the golden
+vectors) over all host cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+FLOP_PER_EVAL = 30  # literal count of posest.py:203-219
+
+WORKLOADS = {
+    "c3": dict(name="C3 Aachen-style batch: 1000 queries x 50k corrs per GPU, eps=0.3, sigma=1px, "
+                    "fixed 10k minimal samples/query (eta=1e-300)",
+               queries=1000, n=50_000, outlier=0.7, sigma=1.0, max_iterations=10_000, eta=1e-300,
+               cpu_queries_per_core=1),
+    "c3a": dict(name="C3 Aachen-style batch, adaptive stop (eta=1e-4): 1000 queries x 50k corrs per GPU, "
+                     "eps=0.3, sigma=1px",
+                queries=1000, n=50_000, outlier=0.7, sigma=1.0, max_iterations=100_000, eta=1e-4,
+                cpu_queries_per_core=2),
+    "c1": dict(name="C1 single query: 2k corrs, eps=0.3, sigma=1px, fixed 10k minimal samples",
+               queries=1, n=2_000, outlier=0.7, sigma=1.0, max_iterations=10_000, eta=1e-300,
+               cpu_queries_per_core=1),
+    "c4": dict(name="C4 low inlier ratio: 10k corrs, eps=0.05, 100k minimal samples (LO-heavy)",
+               queries=1, n=10_000, outlier=0.95, sigma=1.0, max_iterations=100_000, eta=1e-300,
+               cpu_queries_per_core=1),
+}
+
+
+def query_a(qi: int, n: int, outlier: float, sigma: float, seed0: int):
+    """Deterministic generator-A query (test_posest.py:22-35 model, per-query GT pose)."""
+    from synth_inputs import matches_a, random_pose
+    rng = np.random.default_rng(seed0 + qi)
+    _, R, t = random_pose(rng, 0.2, 0.2)
+    px, X, w, _ = matches_a(n, outlier, sigma, seed=seed0 + 7919 * qi + 1, R=R, t=t)
+    return px, X, w
+
+
+def query_seed(qi: int, seed0: int) -> int:
+    return 1_000_003 * seed0 + qi
+
+
+# ----------------------------------------------------------------------------- CPU arm
+def _cpu_worker(job):
+    qi, wl, seed0 = job
+    from oracle.posest import Config, ransac
+    px, X, w = query_a(qi, wl["n"], wl["outlier"], wl["sigma"], seed0)
+    t0 = time.perf_counter()
+    r = ransac(px, X, w, (700.0, 700.0, 350.0, 350.0),
+               Config(seed=query_seed(qi, seed0), max_iterations=wl["max_iterations"],
+                      miss_probability=wl["eta"]))
+    return r.evals, time.perf_counter() - t0
+
+
+def cpu_sample(wl, seed0, n_queries, cores):
+    """Run the oracle port on `n_queries` queries over `cores` processes; (evals, wall s)."""
+    import multiprocessing as mp
+    saved = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in saved:
+        os.environ[k] = "1"
+    try:
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(cores) as pool:
+            pool.map(_cpu_worker, [(0, dict(wl, n=64, max_iterations=wl.get("batch", 1000)), seed0)] * cores)
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_worker, [(qi, wl, seed0) for qi in range(n_queries)])
+            wall = time.perf_counter() - t0
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return sum(r[0] for r in res), wall
+
+
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+def run_reference_arm(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = host_cores()
+    nq = cores * wl["cpu_queries_per_core"]
+    seed0 = 3000
+    for _ in range(args.warmup):
+        cpu_sample(wl, seed0, cores, cores)
+    vals, walls = [], []
+    total_evals = 0
+    for _ in range(args.steps):
+        ev, wall = cpu_sample(wl, seed0, nq, cores)
+        vals.append(ev / wall)
+        walls.append(wall)
+        total_evals += ev
+    value = total_evals / sum(walls)
+    sample = f"{nq} queries of the workload per step ({wl['cpu_queries_per_core']}/core), oracle port"
+    line = {
+        "impl": "reference", "metric": "hyp×corr evals/s", "value": value, "unit": "evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * statistics.mean(walls), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "queries_per_step": nq, "corrs_per_query": wl["n"]},
+        "queries_per_s": nq / statistics.mean(walls),
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons, pw = [], None, set(), []
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+                pw.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "power_w_max": max(pw) if pw else None, "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--queries", type=int, default=None, help="override queries per GPU")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    wl = dict(WORKLOADS[args.workload])
+    if args.queries:
+        wl["queries"] = args.queries
+    if args.impl == "reference":
+        run_reference_arm(args, wl)
+        return
+
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2601_04185_b200 import _lib
+    from paper_2601_04185_b200.geometry import CameraIntrinsics
+    from paper_2601_04185_b200.posest import RansacConfig, ransac_pnp_device, ransac_pnp_host
+
+    Q, n = wl["queries"], wl["n"]
+    seed0 = 3000 + 100_000 * rank
+    qs = [query_a(qi, n, wl["outlier"], wl["sigma"], seed0) for qi in range(Q)]
+    px_h = torch.from_numpy(np.concatenate([q[0] for q in qs])).pin_memory()
+    X_h = torch.from_numpy(np.concatenate([q[1] for q in qs])).pin_memory()
+    w_h = torch.from_numpy(np.concatenate([q[2] for q in qs])).pin_memory()
+    del qs
+    offsets = np.arange(Q + 1, dtype=np.int64) * n
+    intr = [CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)] * Q
+    seeds = [query_seed(qi, seed0) for qi in range(Q)]
+    cfg = RansacConfig(max_iterations=wl["max_iterations"], miss_probability=wl["eta"])
+    px_d, X_d, w_d = px_h.cuda(), X_h.cuda(), w_h.cuda()
+    ctx = _lib.context(local)
+    stream = torch.cuda.current_stream()
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    out = None
+    for _ in range(args.warmup):
+        out = ransac_pnp_device(px_d, X_d, w_d, offsets, intr, seeds, cfg, out=out)
+    stats0 = out["stats"].cpu().numpy()
+    evals_per_step = int(stats0[:, 2].sum())
+    conv_rate = float(out["converged"].float().mean().item())
+
+    # ---- device-resident timed region (value)
+    ctx.profile(True)
+    l0 = ctx.launches()
+    sync_all()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            out = ransac_pnp_device(px_d, X_d, w_d, offsets, intr, seeds, cfg, out=out)
+        e1.record(stream)
+        sync_all()
+    launches = ctx.launches() - l0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    ms = e0.elapsed_time(e1)
+    t_local = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    evals_local = torch.tensor([float(evals_per_step)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(evals_local)
+    evals_total = float(evals_local.item()) * args.steps
+    value = evals_total / (ms_max / 1000.0)
+    queries_per_s = Q * world * args.steps / (ms_max / 1000.0)
+
+    # ---- end-to-end through the host-buffer API
+    e2e = None
+    if not args.no_e2e:
+        ransac_pnp_host(px_h, X_h, w_h, offsets, intr, seeds, cfg)  # warm
+        sync_all()
+        e0.record(stream)
+        h2d = d2h = 0
+        for _ in range(args.steps):
+            _, h2d, d2h = ransac_pnp_host(px_h, X_h, w_h, offsets, intr, seeds, cfg)
+        e1.record(stream)
+        sync_all()
+        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": evals_total / (float(ems.item()) / 1000.0), "unit": "evals/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "queries_per_s": Q * world * args.steps / (float(ems.item()) / 1000.0)}
+
+    # ---- roofline of the dominant kernel (fp32 MSAC scoring), live CUDA events
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    props = torch.cuda.get_device_properties(local)
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+    score_ms, score_launches = prof["score"]
+    achieved = (evals_per_step * args.steps * FLOP_PER_EVAL) / (score_ms / 1000.0) / 1e12 if score_ms else None
+    stage_ms = {k: round(v[0] / args.steps, 3) for k, v in prof.items()}
+    roof = {"bound": "fp32", "kernel": "k_score", "achieved": achieved, "peak": round(fp32_peak, 2),
+            "unit": "TFLOP/s", "frac": (achieved / fp32_peak) if achieved else None,
+            "peak_source": "derived SMs*128*2*sm_max_mhz (MEASURED_PEAKS.json has no FP32 entry)",
+            "flop_per_eval": FLOP_PER_EVAL, "traffic": None,
+            "evals_per_s_kernel": (evals_per_step * args.steps) / (score_ms / 1000.0) if score_ms else None,
+            "score_share_of_step": (score_ms / ms) if ms else None,
+            "score_launches": score_launches}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = host_cores()
+        ev, wall = cpu_sample(wl, seed0, cores * wl["cpu_queries_per_core"], cores)
+        cpu = {"value": ev / wall, "unit": "evals/s", "cores": cores, "kind": "port",
+               "sample": f"{cores * wl['cpu_queries_per_core']} queries of the same workload "
+                         f"(first queries, same seeds), oracle port, 1 process/core"}
+
+    if rank == 0:
+        line = {
+            "metric": "hyp×corr evals/s", "value": value, "unit": "evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+            "data": "synthetic",
+            "config": {"workload": wl["name"], "queries_per_gpu": Q, "corrs_per_query": n,
+                       "n_sub": min(n, 10_000), "max_iterations": wl["max_iterations"],
+                       "miss_probability": wl["eta"],
+                       "l2": f"inputs {px_h.numel() * 8 * 3 / 1e9:.2f} GB/GPU (> 126 MB L2; no flush needed)",
+                       "parallelism": f"query-sharded x{world}, no collective"},
+            "queries_per_s": queries_per_s, "converged_frac": conv_rate,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "clocks": clk.summary(), "gpu_launches": launches, "stage_ms_per_step": stage_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -98,6 +98,12 @@ int vl_reserve(vl_ctx* ctx, int32_t max_queries, int64_t max_n_per_query, int32_
 /* Number of kernel launches issued by this context since creation. */
 int64_t vl_launch_count(vl_ctx* ctx);
 
+/* Profiling: when enabled, every stage launch of vl_ransac_pnp is bracketed
+ * by CUDA events on the caller's stream and accumulated per stage (order:
+ * prep, sample, p3p, compact, score, scan, active, final).  Enabling resets. */
+int vl_profile(vl_ctx* ctx, int enable);
+int vl_profile_read(vl_ctx* ctx, double* ms, int64_t* launches, int32_t n);
+
 /* numpy SeedSequence(seed) -> PCG64 state (np.random.default_rng(seed),
  * posest.py:243).  Host-only helper, no device work. */
 int vl_pcg64_seed(uint64_t seed, vl_pcg64_state* out);

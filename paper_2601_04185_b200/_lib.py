@@ -83,13 +83,16 @@ def lib():
         L.vl_launch_count.restype = i64
         L.vl_reserve.argtypes = [vp, i32, i64, i32]
         L.vl_pcg64_seed.argtypes = [C.c_uint64, C.POINTER(PCG64State)]
+        L.vl_profile.argtypes = [vp, C.c_int]
+        L.vl_profile_read.argtypes = [vp, dp, C.POINTER(C.c_int64), i32]
         L.vl_ransac_pnp.argtypes = [vp, C.POINTER(RansacArgs), C.POINTER(RansacOut), vp]
         L.vl_msac_score.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, dbl, dp, vp, vp]
         L.vl_refine_pose.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, i32, dbl, i32, dbl, dbl,
                                      ip, ip, dp, ip, vp]
         L.vl_p3p_solve_batch.argtypes = [vp, vp, vp, i32, vp, vp, vp, ip, vp]
         L.vl_sample_minimal_sets.argtypes = [vp, C.POINTER(PCG64State), i64, i32, vp, vp]
-        for name in ("vl_create", "vl_destroy", "vl_reserve", "vl_pcg64_seed", "vl_ransac_pnp",
+        for name in ("vl_create", "vl_destroy", "vl_reserve", "vl_pcg64_seed", "vl_ransac_pnp", "vl_profile",
+                     "vl_profile_read",
                      "vl_msac_score", "vl_refine_pose", "vl_p3p_solve_batch", "vl_sample_minimal_sets"):
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -99,8 +102,10 @@ def lib():
 EXPORTED_SYMBOLS = (
     "vl_create", "vl_destroy", "vl_last_error", "vl_reserve", "vl_launch_count", "vl_pcg64_seed",
     "vl_ransac_pnp", "vl_msac_score", "vl_refine_pose", "vl_p3p_solve_batch",
-    "vl_sample_minimal_sets",
+    "vl_sample_minimal_sets", "vl_profile", "vl_profile_read",
 )
+
+STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final")
 
 
 class Context:
@@ -129,6 +134,15 @@ class Context:
 
     def launches(self) -> int:
         return int(lib().vl_launch_count(self.handle))
+
+    def profile(self, enable: bool):
+        lib().vl_profile(self.handle, 1 if enable else 0)
+
+    def profile_read(self) -> dict:
+        ms = (C.c_double * len(STAGES))()
+        cnt = (C.c_int64 * len(STAGES))()
+        lib().vl_profile_read(self.handle, ms, cnt, len(STAGES))
+        return {s: (float(ms[i]), int(cnt[i])) for i, s in enumerate(STAGES)}
 
     def __del__(self):
         try:

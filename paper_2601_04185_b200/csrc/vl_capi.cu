@@ -28,7 +28,45 @@ struct vl_ctx {
   DevBuf scratch;  // small standalone-call scratch
   void* h_pinned = nullptr;
   size_t h_pinned_cap = 0;
+  // profiling: CUDA-event brackets around every stage launch (vl_profile)
+  int prof = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> ev_stage;  // stage of each recorded pair
+  size_t ev_used = 0;
+  double stage_ms[kNumStages] = {0};
+  int64_t stage_launches[kNumStages] = {0};
+  cudaStream_t prof_stream = nullptr;
 };
+
+static void prof_hook(void* arg, int stage, bool begin) {
+  vl_ctx* c = (vl_ctx*)arg;
+  if (!c->prof) return;
+  if (begin) {
+    if (c->ev_used + 2 > c->ev_pool.size()) {
+      for (int k = 0; k < 64; ++k) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->ev_pool.push_back(e);
+      }
+    }
+    c->ev_stage.push_back(stage);
+  }
+  cudaEventRecord(c->ev_pool[c->ev_used++], c->prof_stream);
+}
+
+// Called after a stream sync: fold the recorded event pairs into the totals.
+static void prof_collect(vl_ctx* c) {
+  if (!c->prof) return;
+  for (size_t i = 0; i < c->ev_stage.size(); ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]) == cudaSuccess) {
+      c->stage_ms[c->ev_stage[i]] += ms;
+      c->stage_launches[c->ev_stage[i]] += 1;
+    }
+  }
+  c->ev_stage.clear();
+  c->ev_used = 0;
+}
 
 static int fail(vl_ctx* c, int code, const std::string& msg) {
   if (c) c->err = msg;
@@ -148,6 +186,7 @@ int vl_destroy(vl_ctx* c) {
                     &c->comp_X,  &c->comp_w, &c->scratch};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   delete c;
   return VL_OK;
@@ -156,6 +195,27 @@ int vl_destroy(vl_ctx* c) {
 const char* vl_last_error(vl_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 int64_t vl_launch_count(vl_ctx* c) { return c ? c->launches : -1; }
+
+int vl_profile(vl_ctx* c, int enable) {
+  if (!c) return VL_ERR_INVALID;
+  c->prof = enable ? 1 : 0;
+  for (int k = 0; k < kNumStages; ++k) {
+    c->stage_ms[k] = 0;
+    c->stage_launches[k] = 0;
+  }
+  c->ev_stage.clear();
+  c->ev_used = 0;
+  return VL_OK;
+}
+
+int vl_profile_read(vl_ctx* c, double* ms, int64_t* launches, int32_t n) {
+  if (!c || !ms || !launches) return VL_ERR_INVALID;
+  for (int k = 0; k < n && k < kNumStages; ++k) {
+    ms[k] = c->stage_ms[k];
+    launches[k] = c->stage_launches[k];
+  }
+  return VL_OK;
+}
 
 int vl_pcg64_seed(uint64_t seed, vl_pcg64_state* out) {
   if (!out) return VL_ERR_INVALID;
@@ -300,22 +360,31 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     VL_CUDA(c, cudaMemcpyAsync(wk.qs, h_qs, Qn * sizeof(QState), cudaMemcpyHostToDevice, st));
     VL_CUDA(c, cudaMemcpyAsync(wk.active_list, h_active, Qn * sizeof(int), cudaMemcpyHostToDevice, st));
     VL_CUDA(c, cudaMemsetAsync(wk.item_count, 0, sizeof(int), st));
+    c->prof_stream = st;
+    prof_hook(c, kStagePrep, true);
     c->launches += launch_prep(wk, in, Qn, st);
+    prof_hook(c, kStagePrep, false);
     if ((rc = check_launch(c))) return rc;
     int nactive = Qn;
     int guard = 0;
     const int64_t max_rounds = (cfg.max_iterations + B - 1) / B + 1;
     while (nactive > 0) {
-      c->launches += launch_round(wk, in, p, nactive, c->num_sms, st);
+      c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c);
       if ((rc = check_launch(c))) return rc;
       VL_CUDA(c, cudaMemcpyAsync(h_count, wk.active_count, sizeof(int), cudaMemcpyDeviceToHost, st));
       VL_CUDA(c, cudaStreamSynchronize(st));
+      prof_collect(c);
       nactive = *h_count;
       if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
     }
+    prof_hook(c, kStageFinal, true);
     c->launches += launch_final(wk, in, out, p, Qn, (int)q0, st);
+    prof_hook(c, kStageFinal, false);
     if ((rc = check_launch(c))) return rc;
-    if (q0 + Qc < Q) VL_CUDA(c, cudaStreamSynchronize(st));  // staging buffer reuse
+    if (q0 + Qc < Q || c->prof) {
+      VL_CUDA(c, cudaStreamSynchronize(st));  // staging buffer reuse / event readout
+      prof_collect(c);
+    }
   }
   return VL_OK;
 }

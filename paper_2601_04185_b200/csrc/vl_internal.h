@@ -90,8 +90,11 @@ struct Outputs {
 
 // ---- launchers (return number of kernels launched) -------------------------
 int launch_prep(const Work& wk, const Inputs& in, int Q, cudaStream_t st);
+// profiling stages (vl_profile_read order)
+enum { kStagePrep = 0, kStageSample, kStageP3P, kStageCompact, kStageScore, kStageScan, kStageActive,
+       kStageFinal, kNumStages };
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
-                 cudaStream_t st);
+                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg);
 int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
                  int q_base, cudaStream_t st);
 

@@ -400,23 +400,34 @@ __global__ void __launch_bounds__(1024) k_active(Work wk, int nactive) {
 
 int launch_score(const Work& wk, float tau2, int num_sms, cudaStream_t st);  // vl_score.cu
 
+// One round, kernel by kernel; `hook(stage, begin)` lets the caller bracket
+// each launch with CUDA events (profiling) without touching the kernels.
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
-                 cudaStream_t st) {
-  int n = 0;
+                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg) {
+  auto H = [&](int stage, bool begin) {
+    if (hook) hook(hook_arg, stage, begin);
+  };
+  H(kStageSample, true);
   k_sample<<<nactive, 256, 0, st>>>(wk, p);
-  ++n;
+  H(kStageSample, false);
+  H(kStageP3P, true);
   dim3 gp(nactive, (wk.B + 127) / 128);
   k_p3p<<<gp, 128, 0, st>>>(wk, in);
-  ++n;
+  H(kStageP3P, false);
+  H(kStageCompact, true);
   k_compact<<<nactive, 1024, 0, st>>>(wk);
-  ++n;
-  n += launch_score(wk, (float)(p.tau * p.tau), num_sms, st);
+  H(kStageCompact, false);
+  H(kStageScore, true);
+  launch_score(wk, (float)(p.tau * p.tau), num_sms, st);
+  H(kStageScore, false);
+  H(kStageScan, true);
   const size_t smem = (size_t)wk.HCAP * sizeof(float);
   k_scan<<<nactive, kScanThreads, smem, st>>>(wk, p);
-  ++n;
+  H(kStageScan, false);
+  H(kStageActive, true);
   k_active<<<1, 1024, 0, st>>>(wk, nactive);
-  ++n;
-  return n;
+  H(kStageActive, false);
+  return 6;
 }
 
 // ------------------------------------------------------------------ final stage

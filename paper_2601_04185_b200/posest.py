@@ -213,6 +213,27 @@ def _estimates_from(out, offsets) -> list[PoseEstimate]:
     return res
 
 
+def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig):
+    """Batched estimator on HOST buffers: H2D copy, device run, D2H of the results.
+
+    ``px``/``X``/``w`` are packed host arrays (numpy, or pinned torch CPU
+    tensors for full-bandwidth copies).  Returns a dict of numpy arrays
+    (q, t, flags, count, score, iterations, converged, stats) and the byte
+    counts moved each way.
+    """
+    import torch
+    _lib.context()
+    tens = []
+    for a in (px, X, w):
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        tens.append(t.to("cuda", non_blocking=True))
+    out = ransac_pnp_device(tens[0], tens[1], tens[2], offsets, intrinsics, seeds, cfg)
+    host = {k: v.cpu().numpy() for k, v in out.items()}
+    h2d = sum(int(t.numel() * t.element_size()) for t in tens)
+    d2h = sum(int(v.nbytes) for v in host.values())
+    return host, h2d, d2h
+
+
 def ransac_pnp_batch(queries, intrinsics, cfg: RansacConfig, seeds=None) -> list[PoseEstimate]:
     """Estimate many independent queries in one device-resident run.
 

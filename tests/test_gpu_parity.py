@@ -149,7 +149,7 @@ def test_ransac_matches_reference_golden(vl, intr, golden):
         _check_pose(e.pose.q, e.pose.t, g[f"r{k}_q"], g[f"r{k}_t"])
         ref_flags = np.unpackbits(g[f"r{k}_flags"])[: int(n)].astype(bool)
         _check_mask(e.inlier_flags, ref_flags, g[f"r{k}_q"], g[f"r{k}_t"], px, X)
-        assert math.isclose(e.score, float(g[f"r{k}_score"]), rel_tol=1e-6)
+        assert math.isclose(e.score, float(g[f"r{k}_score"]), rel_tol=1e-6, abs_tol=1e-9)
 
 
 def test_ransac_reference_behaviours(vl, intr):
