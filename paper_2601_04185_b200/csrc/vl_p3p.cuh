@@ -1,17 +1,21 @@
-// Per-thread fp64 P3P minimal solver, register resident.
+// fp64 P3P minimal solver building blocks, register resident.
 //
 // Same contract as pkg/src/visloc/p3p.py (p3p_solve_batch :57-203):
 //  * degeneracy gate (:91-98);
 //  * resultant quartic in v = s3/s1 with the reference's coefficient
 //    assembly (:108-141), so the polynomial is bit-identical;
 //  * real positive roots with |Im| <= 1e-6 (1 + |Re|), ascending (:147-166) —
-//    found here with Aberth-Ehrlich iterations seeded from the Newton
-//    polygon instead of a LAPACK companion-matrix eigensolve;
+//    all four complex roots are found with Aberth-Ehrlich iterations seeded
+//    from the Newton polygon (instead of a LAPACK companion-matrix eigensolve)
+//    and stopped once |p(z)| is at the rounding-error level of the
+//    evaluation, which is where geev's roots sit too;
 //  * u from the linear relation or both quadratic branches (:206-231);
 //  * 12 Newton steps on the three law-of-cosines quadrics (:245-277);
-//  * orthogonal Procrustes R = V D U^T (:279-293) — computed with a one-sided
-//    Jacobi SVD of the 3x3 cross-covariance; with three points the
-//    covariance has rank 2 and V D U^T = v1u1' + v2u2' + (v1xv2)(u1xu2)';
+//  * orthogonal Procrustes (:279-293): with three points both centred point
+//    sets are planar, so the SVD solution R = V D U^T equals "map the world
+//    triangle's plane frame onto the camera triangle's plane frame, then the
+//    closed-form 2-D Procrustes rotation in that plane" — evaluated here
+//    without an iterative SVD;
 //  * bearing-residual contract <= 1e-8 rad and positive depths (:295-305);
 //  * per-sample dedup (||dR||_F < 1e-6, ||dt|| < 1e-6 sqrt(scale2)), <= 4.
 #pragma once
@@ -23,153 +27,283 @@ constexpr double kBearingTol = 1e-8;
 constexpr double kCollinearTol = 1e-9;
 constexpr double kDedupTol = 1e-6;
 constexpr int kNewtonIters = 12;
+constexpr int kMaxCand = 8;  // 4 roots x 2 branches
+constexpr double kEps = 2.220446049250313e-16;
 
-struct cplx {
-  double re, im;
+// Per-sample geometry shared by root finding and candidate polishing.
+struct P3PGeo {
+  double f[9], P[9];
+  double a2, b2, c2, ca, cb, cg, scale2;
 };
-VL_HD cplx cmk(double r, double i) { return cplx{r, i}; }
-VL_HD cplx cadd(cplx a, cplx b) { return cplx{a.re + b.re, a.im + b.im}; }
-VL_HD cplx csub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
-VL_HD cplx cmul(cplx a, cplx b) { return cplx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
-VL_HD cplx cdiv(cplx a, cplx b) {
-  // Smith's algorithm
-  if (fabs(b.re) >= fabs(b.im)) {
-    const double r = b.im / b.re, d = b.re + b.im * r;
-    return cplx{(a.re + a.im * r) / d, (a.im - a.re * r) / d};
-  }
-  const double r = b.re / b.im, d = b.im + b.re * r;
-  return cplx{(a.re * r + a.im) / d, (a.im * r - a.re) / d};
-}
-VL_HD double cabs_(cplx a) { return hypot(a.re, a.im); }
 
-// Real positive roots (ascending) of sum_k c[k] v^(4-k); returns count.
+VL_HD void cross3(const double* a, const double* b, double* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+VL_HD double dot3(const double* a, const double* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+VL_HD double nrm3(const double* a) { return sqrt(dot3(a, a)); }
+
+// Gate + quartic coefficients (highest power first).  Returns false for a
+// degenerate sample.
+VL_HD bool p3p_setup(const double* f, const double* P, P3PGeo& g, double* quart) {
+  for (int i = 0; i < 9; ++i) {
+    g.f[i] = f[i];
+    g.P[i] = P[i];
+  }
+  double d12[3], d02[3], d01[3], e1v[3], e2v[3], cr[3];
+  for (int i = 0; i < 3; ++i) {
+    d12[i] = P[3 + i] - P[6 + i];
+    d02[i] = P[i] - P[6 + i];
+    d01[i] = P[i] - P[3 + i];
+    e1v[i] = P[3 + i] - P[i];
+    e2v[i] = P[6 + i] - P[i];
+  }
+  const double a2 = dot3(d12, d12), b2 = dot3(d02, d02), c2 = dot3(d01, d01);
+  const double ca = dot3(f + 3, f + 6), cb = dot3(f, f + 6), cg = dot3(f, f + 3);
+  cross3(e1v, e2v, cr);
+  const double scale2 = fmax(fmax(a2, b2), c2);
+  const double smin = fmin(fmin(a2, b2), c2);
+  g.a2 = a2;
+  g.b2 = b2;
+  g.c2 = c2;
+  g.ca = ca;
+  g.cb = cb;
+  g.cg = cg;
+  g.scale2 = scale2;
+  const bool ok = (scale2 > 0) && (smin > 1e-24 * scale2) &&
+                  (nrm3(cr) > kCollinearTol * nrm3(e1v) * nrm3(e2v)) && (fabs(ca) < 1.0) &&
+                  (fabs(cb) < 1.0) && (fabs(cg) < 1.0);
+  if (!ok) return false;
+  // quartic coefficients, assembled exactly like p3p.py:108-141
+  const double rb = 1.0 / (b2 > 0 ? b2 : 1.0);
+  const double q10 = -(c2 - b2) * rb, q11 = -(-2.0 * c2 * cb) * rb, q12 = -c2 * rb;
+  const double q20 = -a2 * rb, q21 = 2.0 * a2 * cb * rb, q22 = (b2 - a2) * rb;
+  const double d0 = q20 - q10, d1 = q21 - q11, d2 = q22 - q12;
+  const double e0 = -2.0 * cg, e1 = 2.0 * ca;
+  const double g0 = e0 * e0, g1 = 2 * e0 * e1, g2 = e1 * e1;
+  quart[0] = d2 * d2 + q12 * g2;
+  quart[1] = 2 * d1 * d2 + e0 * (d2 * e1) + (q11 * g2 + q12 * g1);
+  quart[2] = (d1 * d1 + 2 * d0 * d2) + e0 * (d1 * e1 + d2 * e0) + (q10 * g2 + q11 * g1 + q12 * g0);
+  quart[3] = 2 * d0 * d1 + e0 * (d0 * e1 + d1 * e0) + (q10 * g1 + q11 * g0);
+  quart[4] = d0 * d0 + e0 * (d0 * e0) + q10 * g0;
+  return true;
+}
+
+// Real positive roots (ascending) of sum_k c[k] v^(4-k); returns the count.
 // Mirrors np.roots' degree handling: exact leading/trailing zeros stripped,
 // zero roots never count (Re > 0 required).
 VL_HD int quartic_real_pos_roots(const double* c_in, double* out) {
   double mx = 0;
+#pragma unroll
   for (int k = 0; k < 5; ++k) mx = fmax(mx, fabs(c_in[k]));
-  if (!isfinite(mx) || mx == 0) return 0;  // non-finite or all-zero
+  if (!isfinite(mx) || mx == 0) return 0;
   double c[5];
+#pragma unroll
   for (int k = 0; k < 5; ++k) c[k] = c_in[k] / mx;
   int lead = 0;
-  while (lead < 5 && c[lead] == 0) ++lead;
+  while (lead < 4 && c[lead] == 0) ++lead;
   int last = 4;
   while (last > lead && c[last] == 0) --last;
-  const int d = last - lead;  // degree after stripping
+  const int d = last - lead;
   if (d <= 0) return 0;
-  // ascending coefficients b[k] of z^k, monic
+  // ascending monic coefficients b[k] of z^k (k <= d), zero-padded to 5
   double b[5];
-  for (int k = 0; k <= d; ++k) b[k] = c[last - k] / c[lead];
-  cplx z[4];
+  const double il = 1.0 / c[lead];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) b[k] = (k <= d) ? c[last - k] * il : 0.0;
+  double zr[4], zi[4];
+  bool conv[4];
   if (d == 1) {
-    z[0] = cmk(-b[0], 0.0);
+    zr[0] = -b[0];
+    zi[0] = 0.0;
   } else {
-    // Newton-polygon initial radii (upper convex hull of (k, log|b_k|)).
+    // Newton-polygon initial radii: upper convex hull of (k, log|b_k|).
     int hk[5];
-    double hl[5];
+    float hl[5];
     int nh = 0;
     for (int k = 0; k <= d; ++k) {
       if (b[k] == 0) continue;
-      const double lk = log(fabs(b[k]));
+      const float lk = logf((float)fabs(b[k]));
       while (nh >= 2) {
-        // pop if (hk[nh-2],hl[nh-2]) -> (hk[nh-1],hl[nh-1]) -> (k,lk) is not a right turn
-        const double cr = (hk[nh - 1] - hk[nh - 2]) * (lk - hl[nh - 2]) -
-                          (hl[nh - 1] - hl[nh - 2]) * (k - hk[nh - 2]);
-        if (cr >= 0) --nh;
+        const float cr = (float)(hk[nh - 1] - hk[nh - 2]) * (lk - hl[nh - 2]) -
+                         (hl[nh - 1] - hl[nh - 2]) * (float)(k - hk[nh - 2]);
+        if (cr >= 0.f) --nh;
         else break;
       }
       hk[nh] = k;
       hl[nh] = lk;
       ++nh;
     }
-    int zi = 0;
+    int zc = 0;
     for (int s = 0; s + 1 < nh; ++s) {
       const int m = hk[s + 1] - hk[s];
-      const double r = exp((hl[s] - hl[s + 1]) / m);
-      for (int j = 0; j < m && zi < d; ++j) {
-        const double ang = 6.283185307179586 * j / m + 1.5707963267948966 / d + 0.4 * s + 0.3;
-        z[zi++] = cmk(r * cos(ang), r * sin(ang));
+      const float r = expf((hl[s] - hl[s + 1]) / (float)m);
+      for (int j = 0; j < m && zc < d; ++j) {
+        const float ang = 6.2831853f * (float)j / (float)m + 1.5707963f / (float)d + 0.4f * s + 0.3f;
+        float sn, cs;
+        sincosf(ang, &sn, &cs);
+        zr[zc] = (double)(r * cs);
+        zi[zc] = (double)(r * sn);
+        ++zc;
       }
     }
-    while (zi < d) {  // defensive: hull always covers degree d
-      z[zi] = cmk(cos(1.0 + zi), sin(1.0 + zi));
-      ++zi;
+    for (; zc < d; ++zc) {  // defensive: the hull always covers degree d
+      zr[zc] = cos(1.0 + zc);
+      zi[zc] = sin(1.0 + zc);
     }
-    bool conv[4] = {false, false, false, false};
-    for (int it = 0; it < 80; ++it) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) conv[k] = (k >= d);
+    for (int it = 0; it < 60; ++it) {
       bool all = true;
-      for (int k = 0; k < d; ++k) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
         if (conv[k]) continue;
-        // Horner for p and p'
-        cplx p = cmk(b[d], 0.0), dp = cmk(0.0, 0.0);
-        for (int j = d - 1; j >= 0; --j) {
-          dp = cadd(cmul(dp, z[k]), p);
-          p = cadd(cmul(p, z[k]), cmk(b[j], 0.0));
+        const double xr = zr[k], xi = zi[k];
+        // Horner for p, p' and the rounding bound sum |b_j| |z|^j
+        const double az = sqrt(xr * xr + xi * xi);
+        double pr = b[4], pi = 0.0, dr = 0.0, di = 0.0, bnd = fabs(b[4]);
+#pragma unroll
+        for (int j = 3; j >= 0; --j) {
+          if (j >= d) {
+            pr = b[j];  // leading coefficient (monic 1 at j == d)
+            bnd = fabs(b[j]);
+            continue;
+          }
+          const double ndr = dr * xr - di * xi + pr, ndi = dr * xi + di * xr + pi;
+          const double npr = pr * xr - pi * xi + b[j], npi = pr * xi + pi * xr;
+          dr = ndr;
+          di = ndi;
+          pr = npr;
+          pi = npi;
+          bnd = bnd * az + fabs(b[j]);
         }
-        if (p.re == 0 && p.im == 0) {
+        if (sqrt(pr * pr + pi * pi) <= 8.0 * kEps * bnd) {
           conv[k] = true;
           continue;
         }
-        const cplx ratio = cdiv(p, dp);
-        cplx s = cmk(0.0, 0.0);
-        for (int j = 0; j < d; ++j)
-          if (j != k) s = cadd(s, cdiv(cmk(1.0, 0.0), csub(z[k], z[j])));
-        const cplx den = csub(cmk(1.0, 0.0), cmul(ratio, s));
-        const cplx corr = cdiv(ratio, den);
-        if (!(isfinite(corr.re) && isfinite(corr.im))) {
+        // ratio = p / p'
+        const double idd = 1.0 / (dr * dr + di * di);
+        const double rr = (pr * dr + pi * di) * idd, ri = (pi * dr - pr * di) * idd;
+        // S = sum_{j != k} 1 / (z_k - z_j)
+        double sr = 0.0, si = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j == k || j >= d) continue;
+          const double ur = xr - zr[j], ui = xi - zi[j];
+          const double iu = 1.0 / (ur * ur + ui * ui);
+          sr += ur * iu;
+          si -= ui * iu;
+        }
+        // corr = ratio / (1 - ratio * S)
+        const double er = 1.0 - (rr * sr - ri * si), ei = -(rr * si + ri * sr);
+        const double ie = 1.0 / (er * er + ei * ei);
+        const double cr_ = (rr * er + ri * ei) * ie, ci_ = (ri * er - rr * ei) * ie;
+        if (!(isfinite(cr_) && isfinite(ci_))) {
           conv[k] = true;
           continue;
         }
-        z[k] = csub(z[k], corr);
-        if (cabs_(corr) <= 4.0 * 2.220446049250313e-16 * cabs_(z[k])) conv[k] = true;
+        zr[k] = xr - cr_;
+        zi[k] = xi - ci_;
+        if (sqrt(cr_ * cr_ + ci_ * ci_) <= 4.0 * kEps * sqrt(zr[k] * zr[k] + zi[k] * zi[k])) conv[k] = true;
         else all = false;
       }
       if (all) break;
     }
   }
   int nr = 0;
-  for (int k = 0; k < d; ++k) {
-    if (fabs(z[k].im) <= 1e-6 * (1.0 + fabs(z[k].re)) && z[k].re > 0) {
-      // insertion sort ascending
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < d && fabs(zi[k]) <= 1e-6 * (1.0 + fabs(zr[k])) && zr[k] > 0) {
       int p = nr++;
-      while (p > 0 && out[p - 1] > z[k].re) {
+      while (p > 0 && out[p - 1] > zr[k]) {
         out[p] = out[p - 1];
         --p;
       }
-      out[p] = z[k].re;
+      out[p] = zr[k];
     }
   }
   return nr;
 }
 
-// 3x3 solve with partial pivoting; returns false if singular.
-VL_HD bool solve3(const double* Ain, const double* bin, double* x) {
-  double A[9], b[3];
-  for (int i = 0; i < 9; ++i) A[i] = Ain[i];
-  for (int i = 0; i < 3; ++i) b[i] = bin[i];
-  for (int k = 0; k < 3; ++k) {
-    int p = k;
-    for (int i = k + 1; i < 3; ++i)
-      if (fabs(A[3 * i + k]) > fabs(A[3 * p + k])) p = i;
-    if (A[3 * p + k] == 0) return false;
-    if (p != k) {
-      for (int j = 0; j < 3; ++j) {
-        double tmp = A[3 * k + j];
-        A[3 * k + j] = A[3 * p + j];
-        A[3 * p + j] = tmp;
-      }
-      double tb = b[k];
-      b[k] = b[p];
-      b[p] = tb;
+// Distance-triple candidates (s1, s2, s3) from the roots (p3p.py:206-231),
+// in reference order.  Returns the count (<= 8); candidate k is written to
+// cand[k*stride + 0..2] unless cand is null (count only).
+VL_HD int p3p_candidates(const P3PGeo& g, const double* vs, int nv, double* cand, int stride) {
+  int nc = 0;
+  auto put = [&](double a, double b, double c) {
+    if (cand) {
+      cand[stride * nc] = a;
+      cand[stride * nc + 1] = b;
+      cand[stride * nc + 2] = c;
     }
-    for (int i = k + 1; i < 3; ++i) {
-      const double f = A[3 * i + k] / A[3 * k + k];
-      for (int j = k; j < 3; ++j) A[3 * i + j] -= f * A[3 * k + j];
-      b[i] -= f * b[k];
+    ++nc;
+  };
+  for (int iv = 0; iv < nv; ++iv) {
+    const double v = vs[iv];
+    const double den = 1.0 + v * v - 2.0 * v * g.cb;
+    if (den <= 0) continue;
+    const double s1 = sqrt(g.b2 / den);
+    const double q1v = -((g.c2 * den - g.b2) / g.b2);
+    const double q2v = (g.b2 * v * v - g.a2 * den) / g.b2;
+    const double pd = -2.0 * g.cg + 2.0 * v * g.ca;
+    if (fabs(pd) > 1e-10) {
+      const double u = (q2v - q1v) / pd;
+      if (u > 0) put(s1, u * s1, v * s1);
+    } else {
+      const double disc = g.cg * g.cg - q1v;
+      if (disc < 0) continue;
+      const double r = sqrt(disc);
+      const double u0 = g.cg + r, u1 = g.cg - r;
+      if (u0 > 0) put(s1, u0 * s1, v * s1);
+      if (u1 > 0) put(s1, u1 * s1, v * s1);
     }
   }
+  return nc;
+}
+
+// 3x3 solve with partial pivoting; returns false on an exactly zero pivot.
+VL_HD bool solve3(const double* Ain, const double* bin, double* x) {
+  double A[9], b[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) A[i] = Ain[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) b[i] = bin[i];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    int p = k;
+#pragma unroll
+    for (int i = k + 1; i < 3; ++i)
+      if (fabs(A[3 * i + k]) > fabs(A[3 * p + k])) p = i;
+    // branch-free row swap (keeps A in registers)
+#pragma unroll
+    for (int i = k + 1; i < 3; ++i) {
+      if (p == i) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const double tmp = A[3 * k + j];
+          A[3 * k + j] = A[3 * i + j];
+          A[3 * i + j] = tmp;
+        }
+        const double tb = b[k];
+        b[k] = b[i];
+        b[i] = tb;
+      }
+    }
+    if (A[3 * k + k] == 0) return false;
+    const double inv = 1.0 / A[3 * k + k];
+#pragma unroll
+    for (int i = k + 1; i < 3; ++i) {
+      const double fct = A[3 * i + k] * inv;
+#pragma unroll
+      for (int j = k; j < 3; ++j) A[3 * i + j] -= fct * A[3 * k + j];
+      b[i] -= fct * b[k];
+    }
+  }
+#pragma unroll
   for (int i = 2; i >= 0; --i) {
     double s = b[i];
+#pragma unroll
     for (int j = i + 1; j < 3; ++j) s -= A[3 * i + j] * x[j];
     x[i] = s / A[3 * i + i];
   }
@@ -181,225 +315,139 @@ VL_HD double det3(const double* J) {
          J[2] * (J[3] * J[7] - J[4] * J[6]);
 }
 
-VL_HD void cross3(const double* a, const double* b, double* o) {
-  o[0] = a[1] * b[2] - a[2] * b[1];
-  o[1] = a[2] * b[0] - a[0] * b[2];
-  o[2] = a[0] * b[1] - a[1] * b[0];
+// Orthonormal frame (a, b, n) of the plane through three points.
+VL_HD void plane_frame(const double* X0, const double* X1, const double* X2, double* a, double* b, double* n) {
+  double e1[3], e2[3];
+  for (int i = 0; i < 3; ++i) {
+    e1[i] = X1[i] - X0[i];
+    e2[i] = X2[i] - X0[i];
+  }
+  cross3(e1, e2, n);
+  const double in = 1.0 / nrm3(n);
+  const double ia = 1.0 / nrm3(e1);
+  for (int i = 0; i < 3; ++i) {
+    n[i] *= in;
+    a[i] = e1[i] * ia;
+  }
+  cross3(n, a, b);
 }
-VL_HD double dot3(const double* a, const double* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
-VL_HD double nrm3(const double* a) { return sqrt(dot3(a, a)); }
 
-// Orthogonal Procrustes: R maximising tr(R^T ...) for H = sum Pc Yc^T,
-// R = V D U^T with H = U S V^T (one-sided Jacobi on H's columns).
-VL_HD void procrustes_R(const double* H, double* R) {
-  double A[9], V[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-  for (int i = 0; i < 9; ++i) A[i] = H[i];
-  for (int sweep = 0; sweep < 12; ++sweep) {
-    double off = 0;
-    for (int pq = 0; pq < 3; ++pq) {
-      const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2;
-      double al = 0, be = 0, ga = 0;
-      for (int i = 0; i < 3; ++i) {
-        al += A[3 * i + p] * A[3 * i + p];
-        be += A[3 * i + q] * A[3 * i + q];
-        ga += A[3 * i + p] * A[3 * i + q];
-      }
-      if (ga == 0) continue;
-      const double sc = fabs(ga) / sqrt(al * be);
-      if (!(sc > 1e-17)) continue;
-      off = fmax(off, sc);
-      const double zeta = (be - al) / (2.0 * ga);
-      const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-      const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
-      for (int i = 0; i < 3; ++i) {
-        const double ap = A[3 * i + p], aq = A[3 * i + q];
-        A[3 * i + p] = cs * ap - sn * aq;
-        A[3 * i + q] = sn * ap + cs * aq;
-        const double vp = V[3 * i + p], vq = V[3 * i + q];
-        V[3 * i + p] = cs * vp - sn * vq;
-        V[3 * i + q] = sn * vp + cs * vq;
-      }
+// Newton polish of one distance triple, then Procrustes and the bearing
+// contract.  Returns false for an invalid candidate.
+VL_HD bool p3p_polish(const P3PGeo& g, const double* s_in, double* R, double* t) {
+  double s0 = s_in[0], s1 = s_in[1], s2 = s_in[2];
+  for (int it = 0; it < kNewtonIters; ++it) {
+    const double r0 = s0 * s0 + s1 * s1 - 2 * s0 * s1 * g.cg - g.c2;
+    const double r1 = s0 * s0 + s2 * s2 - 2 * s0 * s2 * g.cb - g.b2;
+    const double r2 = s1 * s1 + s2 * s2 - 2 * s1 * s2 * g.ca - g.a2;
+    const double mr = fmax(fmax(fabs(r0), fabs(r1)), fabs(r2));
+    if (!(mr >= 1e-14 * g.scale2)) break;  // converged (inactive)
+    const double J[9] = {2 * s0 - 2 * s1 * g.cg, 2 * s1 - 2 * s0 * g.cg, 0.0,
+                         2 * s0 - 2 * s2 * g.cb, 0.0,                    2 * s2 - 2 * s0 * g.cb,
+                         0.0,                    2 * s1 - 2 * s2 * g.ca, 2 * s2 - 2 * s1 * g.ca};
+    const double dj = det3(J);
+    if (!(fabs(dj) > 1e-300 && isfinite(dj))) return false;
+    const double rhs[3] = {-r0, -r1, -r2};
+    double st[3];
+    if (!solve3(J, rhs, st)) return false;
+    s0 += st[0];
+    s1 += st[1];
+    s2 += st[2];
+    if (!(isfinite(s0) && isfinite(s1) && isfinite(s2)) || s0 <= 0 || s1 <= 0 || s2 <= 0) return false;
+  }
+  const double* f = g.f;
+  const double* P = g.P;
+  double Y[9];
+  for (int i = 0; i < 3; ++i) {
+    Y[i] = s0 * f[i];
+    Y[3 + i] = s1 * f[3 + i];
+    Y[6 + i] = s2 * f[6 + i];
+  }
+  double Pm[3], Ym[3];
+  for (int i = 0; i < 3; ++i) {
+    Pm[i] = ((P[i] + P[3 + i]) + P[6 + i]) / 3.0;
+    Ym[i] = ((Y[i] + Y[3 + i]) + Y[6 + i]) / 3.0;
+  }
+  // Plane frames of both triangles; R = F_Y * Rot2(theta) * F_P^T with the
+  // closed-form 2-D Procrustes angle of the centred in-plane coordinates.
+  double aP[3], bP[3], nP[3], aY[3], bY[3], nY[3];
+  plane_frame(P, P + 3, P + 6, aP, bP, nP);
+  plane_frame(Y, Y + 3, Y + 6, aY, bY, nY);
+  double sc = 0.0, ss = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    double pc[3], yc[3];
+    for (int i = 0; i < 3; ++i) {
+      pc[i] = P[3 * k + i] - Pm[i];
+      yc[i] = Y[3 * k + i] - Ym[i];
     }
-    if (off < 1e-15) break;
+    const double px = dot3(pc, aP), py = dot3(pc, bP);
+    const double yx = dot3(yc, aY), yy = dot3(yc, bY);
+    sc += px * yx + py * yy;
+    ss += px * yy - py * yx;
   }
-  double sg[3];
-  for (int k = 0; k < 3; ++k) sg[k] = sqrt(A[k] * A[k] + A[3 + k] * A[3 + k] + A[6 + k] * A[6 + k]);
-  // indices of the two largest singular values
-  int i1 = 0;
-  for (int k = 1; k < 3; ++k)
-    if (sg[k] > sg[i1]) i1 = k;
-  int i2 = i1 == 0 ? 1 : 0;
-  for (int k = 0; k < 3; ++k)
-    if (k != i1 && sg[k] > sg[i2]) i2 = k;
-  double u1[3], u2[3], v1[3], v2[3], u3[3], v3[3];
+  const double ih = 1.0 / sqrt(sc * sc + ss * ss);
+  const double cth = sc * ih, sth = ss * ih;
+  // columns of the rotated camera frame: a' = c aY + s bY, b' = -s aY + c bY
+  double ar[3], br[3];
   for (int i = 0; i < 3; ++i) {
-    u1[i] = A[3 * i + i1] / sg[i1];
-    u2[i] = A[3 * i + i2] / sg[i2];
-    v1[i] = V[3 * i + i1];
-    v2[i] = V[3 * i + i2];
+    ar[i] = cth * aY[i] + sth * bY[i];
+    br[i] = -sth * aY[i] + cth * bY[i];
   }
-  cross3(u1, u2, u3);
-  cross3(v1, v2, v3);
   for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) R[3 * i + j] = v1[i] * u1[j] + v2[i] * u2[j] + v3[i] * u3[j];
+    for (int j = 0; j < 3; ++j) R[3 * i + j] = ar[i] * aP[j] + br[i] * bP[j] + nY[i] * nP[j];
+  for (int i = 0; i < 3; ++i) t[i] = Ym[i] - (R[3 * i] * Pm[0] + R[3 * i + 1] * Pm[1] + R[3 * i + 2] * Pm[2]);
+  // contract: every bearing reproduced to 1e-8 rad, positive norms
+  for (int k = 0; k < 3; ++k) {
+    double pr[3];
+    for (int i = 0; i < 3; ++i)
+      pr[i] = (R[3 * i] * P[3 * k] + R[3 * i + 1] * P[3 * k + 1] + R[3 * i + 2] * P[3 * k + 2]) + t[i];
+    const double nr = nrm3(pr);
+    if (!(nr > 0)) return false;
+    const double inr = 1.0 / nr;
+    for (int i = 0; i < 3; ++i) pr[i] *= inr;
+    double cx[3];
+    cross3(pr, f + 3 * k, cx);
+    const double ang = atan2(nrm3(cx), dot3(pr, f + 3 * k));
+    if (!(ang <= kBearingTol)) return false;
+  }
+  return true;
 }
 
-// Solve one minimal sample.  f, P: row-major (3 points x 3).  Returns the
-// number of solutions written to Rs[k*9], ts[k*3] in reference order.
+VL_HD bool p3p_is_dup(const double* R, const double* t, const double* Rk, const double* tk, double ttol) {
+  double dr = 0, dt = 0;
+  for (int i = 0; i < 9; ++i) {
+    const double e = R[i] - Rk[i];
+    dr += e * e;
+  }
+  for (int i = 0; i < 3; ++i) {
+    const double e = t[i] - tk[i];
+    dt += e * e;
+  }
+  return sqrt(dr) < kDedupTol && sqrt(dt) < ttol;
+}
+
+// Whole-sample solve (sequential over candidates).  Returns the number of
+// solutions written to Rs[k*9], ts[k*3] in reference order.
 VL_HD int p3p_solve_one(const double* f, const double* P, double* Rs, double* ts) {
-  double d12[3], d02[3], d01[3];
-  for (int i = 0; i < 3; ++i) {
-    d12[i] = P[3 + i] - P[6 + i];
-    d02[i] = P[i] - P[6 + i];
-    d01[i] = P[i] - P[3 + i];
-  }
-  const double a2 = dot3(d12, d12), b2 = dot3(d02, d02), c2 = dot3(d01, d01);
-  const double ca = dot3(f + 3, f + 6), cb = dot3(f, f + 6), cg = dot3(f, f + 3);
-  double e1v[3], e2v[3], cr[3];
-  for (int i = 0; i < 3; ++i) {
-    e1v[i] = P[3 + i] - P[i];
-    e2v[i] = P[6 + i] - P[i];
-  }
-  cross3(e1v, e2v, cr);
-  const double scale2 = fmax(fmax(a2, b2), c2);
-  const double smin = fmin(fmin(a2, b2), c2);
-  const bool ok = (scale2 > 0) && (smin > 1e-24 * scale2) &&
-                  (nrm3(cr) > kCollinearTol * nrm3(e1v) * nrm3(e2v)) && (fabs(ca) < 1.0) &&
-                  (fabs(cb) < 1.0) && (fabs(cg) < 1.0);
-  if (!ok) return 0;
-
-  // quartic coefficients, assembled exactly like p3p.py:108-141
-  const double rb = 1.0 / (b2 > 0 ? b2 : 1.0);
-  const double q10 = -(c2 - b2) * rb, q11 = -(-2.0 * c2 * cb) * rb, q12 = -c2 * rb;
-  const double q20 = -a2 * rb, q21 = 2.0 * a2 * cb * rb, q22 = (b2 - a2) * rb;
-  const double d0 = q20 - q10, d1 = q21 - q11, d2 = q22 - q12;
-  const double e0 = -2.0 * cg, e1 = 2.0 * ca;
-  const double g0 = e0 * e0, g1 = 2 * e0 * e1, g2 = e1 * e1;
+  P3PGeo g;
   double quart[5];
-  quart[0] = d2 * d2 + q12 * g2;
-  quart[1] = 2 * d1 * d2 + e0 * (d2 * e1) + (q11 * g2 + q12 * g1);
-  quart[2] = (d1 * d1 + 2 * d0 * d2) + e0 * (d1 * e1 + d2 * e0) + (q10 * g2 + q11 * g1 + q12 * g0);
-  quart[3] = 2 * d0 * d1 + e0 * (d0 * e1 + d1 * e0) + (q10 * g1 + q11 * g0);
-  quart[4] = d0 * d0 + e0 * (d0 * e0) + q10 * g0;
-
+  if (!p3p_setup(f, P, g, quart)) return 0;
   double vs[4];
   const int nv = quartic_real_pos_roots(quart, vs);
   if (nv == 0) return 0;
-
+  double cand[3 * kMaxCand];
+  const int nc = p3p_candidates(g, vs, nv, cand, 3);
+  const double ttol = kDedupTol * sqrt(g.scale2);
   int nsol = 0;
-  const double ttol = kDedupTol * sqrt(scale2);
-  for (int iv = 0; iv < nv; ++iv) {
-    const double v = vs[iv];
-    const double den = 1.0 + v * v - 2.0 * v * cb;
-    if (den <= 0) continue;
-    const double s1 = sqrt(b2 / den);
-    const double q1v = -((c2 * den - b2) / b2);
-    const double q2v = (b2 * v * v - a2 * den) / b2;
-    const double pd = -2.0 * cg + 2.0 * v * ca;
-    double us[2];
-    int nu = 0;
-    if (fabs(pd) > 1e-10) {
-      us[nu++] = (q2v - q1v) / pd;
-    } else {
-      const double disc = cg * cg - q1v;
-      if (disc < 0) continue;
-      const double r = sqrt(disc);
-      us[nu++] = cg + r;
-      us[nu++] = cg - r;
-    }
-    for (int iu = 0; iu < nu; ++iu) {
-      const double u = us[iu];
-      if (u <= 0) continue;
-      if (nsol >= kMaxSolPerSample) return nsol;
-      // ---- Newton polish of (s1, s2, s3)
-      double s[3] = {s1, u * s1, v * s1};
-      bool valid = true;
-      for (int it = 0; it < kNewtonIters; ++it) {
-        const double x = s[0], y = s[1], z = s[2];
-        double r[3] = {x * x + y * y - 2 * x * y * cg - c2, x * x + z * z - 2 * x * z * cb - b2,
-                       y * y + z * z - 2 * y * z * ca - a2};
-        const double mr = fmax(fmax(fabs(r[0]), fabs(r[1])), fabs(r[2]));
-        if (!(mr >= 1e-14 * scale2)) break;  // inactive (converged)
-        const double J[9] = {2 * x - 2 * y * cg, 2 * y - 2 * x * cg, 0.0,
-                             2 * x - 2 * z * cb, 0.0,                2 * z - 2 * x * cb,
-                             0.0,                2 * y - 2 * z * ca, 2 * z - 2 * y * ca};
-        const double dj = det3(J);
-        if (!(fabs(dj) > 1e-300 && isfinite(dj))) {
-          valid = false;
-          break;
-        }
-        const double mrhs[3] = {-r[0], -r[1], -r[2]};
-        double st[3];
-        if (!solve3(J, mrhs, st)) {
-          valid = false;
-          break;
-        }
-        s[0] = x + st[0];
-        s[1] = y + st[1];
-        s[2] = z + st[2];
-        if (!(isfinite(s[0]) && isfinite(s[1]) && isfinite(s[2])) || s[0] <= 0 || s[1] <= 0 ||
-            s[2] <= 0) {
-          valid = false;
-          break;
-        }
-      }
-      if (!valid) continue;
-      // ---- Procrustes
-      double Y[9];
-      for (int n = 0; n < 3; ++n)
-        for (int i = 0; i < 3; ++i) Y[3 * n + i] = s[n] * f[3 * n + i];
-      double Pm[3], Ym[3];
-      for (int i = 0; i < 3; ++i) {
-        Pm[i] = ((P[i] + P[3 + i]) + P[6 + i]) / 3.0;
-        Ym[i] = ((Y[i] + Y[3 + i]) + Y[6 + i]) / 3.0;
-      }
-      double H[9];
-      for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) {
-          double acc = 0;
-          for (int n = 0; n < 3; ++n) acc += (P[3 * n + i] - Pm[i]) * (Y[3 * n + j] - Ym[j]);
-          H[3 * i + j] = acc;
-        }
-      double R[9], t[3];
-      procrustes_R(H, R);
-      for (int i = 0; i < 3; ++i) t[i] = Ym[i] - (R[3 * i] * Pm[0] + R[3 * i + 1] * Pm[1] + R[3 * i + 2] * Pm[2]);
-      // ---- contract: every bearing reproduced to 1e-8 rad, positive norms
-      bool good = true;
-      for (int n = 0; n < 3 && good; ++n) {
-        double pr[3];
-        for (int i = 0; i < 3; ++i)
-          pr[i] = (R[3 * i] * P[3 * n] + R[3 * i + 1] * P[3 * n + 1] + R[3 * i + 2] * P[3 * n + 2]) + t[i];
-        const double nr = nrm3(pr);
-        if (!(nr > 0)) {
-          good = false;
-          break;
-        }
-        for (int i = 0; i < 3; ++i) pr[i] /= nr;
-        double cx[3];
-        cross3(pr, f + 3 * n, cx);
-        const double ang = atan2(nrm3(cx), dot3(pr, f + 3 * n));
-        if (!(ang <= kBearingTol)) good = false;
-      }
-      if (!good) continue;
-      // ---- dedup against kept solutions of this sample
-      bool dup = false;
-      for (int k = 0; k < nsol && !dup; ++k) {
-        double dr = 0, dt = 0;
-        for (int i = 0; i < 9; ++i) {
-          const double e = R[i] - Rs[9 * k + i];
-          dr += e * e;
-        }
-        for (int i = 0; i < 3; ++i) {
-          const double e = t[i] - ts[3 * k + i];
-          dt += e * e;
-        }
-        if (sqrt(dr) < kDedupTol && sqrt(dt) < ttol) dup = true;
-      }
-      if (dup) continue;
-      for (int i = 0; i < 9; ++i) Rs[9 * nsol + i] = R[i];
-      for (int i = 0; i < 3; ++i) ts[3 * nsol + i] = t[i];
-      ++nsol;
-    }
+  for (int c = 0; c < nc && nsol < kMaxSolPerSample; ++c) {
+    double R[9], t[3];
+    if (!p3p_polish(g, cand + 3 * c, R, t)) continue;
+    bool dup = false;
+    for (int k = 0; k < nsol && !dup; ++k) dup = p3p_is_dup(R, t, Rs + 9 * k, ts + 3 * k, ttol);
+    if (dup) continue;
+    for (int i = 0; i < 9; ++i) Rs[9 * nsol + i] = R[i];
+    for (int i = 0; i < 3; ++i) ts[3 * nsol + i] = t[i];
+    ++nsol;
   }
   return nsol;
 }

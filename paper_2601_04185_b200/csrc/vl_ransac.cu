@@ -135,28 +135,92 @@ __device__ __forceinline__ void bearing(const double* px, const Intr& in, double
   f[2] = 1.0 / nr;
 }
 
-__global__ void __launch_bounds__(128) k_p3p(Work wk, Inputs in) {
+// Warp-cooperative P3P.  Phase 1: lane = minimal sample (gate, quartic,
+// roots, distance-triple candidates).  The warp's candidates are compacted
+// in (sample, root) order into shared memory; phase 2 polishes them 32 at a
+// time (lane = candidate: Newton + Procrustes + contract), so the ~1.5
+// candidates per sample keep every lane busy instead of diverging per
+// sample.  Phase 3: each sample's owner lane dedups its candidates in order
+// into the sample's solution slots (<= 4), exactly the reference's order.
+constexpr int kP3PThreads = 64;
+struct CandRec {
+  double s0, s1, s2;
+  int lane, pad;
+};
+
+__global__ void __launch_bounds__(kP3PThreads) k_p3p(Work wk, Inputs in) {
+  __shared__ P3PGeo geo[kP3PThreads];
+  __shared__ CandRec cand[kP3PThreads / 32][32 * kMaxCand];
+  __shared__ double res[kP3PThreads / 32][32][13];
   const int q = wk.active_list[blockIdx.x];
   const QState& S = wk.qs[q];
-  const int s = blockIdx.y * blockDim.x + threadIdx.x;
-  if (s >= S.batch_n) return;
-  const int* smp = wk.samples + ((int64_t)q * wk.B + s) * 3;
-  double f[9], P[9];
-  for (int k = 0; k < 3; ++k) {
-    const int64_t r = S.off + smp[k];
-    bearing(in.px + 2 * r, S.in, f + 3 * k);
-    P[3 * k] = in.X[3 * r];
-    P[3 * k + 1] = in.X[3 * r + 1];
-    P[3 * k + 2] = in.X[3 * r + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = blockIdx.y * kP3PThreads + threadIdx.x;
+  const bool live = s < S.batch_n;
+  int nc = 0, nv = 0;
+  double vs[4];
+  P3PGeo& g = geo[threadIdx.x];
+  if (live) {
+    const int* smp = wk.samples + ((int64_t)q * wk.B + s) * 3;
+    double f[9], P[9];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int64_t r = S.off + smp[k];
+      bearing(in.px + 2 * r, S.in, f + 3 * k);
+      P[3 * k] = in.X[3 * r];
+      P[3 * k + 1] = in.X[3 * r + 1];
+      P[3 * k + 2] = in.X[3 * r + 2];
+    }
+    double quart[5];
+    if (p3p_setup(f, P, g, quart)) {
+      nv = quartic_real_pos_roots(quart, vs);
+      if (nv) nc = p3p_candidates(g, vs, nv, nullptr, 0);
+    }
   }
-  double Rs[36], ts[12];
-  const int c = p3p_solve_one(f, P, Rs, ts);
+  // warp exclusive scan of candidate counts
+  int incl = nc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int base = incl - nc;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (nc) {
+    p3p_candidates(g, vs, nv, &cand[wid][base].s0, 4);
+    for (int i = 0; i < nc; ++i) cand[wid][base + i].lane = lane;
+  }
+  __syncwarp();
   double* slot = wk.slots + ((int64_t)q * wk.B + s) * (4 * 12);
-  for (int k = 0; k < c; ++k) {
-    for (int i = 0; i < 9; ++i) slot[12 * k + i] = Rs[9 * k + i];
-    for (int i = 0; i < 3; ++i) slot[12 * k + 9 + i] = ts[3 * k + i];
+  const double ttol = live ? kDedupTol * sqrt(g.scale2) : 0.0;
+  int kept = 0;
+  for (int ch = 0; ch < total; ch += 32) {
+    const int j = ch + lane;
+    if (j < total) {
+      const CandRec cr = cand[wid][j];
+      double R[9], t[3];
+      const double sv[3] = {cr.s0, cr.s1, cr.s2};
+      const bool ok = p3p_polish(geo[wid * 32 + cr.lane], sv, R, t);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) res[wid][lane][i] = R[i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) res[wid][lane][9 + i] = t[i];
+      res[wid][lane][12] = ok ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    const int e0 = max(base, ch), e1 = min(base + nc, ch + 32);
+    for (int e = e0; e < e1; ++e) {
+      const double* rr = res[wid][e - ch];
+      if (rr[12] == 0.0 || kept >= kMaxSolPerSample) continue;
+      bool dup = false;
+      for (int k = 0; k < kept && !dup; ++k) dup = p3p_is_dup(rr, rr + 9, slot + 12 * k, slot + 12 * k + 9, ttol);
+      if (dup) continue;
+      for (int i = 0; i < 12; ++i) slot[12 * kept + i] = rr[i];
+      ++kept;
+    }
+    __syncwarp();
   }
-  wk.slot_cnt[(int64_t)q * wk.B + s] = c;
+  if (live) wk.slot_cnt[(int64_t)q * wk.B + s] = kept;
 }
 
 __global__ void __launch_bounds__(128) k_p3p_batch(const double* f, const double* P, int B, double* slots,
@@ -411,8 +475,8 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   k_sample<<<nactive, 256, 0, st>>>(wk, p);
   H(kStageSample, false);
   H(kStageP3P, true);
-  dim3 gp(nactive, (wk.B + 127) / 128);
-  k_p3p<<<gp, 128, 0, st>>>(wk, in);
+  dim3 gp(nactive, (wk.B + kP3PThreads - 1) / kP3PThreads);
+  k_p3p<<<gp, kP3PThreads, 0, st>>>(wk, in);
   H(kStageP3P, false);
   H(kStageCompact, true);
   k_compact<<<nactive, 1024, 0, st>>>(wk);
