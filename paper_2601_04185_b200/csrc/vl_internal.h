@@ -9,8 +9,8 @@ namespace vl {
 
 // Scoring tile geometry (vl_score.cu).
 constexpr int kScoreThreads = 128;
-constexpr int kScoreHypPerThread = 4;
-constexpr int kScoreTileHyps = kScoreThreads * kScoreHypPerThread;  // 512
+constexpr int kScoreHypPerThread = 6;  // 3 f32x2 pairs (tools/score_bench.cu sweep)
+constexpr int kScoreTileHyps = kScoreThreads * kScoreHypPerThread;  // 768
 constexpr int kScoreChunk = 512;  // correspondences per split (fixed => launch-independent sums)
 
 // Per-query device state of the batched estimator.

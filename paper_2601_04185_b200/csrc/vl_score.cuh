@@ -1,0 +1,150 @@
+// fp32 MSAC hypothesis scoring — kernel template (see vl_score.cu).
+#pragma once
+#include "vl_internal.h"
+
+namespace vl {
+
+__device__ __forceinline__ float rsqrt_approx_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// One evaluation: e = w * min(|pi(P X) - px|^2, tau^2), behind-camera -> tau^2.
+// P rows are pre-multiplied by fx / fy; a.w, b.x hold f32(cx - u), f32(cy - v).
+#define VL_SCORE_EVAL(Pj, accj)                                                       \
+  {                                                                                   \
+    const float x_ = fmaf(Pj[0], a.x, fmaf(Pj[1], a.y, fmaf(Pj[2], a.z, Pj[3])));     \
+    const float y_ = fmaf(Pj[4], a.x, fmaf(Pj[5], a.y, fmaf(Pj[6], a.z, Pj[7])));     \
+    const float z_ = fmaf(Pj[8], a.x, fmaf(Pj[9], a.y, fmaf(Pj[10], a.z, Pj[11])));   \
+    const float rs_ = rsqrt_approx_ftz(z_);                                           \
+    const float r_ = rs_ * rs_;                                                       \
+    const float du_ = fmaf(x_, r_, a.w);                                              \
+    const float dv_ = fmaf(y_, r_, b.x);                                              \
+    const float e2_ = fminf(fmaf(du_, du_, dv_ * dv_), tau2);                         \
+    accj = fmaf(b.y, e2_, accj);                                                      \
+  }
+
+// Persistent grid over work items (query, tile of NT*HT hypotheses, split of
+// CH correspondences).  Thread t owns hypotheses tile*NT*HT + j*NT + t.
+template <int NT, int HT, int CH, int MINB, int UNR>
+__global__ void __launch_bounds__(NT, MINB) k_score_t(Work wk, float tau2) {
+  __shared__ float4 rec[2 * CH];
+  const int nitems = *wk.item_count;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const ScoreItem item = wk.items[it];
+    const QState& S = wk.qs[item.q];
+    const int nh = S.nh, nsub = S.nsub;
+    const int c0 = item.split * CH;
+    const int cn = min(CH, nsub - c0);
+    const float4* src = wk.sub32 + 2 * (S.sub_off + c0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < 2 * cn; k += NT) rec[k] = src[k];
+    float P[HT][12];
+    int hid[HT];
+    const float* Pq = wk.P32 + (int64_t)item.q * 12 * wk.HCAP;
+#pragma unroll
+    for (int j = 0; j < HT; ++j) {
+      const int h = item.tile * (NT * HT) + j * NT + threadIdx.x;
+      hid[j] = h;
+      const int hc = h < nh ? h : 0;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) P[j][c] = Pq[(int64_t)c * wk.HCAP + hc];
+    }
+    __syncthreads();
+    float acc[HT];
+#pragma unroll
+    for (int j = 0; j < HT; ++j) acc[j] = 0.f;
+#pragma unroll UNR
+    for (int c = 0; c < cn; ++c) {
+      const float4 a = rec[2 * c];
+      const float4 b = rec[2 * c + 1];
+#pragma unroll
+      for (int j = 0; j < HT; ++j) VL_SCORE_EVAL(P[j], acc[j]);
+    }
+    float* out = wk.partial + ((int64_t)item.q * wk.NSPLIT + item.split) * wk.HCAP;
+#pragma unroll
+    for (int j = 0; j < HT; ++j)
+      if (hid[j] < nh) out[hid[j]] = acc[j];
+  }
+}
+
+// ---------------------------------------------------------------- f32x2 path
+// Blackwell packed FP32 (FFMA2 / FMUL2): one instruction evaluates the same
+// step for two hypotheses; the correspondence coordinate is a scalar operand
+// broadcast to both halves (SASS `Rn.F32`).  Per pair of evaluations:
+// 9 + 1 + 2 + 2 + 1 = 15 FFMA2/FMUL2, 2 MUFU.RSQ, 2 FMNMX — ~10 issue slots
+// per evaluation instead of ~17, so the kernel becomes FMA-pipe bound
+// rather than issue bound.  Arithmetic per component is identical to the
+// scalar path (same fused operations, same order).
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __ffma2_rn(a, b, make_float2(-0.f, -0.f)); }
+
+#define VL_SCORE_EVAL2(Pp, accp)                                                                  \
+  {                                                                                               \
+    const float2 x_ = fma2(Pp[0], f2(a.x), fma2(Pp[1], f2(a.y), fma2(Pp[2], f2(a.z), Pp[3])));    \
+    const float2 y_ = fma2(Pp[4], f2(a.x), fma2(Pp[5], f2(a.y), fma2(Pp[6], f2(a.z), Pp[7])));    \
+    const float2 z_ = fma2(Pp[8], f2(a.x), fma2(Pp[9], f2(a.y), fma2(Pp[10], f2(a.z), Pp[11])));  \
+    const float2 rs_ = make_float2(rsqrt_approx_ftz(z_.x), rsqrt_approx_ftz(z_.y));              \
+    const float2 r_ = mul2(rs_, rs_);                                                             \
+    const float2 du_ = fma2(x_, r_, f2(a.w));                                                     \
+    const float2 dv_ = fma2(y_, r_, f2(b.x));                                                     \
+    float2 e2_ = fma2(du_, du_, mul2(dv_, dv_));                                                  \
+    e2_.x = fminf(e2_.x, tau2);                                                                   \
+    e2_.y = fminf(e2_.y, tau2);                                                                   \
+    accp = fma2(f2(b.y), e2_, accp);                                                              \
+  }
+
+template <int NT, int HT, int CH, int MINB, int UNR>
+__global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
+  static_assert(HT % 2 == 0, "hypotheses are processed in pairs");
+  constexpr int HP = HT / 2;
+  __shared__ float4 rec[2 * CH];
+  const int nitems = *wk.item_count;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const ScoreItem item = wk.items[it];
+    const QState& S = wk.qs[item.q];
+    const int nh = S.nh, nsub = S.nsub;
+    const int c0 = item.split * CH;
+    const int cn = min(CH, nsub - c0);
+    const float4* src = wk.sub32 + 2 * (S.sub_off + c0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < 2 * cn; k += NT) rec[k] = src[k];
+    float2 P[HP][12];
+    int hid[HT];
+    const float* Pq = wk.P32 + (int64_t)item.q * 12 * wk.HCAP;
+#pragma unroll
+    for (int j = 0; j < HT; ++j) {
+      const int h = item.tile * (NT * HT) + j * NT + threadIdx.x;
+      hid[j] = h;
+    }
+#pragma unroll
+    for (int jp = 0; jp < HP; ++jp) {
+      const int h0 = hid[2 * jp] < nh ? hid[2 * jp] : 0;
+      const int h1 = hid[2 * jp + 1] < nh ? hid[2 * jp + 1] : 0;
+#pragma unroll
+      for (int c = 0; c < 12; ++c)
+        P[jp][c] = make_float2(Pq[(int64_t)c * wk.HCAP + h0], Pq[(int64_t)c * wk.HCAP + h1]);
+    }
+    __syncthreads();
+    float2 acc[HP];
+#pragma unroll
+    for (int jp = 0; jp < HP; ++jp) acc[jp] = make_float2(0.f, 0.f);
+#pragma unroll UNR
+    for (int c = 0; c < cn; ++c) {
+      const float4 a = rec[2 * c];
+      const float4 b = rec[2 * c + 1];
+#pragma unroll
+      for (int jp = 0; jp < HP; ++jp) VL_SCORE_EVAL2(P[jp], acc[jp]);
+    }
+    float* out = wk.partial + ((int64_t)item.q * wk.NSPLIT + item.split) * wk.HCAP;
+#pragma unroll
+    for (int jp = 0; jp < HP; ++jp) {
+      if (hid[2 * jp] < nh) out[hid[2 * jp]] = acc[jp].x;
+      if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = acc[jp].y;
+    }
+  }
+}
+
+}  // namespace vl

@@ -1,0 +1,148 @@
+// Microbenchmark of k_score_t variants on synthetic C3-shaped data
+// (Q queries x 1530 hypotheses x 10k scoring correspondences).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+//        -I include -I paper_2601_04185_b200/csrc tools/score_bench.cu -o tools/score_bench
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "vl_score.cuh"
+
+using namespace vl;
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e = (x);                                                        \
+    if (e != cudaSuccess) {                                                     \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      exit(1);                                                                  \
+    }                                                                           \
+  } while (0)
+
+struct Bench {
+  int Q, nsub, nh, HCAP, NSPLIT;
+  Work wk;
+  std::vector<QState> hq;
+};
+
+template <int NT, int HT, int CH, int MINB, int UNR, bool PAIR = false>
+double run_variant(Bench& b, const char* name, std::vector<float>& ref, int reps, int grid_mult) {
+  const int tile = NT * HT;
+  const int ntile = (b.nh + tile - 1) / tile;
+  const int nsplit = (b.nsub + CH - 1) / CH;
+  std::vector<ScoreItem> items;
+  for (int q = 0; q < b.Q; ++q)
+    for (int t = 0; t < ntile; ++t)
+      for (int s = 0; s < nsplit; ++s) items.push_back(ScoreItem{q, t, s, 0});
+  // split count differs per variant: set QState.nsplit accordingly
+  for (auto& s : b.hq) s.nsplit = nsplit;
+  CK(cudaMemcpy(b.wk.qs, b.hq.data(), b.Q * sizeof(QState), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b.wk.items, items.data(), items.size() * sizeof(ScoreItem), cudaMemcpyHostToDevice));
+  int n = (int)items.size();
+  CK(cudaMemcpy(b.wk.item_count, &n, sizeof(int), cudaMemcpyHostToDevice));
+  int dev = 0, sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int occ = 0;
+  auto kern = PAIR ? k_score2_t<NT, HT, CH, MINB, UNR> : k_score_t<NT, HT, CH, MINB, UNR>;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0));
+  const int grid = sms * occ * grid_mult;
+  const float tau2 = 144.f;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int r = 0; r < 2; ++r) kern<<<grid, NT>>>(b.wk, tau2);
+  CK(cudaDeviceSynchronize());
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) kern<<<grid, NT>>>(b.wk, tau2);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double evals = (double)b.Q * b.nh * b.nsub * reps;
+  const double eps = evals / (ms / 1e3);
+  // result check: sum partials over splits
+  std::vector<float> part((size_t)b.Q * b.NSPLIT * b.HCAP);
+  CK(cudaMemcpy(part.data(), b.wk.partial, part.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  std::vector<float> costs((size_t)b.Q * b.nh);
+  for (int q = 0; q < b.Q; ++q)
+    for (int h = 0; h < b.nh; ++h) {
+      double c = 0;
+      for (int s = 0; s < nsplit; ++s) c += part[((size_t)q * b.NSPLIT + s) * b.HCAP + h];
+      costs[(size_t)q * b.nh + h] = (float)c;
+    }
+  double maxrel = 0;
+  if (ref.empty()) ref = costs;
+  else
+    for (size_t i = 0; i < costs.size(); ++i)
+      maxrel = fmax(maxrel, fabs(costs[i] - ref[i]) / fmax(1e-3, fabs(ref[i])));
+  printf("%-28s NT=%3d HT=%d CH=%4d minB=%d unr=%d occ=%d grid=%5d  %8.3f ms/rep  %.4e evals/s  %.1f TF(30/eval)  maxrel %.2e\n",
+         name, NT, HT, CH, MINB, UNR, occ, grid, ms / reps, eps, eps * 30 / 1e12, maxrel);
+  return eps;
+}
+
+int main(int argc, char** argv) {
+  Bench b;
+  b.Q = argc > 1 ? atoi(argv[1]) : 200;
+  b.nsub = 10000;
+  b.nh = 1530;
+  b.HCAP = 4000;
+  b.NSPLIT = (b.nsub + 127) / 128;
+  std::mt19937 rng(1);
+  std::uniform_real_distribution<float> U(-1.f, 1.f);
+  // correspondences: points in front of a camera near identity, pixels near projections
+  std::vector<float4> sub((size_t)b.Q * b.nsub * 2);
+  for (size_t i = 0; i < (size_t)b.Q * b.nsub; ++i) {
+    const float X = 1.2f * U(rng), Y = 1.2f * U(rng), Z = 3.5f + 1.5f * U(rng);
+    const float u = 700.f * X / Z + 350.f + 20.f * U(rng), v = 700.f * Y / Z + 350.f + 20.f * U(rng);
+    sub[2 * i] = make_float4(X, Y, Z, 350.f - u);
+    sub[2 * i + 1] = make_float4(350.f - v, 0.5f + 0.5f * fabsf(U(rng)), 0.f, 0.f);
+  }
+  std::vector<float> P((size_t)b.Q * 12 * b.HCAP, 0.f);
+  for (int q = 0; q < b.Q; ++q)
+    for (int h = 0; h < b.nh; ++h) {
+      const float a = 0.05f * U(rng), bb = 0.05f * U(rng), tx = 0.1f * U(rng), ty = 0.1f * U(rng);
+      const float R[9] = {1, -a, bb, a, 1, 0, -bb, 0, 1};
+      const float t[3] = {tx, ty, 0.1f * U(rng)};
+      float vals[12] = {700 * R[0], 700 * R[1], 700 * R[2], 700 * t[0], 700 * R[3], 700 * R[4],
+                        700 * R[5], 700 * t[1], R[6], R[7], R[8], t[2]};
+      for (int c = 0; c < 12; ++c) P[((size_t)q * 12 + c) * b.HCAP + h] = vals[c];
+    }
+  b.hq.resize(b.Q);
+  for (int q = 0; q < b.Q; ++q) {
+    QState s{};
+    s.nh = b.nh;
+    s.nsub = b.nsub;
+    s.sub_off = (int64_t)q * b.nsub;
+    b.hq[q] = s;
+  }
+  Work& wk = b.wk;
+  wk = Work{};
+  CK(cudaMalloc(&wk.qs, b.Q * sizeof(QState)));
+  CK(cudaMalloc(&wk.sub32, sub.size() * sizeof(float4)));
+  CK(cudaMalloc(&wk.P32, P.size() * sizeof(float)));
+  CK(cudaMalloc(&wk.partial, (size_t)b.Q * b.NSPLIT * b.HCAP * sizeof(float)));
+  CK(cudaMalloc(&wk.items, (size_t)b.Q * 32 * b.NSPLIT * sizeof(ScoreItem)));
+  CK(cudaMalloc(&wk.item_count, sizeof(int)));
+  CK(cudaMemcpy(wk.sub32, sub.data(), sub.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(wk.P32, P.data(), P.size() * sizeof(float), cudaMemcpyHostToDevice));
+  wk.HCAP = b.HCAP;
+  wk.NSPLIT = b.NSPLIT;
+  std::vector<float> ref;
+  const int reps = 5;
+  run_variant<128, 4, 512, 4, 2>(b, "baseline", ref, reps, 1);
+  run_variant<128, 6, 512, 3, 2, true>(b, "pair HT6", ref, reps, 1);
+  run_variant<128, 6, 512, 3, 1, true>(b, "pair HT6 unr1", ref, reps, 1);
+  run_variant<128, 6, 512, 3, 4, true>(b, "pair HT6 unr4", ref, reps, 1);
+  run_variant<128, 6, 512, 4, 2, true>(b, "pair HT6 minB4", ref, reps, 1);
+  run_variant<64, 6, 512, 8, 2, true>(b, "pair NT64 HT6", ref, reps, 1);
+  run_variant<64, 6, 512, 6, 2, true>(b, "pair NT64 HT6 minB6", ref, reps, 1);
+  run_variant<96, 6, 512, 5, 2, true>(b, "pair NT96 HT6", ref, reps, 1);
+  run_variant<128, 6, 1024, 3, 2, true>(b, "pair HT6 CH1024", ref, reps, 1);
+  run_variant<64, 10, 512, 4, 2, true>(b, "pair NT64 HT10", ref, reps, 1);
+  run_variant<64, 12, 512, 4, 1, true>(b, "pair NT64 HT12", ref, reps, 1);
+  run_variant<128, 4, 512, 5, 4, true>(b, "pair HT4 unr4 minB5", ref, reps, 1);
+  run_variant<32, 8, 512, 12, 2, true>(b, "pair NT32 HT8", ref, reps, 1);
+  return 0;
+}
