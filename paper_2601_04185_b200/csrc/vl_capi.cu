@@ -359,7 +359,7 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     wk.item_cap = item_cap;
     VL_CUDA(c, cudaMemcpyAsync(wk.qs, h_qs, Qn * sizeof(QState), cudaMemcpyHostToDevice, st));
     VL_CUDA(c, cudaMemcpyAsync(wk.active_list, h_active, Qn * sizeof(int), cudaMemcpyHostToDevice, st));
-    VL_CUDA(c, cudaMemsetAsync(wk.item_count, 0, sizeof(int), st));
+    VL_CUDA(c, cudaMemsetAsync(wk.item_count, 0, 2 * sizeof(int), st));
     c->prof_stream = st;
     prof_hook(c, kStagePrep, true);
     c->launches += launch_prep(wk, in, Qn, st);

@@ -58,7 +58,7 @@ struct Work {
   float* P32;            // [Qc][12][HCAP]
   int* hsrc;             // [Qc][HCAP]
   ScoreItem* items;      // [item_cap]
-  int* item_count;       // device scalar
+  int* item_count;       // [0] items appended this round, [1] scoring work cursor
   float* partial;        // [Qc][NSPLIT][HCAP]
   double* sub_px;        // [Nsub][2]
   double* sub_X;         // [Nsub][3]

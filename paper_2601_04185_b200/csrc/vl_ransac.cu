@@ -458,7 +458,8 @@ __global__ void __launch_bounds__(1024) k_active(Work wk, int nactive) {
   }
   if (threadIdx.x == 0) {
     *wk.active_count = running;
-    *wk.item_count = 0;
+    wk.item_count[0] = 0;  // items appended next round
+    wk.item_count[1] = 0;  // scoring work cursor
   }
 }
 

@@ -100,25 +100,44 @@ template <int NT, int HT, int CH, int MINB, int UNR>
 __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   static_assert(HT % 2 == 0, "hypotheses are processed in pairs");
   constexpr int HP = HT / 2;
+  constexpr int NW = NT / 32;
+  constexpr int WHYP = 32 * HT;  // hypotheses per warp slice
   __shared__ float4 rec[2 * CH];
-  const int nitems = *wk.item_count;
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+  __shared__ float red[NW * WHYP];
+  __shared__ int s_it;
+  const int nitems = wk.item_count[0];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // dynamic work cursor: items differ in cost (partial tiles), and a static
+  // grid stride can alias with the per-query item period
+  while (true) {
+    if (threadIdx.x == 0) s_it = atomicAdd(&wk.item_count[1], 1);
+    __syncthreads();
+    const int it = s_it;
+    if (it >= nitems) break;
     const ScoreItem item = wk.items[it];
     const QState& S = wk.qs[item.q];
     const int nh = S.nh, nsub = S.nsub;
     const int c0 = item.split * CH;
     const int cn = min(CH, nsub - c0);
     const float4* src = wk.sub32 + 2 * (S.sub_off + c0);
+    // A partially filled (last) tile of r hypotheses needs WH = ceil(r / WHYP)
+    // warp slices; the other warps then split the correspondences instead
+    // (G groups), so every warp stays busy.  Group partial sums are combined
+    // in fixed order through shared memory (deterministic per query).
+    const int tile0 = item.tile * (NT * HT);
+    const int r = min(NT * HT, nh - tile0);
+    const int WH = (r + WHYP - 1) / WHYP;
+    const int G = NW / WH;
+    const int hs = w % WH, grp = w / WH;
+    const bool active = grp < G;
+    const int cb = (grp * cn) / G, ce = ((grp + 1) * cn) / G;
     __syncthreads();
     for (int k = threadIdx.x; k < 2 * cn; k += NT) rec[k] = src[k];
     float2 P[HP][12];
     int hid[HT];
     const float* Pq = wk.P32 + (int64_t)item.q * 12 * wk.HCAP;
 #pragma unroll
-    for (int j = 0; j < HT; ++j) {
-      const int h = item.tile * (NT * HT) + j * NT + threadIdx.x;
-      hid[j] = h;
-    }
+    for (int j = 0; j < HT; ++j) hid[j] = tile0 + hs * WHYP + lane * HT + j;
 #pragma unroll
     for (int jp = 0; jp < HP; ++jp) {
       const int h0 = hid[2 * jp] < nh ? hid[2 * jp] : 0;
@@ -131,18 +150,44 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     float2 acc[HP];
 #pragma unroll
     for (int jp = 0; jp < HP; ++jp) acc[jp] = make_float2(0.f, 0.f);
+    if (active) {
 #pragma unroll UNR
-    for (int c = 0; c < cn; ++c) {
-      const float4 a = rec[2 * c];
-      const float4 b = rec[2 * c + 1];
+      for (int c = cb; c < ce; ++c) {
+        const float4 a = rec[2 * c];
+        const float4 b = rec[2 * c + 1];
 #pragma unroll
-      for (int jp = 0; jp < HP; ++jp) VL_SCORE_EVAL2(P[jp], acc[jp]);
+        for (int jp = 0; jp < HP; ++jp) VL_SCORE_EVAL2(P[jp], acc[jp]);
+      }
     }
     float* out = wk.partial + ((int64_t)item.q * wk.NSPLIT + item.split) * wk.HCAP;
+    if (G == 1) {
 #pragma unroll
-    for (int jp = 0; jp < HP; ++jp) {
-      if (hid[2 * jp] < nh) out[hid[2 * jp]] = acc[jp].x;
-      if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = acc[jp].y;
+      for (int jp = 0; jp < HP; ++jp) {
+        if (hid[2 * jp] < nh) out[hid[2 * jp]] = acc[jp].x;
+        if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = acc[jp].y;
+      }
+    } else {
+      // groups g = 1..G-1 park their sums; group 0 adds them in order
+      if (active && grp > 0) {
+#pragma unroll
+        for (int jp = 0; jp < HP; ++jp) {
+          red[(grp - 1) * WH * WHYP + hs * WHYP + lane * HT + 2 * jp] = acc[jp].x;
+          red[(grp - 1) * WH * WHYP + hs * WHYP + lane * HT + 2 * jp + 1] = acc[jp].y;
+        }
+      }
+      __syncthreads();
+      if (grp == 0) {
+#pragma unroll
+        for (int jp = 0; jp < HP; ++jp) {
+          float sx = acc[jp].x, sy = acc[jp].y;
+          for (int g = 1; g < G; ++g) {
+            sx += red[(g - 1) * WH * WHYP + hs * WHYP + lane * HT + 2 * jp];
+            sy += red[(g - 1) * WH * WHYP + hs * WHYP + lane * HT + 2 * jp + 1];
+          }
+          if (hid[2 * jp] < nh) out[hid[2 * jp]] = sx;
+          if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = sy;
+        }
+      }
     }
   }
 }
