@@ -138,6 +138,51 @@ int vl_p3p_solve_batch(vl_ctx* ctx, const double* bearings, const double* points
 int vl_sample_minimal_sets(vl_ctx* ctx, vl_pcg64_state* st, int64_t n, int32_t count,
                            int32_t* out, void* stream);
 
+/* ---- depth lifting (localizer.lift, localizer.py:134-197) -------------- */
+/* One correspondence field, in output order (entry id, then db->query
+ * (direction 0, direct depth lookup) before query->db (direction 1,
+ * bilinear depth)).  Arrays DEVICE; targets (gh,gw,2), confidence (gh,gw)
+ * in f32 (file-backed IMLC) or f64 (in-memory) — one dtype per call. */
+typedef struct {
+  int32_t query, entry, direction, depth; /* depth: index into the vl_lift_depth array */
+  int32_t grid_w, grid_h;
+  double scale_x, scale_y;                /* cell -> pixel (matchio.py:83-84) */
+  const void* targets;
+  const void* confidence;
+} vl_lift_segment;
+
+/* A database entry's stored depth + camera.  kind: 0 f32 values + valid,
+ * 1 f16 values + valid, 2 u8 log codes, 3 u16 log codes (code 0 invalid;
+ * `lut` = dequantize_depth table, mapstore.py:122-134). */
+typedef struct {
+  int32_t width, height, kind, _pad;
+  const void* values;                     /* DEVICE [h,w] */
+  const uint8_t* valid;                   /* DEVICE [h,w] (kinds 0, 1) */
+  const float* lut;                       /* DEVICE [levels+1] (kinds 2, 3) */
+  double fx, fy, cx, cy;                  /* database intrinsics */
+  double sx_depth, sy_depth;              /* depth width / image width, depth height / image height */
+  double R[9], t[3];                      /* database pose, camera-from-world */
+} vl_lift_depth;
+
+/* replaces localizer.lift for many (query, entry) field pairs at once;
+ * mode 0 = lift, mode 1 = confidence gate only (matchio.filter_matches_arrays,
+ * outputs px = source px, X = (target x, target y, flat cell index)).
+ * Outputs DEVICE (capacity rows); seg_offsets HOST [nseg+1] receives the
+ * exclusive output offset of every segment (last = total matches). */
+int vl_lift(vl_ctx* ctx, const vl_lift_segment* segs, int32_t nseg, const vl_lift_depth* depths,
+            int32_t ndepth, int32_t field_f64, double threshold, int32_t mode, double* px_out,
+            double* X_out, double* w_out, int32_t* entry_out, int64_t capacity, int64_t* seg_offsets,
+            void* stream);
+
+/* replaces localizer.interp_depth_many (localizer.py:87-115): pts DEVICE
+ * [n,2] depth-map subpixels; vals DEVICE [n] (0 where invalid), ok DEVICE [n]. */
+int vl_interp_depth(vl_ctx* ctx, const vl_lift_depth* depth, const double* pts, int64_t n, double* vals,
+                    uint8_t* ok, void* stream);
+
+/* replaces mapstore.dequantize_depth (mapstore.py:122-134) applied on device:
+ * codes (kinds 2, 3) -> f32 depth (0 where invalid) + valid. */
+int vl_decode_depth(vl_ctx* ctx, const vl_lift_depth* depth, float* vals, uint8_t* valid, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

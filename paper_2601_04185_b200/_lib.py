@@ -51,6 +51,20 @@ class RansacOut(C.Structure):
                 ("converged", C.c_void_p), ("stats", C.c_void_p)]
 
 
+class LiftSegment(C.Structure):
+    _fields_ = [("query", C.c_int32), ("entry", C.c_int32), ("direction", C.c_int32), ("depth", C.c_int32),
+                ("grid_w", C.c_int32), ("grid_h", C.c_int32), ("scale_x", C.c_double), ("scale_y", C.c_double),
+                ("targets", C.c_void_p), ("confidence", C.c_void_p)]
+
+
+class LiftDepth(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("kind", C.c_int32), ("_pad", C.c_int32),
+                ("values", C.c_void_p), ("valid", C.c_void_p), ("lut", C.c_void_p),
+                ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("sx_depth", C.c_double), ("sy_depth", C.c_double),
+                ("R", C.c_double * 9), ("t", C.c_double * 3)]
+
+
 class VislocError(RuntimeError):
     pass
 
@@ -91,8 +105,12 @@ def lib():
                                      ip, ip, dp, ip, vp]
         L.vl_p3p_solve_batch.argtypes = [vp, vp, vp, i32, vp, vp, vp, ip, vp]
         L.vl_sample_minimal_sets.argtypes = [vp, C.POINTER(PCG64State), i64, i32, vp, vp]
+        L.vl_lift.argtypes = [vp, C.POINTER(LiftSegment), i32, C.POINTER(LiftDepth), i32, i32, dbl, i32,
+                              vp, vp, vp, vp, i64, C.POINTER(C.c_int64), vp]
+        L.vl_interp_depth.argtypes = [vp, C.POINTER(LiftDepth), vp, i64, vp, vp, vp]
+        L.vl_decode_depth.argtypes = [vp, C.POINTER(LiftDepth), vp, vp, vp]
         for name in ("vl_create", "vl_destroy", "vl_reserve", "vl_pcg64_seed", "vl_ransac_pnp", "vl_profile",
-                     "vl_profile_read",
+                     "vl_profile_read", "vl_lift", "vl_interp_depth", "vl_decode_depth",
                      "vl_msac_score", "vl_refine_pose", "vl_p3p_solve_batch", "vl_sample_minimal_sets"):
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -102,7 +120,8 @@ def lib():
 EXPORTED_SYMBOLS = (
     "vl_create", "vl_destroy", "vl_last_error", "vl_reserve", "vl_launch_count", "vl_pcg64_seed",
     "vl_ransac_pnp", "vl_msac_score", "vl_refine_pose", "vl_p3p_solve_batch",
-    "vl_sample_minimal_sets", "vl_profile", "vl_profile_read",
+    "vl_sample_minimal_sets", "vl_profile", "vl_profile_read", "vl_lift", "vl_interp_depth",
+    "vl_decode_depth",
 )
 
 STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final")

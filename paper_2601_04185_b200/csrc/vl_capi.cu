@@ -26,6 +26,7 @@ struct vl_ctx {
   DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, P32, hsrc, items, item_count,
       partial, sub_px, sub_X, sub_w, sub32, comp_px, comp_X, comp_w;
   DevBuf scratch;  // small standalone-call scratch
+  DevBuf lift_meta, lift_blk_count, lift_blk_off, lift_seg_off;  // vl_lift
   void* h_pinned = nullptr;
   size_t h_pinned_cap = 0;
   // profiling: CUDA-event brackets around every stage launch (vl_profile)
@@ -183,7 +184,8 @@ int vl_destroy(vl_ctx* c) {
   DevBuf* bufs[] = {&c->qs,      &c->active, &c->next_active, &c->active_count, &c->samples, &c->slots,
                     &c->slot_cnt, &c->P32,   &c->hsrc,        &c->items,        &c->item_count,
                     &c->partial, &c->sub_px, &c->sub_X,       &c->sub_w,        &c->sub32,   &c->comp_px,
-                    &c->comp_X,  &c->comp_w, &c->scratch};
+                    &c->comp_X,  &c->comp_w, &c->scratch, &c->lift_meta, &c->lift_blk_count,
+                    &c->lift_blk_off, &c->lift_seg_off};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -499,3 +501,101 @@ int vl_sample_minimal_sets(vl_ctx* c, vl_pcg64_state* stt, int64_t n, int32_t co
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ lifting
+#include "vl_lift.h"
+static_assert(sizeof(vl_lift_segment) == sizeof(vl::LiftSeg), "segment layout");
+static_assert(sizeof(vl_lift_depth) == sizeof(vl::LiftDepth), "depth layout");
+
+
+extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, const vl_lift_depth* depths,
+                       int32_t ndepth, int32_t field_f64, double threshold, int32_t mode, double* px_out,
+                       double* X_out, double* w_out, int32_t* entry_out, int64_t capacity,
+                       int64_t* seg_offsets, void* stream) {
+  if (!c || nseg < 0 || (nseg > 0 && !segs) || !seg_offsets || (mode != 0 && mode != 1))
+    return fail(c, VL_ERR_INVALID, "bad argument");
+  if (!(threshold >= 0 && threshold <= 1))
+    return fail(c, VL_ERR_INVALID, "threshold must be in [0, 1], got " + std::to_string(threshold));
+  seg_offsets[0] = 0;
+  if (nseg == 0) return VL_OK;
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t BC = lift_block_cells();
+  std::vector<int64_t> blk0(nseg);
+  int64_t nblk = 0;
+  for (int s = 0; s < nseg; ++s) {
+    const vl_lift_segment& S = segs[s];
+    if (S.grid_w <= 0 || S.grid_h <= 0 || !S.targets || !S.confidence)
+      return fail(c, VL_ERR_INVALID, "segment " + std::to_string(s) + ": empty grid or null arrays");
+    if (mode == 0 && (S.depth < 0 || S.depth >= ndepth))
+      return fail(c, VL_ERR_INVALID, "segment " + std::to_string(s) + ": bad depth index");
+    if (S.direction != 0 && S.direction != 1) return fail(c, VL_ERR_INVALID, "bad direction");
+    blk0[s] = nblk;
+    nblk += ((int64_t)S.grid_w * S.grid_h + BC - 1) / BC;
+  }
+  if (mode == 0)
+    for (int d = 0; d < ndepth; ++d) {
+      const vl_lift_depth& D = depths[d];
+      if (D.width < 2 || D.height < 2 || !D.values || (D.kind < 2 && !D.valid) || (D.kind >= 2 && !D.lut))
+        return fail(c, VL_ERR_INVALID, "depth " + std::to_string(d) + ": bad map");
+    }
+  const size_t seg_bytes = nseg * sizeof(vl_lift_segment), dep_bytes = (mode == 0 ? ndepth : 0) * sizeof(vl_lift_depth);
+  const size_t meta = seg_bytes + dep_bytes + nseg * sizeof(int64_t) + 64;
+  int rc;
+  if ((rc = ensure(c, c->lift_meta, meta)) || (rc = ensure(c, c->lift_blk_count, nblk * sizeof(int))) ||
+      (rc = ensure(c, c->lift_blk_off, nblk * sizeof(int64_t))) || (rc = ensure(c, c->lift_seg_off, (nseg + 1) * sizeof(int64_t))) ||
+      (rc = ensure_host(c, meta + (nseg + 1) * sizeof(int64_t))))
+    return rc;
+  char* h = (char*)c->h_pinned;
+  std::memcpy(h, segs, seg_bytes);
+  if (dep_bytes) std::memcpy(h + seg_bytes, depths, dep_bytes);
+  std::memcpy(h + seg_bytes + dep_bytes, blk0.data(), nseg * sizeof(int64_t));
+  char* d = (char*)c->lift_meta.p;
+  VL_CUDA(c, cudaMemcpyAsync(d, h, seg_bytes + dep_bytes + nseg * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  LiftArgs a;
+  a.segs = (const LiftSeg*)d;
+  a.nseg = nseg;
+  a.depths = (const LiftDepth*)(d + seg_bytes);
+  a.seg_blk0 = (const int64_t*)(d + seg_bytes + dep_bytes);
+  a.nblk = nblk;
+  a.blk_count = (int*)c->lift_blk_count.p;
+  a.blk_off = (int64_t*)c->lift_blk_off.p;
+  a.seg_off = (int64_t*)c->lift_seg_off.p;
+  a.threshold = threshold;
+  a.px_out = px_out;
+  a.X_out = X_out;
+  a.w_out = w_out;
+  a.entry_out = entry_out;
+  a.capacity = capacity;
+  c->launches += launch_lift(a, field_f64, mode, st);
+  if ((rc = check_launch(c))) return rc;
+  int64_t* hoff = (int64_t*)(h + meta);
+  VL_CUDA(c, cudaMemcpyAsync(hoff, a.seg_off, (nseg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  VL_CUDA(c, cudaStreamSynchronize(st));
+  std::memcpy(seg_offsets, hoff, (nseg + 1) * sizeof(int64_t));
+  if (hoff[nseg] > capacity)
+    return fail(c, VL_ERR_INVALID, "output capacity " + std::to_string(capacity) + " < " + std::to_string(hoff[nseg]) + " matches");
+  if (!px_out || !X_out || !w_out) return fail(c, VL_ERR_INVALID, "null output array");
+  c->launches += launch_lift_write(a, field_f64, mode, st);
+  return check_launch(c);
+}
+
+extern "C" int vl_interp_depth(vl_ctx* c, const vl_lift_depth* depth, const double* pts, int64_t n, double* vals,
+                               uint8_t* ok, void* stream) {
+  if (!c || !depth || n < 0 || n > 0x7FFFFFFF) return fail(c, VL_ERR_INVALID, "bad argument");
+  if (depth->width < 2 || depth->height < 2) return fail(c, VL_ERR_INVALID, "depth map must be at least 2x2");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  LiftDepth D;
+  std::memcpy(&D, depth, sizeof(D));
+  c->launches += launch_interp(D, pts, (int)n, vals, ok, (cudaStream_t)stream);
+  return check_launch(c);
+}
+
+extern "C" int vl_decode_depth(vl_ctx* c, const vl_lift_depth* depth, float* vals, uint8_t* valid, void* stream) {
+  if (!c || !depth || !vals || !valid) return fail(c, VL_ERR_INVALID, "bad argument");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  LiftDepth D;
+  std::memcpy(&D, depth, sizeof(D));
+  c->launches += launch_decode(D, (int64_t)D.w * D.h, vals, valid, (cudaStream_t)stream);
+  return check_launch(c);
+}

@@ -1,0 +1,496 @@
+"""Query-time lifting and localisation — drop-in for ``visloc.localizer``.
+
+``lift`` / ``lift_arrays`` / ``localize`` / ``localize_batch`` run the
+confidence gate, depth decode (f32, f16 or log-quantised codes), depth fetch
+(direct or bilinear with the all-4-valid rule), unprojection and world
+transform on the GPU (``vl_lift``), then feed the device-resident matches
+straight into the batched estimator (``vl_ransac_pnp``).
+
+Reference: ``localizer.py`` — ``interp_depth_many`` :87-115, ``lift``
+:134-197, ``localize`` :200-238; ``matchio.filter_matches_arrays``
+:203-218; ``mapstore.dequantize_depth`` :122-134.  Inputs are duck-typed so
+the reference's own ``QueryJob`` / ``FieldPair`` / ``CorrespondenceField`` /
+``DepthMap`` / ``QuantizedDepthMap`` / ``MapEntry`` objects work unchanged.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .geometry import CameraIntrinsics, Pose
+from .posest import (Match2D3D, PoseEstimate, RansacConfig, _estimates_from, _intr_c,
+                     ransac_pnp_device)
+
+__all__ = [
+    "CONFIDENCE_THRESHOLD", "CorrespondenceField", "DepthMap", "DescriptorIndex", "FieldPair",
+    "QuantizedDepthMap", "QueryJob", "dequantize_depth", "filter_matches_arrays", "interp_depth",
+    "interp_depth_many", "lift", "lift_arrays", "localize", "localize_batch",
+]
+
+CONFIDENCE_THRESHOLD = 0.05
+DEFAULT_D_MIN = 0.25
+DEFAULT_D_MAX = 128.0
+
+KIND_F32, KIND_F16, KIND_CODE8, KIND_CODE16 = 0, 1, 2, 3
+
+
+# ----------------------------------------------------------------------------- types
+@dataclass
+class CorrespondenceField:
+    """Per-cell targets (h,w,2) and confidences (h,w) (matchio.py:74-123)."""
+
+    source_id: str
+    target_id: str
+    targets: np.ndarray
+    confidence: np.ndarray
+    scale_x: float = 1.0
+    scale_y: float = 1.0
+
+    def __post_init__(self):
+        t32 = np.asarray(self.targets).dtype == np.float32
+        c32 = np.asarray(self.confidence).dtype == np.float32
+        self.targets = np.ascontiguousarray(self.targets, dtype=np.float32 if t32 else np.float64)
+        self.confidence = np.ascontiguousarray(self.confidence, dtype=np.float32 if c32 else np.float64)
+        if self.targets.ndim != 3 or self.targets.shape[2] != 2:
+            raise ValueError(f"targets must be (H, W, 2), got {self.targets.shape}")
+        if self.confidence.shape != self.targets.shape[:2]:
+            raise ValueError("confidence shape does not match targets")
+        h, w = self.confidence.shape
+        if h <= 0 or w <= 0:
+            raise ValueError(f"grid dimensions must be positive, got {w}x{h}")
+        c = self.confidence
+        if np.any(~np.isfinite(c)) or c.min() < 0 or c.max() > 1:
+            raise ValueError("confidences must be finite and within [0, 1]")
+        if np.any(~np.isfinite(self.targets[c > 0])):
+            raise ValueError("matched cells (confidence > 0) must have finite targets")
+
+    @property
+    def grid_w(self) -> int:
+        return self.confidence.shape[1]
+
+    @property
+    def grid_h(self) -> int:
+        return self.confidence.shape[0]
+
+
+@dataclass
+class DepthMap:
+    """z-depth (f32) + validity at match-grid resolution (depthbuild.py:45-77)."""
+
+    values: np.ndarray
+    valid: np.ndarray
+    intrinsics: CameraIntrinsics
+
+    def __post_init__(self):
+        self.values = np.ascontiguousarray(self.values, dtype=np.float32)
+        self.valid = np.ascontiguousarray(self.valid, dtype=bool)
+        if self.values.shape != self.valid.shape or self.values.ndim != 2:
+            raise ValueError("values and valid must be equal 2-D shapes")
+        if np.any(self.valid & ~(np.isfinite(self.values) & (self.values > 0))):
+            raise ValueError("valid pixels must hold positive finite depth")
+
+    @property
+    def height(self) -> int:
+        return self.values.shape[0]
+
+    @property
+    def width(self) -> int:
+        return self.values.shape[1]
+
+
+@dataclass
+class QuantizedDepthMap:
+    """Log-space depth codes; 0 invalid (mapstore.py:65-93)."""
+
+    codes: np.ndarray
+    d_min: float = DEFAULT_D_MIN
+    d_max: float = DEFAULT_D_MAX
+    levels: int = 255
+    intrinsics: CameraIntrinsics | None = None
+
+    def __post_init__(self):
+        if not 0 < self.d_min < self.d_max:
+            raise ValueError(f"need 0 < d_min < d_max, got [{self.d_min}, {self.d_max}]")
+        if not 1 <= self.levels <= 65535:
+            raise ValueError(f"levels out of range: {self.levels}")
+        self.codes = np.ascontiguousarray(self.codes, dtype=np.uint8 if self.levels <= 255 else np.uint16)
+        if self.codes.ndim != 2:
+            raise ValueError("codes must be 2-D")
+        if self.codes.max(initial=0) > self.levels:
+            raise ValueError(f"code {self.codes.max()} exceeds {self.levels} levels")
+
+    @property
+    def height(self) -> int:
+        return self.codes.shape[0]
+
+    @property
+    def width(self) -> int:
+        return self.codes.shape[1]
+
+
+@dataclass(frozen=True)
+class FieldPair:
+    query_to_db: object
+    db_to_query: object
+
+
+@dataclass
+class QueryJob:
+    query_id: str
+    intrinsics: CameraIntrinsics
+    descriptor: np.ndarray
+    fields: dict = field(default_factory=dict)
+    k_loc: int = 10
+
+
+class DescriptorIndex:
+    """Exact cosine top-K with ascending-id tie-break (retrieval.py:16-85).
+
+    Retrieval is upstream of the GPU path (out of scope); this
+    host mirror keeps ``localize(index=None)`` working like the reference.
+    """
+
+    def __init__(self, dim: int):
+        if dim < 1:
+            raise ValueError(f"descriptor dimension must be >= 1, got {dim}")
+        self.dim = int(dim)
+        self._ids, self._vecs = [], []
+        self._M = None
+
+    @classmethod
+    def from_entries(cls, entries):
+        idx = None
+        for eid, vec in entries:
+            if idx is None:
+                idx = cls(np.asarray(vec).shape[-1])
+            idx.add(eid, vec)
+        return idx if idx is not None else cls(1)
+
+    @property
+    def size(self) -> int:
+        return len(self._ids)
+
+    def add(self, entry_id, vector):
+        v = np.asarray(vector, dtype=np.float32).reshape(-1)
+        if v.shape[0] != self.dim:
+            raise ValueError("dimension mismatch")
+        n = float(np.linalg.norm(v.astype(np.float64)))
+        if n == 0.0 or not np.isfinite(n):
+            raise ValueError(f"cannot index zero or non-finite vector for id {entry_id!r}")
+        if entry_id in self._ids:
+            raise ValueError(f"duplicate id {entry_id!r}")
+        self._ids.append(entry_id)
+        self._vecs.append((v.astype(np.float64) / n).astype(np.float32))
+        self._M = None
+        return self
+
+    def topk(self, query, k):
+        if k < 1:
+            raise ValueError(f"k must be >= 1, got {k}")
+        q = np.asarray(query, dtype=np.float64).reshape(-1)
+        if q.shape[0] != self.dim:
+            raise ValueError("dimension mismatch")
+        if not self._ids:
+            return []
+        n = float(np.linalg.norm(q))
+        if n == 0.0 or not np.isfinite(n):
+            raise ValueError("query vector must be non-zero and finite")
+        if self._M is None:
+            self._M = np.stack(self._vecs).astype(np.float64)
+            order = sorted(range(len(self._ids)), key=lambda i: self._ids[i])
+            self._rank = np.empty(len(self._ids), dtype=np.int64)
+            self._rank[order] = np.arange(len(order))
+        sims = self._M @ (q / n)
+        sel = np.lexsort((self._rank, -sims))[: min(k, len(self._ids))]
+        return [(self._ids[i], float(sims[i])) for i in sel]
+
+    def ids(self):
+        return list(self._ids)
+
+
+# ----------------------------------------------------------------------------- device helpers
+class _DeviceDepth:
+    """One entry's stored depth resident in HBM + its vl_lift_depth record."""
+
+    def __init__(self, depth, intr_db: CameraIntrinsics | None):
+        import torch
+        self.keep = []
+        if hasattr(depth, "codes"):  # QuantizedDepthMap: decode through the reference table
+            q = depth
+            span = math.log(q.d_max / q.d_min)
+            denom = max(q.levels - 1, 1)
+            c = np.arange(q.levels + 1, dtype=np.float64)
+            lut = (q.d_min * np.exp((c - 1.0) / denom * span)).astype(np.float32)
+            lut[0] = 0.0
+            codes = np.ascontiguousarray(q.codes)
+            self.kind = KIND_CODE8 if codes.dtype == np.uint8 else KIND_CODE16
+            vals = torch.from_numpy(codes.view(np.int16) if codes.dtype == np.uint16 else codes).cuda()
+            self.lut = torch.from_numpy(lut).cuda()
+            self.values, self.valid = vals, None
+            h, w = codes.shape
+            grid_intr = q.intrinsics
+        else:
+            v = np.asarray(depth.values)
+            self.kind = KIND_F16 if v.dtype == np.float16 else KIND_F32
+            v = np.ascontiguousarray(v, dtype=np.float16 if self.kind == KIND_F16 else np.float32)
+            self.values = torch.from_numpy(v.view(np.int16) if self.kind == KIND_F16 else v).cuda()
+            self.valid = torch.from_numpy(np.ascontiguousarray(depth.valid, dtype=np.uint8)).cuda()
+            self.lut = None
+            h, w = v.shape
+            grid_intr = depth.intrinsics
+        self.h, self.w = h, w
+        self.grid_intr = grid_intr
+
+    def record(self, intr_db, pose: Pose) -> _lib.LiftDepth:
+        r = _lib.LiftDepth()
+        r.width, r.height, r.kind = self.w, self.h, self.kind
+        r.values = self.values.data_ptr()
+        r.valid = self.valid.data_ptr() if self.valid is not None else None
+        r.lut = self.lut.data_ptr() if self.lut is not None else None
+        r.fx, r.fy, r.cx, r.cy = float(intr_db.fx), float(intr_db.fy), float(intr_db.cx), float(intr_db.cy)
+        r.sx_depth = self.w / intr_db.width
+        r.sy_depth = self.h / intr_db.height
+        R = pose.R
+        for i in range(9):
+            r.R[i] = float(R.flat[i])
+        for i in range(3):
+            r.t[i] = float(pose.t[i])
+        return r
+
+
+def _check_span(fld, intr, what):
+    if abs(fld.grid_w * fld.scale_x - intr.width) > 1e-6 * intr.width or \
+       abs(fld.grid_h * fld.scale_y - intr.height) > 1e-6 * intr.height:
+        raise ValueError(f"{what}: field grid {fld.grid_w}x{fld.grid_h} at scale "
+                         f"({fld.scale_x}, {fld.scale_y}) does not span image {intr.width}x{intr.height}")
+
+
+class _FieldUpload:
+    """Packs many fields into two device arrays (one dtype per call)."""
+
+    def __init__(self, fields):
+        import torch
+        self.f64 = any(np.asarray(f.confidence).dtype != np.float32 or np.asarray(f.targets).dtype != np.float32
+                       for f in fields)
+        dt = np.float64 if self.f64 else np.float32
+        tg = [np.ascontiguousarray(f.targets, dtype=dt).reshape(-1) for f in fields]
+        cf = [np.ascontiguousarray(f.confidence, dtype=dt).reshape(-1) for f in fields]
+        self.t_off = np.concatenate([[0], np.cumsum([a.size for a in tg])])
+        self.c_off = np.concatenate([[0], np.cumsum([a.size for a in cf])])
+        self.targets = torch.from_numpy(np.concatenate(tg) if tg else np.zeros(0, dt)).cuda()
+        self.conf = torch.from_numpy(np.concatenate(cf) if cf else np.zeros(0, dt)).cuda()
+        self.item = 8 if self.f64 else 4
+
+    def ptrs(self, i):
+        return (self.targets.data_ptr() + int(self.t_off[i]) * self.item,
+                self.conf.data_ptr() + int(self.c_off[i]) * self.item)
+
+
+def _run_lift(segs_spec, depth_records, threshold, mode=0):
+    """segs_spec: list of (query, entry, direction, depth_index, field).  Returns
+    (px, X, w, entry) CUDA tensors and host segment offsets."""
+    import torch
+    if not 0 <= threshold <= 1:
+        raise ValueError(f"threshold must be in [0, 1], got {threshold}")
+    ctx = _lib.context()
+    n = len(segs_spec)
+    up = _FieldUpload([s[4] for s in segs_spec])
+    segs = (_lib.LiftSegment * max(n, 1))()
+    cap = 0
+    for i, (q, e, d, di, f) in enumerate(segs_spec):
+        s = segs[i]
+        s.query, s.entry, s.direction, s.depth = q, e, d, di
+        s.grid_w, s.grid_h = f.grid_w, f.grid_h
+        s.scale_x, s.scale_y = float(f.scale_x), float(f.scale_y)
+        s.targets, s.confidence = up.ptrs(i)
+        cap += f.grid_w * f.grid_h
+    deps = (_lib.LiftDepth * max(len(depth_records), 1))(*depth_records)
+    cap = max(cap, 1)
+    px = torch.empty((cap, 2), dtype=torch.float64, device="cuda")
+    X = torch.empty((cap, 3), dtype=torch.float64, device="cuda")
+    w = torch.empty((cap,), dtype=torch.float64, device="cuda")
+    ent = torch.empty((cap,), dtype=torch.int32, device="cuda")
+    offs = np.zeros(n + 1, dtype=np.int64)
+    rc = _lib.lib().vl_lift(ctx.handle, segs, n, deps, len(depth_records), 1 if up.f64 else 0, float(threshold),
+                            mode, px.data_ptr(), X.data_ptr(), w.data_ptr(), ent.data_ptr(), cap,
+                            offs.ctypes.data_as(C.POINTER(C.c_int64)), _lib.stream_ptr())
+    ctx.check(rc, "vl_lift")
+    tot = int(offs[-1])
+    return px[:tot], X[:tot], w[:tot], ent[:tot], offs, up
+
+
+# ----------------------------------------------------------------------------- API
+def filter_matches_arrays(fld, threshold: float):
+    """(source_px (M,2), target_px (M,2), confidence (M,), flat cell index (M,)) (matchio.py:203-218)."""
+    px, X, w, _, _, _ = _run_lift([(0, 0, 0, 0, fld)], [], threshold, mode=1)
+    Xh = X.cpu().numpy()
+    return px.cpu().numpy(), Xh[:, :2].copy(), w.cpu().numpy(), Xh[:, 2].astype(np.int64)
+
+
+def dequantize_depth(q) -> DepthMap:
+    """Codes -> f32 depth + validity on the GPU (mapstore.py:122-134)."""
+    import torch
+    dd = _DeviceDepth(q, None)
+    ctx = _lib.context()
+    vals = torch.empty((dd.h, dd.w), dtype=torch.float32, device="cuda")
+    ok = torch.empty((dd.h, dd.w), dtype=torch.uint8, device="cuda")
+    intr = q.intrinsics if q.intrinsics is not None else CameraIntrinsics(1.0, 1.0, 0.0, 0.0, q.width, q.height)
+    rec = dd.record(intr, Pose.identity())
+    rc = _lib.lib().vl_decode_depth(ctx.handle, C.byref(rec), vals.data_ptr(), ok.data_ptr(), _lib.stream_ptr())
+    ctx.check(rc, "vl_decode_depth")
+    return DepthMap(values=vals.cpu().numpy(), valid=ok.cpu().numpy().astype(bool), intrinsics=intr)
+
+
+def interp_depth_many(depth, subpixels):
+    """Bilinear depth at depth-map subpixels with the all-4-valid rule (localizer.py:87-115)."""
+    import torch
+    from .posest import _to_device
+    pts = np.ascontiguousarray(np.asarray(subpixels, dtype=np.float64).reshape(-1, 2))
+    n = pts.shape[0]
+    dd = _DeviceDepth(depth, None)
+    if dd.w < 2 or dd.h < 2:
+        raise ValueError("depth map must be at least 2x2")
+    ctx = _lib.context()
+    dp = _to_device(pts)
+    vals = torch.empty((max(n, 1),), dtype=torch.float64, device="cuda")
+    ok = torch.empty((max(n, 1),), dtype=torch.uint8, device="cuda")
+    rec = dd.record(CameraIntrinsics(1.0, 1.0, 0.0, 0.0, dd.w, dd.h), Pose.identity())
+    rc = _lib.lib().vl_interp_depth(ctx.handle, C.byref(rec), dp.data_ptr(), n, vals.data_ptr(), ok.data_ptr(),
+                                    _lib.stream_ptr())
+    ctx.check(rc, "vl_interp_depth")
+    return vals[:n].cpu().numpy(), ok[:n].cpu().numpy().astype(bool)
+
+
+def interp_depth(depth, subpixel):
+    v, ok = interp_depth_many(depth, np.asarray(subpixel, dtype=np.float64)[None])
+    return float(v[0]) if ok[0] else None
+
+
+def _entry_segments(query_job, entry, q_index, e_index, d_index):
+    pair = query_job.fields[entry.id]
+    intr_db = entry.intrinsics
+    _check_span(pair.db_to_query, intr_db, f"entry {entry.id} db->query")
+    _check_span(pair.query_to_db, query_job.intrinsics, f"entry {entry.id} query->db")
+    return [(q_index, e_index, 0, d_index, pair.db_to_query), (q_index, e_index, 1, d_index, pair.query_to_db)]
+
+
+def _depth_record(entry, depth, cache=None):
+    key = getattr(entry, "id", None)
+    dd = cache.get(key) if (cache is not None and key is not None) else None
+    if dd is None:
+        dd = _DeviceDepth(depth, entry.intrinsics)
+        if cache is not None and key is not None:
+            cache[key] = dd
+    gi = dd.grid_intr
+    if gi is not None and (gi.width != entry.intrinsics.width or gi.height != entry.intrinsics.height):
+        raise ValueError(f"entry {entry.id}: depth map covers {gi.width}x{gi.height}, "
+                         f"entry image is {entry.intrinsics.width}x{entry.intrinsics.height}")
+    return dd.record(entry.intrinsics, entry.pose)
+
+
+def lift_arrays(query_job, entry, depth, threshold: float = CONFIDENCE_THRESHOLD):
+    """Device (px, X, w) of one entry's lift (localizer.py:134-197 order)."""
+    rec = _depth_record(entry, depth)
+    px, X, w, _, _, _ = _run_lift(_entry_segments(query_job, entry, 0, 0, 0), [rec], threshold)
+    return px, X, w
+
+
+def lift(query_job, entry, depth, threshold: float = CONFIDENCE_THRESHOLD) -> list:
+    """Drop-in ``visloc.localizer.lift``: list of Match2D3D in reference order."""
+    px, X, w = lift_arrays(query_job, entry, depth, threshold)
+    P, Xh, wh = px.cpu().numpy(), X.cpu().numpy(), w.cpu().numpy()
+    return [Match2D3D(P[i], Xh[i], float(wh[i]), entry.id) for i in range(wh.shape[0])]
+
+
+def _failure(n):
+    return PoseEstimate(pose=Pose.identity(), inlier_count=0, inlier_flags=np.zeros(n, dtype=bool),
+                        score=math.inf, iterations=0, converged=False)
+
+
+def _plan(jobs, vmap, index, depth_cache, device_cache):
+    """Segments + depth records for every query (sorted retrieved ids, localizer.py:220-235)."""
+    from .geometry import CameraIntrinsics  # noqa: F401
+    if index is None:
+        index = DescriptorIndex.from_entries((e.id, e.descriptor) for e in vmap.entries)
+    by_id = {e.id: e for e in vmap.entries}
+    segs, recs, rec_of = [], [], {}
+    for qi, job in enumerate(jobs):
+        if index.size == 0:
+            continue
+        ranked = index.topk(np.asarray(job.descriptor, dtype=np.float64), job.k_loc)
+        for eid in sorted(eid for eid, _ in ranked):
+            if eid not in job.fields:
+                continue
+            entry = by_id[eid]
+            if eid not in rec_of:
+                if depth_cache is not None and eid in depth_cache:
+                    depth = depth_cache[eid]
+                else:
+                    if getattr(entry, "qdepth", None) is None:
+                        raise ValueError(f"entry {eid} has no stored depth")
+                    depth = entry.qdepth
+                rec_of[eid] = len(recs)
+                recs.append(_depth_record(entry, depth, device_cache))
+            segs += _entry_segments(job, entry, qi, rec_of[eid], rec_of[eid])
+    return segs, recs
+
+
+def localize_batch(jobs, vmap, cfg: RansacConfig, seeds=None, index=None, depth_cache=None,
+                   confidence_threshold: float = CONFIDENCE_THRESHOLD, device_cache=None):
+    """Retrieve, lift (one GPU launch sequence for every query) and estimate every pose.
+
+    Each query behaves like ``localize(job, vmap, RansacConfig(seed=seeds[i]))``.
+    ``device_cache`` (dict) keeps decoded depth resident in HBM across calls.
+    """
+    jobs = list(jobs)
+    Q = len(jobs)
+    if Q == 0:
+        return []
+    if seeds is None:
+        seeds = [cfg.seed] * Q
+    if device_cache is None:
+        device_cache = {}
+    segs, recs = _plan(jobs, vmap, index, depth_cache, device_cache)
+    px, X, w, _, offs, _ = _run_lift(segs, recs, confidence_threshold)
+    # per-query ranges: segments are grouped by query in order
+    q_start = np.zeros(Q + 1, dtype=np.int64)
+    seg_q = np.array([s[0] for s in segs], dtype=np.int64)
+    for qi in range(Q):
+        idx = np.nonzero(seg_q == qi)[0]
+        q_start[qi] = offs[idx[0]] if idx.size else (q_start[qi - 1] if qi else 0)
+    q_end = np.array([offs[np.nonzero(seg_q == qi)[0][-1] + 1] if np.any(seg_q == qi) else q_start[qi]
+                      for qi in range(Q)], dtype=np.int64)
+    res: list = [None] * Q
+    run = [qi for qi in range(Q) if q_end[qi] - q_start[qi] >= 3]
+    for qi in range(Q):
+        if qi not in run:
+            res[qi] = _failure(int(q_end[qi] - q_start[qi]))
+    if run:
+        offsets = np.concatenate([[0], np.cumsum([q_end[qi] - q_start[qi] for qi in run])]).astype(np.int64)
+        contiguous = all(q_start[run[i + 1]] == q_end[run[i]] for i in range(len(run) - 1))
+        if contiguous:
+            a, b = int(q_start[run[0]]), int(q_end[run[-1]])
+            dpx, dX, dw = px[a:b], X[a:b], w[a:b]
+        else:
+            import torch
+            sl = [slice(int(q_start[qi]), int(q_end[qi])) for qi in run]
+            dpx = torch.cat([px[s] for s in sl]).contiguous()
+            dX = torch.cat([X[s] for s in sl]).contiguous()
+            dw = torch.cat([w[s] for s in sl]).contiguous()
+        out = ransac_pnp_device(dpx.contiguous(), dX.contiguous(), dw.contiguous(), offsets,
+                                [jobs[qi].intrinsics for qi in run], [seeds[qi] for qi in run], cfg)
+        for qi, est in zip(run, _estimates_from(out, offsets)):
+            res[qi] = est
+    return res
+
+
+def localize(query_job, vmap, cfg: RansacConfig, index=None, depth_cache=None,
+             confidence_threshold: float = CONFIDENCE_THRESHOLD) -> PoseEstimate:
+    """Drop-in ``visloc.localizer.localize`` (localizer.py:200-238)."""
+    return localize_batch([query_job], vmap, cfg, seeds=[cfg.seed], index=index, depth_cache=depth_cache,
+                          confidence_threshold=confidence_threshold)[0]

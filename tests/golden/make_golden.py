@@ -126,7 +126,79 @@ def ransac_vectors():
     np.savez_compressed(OUT / "ransac.npz", **flat)
 
 
+def lift_vectors():
+    """Reference lift + localize on a small synthetic plane scene (test_localizer._bench style)."""
+    from visloc.depthbuild import DepthMap
+    from visloc.localizer import lift, localize
+    from visloc.mapbuild import synthetic_posed_entries, synthetic_query_jobs
+    from visloc.mapstore import dequantize_depth, quantize_depth
+    from visloc.matchio import CorrespondenceField
+    from visloc.localizer import FieldPair
+    from visloc.synth import NoiseSpec, SceneSpec, make_queries, make_scene
+    from scene_io import pack_scene
+
+    f = 70.0
+    intr = CameraIntrinsics(f, f, 70.0, 70.0, 140, 140)
+    spec = SceneSpec(num_cameras=6, width=140, height=140, camera_spread=0.3, camera_backoff=0.25,
+                     rotation_jitter_deg=3.0, seed=21, intrinsics=intr)
+    scene = make_scene(spec)
+    grid = 32
+    entries = synthetic_posed_entries(scene)
+    gt = {}
+    for i, e in enumerate(entries):
+        d, v = scene.gt_depth_grid(i, grid, grid)
+        gt[e.id] = DepthMap(d.astype(np.float32), v, intr)
+        e.qdepth = quantize_depth(gt[e.id])
+    queries = make_queries(scene, 4, 22)
+    pairs = synthetic_query_jobs(scene, queries, grid, k_loc=4,
+                                 noise=NoiseSpec(sigma_px=1.0, outlier_fraction=0.3), noise_seed=23)
+    jobs = [p[0] for p in pairs]
+
+    class _Map:
+        pass
+
+    vmap = _Map()
+    vmap.entries = entries
+    out = pack_scene(entries, jobs)
+    for i, e in enumerate(entries):
+        out[f"gt{i}_values"], out[f"gt{i}_valid"] = gt[e.id].values, gt[e.id].valid
+    # lift per (job, entry): f64 fields x {gt f32 depth, dequantized codes}; f32 fields x gt depth
+    k = 0
+    for j, job in enumerate(jobs[:1]):
+        for i, e in enumerate(entries[:3]):
+            for depth_kind in ("gt", "deq"):
+                depth = gt[e.id] if depth_kind == "gt" else dequantize_depth(e.qdepth)
+                for fdt in ("f64", "f32"):
+                    jb = job
+                    if fdt == "f32":
+                        fp = job.fields[e.id]
+
+                        def c32(fl):
+                            return CorrespondenceField(fl.source_id, fl.target_id, fl.targets.astype(np.float32),
+                                                       fl.confidence.astype(np.float32), fl.scale_x, fl.scale_y)
+                        import copy
+                        jb = copy.copy(job)
+                        jb.fields = dict(job.fields)
+                        jb.fields[e.id] = FieldPair(c32(fp.query_to_db), c32(fp.db_to_query))
+                    ms = lift(jb, e, depth, 0.05)
+                    out[f"L{k}_meta"] = np.array([j, i, 0 if depth_kind == "gt" else 1, 0 if fdt == "f64" else 1])
+                    out[f"L{k}_px"] = np.array([m.query_px for m in ms]).reshape(-1, 2)
+                    out[f"L{k}_X"] = np.array([m.world_point for m in ms]).reshape(-1, 3)
+                    out[f"L{k}_w"] = np.array([m.weight for m in ms])
+                    k += 1
+    out["nlift"] = np.array(k)
+    for j, job in enumerate(jobs):
+        est = localize(job, vmap, RansacConfig(seed=100 + j), depth_cache={})
+        out[f"loc{j}_q"], out[f"loc{j}_t"] = est.pose.q, est.pose.t
+        out[f"loc{j}_flags"] = est.inlier_flags
+        out[f"loc{j}_iters"] = np.array(est.iterations)
+        out[f"loc{j}_conv"] = np.array(est.converged)
+        out[f"loc{j}_score"] = np.array(est.score)
+    np.savez_compressed(OUT / "lift.npz", **out)
+
+
 if __name__ == "__main__":
+    lift_vectors()
     rng_vectors()
     R, t, px, X, w = p3p_vectors()
     score_vectors(R, t, px, X, w)
