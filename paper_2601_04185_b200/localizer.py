@@ -379,13 +379,14 @@ def _entry_segments(query_job, entry, q_index, e_index, d_index):
     return [(q_index, e_index, 0, d_index, pair.db_to_query), (q_index, e_index, 1, d_index, pair.query_to_db)]
 
 
-def _depth_record(entry, depth, cache=None):
+def _depth_record(entry, depth, cache):
+    """vl_lift_depth record of an entry; the device copy lives in `cache` (dict),
+    which the caller must keep alive until the lift has been enqueued."""
     key = getattr(entry, "id", None)
-    dd = cache.get(key) if (cache is not None and key is not None) else None
+    dd = cache.get(key)
     if dd is None:
         dd = _DeviceDepth(depth, entry.intrinsics)
-        if cache is not None and key is not None:
-            cache[key] = dd
+        cache[key] = dd
     gi = dd.grid_intr
     if gi is not None and (gi.width != entry.intrinsics.width or gi.height != entry.intrinsics.height):
         raise ValueError(f"entry {entry.id}: depth map covers {gi.width}x{gi.height}, "
@@ -395,7 +396,8 @@ def _depth_record(entry, depth, cache=None):
 
 def lift_arrays(query_job, entry, depth, threshold: float = CONFIDENCE_THRESHOLD):
     """Device (px, X, w) of one entry's lift (localizer.py:134-197 order)."""
-    rec = _depth_record(entry, depth)
+    keep = {}
+    rec = _depth_record(entry, depth, keep)
     px, X, w, _, _, _ = _run_lift(_entry_segments(query_job, entry, 0, 0, 0), [rec], threshold)
     return px, X, w
 
