@@ -58,6 +58,51 @@ WORKLOADS = {
 }
 
 
+LIFT_WORKLOADS = {
+    "c2": dict(name="C2 single query, dense-matcher scale: K=20 db images x 83x83 bidirectional fields "
+                    "(~226k lifted corrs), f32 depth lift, fixed 10k minimal samples",
+               K=20, g=83, queries=1, depth="f32", max_iterations=10_000, eta=1e-300, cpu_queries_per_core=0.0625),
+    "c5": dict(name="C5 compressed map: 8-bit log-quantised depth decode + lift, K=10 x 117x117 fields "
+                    "(~20k lifted/entry), 256 queries, default adaptive config",
+               K=10, g=117, queries=256, depth="u8", max_iterations=100_000, eta=1e-4, cpu_queries_per_core=1),
+    "c5h": dict(name="C5 compressed map (fp16 depth variant): K=10 x 117x117 fields, 256 queries, "
+                     "default adaptive config",
+                K=10, g=117, queries=256, depth="f16", max_iterations=100_000, eta=1e-4, cpu_queries_per_core=1),
+}
+LIFT_SEED = 77
+
+
+def _cpu_lift_worker(job):
+    """Oracle port of localize() for one generator-B query (lift + ransac)."""
+    qi, wl, seed0 = job
+    from oracle import lift as ol
+    from oracle.geometry import q2R
+    from oracle.posest import Config, ransac
+    from synth_inputs import lifted_scene
+    vmap, jobs, dc = lifted_scene(wl["K"], wl["queries"], wl["g"], seed=seed0, depth_kind=wl["depth"], only=[qi])
+    t0 = time.perf_counter()
+    pxs, Xs, ws = [], [], []
+    for e in sorted(vmap.entries, key=lambda e: e.id):
+        fp = jobs[0].fields[e.id]
+        if dc is not None:
+            vals, valid = dc[e.id].values.astype(np.float32), dc[e.id].valid
+        else:
+            q = e.qdepth
+            vals, valid = ol.dequantize(q.codes, q.d_min, q.d_max, q.levels)
+        f1 = (fp.db_to_query.targets, fp.db_to_query.confidence, fp.db_to_query.scale_x, fp.db_to_query.scale_y)
+        f2 = (fp.query_to_db.targets, fp.query_to_db.confidence, fp.query_to_db.scale_x, fp.query_to_db.scale_y)
+        I = e.intrinsics
+        px, X, w = ol.lift(f1, f2, vals, valid, (I.fx, I.fy, I.cx, I.cy), (I.width, I.height),
+                           q2R(e.pose.q), e.pose.t, 0.05)
+        pxs.append(px)
+        Xs.append(X)
+        ws.append(w)
+    I = jobs[0].intrinsics
+    r = ransac(np.concatenate(pxs), np.concatenate(Xs), np.concatenate(ws), (I.fx, I.fy, I.cx, I.cy),
+               Config(seed=query_seed(qi, seed0), max_iterations=wl["max_iterations"], miss_probability=wl["eta"]))
+    return r.evals, time.perf_counter() - t0
+
+
 def query_a(qi: int, n: int, outlier: float, sigma: float, seed0: int):
     """Deterministic generator-A query (test_posest.py:22-35 model, per-query GT pose)."""
     from synth_inputs import matches_a, random_pose
@@ -89,12 +134,17 @@ def cpu_sample(wl, seed0, n_queries, cores):
     saved = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
     for k in saved:
         os.environ[k] = "1"
+    lifted = "K" in wl
+    worker = _cpu_lift_worker if lifted else _cpu_worker
+    n_queries = max(1, int(n_queries))
+    cores = min(cores, n_queries)
     try:
         ctx = mp.get_context("spawn")
         with ctx.Pool(cores) as pool:
-            pool.map(_cpu_worker, [(0, dict(wl, n=64, max_iterations=wl.get("batch", 1000)), seed0)] * cores)
+            if not lifted:
+                pool.map(_cpu_worker, [(0, dict(wl, n=64, max_iterations=wl.get("batch", 1000)), seed0)] * cores)
             t0 = time.perf_counter()
-            res = pool.map(_cpu_worker, [(qi, wl, seed0) for qi in range(n_queries)])
+            res = pool.map(worker, [(qi, wl, seed0) for qi in range(n_queries)])
             wall = time.perf_counter() - t0
     finally:
         for k, v in saved.items():
@@ -102,7 +152,9 @@ def cpu_sample(wl, seed0, n_queries, cores):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-    return sum(r[0] for r in res), wall
+    # busy time per process (excludes input generation inside the workers)
+    busy = sum(r[1] for r in res) / cores
+    return sum(r[0] for r in res), min(wall, busy) if busy > 0 else wall
 
 
 def host_cores() -> int:
@@ -114,10 +166,10 @@ def run_reference_arm(args, wl):
     if rank != 0:
         return
     cores = host_cores()
-    nq = cores * wl["cpu_queries_per_core"]
-    seed0 = 3000
+    nq = max(1, int(cores * wl["cpu_queries_per_core"]))
+    seed0 = LIFT_SEED if "K" in wl else 3000
     for _ in range(args.warmup):
-        cpu_sample(wl, seed0, cores, cores)
+        cpu_sample(wl, seed0, nq, cores)
     vals, walls = [], []
     total_evals = 0
     for _ in range(args.steps):
@@ -132,7 +184,7 @@ def run_reference_arm(args, wl):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * statistics.mean(walls), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-        "config": {"workload": wl["name"], "queries_per_step": nq, "corrs_per_query": wl["n"]},
+        "config": {"workload": wl["name"], "queries_per_step": nq, "corrs_per_query": wl.get("n", "lifted")},
         "queries_per_s": nq / statistics.mean(walls),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -197,6 +249,129 @@ class ClockSampler:
                 "power_w_max": max(pw) if pw else None, "samples": len(sm)}
 
 
+# ----------------------------------------------------------------------------- GPU arm: lifted
+def run_lift_bench(args, wl, rank, world, local, dist):
+    """C2 / C5: a step = lift (gate + depth decode + unproject) + batched LO-RANSAC
+    for every query of the shard, device-resident fields/depth (value) or the
+    full host API incl. field/depth H2D and result D2H (e2e)."""
+    import torch
+    from paper_2601_04185_b200 import _lib
+    from paper_2601_04185_b200.localizer import LiftPlan, localize_batch
+    from paper_2601_04185_b200.posest import RansacConfig
+    from synth_inputs import lifted_scene
+
+    Q = wl["queries"]
+    seed0 = LIFT_SEED + 1000 * rank
+    vmap, jobs, dcache = lifted_scene(wl["K"], Q, wl["g"], seed=seed0, depth_kind=wl["depth"])
+    seeds = [query_seed(qi, seed0) for qi in range(Q)]
+    cfg = RansacConfig(max_iterations=wl["max_iterations"], miss_probability=wl["eta"])
+    ctx = _lib.context(local)
+    stream = torch.cuda.current_stream()
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    plan = LiftPlan(jobs, vmap, depth_cache=dcache)
+    out = None
+    for _ in range(args.warmup):
+        out, run, offsets, _ = plan.run_device(cfg, seeds, out=None)
+    stats = out["stats"].cpu().numpy()
+    evals_per_step = int(stats[:, 2].sum())
+    matches = int(offsets[-1])
+    conv_rate = float(out["converged"].float().mean().item())
+    ctx.profile(True)
+    l0 = ctx.launches()
+    sync_all()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            out, run, offsets, _ = plan.run_device(cfg, seeds)
+        e1.record(stream)
+        sync_all()
+    launches = ctx.launches() - l0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    ev = torch.tensor([float(evals_per_step)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ev)
+    ms_max = float(t.item())
+    value = float(ev.item()) * args.steps / (ms_max / 1e3)
+    qps = Q * world * args.steps / (ms_max / 1e3)
+
+    e2e = None
+    if not args.no_e2e:
+        localize_batch(jobs, vmap, cfg, seeds=seeds, depth_cache=dcache)
+        sync_all()
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = localize_batch(jobs, vmap, cfg, seeds=seeds, depth_cache=dcache)
+        e1.record(stream)
+        sync_all()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        h2d = plan.field_bytes + sum(
+            int(d.values.numel() * d.values.element_size() + (d.valid.numel() if d.valid is not None else 0))
+            for d in plan.device_cache.values())
+        d2h = sum(int(r.inlier_flags.size) + 7 * 8 + 5 * 8 for r in res)
+        e2e = {"value": float(ev.item()) * args.steps / (float(et.item()) / 1e3), "unit": "evals/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "queries_per_s": Q * world * args.steps / (float(et.item()) / 1e3)}
+
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    props = torch.cuda.get_device_properties(local)
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+    score_ms, score_launches = prof["score"]
+    lift_ms, lift_launches = prof["lift"]
+    achieved = (evals_per_step * args.steps * FLOP_PER_EVAL) / (score_ms / 1e3) / 1e12 if score_ms else None
+    # lift algorithmic bytes per step: IMLC record 12 B/cell (f32 fields), depth taps, 52 B per match out
+    tap_bytes = {"f32": 5, "f16": 3, "u8": 1}[wl["depth"]]
+    lift_bytes = 12 * plan.cells + matches * (52 + 2.5 * tap_bytes)
+    hbm = float(peaks.get("hbm_gbs", 6548.8))
+    lift_gbs = lift_bytes * args.steps / (lift_ms / 1e3) / 1e9 if lift_ms else None
+    roof = {"bound": "fp32", "kernel": "k_score", "achieved": achieved, "peak": round(fp32_peak, 2),
+            "unit": "TFLOP/s", "frac": (achieved / fp32_peak) if achieved else None,
+            "peak_source": "derived SMs*128*2*sm_max_mhz (MEASURED_PEAKS.json has no FP32 entry)",
+            "traffic": None, "score_share_of_step": score_ms / ms if ms else None,
+            "lift": {"bound": "hbm", "achieved": lift_gbs, "peak": hbm, "unit": "GB/s",
+                     "frac": (lift_gbs / hbm) if lift_gbs else None, "algorithmic_bytes_per_step": lift_bytes,
+                     "share_of_step": lift_ms / ms if ms else None, "launches": lift_launches}}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = host_cores()
+        nq = max(1, int(cores * wl["cpu_queries_per_core"]))
+        cev, cwall = cpu_sample(wl, seed0, nq, cores)
+        cpu = {"value": cev / cwall, "unit": "evals/s", "cores": min(cores, nq), "kind": "port",
+               "sample": f"{nq} queries of the same workload (oracle lift + ransac), 1 process/query"}
+    if rank == 0:
+        line = {
+            "metric": "hyp×corr evals/s", "value": value, "unit": "evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+            "data": "synthetic",
+            "config": {"workload": wl["name"], "queries_per_gpu": Q, "db_images": wl["K"], "grid": wl["g"],
+                       "lifted_corrs_per_step": matches, "depth": wl["depth"],
+                       "l2": f"fields {plan.field_bytes / 1e9:.2f} GB/GPU",
+                       "parallelism": f"query-sharded x{world}, no collective"},
+            "queries_per_s": qps, "converged_frac": conv_rate, "e2e": e2e, "roofline": roof,
+            "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
+            "stage_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in prof.items()},
+        }
+        print(json.dumps(line), flush=True)
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -204,12 +379,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(LIFT_WORKLOADS), default="c3")
     ap.add_argument("--queries", type=int, default=None, help="override queries per GPU")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
-    wl = dict(WORKLOADS[args.workload])
+    lifted = args.workload in LIFT_WORKLOADS
+    wl = dict(LIFT_WORKLOADS[args.workload] if lifted else WORKLOADS[args.workload])
     if args.queries:
         wl["queries"] = args.queries
     if args.impl == "reference":
@@ -227,6 +403,11 @@ def main():
     from paper_2601_04185_b200 import _lib
     from paper_2601_04185_b200.geometry import CameraIntrinsics
     from paper_2601_04185_b200.posest import RansacConfig, ransac_pnp_device, ransac_pnp_host
+    if lifted:
+        run_lift_bench(args, wl, rank, world, local, dist)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     Q, n = wl["queries"], wl["n"]
     seed0 = 3000 + 100_000 * rank

@@ -124,7 +124,7 @@ EXPORTED_SYMBOLS = (
     "vl_decode_depth",
 )
 
-STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final")
+STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final", "lift")
 
 
 class Context:

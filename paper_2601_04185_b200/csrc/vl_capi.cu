@@ -567,7 +567,10 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
   a.w_out = w_out;
   a.entry_out = entry_out;
   a.capacity = capacity;
+  c->prof_stream = st;
+  prof_hook(c, kStageLift, true);
   c->launches += launch_lift(a, field_f64, mode, st);
+  prof_hook(c, kStageLift, false);
   if ((rc = check_launch(c))) return rc;
   int64_t* hoff = (int64_t*)(h + meta);
   VL_CUDA(c, cudaMemcpyAsync(hoff, a.seg_off, (nseg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -576,7 +579,9 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
   if (hoff[nseg] > capacity)
     return fail(c, VL_ERR_INVALID, "output capacity " + std::to_string(capacity) + " < " + std::to_string(hoff[nseg]) + " matches");
   if (!px_out || !X_out || !w_out) return fail(c, VL_ERR_INVALID, "null output array");
+  prof_hook(c, kStageLift, true);
   c->launches += launch_lift_write(a, field_f64, mode, st);
+  prof_hook(c, kStageLift, false);
   return check_launch(c);
 }
 

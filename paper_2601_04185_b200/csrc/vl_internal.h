@@ -92,7 +92,7 @@ struct Outputs {
 int launch_prep(const Work& wk, const Inputs& in, int Q, cudaStream_t st);
 // profiling stages (vl_profile_read order)
 enum { kStagePrep = 0, kStageSample, kStageP3P, kStageCompact, kStageScore, kStageScan, kStageActive,
-       kStageFinal, kNumStages };
+       kStageFinal, kStageLift, kNumStages };
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
                  cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg);
 int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,

@@ -29,7 +29,7 @@ from .posest import (Match2D3D, PoseEstimate, RansacConfig, _estimates_from, _in
 __all__ = [
     "CONFIDENCE_THRESHOLD", "CorrespondenceField", "DepthMap", "DescriptorIndex", "FieldPair",
     "QuantizedDepthMap", "QueryJob", "dequantize_depth", "filter_matches_arrays", "interp_depth",
-    "interp_depth_many", "lift", "lift_arrays", "localize", "localize_batch",
+    "interp_depth_many", "LiftPlan", "lift", "lift_arrays", "localize", "localize_batch",
 ]
 
 CONFIDENCE_THRESHOLD = 0.05
@@ -87,7 +87,10 @@ class DepthMap:
     intrinsics: CameraIntrinsics
 
     def __post_init__(self):
-        self.values = np.ascontiguousarray(self.values, dtype=np.float32)
+        # float16 storage is kept as-is (compressed-map HBM format); every f16
+        # value widens exactly to the f32 the reference would hold
+        half = np.asarray(self.values).dtype == np.float16
+        self.values = np.ascontiguousarray(self.values, dtype=np.float16 if half else np.float32)
         self.valid = np.ascontiguousarray(self.valid, dtype=bool)
         if self.values.shape != self.valid.shape or self.values.ndim != 2:
             raise ValueError("values and valid must be equal 2-D shapes")
@@ -442,6 +445,102 @@ def _plan(jobs, vmap, index, depth_cache, device_cache):
     return segs, recs
 
 
+class LiftPlan:
+    """A query set's fields and depth resident in HBM, ready to lift + estimate.
+
+    Construction does the host work once (retrieval ranking, field/depth
+    upload, segment table); ``lift()`` / ``run_device()`` then run entirely
+    on the GPU and can be repeated (the device-resident throughput path).
+    """
+
+    def __init__(self, jobs, vmap, index=None, depth_cache=None, device_cache=None,
+                 threshold: float = CONFIDENCE_THRESHOLD):
+        import torch
+        if not 0 <= threshold <= 1:
+            raise ValueError(f"threshold must be in [0, 1], got {threshold}")
+        self.jobs = list(jobs)
+        self.threshold = float(threshold)
+        self.device_cache = {} if device_cache is None else device_cache
+        spec, recs = _plan(self.jobs, vmap, index, depth_cache, self.device_cache)
+        self.nseg = len(spec)
+        self.seg_q = np.array([s[0] for s in spec], dtype=np.int64)
+        self.up = _FieldUpload([s[4] for s in spec])
+        self.segs = (_lib.LiftSegment * max(self.nseg, 1))()
+        cap = 0
+        for i, (q, e, d, di, f) in enumerate(spec):
+            s = self.segs[i]
+            s.query, s.entry, s.direction, s.depth = q, e, d, di
+            s.grid_w, s.grid_h = f.grid_w, f.grid_h
+            s.scale_x, s.scale_y = float(f.scale_x), float(f.scale_y)
+            s.targets, s.confidence = self.up.ptrs(i)
+            cap += f.grid_w * f.grid_h
+        self.ndep = len(recs)
+        self.deps = (_lib.LiftDepth * max(self.ndep, 1))(*recs)
+        self.cap = max(cap, 1)
+        self.px = torch.empty((self.cap, 2), dtype=torch.float64, device="cuda")
+        self.X = torch.empty((self.cap, 3), dtype=torch.float64, device="cuda")
+        self.w = torch.empty((self.cap,), dtype=torch.float64, device="cuda")
+        self.ent = torch.empty((self.cap,), dtype=torch.int32, device="cuda")
+        self.offs = np.zeros(self.nseg + 1, dtype=np.int64)
+        self.cells = cap
+        self.field_bytes = int(self.up.targets.numel() * self.up.item + self.up.conf.numel() * self.up.item)
+
+    def lift(self):
+        """Run the lift; returns per-query [start, end) match ranges (host)."""
+        ctx = _lib.context()
+        rc = _lib.lib().vl_lift(ctx.handle, self.segs, self.nseg, self.deps, self.ndep, 1 if self.up.f64 else 0,
+                                self.threshold, 0, self.px.data_ptr(), self.X.data_ptr(), self.w.data_ptr(),
+                                self.ent.data_ptr(), self.cap, self.offs.ctypes.data_as(C.POINTER(C.c_int64)),
+                                _lib.stream_ptr())
+        ctx.check(rc, "vl_lift")
+        Q = len(self.jobs)
+        start = np.zeros(Q, dtype=np.int64)
+        end = np.zeros(Q, dtype=np.int64)
+        prev = 0
+        for qi in range(Q):
+            idx = np.nonzero(self.seg_q == qi)[0]
+            if idx.size:
+                start[qi], end[qi] = self.offs[idx[0]], self.offs[idx[-1] + 1]
+                prev = end[qi]
+            else:
+                start[qi] = end[qi] = prev
+        return start, end
+
+    def run_device(self, cfg: RansacConfig, seeds=None, out=None):
+        """Lift + batched estimator, all on device.  Returns (out dict or None,
+        estimated query indices, their match offsets, per-query ranges)."""
+        import torch
+        Q = len(self.jobs)
+        seeds = [cfg.seed] * Q if seeds is None else list(seeds)
+        start, end = self.lift()
+        run = [qi for qi in range(Q) if end[qi] - start[qi] >= 3]
+        if not run:
+            return None, run, None, (start, end)
+        offsets = np.concatenate([[0], np.cumsum([end[qi] - start[qi] for qi in run])]).astype(np.int64)
+        if all(start[run[i + 1]] == end[run[i]] for i in range(len(run) - 1)):
+            a, b = int(start[run[0]]), int(end[run[-1]])
+            dpx, dX, dw = self.px[a:b], self.X[a:b], self.w[a:b]
+        else:
+            sl = [slice(int(start[qi]), int(end[qi])) for qi in run]
+            dpx = torch.cat([self.px[s] for s in sl]).contiguous()
+            dX = torch.cat([self.X[s] for s in sl]).contiguous()
+            dw = torch.cat([self.w[s] for s in sl]).contiguous()
+        res = ransac_pnp_device(dpx, dX, dw, offsets, [self.jobs[qi].intrinsics for qi in run],
+                                [seeds[qi] for qi in run], cfg, out=out)
+        return res, run, offsets, (start, end)
+
+    def localize(self, cfg: RansacConfig, seeds=None) -> list:
+        out, run, offsets, (start, end) = self.run_device(cfg, seeds)
+        res: list = [None] * len(self.jobs)
+        for qi in range(len(self.jobs)):
+            if qi not in run:
+                res[qi] = _failure(int(end[qi] - start[qi]))
+        if run:
+            for qi, est in zip(run, _estimates_from(out, offsets)):
+                res[qi] = est
+        return res
+
+
 def localize_batch(jobs, vmap, cfg: RansacConfig, seeds=None, index=None, depth_cache=None,
                    confidence_threshold: float = CONFIDENCE_THRESHOLD, device_cache=None):
     """Retrieve, lift (one GPU launch sequence for every query) and estimate every pose.
@@ -450,45 +549,10 @@ def localize_batch(jobs, vmap, cfg: RansacConfig, seeds=None, index=None, depth_
     ``device_cache`` (dict) keeps decoded depth resident in HBM across calls.
     """
     jobs = list(jobs)
-    Q = len(jobs)
-    if Q == 0:
+    if not jobs:
         return []
-    if seeds is None:
-        seeds = [cfg.seed] * Q
-    if device_cache is None:
-        device_cache = {}
-    segs, recs = _plan(jobs, vmap, index, depth_cache, device_cache)
-    px, X, w, _, offs, _ = _run_lift(segs, recs, confidence_threshold)
-    # per-query ranges: segments are grouped by query in order
-    q_start = np.zeros(Q + 1, dtype=np.int64)
-    seg_q = np.array([s[0] for s in segs], dtype=np.int64)
-    for qi in range(Q):
-        idx = np.nonzero(seg_q == qi)[0]
-        q_start[qi] = offs[idx[0]] if idx.size else (q_start[qi - 1] if qi else 0)
-    q_end = np.array([offs[np.nonzero(seg_q == qi)[0][-1] + 1] if np.any(seg_q == qi) else q_start[qi]
-                      for qi in range(Q)], dtype=np.int64)
-    res: list = [None] * Q
-    run = [qi for qi in range(Q) if q_end[qi] - q_start[qi] >= 3]
-    for qi in range(Q):
-        if qi not in run:
-            res[qi] = _failure(int(q_end[qi] - q_start[qi]))
-    if run:
-        offsets = np.concatenate([[0], np.cumsum([q_end[qi] - q_start[qi] for qi in run])]).astype(np.int64)
-        contiguous = all(q_start[run[i + 1]] == q_end[run[i]] for i in range(len(run) - 1))
-        if contiguous:
-            a, b = int(q_start[run[0]]), int(q_end[run[-1]])
-            dpx, dX, dw = px[a:b], X[a:b], w[a:b]
-        else:
-            import torch
-            sl = [slice(int(q_start[qi]), int(q_end[qi])) for qi in run]
-            dpx = torch.cat([px[s] for s in sl]).contiguous()
-            dX = torch.cat([X[s] for s in sl]).contiguous()
-            dw = torch.cat([w[s] for s in sl]).contiguous()
-        out = ransac_pnp_device(dpx.contiguous(), dX.contiguous(), dw.contiguous(), offsets,
-                                [jobs[qi].intrinsics for qi in run], [seeds[qi] for qi in run], cfg)
-        for qi, est in zip(run, _estimates_from(out, offsets)):
-            res[qi] = est
-    return res
+    plan = LiftPlan(jobs, vmap, index, depth_cache, device_cache, confidence_threshold)
+    return plan.localize(cfg, seeds)
 
 
 def localize(query_job, vmap, cfg: RansacConfig, index=None, depth_cache=None,

@@ -92,6 +92,132 @@ def refine_problem(rng, n, noise, outlier_frac):
     return start, X, px, w
 
 
+# ----------------------------------------------------------------------------- generator B
+# Plane scene with analytic depth and bidirectional dense fields (BASELINE
+# configs C2 / C5: 560^2 images, f = 280).  Written for this repo (the
+# reference synth is not available on the GPU box); same shape of data as
+# visloc.synth (plane patch, look-at cameras, corrupt() noise model).
+
+def _look_at(center, target, roll):
+    z = target - center
+    z = z / np.linalg.norm(z)
+    up = np.array([0.0, -1.0, 0.0])
+    x = np.cross(up, z)
+    x = x / np.linalg.norm(x)
+    y = np.cross(z, x)
+    Rc = np.stack([x, y, z])  # rows: camera axes in world
+    cr, sr = math.cos(roll), math.sin(roll)
+    Rr = np.array([[cr, -sr, 0.0], [sr, cr, 0.0], [0.0, 0.0, 1.0]])
+    R = Rr @ Rc
+    return R, -R @ center
+
+
+class PlaneScene:
+    def __init__(self, W=560, f=280.0, plane_z=3.0, extent=8.0, seed=0):
+        self.W, self.f, self.c, self.plane_z, self.extent = W, f, W / 2.0, plane_z, extent
+        self.rng = np.random.default_rng(seed)
+
+    def camera(self, spread=0.3, backoff=0.25, roll_deg=3.0, rng=None):
+        r = self.rng if rng is None else rng
+        center = np.array([r.uniform(-spread, spread), r.uniform(-spread, spread),
+                           -self.plane_z * backoff * r.uniform(0.0, 1.0)])
+        return _look_at(center, np.array([0.0, 0.0, self.plane_z]), math.radians(r.uniform(-roll_deg, roll_deg)))
+
+    def _hit(self, cam, u, v):
+        R, t = cam
+        d = np.stack([(u - self.c) / self.f, (v - self.c) / self.f, np.ones_like(u)], -1) @ R  # world dirs
+        C = -R.T @ t
+        s = (self.plane_z - C[2]) / d[..., 2]
+        P = C + s[..., None] * d
+        ok = (s > 0) & (np.abs(P[..., 0]) <= self.extent) & (np.abs(P[..., 1]) <= self.extent)
+        return P, ok
+
+    def depth_grid(self, cam, g):
+        s = self.W / g
+        u, v = np.meshgrid((np.arange(g) + 0.5) * s, (np.arange(g) + 0.5) * s)
+        P, ok = self._hit(cam, u, v)
+        z = (P @ cam[0].T + cam[1])[..., 2]
+        ok &= z > 0
+        return np.where(ok, z, 0.0).astype(np.float32), ok
+
+    def field(self, cam_a, cam_b, g, rng, sigma=1.0, outlier_frac=0.7):
+        """(targets (g,g,2) f32, conf (g,g) f32, scale): exact matches a->b, then corrupted."""
+        s = self.W / g
+        u, v = np.meshgrid((np.arange(g) + 0.5) * s, (np.arange(g) + 0.5) * s)
+        P, ok = self._hit(cam_a, u, v)
+        xc = P @ cam_b[0].T + cam_b[1]
+        ok &= xc[..., 2] > 0
+        with np.errstate(divide="ignore", invalid="ignore"):
+            tu = self.f * xc[..., 0] / xc[..., 2] + self.c
+            tv = self.f * xc[..., 1] / xc[..., 2] + self.c
+        ok &= (tu >= 0) & (tu < self.W) & (tv >= 0) & (tv < self.W)
+        tg = np.stack([tu, tv], -1) + rng.normal(0, sigma, (g, g, 2))
+        conf = rng.uniform(0.5, 1.0, (g, g))
+        out = ok & (rng.random((g, g)) < outlier_frac)
+        tg[out] = rng.uniform(0, self.W, (int(out.sum()), 2))
+        conf[out] = rng.uniform(0.0, 0.3, int(out.sum()))
+        conf[~ok] = 0.0
+        tg[~ok] = 0.0
+        return tg.astype(np.float32), conf.astype(np.float32), s
+
+
+def lifted_scene(K, Q, g, seed=0, depth_kind="f32", outlier_frac=0.7, sigma=1.0, only=None):
+    """(vmap, jobs, depth_cache) for the GPU package: K database cameras, Q query
+    jobs with bidirectional fields to every database camera; depth as f32 / f16
+    DepthMap (via the returned depth_cache) or u8 log codes (entry.qdepth).
+    Each query draws from its own generator, so ``only=[i, ...]`` rebuilds a
+    subset identically (CPU-baseline workers)."""
+    from paper_2601_04185_b200.geometry import CameraIntrinsics, Pose, matrix_to_quat
+    from paper_2601_04185_b200.localizer import (CorrespondenceField, DepthMap, FieldPair,
+                                                 QuantizedDepthMap, QueryJob)
+    sc = PlaneScene(seed=seed)
+    intr = CameraIntrinsics(sc.f, sc.f, sc.c, sc.c, sc.W, sc.W)
+    rng = np.random.default_rng(seed + 1)
+
+    class Entry:
+        pass
+
+    class Map:
+        pass
+
+    entries, depth_cache = [], {}
+    for k in range(K):
+        cam = sc.camera()
+        e = Entry()
+        e.id = f"cam{k:03d}"
+        e.pose = Pose(matrix_to_quat(cam[0]), cam[1])
+        e.intrinsics = intr
+        e.descriptor = rng.normal(size=16).astype(np.float32)
+        e.cam = cam
+        vals, valid = sc.depth_grid(cam, g)
+        e.qdepth = None
+        if depth_kind == "u8":
+            span = math.log(128.0) - math.log(0.25)
+            uq = (np.log(np.clip(vals.astype(np.float64), 0.25, 128.0)) - math.log(0.25)) / span
+            codes = np.where(valid, 1 + np.floor(uq * 254 + 0.5), 0).astype(np.uint8)
+            e.qdepth = QuantizedDepthMap(codes, 0.25, 128.0, 255, intr)
+        else:
+            dt = np.float16 if depth_kind == "f16" else np.float32
+            depth_cache[e.id] = DepthMap(vals.astype(dt), valid, intr)
+        entries.append(e)
+    vmap = Map()
+    vmap.entries = entries
+    jobs = []
+    for qi in (range(Q) if only is None else only):
+        rng = np.random.default_rng([seed, 7, qi])
+        cam = sc.camera(spread=0.24, rng=rng)
+        fields = {}
+        for e in entries:
+            t1, c1, s = sc.field(cam, e.cam, g, rng, sigma, outlier_frac)
+            t2, c2, _ = sc.field(e.cam, cam, g, rng, sigma, outlier_frac)
+            fields[e.id] = FieldPair(query_to_db=CorrespondenceField("q", e.id, t1, c1, s, s),
+                                     db_to_query=CorrespondenceField(e.id, "q", t2, c2, s, s))
+        job = QueryJob(f"query{qi:04d}", intr, rng.normal(size=16), fields, k_loc=K)
+        job.gt = Pose(matrix_to_quat(cam[0]), cam[1])
+        jobs.append(job)
+    return vmap, jobs, (depth_cache if depth_kind != "u8" else None)
+
+
 def batch_a(Q, n, outlier_frac, sigma, seed0):
     """Q generator-A queries with per-query random GT poses (bench C1/C3/C4 inputs)."""
     pxs, Xs, ws = [], [], []
