@@ -90,6 +90,92 @@ VL_HD bool p3p_setup(const double* f, const double* P, P3PGeo& g, double* quart)
   return true;
 }
 
+// Ferrari / resolvent-cubic approximations of the four roots of the monic
+// quartic x^4 + b3 x^3 + b2 x^2 + b1 x + b0 (b[k] = coefficient of x^k).
+// Only a starting point: the Aberth iterations below polish (and repair) it.
+VL_HD bool ferrari_init(const double* b, double* zr, double* zi) {
+  const double A = b[3], B = b[2], Cc = b[1], D = b[0];
+  const double A2 = A * A;
+  const double p = B - 0.375 * A2;
+  const double q = Cc - 0.5 * A * B + 0.125 * A2 * A;
+  const double r = D - 0.25 * A * Cc + 0.0625 * A2 * B - 0.01171875 * A2 * A2;
+  // resolvent m^3 + p m^2 + (p^2/4 - r) m - q^2/8 = 0: largest real root
+  const double a = p, bb = 0.25 * p * p - r, cc = -0.125 * q * q;
+  const double Q = (a * a - 3.0 * bb) / 9.0, R = (2.0 * a * a * a - 9.0 * a * bb + 27.0 * cc) / 54.0;
+  double m;
+  if (R * R < Q * Q * Q) {
+    const double sq = sqrt(Q);
+    const double th = acos(fmin(fmax(R / (sq * sq * sq), -1.0), 1.0));
+    m = -2.0 * sq * cos(th / 3.0) - a / 3.0;  // k = 0 gives the largest root
+    m = fmax(m, -2.0 * sq * cos((th + 6.283185307179586) / 3.0) - a / 3.0);
+    m = fmax(m, -2.0 * sq * cos((th - 6.283185307179586) / 3.0) - a / 3.0);
+  } else {
+    const double Aa = -copysign(cbrt(fabs(R) + sqrt(R * R - Q * Q * Q)), R);
+    const double Bb = (Aa != 0.0) ? Q / Aa : 0.0;
+    m = (Aa + Bb) - a / 3.0;
+  }
+  for (int it = 0; it < 2; ++it) {  // Newton polish of m
+    const double f = ((m + a) * m + bb) * m + cc, fp = (3.0 * m + 2.0 * a) * m + bb;
+    if (fp != 0.0) m -= f / fp;
+  }
+  const double sh = 0.25 * A;
+  if (!(m > 1e-14 * (fabs(p) + 1e-300))) {
+    // (near-)biquadratic: y^2 = (-p +- sqrt(p^2 - 4r)) / 2
+    const double dsc = p * p - 4.0 * r;
+    double wr[2], wi[2];
+    if (dsc >= 0) {
+      const double s = sqrt(dsc);
+      wr[0] = 0.5 * (-p + s);
+      wr[1] = 0.5 * (-p - s);
+      wi[0] = wi[1] = 0.0;
+    } else {
+      wr[0] = wr[1] = -0.5 * p;
+      wi[0] = 0.5 * sqrt(-dsc);
+      wi[1] = -wi[0];
+    }
+    for (int k = 0; k < 2; ++k) {  // complex square roots of w
+      const double mod = sqrt(wr[k] * wr[k] + wi[k] * wi[k]);
+      double sr = sqrt(fmax(0.5 * (mod + wr[k]), 0.0));
+      double si = sqrt(fmax(0.5 * (mod - wr[k]), 0.0));
+      if (wi[k] < 0) si = -si;
+      zr[2 * k] = sr - sh;
+      zi[2 * k] = si;
+      zr[2 * k + 1] = -sr - sh;
+      zi[2 * k + 1] = -si;
+    }
+  } else {
+    const double s = sqrt(2.0 * m);
+    const double h = 0.5 * p + m, g = q / (2.0 * s);
+    // y^2 - s y + (h + g) = 0 and y^2 + s y + (h - g) = 0
+    const double c0[2] = {h + g, h - g};
+    const double sg[2] = {s, -s};
+    for (int k = 0; k < 2; ++k) {
+      const double dsc = sg[k] * sg[k] - 4.0 * c0[k];
+      if (dsc >= 0) {
+        const double sd = sqrt(dsc);
+        zr[2 * k] = 0.5 * (sg[k] + sd) - sh;
+        zr[2 * k + 1] = 0.5 * (sg[k] - sd) - sh;
+        zi[2 * k] = zi[2 * k + 1] = 0.0;
+      } else {
+        const double sd = sqrt(-dsc);
+        zr[2 * k] = zr[2 * k + 1] = 0.5 * sg[k] - sh;
+        zi[2 * k] = 0.5 * sd;
+        zi[2 * k + 1] = -0.5 * sd;
+      }
+    }
+  }
+  bool ok = true;
+  for (int k = 0; k < 4; ++k) ok &= isfinite(zr[k]) && isfinite(zi[k]);
+  // Aberth needs distinct starting points
+  for (int k = 0; k < 4 && ok; ++k)
+    for (int j = k + 1; j < 4; ++j)
+      if (zr[k] == zr[j] && zi[k] == zi[j]) {
+        const double bump = 1e-7 * (1.0 + fabs(zr[k]));
+        zi[j] += (j - k) * bump;
+      }
+  return ok;
+}
+
 // Real positive roots (ascending) of sum_k c[k] v^(4-k); returns the count.
 // Mirrors np.roots' degree handling: exact leading/trailing zeros stripped,
 // zero roots never count (Re > 0 required).
@@ -118,6 +204,8 @@ VL_HD int quartic_real_pos_roots(const double* c_in, double* out) {
     zr[0] = -b[0];
     zi[0] = 0.0;
   } else {
+    const bool seeded = (d == 4) && ferrari_init(b, zr, zi);
+    if (!seeded) {
     // Newton-polygon initial radii: upper convex hull of (k, log|b_k|).
     int hk[5];
     float hl[5];
@@ -152,6 +240,7 @@ VL_HD int quartic_real_pos_roots(const double* c_in, double* out) {
       zr[zc] = cos(1.0 + zc);
       zi[zc] = sin(1.0 + zc);
     }
+    }  // !seeded
 #pragma unroll
     for (int k = 0; k < 4; ++k) conv[k] = (k >= d);
     for (int it = 0; it < 60; ++it) {
