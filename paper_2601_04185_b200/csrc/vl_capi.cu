@@ -24,7 +24,7 @@ struct vl_ctx {
   std::string err;
   int64_t launches = 0;
   DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, P32, hsrc, items, item_count,
-      partial, sub_px, sub_X, sub_w, sub32, comp_px, comp_X, comp_w;
+      partial, sub_pk, sub32, comp_pk;
   DevBuf scratch;  // small standalone-call scratch
   DevBuf lift_meta, lift_blk_count, lift_blk_off, lift_seg_off;  // vl_lift
   void* h_pinned = nullptr;
@@ -183,8 +183,8 @@ int vl_destroy(vl_ctx* c) {
   cudaSetDevice(c->device);
   DevBuf* bufs[] = {&c->qs,      &c->active, &c->next_active, &c->active_count, &c->samples, &c->slots,
                     &c->slot_cnt, &c->P32,   &c->hsrc,        &c->items,        &c->item_count,
-                    &c->partial, &c->sub_px, &c->sub_X,       &c->sub_w,        &c->sub32,   &c->comp_px,
-                    &c->comp_X,  &c->comp_w, &c->scratch, &c->lift_meta, &c->lift_blk_count,
+                    &c->partial, &c->sub_pk, &c->sub32,       &c->comp_pk,
+                    &c->scratch, &c->lift_meta, &c->lift_blk_count,
                     &c->lift_blk_off, &c->lift_seg_off};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
@@ -318,13 +318,9 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
         (rc = ensure(c, c->items, item_cap * sizeof(ScoreItem))) ||
         (rc = ensure(c, c->item_count, 2 * sizeof(int))) ||
         (rc = ensure(c, c->partial, (size_t)Qn * max_split * HCAP * sizeof(float))) ||
-        (rc = ensure(c, c->sub_px, nsub_tot * 2 * sizeof(double))) ||
-        (rc = ensure(c, c->sub_X, nsub_tot * 3 * sizeof(double))) ||
-        (rc = ensure(c, c->sub_w, nsub_tot * sizeof(double))) ||
+        (rc = ensure(c, c->sub_pk, nsub_tot * 3 * sizeof(double2))) ||
         (rc = ensure(c, c->sub32, nsub_tot * 2 * sizeof(float4))) ||
-        (rc = ensure(c, c->comp_px, ncomp * 2 * sizeof(double))) ||
-        (rc = ensure(c, c->comp_X, ncomp * 3 * sizeof(double))) ||
-        (rc = ensure(c, c->comp_w, ncomp * sizeof(double))))
+        (rc = ensure(c, c->comp_pk, ncomp * 3 * sizeof(double2))))
       return rc;
     const size_t host_bytes = Qn * sizeof(QState) + Qn * sizeof(int) + 64;
     if ((rc = ensure_host(c, host_bytes))) return rc;
@@ -348,13 +344,9 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     wk.items = (ScoreItem*)c->items.p;
     wk.item_count = (int*)c->item_count.p;
     wk.partial = (float*)c->partial.p;
-    wk.sub_px = (double*)c->sub_px.p;
-    wk.sub_X = (double*)c->sub_X.p;
-    wk.sub_w = (double*)c->sub_w.p;
+    wk.sub_pk = (double2*)c->sub_pk.p;
     wk.sub32 = (float4*)c->sub32.p;
-    wk.comp_px = (double*)c->comp_px.p;
-    wk.comp_X = (double*)c->comp_X.p;
-    wk.comp_w = (double*)c->comp_w.p;
+    wk.comp_pk = (double2*)c->comp_pk.p;
     wk.B = (int)B;
     wk.HCAP = (int)HCAP;
     wk.NSPLIT = max_split;

@@ -60,13 +60,9 @@ struct Work {
   ScoreItem* items;      // [item_cap]
   int* item_count;       // [0] items appended this round, [1] scoring work cursor
   float* partial;        // [Qc][NSPLIT][HCAP]
-  double* sub_px;        // [Nsub][2]
-  double* sub_X;         // [Nsub][3]
-  double* sub_w;         // [Nsub]
+  double2* sub_pk;       // [Nsub][3] packed fp64 scoring subset: (X,Y) (Z,u) (v,w)
   float4* sub32;         // [Nsub][2]
-  double* comp_px;       // [N][2]
-  double* comp_X;        // [N][3]
-  double* comp_w;        // [N]
+  double2* comp_pk;      // [N][3] packed full-set inliers (final refinement)
   int B, HCAP, NSPLIT;
   int64_t item_cap;
 };

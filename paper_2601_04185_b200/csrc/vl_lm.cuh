@@ -13,6 +13,11 @@
 //    already carries the next iteration's normal equations (the reference
 //    recomputes them at the same pose, so the values are identical).
 //  Reductions are deterministic (fixed warp-shuffle tree + ordered warp sum).
+//
+// Point sets come in two layouts: the caller's AoS arrays (px (n,2), X (n,3),
+// w (n)) and the packed layout the library writes for data it re-reads many
+// times (scoring subset, compacted inliers): three double2 per point,
+// (X, Y), (Z, u), (v, w) — three coalesced 16-byte loads per point.
 #pragma once
 #include "vl_common.cuh"
 
@@ -21,12 +26,48 @@ namespace vl {
 enum LossKind { kTruncated = 0, kCauchy = 1 };
 constexpr int kRed = 28;  // cost, g[6], H upper triangle [21]
 
+struct AosPts {
+  const double* px;
+  const double* X;
+  const double* w;
+  int n;
+  __device__ __forceinline__ void load(int i, double* P, double& u, double& v, double& ww) const {
+    P[0] = X[3 * i];
+    P[1] = X[3 * i + 1];
+    P[2] = X[3 * i + 2];
+    u = px[2 * i];
+    v = px[2 * i + 1];
+    ww = w[i];
+  }
+};
+
+struct PackedPts {
+  const double2* p;  // [3n]
+  int n;
+  __device__ __forceinline__ void load(int i, double* P, double& u, double& v, double& ww) const {
+    const double2 a = __ldg(p + 3 * i), b = __ldg(p + 3 * i + 1), c = __ldg(p + 3 * i + 2);
+    P[0] = a.x;
+    P[1] = a.y;
+    P[2] = b.x;
+    u = b.y;
+    v = c.x;
+    ww = c.y;
+  }
+};
+
+__device__ __forceinline__ void pack_point(double2* dst, int i, const double* P, double u, double v, double w) {
+  dst[3 * i] = make_double2(P[0], P[1]);
+  dst[3 * i + 1] = make_double2(P[2], u);
+  dst[3 * i + 2] = make_double2(v, w);
+}
+
 template <int NT>
 struct LMShared {
   double R[9], t[3];
   Pose cur, cand;
   double red[kRed];
   double scratch[(NT / 32) * kRed];
+  double A[36], b[6];
   int flag;
   int ibuf[NT / 32];
 };
@@ -51,100 +92,145 @@ __device__ __forceinline__ void cam_point(const double* R, const double* t, cons
   z = dadd(dadd(dadd(dmul(X[0], R[6]), dmul(X[1], R[7])), dmul(X[2], R[8])), t[2]);
 }
 
+// fp64 MSAC error of one point (posest._errors_sq order); +inf behind camera.
+__device__ __forceinline__ double msac_e2(const double* R, const double* t, const Intr& in, const double* P,
+                                          double u, double v) {
+  double x, y, z;
+  cam_point(R, t, P, x, y, z);
+  const bool front = z > 0;
+  const double zs = front ? z : 1.0;
+  double du = dmul(in.fx, x);
+  du = __ddiv_rn(du, zs);
+  du = dadd(du, dsub(in.cx, u));
+  double dv = dmul(in.fy, y);
+  dv = __ddiv_rn(dv, zs);
+  dv = dadd(dv, dsub(in.cy, v));
+  double e2 = dmul(du, du);
+  e2 = dadd(e2, dmul(dv, dv));
+  return front ? e2 : CUDART_INF;
+}
+
 // MSAC pass with the pose currently in sm.R / sm.t.  Writes flags (if not
 // null), returns cost and inlier count in sm.red[0], sm.red[1].
-template <int NT>
-__device__ void msac_pass(LMShared<NT>& sm, const PointSet& ps, const Intr& in, double tau,
-                          uint8_t* flags) {
+template <int NT, typename PS>
+__device__ void msac_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, double tau, uint8_t* flags) {
   const double t2 = dmul(tau, tau);
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = sm.R[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = sm.t[k];
   double acc[2] = {0.0, 0.0};
-  for (int i = threadIdx.x; i < ps.n; i += NT) {
-    const double X[3] = {ps.X[3 * i], ps.X[3 * i + 1], ps.X[3 * i + 2]};
-    double x, y, z;
-    cam_point(sm.R, sm.t, X, x, y, z);
-    const bool front = z > 0;
-    const double zs = front ? z : 1.0;
-    double du = dmul(in.fx, x);
-    du = __ddiv_rn(du, zs);
-    du = dadd(du, dsub(in.cx, ps.px[2 * i]));
-    double dv = dmul(in.fy, y);
-    dv = __ddiv_rn(dv, zs);
-    dv = dadd(dv, dsub(in.cy, ps.px[2 * i + 1]));
-    double e2 = dmul(du, du);
-    e2 = dadd(e2, dmul(dv, dv));
-    if (!front) e2 = CUDART_INF;
-    acc[0] = acc[0] + dmul(ps.w[i], fmin(e2, t2));
-    const bool inl = e2 < t2;
-    acc[1] += inl ? 1.0 : 0.0;
-    if (flags) flags[i] = inl ? 1 : 0;
+  int i = threadIdx.x;
+  // two points per trip: both loads in flight before the arithmetic
+  for (; i + NT < ps.n; i += 2 * NT) {
+    double P0[3], u0, v0, w0, P1[3], u1, v1, w1;
+    ps.load(i, P0, u0, v0, w0);
+    ps.load(i + NT, P1, u1, v1, w1);
+    const double e0 = msac_e2(R, t, in, P0, u0, v0);
+    const double e1 = msac_e2(R, t, in, P1, u1, v1);
+    acc[0] = acc[0] + dmul(w0, fmin(e0, t2));
+    acc[0] = acc[0] + dmul(w1, fmin(e1, t2));
+    acc[1] += (e0 < t2 ? 1.0 : 0.0) + (e1 < t2 ? 1.0 : 0.0);
+    if (flags) {
+      flags[i] = e0 < t2 ? 1 : 0;
+      flags[i + NT] = e1 < t2 ? 1 : 0;
+    }
   }
-  double* out = sm.red;
-  block_sum<NT, 2>(acc, sm.scratch, out);
+  if (i < ps.n) {
+    double P0[3], u0, v0, w0;
+    ps.load(i, P0, u0, v0, w0);
+    const double e0 = msac_e2(R, t, in, P0, u0, v0);
+    acc[0] = acc[0] + dmul(w0, fmin(e0, t2));
+    acc[1] += e0 < t2 ? 1.0 : 0.0;
+    if (flags) flags[i] = e0 < t2 ? 1 : 0;
+  }
+  block_sum<NT, 2>(acc, sm.scratch, sm.red);
+}
+
+// Cost / gradient / normal-matrix contribution of one point.
+template <bool GRAD>
+__device__ __forceinline__ void lm_point(const double* R, const double* t, const Intr& in, int kind, double s2,
+                                         const double* P, double u_obs, double v_obs, double w, double* acc,
+                                         double& behind) {
+  double x, y, z;
+  cam_point(R, t, P, x, y, z);
+  if (!(z > 0)) {
+    behind = 1.0;
+    if (kind == kTruncated) acc[0] += dmul(w, s2);
+    return;
+  }
+  const double u = dadd(__ddiv_rn(dmul(in.fx, x), z), in.cx);
+  const double v = dadd(__ddiv_rn(dmul(in.fy, y), z), in.cy);
+  const double ru = dsub(u, u_obs);
+  const double rv = dsub(v, v_obs);
+  const double e2 = dadd(dmul(ru, ru), dmul(rv, rv));
+  double rho, wt;
+  if (kind == kTruncated) {
+    rho = fmin(e2, s2);
+    wt = (e2 < s2) ? 1.0 : 0.0;
+  } else {
+    const double r = __ddiv_rn(e2, s2);
+    rho = dmul(dmul(0.5, s2), log1p(r));
+    wt = __ddiv_rn(0.5, dadd(1.0, r));
+  }
+  acc[0] += dmul(w, rho);
+  if (GRAD) {
+    const double wr = dmul(w, wt);
+    if (wr != 0.0) {
+      const double p00 = in.fx / z, p02 = -in.fx * x / (z * z);
+      const double p11 = in.fy / z, p12 = -in.fy * y / (z * z);
+      double J0[6], J1[6];
+      J0[0] = p02 * y;
+      J0[1] = p00 * z + p02 * (-x);
+      J0[2] = p00 * (-y);
+      J0[3] = p00;
+      J0[4] = 0.0;
+      J0[5] = p02;
+      J1[0] = p11 * (-z) + p12 * y;
+      J1[1] = p12 * (-x);
+      J1[2] = p11 * x;
+      J1[3] = 0.0;
+      J1[4] = p11;
+      J1[5] = p12;
+#pragma unroll
+      for (int a = 0; a < 6; ++a) acc[1 + a] += wr * (J0[a] * ru + J1[a] * rv);
+      int k = 7;
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int b = a; b < 6; ++b) acc[k++] += wr * (J0[a] * J0[b] + J1[a] * J1[b]);
+    }
+  }
 }
 
 // Fused robust-cost (+ gradient + normal matrix) pass at the pose in sm.R/t.
 // Result: sm.red[0] = cost (inf for Cauchy with a point behind the camera),
 // sm.red[1..6] = g (without the factor 2), sm.red[7..27] = H upper (no 2).
-template <int NT, bool GRAD>
-__device__ void lm_pass(LMShared<NT>& sm, const PointSet& ps, const Intr& in, int kind,
-                        double scale) {
+template <int NT, bool GRAD, typename PS>
+__device__ void lm_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, int kind, double scale) {
   const double s2 = dmul(scale, scale);
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = sm.R[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = sm.t[k];
   double acc[kRed];
 #pragma unroll
   for (int k = 0; k < kRed; ++k) acc[k] = 0.0;
   double behind = 0.0;
-  for (int i = threadIdx.x; i < ps.n; i += NT) {
-    const double X[3] = {ps.X[3 * i], ps.X[3 * i + 1], ps.X[3 * i + 2]};
-    const double w = ps.w[i];
-    double x, y, z;
-    cam_point(sm.R, sm.t, X, x, y, z);
-    if (!(z > 0)) {
-      behind = 1.0;
-      if (kind == kTruncated) acc[0] += dmul(w, s2);
-      continue;
-    }
-    const double u = dadd(__ddiv_rn(dmul(in.fx, x), z), in.cx);
-    const double v = dadd(__ddiv_rn(dmul(in.fy, y), z), in.cy);
-    const double ru = dsub(u, ps.px[2 * i]);
-    const double rv = dsub(v, ps.px[2 * i + 1]);
-    const double e2 = dadd(dmul(ru, ru), dmul(rv, rv));
-    double rho, wt;
-    if (kind == kTruncated) {
-      rho = fmin(e2, s2);
-      wt = (e2 < s2) ? 1.0 : 0.0;
-    } else {
-      const double r = __ddiv_rn(e2, s2);
-      rho = dmul(dmul(0.5, s2), log1p(r));
-      wt = __ddiv_rn(0.5, dadd(1.0, r));
-    }
-    acc[0] += dmul(w, rho);
-    if (GRAD) {
-      const double wr = dmul(w, wt);
-      if (wr != 0.0) {
-        const double p00 = in.fx / z, p02 = -in.fx * x / (z * z);
-        const double p11 = in.fy / z, p12 = -in.fy * y / (z * z);
-        double J0[6], J1[6];
-        J0[0] = p02 * y;
-        J0[1] = p00 * z + p02 * (-x);
-        J0[2] = p00 * (-y);
-        J0[3] = p00;
-        J0[4] = 0.0;
-        J0[5] = p02;
-        J1[0] = p11 * (-z) + p12 * y;
-        J1[1] = p12 * (-x);
-        J1[2] = p11 * x;
-        J1[3] = 0.0;
-        J1[4] = p11;
-        J1[5] = p12;
-#pragma unroll
-        for (int a = 0; a < 6; ++a) acc[1 + a] += wr * (J0[a] * ru + J1[a] * rv);
-        int k = 7;
-#pragma unroll
-        for (int a = 0; a < 6; ++a)
-#pragma unroll
-          for (int b = a; b < 6; ++b) acc[k++] += wr * (J0[a] * J0[b] + J1[a] * J1[b]);
-      }
-    }
+  int i = threadIdx.x;
+  for (; i + NT < ps.n; i += 2 * NT) {
+    double P0[3], u0, v0, w0, P1[3], u1, v1, w1;
+    ps.load(i, P0, u0, v0, w0);
+    ps.load(i + NT, P1, u1, v1, w1);
+    lm_point<GRAD>(R, t, in, kind, s2, P0, u0, v0, w0, acc, behind);
+    lm_point<GRAD>(R, t, in, kind, s2, P1, u1, v1, w1, acc, behind);
+  }
+  if (i < ps.n) {
+    double P0[3], u0, v0, w0;
+    ps.load(i, P0, u0, v0, w0);
+    lm_point<GRAD>(R, t, in, kind, s2, P0, u0, v0, w0, acc, behind);
   }
   if (GRAD) {
     block_sum<NT, kRed>(acc, sm.scratch, sm.red);
@@ -160,9 +246,9 @@ __device__ void lm_pass(LMShared<NT>& sm, const PointSet& ps, const Intr& in, in
   __syncthreads();
 }
 
-// 6x6 LU with partial pivoting (np.linalg.solve / LAPACK gesv semantics:
-// fails only on an exactly zero pivot).
-__device__ __forceinline__ bool solve6(double (&A)[36], double (&b)[6]) {
+// 6x6 LU with partial pivoting in shared memory (np.linalg.solve / LAPACK
+// gesv semantics: fails only on an exactly zero pivot).  One thread.
+__device__ __forceinline__ bool solve6_smem(double* A, double* b) {
   for (int k = 0; k < 6; ++k) {
     int p = k;
     double pv = fabs(A[6 * k + k]);
@@ -207,60 +293,55 @@ struct LMResult {
 
 // Levenberg-Marquardt refinement of `start` (all threads pass the same
 // value).  Result pose in sm.cur.  trace (global, optional): accepted costs.
-template <int NT>
-__device__ LMResult lm_refine(LMShared<NT>& sm, const PointSet& ps, const Intr& in,
-                              const Pose& start, int kind, double scale, int max_iters,
-                              double gtol, double ctol, double* trace, int* trace_len) {
+// g and the upper triangle of H live in shared memory (sm.red after each
+// pass); every thread keeps only the scalars of the schedule.
+template <int NT, typename PS>
+__device__ LMResult lm_refine(LMShared<NT>& sm, const PS& ps, const Intr& in, const Pose& start, int kind,
+                              double scale, int max_iters, double gtol, double ctol, double* trace,
+                              int* trace_len) {
+  __shared__ double gH[kRed];
   if (threadIdx.x == 0) sm.cur = start;
   __syncthreads();
   set_eval_pose(sm, sm.cur);
   lm_pass<NT, true>(sm, ps, in, kind, scale);
   double cost = sm.red[0];
-  double g[6], Hu[21];
-#pragma unroll
-  for (int a = 0; a < 6; ++a) g[a] = 2.0 * sm.red[1 + a];
-#pragma unroll
-  for (int k = 0; k < 21; ++k) Hu[k] = 2.0 * sm.red[7 + k];
+  if (threadIdx.x < kRed) gH[threadIdx.x] = 2.0 * sm.red[threadIdx.x];
   int ntr = 0;
   if (trace && threadIdx.x == 0) trace[0] = cost;
   ntr = 1;
   double lam = 1e-6;
   int conv = 0;
   int it = 0;
+  __syncthreads();
   for (it = 1; it <= max_iters; ++it) {
     double gn = 0.0;
 #pragma unroll
-    for (int a = 0; a < 6; ++a) gn += g[a] * g[a];
+    for (int a = 0; a < 6; ++a) gn += gH[1 + a] * gH[1 + a];
     if (sqrt(gn) < gtol) {
       conv = 1;
       break;
-    }
-    double dg[6];
-    {
-      int k = 0;
-      for (int a = 0; a < 6; ++a)
-        for (int b = a; b < 6; ++b, ++k)
-          if (a == b) dg[a] = fmax(Hu[k], 1e-12);
     }
     bool accepted = false;
     double cc = 0.0;
     for (int trial = 0; trial < 25; ++trial) {
       if (threadIdx.x == 0) {
-        double A[36], bb[6];
-        int k = 0;
+        int k = 7;
         for (int a = 0; a < 6; ++a)
           for (int b = a; b < 6; ++b, ++k) {
-            A[6 * a + b] = Hu[k];
-            A[6 * b + a] = Hu[k];
+            sm.A[6 * a + b] = gH[k];
+            sm.A[6 * b + a] = gH[k];
           }
+        k = 7;
         for (int a = 0; a < 6; ++a) {
-          A[7 * a] = A[7 * a] + lam * dg[a];
-          bb[a] = -g[a];
+          const double dga = fmax(gH[k], 1e-12);  // diag(H) entry
+          sm.A[7 * a] = sm.A[7 * a] + lam * dga;
+          sm.b[a] = -gH[1 + a];
+          k += 6 - a;
         }
-        const bool ok = solve6(A, bb);
+        const bool ok = solve6_smem(sm.A, sm.b);
         sm.flag = ok ? 1 : 0;
         if (ok) {
-          apply_delta(sm.cur, bb, sm.cand);
+          apply_delta(sm.cur, sm.b, sm.cand);
           q2R(sm.cand.q, sm.R);
           sm.t[0] = sm.cand.t[0];
           sm.t[1] = sm.cand.t[1];
@@ -286,11 +367,8 @@ __device__ LMResult lm_refine(LMShared<NT>& sm, const PointSet& ps, const Intr& 
     lam = fmax(lam / 3.0, 1e-12);
     const double drop = cost - cc;
     cost = cc;
-#pragma unroll
-    for (int a = 0; a < 6; ++a) g[a] = 2.0 * sm.red[1 + a];
-#pragma unroll
-    for (int k = 0; k < 21; ++k) Hu[k] = 2.0 * sm.red[7 + k];
     __syncthreads();
+    if (threadIdx.x < kRed) gH[threadIdx.x] = 2.0 * sm.red[threadIdx.x];
     if (threadIdx.x == 0) {
       sm.cur = sm.cand;
       if (trace) trace[ntr] = cost;

@@ -31,12 +31,9 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in) {
     const double X = in.X[3 * src], Y = in.X[3 * src + 1], Z = in.X[3 * src + 2];
     const double w = in.w[src];
     const int64_t d = so + i;
-    wk.sub_px[2 * d] = pu;
-    wk.sub_px[2 * d + 1] = pv;
-    wk.sub_X[3 * d] = X;
-    wk.sub_X[3 * d + 1] = Y;
-    wk.sub_X[3 * d + 2] = Z;
-    wk.sub_w[d] = w;
+    wk.sub_pk[3 * d] = make_double2(X, Y);
+    wk.sub_pk[3 * d + 1] = make_double2(Z, pu);
+    wk.sub_pk[3 * d + 2] = make_double2(pv, w);
     // fp32 scoring record: X32, Y32, Z32, f32(cx - u), f32(cy - v), w32
     wk.sub32[2 * d] = make_float4((float)X, (float)Y, (float)Z, (float)(cx - pu));
     wk.sub32[2 * d + 1] = make_float4((float)(cy - pv), (float)w, 0.f, 0.f);
@@ -360,7 +357,7 @@ __device__ __forceinline__ int64_t required_iters_dev(double eps, double eta, in
 
 constexpr int kScanThreads = 256;
 
-__global__ void __launch_bounds__(kScanThreads) k_scan(Work wk, RansacParams p) {
+__global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams p) {
   extern __shared__ float costs[];
   __shared__ LMShared<kScanThreads> sm;
   __shared__ Pose s_start;
@@ -375,7 +372,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Work wk, RansacParams p) 
   }
   __syncthreads();
   const Intr in = S.in;
-  const PointSet sub{wk.sub_px + 2 * S.sub_off, wk.sub_X + 3 * S.sub_off, wk.sub_w + S.sub_off, S.nsub};
+  const PackedPts sub{wk.sub_pk + 3 * S.sub_off, S.nsub};
   double best_cost = S.best_cost;
   int has_best = S.has_best;
   Pose best = S.best;
@@ -496,9 +493,9 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
 }
 
 // ------------------------------------------------------------------ final stage
-constexpr int kFinalThreads = 512;
+constexpr int kFinalThreads = 256;
 
-__global__ void __launch_bounds__(kFinalThreads) k_final(Work wk, Inputs in, Outputs out, RansacParams p,
+__global__ void __launch_bounds__(kFinalThreads, 2) k_final(Work wk, Inputs in, Outputs out, RansacParams p,
                                                          int q_base) {
   __shared__ LMShared<kFinalThreads> sm;
   __shared__ int warp_tot[32];
@@ -507,7 +504,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(Work wk, Inputs in, Out
   const int64_t gq = q_base + q;
   const int n = S.n;
   uint8_t* flags = out.flags + S.off;
-  const PointSet full{in.px + 2 * S.off, in.X + 3 * S.off, in.w + S.off, n};
+  const AosPts full{in.px + 2 * S.off, in.X + 3 * S.off, in.w + S.off, n};
   const Intr cin = S.in;
   auto write_small = [&](const Pose& ps, int64_t cnt, double score, int conv) {
     if (threadIdx.x == 0) {
@@ -545,9 +542,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(Work wk, Inputs in, Out
   }
   // ordered compaction of the full-set inliers (X[flags_full], posest.py:291-294)
   __syncthreads();
-  double* cpx = wk.comp_px + 2 * S.coff;
-  double* cX = wk.comp_X + 3 * S.coff;
-  double* cw = wk.comp_w + S.coff;
+  double2* cpk = wk.comp_pk + 3 * S.coff;
   int running = 0;
   for (int base = 0; base < n; base += kFinalThreads) {
     const int i = base + threadIdx.x;
@@ -555,19 +550,15 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(Work wk, Inputs in, Out
     int total;
     const int ex = block_excl_scan<kFinalThreads>(f, warp_tot, total);
     if (f) {
-      const int d = running + ex;
-      cpx[2 * d] = full.px[2 * i];
-      cpx[2 * d + 1] = full.px[2 * i + 1];
-      cX[3 * d] = full.X[3 * i];
-      cX[3 * d + 1] = full.X[3 * i + 1];
-      cX[3 * d + 2] = full.X[3 * i + 2];
-      cw[d] = full.w[i];
+      double P[3], u, v, w;
+      full.load(i, P, u, v, w);
+      pack_point(cpk, running + ex, P, u, v, w);
     }
     running += total;
   }
   __threadfence_block();
   __syncthreads();
-  const PointSet inl{cpx, cX, cw, running};
+  const PackedPts inl{cpk, running};
   lm_refine<kFinalThreads>(sm, inl, cin, best, kCauchy, p.cauchy, p.lm_max_iters, 1e-10, 1e-12, nullptr,
                            nullptr);
   const Pose fin = sm.cur;
@@ -583,7 +574,7 @@ int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const Ran
 }
 
 // ------------------------------------------------------------------ standalone msac / refine
-__global__ void __launch_bounds__(512) k_msac(Pose pose, PointSet ps, Intr in, double tau, double* red_out,
+__global__ void __launch_bounds__(512) k_msac(Pose pose, AosPts ps, Intr in, double tau, double* red_out,
                                               uint8_t* flags) {
   __shared__ LMShared<512> sm;
   set_eval_pose(sm, pose);
@@ -596,11 +587,11 @@ __global__ void __launch_bounds__(512) k_msac(Pose pose, PointSet ps, Intr in, d
 
 int launch_msac(const Pose& pose, const double* px, const double* X, const double* w, int n, Intr in,
                 double tau, double* red_out, uint8_t* flags, cudaStream_t st) {
-  k_msac<<<1, 512, 0, st>>>(pose, PointSet{px, X, w, n}, in, tau, red_out, flags);
+  k_msac<<<1, 512, 0, st>>>(pose, AosPts{px, X, w, n}, in, tau, red_out, flags);
   return 1;
 }
 
-__global__ void __launch_bounds__(512) k_refine(Pose start, PointSet ps, Intr in, int kind, double scale,
+__global__ void __launch_bounds__(512) k_refine(Pose start, AosPts ps, Intr in, int kind, double scale,
                                                 int max_iters, double gtol, double ctol, Pose* pose_out,
                                                 int* info_out, double* trace) {
   __shared__ LMShared<512> sm;
@@ -617,7 +608,7 @@ __global__ void __launch_bounds__(512) k_refine(Pose start, PointSet ps, Intr in
 int launch_refine(const Pose& start, const double* px, const double* X, const double* w, int n, Intr in,
                   int kind, double scale, int max_iters, double gtol, double ctol, Pose* pose_out,
                   int* info_out, double* trace, cudaStream_t st) {
-  k_refine<<<1, 512, 0, st>>>(start, PointSet{px, X, w, n}, in, kind, scale, max_iters, gtol, ctol,
+  k_refine<<<1, 512, 0, st>>>(start, AosPts{px, X, w, n}, in, kind, scale, max_iters, gtol, ctol,
                               pose_out, info_out, trace);
   return 1;
 }
