@@ -65,12 +65,65 @@ template <int NT>
 struct LMShared {
   double R[9], t[3];
   Pose cur, cand;
-  double red[kRed];
-  double scratch[(NT / 32) * kRed];
+  double red[kRed + 2];
+  double red2[kRed + 2];
+  double scratch[(NT / 32) * (kRed + 2)];
   double A[36], b[6];
   int flag;
   int ibuf[NT / 32];
+  long long cnt[16];
 };
+
+// ---------------------------------------------------------------- clusters
+// A query may be processed by a thread-block cluster (up to 8 CTAs on 8
+// SMs): every pass splits the points over the cluster, CTA partial sums are
+// combined through distributed shared memory in fixed rank order (so every
+// CTA holds bit-identical totals), and the LM control flow runs redundantly
+// in every CTA.  With a 1-CTA launch these are no-ops.
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_size() {
+  unsigned n;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+  return n;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double cl_load(const double* local_smem, unsigned rank) {
+  unsigned addr = (unsigned)__cvta_generic_to_shared(local_smem), raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(addr), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(raddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long cl_load_ll(const long long* local_smem, unsigned rank) {
+  unsigned addr = (unsigned)__cvta_generic_to_shared(local_smem), raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(addr), "r"(rank));
+  long long v;
+  asm volatile("ld.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(raddr) : "memory");
+  return v;
+}
+
+// sm.red[0..K) holds this CTA's block totals; replace them by the cluster
+// totals (sum over ranks 0..n-1 in order).  Call from all threads.
+template <int NT, int K>
+__device__ __forceinline__ void cluster_total(LMShared<NT>& sm) {
+  const unsigned n = cl_size();
+  if (n == 1) return;
+  cl_sync();
+  if (threadIdx.x < K) {
+    double s = 0.0;
+    for (unsigned r = 0; r < n; ++r) s += cl_load(&sm.red[threadIdx.x], r);
+    sm.red2[threadIdx.x] = s;
+  }
+  cl_sync();  // every rank has read every partial before anyone overwrites sm.red
+  if (threadIdx.x < K) sm.red[threadIdx.x] = sm.red2[threadIdx.x];
+  __syncthreads();
+}
 
 // Load rotation matrix + translation of `p` into shared memory (thread 0).
 template <int NT>
@@ -121,12 +174,13 @@ __device__ void msac_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, double
 #pragma unroll
   for (int k = 0; k < 3; ++k) t[k] = sm.t[k];
   double acc[2] = {0.0, 0.0};
-  int i = threadIdx.x;
+  const int step = NT * (int)cl_size();
+  int i = threadIdx.x + NT * (int)cl_rank();
   // two points per trip: both loads in flight before the arithmetic
-  for (; i + NT < ps.n; i += 2 * NT) {
+  for (; i + step < ps.n; i += 2 * step) {
     double P0[3], u0, v0, w0, P1[3], u1, v1, w1;
     ps.load(i, P0, u0, v0, w0);
-    ps.load(i + NT, P1, u1, v1, w1);
+    ps.load(i + step, P1, u1, v1, w1);
     const double e0 = msac_e2(R, t, in, P0, u0, v0);
     const double e1 = msac_e2(R, t, in, P1, u1, v1);
     acc[0] = acc[0] + dmul(w0, fmin(e0, t2));
@@ -134,7 +188,7 @@ __device__ void msac_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, double
     acc[1] += (e0 < t2 ? 1.0 : 0.0) + (e1 < t2 ? 1.0 : 0.0);
     if (flags) {
       flags[i] = e0 < t2 ? 1 : 0;
-      flags[i + NT] = e1 < t2 ? 1 : 0;
+      flags[i + step] = e1 < t2 ? 1 : 0;
     }
   }
   if (i < ps.n) {
@@ -146,6 +200,7 @@ __device__ void msac_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, double
     if (flags) flags[i] = e0 < t2 ? 1 : 0;
   }
   block_sum<NT, 2>(acc, sm.scratch, sm.red);
+  cluster_total<NT, 2>(sm);
 }
 
 // Cost / gradient / normal-matrix contribution of one point.
@@ -219,11 +274,12 @@ __device__ void lm_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, int kind
 #pragma unroll
   for (int k = 0; k < kRed; ++k) acc[k] = 0.0;
   double behind = 0.0;
-  int i = threadIdx.x;
-  for (; i + NT < ps.n; i += 2 * NT) {
+  const int step = NT * (int)cl_size();
+  int i = threadIdx.x + NT * (int)cl_rank();
+  for (; i + step < ps.n; i += 2 * step) {
     double P0[3], u0, v0, w0, P1[3], u1, v1, w1;
     ps.load(i, P0, u0, v0, w0);
-    ps.load(i + NT, P1, u1, v1, w1);
+    ps.load(i + step, P1, u1, v1, w1);
     lm_point<GRAD>(R, t, in, kind, s2, P0, u0, v0, w0, acc, behind);
     lm_point<GRAD>(R, t, in, kind, s2, P1, u1, v1, w1, acc, behind);
   }
@@ -232,15 +288,23 @@ __device__ void lm_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, int kind
     ps.load(i, P0, u0, v0, w0);
     lm_point<GRAD>(R, t, in, kind, s2, P0, u0, v0, w0, acc, behind);
   }
+  // slot kRed carries the behind-camera count (a deterministic OR)
   if (GRAD) {
-    block_sum<NT, kRed>(acc, sm.scratch, sm.red);
+    double a[kRed + 1];
+#pragma unroll
+    for (int k = 0; k < kRed; ++k) a[k] = acc[k];
+    a[kRed] = behind;
+    block_sum<NT, kRed + 1>(a, sm.scratch, sm.red);
+    cluster_total<NT, kRed + 1>(sm);
   } else {
-    double a1[1] = {acc[0]};
-    block_sum<NT, 1>(a1, sm.scratch, sm.red);
+    double a1[2] = {acc[0], behind};
+    block_sum<NT, 2>(a1, sm.scratch, sm.red);
+    cluster_total<NT, 2>(sm);
+    if (threadIdx.x == 0) sm.red[kRed] = sm.red[1];
+    __syncthreads();
   }
-  // any-behind flag (deterministic OR)
-  const int anyb = __syncthreads_or(behind != 0.0);
-  if (kind == kCauchy && anyb) {
+  if (kind == kCauchy && sm.red[kRed] != 0.0) {
+    __syncthreads();
     if (threadIdx.x == 0) sm.red[0] = CUDART_INF;
   }
   __syncthreads();

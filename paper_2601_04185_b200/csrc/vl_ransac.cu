@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams 
   extern __shared__ float costs[];
   __shared__ LMShared<kScanThreads> sm;
   __shared__ Pose s_start;
-  const int q = wk.active_list[blockIdx.x];
+  const int q = wk.active_list[blockIdx.x / cl_size()];
   QState& S = wk.qs[q];
   const int nh = S.nh, NS = S.nsplit;
   const float* part = wk.partial + (int64_t)q * wk.NSPLIT * wk.HCAP;
@@ -431,7 +431,8 @@ __global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams 
   }
   if (S.iters >= p.max_iterations) active = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (cl_size() > 1) cl_sync();  // every CTA of the cluster has read S
+  if (threadIdx.x == 0 && cl_rank() == 0) {
     S.best_cost = best_cost;
     S.has_best = has_best;
     S.best = best;
@@ -462,6 +463,33 @@ __global__ void __launch_bounds__(1024) k_active(Work wk, int nactive) {
 
 int launch_score(const Work& wk, float tau2, int num_sms, cudaStream_t st);  // vl_score.cu
 
+// Cluster size for a per-query kernel: spread few queries over up to 8 SMs
+// each (single-query latency), keep one CTA per query when the batch alone
+// fills the GPU (`slots` = resident CTAs the GPU holds).
+static int pick_cluster(int nq, int slots) {
+  int cs = 1;
+  while (cs < 8 && (int64_t)nq * cs * 2 <= slots) cs *= 2;
+  return cs;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_clustered(void (*k)(KArgs...), int nq, int block, size_t smem, int cs, cudaStream_t st,
+                             Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nq * cs, 1, 1);
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // One round, kernel by kernel; `hook(stage, begin)` lets the caller bracket
 // each launch with CUDA events (profiling) without touching the kernels.
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
@@ -484,7 +512,7 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   H(kStageScore, false);
   H(kStageScan, true);
   const size_t smem = (size_t)wk.HCAP * sizeof(float);
-  k_scan<<<nactive, kScanThreads, smem, st>>>(wk, p);
+  launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, 2 * num_sms), st, wk, p);
   H(kStageScan, false);
   H(kStageActive, true);
   k_active<<<1, 1024, 0, st>>>(wk, nactive);
@@ -499,7 +527,8 @@ __global__ void __launch_bounds__(kFinalThreads, 2) k_final(Work wk, Inputs in, 
                                                          int q_base) {
   __shared__ LMShared<kFinalThreads> sm;
   __shared__ int warp_tot[32];
-  const int q = blockIdx.x;
+  const unsigned cr = cl_rank(), cs = cl_size();
+  const int q = blockIdx.x / cs;
   const QState& S = wk.qs[q];
   const int64_t gq = q_base + q;
   const int n = S.n;
@@ -507,7 +536,7 @@ __global__ void __launch_bounds__(kFinalThreads, 2) k_final(Work wk, Inputs in, 
   const AosPts full{in.px + 2 * S.off, in.X + 3 * S.off, in.w + S.off, n};
   const Intr cin = S.in;
   auto write_small = [&](const Pose& ps, int64_t cnt, double score, int conv) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && cr == 0) {
       for (int i = 0; i < 4; ++i) out.q[4 * gq + i] = ps.q[i];
       for (int i = 0; i < 3; ++i) out.t[3 * gq + i] = ps.t[i];
       out.inlier_count[gq] = cnt;
@@ -523,7 +552,7 @@ __global__ void __launch_bounds__(kFinalThreads, 2) k_final(Work wk, Inputs in, 
     }
   };
   if (!S.has_best) {
-    for (int i = threadIdx.x; i < n; i += kFinalThreads) flags[i] = 0;
+    for (int i = threadIdx.x + kFinalThreads * cr; i < n; i += kFinalThreads * cs) flags[i] = 0;
     Pose id;
     id.q[0] = 1;
     id.q[1] = id.q[2] = id.q[3] = 0;
@@ -533,20 +562,34 @@ __global__ void __launch_bounds__(kFinalThreads, 2) k_final(Work wk, Inputs in, 
   }
   const Pose best = S.best;
   set_eval_pose(sm, best);
-  msac_pass<kFinalThreads>(sm, full, cin, p.tau, flags);
+  msac_pass<kFinalThreads>(sm, full, cin, p.tau, flags);  // cluster-wide; flags visible after its cluster barrier
   const double cost_full = sm.red[0];
   const int64_t cnt_full = (int64_t)sm.red[1];
   if (cnt_full < 3) {
     write_small(best, cnt_full, cost_full, 0);
     return;
   }
-  // ordered compaction of the full-set inliers (X[flags_full], posest.py:291-294)
+  // ordered compaction of the full-set inliers (X[flags_full], posest.py:291-294):
+  // CTA r of the cluster owns the contiguous range [lo, hi) of the point list
   __syncthreads();
+  const int lo = (int)((int64_t)n * cr / cs), hi = (int)((int64_t)n * (cr + 1) / cs);
+  int mine = 0;
+  for (int i = lo + threadIdx.x; i < hi; i += kFinalThreads) mine += flags[i] ? 1 : 0;
+  {
+    double c[1] = {(double)mine};
+    block_sum<kFinalThreads, 1>(c, sm.scratch, sm.red2);
+  }
+  if (threadIdx.x == 0) sm.cnt[0] = (long long)sm.red2[0];
+  int start = 0;
+  if (cs > 1) {
+    cl_sync();
+    for (unsigned r = 0; r < cr; ++r) start += (int)cl_load_ll(&sm.cnt[0], r);
+  }
   double2* cpk = wk.comp_pk + 3 * S.coff;
-  int running = 0;
-  for (int base = 0; base < n; base += kFinalThreads) {
+  int running = start;
+  for (int base = lo; base < hi; base += kFinalThreads) {
     const int i = base + threadIdx.x;
-    const int f = (i < n && flags[i]) ? 1 : 0;
+    const int f = (i < hi && flags[i]) ? 1 : 0;
     int total;
     const int ex = block_excl_scan<kFinalThreads>(f, warp_tot, total);
     if (f) {
@@ -556,9 +599,10 @@ __global__ void __launch_bounds__(kFinalThreads, 2) k_final(Work wk, Inputs in, 
     }
     running += total;
   }
-  __threadfence_block();
+  __threadfence();
   __syncthreads();
-  const PackedPts inl{cpk, running};
+  if (cs > 1) cl_sync();  // compacted points of every CTA visible cluster-wide
+  const PackedPts inl{cpk, (int)cnt_full};
   lm_refine<kFinalThreads>(sm, inl, cin, best, kCauchy, p.cauchy, p.lm_max_iters, 1e-10, 1e-12, nullptr,
                            nullptr);
   const Pose fin = sm.cur;
@@ -569,7 +613,7 @@ __global__ void __launch_bounds__(kFinalThreads, 2) k_final(Work wk, Inputs in, 
 
 int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
                  int q_base, cudaStream_t st) {
-  k_final<<<Q, kFinalThreads, 0, st>>>(wk, in, out, p, q_base);
+  launch_clustered(k_final, Q, kFinalThreads, 0, pick_cluster(Q, 2 * 148), st, wk, in, out, p, q_base);
   return 1;
 }
 
