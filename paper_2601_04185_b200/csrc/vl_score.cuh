@@ -81,13 +81,22 @@ __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __ffma2_rn(a, b, make_float2(-0.f, -0.f)); }
 
+__device__ __forceinline__ float rcp_approx_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// r = 1 / max(z, 0): +inf for z <= 0 (behind camera / on the camera plane),
+// so e2 becomes inf or NaN and fminf (IEEE minNum) maps it to tau^2.  The
+// clamp runs on the ALU pipe, the reciprocal on the MUFU pipe: the FMA pipe
+// only sees the 14 FFMA2/FMUL2 of the evaluation pair.
 #define VL_SCORE_EVAL2(Pp, accp)                                                                  \
   {                                                                                               \
     const float2 x_ = fma2(Pp[0], f2(a.x), fma2(Pp[1], f2(a.y), fma2(Pp[2], f2(a.z), Pp[3])));    \
     const float2 y_ = fma2(Pp[4], f2(a.x), fma2(Pp[5], f2(a.y), fma2(Pp[6], f2(a.z), Pp[7])));    \
     const float2 z_ = fma2(Pp[8], f2(a.x), fma2(Pp[9], f2(a.y), fma2(Pp[10], f2(a.z), Pp[11])));  \
-    const float2 rs_ = make_float2(rsqrt_approx_ftz(z_.x), rsqrt_approx_ftz(z_.y));              \
-    const float2 r_ = mul2(rs_, rs_);                                                             \
+    const float2 r_ = make_float2(rcp_approx_ftz(fmaxf(z_.x, 0.f)), rcp_approx_ftz(fmaxf(z_.y, 0.f))); \
     const float2 du_ = fma2(x_, r_, f2(a.w));                                                     \
     const float2 dv_ = fma2(y_, r_, f2(b.x));                                                     \
     float2 e2_ = fma2(du_, du_, mul2(dv_, dv_));                                                  \
