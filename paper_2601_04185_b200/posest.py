@@ -213,25 +213,83 @@ def _estimates_from(out, offsets) -> list[PoseEstimate]:
     return res
 
 
-def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig):
+def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chunk_queries: int = 256):
     """Batched estimator on HOST buffers: H2D copy, device run, D2H of the results.
 
     ``px``/``X``/``w`` are packed host arrays (numpy, or pinned torch CPU
-    tensors for full-bandwidth copies).  Returns a dict of numpy arrays
-    (q, t, flags, count, score, iterations, converged, stats) and the byte
-    counts moved each way.
+    tensors for full-bandwidth copies).  Queries are processed in chunks on
+    the caller's stream while a second stream copies the next chunk's
+    matches to HBM and the previous chunk's results back (double-buffered,
+    event-ordered), so PCIe traffic overlaps estimation.  Returns a dict of
+    numpy arrays (q, t, flags, count, score, iterations, converged, stats) and
+    the byte counts moved each way.
     """
     import torch
     _lib.context()
-    tens = []
+    offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    Q = offsets.shape[0] - 1
+    N = int(offsets[-1])
+    host_in = []
     for a in (px, X, w):
         t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
-        tens.append(t.to("cuda", non_blocking=True))
-    out = ransac_pnp_device(tens[0], tens[1], tens[2], offsets, intrinsics, seeds, cfg)
-    host = {k: v.cpu().numpy() for k, v in out.items()}
-    h2d = sum(int(t.numel() * t.element_size()) for t in tens)
-    d2h = sum(int(v.nbytes) for v in host.values())
-    return host, h2d, d2h
+        if not t.is_pinned():
+            t = t.pin_memory()
+        host_in.append(t)
+    intrinsics = list(intrinsics)
+    seeds = list(seeds)
+    comp = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    chunks = [(q0, min(Q, q0 + chunk_queries)) for q0 in range(0, Q, chunk_queries)]
+    max_rows = max(int(offsets[b] - offsets[a]) for a, b in chunks)
+    bufs = [[torch.empty((max_rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in host_in]
+            for _ in range(min(2, len(chunks)))]
+    out = {
+        "q": torch.empty((Q, 4), dtype=torch.float64, device=dev),
+        "t": torch.empty((Q, 3), dtype=torch.float64, device=dev),
+        "flags": torch.empty((max(N, 1),), dtype=torch.uint8, device=dev),
+        "count": torch.empty((Q,), dtype=torch.int64, device=dev),
+        "score": torch.empty((Q,), dtype=torch.float64, device=dev),
+        "iterations": torch.empty((Q,), dtype=torch.int64, device=dev),
+        "converged": torch.empty((Q,), dtype=torch.int32, device=dev),
+        "stats": torch.empty((Q, 4), dtype=torch.int64, device=dev),
+    }
+    host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()}
+    ev_in = [torch.cuda.Event() for _ in chunks]
+    ev_done = [torch.cuda.Event() for _ in chunks]
+
+    def h2d(k):
+        a, b = chunks[k]
+        r0, r1 = int(offsets[a]), int(offsets[b])
+        with torch.cuda.stream(copy):
+            if k >= 2:
+                copy.wait_event(ev_done[k - 2])  # buffer k%2 was read by chunk k-2
+            for dst, src in zip(bufs[k % 2], host_in):
+                dst[: r1 - r0].copy_(src[r0:r1], non_blocking=True)
+            ev_in[k].record(copy)
+
+    h2d(0)
+    for k, (a, b) in enumerate(chunks):
+        r0, r1 = int(offsets[a]), int(offsets[b])
+        if k + 1 < len(chunks):
+            h2d(k + 1)
+        comp.wait_event(ev_in[k])
+        view = {key: (v[a:b] if key != "flags" else v[r0:r1]) for key, v in out.items()}
+        d = [buf[: r1 - r0] for buf in bufs[k % 2]]
+        ransac_pnp_device(d[0], d[1], d[2], offsets[a:b + 1] - offsets[a], intrinsics[a:b], seeds[a:b], cfg,
+                          out=view)
+        ev_done[k].record(comp)
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev_done[k])
+            for key, v in view.items():
+                dst = host_out[key][a:b] if key != "flags" else host_out[key][r0:r1]
+                dst.copy_(v, non_blocking=True)
+    copy.synchronize()
+    comp.wait_stream(copy)
+    host = {k: v.numpy()[:N] if k == "flags" else v.numpy() for k, v in host_out.items()}
+    h2d_bytes = sum(int(t.numel() * t.element_size()) for t in host_in)
+    d2h_bytes = sum(int(v.nbytes) for v in host.values())
+    return host, h2d_bytes, d2h_bytes
 
 
 def ransac_pnp_batch(queries, intrinsics, cfg: RansacConfig, seeds=None) -> list[PoseEstimate]:

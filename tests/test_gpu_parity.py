@@ -194,3 +194,23 @@ def test_batch_equals_single_and_oracle(vl, intr):
         assert res[i].iterations == o.iterations
         _check_pose(res[i].pose.q, res[i].pose.t, o.q, o.t)
         _check_mask(res[i].inlier_flags, o.inlier_flags, o.q, o.t, pxs[i], Xs[i])
+
+
+def test_host_api_chunked_pipeline_equals_device(vl):
+    """ransac_pnp_host (double-buffered H2D/D2H on a copy stream) == one device call."""
+    import torch
+    from paper_2601_04185_b200.posest import ransac_pnp_device, ransac_pnp_host
+    pxs, Xs, ws = batch_a(7, 1200, 0.5, 1.0, seed0=90)
+    offsets = np.concatenate([[0], np.cumsum([p.shape[0] for p in pxs])]).astype(np.int64)
+    px, X, w = np.concatenate(pxs), np.concatenate(Xs), np.concatenate(ws)
+    intr = [vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)] * 7
+    seeds = [3 * i + 2 for i in range(7)]
+    cfg = vl.RansacConfig(max_iterations=3000, miss_probability=1e-300)
+    ref = ransac_pnp_device(torch.from_numpy(px).cuda(), torch.from_numpy(X).cuda(), torch.from_numpy(w).cuda(),
+                            offsets, intr, seeds, cfg)
+    ref = {k: v.cpu().numpy() for k, v in ref.items()}
+    for chunk in (1, 3, 7):
+        host, h2d, d2h = ransac_pnp_host(px, X, w, offsets, intr, seeds, cfg, chunk_queries=chunk)
+        assert h2d == px.nbytes + X.nbytes + w.nbytes
+        for k in ("q", "t", "flags", "count", "score", "iterations", "converged", "stats"):
+            assert np.array_equal(host[k], ref[k]), (chunk, k)
