@@ -494,10 +494,20 @@ def main():
     score_ms, score_launches = prof["score"]
     achieved = (evals_per_step * args.steps * FLOP_PER_EVAL) / (score_ms / 1000.0) / 1e12 if score_ms else None
     stage_ms = {k: round(v[0] / args.steps, 3) for k, v in prof.items()}
+    traffic = None
+    try:  # DRAM bytes per k_score launch from the committed ncu --set full capture (profiles/)
+        tr = json.loads((ROOT / "profiles" / "traffic.json").read_text())["k_score"]
+        if tr.get("workload") == args.workload and Q == 1000:
+            traffic = {"dram_bytes_per_launch": tr["dram_bytes_per_launch"], "source": tr["source"],
+                       "algorithmic_bytes_per_launch": int(evals_per_step / score_launches * args.steps
+                                                           / 10_000 * (48 + 4 * 20)) +
+                       (Q * 10_000 * 32 if score_launches else 0)}
+    except Exception:
+        traffic = None
     roof = {"bound": "fp32", "kernel": "k_score", "achieved": achieved, "peak": round(fp32_peak, 2),
             "unit": "TFLOP/s", "frac": (achieved / fp32_peak) if achieved else None,
             "peak_source": "derived SMs*128*2*sm_max_mhz (MEASURED_PEAKS.json has no FP32 entry)",
-            "flop_per_eval": FLOP_PER_EVAL, "traffic": None,
+            "flop_per_eval": FLOP_PER_EVAL, "traffic": traffic,
             "evals_per_s_kernel": (evals_per_step * args.steps) / (score_ms / 1000.0) if score_ms else None,
             "score_share_of_step": (score_ms / ms) if ms else None,
             "score_launches": score_launches}

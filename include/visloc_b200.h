@@ -126,6 +126,17 @@ int vl_refine_pose(vl_ctx* ctx, double* q_io, double* t_io, const double* px, co
                    int32_t max_iters, double gradient_tol, double cost_tol, int32_t* converged,
                    int32_t* iterations, double* trace, int32_t* trace_len, void* stream);
 
+/* replaces visloc.refine.robust_cost (refine.py:135-149): pose q/t HOST,
+ * arrays DEVICE, *cost_out HOST (inf for Cauchy with a point behind). */
+int vl_robust_cost(vl_ctx* ctx, const double* q, const double* t, const double* px, const double* X,
+                   const double* w, int64_t n, vl_intrinsics intr, int32_t loss, double scale,
+                   double* cost_out, void* stream);
+
+/* replaces visloc.refine.pose_residuals + pose_jacobian (refine.py:90-132):
+ * res DEVICE [n,2], z DEVICE [n], J DEVICE [n,2,6] (each may be NULL). */
+int vl_pose_residuals(vl_ctx* ctx, const double* q, const double* t, const double* px, const double* X,
+                      int64_t n, vl_intrinsics intr, double* res, double* z, double* J, void* stream);
+
 /* replaces visloc.p3p.p3p_solve_batch (p3p.py:57).  bearings/points DEVICE
  * [B,3,3]; outputs DEVICE R [4B,3,3], t [4B,3], sample [4B]; *m_out HOST. */
 int vl_p3p_solve_batch(vl_ctx* ctx, const double* bearings, const double* points, int32_t B,

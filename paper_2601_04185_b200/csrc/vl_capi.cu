@@ -596,3 +596,32 @@ extern "C" int vl_decode_depth(vl_ctx* c, const vl_lift_depth* depth, float* val
   c->launches += launch_decode(D, (int64_t)D.w * D.h, vals, valid, (cudaStream_t)stream);
   return check_launch(c);
 }
+
+extern "C" int vl_robust_cost(vl_ctx* c, const double* q, const double* t, const double* px, const double* X,
+                              const double* w, int64_t n, vl_intrinsics intr, int32_t loss, double scale,
+                              double* cost_out, void* stream) {
+  if (!c || !q || !t || !cost_out || n < 0 || n > 0x7FFFFFFF || (loss != 0 && loss != 1))
+    return fail(c, VL_ERR_INVALID, "bad argument");
+  if (!(scale > 0)) return fail(c, VL_ERR_INVALID, "scale must be positive");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if ((rc = ensure(c, c->scratch, 4096)) || (rc = ensure_host(c, 4096))) return rc;
+  c->launches += launch_robust_cost(pose_from_host(q, t), px, X, w, (int)n,
+                                    Intr{intr.fx, intr.fy, intr.cx, intr.cy}, loss, scale, (double*)c->scratch.p, st);
+  if ((rc = check_launch(c))) return rc;
+  double* h = (double*)c->h_pinned;
+  VL_CUDA(c, cudaMemcpyAsync(h, c->scratch.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  VL_CUDA(c, cudaStreamSynchronize(st));
+  *cost_out = h[0];
+  return VL_OK;
+}
+
+extern "C" int vl_pose_residuals(vl_ctx* c, const double* q, const double* t, const double* px, const double* X,
+                                 int64_t n, vl_intrinsics intr, double* res, double* z, double* J, void* stream) {
+  if (!c || !q || !t || n < 0 || n > 0x7FFFFFFF) return fail(c, VL_ERR_INVALID, "bad argument");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  c->launches += launch_residuals(pose_from_host(q, t), px, X, (int)n, Intr{intr.fx, intr.fy, intr.cx, intr.cy},
+                                  res, z, J, (cudaStream_t)stream);
+  return check_launch(c);
+}

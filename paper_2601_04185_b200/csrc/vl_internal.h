@@ -96,6 +96,10 @@ int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const Ran
 
 int launch_msac(const Pose& pose, const double* px, const double* X, const double* w, int n, Intr in,
                 double tau, double* red_out, uint8_t* flags, cudaStream_t st);
+int launch_robust_cost(const Pose& pose, const double* px, const double* X, const double* w, int n, Intr in,
+                       int kind, double scale, double* out, cudaStream_t st);
+int launch_residuals(const Pose& pose, const double* px, const double* X, int n, Intr in, double* res, double* z,
+                     double* J, cudaStream_t st);
 int launch_refine(const Pose& start, const double* px, const double* X, const double* w, int n, Intr in,
                   int kind, double scale, int max_iters, double gtol, double ctol, Pose* pose_out,
                   int* info_out, double* trace, cudaStream_t st);

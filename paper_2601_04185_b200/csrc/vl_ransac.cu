@@ -657,4 +657,67 @@ int launch_refine(const Pose& start, const double* px, const double* X, const do
   return 1;
 }
 
+// robust_cost (refine.py:135-149): one fused cost pass.
+__global__ void __launch_bounds__(512) k_robust_cost(Pose pose, AosPts ps, Intr in, int kind, double scale,
+                                                     double* out) {
+  __shared__ LMShared<512> sm;
+  set_eval_pose(sm, pose);
+  lm_pass<512, false>(sm, ps, in, kind, scale);
+  if (threadIdx.x == 0) out[0] = sm.red[0];
+}
+
+int launch_robust_cost(const Pose& pose, const double* px, const double* X, const double* w, int n, Intr in,
+                       int kind, double scale, double* out, cudaStream_t st) {
+  k_robust_cost<<<1, 512, 0, st>>>(pose, AosPts{px, X, w, n}, in, kind, scale, out);
+  return 1;
+}
+
+// pose_residuals + pose_jacobian (refine.py:90-132): per-point residual,
+// camera z and the analytic 2x6 Jacobian (rows zeroed at/behind the camera).
+__global__ void k_residuals(Pose pose, const double* px, const double* X, int n, Intr in, double* res,
+                            double* z_out, double* J) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double R[9];
+  q2R(pose.q, R);
+  const double P[3] = {X[3 * i], X[3 * i + 1], X[3 * i + 2]};
+  double x, y, z;
+  cam_point(R, pose.t, P, x, y, z);
+  const double u = dadd(__ddiv_rn(dmul(in.fx, x), z), in.cx);
+  const double v = dadd(__ddiv_rn(dmul(in.fy, y), z), in.cy);
+  if (res) {
+    res[2 * i] = dsub(u, px[2 * i]);
+    res[2 * i + 1] = dsub(v, px[2 * i + 1]);
+  }
+  if (z_out) z_out[i] = z;
+  if (J) {
+    double* Ji = J + 12 * (int64_t)i;
+    if (!(z > 0)) {
+      for (int k = 0; k < 12; ++k) Ji[k] = 0.0;
+      return;
+    }
+    const double p00 = in.fx / z, p02 = -in.fx * x / (z * z);
+    const double p11 = in.fy / z, p12 = -in.fy * y / (z * z);
+    Ji[0] = p02 * y;
+    Ji[1] = p00 * z + p02 * (-x);
+    Ji[2] = p00 * (-y);
+    Ji[3] = p00;
+    Ji[4] = 0.0;
+    Ji[5] = p02;
+    Ji[6] = p11 * (-z) + p12 * y;
+    Ji[7] = p12 * (-x);
+    Ji[8] = p11 * x;
+    Ji[9] = 0.0;
+    Ji[10] = p11;
+    Ji[11] = p12;
+  }
+}
+
+int launch_residuals(const Pose& pose, const double* px, const double* X, int n, Intr in, double* res, double* z,
+                     double* J, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_residuals<<<(n + 255) / 256, 256, 0, st>>>(pose, px, X, n, in, res, z, J);
+  return 1;
+}
+
 }  // namespace vl

@@ -18,7 +18,8 @@ import numpy as np
 from . import _lib
 from .geometry import CameraIntrinsics, Pose, quat_multiply, rotvec_to_quat
 
-__all__ = ["CauchyLoss", "RefineResult", "TruncatedLoss", "apply_delta", "refine_pose"]
+__all__ = ["CauchyLoss", "RefineResult", "TruncatedLoss", "apply_delta", "pose_jacobian", "pose_residuals",
+           "refine_pose", "robust_cost"]
 
 
 @dataclass(frozen=True)
@@ -67,6 +68,75 @@ def apply_delta(pose: Pose, delta) -> Pose:
     return Pose(q, Pose(dq, np.zeros(3)).R @ pose.t + nu)
 
 
+def _loss_kind(loss):
+    if isinstance(loss, TruncatedLoss):
+        return 0, float(loss.tau)
+    if isinstance(loss, CauchyLoss):
+        return 1, float(loss.scale)
+    # duck-typed reference losses
+    if hasattr(loss, "tau"):
+        return 0, float(loss.tau)
+    if hasattr(loss, "scale"):
+        return 1, float(loss.scale)
+    raise TypeError(f"unsupported loss {type(loss).__name__}")
+
+
+def _pose_ptrs(pose):
+    q = np.ascontiguousarray(pose.q, dtype=np.float64)
+    t = np.ascontiguousarray(pose.t, dtype=np.float64)
+    dp = C.POINTER(C.c_double)
+    return q, t, q.ctypes.data_as(dp), t.ctypes.data_as(dp)
+
+
+def robust_cost(pose: Pose, points, pixels, weights, loss, intr: CameraIntrinsics) -> float:
+    """Weighted robust cost (refine.py:135-149), one fused GPU pass."""
+    from .posest import _intr_c, _to_device
+    X = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
+    px = np.ascontiguousarray(np.asarray(pixels, dtype=np.float64).reshape(-1, 2))
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64).reshape(-1))
+    kind, scale = _loss_kind(loss)
+    ctx = _lib.context()
+    dX, dpx, dw = _to_device(X), _to_device(px), _to_device(w)
+    q, t, qp, tp = _pose_ptrs(pose)
+    out = C.c_double()
+    rc = _lib.lib().vl_robust_cost(ctx.handle, qp, tp, dpx.data_ptr(), dX.data_ptr(), dw.data_ptr(), X.shape[0],
+                                   _intr_c(intr), kind, scale, C.byref(out), _lib.stream_ptr())
+    ctx.check(rc, "vl_robust_cost")
+    return float(out.value)
+
+
+def _residuals_gpu(pose, points, pixels, intr, want_res, want_J):
+    import torch
+    from .posest import _intr_c, _to_device
+    X = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
+    n = X.shape[0]
+    px = np.ascontiguousarray(np.asarray(pixels, dtype=np.float64).reshape(-1, 2)) if pixels is not None \
+        else np.zeros((n, 2))
+    ctx = _lib.context()
+    dX, dpx = _to_device(X), _to_device(px)
+    res = torch.empty((max(n, 1), 2), dtype=torch.float64, device="cuda")
+    z = torch.empty((max(n, 1),), dtype=torch.float64, device="cuda")
+    J = torch.empty((max(n, 1), 2, 6), dtype=torch.float64, device="cuda") if want_J else None
+    q, t, qp, tp = _pose_ptrs(pose)
+    rc = _lib.lib().vl_pose_residuals(ctx.handle, qp, tp, dpx.data_ptr(), dX.data_ptr(), n, _intr_c(intr),
+                                      res.data_ptr(), z.data_ptr(), J.data_ptr() if J is not None else None,
+                                      _lib.stream_ptr())
+    ctx.check(rc, "vl_pose_residuals")
+    return res[:n].cpu().numpy(), z[:n].cpu().numpy(), (J[:n].cpu().numpy() if J is not None else None)
+
+
+def pose_residuals(pose: Pose, points, pixels, intr: CameraIntrinsics):
+    """Reprojection residuals (N,2) and camera-frame z (N,) (refine.py:90-100)."""
+    r, z, _ = _residuals_gpu(pose, points, pixels, intr, True, False)
+    return r, z
+
+
+def pose_jacobian(pose: Pose, points, intr: CameraIntrinsics) -> np.ndarray:
+    """Analytic residual Jacobian (N,2,6) at delta = 0, rows zeroed at/behind the camera (refine.py:103-132)."""
+    _, _, J = _residuals_gpu(pose, points, None, intr, False, True)
+    return J
+
+
 @dataclass
 class RefineResult:
     pose: Pose
@@ -89,12 +159,7 @@ def refine_pose(initial: Pose, points, pixels, weights, loss, intr: CameraIntrin
     w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64).reshape(-1))
     if X.shape[0] < 3:
         raise ValueError(f"refinement needs >= 3 matches, got {X.shape[0]}")
-    if isinstance(loss, TruncatedLoss):
-        kind, scale = 0, float(loss.tau)
-    elif isinstance(loss, CauchyLoss):
-        kind, scale = 1, float(loss.scale)
-    else:
-        raise TypeError(f"unsupported loss {type(loss).__name__}")
+    kind, scale = _loss_kind(loss)
     ctx = _lib.context()
     dX, dpx, dw = _to_device(X), _to_device(px), _to_device(w)
     q = np.ascontiguousarray(initial.q, dtype=np.float64).copy()
