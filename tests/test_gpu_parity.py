@@ -214,3 +214,34 @@ def test_host_api_chunked_pipeline_equals_device(vl):
         assert h2d == px.nbytes + X.nbytes + w.nbytes
         for k in ("q", "t", "flags", "count", "score", "iterations", "converged", "stats"):
             assert np.array_equal(host[k], ref[k]), (chunk, k)
+
+
+def test_randomized_parity_sweep(vl, intr):
+    """40 seeded problems across inlier ratio / noise / size / config regimes:
+    GPU ransac_pnp vs the CPU oracle (itself bit-identical to the reference)."""
+    rng = np.random.default_rng(2024)
+    cases = []
+    for k in range(40):
+        n = int(rng.choice([50, 300, 1500, 4000, 12000]))
+        of = float(rng.choice([0.0, 0.3, 0.5, 0.7, 0.85]))
+        sg = float(rng.choice([0.0, 0.5, 1.0, 3.0]))
+        mi = int(rng.choice([1000, 3000, 100_000]))
+        eta = float(rng.choice([1e-4, 1e-300]))
+        cases.append((n, of, sg, 500 + k, 17 * k + 3, mi, eta))
+    exact_pose = exact_mask = 0
+    for n, of, sg, ds, rs, mi, eta in cases:
+        if eta == 1e-300 and mi == 100_000:
+            mi = 5000
+        px, X, w, _ = matches_a(n, of, sg, seed=ds)
+        cfg = vl.RansacConfig(seed=rs, max_iterations=mi, miss_probability=eta)
+        e = vl.ransac_pnp((px, X, w), intr, cfg)
+        o = ransac(px, X, w, INTR_T, Config(seed=rs, max_iterations=mi, miss_probability=eta))
+        assert e.iterations == o.iterations, (n, of, sg, ds, rs)
+        assert e.converged == o.converged
+        if not o.converged:
+            continue
+        _check_pose(e.pose.q, e.pose.t, o.q, o.t)
+        _check_mask(e.inlier_flags, o.inlier_flags, o.q, o.t, px, X)
+        exact_pose += int(og.rot_err_deg(e.pose.q, o.q) < 1e-7)
+        exact_mask += int(np.array_equal(e.inlier_flags, o.inlier_flags))
+    print(f"sweep: {exact_pose}/40 poses within 1e-7 deg, {exact_mask}/40 masks identical")
