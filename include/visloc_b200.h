@@ -112,6 +112,23 @@ int vl_pcg64_seed(uint64_t seed, vl_pcg64_state* out);
 /* replaces visloc.posest.ransac_pnp (posest.py:223) — batched over queries */
 int vl_ransac_pnp(vl_ctx* ctx, const vl_ransac_args* args, const vl_ransac_out* out, void* stream);
 
+/* Stepwise driver of the same estimator, for the optional single-query
+ * hypothesis-split mode across GPUs.  Every rank calls
+ * vl_ransac_begin with identical args and its (split_rank, split_size):
+ * samples, P3P and scans are replicated, the scoring work items are dealt
+ * round-robin and non-owned items contribute zeros.  Per round:
+ *   vl_ransac_step_score(ctx, buf)      -> this rank's partial costs into buf (DEVICE)
+ *   SUM all-reduce of buf across ranks  (NCCL over NVLink; exact: one non-zero term)
+ *   vl_ransac_step_finish(ctx, buf, &n) -> ordered scan / LO / stop; n active queries
+ * until n == 0, then vl_ransac_end(ctx, out).  Results are bit-identical on
+ * every rank and to vl_ransac_pnp.  One workspace chunk of queries. */
+int vl_ransac_begin(vl_ctx* ctx, const vl_ransac_args* args, int32_t split_rank, int32_t split_size,
+                    void* stream);
+int vl_ransac_partial_bytes(vl_ctx* ctx, int64_t* bytes);
+int vl_ransac_step_score(vl_ctx* ctx, void* partial_out, void* stream);
+int vl_ransac_step_finish(vl_ctx* ctx, const void* partial_in, int32_t* nactive, void* stream);
+int vl_ransac_end(vl_ctx* ctx, const vl_ransac_out* out, void* stream);
+
 /* replaces visloc.posest.msac_score (posest.py:160).  pose q[4], t[3] HOST;
  * arrays DEVICE; cost -> *cost_out (HOST), flags -> DEVICE (may be NULL). */
 int vl_msac_score(vl_ctx* ctx, const double* q, const double* t, const double* px,

@@ -111,6 +111,14 @@ def lib():
         L.vl_decode_depth.argtypes = [vp, C.POINTER(LiftDepth), vp, vp, vp]
         L.vl_robust_cost.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, i32, dbl, dp, vp]
         L.vl_pose_residuals.argtypes = [vp, dp, dp, vp, vp, i64, Intrinsics, vp, vp, vp, vp]
+        L.vl_ransac_begin.argtypes = [vp, C.POINTER(RansacArgs), i32, i32, vp]
+        L.vl_ransac_partial_bytes.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.vl_ransac_step_score.argtypes = [vp, vp, vp]
+        L.vl_ransac_step_finish.argtypes = [vp, vp, C.POINTER(C.c_int32), vp]
+        L.vl_ransac_end.argtypes = [vp, C.POINTER(RansacOut), vp]
+        for name in ("vl_ransac_begin", "vl_ransac_partial_bytes", "vl_ransac_step_score",
+                     "vl_ransac_step_finish", "vl_ransac_end"):
+            getattr(L, name).restype = C.c_int
         L.vl_robust_cost.restype = C.c_int
         L.vl_pose_residuals.restype = C.c_int
         for name in ("vl_create", "vl_destroy", "vl_reserve", "vl_pcg64_seed", "vl_ransac_pnp", "vl_profile",
@@ -125,7 +133,8 @@ EXPORTED_SYMBOLS = (
     "vl_create", "vl_destroy", "vl_last_error", "vl_reserve", "vl_launch_count", "vl_pcg64_seed",
     "vl_ransac_pnp", "vl_msac_score", "vl_refine_pose", "vl_p3p_solve_batch",
     "vl_sample_minimal_sets", "vl_profile", "vl_profile_read", "vl_lift", "vl_interp_depth",
-    "vl_decode_depth", "vl_robust_cost", "vl_pose_residuals",
+    "vl_decode_depth", "vl_robust_cost", "vl_pose_residuals", "vl_ransac_begin", "vl_ransac_partial_bytes",
+    "vl_ransac_step_score", "vl_ransac_step_finish", "vl_ransac_end",
 )
 
 STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final", "lift")

@@ -37,6 +37,14 @@ struct vl_ctx {
   double stage_ms[kNumStages] = {0};
   int64_t stage_launches[kNumStages] = {0};
   cudaStream_t prof_stream = nullptr;
+  // stepwise driver state (vl_ransac_begin / step_score / step_finish / end)
+  struct {
+    Work wk;
+    Inputs in;
+    RansacParams p;
+    int Q = 0, nactive = 0, open = 0;
+    int64_t rounds = 0, max_rounds = 0;
+  } step;
 };
 
 static void prof_hook(void* arg, int stage, bool begin) {
@@ -241,9 +249,10 @@ int vl_reserve(vl_ctx* c, int32_t max_queries, int64_t max_n_per_query, int32_t 
   return rc ? VL_ERR_OOM : VL_OK;
 }
 
-int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, void* stream) {
-  if (!c || !a || !o) return fail(c, VL_ERR_INVALID, "null argument");
-  cudaStream_t st = (cudaStream_t)stream;
+}  // extern "C"
+
+// Validates the arguments and fills the round parameters.
+static int ransac_params(vl_ctx* c, const vl_ransac_args* a, RansacParams& p) {
   const vl_ransac_config& cfg = a->cfg;
   if (!(cfg.reproj_threshold > 0)) return fail(c, VL_ERR_INVALID, "reproj_threshold must be positive");
   if (!(cfg.miss_probability > 0 && cfg.miss_probability < 1))
@@ -261,25 +270,32 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     if (n < 3) return fail(c, VL_ERR_UNDERCONSTRAINED, "need >= 3 matches, got " + std::to_string(n));
     if (n > 0x7FFFFFFF) return fail(c, VL_ERR_INVALID, "more than 2^31-1 matches in one query");
   }
-  VL_CUDA(c, cudaSetDevice(c->device));
-  RansacParams p;
   p.max_iterations = cfg.max_iterations;
   p.batch_size = cfg.batch_size;
   p.lm_max_iters = cfg.lm_max_iters;
   p.eta = cfg.miss_probability;
   p.tau = cfg.reproj_threshold;
   p.cauchy = cauchy;
-  const int64_t B = cfg.batch_size;
+  return VL_OK;
+}
+
+// Largest query chunk whose per-round workspace stays bounded (~6 GB).
+static int64_t ransac_chunk(int64_t Q, int64_t B) {
   const int64_t HCAP = 4 * B;
-  // chunk the query set so the per-round workspace stays bounded (~6 GB)
   const int64_t per_q = B * (3 * 4 + 48 * 8 + 4) + HCAP * (12 * 4 + 4) + HCAP * 4 * 20;
   int64_t Qc = std::max<int64_t>(1, std::min<int64_t>(Q, (int64_t)6e9 / per_q));
-  Qc = std::min<int64_t>(Qc, 4096);
-  Inputs in{a->px, a->X, a->w};
-  Outputs out{o->q, o->t, o->inlier_flags, o->inlier_count, o->score, o->iterations, o->converged, o->stats};
+  return std::min<int64_t>(Qc, 4096);
+}
+
+// Uploads per-query state for queries [q0, q0+Qn), sizes the workspace and
+// runs k_prep.  Fills `wk`.
+static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, const Inputs& in, Work& wk,
+                       cudaStream_t st) {
+  const vl_ransac_config& cfg = a->cfg;
+  const int64_t B = cfg.batch_size;
+  const int64_t HCAP = 4 * B;
   std::vector<QState> hq;
-  for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
-    const int Qn = (int)std::min<int64_t>(Qc, Q - q0);
+  {
     hq.assign(Qn, QState());
     int64_t nsub_tot = 0, ncomp = 0;
     int max_split = 1;
@@ -327,11 +343,10 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     char* hp = (char*)c->h_pinned;
     QState* h_qs = (QState*)hp;
     int* h_active = (int*)(hp + Qn * sizeof(QState));
-    int* h_count = (int*)(hp + Qn * sizeof(QState) + Qn * sizeof(int));
     // the pinned staging buffer is reused across chunks: previous copies finished at the last sync
     std::memcpy(h_qs, hq.data(), Qn * sizeof(QState));
     for (int i = 0; i < Qn; ++i) h_active[i] = i;
-    Work wk;
+    wk = Work();
     wk.qs = (QState*)c->qs.p;
     wk.active_list = (int*)c->active.p;
     wk.active_count = (int*)c->active_count.p;
@@ -351,6 +366,8 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     wk.HCAP = (int)HCAP;
     wk.NSPLIT = max_split;
     wk.item_cap = item_cap;
+    wk.split_rank = 0;
+    wk.split_size = 1;
     VL_CUDA(c, cudaMemcpyAsync(wk.qs, h_qs, Qn * sizeof(QState), cudaMemcpyHostToDevice, st));
     VL_CUDA(c, cudaMemcpyAsync(wk.active_list, h_active, Qn * sizeof(int), cudaMemcpyHostToDevice, st));
     VL_CUDA(c, cudaMemsetAsync(wk.item_count, 0, 2 * sizeof(int), st));
@@ -359,16 +376,45 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     c->launches += launch_prep(wk, in, Qn, st);
     prof_hook(c, kStagePrep, false);
     if ((rc = check_launch(c))) return rc;
+  }
+  return VL_OK;
+}
+
+// Reads back the active-query count after a round (the one host sync per round).
+static int read_active(vl_ctx* c, const Work& wk, cudaStream_t st, int* nactive) {
+  int* h_count = (int*)((char*)c->h_pinned + c->h_pinned_cap - 16);
+  VL_CUDA(c, cudaMemcpyAsync(h_count, wk.active_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+  VL_CUDA(c, cudaStreamSynchronize(st));
+  prof_collect(c);
+  *nactive = *h_count;
+  return VL_OK;
+}
+
+extern "C" {
+
+int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, void* stream) {
+  if (!c || !a || !o) return fail(c, VL_ERR_INVALID, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  RansacParams p;
+  int rc;
+  if ((rc = ransac_params(c, a, p))) return rc;
+  VL_CUDA(c, cudaSetDevice(c->device));
+  const int Q = a->num_queries;
+  const int64_t B = a->cfg.batch_size;
+  const int64_t Qc = ransac_chunk(Q, B);
+  Inputs in{a->px, a->X, a->w};
+  Outputs out{o->q, o->t, o->inlier_flags, o->inlier_count, o->score, o->iterations, o->converged, o->stats};
+  const int64_t max_rounds = (a->cfg.max_iterations + B - 1) / B + 1;
+  for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
+    const int Qn = (int)std::min<int64_t>(Qc, Q - q0);
+    Work wk;
+    if ((rc = setup_chunk(c, a, q0, Qn, in, wk, st))) return rc;
     int nactive = Qn;
     int guard = 0;
-    const int64_t max_rounds = (cfg.max_iterations + B - 1) / B + 1;
     while (nactive > 0) {
-      c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c);
+      c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c, 0);
       if ((rc = check_launch(c))) return rc;
-      VL_CUDA(c, cudaMemcpyAsync(h_count, wk.active_count, sizeof(int), cudaMemcpyDeviceToHost, st));
-      VL_CUDA(c, cudaStreamSynchronize(st));
-      prof_collect(c);
-      nactive = *h_count;
+      if ((rc = read_active(c, wk, st, &nactive))) return rc;
       if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
     }
     prof_hook(c, kStageFinal, true);
@@ -381,6 +427,84 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     }
   }
   return VL_OK;
+}
+
+// ---- stepwise driver (hypothesis-split mode) ------------------
+// Every rank runs the same queries with the same seeds (identical samples,
+// P3P and scans); the scoring work items are dealt round-robin to ranks and
+// non-owned items write zero partial sums, so a SUM all-reduce of the
+// partial-cost buffer between vl_ransac_step_score and
+// vl_ransac_step_finish gives every rank bit-identical costs — and the same
+// final estimate as the single-GPU path.
+int vl_ransac_begin(vl_ctx* c, const vl_ransac_args* a, int32_t split_rank, int32_t split_size, void* stream) {
+  if (!c || !a) return fail(c, VL_ERR_INVALID, "null argument");
+  if (split_size < 1 || split_rank < 0 || split_rank >= split_size) return fail(c, VL_ERR_INVALID, "bad split");
+  RansacParams p;
+  int rc;
+  if ((rc = ransac_params(c, a, p))) return rc;
+  if (ransac_chunk(a->num_queries, a->cfg.batch_size) < a->num_queries)
+    return fail(c, VL_ERR_INVALID, "stepwise driver takes one workspace chunk of queries");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  c->step.in = Inputs{a->px, a->X, a->w};
+  if ((rc = setup_chunk(c, a, 0, a->num_queries, c->step.in, c->step.wk, st))) return rc;
+  c->step.wk.split_rank = split_rank;
+  c->step.wk.split_size = split_size;
+  c->step.p = p;
+  c->step.Q = a->num_queries;
+  c->step.nactive = a->num_queries;
+  c->step.rounds = 0;
+  c->step.max_rounds = (a->cfg.max_iterations + a->cfg.batch_size - 1) / a->cfg.batch_size + 1;
+  c->step.open = 1;
+  return VL_OK;
+}
+
+int vl_ransac_partial_bytes(vl_ctx* c, int64_t* bytes) {
+  if (!c || !c->step.open || !bytes) return fail(c, VL_ERR_INVALID, "no open stepwise run");
+  *bytes = (int64_t)c->step.Q * c->step.wk.NSPLIT * c->step.wk.HCAP * (int64_t)sizeof(float);
+  return VL_OK;
+}
+
+int vl_ransac_step_score(vl_ctx* c, void* partial_out, void* stream) {
+  if (!c || !c->step.open) return fail(c, VL_ERR_INVALID, "no open stepwise run");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c->step.nactive <= 0) return fail(c, VL_ERR_INVALID, "no active queries");
+  c->launches += launch_round(c->step.wk, c->step.in, c->step.p, c->step.nactive, c->num_sms, st, prof_hook, c, 1);
+  int rc;
+  if ((rc = check_launch(c))) return rc;
+  if (partial_out) {
+    const size_t bytes = (size_t)c->step.Q * c->step.wk.NSPLIT * c->step.wk.HCAP * sizeof(float);
+    VL_CUDA(c, cudaMemcpyAsync(partial_out, c->step.wk.partial, bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  return VL_OK;
+}
+
+int vl_ransac_step_finish(vl_ctx* c, const void* partial_in, int32_t* nactive, void* stream) {
+  if (!c || !c->step.open || !nactive) return fail(c, VL_ERR_INVALID, "no open stepwise run");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (partial_in) {
+    const size_t bytes = (size_t)c->step.Q * c->step.wk.NSPLIT * c->step.wk.HCAP * sizeof(float);
+    VL_CUDA(c, cudaMemcpyAsync(c->step.wk.partial, partial_in, bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  c->launches += launch_round(c->step.wk, c->step.in, c->step.p, c->step.nactive, c->num_sms, st, prof_hook, c, 2);
+  int rc;
+  if ((rc = check_launch(c))) return rc;
+  int na = 0;
+  if ((rc = read_active(c, c->step.wk, st, &na))) return rc;
+  c->step.nactive = na;
+  *nactive = na;
+  if (++c->step.rounds > c->step.max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
+  return VL_OK;
+}
+
+int vl_ransac_end(vl_ctx* c, const vl_ransac_out* o, void* stream) {
+  if (!c || !c->step.open || !o) return fail(c, VL_ERR_INVALID, "no open stepwise run");
+  if (c->step.nactive != 0) return fail(c, VL_ERR_INVALID, "queries still active");
+  cudaStream_t st = (cudaStream_t)stream;
+  Outputs out{o->q, o->t, o->inlier_flags, o->inlier_count, o->score, o->iterations, o->converged, o->stats};
+  c->launches += launch_final(c->step.wk, c->step.in, out, c->step.p, c->step.Q, 0, st);
+  c->step.open = 0;
+  return check_launch(c);
 }
 
 static Pose pose_from_host(const double* q, const double* t) {

@@ -65,6 +65,7 @@ struct Work {
   double2* comp_pk;      // [N][3] packed full-set inliers (final refinement)
   int B, HCAP, NSPLIT;
   int64_t item_cap;
+  int split_rank, split_size;  // hypothesis-split mode: scoring items dealt round-robin
 };
 
 struct Inputs {
@@ -89,8 +90,9 @@ int launch_prep(const Work& wk, const Inputs& in, int Q, cudaStream_t st);
 // profiling stages (vl_profile_read order)
 enum { kStagePrep = 0, kStageSample, kStageP3P, kStageCompact, kStageScore, kStageScan, kStageActive,
        kStageFinal, kStageLift, kNumStages };
+// phase 0: whole round; 1: sample .. score; 2: scan + active (stepwise driver)
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
-                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg);
+                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg, int phase);
 int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
                  int q_base, cudaStream_t st);
 

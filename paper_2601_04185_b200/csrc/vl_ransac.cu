@@ -493,31 +493,38 @@ static void launch_clustered(void (*k)(KArgs...), int nq, int block, size_t smem
 // One round, kernel by kernel; `hook(stage, begin)` lets the caller bracket
 // each launch with CUDA events (profiling) without touching the kernels.
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
-                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg) {
+                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg, int phase) {
   auto H = [&](int stage, bool begin) {
     if (hook) hook(hook_arg, stage, begin);
   };
-  H(kStageSample, true);
-  k_sample<<<nactive, 256, 0, st>>>(wk, p);
-  H(kStageSample, false);
-  H(kStageP3P, true);
-  dim3 gp(nactive, (wk.B + kP3PThreads - 1) / kP3PThreads);
-  k_p3p<<<gp, kP3PThreads, 0, st>>>(wk, in);
-  H(kStageP3P, false);
-  H(kStageCompact, true);
-  k_compact<<<nactive, 1024, 0, st>>>(wk);
-  H(kStageCompact, false);
-  H(kStageScore, true);
-  launch_score(wk, (float)(p.tau * p.tau), num_sms, st);
-  H(kStageScore, false);
-  H(kStageScan, true);
-  const size_t smem = (size_t)wk.HCAP * sizeof(float);
-  launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, 2 * num_sms), st, wk, p);
-  H(kStageScan, false);
-  H(kStageActive, true);
-  k_active<<<1, 1024, 0, st>>>(wk, nactive);
-  H(kStageActive, false);
-  return 6;
+  int n = 0;
+  if (phase != 2) {
+    H(kStageSample, true);
+    k_sample<<<nactive, 256, 0, st>>>(wk, p);
+    H(kStageSample, false);
+    H(kStageP3P, true);
+    dim3 gp(nactive, (wk.B + kP3PThreads - 1) / kP3PThreads);
+    k_p3p<<<gp, kP3PThreads, 0, st>>>(wk, in);
+    H(kStageP3P, false);
+    H(kStageCompact, true);
+    k_compact<<<nactive, 1024, 0, st>>>(wk);
+    H(kStageCompact, false);
+    H(kStageScore, true);
+    launch_score(wk, (float)(p.tau * p.tau), num_sms, st);
+    H(kStageScore, false);
+    n += 4;
+  }
+  if (phase != 1) {
+    H(kStageScan, true);
+    const size_t smem = (size_t)wk.HCAP * sizeof(float);
+    launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, 2 * num_sms), st, wk, p);
+    H(kStageScan, false);
+    H(kStageActive, true);
+    k_active<<<1, 1024, 0, st>>>(wk, nactive);
+    H(kStageActive, false);
+    n += 2;
+  }
+  return n;
 }
 
 // ------------------------------------------------------------------ final stage

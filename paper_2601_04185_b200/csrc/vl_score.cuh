@@ -126,6 +126,15 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     const ScoreItem item = wk.items[it];
     const QState& S = wk.qs[item.q];
     const int nh = S.nh, nsub = S.nsub;
+    if (wk.split_size > 1 && it % wk.split_size != wk.split_rank) {
+      // hypothesis-split mode: another rank owns this item; contribute zeros
+      // to the SUM all-reduce of the partial buffer
+      float* out = wk.partial + ((int64_t)item.q * wk.NSPLIT + item.split) * wk.HCAP;
+      const int h1 = min(nh, (item.tile + 1) * NT * HT);
+      for (int h = item.tile * NT * HT + threadIdx.x; h < h1; h += NT) out[h] = 0.f;
+      __syncthreads();  // every thread has read s_it before it is rewritten
+      continue;
+    }
     const int c0 = item.split * CH;
     const int cn = min(CH, nsub - c0);
     const float4* src = wk.sub32 + 2 * (S.sub_off + c0);

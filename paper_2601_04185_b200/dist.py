@@ -40,6 +40,118 @@ def run_sharded(items, fn, group=None):
     return out
 
 
+class SplitRun:
+    """One rank's side of the hypothesis-split estimator.
+
+    Drives the C ABI stepwise driver (``vl_ransac_begin`` / ``step_score`` /
+    ``step_finish`` / ``end``) for queries whose matches are already on this
+    rank's device.  The caller reduces ``self.partial`` (SUM) across ranks
+    between ``score()`` and ``finish()``.
+    """
+
+    def __init__(self, ctx, px, X, w, offsets, intrinsics, seeds, cfg, rank: int, size: int):
+        import ctypes as C
+
+        import numpy as np
+        import torch
+
+        from . import _lib
+        from .posest import _cfg_c, _intr_c
+        self.ctx, self.L = ctx, _lib.lib()
+        self._keep = (px, X, w)
+        offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+        Q = offsets.shape[0] - 1
+        self.offsets, self.Q = offsets, Q
+        self._intr = (_lib.Intrinsics * Q)(*[_intr_c(i) for i in intrinsics])
+        self._rng = (_lib.PCG64State * Q)(*[_lib.pcg64_state(int(s)) for s in seeds])
+        a = _lib.RansacArgs()
+        a.num_queries = Q
+        a.offsets = offsets.ctypes.data_as(C.POINTER(C.c_int64))
+        a.intr, a.rng = self._intr, self._rng
+        a.px, a.X, a.w = px.data_ptr(), X.data_ptr(), w.data_ptr()
+        a.cfg = _cfg_c(cfg)
+        self._args = a
+        ctx.check(self.L.vl_ransac_begin(ctx.handle, C.byref(a), rank, size, _lib.stream_ptr()), "vl_ransac_begin")
+        nb = C.c_int64()
+        ctx.check(self.L.vl_ransac_partial_bytes(ctx.handle, C.byref(nb)), "vl_ransac_partial_bytes")
+        self.partial = torch.empty((nb.value // 4,), dtype=torch.float32, device=px.device)
+        self.nactive = Q
+
+    def score(self):
+        from . import _lib
+        self.ctx.check(self.L.vl_ransac_step_score(self.ctx.handle, self.partial.data_ptr(), _lib.stream_ptr()),
+                       "vl_ransac_step_score")
+
+    def finish(self) -> int:
+        import ctypes as C
+
+        from . import _lib
+        n = C.c_int32()
+        self.ctx.check(self.L.vl_ransac_step_finish(self.ctx.handle, self.partial.data_ptr(), C.byref(n),
+                                                    _lib.stream_ptr()), "vl_ransac_step_finish")
+        self.nactive = int(n.value)
+        return self.nactive
+
+    def end(self):
+        import ctypes as C
+
+        import torch
+
+        from . import _lib
+        from .posest import _estimates_from
+        dev = self.partial.device
+        N = int(self.offsets[-1])
+        Q = self.Q
+        out = {"q": torch.empty((Q, 4), dtype=torch.float64, device=dev),
+               "t": torch.empty((Q, 3), dtype=torch.float64, device=dev),
+               "flags": torch.empty((max(N, 1),), dtype=torch.uint8, device=dev),
+               "count": torch.empty((Q,), dtype=torch.int64, device=dev),
+               "score": torch.empty((Q,), dtype=torch.float64, device=dev),
+               "iterations": torch.empty((Q,), dtype=torch.int64, device=dev),
+               "converged": torch.empty((Q,), dtype=torch.int32, device=dev),
+               "stats": torch.empty((Q, 4), dtype=torch.int64, device=dev)}
+        o = _lib.RansacOut()
+        o.q, o.t, o.inlier_flags = out["q"].data_ptr(), out["t"].data_ptr(), out["flags"].data_ptr()
+        o.inlier_count, o.score = out["count"].data_ptr(), out["score"].data_ptr()
+        o.iterations, o.converged = out["iterations"].data_ptr(), out["converged"].data_ptr()
+        o.stats = out["stats"].data_ptr()
+        self.ctx.check(self.L.vl_ransac_end(self.ctx.handle, C.byref(o), _lib.stream_ptr()), "vl_ransac_end")
+        out["flags"] = out["flags"][:N]
+        return _estimates_from(out, self.offsets)
+
+
+def ransac_pnp_split(matches, intr, cfg, group=None):
+    """One query's hypotheses split across the ranks of `group` (one GPU each).
+
+    Every rank passes the same matches and config; per round, one NCCL SUM
+    all-reduce of the partial-cost buffer (SURVEY §8e "exact reference
+    semantics" variant: the full cost vector, so the ordered first-better
+    scan is unchanged).  Returns the same PoseEstimate on every rank,
+    bit-identical to ``ransac_pnp``.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+    from .posest import UnderConstrainedError, _host_arrays, _to_device
+    distributed = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank(group) if distributed else 0
+    world = dist.get_world_size(group) if distributed else 1
+    px, X, w = _host_arrays(matches)
+    if px.shape[0] < 3:
+        raise UnderConstrainedError(f"need >= 3 matches, got {px.shape[0]}")
+    ctx = _lib.context()
+    dpx, dX, dw = _to_device(px), _to_device(X), _to_device(w)
+    run = SplitRun(ctx, dpx, dX, dw, [0, px.shape[0]], [intr], [cfg.seed], cfg, rank, world)
+    while run.nactive > 0:
+        run.score()
+        if world > 1:
+            dist.all_reduce(run.partial, op=dist.ReduceOp.SUM, group=group)
+        run.finish()
+    torch.cuda.current_stream().synchronize()
+    return run.end()[0]
+
+
 def localize_sharded(jobs, vmap, cfg, seeds=None, group=None, **kw):
     """``localize_batch`` over all ranks' GPUs (each rank: its own shard, its own device)."""
     from .localizer import localize_batch

@@ -245,3 +245,33 @@ def test_randomized_parity_sweep(vl, intr):
         exact_pose += int(og.rot_err_deg(e.pose.q, o.q) < 1e-7)
         exact_mask += int(np.array_equal(e.inlier_flags, o.inlier_flags))
     print(f"sweep: {exact_pose}/40 poses within 1e-7 deg, {exact_mask}/40 masks identical")
+
+
+def test_hypothesis_split_emulated_ranks_bit_identical(vl, intr):
+    """§8e hypothesis-split: G ranks emulated sequentially on one GPU (separate
+    contexts; the NCCL SUM all-reduce replaced by a device sum of the ranks'
+    partial buffers).  Every rank must end with the single-GPU result, bit-exact."""
+    import torch
+    from paper_2601_04185_b200 import _lib
+    from paper_2601_04185_b200.dist import SplitRun, ransac_pnp_split
+    px, X, w, _ = matches_a(6000, 0.6, 1.0, seed=77)
+    cfg = vl.RansacConfig(seed=12, max_iterations=4000, miss_probability=1e-300)
+    ref = vl.ransac_pnp((px, X, w), intr, cfg)
+    assert np.array_equal(ransac_pnp_split((px, X, w), intr, cfg).pose.q, ref.pose.q)  # world = 1
+    d = [torch.from_numpy(a).cuda() for a in (px, X, w)]
+    for G in (2, 3):
+        ctxs = [_lib.Context(0) for _ in range(G)]
+        runs = [SplitRun(ctxs[r], d[0], d[1], d[2], [0, px.shape[0]], [intr], [cfg.seed], cfg, r, G)
+                for r in range(G)]
+        while runs[0].nactive > 0:
+            for r in runs:
+                r.score()
+            total = torch.stack([r.partial for r in runs]).sum(0)
+            for r in runs:
+                r.partial.copy_(total)
+            n = [r.finish() for r in runs]
+            assert len(set(n)) == 1
+        for r in runs:
+            e = r.end()[0]
+            assert np.array_equal(e.pose.q, ref.pose.q) and np.array_equal(e.pose.t, ref.pose.t)
+            assert np.array_equal(e.inlier_flags, ref.inlier_flags) and e.iterations == ref.iterations
