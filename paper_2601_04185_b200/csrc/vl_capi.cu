@@ -320,7 +320,8 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
       ncomp += n;
       max_split = std::max(max_split, S.nsplit);
     }
-    const int64_t ntile = (HCAP + kScoreTileHyps - 1) / kScoreTileHyps;
+    // worst case: fine items (256-hypothesis tiles x 1 split)
+    const int64_t ntile = (HCAP + kScoreTileHypsFine - 1) / kScoreTileHypsFine;
     const int64_t item_cap = (int64_t)Qn * ntile * max_split;
     int rc = VL_OK;
     if ((rc = ensure(c, c->qs, Qn * sizeof(QState))) ||

@@ -9,9 +9,15 @@ namespace vl {
 
 // Scoring tile geometry (vl_score.cu).
 constexpr int kScoreThreads = 128;
-constexpr int kScoreHypPerThread = 6;  // 3 f32x2 pairs (tools/score_bench.cu sweep)
+constexpr int kScoreHypPerThread = 6;  // coarse items: 3 f32x2 pairs (tools/score_bench.cu sweep)
 constexpr int kScoreTileHyps = kScoreThreads * kScoreHypPerThread;  // 768
-constexpr int kScoreChunk = 512;  // correspondences per split (fixed => launch-independent sums)
+constexpr int kScoreItemSplits = 4;    // coarse items: 4 splits = 512 correspondences
+constexpr int kScoreHypPerThreadFine = 2;  // fine items (small batches): 1 pair, 1 split
+constexpr int kScoreTileHypsFine = kScoreThreads * kScoreHypPerThreadFine;  // 256
+// correspondences per split: the canonical fp32 summation unit (each split is
+// summed sequentially by one thread, splits are combined in order by k_scan),
+// so the cost bits do not depend on the tile shape, item size or grid
+constexpr int kScoreChunk = 128;
 
 // Per-query device state of the batched estimator.
 struct __align__(16) QState {
@@ -34,7 +40,7 @@ struct __align__(16) QState {
 };
 
 struct ScoreItem {
-  int q, tile, split, pad;
+  int q, tile, split, nsplit;  // query, hypothesis tile, first split, splits in the item
 };
 
 struct RansacParams {

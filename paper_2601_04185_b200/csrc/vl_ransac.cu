@@ -287,7 +287,7 @@ int launch_p3p_batch(const double* f, const double* P, int B, double* slots, int
   return 2;
 }
 
-__global__ void __launch_bounds__(1024) k_compact(Work wk) {
+__global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
   __shared__ int warp_tot[32];
   __shared__ int s_item0;
   const int q = wk.active_list[blockIdx.x];
@@ -322,8 +322,13 @@ __global__ void __launch_bounds__(1024) k_compact(Work wk) {
     running += total;
   }
   const int nh = running;
-  const int ntile = (nh + kScoreTileHyps - 1) / kScoreTileHyps;
-  const int nitems = ntile * S.nsplit;
+  // score work items: coarse (768-hypothesis tiles x 4 splits) for big batches,
+  // fine (256 x 1) when the batch is too small to fill the GPU otherwise
+  const int tile_h = fine ? kScoreTileHypsFine : kScoreTileHyps;
+  const int spi = fine ? 1 : kScoreItemSplits;
+  const int ntile = (nh + tile_h - 1) / tile_h;
+  const int ngroups = (S.nsplit + spi - 1) / spi;
+  const int nitems = ntile * ngroups;
   if (threadIdx.x == 0) {
     S.nh = nh;
     S.hyps += nh;
@@ -334,9 +339,9 @@ __global__ void __launch_bounds__(1024) k_compact(Work wk) {
   for (int i = threadIdx.x; i < nitems; i += 1024) {
     ScoreItem it;
     it.q = q;
-    it.tile = i / S.nsplit;
-    it.split = i % S.nsplit;
-    it.pad = 0;
+    it.tile = i / ngroups;
+    it.split = (i % ngroups) * spi;
+    it.nsplit = min(spi, S.nsplit - it.split);
     const int64_t pos = (int64_t)s_item0 + i;
     if (pos < wk.item_cap) wk.items[pos] = it;
   }
@@ -461,7 +466,7 @@ __global__ void __launch_bounds__(1024) k_active(Work wk, int nactive) {
   }
 }
 
-int launch_score(const Work& wk, float tau2, int num_sms, cudaStream_t st);  // vl_score.cu
+int launch_score(const Work& wk, float tau2, int num_sms, int fine, cudaStream_t st);  // vl_score.cu
 
 // Cluster size for a per-query kernel: spread few queries over up to 8 SMs
 // each (single-query latency), keep one CTA per query when the batch alone
@@ -498,6 +503,9 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     if (hook) hook(hook_arg, stage, begin);
   };
   int n = 0;
+  // coarse work items unless the whole batch would not fill ~3 waves of SMs
+  const int coarse_items = nactive * 2 * ((wk.NSPLIT + kScoreItemSplits - 1) / kScoreItemSplits);
+  const int fine = coarse_items < 3 * num_sms ? 1 : 0;
   if (phase != 2) {
     H(kStageSample, true);
     k_sample<<<nactive, 256, 0, st>>>(wk, p);
@@ -507,10 +515,10 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     k_p3p<<<gp, kP3PThreads, 0, st>>>(wk, in);
     H(kStageP3P, false);
     H(kStageCompact, true);
-    k_compact<<<nactive, 1024, 0, st>>>(wk);
+    k_compact<<<nactive, 1024, 0, st>>>(wk, fine);
     H(kStageCompact, false);
     H(kStageScore, true);
-    launch_score(wk, (float)(p.tau * p.tau), num_sms, st);
+    launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, st);
     H(kStageScore, false);
     n += 4;
   }

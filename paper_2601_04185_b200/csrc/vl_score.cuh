@@ -105,14 +105,19 @@ __device__ __forceinline__ float rcp_approx_ftz(float x) {
     accp = fma2(f2(b.y), e2_, accp);                                                              \
   }
 
-template <int NT, int HT, int CH, int MINB, int UNR>
+// Work item = (query, tile of NT*HT hypotheses, ns <= SPI consecutive
+// correspondence splits of SCH records).  The canonical fp32 cost of a
+// hypothesis is  sum over splits (in order) of  [sequential sum over the
+// split's records]  — every split is accumulated by exactly one thread in
+// record order and written to its own partial slot, so neither the tile
+// shape (HT), the splits per item (SPI) nor the grid changes a single bit.
+template <int NT, int HT, int SPI, int SCH, int MINB, int UNR>
 __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   static_assert(HT % 2 == 0, "hypotheses are processed in pairs");
   constexpr int HP = HT / 2;
   constexpr int NW = NT / 32;
   constexpr int WHYP = 32 * HT;  // hypotheses per warp slice
-  __shared__ float4 rec[2 * CH];
-  __shared__ float red[NW * WHYP];
+  __shared__ float4 rec[2 * SPI * SCH];
   __shared__ int s_it;
   const int nitems = wk.item_count[0];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -126,29 +131,28 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     const ScoreItem item = wk.items[it];
     const QState& S = wk.qs[item.q];
     const int nh = S.nh, nsub = S.nsub;
+    const int tile0 = item.tile * (NT * HT);
+    const int ns = item.nsplit;
+    float* outq = wk.partial + (int64_t)item.q * wk.NSPLIT * wk.HCAP;
     if (wk.split_size > 1 && it % wk.split_size != wk.split_rank) {
       // hypothesis-split mode: another rank owns this item; contribute zeros
       // to the SUM all-reduce of the partial buffer
-      float* out = wk.partial + ((int64_t)item.q * wk.NSPLIT + item.split) * wk.HCAP;
-      const int h1 = min(nh, (item.tile + 1) * NT * HT);
-      for (int h = item.tile * NT * HT + threadIdx.x; h < h1; h += NT) out[h] = 0.f;
+      const int h1 = min(nh, tile0 + NT * HT);
+      for (int s = 0; s < ns; ++s)
+        for (int h = tile0 + threadIdx.x; h < h1; h += NT) outq[(int64_t)(item.split + s) * wk.HCAP + h] = 0.f;
       __syncthreads();  // every thread has read s_it before it is rewritten
       continue;
     }
-    const int c0 = item.split * CH;
-    const int cn = min(CH, nsub - c0);
+    const int c0 = item.split * SCH;
+    const int cn = min(ns * SCH, nsub - c0);
     const float4* src = wk.sub32 + 2 * (S.sub_off + c0);
     // A partially filled (last) tile of r hypotheses needs WH = ceil(r / WHYP)
-    // warp slices; the other warps then split the correspondences instead
-    // (G groups), so every warp stays busy.  Group partial sums are combined
-    // in fixed order through shared memory (deterministic per query).
-    const int tile0 = item.tile * (NT * HT);
+    // warp slices; the other warps take other splits of the item (G groups),
+    // so a short tile does not leave warps idle.
     const int r = min(NT * HT, nh - tile0);
     const int WH = (r + WHYP - 1) / WHYP;
     const int G = NW / WH;
     const int hs = w % WH, grp = w / WH;
-    const bool active = grp < G;
-    const int cb = (grp * cn) / G, ce = ((grp + 1) * cn) / G;
     __syncthreads();
     for (int k = threadIdx.x; k < 2 * cn; k += NT) rec[k] = src[k];
     float2 P[HP][12];
@@ -165,10 +169,11 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
         P[jp][c] = make_float2(Pq[(int64_t)c * wk.HCAP + h0], Pq[(int64_t)c * wk.HCAP + h1]);
     }
     __syncthreads();
-    float2 acc[HP];
+    for (int s = grp; s < ns && grp < G; s += G) {
+      float2 acc[HP];
 #pragma unroll
-    for (int jp = 0; jp < HP; ++jp) acc[jp] = make_float2(0.f, 0.f);
-    if (active) {
+      for (int jp = 0; jp < HP; ++jp) acc[jp] = make_float2(0.f, 0.f);
+      const int cb = s * SCH, ce = min(cb + SCH, cn);
 #pragma unroll UNR
       for (int c = cb; c < ce; ++c) {
         const float4 a = rec[2 * c];
@@ -176,35 +181,11 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
 #pragma unroll
         for (int jp = 0; jp < HP; ++jp) VL_SCORE_EVAL2(P[jp], acc[jp]);
       }
-    }
-    float* out = wk.partial + ((int64_t)item.q * wk.NSPLIT + item.split) * wk.HCAP;
-    if (G == 1) {
+      float* out = outq + (int64_t)(item.split + s) * wk.HCAP;
 #pragma unroll
       for (int jp = 0; jp < HP; ++jp) {
         if (hid[2 * jp] < nh) out[hid[2 * jp]] = acc[jp].x;
         if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = acc[jp].y;
-      }
-    } else {
-      // groups g = 1..G-1 park their sums; group 0 adds them in order
-      if (active && grp > 0) {
-#pragma unroll
-        for (int jp = 0; jp < HP; ++jp) {
-          red[(grp - 1) * WH * WHYP + hs * WHYP + lane * HT + 2 * jp] = acc[jp].x;
-          red[(grp - 1) * WH * WHYP + hs * WHYP + lane * HT + 2 * jp + 1] = acc[jp].y;
-        }
-      }
-      __syncthreads();
-      if (grp == 0) {
-#pragma unroll
-        for (int jp = 0; jp < HP; ++jp) {
-          float sx = acc[jp].x, sy = acc[jp].y;
-          for (int g = 1; g < G; ++g) {
-            sx += red[(g - 1) * WH * WHYP + hs * WHYP + lane * HT + 2 * jp];
-            sy += red[(g - 1) * WH * WHYP + hs * WHYP + lane * HT + 2 * jp + 1];
-          }
-          if (hid[2 * jp] < nh) out[hid[2 * jp]] = sx;
-          if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = sy;
-        }
       }
     }
   }

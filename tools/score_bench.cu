@@ -27,15 +27,15 @@ struct Bench {
   std::vector<QState> hq;
 };
 
-template <int NT, int HT, int CH, int MINB, int UNR, bool PAIR = false>
+template <int NT, int HT, int SPI, int MINB, int UNR>
 double run_variant(Bench& b, const char* name, std::vector<float>& ref, int reps, int grid_mult) {
   const int tile = NT * HT;
   const int ntile = (b.nh + tile - 1) / tile;
-  const int nsplit = (b.nsub + CH - 1) / CH;
+  const int nsplit = (b.nsub + 127) / 128;
   std::vector<ScoreItem> items;
   for (int q = 0; q < b.Q; ++q)
     for (int t = 0; t < ntile; ++t)
-      for (int s = 0; s < nsplit; ++s) items.push_back(ScoreItem{q, t, s, 0});
+      for (int s = 0; s < nsplit; s += SPI) items.push_back(ScoreItem{q, t, s, nsplit - s < SPI ? nsplit - s : SPI});
   // split count differs per variant: set QState.nsplit accordingly
   for (auto& s : b.hq) s.nsplit = nsplit;
   CK(cudaMemcpy(b.wk.qs, b.hq.data(), b.Q * sizeof(QState), cudaMemcpyHostToDevice));
@@ -45,7 +45,7 @@ double run_variant(Bench& b, const char* name, std::vector<float>& ref, int reps
   int dev = 0, sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int occ = 0;
-  auto kern = PAIR ? k_score2_t<NT, HT, CH, MINB, UNR> : k_score_t<NT, HT, CH, MINB, UNR>;
+  auto kern = k_score2_t<NT, HT, SPI, 128, MINB, UNR>;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0));
   const int grid = sms * occ * grid_mult;
   const float tau2 = 144.f;
@@ -83,8 +83,8 @@ double run_variant(Bench& b, const char* name, std::vector<float>& ref, int reps
   else
     for (size_t i = 0; i < costs.size(); ++i)
       maxrel = fmax(maxrel, fabs(costs[i] - ref[i]) / fmax(1e-3, fabs(ref[i])));
-  printf("%-28s NT=%3d HT=%d CH=%4d minB=%d unr=%d occ=%d grid=%5d  %8.3f ms/rep  %.4e evals/s  %.1f TF(30/eval)  maxrel %.2e\n",
-         name, NT, HT, CH, MINB, UNR, occ, grid, ms / reps, eps, eps * 30 / 1e12, maxrel);
+  printf("%-28s NT=%3d HT=%d SPI=%d minB=%d unr=%d occ=%d grid=%5d  %8.3f ms/rep  %.4e evals/s  %.1f TF(30/eval)  maxrel %.2e\n",
+         name, NT, HT, SPI, MINB, UNR, occ, grid, ms / reps, eps, eps * 30 / 1e12, maxrel);
   return eps;
 }
 
@@ -139,11 +139,8 @@ int main(int argc, char** argv) {
   wk.NSPLIT = b.NSPLIT;
   std::vector<float> ref;
   const int reps = 5;
-  run_variant<128, 4, 512, 4, 2>(b, "baseline", ref, reps, 1);
-  run_variant<128, 6, 512, 3, 2, true>(b, "pair HT6", ref, reps, 1);
-  run_variant<128, 6, 512, 4, 2, true>(b, "pair HT6 minB4", ref, reps, 1);
-  run_variant<64, 6, 512, 8, 2, true>(b, "pair NT64 HT6", ref, reps, 1);
-  run_variant<64, 6, 512, 6, 2, true>(b, "pair NT64 HT6 minB6", ref, reps, 1);
-  run_variant<128, 4, 512, 4, 2, true>(b, "pair HT4", ref, reps, 1);
+  run_variant<128, 6, 4, 3, 2>(b, "coarse HT6 x4 splits", ref, reps, 1);
+  run_variant<128, 2, 1, 6, 2>(b, "fine HT2 x1 split", ref, reps, 1);
+  run_variant<128, 4, 4, 4, 2>(b, "HT4 x4 splits", ref, reps, 1);
   return 0;
 }
