@@ -12,6 +12,9 @@ constexpr int kScoreThreads = 128;
 constexpr int kScoreHypPerThread = 6;  // coarse items: 3 f32x2 pairs (tools/score_bench.cu sweep)
 constexpr int kScoreTileHyps = kScoreThreads * kScoreHypPerThread;  // 768
 constexpr int kScoreItemSplits = 4;    // coarse items: 4 splits = 512 correspondences
+// canonical cost = sum over split groups (in order) of the group sum
+// ((p0 + p1) + p2) + p3 over its splits; coarse items produce one group
+constexpr int kGroupSplits = kScoreItemSplits;
 constexpr int kScoreHypPerThreadFine = 2;  // fine items (small batches): 1 pair, 1 split
 constexpr int kScoreTileHypsFine = kScoreThreads * kScoreHypPerThreadFine;  // 256
 // correspondences per split: the canonical fp32 summation unit (each split is

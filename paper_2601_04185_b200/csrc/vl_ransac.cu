@@ -362,7 +362,7 @@ __device__ __forceinline__ int64_t required_iters_dev(double eps, double eta, in
 
 constexpr int kScanThreads = 256;
 
-__global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams p) {
+__global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams p, int fine) {
   extern __shared__ float costs[];
   __shared__ LMShared<kScanThreads> sm;
   __shared__ Pose s_start;
@@ -370,9 +370,21 @@ __global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams 
   QState& S = wk.qs[q];
   const int nh = S.nh, NS = S.nsplit;
   const float* part = wk.partial + (int64_t)q * wk.NSPLIT * wk.HCAP;
+  // canonical fp32 cost: groups of kGroupSplits splits in order, each group
+  // summed in split order; coarse rounds stored the group sums already
+  const int NG = (NS + kGroupSplits - 1) / kGroupSplits;
   for (int h = threadIdx.x; h < nh; h += kScanThreads) {
     float c = 0.f;
-    for (int s = 0; s < NS; ++s) c += part[(int64_t)s * wk.HCAP + h];
+    if (fine) {
+      for (int g = 0; g < NG; ++g) {
+        const int s0 = g * kGroupSplits, s1 = min(NS, s0 + kGroupSplits);
+        float gs = part[(int64_t)s0 * wk.HCAP + h];
+        for (int s = s0 + 1; s < s1; ++s) gs += part[(int64_t)s * wk.HCAP + h];
+        c += gs;
+      }
+    } else {
+      for (int g = 0; g < NG; ++g) c += part[(int64_t)g * wk.HCAP + h];
+    }
     costs[h] = c;
   }
   __syncthreads();
@@ -525,7 +537,7 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   if (phase != 1) {
     H(kStageScan, true);
     const size_t smem = (size_t)wk.HCAP * sizeof(float);
-    launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, 2 * num_sms), st, wk, p);
+    launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, 2 * num_sms), st, wk, p, fine);
     H(kStageScan, false);
     H(kStageActive, true);
     k_active<<<1, 1024, 0, st>>>(wk, nactive);

@@ -117,7 +117,9 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   constexpr int HP = HT / 2;
   constexpr int NW = NT / 32;
   constexpr int WHYP = 32 * HT;  // hypotheses per warp slice
+  static_assert(SPI == 1 || SPI == kGroupSplits, "coarse items are exactly one split group");
   __shared__ float4 rec[2 * SPI * SCH];
+  __shared__ float red[SPI][SPI > 1 ? NT * HT : 1];
   __shared__ int s_it;
   const int nitems = wk.item_count[0];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -134,12 +136,17 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     const int tile0 = item.tile * (NT * HT);
     const int ns = item.nsplit;
     float* outq = wk.partial + (int64_t)item.q * wk.NSPLIT * wk.HCAP;
+    // partial slot layout: fine items (SPI == 1) write one slot per split;
+    // coarse items write one slot per group of kGroupSplits splits, holding
+    // the group sum ((p0 + p1) + p2) + p3 that k_scan forms itself in fine mode
     if (wk.split_size > 1 && it % wk.split_size != wk.split_rank) {
       // hypothesis-split mode: another rank owns this item; contribute zeros
       // to the SUM all-reduce of the partial buffer
       const int h1 = min(nh, tile0 + NT * HT);
-      for (int s = 0; s < ns; ++s)
-        for (int h = tile0 + threadIdx.x; h < h1; h += NT) outq[(int64_t)(item.split + s) * wk.HCAP + h] = 0.f;
+      const int slot0 = SPI == 1 ? item.split : item.split / kGroupSplits;
+      const int nslot = SPI == 1 ? ns : 1;
+      for (int s = 0; s < nslot; ++s)
+        for (int h = tile0 + threadIdx.x; h < h1; h += NT) outq[(int64_t)(slot0 + s) * wk.HCAP + h] = 0.f;
       __syncthreads();  // every thread has read s_it before it is rewritten
       continue;
     }
@@ -169,6 +176,9 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
         P[jp][c] = make_float2(Pq[(int64_t)c * wk.HCAP + h0], Pq[(int64_t)c * wk.HCAP + h1]);
     }
     __syncthreads();
+    float2 gsum[HP];
+#pragma unroll
+    for (int jp = 0; jp < HP; ++jp) gsum[jp] = make_float2(0.f, 0.f);
     for (int s = grp; s < ns && grp < G; s += G) {
       float2 acc[HP];
 #pragma unroll
@@ -181,11 +191,50 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
 #pragma unroll
         for (int jp = 0; jp < HP; ++jp) VL_SCORE_EVAL2(P[jp], acc[jp]);
       }
-      float* out = outq + (int64_t)(item.split + s) * wk.HCAP;
+      if (SPI == 1) {
+        float* out = outq + (int64_t)(item.split + s) * wk.HCAP;
 #pragma unroll
-      for (int jp = 0; jp < HP; ++jp) {
-        if (hid[2 * jp] < nh) out[hid[2 * jp]] = acc[jp].x;
-        if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = acc[jp].y;
+        for (int jp = 0; jp < HP; ++jp) {
+          if (hid[2 * jp] < nh) out[hid[2 * jp]] = acc[jp].x;
+          if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = acc[jp].y;
+        }
+      } else if (G == 1) {
+#pragma unroll
+        for (int jp = 0; jp < HP; ++jp) {
+          gsum[jp].x = (s == 0) ? acc[jp].x : gsum[jp].x + acc[jp].x;
+          gsum[jp].y = (s == 0) ? acc[jp].y : gsum[jp].y + acc[jp].y;
+        }
+      } else {
+        // split s of a partial tile computed by warp group grp: park it
+#pragma unroll
+        for (int jp = 0; jp < HP; ++jp) {
+          red[s][hs * WHYP + lane * HT + 2 * jp] = acc[jp].x;
+          red[s][hs * WHYP + lane * HT + 2 * jp + 1] = acc[jp].y;
+        }
+      }
+    }
+    if (SPI > 1) {
+      float* out = outq + (int64_t)(item.split / kGroupSplits) * wk.HCAP;
+      if (G > 1) {
+        __syncthreads();
+        if (grp == 0) {
+#pragma unroll
+          for (int jp = 0; jp < HP; ++jp) {
+            float sx = red[0][hs * WHYP + lane * HT + 2 * jp], sy = red[0][hs * WHYP + lane * HT + 2 * jp + 1];
+            for (int s = 1; s < ns; ++s) {
+              sx += red[s][hs * WHYP + lane * HT + 2 * jp];
+              sy += red[s][hs * WHYP + lane * HT + 2 * jp + 1];
+            }
+            gsum[jp] = make_float2(sx, sy);
+          }
+        }
+      }
+      if (grp == 0) {
+#pragma unroll
+        for (int jp = 0; jp < HP; ++jp) {
+          if (hid[2 * jp] < nh) out[hid[2 * jp]] = gsum[jp].x;
+          if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = gsum[jp].y;
+        }
       }
     }
   }

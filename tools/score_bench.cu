@@ -74,9 +74,20 @@ double run_variant(Bench& b, const char* name, std::vector<float>& ref, int reps
   std::vector<float> costs((size_t)b.Q * b.nh);
   for (int q = 0; q < b.Q; ++q)
     for (int h = 0; h < b.nh; ++h) {
-      double c = 0;
-      for (int s = 0; s < nsplit; ++s) c += part[((size_t)q * b.NSPLIT + s) * b.HCAP + h];
-      costs[(size_t)q * b.nh + h] = (float)c;
+      // canonical order: group sums of 4 splits, groups in order (k_scan)
+      float c = 0.f;
+      const int ng = (nsplit + 3) / 4;
+      for (int g = 0; g < ng; ++g) {
+        float gs;
+        if (SPI == 1) {
+          gs = part[((size_t)q * b.NSPLIT + 4 * g) * b.HCAP + h];
+          for (int s = 4 * g + 1; s < nsplit && s < 4 * g + 4; ++s) gs += part[((size_t)q * b.NSPLIT + s) * b.HCAP + h];
+        } else {
+          gs = part[((size_t)q * b.NSPLIT + g) * b.HCAP + h];
+        }
+        c += gs;
+      }
+      costs[(size_t)q * b.nh + h] = c;
     }
   double maxrel = 0;
   if (ref.empty()) ref = costs;
