@@ -376,14 +376,35 @@ __global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams 
   for (int h = threadIdx.x; h < nh; h += kScanThreads) {
     float c = 0.f;
     if (fine) {
-      for (int g = 0; g < NG; ++g) {
-        const int s0 = g * kGroupSplits, s1 = min(NS, s0 + kGroupSplits);
-        float gs = part[(int64_t)s0 * wk.HCAP + h];
-        for (int s = s0 + 1; s < s1; ++s) gs += part[(int64_t)s * wk.HCAP + h];
-        c += gs;
+      // all loads of two groups issued before the ordered adds (memory-level parallelism)
+      for (int g = 0; g < NG; g += 2) {
+        float v[2 * kGroupSplits];
+#pragma unroll
+        for (int k = 0; k < 2 * kGroupSplits; ++k) {
+          const int s = g * kGroupSplits + k;
+          v[k] = s < NS ? __ldcg(part + (int64_t)s * wk.HCAP + h) : 0.f;
+        }
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+          const int s0 = (g + gg) * kGroupSplits;
+          if (s0 >= NS) break;
+          float gs = v[gg * kGroupSplits];
+#pragma unroll
+          for (int k = 1; k < kGroupSplits; ++k)
+            if (s0 + k < NS) gs += v[gg * kGroupSplits + k];
+          c += gs;
+        }
       }
     } else {
-      for (int g = 0; g < NG; ++g) c += part[(int64_t)g * wk.HCAP + h];
+      int g = 0;
+      for (; g + 4 <= NG; g += 4) {
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __ldcg(part + (int64_t)(g + k) * wk.HCAP + h);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c += v[k];
+      }
+      for (; g < NG; ++g) c += __ldcg(part + (int64_t)g * wk.HCAP + h);
     }
     costs[h] = c;
   }
