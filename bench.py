@@ -507,7 +507,8 @@ def main():
     roof = {"bound": "fp32", "kernel": "k_score", "achieved": achieved, "peak": round(fp32_peak, 2),
             "unit": "TFLOP/s", "frac": (achieved / fp32_peak) if achieved else None,
             "peak_source": "derived SMs*128*2*sm_max_mhz (MEASURED_PEAKS.json has no FP32 entry)",
-            "flop_per_eval": FLOP_PER_EVAL, "traffic": traffic,
+            "flop_per_eval": FLOP_PER_EVAL,
+            "traffic": traffic["dram_bytes_per_launch"] if traffic else None, "traffic_detail": traffic,
             "evals_per_s_kernel": (evals_per_step * args.steps) / (score_ms / 1000.0) if score_ms else None,
             "score_share_of_step": (score_ms / ms) if ms else None,
             "score_launches": score_launches}

@@ -343,10 +343,8 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
     if ((rc = ensure_host(c, host_bytes))) return rc;
     char* hp = (char*)c->h_pinned;
     QState* h_qs = (QState*)hp;
-    int* h_active = (int*)(hp + Qn * sizeof(QState));
     // the pinned staging buffer is reused across chunks: previous copies finished at the last sync
     std::memcpy(h_qs, hq.data(), Qn * sizeof(QState));
-    for (int i = 0; i < Qn; ++i) h_active[i] = i;
     wk = Work();
     wk.qs = (QState*)c->qs.p;
     wk.active_list = (int*)c->active.p;
@@ -369,12 +367,16 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
     wk.item_cap = item_cap;
     wk.split_rank = 0;
     wk.split_size = 1;
-    VL_CUDA(c, cudaMemcpyAsync(wk.qs, h_qs, Qn * sizeof(QState), cudaMemcpyHostToDevice, st));
-    VL_CUDA(c, cudaMemcpyAsync(wk.active_list, h_active, Qn * sizeof(int), cudaMemcpyHostToDevice, st));
-    VL_CUDA(c, cudaMemsetAsync(wk.item_count, 0, 2 * sizeof(int), st));
+    // k_prep pulls the states from the mapped staging buffer itself: no
+    // copy-engine transfer on this stream (it would queue behind a concurrent
+    // bulk host-to-device prefetch, see posest.ransac_pnp_host)
+    QState* d_hqs = nullptr;
+    VL_CUDA(c, cudaHostGetDevicePointer((void**)&d_hqs, h_qs, 0));
+    VL_CUDA(c, cudaHostGetDevicePointer((void**)&wk.host_count,
+                                        (char*)c->h_pinned + c->h_pinned_cap - 16, 0));
     c->prof_stream = st;
     prof_hook(c, kStagePrep, true);
-    c->launches += launch_prep(wk, in, Qn, st);
+    c->launches += launch_prep(wk, in, Qn, d_hqs, st);
     prof_hook(c, kStagePrep, false);
     if ((rc = check_launch(c))) return rc;
   }
@@ -383,8 +385,9 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
 
 // Reads back the active-query count after a round (the one host sync per round).
 static int read_active(vl_ctx* c, const Work& wk, cudaStream_t st, int* nactive) {
-  int* h_count = (int*)((char*)c->h_pinned + c->h_pinned_cap - 16);
-  VL_CUDA(c, cudaMemcpyAsync(h_count, wk.active_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+  // k_active mirrors the count into this mapped pinned word
+  volatile int* h_count = (volatile int*)((char*)c->h_pinned + c->h_pinned_cap - 16);
+  if (!wk.host_count) VL_CUDA(c, cudaMemcpyAsync((void*)h_count, wk.active_count, sizeof(int), cudaMemcpyDeviceToHost, st));
   VL_CUDA(c, cudaStreamSynchronize(st));
   prof_collect(c);
   *nactive = *h_count;

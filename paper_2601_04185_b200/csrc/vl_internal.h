@@ -75,6 +75,7 @@ struct Work {
   int B, HCAP, NSPLIT;
   int64_t item_cap;
   int split_rank, split_size;  // hypothesis-split mode: scoring items dealt round-robin
+  int* host_count;       // mapped pinned mirror of *active_count (nullable)
 };
 
 struct Inputs {
@@ -95,7 +96,7 @@ struct Outputs {
 };
 
 // ---- launchers (return number of kernels launched) -------------------------
-int launch_prep(const Work& wk, const Inputs& in, int Q, cudaStream_t st);
+int launch_prep(const Work& wk, const Inputs& in, int Q, const QState* host_qs, cudaStream_t st);
 // profiling stages (vl_profile_read order)
 enum { kStagePrep = 0, kStageSample, kStageP3P, kStageCompact, kStageScore, kStageScan, kStageActive,
        kStageFinal, kStageLift, kNumStages };

@@ -20,8 +20,23 @@
 namespace vl {
 
 // ------------------------------------------------------------------ prep
-__global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in) {
+// The per-query states come straight from the mapped pinned staging buffer
+// (kernel loads over PCIe, not a copy-engine transfer, so a chunk never waits
+// behind the host pipeline's bulk prefetch of the next chunk's matches).
+__global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* __restrict__ host_qs) {
   QState& S = wk.qs[blockIdx.x];
+  if (host_qs) {
+    constexpr int kWords = sizeof(QState) / 4;
+    static_assert(sizeof(QState) % 4 == 0, "QState word copy");
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(host_qs + blockIdx.x);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&S);
+    for (int i = threadIdx.x; i < kWords; i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x == 0) {
+      wk.active_list[blockIdx.x] = blockIdx.x;
+      if (blockIdx.x == 0) wk.item_count[0] = wk.item_count[1] = 0;
+    }
+    __syncthreads();
+  }
   const int64_t off = S.off, so = S.sub_off;
   const int stride = S.stride, nsub = S.nsub;
   const double cx = S.in.cx, cy = S.in.cy;
@@ -40,8 +55,8 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in) {
   }
 }
 
-int launch_prep(const Work& wk, const Inputs& in, int Q, cudaStream_t st) {
-  k_prep<<<Q, 256, 0, st>>>(wk, in);
+int launch_prep(const Work& wk, const Inputs& in, int Q, const QState* host_qs, cudaStream_t st) {
+  k_prep<<<Q, 256, 0, st>>>(wk, in, host_qs);
   return 1;
 }
 
@@ -494,6 +509,7 @@ __global__ void __launch_bounds__(1024) k_active(Work wk, int nactive) {
   }
   if (threadIdx.x == 0) {
     *wk.active_count = running;
+    if (wk.host_count) *(volatile int*)wk.host_count = running;  // mapped pinned: read after the stream sync
     wk.item_count[0] = 0;  // items appended next round
     wk.item_count[1] = 0;  // scoring work cursor
   }

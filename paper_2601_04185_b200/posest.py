@@ -213,14 +213,34 @@ def _estimates_from(out, offsets) -> list[PoseEstimate]:
     return res
 
 
-def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chunk_queries: int = 256):
+def _host_chunks(Q: int, chunk_queries=None):
+    """Query chunks of the host pipeline.
+
+    Fixed ``chunk_queries`` gives equal chunks.  The default is a doubling
+    schedule (Q/16, Q/8, Q/4, ... , rest): only the first, small chunk's copy
+    is exposed, each chunk's estimation covers the next chunk's (twice as
+    large) host-to-device copy, and the bulk of the queries still run in
+    large, well-occupied batches.
+    """
+    if chunk_queries:
+        return [(q0, min(Q, q0 + chunk_queries)) for q0 in range(0, Q, chunk_queries)]
+    chunks, q0, size = [], 0, max(1, -(-Q // 16))
+    while q0 < Q:
+        q1 = Q if Q - q0 < 3 * size else q0 + size  # fold a short remainder into the last chunk
+        chunks.append((q0, q1))
+        q0, size = q1, 2 * size
+    return chunks
+
+
+def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chunk_queries=None):
     """Batched estimator on HOST buffers: H2D copy, device run, D2H of the results.
 
     ``px``/``X``/``w`` are packed host arrays (numpy, or pinned torch CPU
-    tensors for full-bandwidth copies).  Queries are processed in chunks on
-    the caller's stream while a second stream copies the next chunk's
-    matches to HBM and the previous chunk's results back (double-buffered,
-    event-ordered), so PCIe traffic overlaps estimation.  Returns a dict of
+    tensors for full-bandwidth copies).  Queries are processed in chunks
+    (``_host_chunks``) on the caller's stream while a second stream copies
+    the next chunk's matches to HBM and the previous chunk's results back
+    (double-buffered, event-ordered), so PCIe traffic overlaps estimation.
+    Returns a dict of
     numpy arrays (q, t, flags, count, score, iterations, converged, stats) and
     the byte counts moved each way.
     """
@@ -240,7 +260,7 @@ def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chu
     comp = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
     dev = torch.device("cuda", torch.cuda.current_device())
-    chunks = [(q0, min(Q, q0 + chunk_queries)) for q0 in range(0, Q, chunk_queries)]
+    chunks = _host_chunks(Q, chunk_queries)
     max_rows = max(int(offsets[b] - offsets[a]) for a, b in chunks)
     bufs = [[torch.empty((max_rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in host_in]
             for _ in range(min(2, len(chunks)))]

@@ -93,3 +93,14 @@ def test_seeding_matches_numpy(hc, seed):
     st = np.random.PCG64(seed).state["state"]
     assert (int(out[0]) << 64) | int(out[1]) == st["state"]
     assert (int(out[2]) << 64) | int(out[3]) == st["inc"]
+
+
+def test_host_chunk_schedule():
+    from paper_2601_04185_b200.posest import _host_chunks
+    for Q in (1, 2, 5, 16, 17, 100, 1000, 4097):
+        ch = _host_chunks(Q)
+        assert ch[0][0] == 0 and ch[-1][1] == Q
+        assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
+        assert all(b > a for a, b in ch)
+    assert _host_chunks(1000) == [(0, 63), (63, 189), (189, 441), (441, 1000)]
+    assert _host_chunks(10, 4) == [(0, 4), (4, 8), (8, 10)]
