@@ -207,7 +207,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-i", str(self.gpu), "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                 "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -249,6 +249,30 @@ class ClockSampler:
                 "power_w_max": max(pw) if pw else None, "samples": len(sm)}
 
 
+# ----------------------------------------------------------------------------- timed regions
+def timed_region(ctx, stream, sync_all, step, steps, profile):
+    """Time `steps` calls of `step` with CUDA events on `stream` (barrier + sync
+    on both sides).  profile=False is the reported measurement; profile=True
+    repeats it with the library's per-stage CUDA events (stage breakdown and the
+    scoring kernel's live launch time for the roofline).  Returns (ms,
+    launches, stage profile or None, clocks)."""
+    import torch
+    ctx.profile(bool(profile))
+    l0 = ctx.launches()
+    sync_all()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        sync_all()
+    launches = ctx.launches() - l0
+    prof = ctx.profile_read() if profile else None
+    ctx.profile(False)
+    return e0.elapsed_time(e1), launches, prof, clk.summary()
+
+
 # ----------------------------------------------------------------------------- GPU arm: lifted
 def run_lift_bench(args, wl, rank, world, local, dist):
     """C2 / C5: a step = lift (gate + depth decode + unproject) + batched LO-RANSAC
@@ -282,20 +306,12 @@ def run_lift_bench(args, wl, rank, world, local, dist):
     evals_per_step = int(stats[:, 2].sum())
     matches = int(offsets[-1])
     conv_rate = float(out["converged"].float().mean().item())
-    ctx.profile(True)
-    l0 = ctx.launches()
-    sync_all()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            out, run, offsets, _ = plan.run_device(cfg, seeds)
-        e1.record(stream)
-        sync_all()
-    launches = ctx.launches() - l0
-    prof = ctx.profile_read()
-    ctx.profile(False)
-    ms = e0.elapsed_time(e1)
+    def step():
+        plan.run_device(cfg, seeds)
+
+    ms, launches, _, clocks = timed_region(ctx, stream, sync_all, step, args.steps, False)
+    ms_prof, _, prof, _ = timed_region(ctx, stream, sync_all, step, args.steps, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     ev = torch.tensor([float(evals_per_step)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -336,6 +352,7 @@ def run_lift_bench(args, wl, rank, world, local, dist):
     score_ms, score_launches = prof["score"]
     lift_ms, lift_launches = prof["lift"]
     achieved = (evals_per_step * args.steps * FLOP_PER_EVAL) / (score_ms / 1e3) / 1e12 if score_ms else None
+    ms = ms_prof  # shares below are of the profiled region
     # lift algorithmic bytes per step: IMLC record 12 B/cell (f32 fields), depth taps, 52 B per match out
     tap_bytes = {"f32": 5, "f16": 3, "u8": 1}[wl["depth"]]
     lift_bytes = 12 * plan.cells + matches * (52 + 2.5 * tap_bytes)
@@ -366,8 +383,9 @@ def run_lift_bench(args, wl, rank, world, local, dist):
                        "l2": f"fields {plan.field_bytes / 1e9:.2f} GB/GPU",
                        "parallelism": f"query-sharded x{world}, no collective"},
             "queries_per_s": qps, "converged_frac": conv_rate, "e2e": e2e, "roofline": roof,
-            "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
+            "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
             "stage_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in prof.items()},
+            "profiled_ms_per_step": ms_prof / args.steps,
         }
         print(json.dumps(line), flush=True)
 
@@ -437,22 +455,13 @@ def main():
     evals_per_step = int(stats0[:, 2].sum())
     conv_rate = float(out["converged"].float().mean().item())
 
-    # ---- device-resident timed region (value)
-    ctx.profile(True)
-    l0 = ctx.launches()
-    sync_all()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            out = ransac_pnp_device(px_d, X_d, w_d, offsets, intr, seeds, cfg, out=out)
-        e1.record(stream)
-        sync_all()
-    launches = ctx.launches() - l0
-    prof = ctx.profile_read()
-    ctx.profile(False)
-    ms = e0.elapsed_time(e1)
+    # ---- device-resident timed region (value), then the same steps profiled
+    def step():
+        ransac_pnp_device(px_d, X_d, w_d, offsets, intr, seeds, cfg, out=out)
+
+    ms, launches, _, clocks = timed_region(ctx, stream, sync_all, step, args.steps, False)
+    ms_prof, _, prof, _ = timed_region(ctx, stream, sync_all, step, args.steps, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_local = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
@@ -510,7 +519,7 @@ def main():
             "flop_per_eval": FLOP_PER_EVAL,
             "traffic": traffic["dram_bytes_per_launch"] if traffic else None, "traffic_detail": traffic,
             "evals_per_s_kernel": (evals_per_step * args.steps) / (score_ms / 1000.0) if score_ms else None,
-            "score_share_of_step": (score_ms / ms) if ms else None,
+            "score_share_of_step": (score_ms / ms_prof) if ms_prof else None,
             "score_launches": score_launches}
 
     cpu = None
@@ -534,7 +543,8 @@ def main():
                        "parallelism": f"query-sharded x{world}, no collective"},
             "queries_per_s": queries_per_s, "converged_frac": conv_rate,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
-            "clocks": clk.summary(), "gpu_launches": launches, "stage_ms_per_step": stage_ms,
+            "clocks": clocks, "gpu_launches": launches, "stage_ms_per_step": stage_ms,
+            "profiled_ms_per_step": ms_prof / args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -166,18 +166,60 @@ int vl_p3p_solve_batch(vl_ctx* ctx, const double* bearings, const double* points
 int vl_sample_minimal_sets(vl_ctx* ctx, vl_pcg64_state* st, int64_t n, int32_t count,
                            int32_t* out, void* stream);
 
+/* ---- IMLC correspondence-field files (matchio.py:9-20, read_field :158-200) */
+enum {
+  VL_IMLC_OK = 0,
+  VL_IMLC_MAGIC = 1,     /* FieldMagicError, offset 0 */
+  VL_IMLC_VERSION = 2,   /* FieldVersionError, offset 4 */
+  VL_IMLC_TRUNCATED = 3, /* FieldTruncatedError: need `need` bytes for `what`, have `have` */
+  VL_IMLC_TRAILING = 4   /* FieldFormatError: `have` trailing bytes after the records */
+};
+
+/* Parsed header of one little-endian IMLC blob.  Byte ranges are relative to
+ * the blob start; records are grid_h*grid_w x (target_x f32, target_y f32,
+ * conf f32), row-major, starting at records_off (not necessarily aligned). */
+typedef struct {
+  int32_t status;         /* VL_IMLC_* */
+  uint32_t version;       /* as read (VL_IMLC_VERSION reports it) */
+  int64_t error_offset;   /* FieldFormatError.offset */
+  int64_t need, have;     /* truncation / trailing-byte details */
+  const char* what;       /* static string: the field being read when truncated */
+  uint8_t magic[4];       /* as read (VL_IMLC_MAGIC reports it) */
+  uint32_t grid_w, grid_h;
+  double scale_x, scale_y;
+  int64_t source_off, source_len, target_off, target_len;
+  int64_t records_off;
+} vl_imlc_header;
+
+/* Host-only header parse with read_field's validation order and error
+ * offsets (matchio.py:160-190).  Returns VL_OK when the call itself worked
+ * (the blob's verdict is out->status), VL_ERR_INVALID on null arguments.
+ * Record CONTENT (confidence finite in [0,1], finite targets where conf > 0;
+ * matchio.py:99-109) is validated on the GPU by vl_lift (VL_LIFT_IMLC). */
+int vl_imlc_parse(const uint8_t* blob, int64_t len, vl_imlc_header* out);
+
 /* ---- depth lifting (localizer.lift, localizer.py:134-197) -------------- */
 /* One correspondence field, in output order (entry id, then db->query
  * (direction 0, direct depth lookup) before query->db (direction 1,
- * bilinear depth)).  Arrays DEVICE; targets (gh,gw,2), confidence (gh,gw)
- * in f32 (file-backed IMLC) or f64 (in-memory) — one dtype per call. */
+ * bilinear depth)).  layout VL_LIFT_PLANAR: targets (gh,gw,2) and confidence
+ * (gh,gw) arrays in f32 (file-backed) or f64 (in-memory) — one dtype per
+ * call (field_f64).  layout VL_LIFT_IMLC: `targets` points at the IMLC
+ * records (12-byte (x, y, conf) f32 triples, 4-byte aligned), `confidence`
+ * is ignored; the records may live in HBM or in mapped pinned host memory.
+ * Arrays are DEVICE-accessible pointers. */
+enum { VL_LIFT_PLANAR = 0, VL_LIFT_IMLC = 1 };
 typedef struct {
   int32_t query, entry, direction, depth; /* depth: index into the vl_lift_depth array */
   int32_t grid_w, grid_h;
+  int32_t layout, _pad;
   double scale_x, scale_y;                /* cell -> pixel (matchio.py:83-84) */
   const void* targets;
   const void* confidence;
 } vl_lift_segment;
+
+/* Per-segment content verdict of VL_LIFT_IMLC segments (vl_lift seg_flags):
+ * the first violated rule in CorrespondenceField.__post_init__ order. */
+enum { VL_FIELD_BAD_CONF = 1, VL_FIELD_BAD_TARGET = 2 };
 
 /* A database entry's stored depth + camera.  kind: 0 f32 values + valid,
  * 1 f16 values + valid, 2 u8 log codes, 3 u16 log codes (code 0 invalid;
@@ -196,11 +238,13 @@ typedef struct {
  * mode 0 = lift, mode 1 = confidence gate only (matchio.filter_matches_arrays,
  * outputs px = source px, X = (target x, target y, flat cell index)).
  * Outputs DEVICE (capacity rows); seg_offsets HOST [nseg+1] receives the
- * exclusive output offset of every segment (last = total matches). */
+ * exclusive output offset of every segment (last = total matches);
+ * seg_flags HOST [nseg] (nullable) receives the VL_FIELD_* content verdict
+ * of every IMLC segment (0 = valid; always 0 for planar segments). */
 int vl_lift(vl_ctx* ctx, const vl_lift_segment* segs, int32_t nseg, const vl_lift_depth* depths,
             int32_t ndepth, int32_t field_f64, double threshold, int32_t mode, double* px_out,
             double* X_out, double* w_out, int32_t* entry_out, int64_t capacity, int64_t* seg_offsets,
-            void* stream);
+            int32_t* seg_flags, void* stream);
 
 /* replaces localizer.interp_depth_many (localizer.py:87-115): pts DEVICE
  * [n,2] depth-map subpixels; vals DEVICE [n] (0 where invalid), ok DEVICE [n]. */

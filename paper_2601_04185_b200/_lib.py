@@ -51,10 +51,33 @@ class RansacOut(C.Structure):
                 ("converged", C.c_void_p), ("stats", C.c_void_p)]
 
 
+LIFT_PLANAR, LIFT_IMLC = 0, 1
+FIELD_BAD_CONF, FIELD_BAD_TARGET = 1, 2
+
+
 class LiftSegment(C.Structure):
     _fields_ = [("query", C.c_int32), ("entry", C.c_int32), ("direction", C.c_int32), ("depth", C.c_int32),
-                ("grid_w", C.c_int32), ("grid_h", C.c_int32), ("scale_x", C.c_double), ("scale_y", C.c_double),
+                ("grid_w", C.c_int32), ("grid_h", C.c_int32), ("layout", C.c_int32), ("_pad", C.c_int32),
+                ("scale_x", C.c_double), ("scale_y", C.c_double),
                 ("targets", C.c_void_p), ("confidence", C.c_void_p)]
+
+
+# numpy view of an array of vl_lift_segment (vectorised segment tables)
+LIFT_SEGMENT_DTYPE = np.dtype([("query", "<i4"), ("entry", "<i4"), ("direction", "<i4"), ("depth", "<i4"),
+                               ("grid_w", "<i4"), ("grid_h", "<i4"), ("layout", "<i4"), ("_pad", "<i4"),
+                               ("scale_x", "<f8"), ("scale_y", "<f8"), ("targets", "<u8"),
+                               ("confidence", "<u8")])
+assert LIFT_SEGMENT_DTYPE.itemsize == C.sizeof(LiftSegment)
+
+IMLC_OK, IMLC_MAGIC, IMLC_VERSION, IMLC_TRUNCATED, IMLC_TRAILING = 0, 1, 2, 3, 4
+
+
+class ImlcHeader(C.Structure):
+    _fields_ = [("status", C.c_int32), ("version", C.c_uint32), ("error_offset", C.c_int64),
+                ("need", C.c_int64), ("have", C.c_int64), ("what", C.c_char_p), ("magic", C.c_uint8 * 4),
+                ("grid_w", C.c_uint32), ("grid_h", C.c_uint32), ("scale_x", C.c_double), ("scale_y", C.c_double),
+                ("source_off", C.c_int64), ("source_len", C.c_int64), ("target_off", C.c_int64),
+                ("target_len", C.c_int64), ("records_off", C.c_int64)]
 
 
 class LiftDepth(C.Structure):
@@ -105,8 +128,10 @@ def lib():
                                      ip, ip, dp, ip, vp]
         L.vl_p3p_solve_batch.argtypes = [vp, vp, vp, i32, vp, vp, vp, ip, vp]
         L.vl_sample_minimal_sets.argtypes = [vp, C.POINTER(PCG64State), i64, i32, vp, vp]
-        L.vl_lift.argtypes = [vp, C.POINTER(LiftSegment), i32, C.POINTER(LiftDepth), i32, i32, dbl, i32,
-                              vp, vp, vp, vp, i64, C.POINTER(C.c_int64), vp]
+        L.vl_lift.argtypes = [vp, vp, i32, C.POINTER(LiftDepth), i32, i32, dbl, i32,
+                              vp, vp, vp, vp, i64, C.POINTER(C.c_int64), C.POINTER(C.c_int32), vp]
+        L.vl_imlc_parse.argtypes = [vp, i64, C.POINTER(ImlcHeader)]
+        L.vl_imlc_parse.restype = C.c_int
         L.vl_interp_depth.argtypes = [vp, C.POINTER(LiftDepth), vp, i64, vp, vp, vp]
         L.vl_decode_depth.argtypes = [vp, C.POINTER(LiftDepth), vp, vp, vp]
         L.vl_robust_cost.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, i32, dbl, dp, vp]
@@ -134,7 +159,7 @@ EXPORTED_SYMBOLS = (
     "vl_ransac_pnp", "vl_msac_score", "vl_refine_pose", "vl_p3p_solve_batch",
     "vl_sample_minimal_sets", "vl_profile", "vl_profile_read", "vl_lift", "vl_interp_depth",
     "vl_decode_depth", "vl_robust_cost", "vl_pose_residuals", "vl_ransac_begin", "vl_ransac_partial_bytes",
-    "vl_ransac_step_score", "vl_ransac_step_finish", "vl_ransac_end",
+    "vl_ransac_step_score", "vl_ransac_step_finish", "vl_ransac_end", "vl_imlc_parse",
 )
 
 STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final", "lift")

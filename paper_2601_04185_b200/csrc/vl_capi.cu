@@ -631,7 +631,7 @@ static_assert(sizeof(vl_lift_depth) == sizeof(vl::LiftDepth), "depth layout");
 extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, const vl_lift_depth* depths,
                        int32_t ndepth, int32_t field_f64, double threshold, int32_t mode, double* px_out,
                        double* X_out, double* w_out, int32_t* entry_out, int64_t capacity,
-                       int64_t* seg_offsets, void* stream) {
+                       int64_t* seg_offsets, int32_t* seg_flags, void* stream) {
   if (!c || nseg < 0 || (nseg > 0 && !segs) || !seg_offsets || (mode != 0 && mode != 1))
     return fail(c, VL_ERR_INVALID, "bad argument");
   if (!(threshold >= 0 && threshold <= 1))
@@ -645,8 +645,14 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
   int64_t nblk = 0;
   for (int s = 0; s < nseg; ++s) {
     const vl_lift_segment& S = segs[s];
-    if (S.grid_w <= 0 || S.grid_h <= 0 || !S.targets || !S.confidence)
+    if (S.grid_w <= 0 || S.grid_h <= 0 || !S.targets || (S.layout == VL_LIFT_PLANAR && !S.confidence))
       return fail(c, VL_ERR_INVALID, "segment " + std::to_string(s) + ": empty grid or null arrays");
+    if (S.layout != VL_LIFT_PLANAR && S.layout != VL_LIFT_IMLC)
+      return fail(c, VL_ERR_INVALID, "segment " + std::to_string(s) + ": bad layout");
+    if (S.layout == VL_LIFT_IMLC && ((uintptr_t)S.targets & 3))
+      return fail(c, VL_ERR_INVALID, "segment " + std::to_string(s) + ": IMLC records must be 4-byte aligned");
+    if ((int64_t)S.grid_w * S.grid_h > INT32_MAX)
+      return fail(c, VL_ERR_INVALID, "segment " + std::to_string(s) + ": grid too large");
     if (mode == 0 && (S.depth < 0 || S.depth >= ndepth))
       return fail(c, VL_ERR_INVALID, "segment " + std::to_string(s) + ": bad depth index");
     if (S.direction != 0 && S.direction != 1) return fail(c, VL_ERR_INVALID, "bad direction");
@@ -660,18 +666,27 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
         return fail(c, VL_ERR_INVALID, "depth " + std::to_string(d) + ": bad map");
     }
   const size_t seg_bytes = nseg * sizeof(vl_lift_segment), dep_bytes = (mode == 0 ? ndepth : 0) * sizeof(vl_lift_depth);
-  const size_t meta = seg_bytes + dep_bytes + nseg * sizeof(int64_t) + 64;
+  const size_t meta = seg_bytes + dep_bytes + nseg * sizeof(int64_t);  // all multiples of 8
+  const size_t host_bytes = meta + (nseg + 1) * sizeof(int64_t) + nseg * sizeof(int) + 64;
   int rc;
-  if ((rc = ensure(c, c->lift_meta, meta)) || (rc = ensure(c, c->lift_blk_count, nblk * sizeof(int))) ||
+  if ((rc = ensure(c, c->lift_meta, meta + nseg * sizeof(int))) || (rc = ensure(c, c->lift_blk_count, nblk * sizeof(int))) ||
       (rc = ensure(c, c->lift_blk_off, nblk * sizeof(int64_t))) || (rc = ensure(c, c->lift_seg_off, (nseg + 1) * sizeof(int64_t))) ||
-      (rc = ensure_host(c, meta + (nseg + 1) * sizeof(int64_t))))
+      (rc = ensure_host(c, host_bytes)))
     return rc;
   char* h = (char*)c->h_pinned;
   std::memcpy(h, segs, seg_bytes);
   if (dep_bytes) std::memcpy(h + seg_bytes, depths, dep_bytes);
   std::memcpy(h + seg_bytes + dep_bytes, blk0.data(), nseg * sizeof(int64_t));
   char* d = (char*)c->lift_meta.p;
-  VL_CUDA(c, cudaMemcpyAsync(d, h, seg_bytes + dep_bytes + nseg * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  int64_t* hoff = (int64_t*)(h + meta);
+  int* hflags = (int*)(h + meta + (nseg + 1) * sizeof(int64_t));
+  void *d_h = nullptr, *d_hoff = nullptr, *d_hflags = nullptr;
+  VL_CUDA(c, cudaHostGetDevicePointer(&d_h, h, 0));
+  VL_CUDA(c, cudaHostGetDevicePointer(&d_hoff, hoff, 0));
+  VL_CUDA(c, cudaHostGetDevicePointer(&d_hflags, hflags, 0));
+  // metadata pulled by a kernel from mapped pinned memory and results pushed
+  // back the same way: no copy-engine transfers queued on this stream
+  c->launches += launch_lift_prep(d, d_h, meta, (int*)(d + meta), nseg, st);
   LiftArgs a;
   a.segs = (const LiftSeg*)d;
   a.nseg = nseg;
@@ -681,6 +696,9 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
   a.blk_count = (int*)c->lift_blk_count.p;
   a.blk_off = (int64_t*)c->lift_blk_off.p;
   a.seg_off = (int64_t*)c->lift_seg_off.p;
+  a.seg_flags = (int*)(d + meta);
+  a.seg_off_host = (int64_t*)d_hoff;
+  a.seg_flags_host = (int*)d_hflags;
   a.threshold = threshold;
   a.px_out = px_out;
   a.X_out = X_out;
@@ -692,10 +710,9 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
   c->launches += launch_lift(a, field_f64, mode, st);
   prof_hook(c, kStageLift, false);
   if ((rc = check_launch(c))) return rc;
-  int64_t* hoff = (int64_t*)(h + meta);
-  VL_CUDA(c, cudaMemcpyAsync(hoff, a.seg_off, (nseg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   VL_CUDA(c, cudaStreamSynchronize(st));
   std::memcpy(seg_offsets, hoff, (nseg + 1) * sizeof(int64_t));
+  if (seg_flags) std::memcpy(seg_flags, hflags, nseg * sizeof(int));
   if (hoff[nseg] > capacity)
     return fail(c, VL_ERR_INVALID, "output capacity " + std::to_string(capacity) + " < " + std::to_string(hoff[nseg]) + " matches");
   if (!px_out || !X_out || !w_out) return fail(c, VL_ERR_INVALID, "null output array");

@@ -9,9 +9,12 @@
 //
 // Output order is the reference's: segments in the caller's order (entry id,
 // then db->query before query->db), cells row-major inside a segment.
-// Three kernels: per-block keep counts -> one-CTA exclusive scan over blocks
-// -> recompute + block-local scan + write.  HBM-bound: every kept match is
-// written once (px 2 f64, X 3 f64, w f64, entry i32 = 52 B).
+// Three kernels: per-block keep counts (+ IMLC content validation) -> one-CTA
+// exclusive scan over blocks -> recompute + block-local ordered scan + write.
+// HBM-bound: every kept match is written once (px 2 f64, X 3 f64, w f64,
+// entry i32 = 52 B).  Fields are read either as planar arrays or straight
+// from IMLC records (12 B/cell, matchio.py:9-20) — in HBM or in mapped pinned
+// host memory.
 #include <climits>
 #include <cuda_fp16.h>
 #include "vl_common.cuh"
@@ -81,33 +84,70 @@ __device__ __forceinline__ void lift_point(const LiftDepth& D, double u, double 
   for (int j = 0; j < 3; ++j) X[j] = dadd(dadd(dmul(v0, D.R[j]), dmul(v1, D.R[3 + j])), dmul(v2, D.R[6 + j]));
 }
 
-template <typename T>
 struct CellResult {
-  bool keep;
   double px[2];
   double X[3];
   double w;
 };
 
-// Evaluate one cell.  mode 0: lift (keep = gate && depth ok); mode 1: gate only
-// (px = source, X[0..1] = target, X[2] = flat cell index).
+// One field cell: confidence + target, in the field's own dtype for the gate.
 template <typename T>
-__device__ __forceinline__ bool cell_eval(const LiftSeg& S, const LiftDepth* depths, int cell, T thr, int mode,
-                                          CellResult<T>& r) {
-  const T* conf = (const T*)S.confidence;
-  const T c = conf[cell];
-  // gate (matchio.py:211): (conf >= thr) & (conf > 0), compared in the field dtype
-  if (!((c >= thr) && (c > (T)0))) return false;
+struct CellIn {
+  T c;
+  double tx, ty;
+};
+
+template <typename T>
+__device__ __forceinline__ CellIn<T> load_cell(const LiftSeg& S, int cell) {
+  CellIn<T> in;
+  if (S.layout == kLayoutImlc) {
+    // IMLC record (x f32, y f32, conf f32), matchio.py:18-19
+    const float* r = (const float*)S.targets + 3 * (int64_t)cell;
+    in.c = (T)r[2];
+    in.tx = (double)r[0];
+    in.ty = (double)r[1];
+  } else {
+    const T* tg = (const T*)S.targets;
+    in.c = ((const T*)S.confidence)[cell];
+    in.tx = (double)tg[2 * (int64_t)cell];
+    in.ty = (double)tg[2 * (int64_t)cell + 1];
+  }
+  return in;
+}
+
+// gate (matchio.py:211): (conf >= thr) & (conf > 0), compared in the field
+// dtype (IMLC records are f32: T = float is exact for them)
+template <typename T>
+__device__ __forceinline__ bool gate(T c, T thr) {
+  return (c >= thr) && (c > (T)0);
+}
+
+__device__ __forceinline__ void source_px(const LiftSeg& S, int cell, double& sx, double& sy) {
   const int row = cell / S.gw, col = cell - row * S.gw;
-  const T* tg = (const T*)S.targets;
-  const double tx = (double)tg[2 * (int64_t)cell], ty = (double)tg[2 * (int64_t)cell + 1];
-  const double sx = dmul((double)col + 0.5, S.scale_x), sy = dmul((double)row + 0.5, S.scale_y);
-  r.w = (double)c;
+  sx = dmul((double)col + 0.5, S.scale_x);
+  sy = dmul((double)row + 0.5, S.scale_y);
+}
+
+__device__ __forceinline__ void direct_tap(const LiftDepth& D, double sx, double sy, int64_t& idx) {
+  const double fxi = floor(dmul(sx, D.sx_depth)), fyi = floor(dmul(sy, D.sy_depth));
+  const int ix = (int)fmin(fmax(fxi, 0.0), (double)(D.w - 1));
+  const int iy = (int)fmin(fmax(fyi, 0.0), (double)(D.h - 1));
+  idx = (int64_t)iy * D.w + ix;
+}
+
+// Evaluate one gated cell.  mode 0: lift (false when the depth is invalid);
+// mode 1: gate only (px = source, X[0..1] = target, X[2] = flat cell index).
+template <typename T>
+__device__ __forceinline__ bool cell_eval(const LiftSeg& S, const LiftDepth* depths, int cell, const CellIn<T>& in,
+                                          int mode, CellResult& r) {
+  double sx, sy;
+  source_px(S, cell, sx, sy);
+  r.w = (double)in.c;
   if (mode == 1) {
     r.px[0] = sx;
     r.px[1] = sy;
-    r.X[0] = tx;
-    r.X[1] = ty;
+    r.X[0] = in.tx;
+    r.X[1] = in.ty;
     r.X[2] = (double)cell;
     return true;
   }
@@ -115,23 +155,49 @@ __device__ __forceinline__ bool cell_eval(const LiftSeg& S, const LiftDepth* dep
   double d;
   if (S.direction == 0) {
     // db -> query: direct lookup at the db cell (localizer.py:164-168)
-    double fxi = floor(dmul(sx, D.sx_depth)), fyi = floor(dmul(sy, D.sy_depth));
-    const int ix = (int)fmin(fmax(fxi, 0.0), (double)(D.w - 1));
-    const int iy = (int)fmin(fmax(fyi, 0.0), (double)(D.h - 1));
+    int64_t idx;
+    direct_tap(D, sx, sy, idx);
     bool ok;
-    d = (double)depth_value(D, (int64_t)iy * D.w + ix, ok);
+    d = (double)depth_value(D, idx, ok);
     if (!ok) return false;
     lift_point(D, sx, sy, d, r.X);
-    r.px[0] = tx;
-    r.px[1] = ty;
+    r.px[0] = in.tx;
+    r.px[1] = in.ty;
   } else {
     // query -> db: bilinear at the subpixel target (localizer.py:181-196)
-    if (!interp_depth(D, dmul(tx, D.sx_depth), dmul(ty, D.sy_depth), d)) return false;
-    lift_point(D, tx, ty, d, r.X);
+    if (!interp_depth(D, dmul(in.tx, D.sx_depth), dmul(in.ty, D.sy_depth), d)) return false;
+    lift_point(D, in.tx, in.ty, d, r.X);
     r.px[0] = sx;
     r.px[1] = sy;
   }
   return true;
+}
+
+// Keep decision only (count pass): gate + depth validity, no lift arithmetic.
+template <typename T>
+__device__ __forceinline__ bool cell_keep(const LiftSeg& S, const LiftDepth* depths, int cell, const CellIn<T>& in,
+                                          int mode) {
+  if (mode == 1) return true;
+  const LiftDepth& D = depths[S.depth];
+  double sx, sy;
+  if (S.direction == 0) {
+    source_px(S, cell, sx, sy);
+    int64_t idx;
+    direct_tap(D, sx, sy, idx);
+    bool ok;
+    (void)depth_value(D, idx, ok);
+    return ok;
+  }
+  double d;
+  return interp_depth(D, dmul(in.tx, D.sx_depth), dmul(in.ty, D.sy_depth), d);
+}
+
+// IMLC content rules of CorrespondenceField.__post_init__ (matchio.py:99-109)
+__device__ __forceinline__ int content_flags(float c, double tx, double ty) {
+  int f = 0;
+  if (!(isfinite(c) && c >= 0.f && c <= 1.f)) f |= kFieldBadConf;
+  if (c > 0.f && !(isfinite(tx) && isfinite(ty))) f |= kFieldBadTarget;
+  return f;
 }
 
 __device__ __forceinline__ int find_seg(const int64_t* seg_blk0, int nseg, int64_t b) {
@@ -144,28 +210,43 @@ __device__ __forceinline__ int find_seg(const int64_t* seg_blk0, int nseg, int64
   return lo;
 }
 
+// A block covers kLiftBlockCells consecutive cells of one segment; iteration
+// i handles cells [i*NT, (i+1)*NT) of it, one per thread, so every load and
+// every output store of a warp touches consecutive addresses.
 template <typename T>
 __global__ void __launch_bounds__(kLiftThreads) k_lift_count(LiftArgs a, int mode) {
   const int64_t b = blockIdx.x;
   const int s = find_seg(a.seg_blk0, a.nseg, b);
   const LiftSeg S = a.segs[s];
   const int cells = S.gw * S.gh;
-  const int base = (int)(b - a.seg_blk0[s]) * kLiftBlockCells + threadIdx.x * kLiftPerThread;
-  int cnt = 0;
+  const int cb = (int)(b - a.seg_blk0[s]) * kLiftBlockCells;
+  const T thr = (T)a.threshold;
+  int cnt = 0, flags = 0;
+#pragma unroll 2
   for (int i = 0; i < kLiftPerThread; ++i) {
-    const int cell = base + i;
+    const int cell = cb + i * kLiftThreads + threadIdx.x;
     if (cell >= cells) break;
-    CellResult<T> r;
-    cnt += cell_eval<T>(S, a.depths, cell, (T)a.threshold, mode, r) ? 1 : 0;
+    const CellIn<T> in = load_cell<T>(S, cell);
+    if (S.layout == kLayoutImlc) flags |= content_flags((float)in.c, in.tx, in.ty);
+    if (gate<T>(in.c, thr) && cell_keep<T>(S, a.depths, cell, in, mode)) ++cnt;
   }
   __shared__ int wsum[kLiftThreads / 32];
+  __shared__ int wflag[kLiftThreads / 32];
   cnt = warp_sum(cnt);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+  flags = __reduce_or_sync(0xffffffffu, (unsigned)flags);
+  if ((threadIdx.x & 31) == 0) {
+    wsum[threadIdx.x >> 5] = cnt;
+    wflag[threadIdx.x >> 5] = flags;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < kLiftThreads / 32; ++w) t += wsum[w];
+    int t = 0, f = 0;
+    for (int w = 0; w < kLiftThreads / 32; ++w) {
+      t += wsum[w];
+      f |= wflag[w];
+    }
     a.blk_count[b] = t;
+    if (f && a.seg_flags) atomicOr(a.seg_flags + s, f);
   }
 }
 
@@ -197,55 +278,76 @@ __global__ void __launch_bounds__(1024) k_lift_scan(LiftArgs a) {
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
   }
-  for (int s = threadIdx.x; s < a.nseg; s += 1024) a.seg_off[s] = a.blk_off[a.seg_blk0[s]];
-  if (threadIdx.x == 0) a.seg_off[a.nseg] = carry;
+  for (int s = threadIdx.x; s < a.nseg; s += 1024) {
+    const int64_t o = a.blk_off[a.seg_blk0[s]];
+    a.seg_off[s] = o;
+    if (a.seg_off_host) a.seg_off_host[s] = o;
+    if (a.seg_flags_host) a.seg_flags_host[s] = a.seg_flags ? a.seg_flags[s] : 0;
+  }
+  if (threadIdx.x == 0) {
+    a.seg_off[a.nseg] = carry;
+    if (a.seg_off_host) a.seg_off_host[a.nseg] = carry;
+  }
+}
+
+__global__ void k_lift_prep(uint64_t* dst, const uint64_t* src, int64_t words, int* zero, int zero_n) {
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0; i < words; i += step) dst[i] = src[i];
+  for (int64_t i = i0; i < zero_n; i += step) zero[i] = 0;
+}
+
+int launch_lift_prep(void* dst, const void* src_host, size_t bytes, int* zero, int zero_n, cudaStream_t st) {
+  const int64_t words = (int64_t)(bytes / 8);
+  const int64_t n = words > zero_n ? words : zero_n;
+  const int blocks = (int)((n + 255) / 256 < 148 ? (n + 255) / 256 : 148);
+  k_lift_prep<<<blocks > 0 ? blocks : 1, 256, 0, st>>>((uint64_t*)dst, (const uint64_t*)src_host, words, zero, zero_n);
+  return 1;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kLiftThreads) k_lift_write(LiftArgs a, int mode) {
-  __shared__ int wtot[kLiftThreads / 32];
+  __shared__ int wcnt[2][kLiftThreads / 32];
   const int64_t b = blockIdx.x;
   const int s = find_seg(a.seg_blk0, a.nseg, b);
   const LiftSeg S = a.segs[s];
   const int cells = S.gw * S.gh;
-  const int base = (int)(b - a.seg_blk0[s]) * kLiftBlockCells + threadIdx.x * kLiftPerThread;
-  CellResult<T> r[kLiftPerThread];
-  unsigned keep = 0;
-  int cnt = 0;
-#pragma unroll
-  for (int i = 0; i < kLiftPerThread; ++i) {
-    const int cell = base + i;
-    if (cell < cells && cell_eval<T>(S, a.depths, cell, (T)a.threshold, mode, r[i])) {
-      keep |= 1u << i;
-      ++cnt;
-    }
-  }
-  // block-local exclusive scan (row-major order preserved)
+  const int cb = (int)(b - a.seg_blk0[s]) * kLiftBlockCells;
+  const T thr = (T)a.threshold;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int x = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wtot[wid] = x;
-  __syncthreads();
-  int wb = 0;
-  for (int w = 0; w < wid; ++w) wb += wtot[w];
-  int64_t pos = a.blk_off[b] + wb + x - cnt;
-#pragma unroll
+  const unsigned lt = (1u << lane) - 1u;
+  int64_t pos0 = a.blk_off[b];
   for (int i = 0; i < kLiftPerThread; ++i) {
-    if (!(keep >> i & 1u)) continue;
-    if (pos < a.capacity) {
-      a.px_out[2 * pos] = r[i].px[0];
-      a.px_out[2 * pos + 1] = r[i].px[1];
-      a.X_out[3 * pos] = r[i].X[0];
-      a.X_out[3 * pos + 1] = r[i].X[1];
-      a.X_out[3 * pos + 2] = r[i].X[2];
-      a.w_out[pos] = r[i].w;
-      if (a.entry_out) a.entry_out[pos] = S.entry;
+    if (cb + i * kLiftThreads >= cells) break;  // uniform across the block
+    const int cell = cb + i * kLiftThreads + threadIdx.x;
+    CellResult r;
+    bool keep = false;
+    if (cell < cells) {
+      const CellIn<T> in = load_cell<T>(S, cell);
+      keep = gate<T>(in.c, thr) && cell_eval<T>(S, a.depths, cell, in, mode, r);
     }
-    ++pos;
+    // order-preserving rank inside iteration i (row-major cell order)
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wcnt[i & 1][wid] = __popc(m);
+    __syncthreads();
+    int before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kLiftThreads / 32; ++w) {
+      const int c = wcnt[i & 1][w];
+      before += w < wid ? c : 0;
+      tot += c;
+    }
+    if (keep) {
+      const int64_t pos = pos0 + before + __popc(m & lt);
+      if (pos < a.capacity) {
+        reinterpret_cast<double2*>(a.px_out)[pos] = make_double2(r.px[0], r.px[1]);
+        a.X_out[3 * pos] = r.X[0];
+        a.X_out[3 * pos + 1] = r.X[1];
+        a.X_out[3 * pos + 2] = r.X[2];
+        a.w_out[pos] = r.w;
+        if (a.entry_out) a.entry_out[pos] = S.entry;
+      }
+    }
+    pos0 += tot;
   }
 }
 

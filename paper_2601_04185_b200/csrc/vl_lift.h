@@ -19,12 +19,16 @@ struct LiftDepth {
 };
 
 // One correspondence field in output order (device copy of vl_lift_segment).
+enum { kLayoutPlanar = 0, kLayoutImlc = 1 };
+enum { kFieldBadConf = 1, kFieldBadTarget = 2 };
+
 struct LiftSeg {
   int query, entry, direction, depth;
   int gw, gh;
+  int layout, pad;
   double scale_x, scale_y;
-  const void* targets;     // [gh*gw*2] f32 or f64
-  const void* confidence;  // [gh*gw]
+  const void* targets;     // planar: [gh*gw*2] f32 or f64; IMLC: [gh*gw*3] f32 records
+  const void* confidence;  // planar: [gh*gw]
 };
 
 struct LiftArgs {
@@ -34,8 +38,11 @@ struct LiftArgs {
   const int64_t* seg_blk0;  // [nseg] first block of each segment
   int64_t nblk;
   int* blk_count;           // [nblk]
+  int* seg_flags;           // [nseg] IMLC content verdicts (VL_FIELD_*), zeroed by the caller
   int64_t* blk_off;         // [nblk]
   int64_t* seg_off;         // [nseg+1]
+  int64_t* seg_off_host;    // [nseg+1] mapped pinned mirror (nullable)
+  int* seg_flags_host;      // [nseg]   mapped pinned mirror (nullable)
   double threshold;
   double* px_out;
   double* X_out;
@@ -44,6 +51,9 @@ struct LiftArgs {
   int64_t capacity;
 };
 
+// copies `bytes` (multiple of 8) from mapped pinned host memory and zeroes
+// zero_n ints — no copy-engine transfer on the stream
+int launch_lift_prep(void* dst, const void* src_host, size_t bytes, int* zero, int zero_n, cudaStream_t st);
 int launch_lift(const LiftArgs& a, int field_f64, int mode, cudaStream_t st);
 int launch_lift_write(const LiftArgs& a, int field_f64, int mode, cudaStream_t st);
 int lift_block_cells();

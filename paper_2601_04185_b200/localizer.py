@@ -23,6 +23,7 @@ import numpy as np
 
 from . import _lib
 from .geometry import CameraIntrinsics, Pose
+from .matchio import CorrespondenceField, FieldBlob, filter_matches_arrays  # noqa: F401
 from .posest import (Match2D3D, PoseEstimate, RansacConfig, _estimates_from, _intr_c,
                      ransac_pnp_device)
 
@@ -40,44 +41,6 @@ KIND_F32, KIND_F16, KIND_CODE8, KIND_CODE16 = 0, 1, 2, 3
 
 
 # ----------------------------------------------------------------------------- types
-@dataclass
-class CorrespondenceField:
-    """Per-cell targets (h,w,2) and confidences (h,w) (matchio.py:74-123)."""
-
-    source_id: str
-    target_id: str
-    targets: np.ndarray
-    confidence: np.ndarray
-    scale_x: float = 1.0
-    scale_y: float = 1.0
-
-    def __post_init__(self):
-        t32 = np.asarray(self.targets).dtype == np.float32
-        c32 = np.asarray(self.confidence).dtype == np.float32
-        self.targets = np.ascontiguousarray(self.targets, dtype=np.float32 if t32 else np.float64)
-        self.confidence = np.ascontiguousarray(self.confidence, dtype=np.float32 if c32 else np.float64)
-        if self.targets.ndim != 3 or self.targets.shape[2] != 2:
-            raise ValueError(f"targets must be (H, W, 2), got {self.targets.shape}")
-        if self.confidence.shape != self.targets.shape[:2]:
-            raise ValueError("confidence shape does not match targets")
-        h, w = self.confidence.shape
-        if h <= 0 or w <= 0:
-            raise ValueError(f"grid dimensions must be positive, got {w}x{h}")
-        c = self.confidence
-        if np.any(~np.isfinite(c)) or c.min() < 0 or c.max() > 1:
-            raise ValueError("confidences must be finite and within [0, 1]")
-        if np.any(~np.isfinite(self.targets[c > 0])):
-            raise ValueError("matched cells (confidence > 0) must have finite targets")
-
-    @property
-    def grid_w(self) -> int:
-        return self.confidence.shape[1]
-
-    @property
-    def grid_h(self) -> int:
-        return self.confidence.shape[0]
-
-
 @dataclass
 class DepthMap:
     """z-depth (f32) + validity at match-grid resolution (depthbuild.py:45-77)."""
@@ -274,24 +237,80 @@ def _check_span(fld, intr, what):
 
 
 class _FieldUpload:
-    """Packs many fields into two device arrays (one dtype per call)."""
+    """Device-side view of many fields for one vl_lift call.
+
+    Planar fields (CorrespondenceField-like: targets/confidence arrays) are
+    packed into two device arrays (one dtype per call: f64 if any planar
+    field is f64).  IMLC fields (``FieldBlob``) are read in place from their
+    arena's HBM mirror (one copy per arena, no repacking)."""
 
     def __init__(self, fields):
         import torch
+        planar = [f for f in fields if not isinstance(f, FieldBlob)]
         self.f64 = any(np.asarray(f.confidence).dtype != np.float32 or np.asarray(f.targets).dtype != np.float32
-                       for f in fields)
+                       for f in planar)
         dt = np.float64 if self.f64 else np.float32
-        tg = [np.ascontiguousarray(f.targets, dtype=dt).reshape(-1) for f in fields]
-        cf = [np.ascontiguousarray(f.confidence, dtype=dt).reshape(-1) for f in fields]
-        self.t_off = np.concatenate([[0], np.cumsum([a.size for a in tg])])
-        self.c_off = np.concatenate([[0], np.cumsum([a.size for a in cf])])
-        self.targets = torch.from_numpy(np.concatenate(tg) if tg else np.zeros(0, dt)).cuda()
-        self.conf = torch.from_numpy(np.concatenate(cf) if cf else np.zeros(0, dt)).cuda()
         self.item = 8 if self.f64 else 4
+        n = len(fields)
+        self.layout = np.zeros(n, dtype=np.int32)
+        self.tptr = np.zeros(n, dtype=np.uint64)
+        self.cptr = np.zeros(n, dtype=np.uint64)
+        tg, cf, where = [], [], []
+        arenas = {}
+        for i, f in enumerate(fields):
+            if isinstance(f, FieldBlob):
+                a = arenas.get(id(f.arena))
+                if a is None:
+                    a = arenas[id(f.arena)] = f.arena.device()
+                self.layout[i] = _lib.LIFT_IMLC
+                self.tptr[i] = a.data_ptr() + f.records_offset
+            else:
+                where.append(i)
+                tg.append(np.ascontiguousarray(f.targets, dtype=dt).reshape(-1))
+                cf.append(np.ascontiguousarray(f.confidence, dtype=dt).reshape(-1))
+        self.keep = list(arenas.values())
+        self.targets = self.conf = None
+        self.bytes = 0
+        if where:
+            t_off = np.concatenate([[0], np.cumsum([a.size for a in tg])]).astype(np.uint64)
+            c_off = np.concatenate([[0], np.cumsum([a.size for a in cf])]).astype(np.uint64)
+            self.targets = torch.from_numpy(np.concatenate(tg)).cuda()
+            self.conf = torch.from_numpy(np.concatenate(cf)).cuda()
+            self.tptr[where] = self.targets.data_ptr() + t_off[:-1] * self.item
+            self.cptr[where] = self.conf.data_ptr() + c_off[:-1] * self.item
+            self.bytes += int(self.targets.numel() + self.conf.numel()) * self.item
+        self.bytes += sum(12 * f.grid_w * f.grid_h for f in fields if isinstance(f, FieldBlob))
 
-    def ptrs(self, i):
-        return (self.targets.data_ptr() + int(self.t_off[i]) * self.item,
-                self.conf.data_ptr() + int(self.c_off[i]) * self.item)
+
+def _seg_table(spec, up: _FieldUpload) -> np.ndarray:
+    """vl_lift_segment array (numpy structured) for (query, entry, direction, depth, field) tuples."""
+    n = len(spec)
+    t = np.zeros(max(n, 1), dtype=_lib.LIFT_SEGMENT_DTYPE)
+    if n:
+        t["query"][:n] = [x[0] for x in spec]
+        t["entry"][:n] = [x[1] for x in spec]
+        t["direction"][:n] = [x[2] for x in spec]
+        t["depth"][:n] = [x[3] for x in spec]
+        t["grid_w"][:n] = [x[4].grid_w for x in spec]
+        t["grid_h"][:n] = [x[4].grid_h for x in spec]
+        t["scale_x"][:n] = [float(x[4].scale_x) for x in spec]
+        t["scale_y"][:n] = [float(x[4].scale_y) for x in spec]
+        t["layout"][:n] = up.layout
+        t["targets"][:n] = up.tptr
+        t["confidence"][:n] = up.cptr
+    return t
+
+
+def _call_lift(table, nseg, deps, ndep, f64, threshold, mode, px, X, w, ent, cap, offs, flags, fields):
+    ctx = _lib.context()
+    rc = _lib.lib().vl_lift(ctx.handle, table.ctypes.data, nseg, deps, ndep, 1 if f64 else 0, float(threshold),
+                            mode, px.data_ptr(), X.data_ptr(), w.data_ptr(), ent.data_ptr(), cap,
+                            offs.ctypes.data_as(C.POINTER(C.c_int64)), flags.ctypes.data_as(C.POINTER(C.c_int32)),
+                            _lib.stream_ptr())
+    ctx.check(rc, "vl_lift")
+    bad = np.nonzero(flags[:nseg])[0]
+    if bad.size:  # IMLC record content rules, checked on the GPU by the counting pass
+        raise fields[int(bad[0])].content_error(int(flags[bad[0]]))
 
 
 def _run_lift(segs_spec, depth_records, threshold, mode=0):
@@ -300,41 +319,26 @@ def _run_lift(segs_spec, depth_records, threshold, mode=0):
     import torch
     if not 0 <= threshold <= 1:
         raise ValueError(f"threshold must be in [0, 1], got {threshold}")
-    ctx = _lib.context()
+    _lib.context()
     n = len(segs_spec)
-    up = _FieldUpload([s[4] for s in segs_spec])
-    segs = (_lib.LiftSegment * max(n, 1))()
-    cap = 0
-    for i, (q, e, d, di, f) in enumerate(segs_spec):
-        s = segs[i]
-        s.query, s.entry, s.direction, s.depth = q, e, d, di
-        s.grid_w, s.grid_h = f.grid_w, f.grid_h
-        s.scale_x, s.scale_y = float(f.scale_x), float(f.scale_y)
-        s.targets, s.confidence = up.ptrs(i)
-        cap += f.grid_w * f.grid_h
+    fields = [s[4] for s in segs_spec]
+    up = _FieldUpload(fields)
+    table = _seg_table(segs_spec, up)
+    cap = max(sum(f.grid_w * f.grid_h for f in fields), 1)
     deps = (_lib.LiftDepth * max(len(depth_records), 1))(*depth_records)
-    cap = max(cap, 1)
     px = torch.empty((cap, 2), dtype=torch.float64, device="cuda")
     X = torch.empty((cap, 3), dtype=torch.float64, device="cuda")
     w = torch.empty((cap,), dtype=torch.float64, device="cuda")
     ent = torch.empty((cap,), dtype=torch.int32, device="cuda")
     offs = np.zeros(n + 1, dtype=np.int64)
-    rc = _lib.lib().vl_lift(ctx.handle, segs, n, deps, len(depth_records), 1 if up.f64 else 0, float(threshold),
-                            mode, px.data_ptr(), X.data_ptr(), w.data_ptr(), ent.data_ptr(), cap,
-                            offs.ctypes.data_as(C.POINTER(C.c_int64)), _lib.stream_ptr())
-    ctx.check(rc, "vl_lift")
+    flags = np.zeros(max(n, 1), dtype=np.int32)
+    _call_lift(table, n, deps, len(depth_records), up.f64, threshold, mode, px, X, w, ent, cap, offs, flags,
+               fields)
     tot = int(offs[-1])
     return px[:tot], X[:tot], w[:tot], ent[:tot], offs, up
 
 
 # ----------------------------------------------------------------------------- API
-def filter_matches_arrays(fld, threshold: float):
-    """(source_px (M,2), target_px (M,2), confidence (M,), flat cell index (M,)) (matchio.py:203-218)."""
-    px, X, w, _, _, _ = _run_lift([(0, 0, 0, 0, fld)], [], threshold, mode=1)
-    Xh = X.cpu().numpy()
-    return px.cpu().numpy(), Xh[:, :2].copy(), w.cpu().numpy(), Xh[:, 2].astype(np.int64)
-
-
 def dequantize_depth(q) -> DepthMap:
     """Codes -> f32 depth + validity on the GPU (mapstore.py:122-134)."""
     import torch
@@ -464,16 +468,10 @@ class LiftPlan:
         spec, recs = _plan(self.jobs, vmap, index, depth_cache, self.device_cache)
         self.nseg = len(spec)
         self.seg_q = np.array([s[0] for s in spec], dtype=np.int64)
-        self.up = _FieldUpload([s[4] for s in spec])
-        self.segs = (_lib.LiftSegment * max(self.nseg, 1))()
-        cap = 0
-        for i, (q, e, d, di, f) in enumerate(spec):
-            s = self.segs[i]
-            s.query, s.entry, s.direction, s.depth = q, e, d, di
-            s.grid_w, s.grid_h = f.grid_w, f.grid_h
-            s.scale_x, s.scale_y = float(f.scale_x), float(f.scale_y)
-            s.targets, s.confidence = self.up.ptrs(i)
-            cap += f.grid_w * f.grid_h
+        self.fields = [s[4] for s in spec]
+        self.up = _FieldUpload(self.fields)
+        self.table = _seg_table(spec, self.up)
+        cap = sum(f.grid_w * f.grid_h for f in self.fields)
         self.ndep = len(recs)
         self.deps = (_lib.LiftDepth * max(self.ndep, 1))(*recs)
         self.cap = max(cap, 1)
@@ -482,28 +480,18 @@ class LiftPlan:
         self.w = torch.empty((self.cap,), dtype=torch.float64, device="cuda")
         self.ent = torch.empty((self.cap,), dtype=torch.int32, device="cuda")
         self.offs = np.zeros(self.nseg + 1, dtype=np.int64)
+        self.flags = np.zeros(max(self.nseg, 1), dtype=np.int32)
         self.cells = cap
-        self.field_bytes = int(self.up.targets.numel() * self.up.item + self.up.conf.numel() * self.up.item)
+        self.field_bytes = self.up.bytes
 
     def lift(self):
         """Run the lift; returns per-query [start, end) match ranges (host)."""
-        ctx = _lib.context()
-        rc = _lib.lib().vl_lift(ctx.handle, self.segs, self.nseg, self.deps, self.ndep, 1 if self.up.f64 else 0,
-                                self.threshold, 0, self.px.data_ptr(), self.X.data_ptr(), self.w.data_ptr(),
-                                self.ent.data_ptr(), self.cap, self.offs.ctypes.data_as(C.POINTER(C.c_int64)),
-                                _lib.stream_ptr())
-        ctx.check(rc, "vl_lift")
-        Q = len(self.jobs)
-        start = np.zeros(Q, dtype=np.int64)
-        end = np.zeros(Q, dtype=np.int64)
-        prev = 0
-        for qi in range(Q):
-            idx = np.nonzero(self.seg_q == qi)[0]
-            if idx.size:
-                start[qi], end[qi] = self.offs[idx[0]], self.offs[idx[-1] + 1]
-                prev = end[qi]
-            else:
-                start[qi] = end[qi] = prev
+        _call_lift(self.table, self.nseg, self.deps, self.ndep, self.up.f64, self.threshold, 0, self.px, self.X,
+                   self.w, self.ent, self.cap, self.offs, self.flags, self.fields)
+        qs = np.arange(len(self.jobs))
+        # segments are in query order: first/last segment of every query
+        start = self.offs[np.searchsorted(self.seg_q, qs, "left")]
+        end = self.offs[np.searchsorted(self.seg_q, qs, "right")]
         return start, end
 
     def run_device(self, cfg: RansacConfig, seeds=None, out=None):

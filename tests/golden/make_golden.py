@@ -197,7 +197,65 @@ def lift_vectors():
     np.savez_compressed(OUT / "lift.npz", **out)
 
 
+def imlc_vectors():
+    """Reference read_field on valid and damaged IMLC blobs (matchio.py:158-200)."""
+    import json
+    import struct
+    import tempfile
+    from visloc.matchio import CorrespondenceField, FieldFormatError, read_field, write_field
+
+    rng = np.random.default_rng(5)
+    h, w = 7, 9
+    tg = rng.uniform(0, 140, (h, w, 2)).astype(np.float32)
+    cf = rng.uniform(0, 1, (h, w)).astype(np.float32)
+    cf[cf < 0.3] = 0.0
+    tg[cf == 0.0] = np.nan  # allowed: unmatched cells may carry NaN targets
+    good = CorrespondenceField("query_0007", "db_\u00e9ntry_12", tg, cf, 2.5, 3.25)
+    tmp = Path(tempfile.mkdtemp())
+    write_field(good, tmp / "good.imlc")
+    base = (tmp / "good.imlc").read_bytes()
+    rec0 = len(base) - 12 * h * w
+    cases = {"good": base}
+    for cut in (0, 2, 4, 6, 8, 10, 12, 15, 12 + 10 + 2, 12 + 10 + 4 + 3, rec0 - 20, rec0 - 1, rec0, rec0 + 5,
+                len(base) - 1):
+        cases[f"cut{cut}"] = base[:cut]
+    cases["magic"] = b"IMLD" + base[4:]
+    cases["version"] = base[:4] + struct.pack("<I", 2) + base[8:]
+    cases["trailing"] = base + b"\x00\x01\x02"
+    gw_off = rec0 - 24
+    cases["zero_grid"] = base[:gw_off] + struct.pack("<II", 0, 3) + base[gw_off + 8:rec0]
+    cases["huge_grid"] = base[:gw_off] + struct.pack("<II", 0xFFFFFFFF, 0xFFFFFFFF) + base[gw_off + 8:]
+
+    def with_rec(i, j, k, v):
+        b = bytearray(base)
+        struct.pack_into("<f", b, rec0 + 12 * (i * w + j) + 4 * k, v)
+        return bytes(b)
+    cases["conf_gt1"] = with_rec(2, 3, 2, 1.5)
+    cases["conf_neg"] = with_rec(0, 0, 2, -0.25)
+    cases["conf_nan"] = with_rec(6, 8, 2, float("nan"))
+    j0 = int(np.argmax(cf.reshape(-1) > 0))
+    cases["target_nan"] = with_rec(j0 // w, j0 % w, 0, float("nan"))
+    cases["target_inf"] = with_rec(j0 // w, j0 % w, 1, float("inf"))
+    out, names = {}, []
+    for i, (name, blob) in enumerate(cases.items()):
+        p_ = tmp / f"{i}.imlc"
+        p_.write_bytes(blob)
+        try:
+            fld = read_field(p_)
+            exp = {"name": name, "ok": True, "source_id": fld.source_id, "target_id": fld.target_id,
+                   "grid_w": fld.grid_w, "grid_h": fld.grid_h, "scale_x": fld.scale_x, "scale_y": fld.scale_y}
+            out[f"targets{i}"], out[f"conf{i}"] = fld.targets, fld.confidence
+        except FieldFormatError as exc:
+            exp = {"name": name, "ok": False, "cls": type(exc).__name__, "msg": str(exc), "offset": exc.offset}
+        out[f"blob{i}"] = np.frombuffer(blob, dtype=np.uint8)
+        out[f"expect{i}"] = np.array(json.dumps(exp))
+        names.append(name)
+    out["n"] = np.array(len(names))
+    np.savez_compressed(OUT / "imlc.npz", **out)
+
+
 if __name__ == "__main__":
+    imlc_vectors()
     lift_vectors()
     rng_vectors()
     R, t, px, X, w = p3p_vectors()
