@@ -161,12 +161,13 @@ class PlaneScene:
         return tg.astype(np.float32), conf.astype(np.float32), s
 
 
-def lifted_scene(K, Q, g, seed=0, depth_kind="f32", outlier_frac=0.7, sigma=1.0, only=None):
+def lifted_scene(K, Q, g, seed=0, depth_kind="f32", outlier_frac=0.7, sigma=1.0, only=None, fields="f64"):
     """(vmap, jobs, depth_cache) for the GPU package: K database cameras, Q query
     jobs with bidirectional fields to every database camera; depth as f32 / f16
     DepthMap (via the returned depth_cache) or u8 log codes (entry.qdepth).
     Each query draws from its own generator, so ``only=[i, ...]`` rebuilds a
-    subset identically (CPU-baseline workers)."""
+    subset identically (CPU-baseline workers).  fields="f32" holds the fields
+    as a file-backed (IMLC) field would: float32 targets and confidences."""
     from paper_2601_04185_b200.geometry import CameraIntrinsics, Pose, matrix_to_quat
     from paper_2601_04185_b200.localizer import (CorrespondenceField, DepthMap, FieldPair,
                                                  QuantizedDepthMap, QueryJob)
@@ -210,6 +211,8 @@ def lifted_scene(K, Q, g, seed=0, depth_kind="f32", outlier_frac=0.7, sigma=1.0,
         for e in entries:
             t1, c1, s = sc.field(cam, e.cam, g, rng, sigma, outlier_frac)
             t2, c2, _ = sc.field(e.cam, cam, g, rng, sigma, outlier_frac)
+            if fields == "f32":
+                t1, c1, t2, c2 = (a.astype(np.float32) for a in (t1, c1, t2, c2))
             fields[e.id] = FieldPair(query_to_db=CorrespondenceField("q", e.id, t1, c1, s, s),
                                      db_to_query=CorrespondenceField(e.id, "q", t2, c2, s, s))
         job = QueryJob(f"query{qi:04d}", intr, rng.normal(size=16), fields, k_loc=K)
