@@ -13,7 +13,10 @@ from pathlib import Path
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libvisloc_b200.so"
+import os
+
+# VISLOC_B200_LIB: alternative in-tree build of the same library (A/B kernel experiments)
+_LIB_PATH = Path(os.environ.get("VISLOC_B200_LIB", Path(__file__).resolve().parent / "_lib" / "libvisloc_b200.so"))
 
 VL_OK = 0
 VL_ERR_INVALID = 1

@@ -179,7 +179,7 @@ VL_HD bool ferrari_init(const double* b, double* zr, double* zi) {
 // Real positive roots (ascending) of sum_k c[k] v^(4-k); returns the count.
 // Mirrors np.roots' degree handling: exact leading/trailing zeros stripped,
 // zero roots never count (Re > 0 required).
-VL_HD int quartic_real_pos_roots(const double* c_in, double* out) {
+VL_HD_BIG int quartic_real_pos_roots(const double* c_in, double* out) {
   double mx = 0;
 #pragma unroll
   for (int k = 0; k < 5; ++k) mx = fmax(mx, fabs(c_in[k]));
@@ -318,7 +318,7 @@ VL_HD int quartic_real_pos_roots(const double* c_in, double* out) {
 // Distance-triple candidates (s1, s2, s3) from the roots (p3p.py:206-231),
 // in reference order.  Returns the count (<= 8); candidate k is written to
 // cand[k*stride + 0..2] unless cand is null (count only).
-VL_HD int p3p_candidates(const P3PGeo& g, const double* vs, int nv, double* cand, int stride) {
+VL_HD_BIG int p3p_candidates(const P3PGeo& g, const double* vs, int nv, double* cand, int stride) {
   int nc = 0;
   auto put = [&](double a, double b, double c) {
     if (cand) {
@@ -423,7 +423,7 @@ VL_HD void plane_frame(const double* X0, const double* X1, const double* X2, dou
 
 // Newton polish of one distance triple, then Procrustes and the bearing
 // contract.  Returns false for an invalid candidate.
-VL_HD bool p3p_polish(const P3PGeo& g, const double* s_in, double* R, double* t) {
+VL_HD_BIG bool p3p_polish(const P3PGeo& g, const double* s_in, double* R, double* t) {
   double s0 = s_in[0], s1 = s_in[1], s2 = s_in[2];
   for (int it = 0; it < kNewtonIters; ++it) {
     const double r0 = s0 * s0 + s1 * s1 - 2 * s0 * s1 * g.cg - g.c2;
