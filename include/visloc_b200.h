@@ -115,10 +115,12 @@ int vl_ransac_pnp(vl_ctx* ctx, const vl_ransac_args* args, const vl_ransac_out* 
 /* Stepwise driver of the same estimator, for the optional single-query
  * hypothesis-split mode across GPUs.  Every rank calls
  * vl_ransac_begin with identical args and its (split_rank, split_size):
- * samples, P3P and scans are replicated, the scoring work items are dealt
- * round-robin and non-owned items contribute zeros.  Per round:
- *   vl_ransac_step_score(ctx, buf)      -> this rank's partial costs into buf (DEVICE)
- *   SUM all-reduce of buf across ranks  (NCCL over NVLink; exact: one non-zero term)
+ * samples, P3P and scans are replicated, the scoring tiles (query, 256 or
+ * 768 hypotheses) are dealt round-robin and non-owned tiles hold zero costs.
+ * Per round:
+ *   vl_ransac_step_score(ctx, buf)      -> this rank's fp32 cost vector [Q][HCAP] into buf (DEVICE)
+ *   SUM all-reduce of buf across ranks  (NCCL over NVLink; exact: one non-zero term;
+ *                                        vl_ransac_partial_bytes = 4*Q*HCAP, 16 KB/query at B=1000)
  *   vl_ransac_step_finish(ctx, buf, &n) -> ordered scan / LO / stop; n active queries
  * until n == 0, then vl_ransac_end(ctx, out).  Results are bit-identical on
  * every rank and to vl_ransac_pnp.  One workspace chunk of queries. */

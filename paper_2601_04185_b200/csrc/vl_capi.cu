@@ -24,7 +24,7 @@ struct vl_ctx {
   std::string err;
   int64_t launches = 0;
   DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, P32, hsrc, items, item_count,
-      partial, sub_pk, sub32, comp_pk;
+      partial, cost32, tile_cnt, sub_pk, sub32, comp_pk;
   DevBuf scratch;  // small standalone-call scratch
   DevBuf lift_meta, lift_blk_count, lift_blk_off, lift_seg_off;  // vl_lift
   void* h_pinned = nullptr;
@@ -191,7 +191,7 @@ int vl_destroy(vl_ctx* c) {
   cudaSetDevice(c->device);
   DevBuf* bufs[] = {&c->qs,      &c->active, &c->next_active, &c->active_count, &c->samples, &c->slots,
                     &c->slot_cnt, &c->P32,   &c->hsrc,        &c->items,        &c->item_count,
-                    &c->partial, &c->sub_pk, &c->sub32,       &c->comp_pk,
+                    &c->partial, &c->cost32, &c->tile_cnt, &c->sub_pk, &c->sub32, &c->comp_pk,
                     &c->scratch, &c->lift_meta, &c->lift_blk_count,
                     &c->lift_blk_off, &c->lift_seg_off};
   for (DevBuf* b : bufs)
@@ -246,6 +246,8 @@ int vl_reserve(vl_ctx* c, int32_t max_queries, int64_t max_n_per_query, int32_t 
   rc |= ensure(c, c->P32, Qc * 12 * H * sizeof(float));
   rc |= ensure(c, c->hsrc, Qc * H * sizeof(int));
   rc |= ensure(c, c->partial, Qc * ns * H * sizeof(float));
+  rc |= ensure(c, c->cost32, Qc * H * sizeof(float));
+  rc |= ensure(c, c->tile_cnt, Qc * ((H + kScoreTileHypsFine - 1) / kScoreTileHypsFine) * sizeof(int));
   return rc ? VL_ERR_OOM : VL_OK;
 }
 
@@ -335,6 +337,8 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
         (rc = ensure(c, c->items, item_cap * sizeof(ScoreItem))) ||
         (rc = ensure(c, c->item_count, 2 * sizeof(int))) ||
         (rc = ensure(c, c->partial, (size_t)Qn * max_split * HCAP * sizeof(float))) ||
+        (rc = ensure(c, c->cost32, (size_t)Qn * HCAP * sizeof(float))) ||
+        (rc = ensure(c, c->tile_cnt, (size_t)Qn * ntile * sizeof(int))) ||
         (rc = ensure(c, c->sub_pk, nsub_tot * 3 * sizeof(double2))) ||
         (rc = ensure(c, c->sub32, nsub_tot * 2 * sizeof(float4))) ||
         (rc = ensure(c, c->comp_pk, ncomp * 3 * sizeof(double2))))
@@ -358,6 +362,9 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
     wk.items = (ScoreItem*)c->items.p;
     wk.item_count = (int*)c->item_count.p;
     wk.partial = (float*)c->partial.p;
+    wk.cost32 = (float*)c->cost32.p;
+    wk.tile_cnt = (int*)c->tile_cnt.p;
+    wk.TCAP = (int)ntile;
     wk.sub_pk = (double2*)c->sub_pk.p;
     wk.sub32 = (float4*)c->sub32.p;
     wk.comp_pk = (double2*)c->comp_pk.p;
@@ -435,9 +442,10 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
 
 // ---- stepwise driver (hypothesis-split mode) ------------------
 // Every rank runs the same queries with the same seeds (identical samples,
-// P3P and scans); the scoring work items are dealt round-robin to ranks and
-// non-owned items write zero partial sums, so a SUM all-reduce of the
-// partial-cost buffer between vl_ransac_step_score and
+// P3P and scans); the scoring tiles (query, 256/768 hypotheses) are dealt
+// round-robin to ranks, the owner computes a tile's final fp32 costs and the
+// other ranks hold zeros, so a SUM all-reduce of the [Q][HCAP] fp32 cost
+// vector (x + 0 = x exactly) between vl_ransac_step_score and
 // vl_ransac_step_finish gives every rank bit-identical costs — and the same
 // final estimate as the single-GPU path.
 int vl_ransac_begin(vl_ctx* c, const vl_ransac_args* a, int32_t split_rank, int32_t split_size, void* stream) {
@@ -465,7 +473,7 @@ int vl_ransac_begin(vl_ctx* c, const vl_ransac_args* a, int32_t split_rank, int3
 
 int vl_ransac_partial_bytes(vl_ctx* c, int64_t* bytes) {
   if (!c || !c->step.open || !bytes) return fail(c, VL_ERR_INVALID, "no open stepwise run");
-  *bytes = (int64_t)c->step.Q * c->step.wk.NSPLIT * c->step.wk.HCAP * (int64_t)sizeof(float);
+  *bytes = (int64_t)c->step.Q * c->step.wk.HCAP * (int64_t)sizeof(float);
   return VL_OK;
 }
 
@@ -477,8 +485,8 @@ int vl_ransac_step_score(vl_ctx* c, void* partial_out, void* stream) {
   int rc;
   if ((rc = check_launch(c))) return rc;
   if (partial_out) {
-    const size_t bytes = (size_t)c->step.Q * c->step.wk.NSPLIT * c->step.wk.HCAP * sizeof(float);
-    VL_CUDA(c, cudaMemcpyAsync(partial_out, c->step.wk.partial, bytes, cudaMemcpyDeviceToDevice, st));
+    const size_t bytes = (size_t)c->step.Q * c->step.wk.HCAP * sizeof(float);
+    VL_CUDA(c, cudaMemcpyAsync(partial_out, c->step.wk.cost32, bytes, cudaMemcpyDeviceToDevice, st));
   }
   return VL_OK;
 }
@@ -487,8 +495,8 @@ int vl_ransac_step_finish(vl_ctx* c, const void* partial_in, int32_t* nactive, v
   if (!c || !c->step.open || !nactive) return fail(c, VL_ERR_INVALID, "no open stepwise run");
   cudaStream_t st = (cudaStream_t)stream;
   if (partial_in) {
-    const size_t bytes = (size_t)c->step.Q * c->step.wk.NSPLIT * c->step.wk.HCAP * sizeof(float);
-    VL_CUDA(c, cudaMemcpyAsync(c->step.wk.partial, partial_in, bytes, cudaMemcpyDeviceToDevice, st));
+    const size_t bytes = (size_t)c->step.Q * c->step.wk.HCAP * sizeof(float);
+    VL_CUDA(c, cudaMemcpyAsync(c->step.wk.cost32, partial_in, bytes, cudaMemcpyDeviceToDevice, st));
   }
   c->launches += launch_round(c->step.wk, c->step.in, c->step.p, c->step.nactive, c->num_sms, st, prof_hook, c, 2);
   int rc;

@@ -68,13 +68,15 @@ struct Work {
   int* hsrc;             // [Qc][HCAP]
   ScoreItem* items;      // [item_cap]
   int* item_count;       // [0] items appended this round, [1] scoring work cursor
-  float* partial;        // [Qc][NSPLIT][HCAP]
+  float* partial;        // [Qc][NSPLIT][HCAP] split / group partial sums
+  float* cost32;         // [Qc][HCAP] final fp32 costs (written by the last item of each tile)
+  int* tile_cnt;         // [Qc][TCAP] per-round completion tickets of the scoring tiles
   double2* sub_pk;       // [Nsub][3] packed fp64 scoring subset: (X,Y) (Z,u) (v,w)
   float4* sub32;         // [Nsub][2]
   double2* comp_pk;      // [N][3] packed full-set inliers (final refinement)
-  int B, HCAP, NSPLIT;
+  int B, HCAP, NSPLIT, TCAP;
   int64_t item_cap;
-  int split_rank, split_size;  // hypothesis-split mode: scoring items dealt round-robin
+  int split_rank, split_size;  // hypothesis-split mode: scoring tiles dealt round-robin
   int* host_count;       // mapped pinned mirror of *active_count (nullable)
 };
 

@@ -343,7 +343,16 @@ __global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
   const int spi = fine ? 1 : kScoreItemSplits;
   const int ntile = (nh + tile_h - 1) / tile_h;
   const int ngroups = (S.nsplit + spi - 1) / spi;
-  const int nitems = ntile * ngroups;
+  // hypothesis-split mode: tile (q, t) belongs to rank (q*TCAP + t) mod size;
+  // the other ranks leave its costs at zero for the SUM all-reduce
+  const int size = wk.split_size;
+  const int t0 = size > 1 ? (int)((((int64_t)wk.split_rank - (int64_t)q * wk.TCAP) % size + size) % size) : 0;
+  const int nown = t0 < ntile ? (ntile - 1 - t0) / size + 1 : 0;
+  const int nitems = nown * ngroups;
+  for (int t = threadIdx.x; t < ntile; t += 1024) wk.tile_cnt[(int64_t)q * wk.TCAP + t] = 0;
+  if (size > 1)
+    for (int h = threadIdx.x; h < nh; h += 1024)
+      if ((h / tile_h) % size != t0) wk.cost32[(int64_t)q * wk.HCAP + h] = 0.f;
   if (threadIdx.x == 0) {
     S.nh = nh;
     S.hyps += nh;
@@ -354,7 +363,7 @@ __global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
   for (int i = threadIdx.x; i < nitems; i += 1024) {
     ScoreItem it;
     it.q = q;
-    it.tile = i / ngroups;
+    it.tile = t0 + (i / ngroups) * size;
     it.split = (i % ngroups) * spi;
     it.nsplit = min(spi, S.nsplit - it.split);
     const int64_t pos = (int64_t)s_item0 + i;
@@ -377,50 +386,17 @@ __device__ __forceinline__ int64_t required_iters_dev(double eps, double eta, in
 
 constexpr int kScanThreads = 256;
 
-__global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams p, int fine) {
+__global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams p) {
   extern __shared__ float costs[];
   __shared__ LMShared<kScanThreads> sm;
   __shared__ Pose s_start;
   const int q = wk.active_list[blockIdx.x / cl_size()];
   QState& S = wk.qs[q];
-  const int nh = S.nh, NS = S.nsplit;
-  const float* part = wk.partial + (int64_t)q * wk.NSPLIT * wk.HCAP;
-  // canonical fp32 cost: groups of kGroupSplits splits in order, each group
-  // summed in split order; coarse rounds stored the group sums already
-  const int NG = (NS + kGroupSplits - 1) / kGroupSplits;
+  const int nh = S.nh;
+  // final fp32 costs (canonical order, reduced by the scorer's tile tickets)
+  const float* cq = wk.cost32 + (int64_t)q * wk.HCAP;
   for (int h = threadIdx.x; h < nh; h += kScanThreads) {
-    float c = 0.f;
-    if (fine) {
-      // all loads of two groups issued before the ordered adds (memory-level parallelism)
-      for (int g = 0; g < NG; g += 2) {
-        float v[2 * kGroupSplits];
-#pragma unroll
-        for (int k = 0; k < 2 * kGroupSplits; ++k) {
-          const int s = g * kGroupSplits + k;
-          v[k] = s < NS ? __ldcg(part + (int64_t)s * wk.HCAP + h) : 0.f;
-        }
-#pragma unroll
-        for (int gg = 0; gg < 2; ++gg) {
-          const int s0 = (g + gg) * kGroupSplits;
-          if (s0 >= NS) break;
-          float gs = v[gg * kGroupSplits];
-#pragma unroll
-          for (int k = 1; k < kGroupSplits; ++k)
-            if (s0 + k < NS) gs += v[gg * kGroupSplits + k];
-          c += gs;
-        }
-      }
-    } else {
-      int g = 0;
-      for (; g + 4 <= NG; g += 4) {
-        float v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = __ldcg(part + (int64_t)(g + k) * wk.HCAP + h);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) c += v[k];
-      }
-      for (; g < NG; ++g) c += __ldcg(part + (int64_t)g * wk.HCAP + h);
-    }
+    const float c = __ldcg(cq + h);
     costs[h] = c;
   }
   __syncthreads();
@@ -574,7 +550,7 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   if (phase != 1) {
     H(kStageScan, true);
     const size_t smem = (size_t)wk.HCAP * sizeof(float);
-    launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, 2 * num_sms), st, wk, p, fine);
+    launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, 2 * num_sms), st, wk, p);
     H(kStageScan, false);
     H(kStageActive, true);
     k_active<<<1, 1024, 0, st>>>(wk, nactive);

@@ -4,71 +4,6 @@
 
 namespace vl {
 
-__device__ __forceinline__ float rsqrt_approx_ftz(float x) {
-  float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-
-// One evaluation: e = w * min(|pi(P X) - px|^2, tau^2), behind-camera -> tau^2.
-// P rows are pre-multiplied by fx / fy; a.w, b.x hold f32(cx - u), f32(cy - v).
-#define VL_SCORE_EVAL(Pj, accj)                                                       \
-  {                                                                                   \
-    const float x_ = fmaf(Pj[0], a.x, fmaf(Pj[1], a.y, fmaf(Pj[2], a.z, Pj[3])));     \
-    const float y_ = fmaf(Pj[4], a.x, fmaf(Pj[5], a.y, fmaf(Pj[6], a.z, Pj[7])));     \
-    const float z_ = fmaf(Pj[8], a.x, fmaf(Pj[9], a.y, fmaf(Pj[10], a.z, Pj[11])));   \
-    const float rs_ = rsqrt_approx_ftz(z_);                                           \
-    const float r_ = rs_ * rs_;                                                       \
-    const float du_ = fmaf(x_, r_, a.w);                                              \
-    const float dv_ = fmaf(y_, r_, b.x);                                              \
-    const float e2_ = fminf(fmaf(du_, du_, dv_ * dv_), tau2);                         \
-    accj = fmaf(b.y, e2_, accj);                                                      \
-  }
-
-// Persistent grid over work items (query, tile of NT*HT hypotheses, split of
-// CH correspondences).  Thread t owns hypotheses tile*NT*HT + j*NT + t.
-template <int NT, int HT, int CH, int MINB, int UNR>
-__global__ void __launch_bounds__(NT, MINB) k_score_t(Work wk, float tau2) {
-  __shared__ float4 rec[2 * CH];
-  const int nitems = *wk.item_count;
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const ScoreItem item = wk.items[it];
-    const QState& S = wk.qs[item.q];
-    const int nh = S.nh, nsub = S.nsub;
-    const int c0 = item.split * CH;
-    const int cn = min(CH, nsub - c0);
-    const float4* src = wk.sub32 + 2 * (S.sub_off + c0);
-    __syncthreads();
-    for (int k = threadIdx.x; k < 2 * cn; k += NT) rec[k] = src[k];
-    float P[HT][12];
-    int hid[HT];
-    const float* Pq = wk.P32 + (int64_t)item.q * 12 * wk.HCAP;
-#pragma unroll
-    for (int j = 0; j < HT; ++j) {
-      const int h = item.tile * (NT * HT) + j * NT + threadIdx.x;
-      hid[j] = h;
-      const int hc = h < nh ? h : 0;
-#pragma unroll
-      for (int c = 0; c < 12; ++c) P[j][c] = Pq[(int64_t)c * wk.HCAP + hc];
-    }
-    __syncthreads();
-    float acc[HT];
-#pragma unroll
-    for (int j = 0; j < HT; ++j) acc[j] = 0.f;
-#pragma unroll UNR
-    for (int c = 0; c < cn; ++c) {
-      const float4 a = rec[2 * c];
-      const float4 b = rec[2 * c + 1];
-#pragma unroll
-      for (int j = 0; j < HT; ++j) VL_SCORE_EVAL(P[j], acc[j]);
-    }
-    float* out = wk.partial + ((int64_t)item.q * wk.NSPLIT + item.split) * wk.HCAP;
-#pragma unroll
-    for (int j = 0; j < HT; ++j)
-      if (hid[j] < nh) out[hid[j]] = acc[j];
-  }
-}
-
 // ---------------------------------------------------------------- f32x2 path
 // Blackwell packed FP32 (FFMA2 / FMUL2): one instruction evaluates the same
 // step for two hypotheses; the correspondence coordinate is a scalar operand
@@ -107,10 +42,12 @@ __device__ __forceinline__ float rcp_approx_ftz(float x) {
 
 // Work item = (query, tile of NT*HT hypotheses, ns <= SPI consecutive
 // correspondence splits of SCH records).  The canonical fp32 cost of a
-// hypothesis is  sum over splits (in order) of  [sequential sum over the
-// split's records]  — every split is accumulated by exactly one thread in
-// record order and written to its own partial slot, so neither the tile
-// shape (HT), the splits per item (SPI) nor the grid changes a single bit.
+// hypothesis is  sum over split groups (in order) of the group sum
+// ((p0 + p1) + p2) + p3  of its splits' sequential record sums — every
+// split is accumulated by exactly one thread in record order, so neither the
+// tile shape (HT), the splits per item (SPI) nor the grid changes a single
+// bit.  The last item to finish a (query, tile) — atomic ticket per tile —
+// reduces the tile's partial slots in that order and writes the final costs.
 template <int NT, int HT, int SPI, int SCH, int MINB, int UNR>
 __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   static_assert(HT % 2 == 0, "hypotheses are processed in pairs");
@@ -120,7 +57,7 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   static_assert(SPI == 1 || SPI == kGroupSplits, "coarse items are exactly one split group");
   __shared__ float4 rec[2 * SPI * SCH];
   __shared__ float red[SPI][SPI > 1 ? NT * HT : 1];
-  __shared__ int s_it;
+  __shared__ int s_it, s_last;
   const int nitems = wk.item_count[0];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // dynamic work cursor: items differ in cost (partial tiles), and a static
@@ -139,17 +76,6 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     // partial slot layout: fine items (SPI == 1) write one slot per split;
     // coarse items write one slot per group of kGroupSplits splits, holding
     // the group sum ((p0 + p1) + p2) + p3 that k_scan forms itself in fine mode
-    if (wk.split_size > 1 && it % wk.split_size != wk.split_rank) {
-      // hypothesis-split mode: another rank owns this item; contribute zeros
-      // to the SUM all-reduce of the partial buffer
-      const int h1 = min(nh, tile0 + NT * HT);
-      const int slot0 = SPI == 1 ? item.split : item.split / kGroupSplits;
-      const int nslot = SPI == 1 ? ns : 1;
-      for (int s = 0; s < nslot; ++s)
-        for (int h = tile0 + threadIdx.x; h < h1; h += NT) outq[(int64_t)(slot0 + s) * wk.HCAP + h] = 0.f;
-      __syncthreads();  // every thread has read s_it before it is rewritten
-      continue;
-    }
     const int c0 = item.split * SCH;
     const int cn = min(ns * SCH, nsub - c0);
     const float4* src = wk.sub32 + 2 * (S.sub_off + c0);
@@ -235,6 +161,50 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
           if (hid[2 * jp] < nh) out[hid[2 * jp]] = gsum[jp].x;
           if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = gsum[jp].y;
         }
+      }
+    }
+    // ---- tile completion ticket (threadfence reduction pattern)
+    __threadfence();
+    __syncthreads();
+    const int NS = S.nsplit;
+    const int NG = (NS + kGroupSplits - 1) / kGroupSplits;
+    if (threadIdx.x == 0) {
+      const int tile_items = SPI == 1 ? NS : NG;
+      s_last = atomicAdd(wk.tile_cnt + (int64_t)item.q * wk.TCAP + item.tile, 1) == tile_items - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const int h1 = min(nh, tile0 + NT * HT);
+      float* costq = wk.cost32 + (int64_t)item.q * wk.HCAP;
+      for (int h = tile0 + threadIdx.x; h < h1; h += NT) {
+        float c = 0.f;
+        if (SPI == 1) {
+          for (int g = 0; g < NG; ++g) {
+            float v[kGroupSplits];
+#pragma unroll
+            for (int k = 0; k < kGroupSplits; ++k) {
+              const int sp = g * kGroupSplits + k;
+              v[k] = sp < NS ? __ldcg(outq + (int64_t)sp * wk.HCAP + h) : 0.f;
+            }
+            float gs = v[0];
+#pragma unroll
+            for (int k = 1; k < kGroupSplits; ++k)
+              if (g * kGroupSplits + k < NS) gs += v[k];
+            c += gs;
+          }
+        } else {
+          int g = 0;
+          for (; g + 4 <= NG; g += 4) {
+            float v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = __ldcg(outq + (int64_t)(g + k) * wk.HCAP + h);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) c += v[k];
+          }
+          for (; g < NG; ++g) c += __ldcg(outq + (int64_t)g * wk.HCAP + h);
+        }
+        costq[h] = c;
       }
     }
   }

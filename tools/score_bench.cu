@@ -1,4 +1,4 @@
-// Microbenchmark of k_score_t variants on synthetic C3-shaped data
+// Microbenchmark of k_score2_t variants on synthetic C3-shaped data
 // (Q queries x 1530 hypotheses x 10k scoring correspondences).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
 //        -I include -I paper_2601_04185_b200/csrc tools/score_bench.cu -o tools/score_bench
@@ -52,14 +52,17 @@ double run_variant(Bench& b, const char* name, std::vector<float>& ref, int reps
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  const size_t tc_bytes = (size_t)b.Q * b.wk.TCAP * sizeof(int);
   for (int r = 0; r < 2; ++r) {
     cudaMemsetAsync(b.wk.item_count + 1, 0, sizeof(int));
+    cudaMemsetAsync(b.wk.tile_cnt, 0, tc_bytes);
     kern<<<grid, NT>>>(b.wk, tau2);
   }
   CK(cudaDeviceSynchronize());
   cudaEventRecord(e0);
   for (int r = 0; r < reps; ++r) {
     cudaMemsetAsync(b.wk.item_count + 1, 0, sizeof(int));
+    cudaMemsetAsync(b.wk.tile_cnt, 0, tc_bytes);  // (k_compact does this per round)
     kern<<<grid, NT>>>(b.wk, tau2);
   }
   cudaEventRecord(e1);
@@ -68,27 +71,12 @@ double run_variant(Bench& b, const char* name, std::vector<float>& ref, int reps
   cudaEventElapsedTime(&ms, e0, e1);
   const double evals = (double)b.Q * b.nh * b.nsub * reps;
   const double eps = evals / (ms / 1e3);
-  // result check: sum partials over splits
-  std::vector<float> part((size_t)b.Q * b.NSPLIT * b.HCAP);
-  CK(cudaMemcpy(part.data(), b.wk.partial, part.size() * sizeof(float), cudaMemcpyDeviceToHost));
-  std::vector<float> costs((size_t)b.Q * b.nh);
+  // result: final costs written by the last item of every tile
+  std::vector<float> costs((size_t)b.Q * b.HCAP);
+  CK(cudaMemcpy(costs.data(), b.wk.cost32, costs.size() * sizeof(float), cudaMemcpyDeviceToHost));
   for (int q = 0; q < b.Q; ++q)
-    for (int h = 0; h < b.nh; ++h) {
-      // canonical order: group sums of 4 splits, groups in order (k_scan)
-      float c = 0.f;
-      const int ng = (nsplit + 3) / 4;
-      for (int g = 0; g < ng; ++g) {
-        float gs;
-        if (SPI == 1) {
-          gs = part[((size_t)q * b.NSPLIT + 4 * g) * b.HCAP + h];
-          for (int s = 4 * g + 1; s < nsplit && s < 4 * g + 4; ++s) gs += part[((size_t)q * b.NSPLIT + s) * b.HCAP + h];
-        } else {
-          gs = part[((size_t)q * b.NSPLIT + g) * b.HCAP + h];
-        }
-        c += gs;
-      }
-      costs[(size_t)q * b.nh + h] = c;
-    }
+    for (int h = 0; h < b.nh; ++h) costs[(size_t)q * b.nh + h] = costs[(size_t)q * b.HCAP + h];
+  costs.resize((size_t)b.Q * b.nh);
   double maxrel = 0;
   if (ref.empty()) ref = costs;
   else
@@ -144,6 +132,9 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&wk.partial, (size_t)b.Q * b.NSPLIT * b.HCAP * sizeof(float)));
   CK(cudaMalloc(&wk.items, (size_t)b.Q * 32 * b.NSPLIT * sizeof(ScoreItem)));
   CK(cudaMalloc(&wk.item_count, 2 * sizeof(int)));
+  wk.TCAP = (b.HCAP + 255) / 256;
+  CK(cudaMalloc(&wk.cost32, (size_t)b.Q * b.HCAP * sizeof(float)));
+  CK(cudaMalloc(&wk.tile_cnt, (size_t)b.Q * wk.TCAP * sizeof(int)));
   CK(cudaMemcpy(wk.sub32, sub.data(), sub.size() * sizeof(float4), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(wk.P32, P.data(), P.size() * sizeof(float), cudaMemcpyHostToDevice));
   wk.HCAP = b.HCAP;
