@@ -343,9 +343,14 @@ def run_lift_bench(args, wl, rank, world, local, dist):
 
     e2e = None
     if not args.no_e2e:
+        copy_stream = torch.cuda.Stream()
+
         def e2e_step():
-            arena.upload(arena_dev)  # H2D of this step's IMLC field payloads (pinned)
-            return localize_batch(jobs, vmap, cfg, seeds=seeds, depth_cache=dcache, device_cache=dev_cache)
+            # H2D of this step's IMLC field payloads (pinned) on a copy stream,
+            # overlapping retrieval and planning; the lift waits on its event
+            arena.upload(arena_dev, stream=copy_stream)
+            return localize_batch(jobs, vmap, cfg, seeds=seeds, depth_cache=dcache, device_cache=dev_cache,
+                                  retrieval="gpu")
 
         e2e_step()
         sync_all()

@@ -168,6 +168,18 @@ int vl_p3p_solve_batch(vl_ctx* ctx, const double* bearings, const double* points
 int vl_sample_minimal_sets(vl_ctx* ctx, vl_pcg64_state* st, int64_t n, int32_t count,
                            int32_t* out, void* stream);
 
+/* ---- retrieval (retrieval.DescriptorIndex.topk, retrieval.py:66-82) ----- */
+/* Exact cosine top-k for Q queries at once.  db DEVICE [E,D] fp64 rows, unit
+ * normalised as DescriptorIndex.add stores them (f32 rows widened); id_rank
+ * DEVICE [E] = position of each entry id in ascending id order (the tie
+ * key); queries DEVICE [Q,D] fp64, normalised here; 1 <= k <= 32.  out_idx
+ * DEVICE [Q, min(k,E)] entry rows best first (similarity descending, ties by
+ * ascending id), out_sim DEVICE [Q, min(k,E)].  A zero or non-finite query
+ * -> VL_ERR_INVALID ("query vector must be non-zero and finite"). */
+int vl_retrieval_topk(vl_ctx* ctx, const double* db, const int64_t* id_rank, int32_t E, int32_t D,
+                      const double* queries, int32_t Q, int32_t k, int32_t* out_idx, double* out_sim,
+                      void* stream);
+
 /* ---- IMLC correspondence-field files (matchio.py:9-20, read_field :158-200) */
 enum {
   VL_IMLC_OK = 0,

@@ -778,3 +778,32 @@ extern "C" int vl_pose_residuals(vl_ctx* c, const double* q, const double* t, co
                                   res, z, J, (cudaStream_t)stream);
   return check_launch(c);
 }
+
+// ---- retrieval (retrieval.py:66-82) -----------------------------------------
+namespace vl {
+int launch_topk(const double* M, const int64_t* rank, int E, int D, const double* Qv, int Q, int K, int* out_idx,
+                double* out_sim, int* bad, cudaStream_t st);
+}
+
+extern "C" int vl_retrieval_topk(vl_ctx* c, const double* db, const int64_t* id_rank, int32_t E, int32_t D,
+                                 const double* queries, int32_t Q, int32_t k, int32_t* out_idx, double* out_sim,
+                                 void* stream) {
+  if (!c || E < 0 || D < 1 || Q < 0) return fail(c, VL_ERR_INVALID, "bad argument");
+  if (k < 1) return fail(c, VL_ERR_INVALID, "k must be >= 1, got " + std::to_string(k));
+  if (k > 32) return fail(c, VL_ERR_INVALID, "k must be <= 32 on the device path");
+  if (Q == 0 || E == 0) return VL_OK;
+  if (!db || !id_rank || !queries || !out_idx || !out_sim) return fail(c, VL_ERR_INVALID, "null array");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if ((rc = ensure(c, c->scratch, 4096)) || (rc = ensure_host(c, 4096))) return rc;
+  int* dbad = (int*)c->scratch.p;
+  VL_CUDA(c, cudaMemsetAsync(dbad, 0, sizeof(int), st));
+  c->launches += launch_topk(db, id_rank, E, D, queries, Q, std::min(k, E), out_idx, out_sim, dbad, st);
+  if ((rc = check_launch(c))) return rc;
+  int* h = (int*)c->h_pinned;
+  VL_CUDA(c, cudaMemcpyAsync(h, dbad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  VL_CUDA(c, cudaStreamSynchronize(st));
+  if (*h) return fail(c, VL_ERR_INVALID, "query vector must be non-zero and finite");
+  return VL_OK;
+}

@@ -24,6 +24,7 @@ import numpy as np
 from . import _lib
 from .geometry import CameraIntrinsics, Pose
 from .matchio import CorrespondenceField, FieldBlob, filter_matches_arrays  # noqa: F401
+from .retrieval import DescriptorIndex
 from .posest import (Match2D3D, PoseEstimate, RansacConfig, _estimates_from, _intr_c,
                      ransac_pnp_device)
 
@@ -114,71 +115,6 @@ class QueryJob:
     k_loc: int = 10
 
 
-class DescriptorIndex:
-    """Exact cosine top-K with ascending-id tie-break (retrieval.py:16-85).
-
-    Retrieval is upstream of the GPU path (out of scope); this
-    host mirror keeps ``localize(index=None)`` working like the reference.
-    """
-
-    def __init__(self, dim: int):
-        if dim < 1:
-            raise ValueError(f"descriptor dimension must be >= 1, got {dim}")
-        self.dim = int(dim)
-        self._ids, self._vecs = [], []
-        self._M = None
-
-    @classmethod
-    def from_entries(cls, entries):
-        idx = None
-        for eid, vec in entries:
-            if idx is None:
-                idx = cls(np.asarray(vec).shape[-1])
-            idx.add(eid, vec)
-        return idx if idx is not None else cls(1)
-
-    @property
-    def size(self) -> int:
-        return len(self._ids)
-
-    def add(self, entry_id, vector):
-        v = np.asarray(vector, dtype=np.float32).reshape(-1)
-        if v.shape[0] != self.dim:
-            raise ValueError("dimension mismatch")
-        n = float(np.linalg.norm(v.astype(np.float64)))
-        if n == 0.0 or not np.isfinite(n):
-            raise ValueError(f"cannot index zero or non-finite vector for id {entry_id!r}")
-        if entry_id in self._ids:
-            raise ValueError(f"duplicate id {entry_id!r}")
-        self._ids.append(entry_id)
-        self._vecs.append((v.astype(np.float64) / n).astype(np.float32))
-        self._M = None
-        return self
-
-    def topk(self, query, k):
-        if k < 1:
-            raise ValueError(f"k must be >= 1, got {k}")
-        q = np.asarray(query, dtype=np.float64).reshape(-1)
-        if q.shape[0] != self.dim:
-            raise ValueError("dimension mismatch")
-        if not self._ids:
-            return []
-        n = float(np.linalg.norm(q))
-        if n == 0.0 or not np.isfinite(n):
-            raise ValueError("query vector must be non-zero and finite")
-        if self._M is None:
-            self._M = np.stack(self._vecs).astype(np.float64)
-            order = sorted(range(len(self._ids)), key=lambda i: self._ids[i])
-            self._rank = np.empty(len(self._ids), dtype=np.int64)
-            self._rank[order] = np.arange(len(order))
-        sims = self._M @ (q / n)
-        sel = np.lexsort((self._rank, -sims))[: min(k, len(self._ids))]
-        return [(self._ids[i], float(sims[i])) for i in sel]
-
-    def ids(self):
-        return list(self._ids)
-
-
 # ----------------------------------------------------------------------------- device helpers
 class _DeviceDepth:
     """One entry's stored depth resident in HBM + its vl_lift_depth record."""
@@ -242,59 +178,74 @@ class _FieldUpload:
     Planar fields (CorrespondenceField-like: targets/confidence arrays) are
     packed into two device arrays (one dtype per call: f64 if any planar
     field is f64).  IMLC fields (``FieldBlob``) are read in place from their
-    arena's HBM mirror (one copy per arena, no repacking)."""
+    arena's HBM mirror (one copy per arena, no repacking); their geometry
+    comes from the arena's arrays, so big batches need no per-field work
+    beyond one attribute read."""
 
     def __init__(self, fields):
         import torch
-        planar = [f for f in fields if not isinstance(f, FieldBlob)]
+        n = len(fields)
+        blob = np.fromiter((type(f) is FieldBlob for f in fields), dtype=bool, count=n)
+        planar_idx = np.nonzero(~blob)[0]
+        planar = [fields[i] for i in planar_idx]
         self.f64 = any(np.asarray(f.confidence).dtype != np.float32 or np.asarray(f.targets).dtype != np.float32
                        for f in planar)
         dt = np.float64 if self.f64 else np.float32
         self.item = 8 if self.f64 else 4
-        n = len(fields)
-        self.layout = np.zeros(n, dtype=np.int32)
+        self.layout = np.where(blob, _lib.LIFT_IMLC, _lib.LIFT_PLANAR).astype(np.int32)
         self.tptr = np.zeros(n, dtype=np.uint64)
         self.cptr = np.zeros(n, dtype=np.uint64)
-        tg, cf, where = [], [], []
-        arenas = {}
-        for i, f in enumerate(fields):
-            if isinstance(f, FieldBlob):
-                a = arenas.get(id(f.arena))
-                if a is None:
-                    a = arenas[id(f.arena)] = f.arena.device()
-                self.layout[i] = _lib.LIFT_IMLC
-                self.tptr[i] = a.data_ptr() + f.records_offset
-            else:
-                where.append(i)
-                tg.append(np.ascontiguousarray(f.targets, dtype=dt).reshape(-1))
-                cf.append(np.ascontiguousarray(f.confidence, dtype=dt).reshape(-1))
-        self.keep = list(arenas.values())
-        self.targets = self.conf = None
+        self.gw = np.zeros(n, dtype=np.int64)
+        self.gh = np.zeros(n, dtype=np.int64)
+        self.sx = np.zeros(n, dtype=np.float64)
+        self.sy = np.zeros(n, dtype=np.float64)
+        self.keep = []
         self.bytes = 0
-        if where:
+        blob_idx = np.nonzero(blob)[0]
+        if blob_idx.size:
+            arenas = {}
+            for i in blob_idx:
+                f = fields[i]
+                arenas.setdefault(id(f.arena), (f.arena, [], []))[1].append(i)
+            for arena, pos, _ in arenas.values():
+                pos = np.asarray(pos)
+                fidx = np.fromiter((fields[i].index for i in pos), dtype=np.int64, count=pos.size)
+                dev = arena.device()
+                arena.wait()  # a side-stream upload must land before the lift reads it
+                self.keep.append(dev)
+                self.tptr[pos] = np.uint64(dev.data_ptr()) + arena.roff[fidx]
+                self.gw[pos], self.gh[pos] = arena.gw[fidx], arena.gh[fidx]
+                self.sx[pos], self.sy[pos] = arena.sx[fidx], arena.sy[fidx]
+                self.bytes += int(12 * (arena.gw[fidx] * arena.gh[fidx]).sum())
+        self.targets = self.conf = None
+        if planar:
+            tg = [np.ascontiguousarray(f.targets, dtype=dt).reshape(-1) for f in planar]
+            cf = [np.ascontiguousarray(f.confidence, dtype=dt).reshape(-1) for f in planar]
             t_off = np.concatenate([[0], np.cumsum([a.size for a in tg])]).astype(np.uint64)
             c_off = np.concatenate([[0], np.cumsum([a.size for a in cf])]).astype(np.uint64)
             self.targets = torch.from_numpy(np.concatenate(tg)).cuda()
             self.conf = torch.from_numpy(np.concatenate(cf)).cuda()
-            self.tptr[where] = self.targets.data_ptr() + t_off[:-1] * self.item
-            self.cptr[where] = self.conf.data_ptr() + c_off[:-1] * self.item
+            self.tptr[planar_idx] = self.targets.data_ptr() + t_off[:-1] * self.item
+            self.cptr[planar_idx] = self.conf.data_ptr() + c_off[:-1] * self.item
+            self.gw[planar_idx] = [f.grid_w for f in planar]
+            self.gh[planar_idx] = [f.grid_h for f in planar]
+            self.sx[planar_idx] = [float(f.scale_x) for f in planar]
+            self.sy[planar_idx] = [float(f.scale_y) for f in planar]
             self.bytes += int(self.targets.numel() + self.conf.numel()) * self.item
-        self.bytes += sum(12 * f.grid_w * f.grid_h for f in fields if isinstance(f, FieldBlob))
+
+    @property
+    def cells(self) -> int:
+        return int((self.gw * self.gh).sum())
 
 
-def _seg_table(spec, up: _FieldUpload) -> np.ndarray:
-    """vl_lift_segment array (numpy structured) for (query, entry, direction, depth, field) tuples."""
-    n = len(spec)
+def _seg_table(q, e, d, dep, up: _FieldUpload) -> np.ndarray:
+    """vl_lift_segment array (numpy structured) from per-segment arrays."""
+    n = len(q)
     t = np.zeros(max(n, 1), dtype=_lib.LIFT_SEGMENT_DTYPE)
     if n:
-        t["query"][:n] = [x[0] for x in spec]
-        t["entry"][:n] = [x[1] for x in spec]
-        t["direction"][:n] = [x[2] for x in spec]
-        t["depth"][:n] = [x[3] for x in spec]
-        t["grid_w"][:n] = [x[4].grid_w for x in spec]
-        t["grid_h"][:n] = [x[4].grid_h for x in spec]
-        t["scale_x"][:n] = [float(x[4].scale_x) for x in spec]
-        t["scale_y"][:n] = [float(x[4].scale_y) for x in spec]
+        t["query"][:n], t["entry"][:n], t["direction"][:n], t["depth"][:n] = q, e, d, dep
+        t["grid_w"][:n], t["grid_h"][:n] = up.gw, up.gh
+        t["scale_x"][:n], t["scale_y"][:n] = up.sx, up.sy
         t["layout"][:n] = up.layout
         t["targets"][:n] = up.tptr
         t["confidence"][:n] = up.cptr
@@ -323,8 +274,8 @@ def _run_lift(segs_spec, depth_records, threshold, mode=0):
     n = len(segs_spec)
     fields = [s[4] for s in segs_spec]
     up = _FieldUpload(fields)
-    table = _seg_table(segs_spec, up)
-    cap = max(sum(f.grid_w * f.grid_h for f in fields), 1)
+    table = _seg_table(*([x[k] for x in segs_spec] for k in range(4)), up)
+    cap = max(up.cells, 1)
     deps = (_lib.LiftDepth * max(len(depth_records), 1))(*depth_records)
     px = torch.empty((cap, 2), dtype=torch.float64, device="cuda")
     X = torch.empty((cap, 3), dtype=torch.float64, device="cuda")
@@ -386,26 +337,41 @@ def _entry_segments(query_job, entry, q_index, e_index, d_index):
     return [(q_index, e_index, 0, d_index, pair.db_to_query), (q_index, e_index, 1, d_index, pair.query_to_db)]
 
 
-def _depth_record(entry, depth, cache):
-    """vl_lift_depth record of an entry; the device copy lives in `cache` (dict),
-    which the caller must keep alive until the lift has been enqueued."""
+def _device_depth(entry, depth, cache):
+    """Device copy of an entry's stored depth, cached in `cache` (dict) by entry id;
+    the caller keeps the cache alive until the lift has been enqueued."""
     key = getattr(entry, "id", None)
     dd = cache.get(key)
     if dd is None:
         dd = _DeviceDepth(depth, entry.intrinsics)
         cache[key] = dd
+    return dd
+
+
+def _depth_mismatch(entry, dd):
+    """localizer.py:151-155 message when the depth map's image size differs from the entry's."""
     gi = dd.grid_intr
     if gi is not None and (gi.width != entry.intrinsics.width or gi.height != entry.intrinsics.height):
-        raise ValueError(f"entry {entry.id}: depth map covers {gi.width}x{gi.height}, "
-                         f"entry image is {entry.intrinsics.width}x{entry.intrinsics.height}")
+        return (f"entry {entry.id}: depth map covers {gi.width}x{gi.height}, "
+                f"entry image is {entry.intrinsics.width}x{entry.intrinsics.height}")
+    return None
+
+
+def _depth_record(entry, depth, cache):
+    """vl_lift_depth record of an entry (device copy cached in `cache`)."""
+    dd = _device_depth(entry, depth, cache)
+    msg = _depth_mismatch(entry, dd)
+    if msg:
+        raise ValueError(msg)
     return dd.record(entry.intrinsics, entry.pose)
 
 
 def lift_arrays(query_job, entry, depth, threshold: float = CONFIDENCE_THRESHOLD):
     """Device (px, X, w) of one entry's lift (localizer.py:134-197 order)."""
     keep = {}
+    segs = _entry_segments(query_job, entry, 0, 0, 0)  # span checks first (localizer.py:147-150)
     rec = _depth_record(entry, depth, keep)
-    px, X, w, _, _, _ = _run_lift(_entry_segments(query_job, entry, 0, 0, 0), [rec], threshold)
+    px, X, w, _, _, _ = _run_lift(segs, [rec], threshold)
     return px, X, w
 
 
@@ -421,32 +387,77 @@ def _failure(n):
                         score=math.inf, iterations=0, converged=False)
 
 
-def _plan(jobs, vmap, index, depth_cache, device_cache):
-    """Segments + depth records for every query (sorted retrieved ids, localizer.py:220-235)."""
-    from .geometry import CameraIntrinsics  # noqa: F401
+def _retrieve(jobs, index, retrieval):
+    """Retrieved entry ids of every job: host (reference-exact numpy) or one GPU launch."""
+    if index.size == 0:
+        return [[] for _ in jobs]
+    if retrieval == "host":
+        return [[eid for eid, _ in index.topk(np.asarray(j.descriptor, dtype=np.float64), j.k_loc)] for j in jobs]
+    if retrieval != "gpu":
+        raise ValueError(f"retrieval must be 'host' or 'gpu', got {retrieval!r}")
+    for j in jobs:
+        if j.k_loc < 1:
+            raise ValueError(f"k must be >= 1, got {j.k_loc}")
+    kmax = max(j.k_loc for j in jobs)
+    desc = np.stack([np.asarray(j.descriptor, dtype=np.float64).reshape(-1) for j in jobs])
+    ids, _ = index.topk_batch(desc, kmax)
+    return [row[: j.k_loc] for row, j in zip(ids, jobs)]
+
+
+def _plan(jobs, vmap, index, depth_cache, device_cache, retrieval="host"):
+    """Segment arrays + depth records for every query (sorted retrieved ids,
+    localizer.py:220-235), with the reference's per-entry checks in its order
+    (db->query span, query->db span, depth size; localizer.py:147-155)."""
     if index is None:
         index = DescriptorIndex.from_entries((e.id, e.descriptor) for e in vmap.entries)
     by_id = {e.id: e for e in vmap.entries}
-    segs, recs, rec_of = [], [], {}
-    for qi, job in enumerate(jobs):
-        if index.size == 0:
-            continue
-        ranked = index.topk(np.asarray(job.descriptor, dtype=np.float64), job.k_loc)
-        for eid in sorted(eid for eid, _ in ranked):
-            if eid not in job.fields:
+    pq, pe, fields, spans, names, derr = [], [], [], [], [], []
+    recs, rec_of, err_of = [], {}, {}
+    for qi, (job, ranked) in enumerate(zip(jobs, _retrieve(jobs, index, retrieval))):
+        qI = job.intrinsics
+        for eid in sorted(ranked):
+            pair = job.fields.get(eid)
+            if pair is None:
                 continue
             entry = by_id[eid]
-            if eid not in rec_of:
+            k = rec_of.get(eid)
+            if k is None:
                 if depth_cache is not None and eid in depth_cache:
                     depth = depth_cache[eid]
                 else:
                     if getattr(entry, "qdepth", None) is None:
                         raise ValueError(f"entry {eid} has no stored depth")
                     depth = entry.qdepth
-                rec_of[eid] = len(recs)
-                recs.append(_depth_record(entry, depth, device_cache))
-            segs += _entry_segments(job, entry, qi, rec_of[eid], rec_of[eid])
-    return segs, recs
+                dd = _device_depth(entry, depth, device_cache)
+                k = rec_of[eid] = len(recs)
+                recs.append(dd.record(entry.intrinsics, entry.pose))
+                err_of[eid] = _depth_mismatch(entry, dd)
+            eI = entry.intrinsics
+            pq.append(qi)
+            pe.append(k)
+            fields += (pair.db_to_query, pair.query_to_db)
+            spans += ((eI.width, eI.height), (qI.width, qI.height))
+            names.append(eid)
+            derr.append(err_of[eid])
+    up = _FieldUpload(fields)
+    n = len(pq)
+    if n:
+        WH = np.array(spans, dtype=np.float64).reshape(-1, 2)
+        bad = (np.abs(up.gw * up.sx - WH[:, 0]) > 1e-6 * WH[:, 0]) | \
+              (np.abs(up.gh * up.sy - WH[:, 1]) > 1e-6 * WH[:, 1])
+        bad_pair = bad.reshape(-1, 2).any(axis=1) | np.fromiter((m is not None for m in derr), bool, n)
+        if bad_pair.any():
+            k = int(np.argmax(bad_pair))
+            for j, what in ((2 * k, "db->query"), (2 * k + 1, "query->db")):
+                if bad[j]:
+                    f, (w, h) = fields[j], spans[j]
+                    raise ValueError(f"entry {names[k]} {what}: field grid {f.grid_w}x{f.grid_h} at scale "
+                                     f"({f.scale_x}, {f.scale_y}) does not span image {w}x{h}")
+            raise ValueError(derr[k])
+    q = np.repeat(np.asarray(pq, dtype=np.int64), 2)
+    e = np.repeat(np.asarray(pe, dtype=np.int64), 2)
+    d = np.tile(np.array([0, 1], dtype=np.int64), n)
+    return q, e, d, fields, up, recs
 
 
 class LiftPlan:
@@ -458,20 +469,19 @@ class LiftPlan:
     """
 
     def __init__(self, jobs, vmap, index=None, depth_cache=None, device_cache=None,
-                 threshold: float = CONFIDENCE_THRESHOLD):
+                 threshold: float = CONFIDENCE_THRESHOLD, retrieval: str = "host"):
         import torch
         if not 0 <= threshold <= 1:
             raise ValueError(f"threshold must be in [0, 1], got {threshold}")
         self.jobs = list(jobs)
         self.threshold = float(threshold)
         self.device_cache = {} if device_cache is None else device_cache
-        spec, recs = _plan(self.jobs, vmap, index, depth_cache, self.device_cache)
-        self.nseg = len(spec)
-        self.seg_q = np.array([s[0] for s in spec], dtype=np.int64)
-        self.fields = [s[4] for s in spec]
-        self.up = _FieldUpload(self.fields)
-        self.table = _seg_table(spec, self.up)
-        cap = sum(f.grid_w * f.grid_h for f in self.fields)
+        q, e, d, self.fields, self.up, recs = _plan(self.jobs, vmap, index, depth_cache, self.device_cache,
+                                                     retrieval)
+        self.nseg = len(self.fields)
+        self.seg_q = q
+        self.table = _seg_table(q, e, d, e, self.up)
+        cap = self.up.cells
         self.ndep = len(recs)
         self.deps = (_lib.LiftDepth * max(self.ndep, 1))(*recs)
         self.cap = max(cap, 1)
@@ -530,16 +540,19 @@ class LiftPlan:
 
 
 def localize_batch(jobs, vmap, cfg: RansacConfig, seeds=None, index=None, depth_cache=None,
-                   confidence_threshold: float = CONFIDENCE_THRESHOLD, device_cache=None):
+                   confidence_threshold: float = CONFIDENCE_THRESHOLD, device_cache=None,
+                   retrieval: str = "host"):
     """Retrieve, lift (one GPU launch sequence for every query) and estimate every pose.
 
     Each query behaves like ``localize(job, vmap, RansacConfig(seed=seeds[i]))``.
     ``device_cache`` (dict) keeps decoded depth resident in HBM across calls.
+    ``retrieval="gpu"`` ranks all queries in one ``vl_retrieval_topk`` launch
+    (ids equal the host ranking except on near-exact similarity ties).
     """
     jobs = list(jobs)
     if not jobs:
         return []
-    plan = LiftPlan(jobs, vmap, index, depth_cache, device_cache, confidence_threshold)
+    plan = LiftPlan(jobs, vmap, index, depth_cache, device_cache, confidence_threshold, retrieval)
     return plan.localize(cfg, seeds)
 
 

@@ -287,7 +287,14 @@ class FieldArena:
         for i, (st, s) in enumerate(zip(starts, sizes)):
             info = parse_header(self.host_u8[st:st + s])
             self.fields.append(FieldBlob(self, i, info, st))
+        # per-field geometry as arrays (vectorised segment tables)
+        self.gw = np.array([f.info.grid_w for f in self.fields], dtype=np.int64)
+        self.gh = np.array([f.info.grid_h for f in self.fields], dtype=np.int64)
+        self.sx = np.array([f.info.scale_x for f in self.fields], dtype=np.float64)
+        self.sy = np.array([f.info.scale_y for f in self.fields], dtype=np.float64)
+        self.roff = np.array([f.start + f.info.records_off for f in self.fields], dtype=np.uint64)
         self._dev = None
+        self.ready = None
 
     @staticmethod
     def _records_off_hint(head: bytes) -> int:
@@ -315,12 +322,25 @@ class FieldArena:
         return self._dev
 
     def upload(self, out, stream=None):
-        """Copy the arena into a caller-owned uint8 CUDA tensor (>= nbytes) and use it."""
+        """Copy the arena into a caller-owned uint8 CUDA tensor (>= nbytes) and use it.
+
+        With a side ``stream`` the copy overlaps whatever the caller does next
+        (retrieval, planning); consumers (the lift) wait on ``ready``."""
         import torch
+        self.ready = None
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
             out[: self.host.numel()].copy_(self.host, non_blocking=True)
+            if stream is not None:
+                self.ready = torch.cuda.Event()
+                self.ready.record(stream)
         self._dev = out
         return out
+
+    def wait(self, stream=None):
+        """Make `stream` (default: current) wait for the arena's device copy."""
+        import torch
+        if getattr(self, "ready", None) is not None:
+            (stream or torch.cuda.current_stream()).wait_event(self.ready)
 
 
 class _nullctx:

@@ -153,9 +153,9 @@ def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, o
     Q = offsets.shape[0] - 1
     if Q <= 0:
         raise ValueError("need at least one query")
-    for i in range(Q):
-        if offsets[i + 1] - offsets[i] < 3:
-            raise UnderConstrainedError(f"need >= 3 matches, got {offsets[i + 1] - offsets[i]}")
+    counts = np.diff(offsets)
+    if counts.min() < 3:
+        raise UnderConstrainedError(f"need >= 3 matches, got {int(counts[np.argmax(counts < 3)])}")
     dev = px.device
     N = int(offsets[-1])
     for a, shape in ((px, (N, 2)), (X, (N, 3)), (w, (N,))):
@@ -194,22 +194,31 @@ def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, o
 
 
 def _estimates_from(out, offsets) -> list[PoseEstimate]:
-    q = out["q"].cpu().numpy()
-    t = out["t"].cpu().numpy()
-    flags = out["flags"].cpu().numpy().astype(bool)
-    cnt = out["count"].cpu().numpy()
-    score = out["score"].cpu().numpy()
-    iters = out["iterations"].cpu().numpy()
-    conv = out["converged"].cpu().numpy()
-    stats = out["stats"].cpu().numpy()
+    """PoseEstimates from the device result dict: one pinned D2H per array
+    (flags viewed as bool without a host conversion pass), per-query masks are
+    views of the one host flag array."""
+    import torch
+    keys = ("q", "t", "flags", "count", "score", "iterations", "converged", "stats")
+    host = {}
+    for k in keys:
+        v = out[k]
+        h = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+        h.copy_(v, non_blocking=True)
+        host[k] = h
+    torch.cuda.current_stream().synchronize()
+    q, t = host["q"].numpy(), host["t"].numpy()
+    flags = host["flags"].numpy().view(np.bool_)
+    cnt, score = host["count"].numpy().tolist(), host["score"].numpy().tolist()
+    iters, conv = host["iterations"].numpy().tolist(), host["converged"].numpy().tolist()
+    stats = host["stats"].numpy().tolist()
+    offs = np.asarray(offsets).tolist()
     res = []
     for i in range(q.shape[0]):
-        a, b = int(offsets[i]), int(offsets[i + 1])
+        st = stats[i]
         res.append(PoseEstimate(
-            pose=Pose(q[i], t[i]), inlier_count=int(cnt[i]), inlier_flags=flags[a:b],
-            score=float(score[i]), iterations=int(iters[i]), converged=bool(conv[i]),
-            stats={"lo_calls": int(stats[i, 0]), "hypotheses": int(stats[i, 1]),
-                   "evals": int(stats[i, 2]), "rounds": int(stats[i, 3])}))
+            pose=Pose._trusted(q[i], t[i]), inlier_count=cnt[i], inlier_flags=flags[offs[i]:offs[i + 1]],
+            score=score[i], iterations=iters[i], converged=bool(conv[i]),
+            stats={"lo_calls": st[0], "hypotheses": st[1], "evals": st[2], "rounds": st[3]}))
     return res
 
 

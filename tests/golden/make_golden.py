@@ -254,7 +254,39 @@ def imlc_vectors():
     np.savez_compressed(OUT / "imlc.npz", **out)
 
 
+def retrieval_vectors():
+    """Reference DescriptorIndex.topk (retrieval.py:66-82) incl. exact ties and k > size."""
+    from visloc.retrieval import DescriptorIndex
+    rng = np.random.default_rng(11)
+    out = {}
+    for tag, E, D in (("a", 300, 16), ("b", 120, 256)):
+        vecs = rng.normal(size=(E, D)).astype(np.float32)
+        vecs[7] = vecs[3] * 2.0        # identical direction: exact tie, broken by id
+        vecs[50] = vecs[3]
+        ids = [f"e{(i * 7919) % 1000:04d}" for i in range(E)]  # ids not in insertion order
+        idx = DescriptorIndex(D)
+        for i in range(E):
+            idx.add(ids[i], vecs[i])
+        Q = 20
+        qs = rng.normal(size=(Q, D))
+        qs[0] = vecs[3].astype(np.float64) * 3.0  # ties at the top
+        res_ids, res_sims = [], []
+        for q in qs:
+            r = idx.topk(q, 12)
+            res_ids.append([ids.index(e) for e, _ in r])
+            res_sims.append([s_ for _, s_ in r])
+        out[f"{tag}_vecs"], out[f"{tag}_qs"] = vecs, qs
+        out[f"{tag}_ids"] = np.array([int(i[1:]) for i in ids])
+        out[f"{tag}_top"], out[f"{tag}_sims"] = np.array(res_ids), np.array(res_sims)
+        small = DescriptorIndex(D)
+        for i in range(5):
+            small.add(ids[i], vecs[i])
+        out[f"{tag}_small_top"] = np.array([ids.index(e) for e, _ in small.topk(qs[1], 12)])
+    np.savez_compressed(OUT / "retrieval.npz", **out)
+
+
 if __name__ == "__main__":
+    retrieval_vectors()
     imlc_vectors()
     lift_vectors()
     rng_vectors()
