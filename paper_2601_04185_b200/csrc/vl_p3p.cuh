@@ -454,8 +454,9 @@ VL_HD_BIG bool p3p_polish(const P3PGeo& g, const double* s_in, double* R, double
   }
   double Pm[3], Ym[3];
   for (int i = 0; i < 3; ++i) {
-    Pm[i] = ((P[i] + P[3 + i]) + P[6 + i]) / 3.0;
-    Ym[i] = ((Y[i] + Y[3 + i]) + Y[6 + i]) / 3.0;
+    // centroids: * (1/3) instead of / 3 (<= 1 ulp from numpy's mean; P3P parity is 1e-9)
+    Pm[i] = ((P[i] + P[3 + i]) + P[6 + i]) * (1.0 / 3.0);
+    Ym[i] = ((Y[i] + Y[3 + i]) + Y[6 + i]) * (1.0 / 3.0);
   }
   // Plane frames of both triangles; R = F_Y * Rot2(theta) * F_P^T with the
   // closed-form 2-D Procrustes angle of the centred in-plane coordinates.
@@ -496,7 +497,13 @@ VL_HD_BIG bool p3p_polish(const P3PGeo& g, const double* s_in, double* R, double
     for (int i = 0; i < 3; ++i) pr[i] *= inr;
     double cx[3];
     cross3(pr, f + 3 * k, cx);
-    const double ang = atan2(nrm3(cx), dot3(pr, f + 3 * k));
+    // ang = atan2(|c|, d) <= tol, decided without atan2 outside a narrow band
+    // around the threshold (atan is monotone and atan(x) <= x): identical
+    // decisions, the fp64 atan2 only runs for |c|/d within 1 % of tol
+    const double c = nrm3(cx), d = dot3(pr, f + 3 * k);
+    if (d > 0.0 && c <= 0.99 * kBearingTol * d) continue;
+    if (!(d > 0.0) || c >= 1.01 * kBearingTol * d) return false;
+    const double ang = atan2(c, d);
     if (!(ang <= kBearingTol)) return false;
   }
   return true;
