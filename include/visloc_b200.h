@@ -112,6 +112,16 @@ int vl_pcg64_seed(uint64_t seed, vl_pcg64_state* out);
 /* replaces visloc.posest.ransac_pnp (posest.py:223) — batched over queries */
 int vl_ransac_pnp(vl_ctx* ctx, const vl_ransac_args* args, const vl_ransac_out* out, void* stream);
 
+/* Same estimator with staged admission, for callers that stream the inputs
+ * to the device: the rows of stage k (queries [stage_end[k-1], stage_end[k]),
+ * stage_end HOST [nstage], last = num_queries) are read only after
+ * stage_events[k] (a cudaEvent_t recorded after that stage's host-to-device
+ * copy, on any stream) has completed.  All stages share one round loop, so
+ * later copies overlap the rounds of admitted queries.  Results equal
+ * vl_ransac_pnp's.  One workspace chunk of queries. */
+int vl_ransac_pnp_staged(vl_ctx* ctx, const vl_ransac_args* args, const vl_ransac_out* out, int32_t nstage,
+                         const int32_t* stage_end, void* const* stage_events, void* stream);
+
 /* Stepwise driver of the same estimator, for the optional single-query
  * hypothesis-split mode across GPUs.  Every rank calls
  * vl_ransac_begin with identical args and its (split_rank, split_size):

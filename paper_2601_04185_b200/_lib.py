@@ -135,6 +135,9 @@ def lib():
                               vp, vp, vp, vp, i64, C.POINTER(C.c_int64), C.POINTER(C.c_int32), vp]
         L.vl_imlc_parse.argtypes = [vp, i64, C.POINTER(ImlcHeader)]
         L.vl_retrieval_topk.argtypes = [vp, vp, vp, i32, i32, vp, i32, i32, vp, vp, vp]
+        L.vl_ransac_pnp_staged.argtypes = [vp, C.POINTER(RansacArgs), C.POINTER(RansacOut), i32,
+                                           C.POINTER(C.c_int32), C.POINTER(vp), vp]
+        L.vl_ransac_pnp_staged.restype = C.c_int
         L.vl_retrieval_topk.restype = C.c_int
         L.vl_imlc_parse.restype = C.c_int
         L.vl_interp_depth.argtypes = [vp, C.POINTER(LiftDepth), vp, i64, vp, vp, vp]
@@ -165,7 +168,7 @@ EXPORTED_SYMBOLS = (
     "vl_sample_minimal_sets", "vl_profile", "vl_profile_read", "vl_lift", "vl_interp_depth",
     "vl_decode_depth", "vl_robust_cost", "vl_pose_residuals", "vl_ransac_begin", "vl_ransac_partial_bytes",
     "vl_ransac_step_score", "vl_ransac_step_finish", "vl_ransac_end", "vl_imlc_parse",
-    "vl_retrieval_topk",
+    "vl_retrieval_topk", "vl_ransac_pnp_staged",
 )
 
 STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final", "lift")

@@ -292,7 +292,7 @@ static int64_t ransac_chunk(int64_t Q, int64_t B) {
 // Uploads per-query state for queries [q0, q0+Qn), sizes the workspace and
 // runs k_prep.  Fills `wk`.
 static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, const Inputs& in, Work& wk,
-                       cudaStream_t st) {
+                       cudaStream_t st, QState** staged_qs = nullptr) {
   const vl_ransac_config& cfg = a->cfg;
   const int64_t B = cfg.batch_size;
   const int64_t HCAP = 4 * B;
@@ -382,8 +382,12 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
     VL_CUDA(c, cudaHostGetDevicePointer((void**)&wk.host_count,
                                         (char*)c->h_pinned + c->h_pinned_cap - 16, 0));
     c->prof_stream = st;
+    if (staged_qs) {  // vl_ransac_pnp_staged admits the queries stage by stage
+      *staged_qs = d_hqs;
+      return VL_OK;
+    }
     prof_hook(c, kStagePrep, true);
-    c->launches += launch_prep(wk, in, Qn, d_hqs, st);
+    c->launches += launch_prep(wk, in, 0, Qn, 0, d_hqs, st);
     prof_hook(c, kStagePrep, false);
     if ((rc = check_launch(c))) return rc;
   }
@@ -436,6 +440,71 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
       VL_CUDA(c, cudaStreamSynchronize(st));  // staging buffer reuse / event readout
       prof_collect(c);
     }
+  }
+  return VL_OK;
+}
+
+// ---- staged admission (host pipeline) --------------------------------------
+// Queries of stage k ([stage_end[k-1], stage_end[k])) join the running round
+// loop as soon as their input copy (event k) has completed; the first stage
+// is waited for on the stream.  One estimator run over all queries, so the
+// host-to-device copy of later stages overlaps the rounds of earlier ones
+// without the tail cost of separate per-chunk runs.  Per-query results are
+// identical to vl_ransac_pnp (each query's computation is independent of
+// which others share its rounds).
+int vl_ransac_pnp_staged(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, int32_t nstage,
+                         const int32_t* stage_end, void* const* stage_events, void* stream) {
+  if (!c || !a || !o || nstage < 1 || !stage_end || !stage_events) return fail(c, VL_ERR_INVALID, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  RansacParams p;
+  int rc;
+  if ((rc = ransac_params(c, a, p))) return rc;
+  const int Q = a->num_queries;
+  for (int k = 0; k < nstage; ++k)
+    if (stage_end[k] <= (k ? stage_end[k - 1] : 0) || !stage_events[k])
+      return fail(c, VL_ERR_INVALID, "stages must be non-empty, increasing, with an event each");
+  if (stage_end[nstage - 1] != Q) return fail(c, VL_ERR_INVALID, "last stage must end at num_queries");
+  if (ransac_chunk(Q, a->cfg.batch_size) < Q) return fail(c, VL_ERR_INVALID, "staged run takes one workspace chunk");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  const int64_t B = a->cfg.batch_size;
+  Inputs in{a->px, a->X, a->w};
+  Outputs out{o->q, o->t, o->inlier_flags, o->inlier_count, o->score, o->iterations, o->converged, o->stats};
+  Work wk;
+  QState* d_hqs = nullptr;
+  if ((rc = setup_chunk(c, a, 0, Q, in, wk, st, &d_hqs))) return rc;
+  const int64_t max_rounds = ((a->cfg.max_iterations + B - 1) / B + 1) * (int64_t)nstage + nstage;
+  int admitted = 0, nactive = 0, guard = 0;
+  while (true) {
+    // admit every stage whose copy has landed (block on the next one only when idle)
+    while (admitted < nstage) {
+      cudaEvent_t ev = (cudaEvent_t)stage_events[admitted];
+      if (nactive > 0) {
+        const cudaError_t e = cudaEventQuery(ev);
+        if (e == cudaErrorNotReady) break;
+        if (e != cudaSuccess) return fail(c, VL_ERR_CUDA, std::string("cudaEventQuery: ") + cudaGetErrorString(e));
+      }
+      VL_CUDA(c, cudaStreamWaitEvent(st, ev, 0));
+      const int q0 = admitted ? stage_end[admitted - 1] : 0, q1 = stage_end[admitted];
+      prof_hook(c, kStagePrep, true);
+      c->launches += launch_prep(wk, in, q0, q1 - q0, nactive, d_hqs, st);
+      prof_hook(c, kStagePrep, false);
+      if ((rc = check_launch(c))) return rc;
+      nactive += q1 - q0;
+      ++admitted;
+    }
+    if (nactive == 0) break;
+    c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c, 0);
+    if ((rc = check_launch(c))) return rc;
+    if ((rc = read_active(c, wk, st, &nactive))) return rc;
+    if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
+  }
+  prof_hook(c, kStageFinal, true);
+  c->launches += launch_final(wk, in, out, p, Q, 0, st);
+  prof_hook(c, kStageFinal, false);
+  if ((rc = check_launch(c))) return rc;
+  if (c->prof) {
+    VL_CUDA(c, cudaStreamSynchronize(st));
+    prof_collect(c);
   }
   return VL_OK;
 }

@@ -98,7 +98,8 @@ struct Outputs {
 };
 
 // ---- launchers (return number of kernels launched) -------------------------
-int launch_prep(const Work& wk, const Inputs& in, int Q, const QState* host_qs, cudaStream_t st);
+int launch_prep(const Work& wk, const Inputs& in, int q0, int nq, int list_pos, const QState* host_qs,
+                cudaStream_t st);
 // profiling stages (vl_profile_read order)
 enum { kStagePrep = 0, kStageSample, kStageP3P, kStageCompact, kStageScore, kStageScan, kStageActive,
        kStageFinal, kStageLift, kNumStages };

@@ -23,17 +23,21 @@ namespace vl {
 // The per-query states come straight from the mapped pinned staging buffer
 // (kernel loads over PCIe, not a copy-engine transfer, so a chunk never waits
 // behind the host pipeline's bulk prefetch of the next chunk's matches).
-__global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* __restrict__ host_qs) {
-  QState& S = wk.qs[blockIdx.x];
+// Block b admits query q0 + b at active-list position list_pos + b (staged
+// admission appends a stage's queries behind the running ones).
+__global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* __restrict__ host_qs, int q0,
+                                              int list_pos) {
+  const int q = q0 + blockIdx.x;
+  QState& S = wk.qs[q];
   if (host_qs) {
     constexpr int kWords = sizeof(QState) / 4;
     static_assert(sizeof(QState) % 4 == 0, "QState word copy");
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(host_qs + blockIdx.x);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(host_qs + q);
     uint32_t* dst = reinterpret_cast<uint32_t*>(&S);
     for (int i = threadIdx.x; i < kWords; i += blockDim.x) dst[i] = src[i];
     if (threadIdx.x == 0) {
-      wk.active_list[blockIdx.x] = blockIdx.x;
-      if (blockIdx.x == 0) wk.item_count[0] = wk.item_count[1] = 0;
+      wk.active_list[list_pos + blockIdx.x] = q;
+      if (list_pos + blockIdx.x == 0) wk.item_count[0] = wk.item_count[1] = 0;
     }
     __syncthreads();
   }
@@ -55,8 +59,10 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
   }
 }
 
-int launch_prep(const Work& wk, const Inputs& in, int Q, const QState* host_qs, cudaStream_t st) {
-  k_prep<<<Q, 256, 0, st>>>(wk, in, host_qs);
+int launch_prep(const Work& wk, const Inputs& in, int q0, int nq, int list_pos, const QState* host_qs,
+                cudaStream_t st) {
+  if (nq <= 0) return 0;
+  k_prep<<<nq, 256, 0, st>>>(wk, in, host_qs, q0, list_pos);
   return 1;
 }
 

@@ -139,7 +139,7 @@ def _to_device(a: np.ndarray):
 
 
 # ----------------------------------------------------------------- device entry
-def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, out=None):
+def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, out=None, stages=None):
     """Batched estimator on device-resident inputs (the HBM-resident hot path).
 
     ``px`` (N,2), ``X`` (N,3), ``w`` (N,) are fp64 CUDA tensors holding Q
@@ -147,6 +147,9 @@ def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, o
     a list of Q intrinsics; ``seeds`` Q seeds (each query behaves exactly like
     ``ransac_pnp`` with ``RansacConfig(seed=seeds[i])``).  Returns a dict of
     CUDA tensors (q, t, flags, count, score, iterations, converged, stats).
+    ``stages``: optional ``(stage_end, events)`` — the inputs of queries
+    ``[stage_end[k-1], stage_end[k])`` are only valid once ``events[k]``
+    (``torch.cuda.Event``) completes (``vl_ransac_pnp_staged``).
     """
     import torch
     offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
@@ -188,8 +191,15 @@ def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, o
     o.iterations, o.converged = out["iterations"].data_ptr(), out["converged"].data_ptr()
     o.stats = out["stats"].data_ptr()
     with torch.cuda.device(dev):
-        rc = _lib.lib().vl_ransac_pnp(ctx.handle, C.byref(args), C.byref(o), _lib.stream_ptr())
-    ctx.check(rc, "vl_ransac_pnp")
+        if stages is None:
+            rc = _lib.lib().vl_ransac_pnp(ctx.handle, C.byref(args), C.byref(o), _lib.stream_ptr())
+        else:
+            ends, events = stages
+            ends_c = (C.c_int32 * len(ends))(*[int(e) for e in ends])
+            evs_c = (C.c_void_p * len(events))(*[ev.cuda_event for ev in events])
+            rc = _lib.lib().vl_ransac_pnp_staged(ctx.handle, C.byref(args), C.byref(o), len(ends), ends_c, evs_c,
+                                                 _lib.stream_ptr())
+    ctx.check(rc, "vl_ransac_pnp_staged" if stages is not None else "vl_ransac_pnp")
     return out
 
 
@@ -241,17 +251,33 @@ def _host_chunks(Q: int, chunk_queries=None):
     return chunks
 
 
-def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chunk_queries=None):
+def _stage_schedule(Q: int):
+    """Staged-admission stage ends: Q/16, then doubling stage sizes (Q/8, Q/4, ...),
+    a short remainder folded into the last stage.  Each admission adds one
+    LO-heavy first round to the shared loop, so few stages beat many small
+    ones (C3 sweep, tools/host_pipe.py: [63, 189, 441, 1000] is the best of the
+    schedules tried)."""
+    ends, q0, size = [], 0, max(1, -(-Q // 16))
+    while q0 < Q:
+        q1 = Q if Q - q0 < 3 * size // 2 else q0 + size
+        ends.append(q1)
+        q0, size = q1, 2 * size
+    return ends
+
+
+def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chunk_queries=None,
+                    stage_ends=None):
     """Batched estimator on HOST buffers: H2D copy, device run, D2H of the results.
 
     ``px``/``X``/``w`` are packed host arrays (numpy, or pinned torch CPU
-    tensors for full-bandwidth copies).  Queries are processed in chunks
-    (``_host_chunks``) on the caller's stream while a second stream copies
-    the next chunk's matches to HBM and the previous chunk's results back
-    (double-buffered, event-ordered), so PCIe traffic overlaps estimation.
-    Returns a dict of
-    numpy arrays (q, t, flags, count, score, iterations, converged, stats) and
-    the byte counts moved each way.
+    tensors for full-bandwidth copies).  Default: the inputs are copied in
+    stages (``_stage_schedule``) on a side stream and ONE estimator run
+    admits each stage's queries as soon as its copy lands
+    (``vl_ransac_pnp_staged``), so PCIe traffic overlaps estimation without
+    splitting the run.  ``chunk_queries=k`` instead runs separate estimator
+    calls on chunks of k queries, double-buffered (``_host_chunks``).
+    Returns a dict of numpy arrays (q, t, flags, count, score, iterations,
+    converged, stats) and the byte counts moved each way.
     """
     import torch
     _lib.context()
@@ -269,10 +295,6 @@ def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chu
     comp = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
     dev = torch.device("cuda", torch.cuda.current_device())
-    chunks = _host_chunks(Q, chunk_queries)
-    max_rows = max(int(offsets[b] - offsets[a]) for a, b in chunks)
-    bufs = [[torch.empty((max_rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in host_in]
-            for _ in range(min(2, len(chunks)))]
     out = {
         "q": torch.empty((Q, 4), dtype=torch.float64, device=dev),
         "t": torch.empty((Q, 3), dtype=torch.float64, device=dev),
@@ -284,6 +306,43 @@ def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chu
         "stats": torch.empty((Q, 4), dtype=torch.int64, device=dev),
     }
     host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()}
+    if not chunk_queries:
+        ends = list(stage_ends) if stage_ends is not None else _stage_schedule(Q)
+        bufs = [torch.empty(t.shape, dtype=t.dtype, device=dev) for t in host_in]
+        events = []
+        copy.wait_stream(comp)  # the device buffers are fresh allocations on the compute stream
+        with torch.cuda.stream(copy):
+            q0 = 0
+            for q1 in ends:
+                r0, r1 = int(offsets[q0]), int(offsets[q1])
+                for dst, src in zip(bufs, host_in):
+                    dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+                events.append(ev)
+                q0 = q1
+        ransac_pnp_device(bufs[0], bufs[1], bufs[2], offsets, intrinsics, seeds, cfg, out=out,
+                          stages=(ends, events))
+        for key, v in out.items():
+            host_out[key].copy_(v[:N] if key == "flags" else v, non_blocking=True)
+        comp.synchronize()
+    else:
+        _host_pipeline_chunks(host_in, offsets, intrinsics, seeds, cfg, chunk_queries, out, host_out, comp, copy,
+                              dev)
+    host = {k: v.numpy()[:N] if k == "flags" else v.numpy() for k, v in host_out.items()}
+    h2d_bytes = sum(int(t.numel() * t.element_size()) for t in host_in)
+    d2h_bytes = sum(int(v.nbytes) for v in host.values())
+    return host, h2d_bytes, d2h_bytes
+
+
+def _host_pipeline_chunks(host_in, offsets, intrinsics, seeds, cfg, chunk_queries, out, host_out, comp, copy, dev):
+    """Separate estimator calls per chunk, double-buffered H2D / D2H on `copy`."""
+    import torch
+    Q = offsets.shape[0] - 1
+    chunks = _host_chunks(Q, chunk_queries)
+    max_rows = max(int(offsets[b] - offsets[a]) for a, b in chunks)
+    bufs = [[torch.empty((max_rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev) for t in host_in]
+            for _ in range(min(2, len(chunks)))]
     ev_in = [torch.cuda.Event() for _ in chunks]
     ev_done = [torch.cuda.Event() for _ in chunks]
 
@@ -297,6 +356,7 @@ def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chu
                 dst[: r1 - r0].copy_(src[r0:r1], non_blocking=True)
             ev_in[k].record(copy)
 
+    copy.wait_stream(comp)
     h2d(0)
     for k, (a, b) in enumerate(chunks):
         r0, r1 = int(offsets[a]), int(offsets[b])
@@ -315,10 +375,6 @@ def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chu
                 dst.copy_(v, non_blocking=True)
     copy.synchronize()
     comp.wait_stream(copy)
-    host = {k: v.numpy()[:N] if k == "flags" else v.numpy() for k, v in host_out.items()}
-    h2d_bytes = sum(int(t.numel() * t.element_size()) for t in host_in)
-    d2h_bytes = sum(int(v.nbytes) for v in host.values())
-    return host, h2d_bytes, d2h_bytes
 
 
 def ransac_pnp_batch(queries, intrinsics, cfg: RansacConfig, seeds=None) -> list[PoseEstimate]:

@@ -209,7 +209,7 @@ def test_host_api_chunked_pipeline_equals_device(vl):
     ref = ransac_pnp_device(torch.from_numpy(px).cuda(), torch.from_numpy(X).cuda(), torch.from_numpy(w).cuda(),
                             offsets, intr, seeds, cfg)
     ref = {k: v.cpu().numpy() for k, v in ref.items()}
-    for chunk in (1, 3, 7, None):  # None: the default doubling schedule
+    for chunk in (1, 3, 7, None):  # None: the default staged-admission run
         host, h2d, d2h = ransac_pnp_host(px, X, w, offsets, intr, seeds, cfg, chunk_queries=chunk)
         assert h2d == px.nbytes + X.nbytes + w.nbytes
         for k in ("q", "t", "flags", "count", "score", "iterations", "converged", "stats"):

@@ -104,3 +104,11 @@ def test_host_chunk_schedule():
         assert all(b > a for a, b in ch)
     assert _host_chunks(1000) == [(0, 63), (63, 189), (189, 441), (441, 1000)]
     assert _host_chunks(10, 4) == [(0, 4), (4, 8), (8, 10)]
+
+
+def test_stage_schedule():
+    from paper_2601_04185_b200.posest import _stage_schedule
+    for Q in (1, 2, 3, 5, 31, 32, 33, 100, 1000, 4096):
+        e = _stage_schedule(Q)
+        assert e[-1] == Q and all(b > a for a, b in zip([0] + e, e))
+    assert _stage_schedule(1000) == [63, 189, 441, 1000]

@@ -60,10 +60,50 @@ def main():
         ms, wall = ev_time(lambda: ransac_pnp_device(px_d[:n_r], X_d[:n_r], w_d[:n_r], o, intr[:qq], seeds[:qq], cfg))
         print(f"device Q={qq:5d}: {ms:8.2f} ms (wall {wall:8.2f})")
 
-    for sched in (None, 256, 125, Q):
+    for sched in (63, 256, Q):
         ms, wall = ev_time(lambda: ransac_pnp_host(px_h, X_h, w_h, offsets, intr, seeds, cfg, chunk_queries=sched))
         print(f"host chunks={posest._host_chunks(Q, sched)[:6]}: {ms:8.2f} ms (wall {wall:8.2f})")
+    f = Q / 1000
+    for ends in (posest._stage_schedule(Q), [int(f * e) for e in (63, 189, 441, 1000)],
+                 [int(f * e) for e in (125, 375, 1000)], [int(f * e) for e in (125, 250, 500, 1000)],
+                 [int(f * e) for e in (250, 1000)], [int(f * e) for e in (100, 200, 300, 400, 500, 600, 700, 800,
+                                                                          900, 1000)]):
+        ms, wall = ev_time(lambda: ransac_pnp_host(px_h, X_h, w_h, offsets, intr, seeds, cfg, stage_ends=ends))
+        print(f"staged ends={ends}: {ms:8.2f} ms (wall {wall:8.2f})")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) <= 2:
     main()
+
+
+def profile_compare():
+    """Stage breakdown: device-resident run vs staged host run (C3)."""
+    from paper_2601_04185_b200 import _lib
+    Q = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
+    wl = bench.WORKLOADS["c3"]
+    qs = [bench.query_a(qi, wl["n"], wl["outlier"], wl["sigma"], 3000) for qi in range(Q)]
+    px_h = torch.from_numpy(np.concatenate([q[0] for q in qs])).pin_memory()
+    X_h = torch.from_numpy(np.concatenate([q[1] for q in qs])).pin_memory()
+    w_h = torch.from_numpy(np.concatenate([q[2] for q in qs])).pin_memory()
+    offsets = np.arange(Q + 1, dtype=np.int64) * wl["n"]
+    intr = [CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)] * Q
+    seeds = [bench.query_seed(qi, 3000) for qi in range(Q)]
+    cfg = RansacConfig(max_iterations=wl["max_iterations"], miss_probability=wl["eta"])
+    px_d, X_d, w_d = px_h.cuda(), X_h.cuda(), w_h.cuda()
+    ctx = _lib.context()
+    for name, fn in (("device", lambda: ransac_pnp_device(px_d, X_d, w_d, offsets, intr, seeds, cfg)),
+                     ("staged", lambda: ransac_pnp_host(px_h, X_h, w_h, offsets, intr, seeds, cfg))):
+        fn()
+        torch.cuda.synchronize()
+        ctx.profile(True)
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        prof = ctx.profile_read()
+        ctx.profile(False)
+        print(name, f"wall {wall:.2f} ms", {k: (round(v[0], 2), v[1]) for k, v in prof.items() if v[1]})
+
+
+if __name__ == "__main__" and len(sys.argv) > 2:
+    profile_compare()
