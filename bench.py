@@ -281,7 +281,7 @@ def run_lift_bench(args, wl, rank, world, local, dist):
     full host API incl. field/depth H2D and result D2H (e2e)."""
     import torch
     from paper_2601_04185_b200 import _lib
-    from paper_2601_04185_b200.localizer import LiftPlan, localize_batch
+    from paper_2601_04185_b200.localizer import LiftPlan
     from paper_2601_04185_b200.posest import RansacConfig
     from synth_inputs import lifted_scene
 
@@ -291,25 +291,38 @@ def run_lift_bench(args, wl, rank, world, local, dist):
     Q = wl["queries"]
     seed0 = LIFT_SEED + 1000 * rank
     vmap, jobs, dcache = lifted_scene(wl["K"], Q, wl["g"], seed=seed0, depth_kind=wl["depth"], fields="f32")
-    # the queries' fields arrive as IMLC payloads (matchio.py:9-20) packed in one
-    # pinned arena; the GPU lift reads the 12-B records in place
-    order = [(qi, eid) for qi, job in enumerate(jobs) for eid in sorted(job.fields)]
-    blobs = []
-    for qi, eid in order:
-        fp = jobs[qi].fields[eid]
-        blobs += [field_bytes(fp.query_to_db), field_bytes(fp.db_to_query)]
-    arena = FieldArena(blobs)
-    del blobs
-    bfields = [dict() for _ in jobs]
-    for k, (qi, eid) in enumerate(order):
-        bfields[qi][eid] = FieldPair(arena[2 * k], arena[2 * k + 1])
-    jobs = [QueryJob(j.query_id, j.intrinsics, j.descriptor, f, j.k_loc) for j, f in zip(jobs, bfields)]
+    # the queries' fields arrive as IMLC payloads (matchio.py:9-20), one pinned
+    # arena per micro-batch of queries (posest._stage_schedule sizes); the GPU
+    # lift reads the 12-B records in place
+    from paper_2601_04185_b200.localizer import localize_pipelined
+    from paper_2601_04185_b200.posest import _stage_schedule
+    ends = _stage_schedule(Q)
+    batches, q0 = [], 0
+    bjobs = []
+    for q1 in ends:
+        order = [(qi, eid) for qi in range(q0, q1) for eid in sorted(jobs[qi].fields)]
+        blobs = []
+        for qi, eid in order:
+            fp = jobs[qi].fields[eid]
+            blobs += [field_bytes(fp.query_to_db), field_bytes(fp.db_to_query)]
+        arena = FieldArena(blobs)
+        del blobs
+        bfields = {qi: {} for qi in range(q0, q1)}
+        for k, (qi, eid) in enumerate(order):
+            bfields[qi][eid] = FieldPair(arena[2 * k], arena[2 * k + 1])
+        bj = [QueryJob(jobs[qi].query_id, jobs[qi].intrinsics, jobs[qi].descriptor, bfields[qi], jobs[qi].k_loc)
+              for qi in range(q0, q1)]
+        batches.append((bj, arena))
+        bjobs += bj
+        q0 = q1
+    jobs = bjobs
+    arena_bytes = sum(int(a.nbytes) for _, a in batches)
     seeds = [query_seed(qi, seed0) for qi in range(Q)]
     cfg = RansacConfig(max_iterations=wl["max_iterations"], miss_probability=wl["eta"])
     ctx = _lib.context(local)
     stream = torch.cuda.current_stream()
-    arena_dev = torch.empty(arena.host.numel(), dtype=torch.uint8, device="cuda")
-    arena.upload(arena_dev)
+    for _, a in batches:
+        a.device()  # device-resident copies for the `value` path
     dev_cache = {}  # the map's depth stays resident in HBM across steps (server state)
 
     def sync_all():
@@ -343,14 +356,15 @@ def run_lift_bench(args, wl, rank, world, local, dist):
 
     e2e = None
     if not args.no_e2e:
-        copy_stream = torch.cuda.Stream()
+        big = max(a.host.numel() for _, a in batches)
+        bufs = [torch.empty(big, dtype=torch.uint8, device="cuda") for _ in range(2)]
 
         def e2e_step():
-            # H2D of this step's IMLC field payloads (pinned) on a copy stream,
-            # overlapping retrieval and planning; the lift waits on its event
-            arena.upload(arena_dev, stream=copy_stream)
-            return localize_batch(jobs, vmap, cfg, seeds=seeds, depth_cache=dcache, device_cache=dev_cache,
-                                  retrieval="gpu")
+            # micro-batched serving loop: batch k+1's IMLC payloads (pinned) go
+            # to HBM on a copy stream while batch k is retrieved, lifted and
+            # estimated; results come back to the host per batch
+            return localize_pipelined(batches, vmap, cfg, seeds=seeds, depth_cache=dcache, device_cache=dev_cache,
+                                      retrieval="gpu", buffers=bufs)
 
         e2e_step()
         sync_all()
@@ -362,7 +376,7 @@ def run_lift_bench(args, wl, rank, world, local, dist):
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        h2d = int(arena.nbytes)
+        h2d = arena_bytes
         d2h = sum(int(r.inlier_flags.size) + 7 * 8 + 5 * 8 for r in res)
         e2e = {"value": float(ev.item()) * args.steps / (float(et.item()) / 1e3), "unit": "evals/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -407,7 +421,8 @@ def run_lift_bench(args, wl, rank, world, local, dist):
             "data": "synthetic",
             "config": {"workload": wl["name"], "queries_per_gpu": Q, "db_images": wl["K"], "grid": wl["g"],
                        "lifted_corrs_per_step": matches, "depth": wl["depth"],
-                       "fields": f"IMLC f32 records, {arena.nbytes / 1e9:.3f} GB/step in one pinned arena",
+                       "fields": f"IMLC f32 records, {arena_bytes / 1e9:.3f} GB/step in pinned arenas, "
+                                 f"micro-batches {ends}",
                        "map": "depth resident in HBM (uploaded once); e2e H2D = the field payloads",
                        "l2": f"fields {plan.field_bytes / 1e9:.2f} GB/GPU",
                        "parallelism": f"query-sharded x{world}, no collective"},

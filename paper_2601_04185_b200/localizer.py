@@ -31,7 +31,7 @@ from .posest import (Match2D3D, PoseEstimate, RansacConfig, _estimates_from, _in
 __all__ = [
     "CONFIDENCE_THRESHOLD", "CorrespondenceField", "DepthMap", "DescriptorIndex", "FieldPair",
     "QuantizedDepthMap", "QueryJob", "dequantize_depth", "filter_matches_arrays", "interp_depth",
-    "interp_depth_many", "LiftPlan", "lift", "lift_arrays", "localize", "localize_batch",
+    "interp_depth_many", "LiftPlan", "lift", "lift_arrays", "localize", "localize_batch", "localize_pipelined",
 ]
 
 CONFIDENCE_THRESHOLD = 0.05
@@ -554,6 +554,47 @@ def localize_batch(jobs, vmap, cfg: RansacConfig, seeds=None, index=None, depth_
         return []
     plan = LiftPlan(jobs, vmap, index, depth_cache, device_cache, confidence_threshold, retrieval)
     return plan.localize(cfg, seeds)
+
+
+def localize_pipelined(batches, vmap, cfg: RansacConfig, seeds=None, index=None, depth_cache=None,
+                       confidence_threshold: float = CONFIDENCE_THRESHOLD, device_cache=None,
+                       retrieval: str = "host", buffers=None):
+    """Micro-batched serving loop: ``batches`` = [(jobs, arena), ...], each
+    batch's IMLC fields in its own ``FieldArena``.  Batch k+1's fields are
+    copied to HBM on a side stream while batch k is retrieved, lifted and
+    estimated (``localize_batch``), so PCIe time hides behind GPU work.
+    ``buffers`` (optional): two uint8 CUDA tensors large enough for any
+    arena, reused across calls.  ``seeds`` covers all jobs, in order.
+    Returns the flat list of PoseEstimates."""
+    import torch
+    batches = list(batches)
+    if not batches:
+        return []
+    njobs = sum(len(j) for j, _ in batches)
+    seeds = [cfg.seed] * njobs if seeds is None else list(seeds)
+    if buffers is None:
+        big = max(a.host.numel() for _, a in batches)
+        buffers = [torch.empty(big, dtype=torch.uint8, device="cuda") for _ in range(min(2, len(batches)))]
+    copy = torch.cuda.Stream()
+    comp = torch.cuda.current_stream()
+    done = [torch.cuda.Event() for _ in batches]
+    copy.wait_stream(comp)
+
+    def upload(k):
+        if k >= 2:
+            copy.wait_event(done[k - 2])  # buffer k % 2 was last read by batch k - 2
+        batches[k][1].upload(buffers[k % len(buffers)], stream=copy)
+
+    upload(0)
+    res, s0 = [], 0
+    for k, (jobs, _) in enumerate(batches):
+        if k + 1 < len(batches):
+            upload(k + 1)
+        res += localize_batch(jobs, vmap, cfg, seeds[s0:s0 + len(jobs)], index, depth_cache, confidence_threshold,
+                              device_cache, retrieval)
+        done[k].record(comp)
+        s0 += len(jobs)
+    return res
 
 
 def localize(query_job, vmap, cfg: RansacConfig, index=None, depth_cache=None,

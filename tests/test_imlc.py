@@ -148,3 +148,38 @@ def test_gpu_lift_from_imlc_equals_reference(golden):
         assert np.array_equal(w.cpu().numpy(), d[f"L{k}_w"])
         checked += 1
     assert checked >= 3
+
+
+@pytest.mark.gpu
+def test_gpu_localize_pipelined_equals_batch(golden):
+    """Micro-batched serving loop (per-batch arenas, side-stream uploads) == one localize_batch."""
+    from paper_2601_04185_b200 import localizer as L
+    from paper_2601_04185_b200 import matchio
+    from paper_2601_04185_b200.posest import RansacConfig
+    from scene_io import unpack_scene
+    vmap, jobs = unpack_scene(golden("lift"))
+    cfg = RansacConfig(seed=3)
+    seeds = [40 + j for j in range(len(jobs))]
+    batches = []
+    for lo, hi in ((0, 1), (1, 3), (3, len(jobs))):
+        blobs, keys = [], []
+        for j in range(lo, hi):
+            for eid, fp in sorted(jobs[j].fields.items()):
+                for f in (fp.query_to_db, fp.db_to_query):
+                    blobs.append(matchio.field_bytes(matchio.CorrespondenceField(
+                        f.source_id, f.target_id, np.asarray(f.targets, np.float32),
+                        np.asarray(f.confidence, np.float32), f.scale_x, f.scale_y)))
+                keys.append((j, eid))
+        arena = matchio.FieldArena(blobs)
+        bj = []
+        for j in range(lo, hi):
+            fields = {eid: L.FieldPair(arena[2 * k], arena[2 * k + 1]) for k, (jj, eid) in enumerate(keys) if jj == j}
+            bj.append(L.QueryJob(jobs[j].query_id, jobs[j].intrinsics, jobs[j].descriptor, fields, jobs[j].k_loc))
+        batches.append((bj, arena))
+    flat = [j for b, _ in batches for j in b]
+    ref = L.localize_batch(flat, vmap, cfg, seeds=seeds, depth_cache={})
+    got = L.localize_pipelined(batches, vmap, cfg, seeds=seeds, depth_cache={})
+    assert len(got) == len(ref)
+    for a, b in zip(ref, got):
+        assert np.array_equal(a.pose.q, b.pose.q) and np.array_equal(a.inlier_flags, b.inlier_flags)
+        assert a.iterations == b.iterations and a.score == b.score
