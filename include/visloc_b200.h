@@ -279,6 +279,33 @@ int vl_interp_depth(vl_ctx* ctx, const vl_lift_depth* depth, const double* pts, 
  * codes (kinds 2, 3) -> f32 depth (0 where invalid) + valid. */
 int vl_decode_depth(vl_ctx* ctx, const vl_lift_depth* depth, float* vals, uint8_t* valid, void* stream);
 
+/* ---- depth-map codecs (mapstore.py:96-134, :390-425) --------------------- */
+/* One depth map.  quantize: kind 0 (f32 values) or 1 (f16 values) + valid
+ * (u8) in, codes out (u8 when levels <= 255, else u16).  reduce: kind 2 (u8
+ * codes) or 3 (u16 codes) with `levels` in, codes of the new level count out
+ * ((h+f-1)/f x (w+f-1)/f, u8 when new_levels <= 255, else u16).  All arrays
+ * DEVICE, row-major [h,w]. */
+typedef struct {
+  int32_t width, height, kind, levels;
+  const void* values;
+  const uint8_t* valid;
+  void* out;
+} vl_depth_codec_job;
+
+/* replaces mapstore.quantize_depth (mapstore.py:96-119) for many maps:
+ * `thresholds` DEVICE [levels-1] ascending f32 — entry k is the smallest f32
+ * depth the reference maps to code k+2 (built on the host with the reference's
+ * own fp64 arithmetic); a valid pixel's code is 1 + #{thresholds <= depth},
+ * invalid pixels get 0. */
+int vl_quantize_depth(vl_ctx* ctx, const vl_depth_codec_job* jobs, int32_t njobs, const float* thresholds,
+                      int32_t levels, void* stream);
+
+/* replaces mapstore._downsample_codes_nearest_valid + _requantize_codes
+ * (mapstore.py:390-425; reduce_map's depth step, :428-497) for many maps:
+ * block factor >= 1, new_levels in [1, 65535]. */
+int vl_reduce_depth_codes(vl_ctx* ctx, const vl_depth_codec_job* jobs, int32_t njobs, int32_t factor,
+                          int32_t new_levels, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,11 @@ class RansacOut(C.Structure):
                 ("converged", C.c_void_p), ("stats", C.c_void_p)]
 
 
+class DepthCodecJob(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("kind", C.c_int32), ("levels", C.c_int32),
+                ("values", C.c_void_p), ("valid", C.c_void_p), ("out", C.c_void_p)]
+
+
 LIFT_PLANAR, LIFT_IMLC = 0, 1
 FIELD_BAD_CONF, FIELD_BAD_TARGET = 1, 2
 
@@ -152,6 +157,10 @@ def lib():
         for name in ("vl_ransac_begin", "vl_ransac_partial_bytes", "vl_ransac_step_score",
                      "vl_ransac_step_finish", "vl_ransac_end"):
             getattr(L, name).restype = C.c_int
+        L.vl_quantize_depth.argtypes = [vp, C.POINTER(DepthCodecJob), i32, vp, i32, vp]
+        L.vl_reduce_depth_codes.argtypes = [vp, C.POINTER(DepthCodecJob), i32, i32, i32, vp]
+        L.vl_quantize_depth.restype = C.c_int
+        L.vl_reduce_depth_codes.restype = C.c_int
         L.vl_robust_cost.restype = C.c_int
         L.vl_pose_residuals.restype = C.c_int
         for name in ("vl_create", "vl_destroy", "vl_reserve", "vl_pcg64_seed", "vl_ransac_pnp", "vl_profile",
@@ -168,7 +177,7 @@ EXPORTED_SYMBOLS = (
     "vl_sample_minimal_sets", "vl_profile", "vl_profile_read", "vl_lift", "vl_interp_depth",
     "vl_decode_depth", "vl_robust_cost", "vl_pose_residuals", "vl_ransac_begin", "vl_ransac_partial_bytes",
     "vl_ransac_step_score", "vl_ransac_step_finish", "vl_ransac_end", "vl_imlc_parse",
-    "vl_retrieval_topk", "vl_ransac_pnp_staged",
+    "vl_retrieval_topk", "vl_ransac_pnp_staged", "vl_quantize_depth", "vl_reduce_depth_codes",
 )
 
 STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final", "lift")

@@ -876,3 +876,57 @@ extern "C" int vl_retrieval_topk(vl_ctx* c, const double* db, const int64_t* id_
   if (*h) return fail(c, VL_ERR_INVALID, "query vector must be non-zero and finite");
   return VL_OK;
 }
+
+// ---- depth-map codecs (mapstore.py:96-134, :390-425) -------------------------
+namespace vl {
+struct CodecJob;
+int launch_quantize(const CodecJob* jobs, int njobs, const uint32_t* thr, int nthr, int out16, int num_sms,
+                    cudaStream_t st);
+int launch_reduce_codes(const CodecJob* jobs, int njobs, int factor, int new_levels, int num_sms, cudaStream_t st);
+}
+
+static int check_codec_jobs(vl_ctx* c, const vl_depth_codec_job* jobs, int32_t njobs, bool codes_in) {
+  if (njobs < 0 || (njobs > 0 && !jobs)) return fail(c, VL_ERR_INVALID, "bad argument");
+  for (int j = 0; j < njobs; ++j) {
+    const vl_depth_codec_job& J = jobs[j];
+    const std::string tag = "map " + std::to_string(j) + ": ";
+    if (J.width < 1 || J.height < 1 || (int64_t)J.width * J.height > INT32_MAX)
+      return fail(c, VL_ERR_INVALID, tag + "bad shape");
+    if (!J.values || !J.out || (!codes_in && !J.valid)) return fail(c, VL_ERR_INVALID, tag + "null array");
+    if (codes_in ? (J.kind != 2 && J.kind != 3) : (J.kind != 0 && J.kind != 1))
+      return fail(c, VL_ERR_INVALID, tag + "bad kind " + std::to_string(J.kind));
+    if (codes_in && (J.levels < 1 || J.levels > 65535 || (J.kind == 2) != (J.levels <= 255)))
+      return fail(c, VL_ERR_INVALID, tag + "levels out of range: " + std::to_string(J.levels));
+  }
+  return VL_OK;
+}
+
+extern "C" int vl_quantize_depth(vl_ctx* c, const vl_depth_codec_job* jobs, int32_t njobs, const float* thresholds,
+                                 int32_t levels, void* stream) {
+  if (!c) return VL_ERR_INVALID;
+  if (levels < 1 || levels > 65535) return fail(c, VL_ERR_INVALID, "levels out of range: " + std::to_string(levels));
+  if (levels > 1 && !thresholds) return fail(c, VL_ERR_INVALID, "null threshold table");
+  int rc;
+  if ((rc = check_codec_jobs(c, jobs, njobs, false))) return rc;
+  if (njobs == 0) return VL_OK;
+  VL_CUDA(c, cudaSetDevice(c->device));
+  static_assert(sizeof(vl_depth_codec_job) == 40, "codec job layout");
+  c->launches += launch_quantize((const CodecJob*)jobs, njobs, (const uint32_t*)thresholds, levels - 1,
+                                 levels > 255, c->num_sms, (cudaStream_t)stream);
+  return check_launch(c);
+}
+
+extern "C" int vl_reduce_depth_codes(vl_ctx* c, const vl_depth_codec_job* jobs, int32_t njobs, int32_t factor,
+                                     int32_t new_levels, void* stream) {
+  if (!c) return VL_ERR_INVALID;
+  if (factor < 1) return fail(c, VL_ERR_INVALID, "resolution factors must be >= 1");
+  if (new_levels < 1 || new_levels > 65535)
+    return fail(c, VL_ERR_INVALID, "levels out of range: " + std::to_string(new_levels));
+  int rc;
+  if ((rc = check_codec_jobs(c, jobs, njobs, true))) return rc;
+  if (njobs == 0) return VL_OK;
+  VL_CUDA(c, cudaSetDevice(c->device));
+  c->launches += launch_reduce_codes((const CodecJob*)jobs, njobs, factor, new_levels, c->num_sms,
+                                     (cudaStream_t)stream);
+  return check_launch(c);
+}

@@ -9,6 +9,7 @@ because the minimal-sample sets come from numpy's PCG64 stream.
 
 from __future__ import annotations
 
+import math
 import sys
 from pathlib import Path
 
@@ -285,7 +286,65 @@ def retrieval_vectors():
     np.savez_compressed(OUT / "retrieval.npz", **out)
 
 
+def mapstore_vectors():
+    """Reference depth codecs (mapstore.py:96-134, :390-425): quantize incl. clip bounds,
+    exact-threshold neighbours and invalid pixels; nearest-valid block reduction; requantization."""
+    from visloc.depthbuild import DepthMap
+    from visloc.mapstore import (QuantizedDepthMap, _downsample_codes_nearest_valid, _requantize_codes,
+                                 dequantize_depth, quantize_depth)
+    rng = np.random.default_rng(2024)
+    intr = CameraIntrinsics(100.0, 100.0, 50.0, 40.0, 100, 80)
+    out = {}
+    qcases = [(0.25, 128.0, 255), (0.25, 128.0, 65535), (0.5, 40.0, 1000), (0.25, 128.0, 2), (1.0, 2.0, 1),
+              (0.1, 300.0, 511), (0.25, 128.0, 31)]
+    for i, (dmin, dmax, L) in enumerate(qcases):
+        h, w = 37, 53
+        vals = np.exp(rng.uniform(np.log(dmin * 0.5), np.log(dmax * 2.0), size=(h, w))).astype(np.float32)
+        flat = vals.reshape(-1)
+        # exact decode points and their f32 neighbours (quantize(dequantize(c)) == c is the reference claim)
+        c = rng.integers(1, L + 1, size=200)
+        d = (dmin * np.exp((c - 1.0) / max(L - 1, 1) * math.log(dmax / dmin))).astype(np.float32)
+        flat[:200] = d
+        flat[200:400] = np.nextafter(d, np.float32(np.inf))
+        flat[400:600] = np.nextafter(d, np.float32(0))
+        # midpoints between adjacent levels (rounding boundaries) and their neighbours
+        cm = rng.integers(1, max(L, 2), size=200)
+        dm = (dmin * np.exp((cm - 0.5) / max(L - 1, 1) * math.log(dmax / dmin))).astype(np.float32)
+        flat[600:800] = dm
+        flat[800:1000] = np.nextafter(dm, np.float32(np.inf))
+        flat[1000:1200] = np.nextafter(dm, np.float32(0))
+        flat[1200:1204] = [dmin, dmax, np.float32(dmin) * 0.999, np.float32(dmax) * 1.001]
+        valid = rng.random((h, w)) > 0.1
+        valid.reshape(-1)[1200:1204] = True
+        vals[~valid] = np.where(rng.random((~valid).sum()) < 0.5, 0.0, np.nan).astype(np.float32)
+        q = quantize_depth(DepthMap(np.where(valid, vals, 1.0), valid, intr), dmin, dmax, L)
+        out[f"q{i}_vals"], out[f"q{i}_valid"], out[f"q{i}_codes"] = vals, valid, q.codes
+        out[f"q{i}_param"] = np.array([dmin, dmax, L], dtype=np.float64)
+        dq = dequantize_depth(q)
+        out[f"q{i}_deq"] = dq.values
+    out["nq"] = np.array(len(qcases))
+    rcases = [(255, 1, 5), (255, 2, 8), (255, 3, 9), (255, 4, 7), (511, 5, 6), (255, 7, 8), (65535, 2, 9),
+              (31, 3, 5), (255, 16, 8)]
+    for i, (L, f, bits) in enumerate(rcases):
+        h, w = int(rng.integers(20, 70)), int(rng.integers(20, 70))
+        codes = rng.integers(1, L + 1, size=(h, w))
+        codes[rng.random((h, w)) < 0.45] = 0
+        codes[:f, :f] = 0                        # an all-invalid block
+        q = QuantizedDepthMap(codes, levels=L, intrinsics=intr)
+        ds = _downsample_codes_nearest_valid(q.codes, f)
+        rq = _requantize_codes(QuantizedDepthMap(ds, q.d_min, q.d_max, q.levels, q.intrinsics), 2**bits - 1)
+        out[f"r{i}_codes"], out[f"r{i}_param"] = q.codes, np.array([L, f, bits])
+        out[f"r{i}_down"], out[f"r{i}_out"] = ds, rq.codes
+    out["nr"] = np.array(len(rcases))
+    np.savez_compressed(OUT / "mapstore.npz", **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `make_golden.py mapstore`
+        for name in sys.argv[1:]:
+            globals()[f"{name}_vectors"]()
+        sys.exit(0)
+    mapstore_vectors()
     retrieval_vectors()
     imlc_vectors()
     lift_vectors()
