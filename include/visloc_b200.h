@@ -306,6 +306,63 @@ int vl_quantize_depth(vl_ctx* ctx, const vl_depth_codec_job* jobs, int32_t njobs
 int vl_reduce_depth_codes(vl_ctx* ctx, const vl_depth_codec_job* jobs, int32_t njobs, int32_t factor,
                           int32_t new_levels, void* stream);
 
+/* ---- dense depth triangulation (depthbuild.py:104-441) ------------------ */
+/* A covisible view of a map being triangulated: the planar correspondence
+ * field from the map's entry to this view (DEVICE targets (gh,gw,2) and
+ * confidence (gh,gw); f32 or f64, one dtype per call) and the view's camera. */
+typedef struct {
+  const void* targets;
+  const void* confidence;
+  double rt[9];                /* R^T of the view pose (world-from-camera rotation), row-major */
+  double center[3];            /* view camera centre (Pose.center()) */
+  double fx, fy, cx, cy;       /* view intrinsics */
+} vl_tri_view;
+
+/* One depth map to build: views [view0, view0+nview) of the view array. */
+typedef struct {
+  int32_t grid_w, grid_h, view0, nview;
+  double fx, fy, cx, cy;       /* entry intrinsics (full image) */
+  double sx, sy;               /* width / grid_w, height / grid_h (depthbuild.py:312-313) */
+  double R[9];                 /* entry pose rotation (camera-from-world), row-major */
+  double center[3];            /* entry camera centre */
+  float* depth;                /* DEVICE (gh,gw) z-depth out (0 where invalid) */
+  uint8_t* valid;              /* DEVICE (gh,gw) out */
+} vl_tri_map;
+
+/* TriangulationConfig (depthbuild.py:80-93) */
+typedef struct {
+  double angular_threshold_rad, confidence_threshold, refine_tol;
+  int32_t min_inliers, max_refine_iters;
+} vl_tri_config;
+
+/* replaces depthbuild.build_depth_map (depthbuild.py:249-375) for many maps in
+ * one launch; maps / views are HOST arrays (copied by the call), nview <= 128
+ * per map.  Returns after the maps are written (stream synchronised). */
+int vl_build_depth_maps(vl_ctx* ctx, const vl_tri_map* maps, int32_t nmap, const vl_tri_view* views,
+                        int32_t nviews, int32_t field_f64, const vl_tri_config* cfg, void* stream);
+
+/* An explicit observation set (triangulate_pixel's arguments, depthbuild.py:151-189). */
+typedef struct {
+  double ray[3], center[3];    /* unit reference ray (world) and reference centre */
+  int32_t obs0, nobs;          /* observations [obs0, obs0+nobs) */
+} vl_tri_problem;
+
+typedef struct {
+  double rt[9], center[3];     /* observing view: R^T, centre */
+  double fx, fy, cx, cy;
+  double target[2];            /* matched pixel in the observing view */
+  double confidence;
+} vl_tri_obs;
+
+/* replaces depthbuild.triangulate_pixel / depth_hypothesis (depthbuild.py:104-189)
+ * for many problems: problems / obs DEVICE; depth_out DEVICE [nprob] (ray
+ * depth, NaN if none), count_out DEVICE [nprob] (winning inlier count, 0 if
+ * none), hyp_out DEVICE [total obs] nullable (each observation's depth
+ * hypothesis, NaN where depth_hypothesis returns None). max_obs <= 128. */
+int vl_triangulate_rays(vl_ctx* ctx, const vl_tri_problem* problems, int32_t nprob, const vl_tri_obs* obs,
+                        int32_t max_obs, const vl_tri_config* cfg, double* depth_out, int32_t* count_out,
+                        double* hyp_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,7 +17,7 @@ CSRC = HERE / "csrc"
 OUT_DIR = HERE / "_lib"
 LIB = OUT_DIR / "libvisloc_b200.so"
 HOSTCHECK = OUT_DIR / "libvisloc_hostcheck.so"
-SOURCES = ["vl_capi.cu", "vl_ransac.cu", "vl_score.cu", "vl_lift.cu", "vl_imlc.cu", "vl_retrieval.cu", "vl_mapcodec.cu"]
+SOURCES = ["vl_capi.cu", "vl_ransac.cu", "vl_score.cu", "vl_lift.cu", "vl_imlc.cu", "vl_retrieval.cu", "vl_mapcodec.cu", "vl_tri.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -59,6 +59,35 @@ class DepthCodecJob(C.Structure):
                 ("values", C.c_void_p), ("valid", C.c_void_p), ("out", C.c_void_p)]
 
 
+class TriView(C.Structure):
+    _fields_ = [("targets", C.c_void_p), ("confidence", C.c_void_p), ("rt", C.c_double * 9),
+                ("center", C.c_double * 3), ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double),
+                ("cy", C.c_double)]
+
+
+class TriMap(C.Structure):
+    _fields_ = [("grid_w", C.c_int32), ("grid_h", C.c_int32), ("view0", C.c_int32), ("nview", C.c_int32),
+                ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("sx", C.c_double), ("sy", C.c_double), ("R", C.c_double * 9), ("center", C.c_double * 3),
+                ("depth", C.c_void_p), ("valid", C.c_void_p)]
+
+
+class TriConfig(C.Structure):
+    _fields_ = [("angular_threshold_rad", C.c_double), ("confidence_threshold", C.c_double),
+                ("refine_tol", C.c_double), ("min_inliers", C.c_int32), ("max_refine_iters", C.c_int32)]
+
+
+class TriProblem(C.Structure):
+    _fields_ = [("ray", C.c_double * 3), ("center", C.c_double * 3), ("obs0", C.c_int32), ("nobs", C.c_int32)]
+
+
+class TriObs(C.Structure):
+    _fields_ = [("rt", C.c_double * 9), ("center", C.c_double * 3), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("target", C.c_double * 2), ("confidence", C.c_double)]
+
+
+ctypes_ref = C.byref
+
 LIFT_PLANAR, LIFT_IMLC = 0, 1
 FIELD_BAD_CONF, FIELD_BAD_TARGET = 1, 2
 
@@ -161,6 +190,11 @@ def lib():
         L.vl_reduce_depth_codes.argtypes = [vp, C.POINTER(DepthCodecJob), i32, i32, i32, vp]
         L.vl_quantize_depth.restype = C.c_int
         L.vl_reduce_depth_codes.restype = C.c_int
+        L.vl_build_depth_maps.argtypes = [vp, C.POINTER(TriMap), i32, C.POINTER(TriView), i32, i32,
+                                          C.POINTER(TriConfig), vp]
+        L.vl_triangulate_rays.argtypes = [vp, vp, i32, vp, i32, C.POINTER(TriConfig), vp, vp, vp, vp]
+        L.vl_build_depth_maps.restype = C.c_int
+        L.vl_triangulate_rays.restype = C.c_int
         L.vl_robust_cost.restype = C.c_int
         L.vl_pose_residuals.restype = C.c_int
         for name in ("vl_create", "vl_destroy", "vl_reserve", "vl_pcg64_seed", "vl_ransac_pnp", "vl_profile",
@@ -178,6 +212,7 @@ EXPORTED_SYMBOLS = (
     "vl_decode_depth", "vl_robust_cost", "vl_pose_residuals", "vl_ransac_begin", "vl_ransac_partial_bytes",
     "vl_ransac_step_score", "vl_ransac_step_finish", "vl_ransac_end", "vl_imlc_parse",
     "vl_retrieval_topk", "vl_ransac_pnp_staged", "vl_quantize_depth", "vl_reduce_depth_codes",
+    "vl_build_depth_maps", "vl_triangulate_rays",
 )
 
 STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final", "lift")

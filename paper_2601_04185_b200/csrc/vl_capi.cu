@@ -27,6 +27,7 @@ struct vl_ctx {
       partial, cost32, tile_cnt, sub_pk, sub32, comp_pk;
   DevBuf scratch;  // small standalone-call scratch
   DevBuf lift_meta, lift_blk_count, lift_blk_off, lift_seg_off;  // vl_lift
+  DevBuf tri_meta;                                               // vl_build_depth_maps
   void* h_pinned = nullptr;
   size_t h_pinned_cap = 0;
   // profiling: CUDA-event brackets around every stage launch (vl_profile)
@@ -928,5 +929,83 @@ extern "C" int vl_reduce_depth_codes(vl_ctx* c, const vl_depth_codec_job* jobs, 
   VL_CUDA(c, cudaSetDevice(c->device));
   c->launches += launch_reduce_codes((const CodecJob*)jobs, njobs, factor, new_levels, c->num_sms,
                                      (cudaStream_t)stream);
+  return check_launch(c);
+}
+
+// ---- dense depth triangulation (depthbuild.py:104-441) -----------------------
+namespace vl {
+struct TriMap;
+struct TriView;
+struct TriProblem;
+struct TriObs;
+struct TriConfig {
+  double thr, conf_thr, refine_tol;
+  int32_t min_inliers, max_refine_iters;
+};
+int launch_tri_maps(const TriMap* d_maps, int nmap, int max_pix, int max_views, const TriView* d_views, int f64,
+                    const TriConfig& cfg, int num_sms, cudaStream_t st);
+int launch_tri_rays(const TriProblem* d_probs, int nprob, int max_obs, const TriObs* d_obs, const TriConfig& cfg,
+                    double* depth_out, int* count_out, double* hyp_out, int num_sms, cudaStream_t st);
+}
+static_assert(sizeof(vl_tri_config) == sizeof(vl::TriConfig) && sizeof(vl_tri_view) == 144 && sizeof(vl_tri_map) == 176 &&
+                  sizeof(vl_tri_problem) == 56 && sizeof(vl_tri_obs) == 152, "tri layouts");
+
+static int tri_config(vl_ctx* c, const vl_tri_config* cfg, TriConfig& out) {
+  if (!cfg) return fail(c, VL_ERR_INVALID, "null config");
+  if (!(cfg->angular_threshold_rad > 0)) return fail(c, VL_ERR_INVALID, "angular threshold must be positive");
+  if (cfg->min_inliers < 1) return fail(c, VL_ERR_INVALID, "min_inliers must be >= 1");
+  if (cfg->max_refine_iters < 0) return fail(c, VL_ERR_INVALID, "max_refine_iters must be >= 0");
+  std::memcpy(&out, cfg, sizeof(out));
+  return VL_OK;
+}
+
+extern "C" int vl_build_depth_maps(vl_ctx* c, const vl_tri_map* maps, int32_t nmap, const vl_tri_view* views,
+                                   int32_t nviews, int32_t field_f64, const vl_tri_config* cfg, void* stream) {
+  if (!c || nmap < 0 || nviews < 0 || (nmap && !maps) || (nviews && !views)) return fail(c, VL_ERR_INVALID, "bad argument");
+  TriConfig tc;
+  int rc;
+  if ((rc = tri_config(c, cfg, tc))) return rc;
+  if (nmap == 0) return VL_OK;
+  int max_pix = 0, max_views = 1;
+  for (int m = 0; m < nmap; ++m) {
+    const vl_tri_map& M = maps[m];
+    const std::string tag = "map " + std::to_string(m) + ": ";
+    if (M.grid_w < 1 || M.grid_h < 1 || (int64_t)M.grid_w * M.grid_h > INT32_MAX) return fail(c, VL_ERR_INVALID, tag + "bad grid");
+    if (M.nview < 1) return fail(c, VL_ERR_INVALID, tag + "need at least one correspondence field");
+    if (M.nview > 128) return fail(c, VL_ERR_INVALID, tag + "at most 128 covisible views per map on the device path");
+    if (M.view0 < 0 || (int64_t)M.view0 + M.nview > nviews) return fail(c, VL_ERR_INVALID, tag + "view range out of bounds");
+    if (!M.depth || !M.valid) return fail(c, VL_ERR_INVALID, tag + "null output");
+    max_pix = std::max(max_pix, M.grid_w * M.grid_h);
+    max_views = std::max(max_views, M.nview);
+  }
+  for (int v = 0; v < nviews; ++v)
+    if (!views[v].targets || !views[v].confidence) return fail(c, VL_ERR_INVALID, "view " + std::to_string(v) + ": null field");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t mb = (size_t)nmap * sizeof(vl_tri_map), vb = (size_t)nviews * sizeof(vl_tri_view);
+  if ((rc = ensure(c, c->tri_meta, mb + vb)) || (rc = ensure_host(c, mb + vb))) return rc;
+  std::memcpy(c->h_pinned, maps, mb);
+  std::memcpy((char*)c->h_pinned + mb, views, vb);
+  VL_CUDA(c, cudaMemcpyAsync(c->tri_meta.p, c->h_pinned, mb + vb, cudaMemcpyHostToDevice, st));
+  c->launches += launch_tri_maps((const TriMap*)c->tri_meta.p, nmap, max_pix, max_views,
+                                 (const TriView*)((char*)c->tri_meta.p + mb), field_f64 ? 1 : 0, tc, c->num_sms, st);
+  if ((rc = check_launch(c))) return rc;
+  VL_CUDA(c, cudaStreamSynchronize(st));  // the pinned staging buffer is reused by the next call
+  return VL_OK;
+}
+
+extern "C" int vl_triangulate_rays(vl_ctx* c, const vl_tri_problem* problems, int32_t nprob, const vl_tri_obs* obs,
+                                   int32_t max_obs, const vl_tri_config* cfg, double* depth_out, int32_t* count_out,
+                                   double* hyp_out, void* stream) {
+  if (!c || nprob < 0 || (nprob && (!problems || !depth_out || !count_out))) return fail(c, VL_ERR_INVALID, "bad argument");
+  if (max_obs < 0 || max_obs > 128) return fail(c, VL_ERR_INVALID, "at most 128 observations per problem on the device path");
+  if (max_obs > 0 && !obs) return fail(c, VL_ERR_INVALID, "null observations");
+  TriConfig tc;
+  int rc;
+  if ((rc = tri_config(c, cfg, tc))) return rc;
+  if (nprob == 0) return VL_OK;
+  VL_CUDA(c, cudaSetDevice(c->device));
+  c->launches += launch_tri_rays((const TriProblem*)problems, nprob, std::max(max_obs, 1), (const TriObs*)obs, tc,
+                                 depth_out, count_out, hyp_out, c->num_sms, (cudaStream_t)stream);
   return check_launch(c);
 }

@@ -339,11 +339,87 @@ def mapstore_vectors():
     np.savez_compressed(OUT / "mapstore.npz", **out)
 
 
+def depthbuild_vectors():
+    """Reference build_depth_map (depthbuild.py:249-375) on synth scenes: exact, noisy, outlier-corrupted,
+    f32 fields, many views (V=20, 40); triangulate_pixel / depth_hypothesis on the noisy scene."""
+    from types import SimpleNamespace
+    from visloc.depthbuild import Observation, TriangulationConfig, build_depth_map, depth_hypothesis, \
+        triangulate_pixel
+    from visloc.synth import NoiseSpec, SceneSpec, corrupt, make_scene, oracle_field
+    out = {}
+    cases = [  # (n_cams, seed, spread, grid, sigma, outlier, f32, cfg kwargs)
+        (6, 11, 0.25, 50, 0.0, 0.0, False, {}),
+        (9, 13, 0.45, 40, 0.0, 0.4, False, {}),
+        (6, 11, 0.25, 16, 0.3, 0.2, False, {}),
+        (6, 11, 0.25, 30, 0.5, 0.3, True, {}),
+        (21, 5, 0.5, 24, 0.4, 0.3, False, {"min_inliers": 3}),
+        (41, 6, 0.6, 20, 0.4, 0.3, True, {"angular_threshold_rad": math.radians(1.0)}),
+        (7, 3, 0.3, 20, 1.0, 0.5, False, {"confidence_threshold": 0.5, "max_refine_iters": 3}),
+    ]
+    for ci, (nc, seed, spread, grid, sigma, outl, f32, kw) in enumerate(cases):
+        intr = CameraIntrinsics(70.0, 70.0, 70.0, 70.0, 140, 140)
+        scene = make_scene(SceneSpec(num_cameras=nc, width=140, height=140, camera_spread=spread,
+                                     camera_backoff=0.25, rotation_jitter_deg=3.0, seed=seed, intrinsics=intr))
+        entry = SimpleNamespace(id=scene.view_id(0), pose=scene.cameras[0][0], intrinsics=scene.cameras[0][1])
+        covis = [SimpleNamespace(id=scene.view_id(i), pose=scene.cameras[i][0], intrinsics=scene.cameras[i][1])
+                 for i in range(1, nc)]
+        fields = []
+        for i in range(1, nc):
+            f = oracle_field(scene, 0, i, grid, grid)
+            if sigma > 0 or outl > 0:
+                f = corrupt(f, NoiseSpec(sigma_px=sigma, outlier_fraction=outl), 100 * ci + i)
+            if f32:
+                f.targets = f.targets.astype(np.float32)
+                f.confidence = f.confidence.astype(np.float32)
+            fields.append(f)
+        # a few cells with confidence on the gate boundary
+        fields[0].confidence[0, :3] = [0.05, np.nextafter(0.05, 0), 0.0]
+        cfg = TriangulationConfig(**kw)
+        dm = build_depth_map(entry, covis, fields, cfg)
+        p = f"c{ci}_"
+        out[p + "targets"] = np.stack([f.targets for f in fields])
+        out[p + "conf"] = np.stack([f.confidence for f in fields])
+        out[p + "scale"] = np.array([fields[0].scale_x, fields[0].scale_y])
+        out[p + "q"] = np.stack([entry.pose.q] + [c.pose.q for c in covis])
+        out[p + "t"] = np.stack([entry.pose.t] + [c.pose.t for c in covis])
+        out[p + "R"] = np.stack([entry.pose.R] + [c.pose.R for c in covis])
+        out[p + "C"] = np.stack([entry.pose.center()] + [c.pose.center() for c in covis])
+        out[p + "intr"] = np.array([[c.intrinsics.fx, c.intrinsics.fy, c.intrinsics.cx, c.intrinsics.cy,
+                                     c.intrinsics.width, c.intrinsics.height] for c in [entry] + covis])
+        out[p + "cfg"] = np.array([cfg.angular_threshold_rad, cfg.min_inliers, cfg.confidence_threshold,
+                                   cfg.max_refine_iters, cfg.refine_tol])
+        out[p + "depth"], out[p + "valid"] = dm.values, dm.valid
+        if ci == 2:  # scalar path on every cell
+            sx, sy = entry.intrinsics.width / grid, entry.intrinsics.height / grid
+            sd, sn, hyp = [], [], []
+            for row in range(grid):
+                for col in range(grid):
+                    obs = []
+                    for i, f in enumerate(fields):
+                        cc = float(f.confidence[row, col])
+                        if cc >= cfg.confidence_threshold and cc > 0:
+                            obs.append(Observation(covis[i].pose, covis[i].intrinsics, f.targets[row, col], cc))
+                    px = np.array([(col + 0.5) * sx, (row + 0.5) * sy])
+                    k = np.array([(px[0] - entry.intrinsics.cx) / entry.intrinsics.fx,
+                                  (px[1] - entry.intrinsics.cy) / entry.intrinsics.fy, 1.0])
+                    ray = entry.pose.R.T @ (k / np.linalg.norm(k))
+                    r = triangulate_pixel(ray, entry.pose.center(), obs, cfg)
+                    sd.append(np.nan if r is None else r[0])
+                    sn.append(0 if r is None else r[1])
+                    hyp.append([np.nan if (h := depth_hypothesis(ray, entry.pose.center(), o)) is None else h
+                                for o in obs] + [np.inf] * (len(fields) - len(obs)))
+            out[p + "scalar_depth"], out[p + "scalar_count"] = np.array(sd), np.array(sn)
+            out[p + "scalar_hyp"] = np.array(hyp)
+    out["n"] = np.array(len(cases))
+    np.savez_compressed(OUT / "depthbuild.npz", **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `make_golden.py mapstore`
         for name in sys.argv[1:]:
             globals()[f"{name}_vectors"]()
         sys.exit(0)
+    depthbuild_vectors()
     mapstore_vectors()
     retrieval_vectors()
     imlc_vectors()
