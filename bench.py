@@ -71,6 +71,33 @@ LIFT_WORKLOADS = {
 }
 LIFT_SEED = 77
 
+MAP_WORKLOADS = {
+    "map": dict(name="Mapping (SURVEY 8f rows 3-4): dense depth triangulation + 8-bit log quantisation of "
+                     "64 db images x 20 covisible views x 83x83 f32 fields, default TriangulationConfig",
+                E=64, V=20, g=83, cpu_maps_per_core=1),
+}
+MAP_SEED = 5
+VOTE_FLOP = 27  # fp64 ops of one (hypothesis, view) angular vote test
+
+
+def _cpu_map_worker(job):
+    """Oracle port of build_depth_map + quantize_depth for one entry of the mapping workload."""
+    i, wl, seed0 = job
+    from oracle import depthbuild as od
+    from oracle import mapstore as om
+    from synth_inputs import mapping_scene
+    (e, cv, fl), = mapping_scene(wl["E"], wl["V"], wl["g"], seed=seed0, only=[i])
+    I = e.intrinsics
+    irow = lambda c: [c.intrinsics.fx, c.intrinsics.fy, c.intrinsics.cx, c.intrinsics.cy,  # noqa: E731
+                      c.intrinsics.width, c.intrinsics.height]
+    t0 = time.perf_counter()
+    d, v = od.build_depth_map(np.stack([f.targets for f in fl]), np.stack([f.confidence for f in fl]), None,
+                              e.pose.R, e.pose.center(), irow(e), np.stack([c.pose.R for c in cv]),
+                              np.stack([c.pose.center() for c in cv]), [irow(c) for c in cv],
+                              math.radians(2.0), 4, 0.05, 20, 1e-8)
+    om.quantize(d, v)
+    return d.size, time.perf_counter() - t0
+
 
 def _cpu_lift_worker(job):
     """Oracle port of localize() for one generator-B query (lift + ransac)."""
@@ -136,13 +163,13 @@ def cpu_sample(wl, seed0, n_queries, cores):
     for k in saved:
         os.environ[k] = "1"
     lifted = "K" in wl
-    worker = _cpu_lift_worker if lifted else _cpu_worker
+    worker = _cpu_map_worker if "E" in wl else (_cpu_lift_worker if lifted else _cpu_worker)
     n_queries = max(1, int(n_queries))
     cores = min(cores, n_queries)
     try:
         ctx = mp.get_context("spawn")
         with ctx.Pool(cores) as pool:
-            if not lifted:
+            if not lifted and "E" not in wl:
                 pool.map(_cpu_worker, [(0, dict(wl, n=64, max_iterations=wl.get("batch", 1000)), seed0)] * cores)
             t0 = time.perf_counter()
             res = pool.map(worker, [(qi, wl, seed0) for qi in range(n_queries)])
@@ -167,6 +194,9 @@ def run_reference_arm(args, wl):
     if rank != 0:
         return
     cores = host_cores()
+    if "E" in wl:
+        run_map_reference_arm(args, wl, cores)
+        return
     nq = max(1, int(cores * wl["cpu_queries_per_core"]))
     seed0 = LIFT_SEED if "K" in wl else 3000
     for _ in range(args.warmup):
@@ -189,6 +219,30 @@ def run_reference_arm(args, wl):
         "queries_per_s": nq / statistics.mean(walls),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_map_reference_arm(args, wl, cores):
+    nm = min(wl["E"], max(1, int(cores * wl["cpu_maps_per_core"])))
+    for _ in range(args.warmup):
+        cpu_sample(wl, MAP_SEED, nm, cores)
+    px = walls = 0.0
+    ws = []
+    for _ in range(args.steps):
+        n, wall = cpu_sample(wl, MAP_SEED, nm, cores)
+        px += n
+        walls += wall
+        ws.append(wall)
+    value = px / walls
+    line = {
+        "impl": "reference", "metric": "depth-map px/s", "value": value, "unit": "px/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(ws),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "maps_per_step": nm},
+        "cpu_baseline": {"value": value, "unit": "px/s", "cores": min(cores, nm), "kind": "port",
+                         "sample": f"{nm} maps of the workload per step (1/core), oracle port"},
+        "e2e": {"value": value, "unit": "px/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -434,6 +488,109 @@ def run_lift_bench(args, wl, rank, world, local, dist):
         print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- GPU arm: mapping
+def run_map_bench(args, wl, rank, world, local, dist):
+    """Mapping: a step = triangulate every entry's depth map (one vl_build_depth_maps
+    launch) + quantise them all (one vl_quantize_depth launch), fields resident
+    in HBM (value) or uploaded from pinned host memory with depth codes read
+    back (e2e, build_map_from_fields's device work)."""
+    import torch
+    from paper_2601_04185_b200 import _lib
+    from paper_2601_04185_b200.depthbuild import DepthBuildPlan, TriangulationConfig
+    from paper_2601_04185_b200.mapstore import quantize_depth_device
+    from synth_inputs import mapping_scene
+
+    seed0 = MAP_SEED + 1000 * rank
+    jobs = mapping_scene(wl["E"], wl["V"], wl["g"], seed=seed0)
+    cfg = TriangulationConfig()
+    ctx = _lib.context(local)
+    stream = torch.cuda.current_stream()
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    plan = DepthBuildPlan(jobs, cfg)
+    for _ in range(args.warmup):
+        codes = quantize_depth_device(plan.run().device_maps())
+    valid_frac = float(plan.valid.float().mean().item())
+
+    def step():
+        quantize_depth_device(plan.run().device_maps())
+
+    ms, launches, _, clocks = timed_region(ctx, stream, sync_all, step, args.steps, False)
+    # kernel-only time of the triangulation launch (live CUDA events on the launching stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sync_all()
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.run()
+    e1.record(stream)
+    sync_all()
+    tri_ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    px = plan.pixels
+    value = px * world * args.steps / (ms_max / 1e3)
+
+    e2e = None
+    if not args.no_e2e:
+        def e2e_step():
+            p = DepthBuildPlan(jobs, cfg).run()
+            cs = quantize_depth_device(p.device_maps())
+            return [c.cpu() for c in cs], p.field_bytes
+        e2e_step()
+        sync_all()
+        e0.record(stream)
+        for _ in range(args.steps):
+            out, h2d = e2e_step()
+        e1.record(stream)
+        sync_all()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": px * world * args.steps / (float(et.item()) / 1e3), "unit": "px/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(sum(c.numel() for c in out))}
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    props = torch.cuda.get_device_properties(local)
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp64_peak = props.multi_processor_count * 64 * 2 * sm_max * 1e6 / 1e12
+    votes = px * wl["V"] * wl["V"]
+    achieved = votes * VOTE_FLOP / (tri_ms / 1e3) / 1e12
+    roof = {"bound": "fp64", "kernel": "k_tri_map", "achieved": achieved, "peak": round(fp64_peak, 2),
+            "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+            "peak_source": "derived SMs*64*2*sm_max_mhz (MEASURED_PEAKS.json has no FP64 entry)",
+            "flop_per_vote": VOTE_FLOP, "votes_per_s": votes / (tri_ms / 1e3),
+            "note": "vote-stage FLOPs only (the Newton refinement is excluded from the count)",
+            "traffic": None, "tri_ms_per_step": tri_ms, "share_of_step": tri_ms / (ms / args.steps)}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = host_cores()
+        nm = min(wl["E"], cores * wl["cpu_maps_per_core"])
+        n, wall = cpu_sample(wl, MAP_SEED, nm, cores)
+        cpu = {"value": n / wall, "unit": "px/s", "cores": min(cores, nm), "kind": "port",
+               "sample": f"{nm} maps of the same workload (oracle build_depth_map + quantize), 1 process/map"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "depth-map px/s", "value": value, "unit": "px/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl["name"], "maps_per_gpu": wl["E"], "views": wl["V"], "grid": wl["g"],
+                       "pixels_per_step": px, "valid_frac": valid_frac,
+                       "l2": f"fields {plan.field_bytes / 1e6:.0f} MB/GPU resident",
+                       "parallelism": f"map-sharded x{world}, no collective"},
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
+        }), flush=True)
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -441,13 +598,16 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(LIFT_WORKLOADS), default="c3")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(LIFT_WORKLOADS) + sorted(MAP_WORKLOADS),
+                    default="c3")
     ap.add_argument("--queries", type=int, default=None, help="override queries per GPU")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     lifted = args.workload in LIFT_WORKLOADS
-    wl = dict(LIFT_WORKLOADS[args.workload] if lifted else WORKLOADS[args.workload])
+    mapping = args.workload in MAP_WORKLOADS
+    wl = dict(MAP_WORKLOADS[args.workload] if mapping else
+              LIFT_WORKLOADS[args.workload] if lifted else WORKLOADS[args.workload])
     if args.queries:
         wl["queries"] = args.queries
     if args.impl == "reference":
@@ -465,8 +625,8 @@ def main():
     from paper_2601_04185_b200 import _lib
     from paper_2601_04185_b200.geometry import CameraIntrinsics
     from paper_2601_04185_b200.posest import RansacConfig, ransac_pnp_device, ransac_pnp_host
-    if lifted:
-        run_lift_bench(args, wl, rank, world, local, dist)
+    if lifted or mapping:
+        (run_map_bench if mapping else run_lift_bench)(args, wl, rank, world, local, dist)
         if world > 1:
             dist.destroy_process_group()
         return

@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 #include "vl_common.cuh"
 
 namespace vl {
@@ -183,6 +184,60 @@ __device__ __forceinline__ void point_on_ray(const double* cref, double d, const
   for (int i = 0; i < 3; ++i) X[i] = dadd(cref[i], dmul(d, ray[i]));
 }
 
+// Sum over the pixel's views of per-lane terms, in numpy's pairwise order,
+// identical in every lane of the group.  vec mode (all V positions, zeros
+// off the inlier set): the 8 partial sums r_j = x_j + x_{j+8} + ... are
+// gathered by lanes j (mod 8) with one shuffle per 8 elements, combined by a
+// 3-level xor butterfly (== ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), addition
+// being commutative) and the n%8 tail is added in order.  scalar mode (the
+// inlier subset only, triangulate_pixel): serial gather through PwSum.
+template <int G, int OPL>
+__device__ __forceinline__ double group_sum(const double* term, const uint32_t* inl, int V, int nin, int lane,
+                                            unsigned gmask, bool scalar_mode) {
+  if (scalar_mode) {
+    PwSum acc;
+    acc.init(nin);
+#pragma unroll
+    for (int s = 0; s < OPL; ++s)
+      for (int l = 0; l < G; ++l) {
+        const int v = s * G + l;
+        if (v >= V) break;
+        const double x = __shfl_sync(gmask, term[s], l, G);
+        if ((inl[s] >> l) & 1u) acc.add(x);
+      }
+    return acc.get();
+  }
+  const int n = V;
+  if (n < 8) {  // sequential from 0 (all in slot 0: G >= 8)
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = dadd(res, __shfl_sync(gmask, term[0], i, G));
+    return res;
+  }
+  const int tail = n - (n & 7);
+  double r = 0.0;
+#pragma unroll
+  for (int s = 0; s < OPL; ++s)
+#pragma unroll
+    for (int b = 0; b < G; b += 8) {
+      const int base = s * G + b;  // elements base .. base+7
+      if (base < tail) {
+        const double v = __shfl_sync(gmask, term[s], b + (lane & 7), G);
+        r = base == 0 ? v : dadd(r, v);
+      }
+    }
+  r = dadd(r, __shfl_xor_sync(gmask, r, 1, G));
+  r = dadd(r, __shfl_xor_sync(gmask, r, 2, G));
+  r = dadd(r, __shfl_xor_sync(gmask, r, 4, G));
+#pragma unroll
+  for (int s = 0; s < OPL; ++s)
+    for (int l = 0; l < G; ++l) {
+      const int i = s * G + l;
+      if (i >= n) break;
+      if (i >= tail) r = dadd(r, __shfl_sync(gmask, term[s], l, G));
+    }
+  return r;
+}
+
 // Weighted squared angular error (scalar_mode: sum over the inlier subset only)
 template <int G, int OPL>
 __device__ double tri_cost(const LaneObs<OPL>& o, const uint32_t* inl, int V, int nin, double d, const double* ray,
@@ -202,17 +257,7 @@ __device__ double tri_cost(const LaneObs<OPL>& o, const uint32_t* inl, int V, in
       term[s] = dmul(dmul(o.conf[s], ang), ang);
     }
   }
-  PwSum acc;
-  acc.init(scalar_mode ? nin : V);
-#pragma unroll
-  for (int s = 0; s < OPL; ++s)
-    for (int l = 0; l < G; ++l) {
-      const int v = s * G + l;
-      if (v >= V) break;
-      const double x = __shfl_sync(gmask, term[s], l, G);
-      if (!scalar_mode || ((inl[s] >> l) & 1u)) acc.add(x);
-    }
-  return acc.get();
+  return group_sum<G, OPL>(term, inl, V, nin, lane, gmask, scalar_mode);
 }
 
 template <int G, int OPL>
@@ -247,17 +292,7 @@ __device__ double tri_grad(const LaneObs<OPL>& o, const uint32_t* inl, int V, in
       term[s] = dmul(dmul(dmul(2.0, o.conf[s]), theta), th_p);
     }
   }
-  PwSum acc;
-  acc.init(scalar_mode ? nin : V);
-#pragma unroll
-  for (int s = 0; s < OPL; ++s)
-    for (int l = 0; l < G; ++l) {
-      const int v = s * G + l;
-      if (v >= V) break;
-      const double x = __shfl_sync(gmask, term[s], l, G);
-      if (!scalar_mode || ((inl[s] >> l) & 1u)) acc.add(x);
-    }
-  return acc.get();
+  return group_sum<G, OPL>(term, inl, V, nin, lane, gmask, scalar_mode);
 }
 
 // Voting + refinement of one pixel; returns the winner's inlier count (0 if
@@ -451,21 +486,33 @@ __global__ void __launch_bounds__(kTriThreads) k_tri_rays(const TriProblem* __re
   }
 }
 
+// One pixel per warp: the Newton refinement diverges across pixels, so
+// packing several pixels in a warp serialises them (measured, V=20, 441k px:
+// G=32 7.8 ms, G=16 17.7 ms, G=8 21.5 ms).
 static void pick(int maxv, int& G, int& OPL) {
-  if (maxv <= 8) G = 8, OPL = 1;
-  else if (maxv <= 16) G = 16, OPL = 1;
-  else if (maxv <= 32) G = 32, OPL = 1;
-  else if (maxv <= 64) G = 32, OPL = 2;
-  else G = 32, OPL = 4;
+  G = 32;
+  OPL = std::max(1, (maxv + 31) / 32);
+  if (const char* e = getenv("VISLOC_TRI_G")) {  // tuning override: lanes per pixel (8, 16, 32)
+    const int g = atoi(e);
+    if (g == 8 || g == 16 || g == 32) {
+      G = g;
+      OPL = std::max(1, (maxv + g - 1) / g);
+      if (OPL > 4) G = 32, OPL = (maxv + 31) / 32;
+    }
+  }
 }
 
+#define VL_TRI_CASE(KERNEL, GG, OO, GRID, ...) \
+  else if (G == GG && OPL == OO) KERNEL<GG, OO><<<GRID, kTriThreads, 0, st>>>(__VA_ARGS__);
 #define VL_TRI_DISPATCH(KERNEL, GRID, ...)                                                      \
   do {                                                                                          \
-    if (G == 8) KERNEL<8, 1><<<GRID, kTriThreads, 0, st>>>(__VA_ARGS__);                        \
-    else if (G == 16) KERNEL<16, 1><<<GRID, kTriThreads, 0, st>>>(__VA_ARGS__);                 \
-    else if (OPL == 1) KERNEL<32, 1><<<GRID, kTriThreads, 0, st>>>(__VA_ARGS__);                \
-    else if (OPL == 2) KERNEL<32, 2><<<GRID, kTriThreads, 0, st>>>(__VA_ARGS__);                \
-    else KERNEL<32, 4><<<GRID, kTriThreads, 0, st>>>(__VA_ARGS__);                              \
+    if (false) {}                                                                               \
+    VL_TRI_CASE(KERNEL, 8, 1, GRID, __VA_ARGS__) VL_TRI_CASE(KERNEL, 8, 2, GRID, __VA_ARGS__)    \
+    VL_TRI_CASE(KERNEL, 8, 3, GRID, __VA_ARGS__) VL_TRI_CASE(KERNEL, 8, 4, GRID, __VA_ARGS__)    \
+    VL_TRI_CASE(KERNEL, 16, 1, GRID, __VA_ARGS__) VL_TRI_CASE(KERNEL, 16, 2, GRID, __VA_ARGS__)  \
+    VL_TRI_CASE(KERNEL, 16, 3, GRID, __VA_ARGS__) VL_TRI_CASE(KERNEL, 16, 4, GRID, __VA_ARGS__)  \
+    VL_TRI_CASE(KERNEL, 32, 1, GRID, __VA_ARGS__) VL_TRI_CASE(KERNEL, 32, 2, GRID, __VA_ARGS__)  \
+    VL_TRI_CASE(KERNEL, 32, 3, GRID, __VA_ARGS__) VL_TRI_CASE(KERNEL, 32, 4, GRID, __VA_ARGS__)  \
   } while (0)
 
 int launch_tri_maps(const TriMap* d_maps, int nmap, int max_pix, int max_views, const TriView* d_views, int f64,

@@ -31,7 +31,7 @@ from .localizer import DepthMap
 from .retrieval import DescriptorIndex
 
 __all__ = [
-    "DepthBuildReport", "DepthMap", "Observation", "TriangulationConfig", "build_depth_map", "build_depth_maps",
+    "DepthBuildPlan", "DepthBuildReport", "DepthMap", "Observation", "TriangulationConfig", "build_depth_map", "build_depth_maps",
     "build_map_from_fields", "depth_hypothesis", "select_covisible", "triangulate_pixel",
 ]
 
@@ -169,71 +169,101 @@ def _check_job(entry, covis, fields):
     return gh, gw
 
 
+class DepthBuildPlan:
+    """Many entries' fields resident in HBM, ready to triangulate (the device-resident path).
+
+    Construction does the host work once (checks, field packing + one H2D,
+    map / view records); ``run()`` launches ``vl_build_depth_maps`` into the
+    plan's device outputs ``depth`` (f32) / ``valid`` (u8), packed map after map."""
+
+    def __init__(self, jobs, cfg: TriangulationConfig):
+        import torch
+        self.jobs = list(jobs)
+        self.cfg = cfg
+        self.shapes = [_check_job(*j) for j in self.jobs]
+        _lib.context()
+        fields = [f for _, _, fl in self.jobs for f in fl]
+        self.f64 = any(np.asarray(f.confidence).dtype != np.float32 or np.asarray(f.targets).dtype != np.float32
+                       for f in fields)
+        dt = np.float64 if self.f64 else np.float32
+        tg = [np.ascontiguousarray(f.targets, dtype=dt).reshape(-1) for f in fields]
+        cf = [np.ascontiguousarray(f.confidence, dtype=dt).reshape(-1) for f in fields]
+        t_off = np.concatenate([[0], np.cumsum([a.size for a in tg])]).astype(np.int64)
+        c_off = np.concatenate([[0], np.cumsum([a.size for a in cf])]).astype(np.int64)
+        self.T = torch.from_numpy(np.concatenate(tg) if tg else np.zeros(1, dt)).pin_memory().cuda(non_blocking=True)
+        self.C = torch.from_numpy(np.concatenate(cf) if cf else np.zeros(1, dt)).pin_memory().cuda(non_blocking=True)
+        self.field_bytes = int(self.T.numel() + self.C.numel()) * (8 if self.f64 else 4)
+        item = 8 if self.f64 else 4
+        self.npix = [h * w for h, w in self.shapes]
+        self.p_off = np.concatenate([[0], np.cumsum(self.npix)]).astype(np.int64)
+        tot = max(int(self.p_off[-1]), 1)
+        self.depth = torch.empty(tot, dtype=torch.float32, device="cuda")
+        self.valid = torch.empty(tot, dtype=torch.uint8, device="cuda")
+        self.views = (_lib.TriView * max(len(fields), 1))()
+        self.maps = (_lib.TriMap * max(len(self.jobs), 1))()
+        self.nviews = len(fields)
+        v = 0
+        for m, ((entry, covis, fl), (gh, gw)) in enumerate(zip(self.jobs, self.shapes)):
+            M = self.maps[m]
+            intr = entry.intrinsics
+            M.grid_w, M.grid_h, M.view0, M.nview = gw, gh, v, len(fl)
+            M.fx, M.fy, M.cx, M.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
+            M.sx, M.sy = intr.width / gw, intr.height / gh
+            R = np.asarray(entry.pose.R, dtype=np.float64)
+            for i in range(9):
+                M.R[i] = float(R.flat[i])
+            c = entry.pose.center()
+            for i in range(3):
+                M.center[i] = float(c[i])
+            M.depth = self.depth.data_ptr() + int(self.p_off[m]) * 4
+            M.valid = self.valid.data_ptr() + int(self.p_off[m])
+            for cov, f in zip(covis, fl):
+                W = self.views[v]
+                W.targets = self.T.data_ptr() + int(t_off[v]) * item
+                W.confidence = self.C.data_ptr() + int(c_off[v]) * item
+                _fill_cam(W, cov.pose, cov.intrinsics)
+                v += 1
+        self._cfg = _cfg_c(cfg)
+
+    @property
+    def pixels(self) -> int:
+        return int(self.p_off[-1])
+
+    def run(self):
+        ctx = _lib.context()
+        if not self.jobs:
+            return self
+        rc = _lib.lib().vl_build_depth_maps(ctx.handle, self.maps, len(self.jobs), self.views, self.nviews,
+                                            1 if self.f64 else 0, _lib.ctypes_ref(self._cfg), _lib.stream_ptr())
+        ctx.check(rc, "vl_build_depth_maps")
+        return self
+
+    def device_maps(self):
+        """[(depth (gh,gw) f32, valid (gh,gw) u8)] CUDA tensor views of the outputs."""
+        out = []
+        for m, (gh, gw) in enumerate(self.shapes):
+            sl = slice(int(self.p_off[m]), int(self.p_off[m + 1]))
+            out.append((self.depth[sl].view(gh, gw), self.valid[sl].view(gh, gw)))
+        return out
+
+    def host_maps(self) -> list:
+        dh, vh = self.depth.cpu().numpy(), self.valid.cpu().numpy().astype(bool)
+        out = []
+        for m, ((entry, _, _), (gh, gw)) in enumerate(zip(self.jobs, self.shapes)):
+            sl = slice(int(self.p_off[m]), int(self.p_off[m + 1]))
+            out.append(DepthMap(values=dh[sl].reshape(gh, gw).copy(), valid=vh[sl].reshape(gh, gw).copy(),
+                                intrinsics=entry.intrinsics))
+        return out
+
+
 def build_depth_maps(jobs, cfg: TriangulationConfig, device_out: bool = False) -> list:
     """``build_depth_map`` of many entries in one launch.
 
     ``jobs``: sequence of (entry, covisible_entries, fields).  Returns
     DepthMaps (host arrays), or (depth f32, valid u8) CUDA tensor pairs with
     ``device_out=True``."""
-    import torch
-    jobs = list(jobs)
-    shapes = [_check_job(*j) for j in jobs]
-    if not jobs:
-        return []
-    ctx = _lib.context()
-    fields = [f for _, _, fl in jobs for f in fl]
-    f64 = any(np.asarray(f.confidence).dtype != np.float32 or np.asarray(f.targets).dtype != np.float32
-              for f in fields)
-    dt = np.float64 if f64 else np.float32
-    tg = [np.ascontiguousarray(f.targets, dtype=dt).reshape(-1) for f in fields]
-    cf = [np.ascontiguousarray(f.confidence, dtype=dt).reshape(-1) for f in fields]
-    t_off = np.concatenate([[0], np.cumsum([a.size for a in tg])]).astype(np.int64)
-    c_off = np.concatenate([[0], np.cumsum([a.size for a in cf])]).astype(np.int64)
-    T = torch.from_numpy(np.concatenate(tg)).pin_memory().cuda(non_blocking=True)
-    Cf = torch.from_numpy(np.concatenate(cf)).pin_memory().cuda(non_blocking=True)
-    item = 8 if f64 else 4
-    npix = [h * w for h, w in shapes]
-    p_off = np.concatenate([[0], np.cumsum(npix)]).astype(np.int64)
-    depth = torch.empty(max(int(p_off[-1]), 1), dtype=torch.float32, device="cuda")
-    valid = torch.empty(max(int(p_off[-1]), 1), dtype=torch.uint8, device="cuda")
-    views = (_lib.TriView * len(fields))()
-    maps = (_lib.TriMap * len(jobs))()
-    v = 0
-    for m, ((entry, covis, fl), (gh, gw)) in enumerate(zip(jobs, shapes)):
-        M = maps[m]
-        intr = entry.intrinsics
-        M.grid_w, M.grid_h, M.view0, M.nview = gw, gh, v, len(fl)
-        M.fx, M.fy, M.cx, M.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
-        M.sx, M.sy = intr.width / gw, intr.height / gh
-        R = np.asarray(entry.pose.R, dtype=np.float64)
-        for i in range(9):
-            M.R[i] = float(R.flat[i])
-        c = entry.pose.center()
-        for i in range(3):
-            M.center[i] = float(c[i])
-        M.depth = depth.data_ptr() + int(p_off[m]) * 4
-        M.valid = valid.data_ptr() + int(p_off[m])
-        for cov, f in zip(covis, fl):
-            W = views[v]
-            W.targets = T.data_ptr() + int(t_off[v]) * item
-            W.confidence = Cf.data_ptr() + int(c_off[v]) * item
-            _fill_cam(W, cov.pose, cov.intrinsics)
-            v += 1
-    rc = _lib.lib().vl_build_depth_maps(ctx.handle, maps, len(jobs), views, len(fields), 1 if f64 else 0,
-                                        _lib.ctypes_ref(_cfg_c(cfg)), _lib.stream_ptr())
-    ctx.check(rc, "vl_build_depth_maps")
-    outs = []
-    if device_out:
-        for m, (gh, gw) in enumerate(shapes):
-            sl = slice(int(p_off[m]), int(p_off[m + 1]))
-            outs.append((depth[sl].view(gh, gw), valid[sl].view(gh, gw)))
-        return outs
-    dh, vh = depth.cpu().numpy(), valid.cpu().numpy().astype(bool)
-    for m, ((entry, _, _), (gh, gw)) in enumerate(zip(jobs, shapes)):
-        sl = slice(int(p_off[m]), int(p_off[m + 1]))
-        outs.append(DepthMap(values=dh[sl].reshape(gh, gw).copy(), valid=vh[sl].reshape(gh, gw).copy(),
-                             intrinsics=entry.intrinsics))
-    return outs
+    plan = DepthBuildPlan(jobs, cfg).run()
+    return plan.device_maps() if device_out else plan.host_maps()
 
 
 def build_depth_map(entry, covisible_entries: Sequence, fields: Sequence, cfg: TriangulationConfig,

@@ -39,7 +39,7 @@ from .localizer import DEFAULT_D_MAX, DEFAULT_D_MIN, DepthMap, QuantizedDepthMap
 
 __all__ = [
     "DEFAULT_D_MAX", "DEFAULT_D_MIN", "DepthMap", "Map", "MapEntry", "QuantizedDepthMap", "dequantize_depth",
-    "quantize_depth", "quantize_depth_batch", "quantize_thresholds", "reduce_depth_codes", "reduce_map",
+    "quantize_depth", "quantize_depth_batch", "quantize_depth_device", "quantize_thresholds", "reduce_depth_codes", "reduce_map",
 ]
 
 _F32_MAX_BITS = 0x7F7FFFFF
@@ -193,6 +193,44 @@ def quantize_depth_batch(depths, d_min: float = DEFAULT_D_MIN, d_max: float = DE
         cls = _qclass(d)
         res.append(cls(codes=c, d_min=d_min, d_max=d_max, levels=levels, intrinsics=d.intrinsics))
     return res
+
+
+def quantize_depth_device(maps, d_min: float = DEFAULT_D_MIN, d_max: float = DEFAULT_D_MAX, levels: int = 255):
+    """Device-resident ``quantize_depth`` of many maps in one launch.
+
+    ``maps``: [(depth (h,w) f32 or f16 CUDA tensor, valid (h,w) u8/bool CUDA
+    tensor)], e.g. ``DepthBuildPlan.device_maps()``.  Returns code tensors
+    ((h,w) uint8, or int16 holding the u16 codes when levels > 255)."""
+    import torch
+    _check_range(d_min, d_max)
+    levels = int(levels)
+    _levels_ok(levels)
+    maps = list(maps)
+    if not maps:
+        return []
+    ctx = _lib.context()
+    sizes = [int(d.numel()) for d, _ in maps]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    out16 = levels > 255
+    out = torch.empty(max(int(off[-1]), 1), dtype=torch.int16 if out16 else torch.uint8, device="cuda")
+    esz = 2 if out16 else 1
+    jobs = (_lib.DepthCodecJob * len(maps))()
+    for k, (d, v) in enumerate(maps):
+        if d.dim() != 2 or tuple(v.shape) != tuple(d.shape) or not d.is_contiguous() or not v.is_contiguous():
+            raise ValueError("values and valid must be equal 2-D contiguous shapes")
+        if d.dtype not in (torch.float32, torch.float16) or v.element_size() != 1:
+            raise ValueError("depth must be float32/float16 and valid 1 byte per pixel")
+        j = jobs[k]
+        j.height, j.width = d.shape
+        j.kind = 1 if d.dtype == torch.float16 else 0
+        j.levels = levels
+        j.values = d.data_ptr()
+        j.valid = v.data_ptr()
+        j.out = out.data_ptr() + int(off[k]) * esz
+    thr = _device_thresholds(d_min, d_max, levels)
+    rc = _lib.lib().vl_quantize_depth(ctx.handle, jobs, len(maps), thr.data_ptr(), levels, _lib.stream_ptr())
+    ctx.check(rc, "vl_quantize_depth")
+    return [out[int(off[k]):int(off[k + 1])].view(tuple(maps[k][0].shape)) for k in range(len(maps))]
 
 
 def _qclass(depth):

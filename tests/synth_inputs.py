@@ -221,6 +221,38 @@ def lifted_scene(K, Q, g, seed=0, depth_kind="f32", outlier_frac=0.7, sigma=1.0,
     return vmap, jobs, (depth_cache if depth_kind != "u8" else None)
 
 
+def mapping_scene(E, V, g, seed=0, sigma=0.5, outlier_frac=0.3, only=None):
+    """Mapping workload on the plane scene: E posed database images, entry i
+    triangulated against the V next cameras (cyclic) with f32 fields i -> j.
+    Returns [(entry, covisible, fields)] (``only`` selects entries; each entry's
+    fields come from its own generator so subsets rebuild identically)."""
+    from paper_2601_04185_b200.geometry import CameraIntrinsics, Pose, matrix_to_quat
+    from paper_2601_04185_b200.matchio import CorrespondenceField
+    sc = PlaneScene(seed=seed)
+    intr = CameraIntrinsics(sc.f, sc.f, sc.c, sc.c, sc.W, sc.W)
+
+    class Entry:
+        pass
+
+    ents = []
+    for k in range(E):
+        cam = sc.camera()
+        e = Entry()
+        e.id, e.cam, e.intrinsics = f"db{k:04d}", cam, intr
+        e.pose = Pose(matrix_to_quat(cam[0]), cam[1])
+        ents.append(e)
+    jobs = []
+    for i in (range(E) if only is None else only):
+        rng = np.random.default_rng([seed, 11, i])
+        covis = [ents[(i + 1 + k) % E] for k in range(V)]
+        fields = []
+        for c in covis:
+            t, cf, s = sc.field(ents[i].cam, c.cam, g, rng, sigma, outlier_frac)
+            fields.append(CorrespondenceField(ents[i].id, c.id, t, cf, s, s))
+        jobs.append((ents[i], covis, fields))
+    return jobs
+
+
 def batch_a(Q, n, outlier_frac, sigma, seed0):
     """Q generator-A queries with per-query random GT poses (bench C1/C3/C4 inputs)."""
     pxs, Xs, ws = [], [], []
