@@ -74,6 +74,9 @@ static_assert(sizeof(TriView) == 144 && sizeof(TriMap) == 176 && sizeof(TriProbl
                   sizeof(TriObs) == 152 && sizeof(TriConfig) == 32, "C ABI layouts (visloc_b200.h)");
 
 constexpr int kTriThreads = 128;
+#ifndef VL_TRI_MINB
+#define VL_TRI_MINB 1  // min resident CTAs per SM for the map kernel (register cap)
+#endif
 constexpr double kParallelTol = 1e-12;  // depthbuild.py:42
 
 VL_HD double ddiv(double a, double b) {
@@ -386,7 +389,7 @@ __device__ __forceinline__ double ld(const void* p, int64_t i) {
 }
 
 template <int G, int OPL>
-__global__ void __launch_bounds__(kTriThreads) k_tri_map(const TriMap* __restrict__ maps,
+__global__ void __launch_bounds__(kTriThreads, (OPL == 1 ? VL_TRI_MINB : 1)) k_tri_map(const TriMap* __restrict__ maps,
                                                          const TriView* __restrict__ views, int field_f64,
                                                          TriConfig cfg) {
   const TriMap& M = maps[blockIdx.y];
