@@ -319,7 +319,7 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
       S.active = 1;
       S.best_cost = INFINITY;
       S.best.q[0] = 1.0;
-      nsub_tot += S.nsub;
+      nsub_tot += S.nsub + (S.nsub & 1);  // even offsets: fp32 records are stored in pairs
       ncomp += n;
       max_split = std::max(max_split, S.nsplit);
     }
@@ -341,7 +341,7 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
         (rc = ensure(c, c->cost32, (size_t)Qn * HCAP * sizeof(float))) ||
         (rc = ensure(c, c->tile_cnt, (size_t)Qn * ntile * sizeof(int))) ||
         (rc = ensure(c, c->sub_pk, nsub_tot * 3 * sizeof(double2))) ||
-        (rc = ensure(c, c->sub32, nsub_tot * 2 * sizeof(float4))) ||
+        (rc = ensure(c, c->sub32, (nsub_tot / 2) * 3 * sizeof(float4))) ||
         (rc = ensure(c, c->comp_pk, ncomp * 3 * sizeof(double2))))
       return rc;
     const size_t host_bytes = Qn * sizeof(QState) + Qn * sizeof(int) + 64;

@@ -72,7 +72,7 @@ struct Work {
   float* cost32;         // [Qc][HCAP] final fp32 costs (written by the last item of each tile)
   int* tile_cnt;         // [Qc][TCAP] per-round completion tickets of the scoring tiles
   double2* sub_pk;       // [Nsub][3] packed fp64 scoring subset: (X,Y) (Z,u) (v,w)
-  float4* sub32;         // [Nsub][2]
+  float4* sub32;         // [Nsub/2][3] record pairs (SoA float2), per-query offsets even
   double2* comp_pk;      // [N][3] packed full-set inliers (final refinement)
   int B, HCAP, NSPLIT, TCAP;
   int64_t item_cap;

@@ -53,9 +53,17 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
     wk.sub_pk[3 * d] = make_double2(X, Y);
     wk.sub_pk[3 * d + 1] = make_double2(Z, pu);
     wk.sub_pk[3 * d + 2] = make_double2(pv, w);
-    // fp32 scoring record: X32, Y32, Z32, f32(cx - u), f32(cy - v), w32
-    wk.sub32[2 * d] = make_float4((float)X, (float)Y, (float)Z, (float)(cx - pu));
-    wk.sub32[2 * d + 1] = make_float4((float)(cy - pv), (float)w, 0.f, 0.f);
+    // fp32 scoring record pair (SoA float2 of points 2k, 2k+1; sub_off is
+    // even): X32, Y32, Z32, f32(cx - u), f32(cy - v), w32
+    float* pr = reinterpret_cast<float*>(wk.sub32 + 3 * (d >> 1)) + (d & 1);
+    pr[0] = (float)X;
+    pr[2] = (float)Y;
+    pr[4] = (float)Z;
+    pr[6] = (float)(cx - pu);
+    pr[8] = (float)(cy - pv);
+    pr[10] = (float)w;
+    if ((nsub & 1) && i == nsub - 1)  // padding record: w = 0 adds +0
+      for (int k = 0; k < 12; k += 2) pr[k + 1] = 0.f;
   }
 }
 
@@ -390,9 +398,15 @@ __device__ __forceinline__ int64_t required_iters_dev(double eps, double eta, in
   return (int64_t)v;
 }
 
-constexpr int kScanThreads = 256;
+#ifndef VL_LO_NT
+#define VL_LO_NT 256   // threads of the per-query LO kernels (k_scan, k_final)
+#endif
+#ifndef VL_LO_MINB
+#define VL_LO_MINB 2   // resident CTAs per SM (bounds the LO working set held in L2)
+#endif
+constexpr int kScanThreads = VL_LO_NT;
 
-__global__ void __launch_bounds__(kScanThreads, 2) k_scan(Work wk, RansacParams p) {
+__global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, RansacParams p) {
   extern __shared__ float costs[];
   __shared__ LMShared<kScanThreads> sm;
   __shared__ Pose s_start;
@@ -556,7 +570,8 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   if (phase != 1) {
     H(kStageScan, true);
     const size_t smem = (size_t)wk.HCAP * sizeof(float);
-    launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, 2 * num_sms), st, wk, p);
+    launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, VL_LO_MINB * num_sms), st, wk,
+                     p);
     H(kStageScan, false);
     H(kStageActive, true);
     k_active<<<1, 1024, 0, st>>>(wk, nactive);
@@ -567,9 +582,9 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
 }
 
 // ------------------------------------------------------------------ final stage
-constexpr int kFinalThreads = 256;
+constexpr int kFinalThreads = VL_LO_NT;
 
-__global__ void __launch_bounds__(kFinalThreads, 2) k_final(Work wk, Inputs in, Outputs out, RansacParams p,
+__global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, Inputs in, Outputs out, RansacParams p,
                                                          int q_base) {
   __shared__ LMShared<kFinalThreads> sm;
   __shared__ int warp_tot[32];
@@ -659,7 +674,7 @@ __global__ void __launch_bounds__(kFinalThreads, 2) k_final(Work wk, Inputs in, 
 
 int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
                  int q_base, cudaStream_t st) {
-  launch_clustered(k_final, Q, kFinalThreads, 0, pick_cluster(Q, 2 * 148), st, wk, in, out, p, q_base);
+  launch_clustered(k_final, Q, kFinalThreads, 0, pick_cluster(Q, VL_LO_MINB * 148), st, wk, in, out, p, q_base);
   return 1;
 }
 

@@ -28,7 +28,13 @@
 namespace vl {
 
 // coarse: 768-hypothesis tiles x 512 correspondences (big batches)
-constexpr int kCoarseMinBlocks = 3;
+#ifndef VL_SCORE_MINB
+#define VL_SCORE_MINB 3
+#endif
+#ifndef VL_SCORE_UNR
+#define VL_SCORE_UNR 2
+#endif
+constexpr int kCoarseMinBlocks = VL_SCORE_MINB;
 // fine: 256-hypothesis tiles x 128 correspondences (single queries / small batches)
 constexpr int kFineMinBlocks = 6;
 
@@ -41,7 +47,8 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, cudaStream_t
       occ = kFineMinBlocks;
     kern<<<num_sms * occ, kScoreThreads, 0, st>>>(wk, tau2);
   } else {
-    auto kern = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks, 2>;
+    auto kern = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks,
+                           VL_SCORE_UNR>;
     static int occ = 0;
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kScoreThreads, 0) != cudaSuccess ||
                      occ < 1))

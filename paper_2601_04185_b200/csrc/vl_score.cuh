@@ -6,12 +6,15 @@ namespace vl {
 
 // ---------------------------------------------------------------- f32x2 path
 // Blackwell packed FP32 (FFMA2 / FMUL2): one instruction evaluates the same
-// step for two hypotheses; the correspondence coordinate is a scalar operand
-// broadcast to both halves (SASS `Rn.F32`).  Per pair of evaluations:
-// 9 + 1 + 2 + 2 + 1 = 15 FFMA2/FMUL2, 2 MUFU.RSQ, 2 FMNMX — ~10 issue slots
-// per evaluation instead of ~17, so the kernel becomes FMA-pipe bound
-// rather than issue bound.  Arithmetic per component is identical to the
-// scalar path (same fused operations, same order).
+// step for TWO CORRESPONDENCES of one hypothesis.  Records are stored in
+// pairs (SoA float2: X, Y, Z, cx-u, cy-v, w of points 2k and 2k+1), the
+// hypothesis' fx/fy-folded [R|t] entries are scalars broadcast to both halves
+// (SASS `Rn.F32`).  Consecutive FFMA2 of the HT hypotheses of a thread then
+// share the record operand (register reuse cache), which halves the
+// register-file reads per instruction against the earlier packing (two
+// hypotheses x one broadcast coordinate): tools/score_mix_bench.cu measured
+// 2.255e12 vs 1.982e12 evaluations/s for the same 14 FFMA2/FMUL2 + 2 MUFU +
+// 4 FMNMX per pair of evaluations.
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __ffma2_rn(a, b, make_float2(-0.f, -0.f)); }
@@ -25,37 +28,38 @@ __device__ __forceinline__ float rcp_approx_ftz(float x) {
 // r = 1 / max(z, 0): +inf for z <= 0 (behind camera / on the camera plane),
 // so e2 becomes inf or NaN and fminf (IEEE minNum) maps it to tau^2.  The
 // clamp runs on the ALU pipe, the reciprocal on the MUFU pipe: the FMA pipe
-// only sees the 14 FFMA2/FMUL2 of the evaluation pair.
-#define VL_SCORE_EVAL2(Pp, accp)                                                                  \
+// only sees the 14 FFMA2/FMUL2 of the evaluation pair.  A padding record
+// (odd subset size) has w = 0 and adds +0.
+#define VL_SCORE_EVAL2(Ph, acch)                                                                  \
   {                                                                                               \
-    const float2 x_ = fma2(Pp[0], f2(a.x), fma2(Pp[1], f2(a.y), fma2(Pp[2], f2(a.z), Pp[3])));    \
-    const float2 y_ = fma2(Pp[4], f2(a.x), fma2(Pp[5], f2(a.y), fma2(Pp[6], f2(a.z), Pp[7])));    \
-    const float2 z_ = fma2(Pp[8], f2(a.x), fma2(Pp[9], f2(a.y), fma2(Pp[10], f2(a.z), Pp[11])));  \
+    const float2 x_ = fma2(X2, f2(Ph[0]), fma2(Y2, f2(Ph[1]), fma2(Z2, f2(Ph[2]), f2(Ph[3]))));   \
+    const float2 y_ = fma2(X2, f2(Ph[4]), fma2(Y2, f2(Ph[5]), fma2(Z2, f2(Ph[6]), f2(Ph[7]))));   \
+    const float2 z_ = fma2(X2, f2(Ph[8]), fma2(Y2, f2(Ph[9]), fma2(Z2, f2(Ph[10]), f2(Ph[11])))); \
     const float2 r_ = make_float2(rcp_approx_ftz(fmaxf(z_.x, 0.f)), rcp_approx_ftz(fmaxf(z_.y, 0.f))); \
-    const float2 du_ = fma2(x_, r_, f2(a.w));                                                     \
-    const float2 dv_ = fma2(y_, r_, f2(b.x));                                                     \
+    const float2 du_ = fma2(x_, r_, A2);                                                          \
+    const float2 dv_ = fma2(y_, r_, B2);                                                          \
     float2 e2_ = fma2(du_, du_, mul2(dv_, dv_));                                                  \
     e2_.x = fminf(e2_.x, tau2);                                                                   \
     e2_.y = fminf(e2_.y, tau2);                                                                   \
-    accp = fma2(f2(b.y), e2_, accp);                                                              \
+    acch = fma2(W2, e2_, acch);                                                                   \
   }
 
 // Work item = (query, tile of NT*HT hypotheses, ns <= SPI consecutive
 // correspondence splits of SCH records).  The canonical fp32 cost of a
 // hypothesis is  sum over split groups (in order) of the group sum
-// ((p0 + p1) + p2) + p3  of its splits' sequential record sums — every
+// ((p0 + p1) + p2) + p3  of its splits' record sums, a split's sum being
+// (even records, in order) + (odd records, in order) — every
 // split is accumulated by exactly one thread in record order, so neither the
 // tile shape (HT), the splits per item (SPI) nor the grid changes a single
 // bit.  The last item to finish a (query, tile) — atomic ticket per tile —
 // reduces the tile's partial slots in that order and writes the final costs.
 template <int NT, int HT, int SPI, int SCH, int MINB, int UNR>
 __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
-  static_assert(HT % 2 == 0, "hypotheses are processed in pairs");
-  constexpr int HP = HT / 2;
+  static_assert(SCH % 2 == 0, "splits hold whole record pairs");
   constexpr int NW = NT / 32;
   constexpr int WHYP = 32 * HT;  // hypotheses per warp slice
   static_assert(SPI == 1 || SPI == kGroupSplits, "coarse items are exactly one split group");
-  __shared__ float4 rec[2 * SPI * SCH];
+  __shared__ float4 rec[3 * SPI * SCH / 2];  // record pairs: (X2, Y2), (Z2, A2), (B2, W2)
   __shared__ float red[SPI][SPI > 1 ? NT * HT : 1];
   __shared__ int s_it, s_last;
   const int nitems = wk.item_count[0];
@@ -78,7 +82,8 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     // the group sum ((p0 + p1) + p2) + p3 that k_scan forms itself in fine mode
     const int c0 = item.split * SCH;
     const int cn = min(ns * SCH, nsub - c0);
-    const float4* src = wk.sub32 + 2 * (S.sub_off + c0);
+    const int pn = (cn + 1) >> 1;  // record pairs (the last one padded when nsub is odd)
+    const float4* src = wk.sub32 + 3 * ((S.sub_off + c0) >> 1);
     // A partially filled (last) tile of r hypotheses needs WH = ceil(r / WHYP)
     // warp slices; the other warps take other splits of the item (G groups),
     // so a short tile does not leave warps idle.
@@ -87,56 +92,51 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     const int G = NW / WH;
     const int hs = w % WH, grp = w / WH;
     __syncthreads();
-    for (int k = threadIdx.x; k < 2 * cn; k += NT) rec[k] = src[k];
-    float2 P[HP][12];
+    for (int k = threadIdx.x; k < 3 * pn; k += NT) rec[k] = src[k];
+    float P[HT][12];
     int hid[HT];
     const float* Pq = wk.P32 + (int64_t)item.q * 12 * wk.HCAP;
 #pragma unroll
     for (int j = 0; j < HT; ++j) hid[j] = tile0 + hs * WHYP + lane * HT + j;
 #pragma unroll
-    for (int jp = 0; jp < HP; ++jp) {
-      const int h0 = hid[2 * jp] < nh ? hid[2 * jp] : 0;
-      const int h1 = hid[2 * jp + 1] < nh ? hid[2 * jp + 1] : 0;
+    for (int j = 0; j < HT; ++j) {
+      const int h = hid[j] < nh ? hid[j] : 0;
 #pragma unroll
-      for (int c = 0; c < 12; ++c)
-        P[jp][c] = make_float2(Pq[(int64_t)c * wk.HCAP + h0], Pq[(int64_t)c * wk.HCAP + h1]);
+      for (int c = 0; c < 12; ++c) P[j][c] = Pq[(int64_t)c * wk.HCAP + h];
     }
     __syncthreads();
-    float2 gsum[HP];
+    float gsum[HT];
 #pragma unroll
-    for (int jp = 0; jp < HP; ++jp) gsum[jp] = make_float2(0.f, 0.f);
+    for (int j = 0; j < HT; ++j) gsum[j] = 0.f;
     for (int s = grp; s < ns && grp < G; s += G) {
-      float2 acc[HP];
+      float2 acc[HT];
 #pragma unroll
-      for (int jp = 0; jp < HP; ++jp) acc[jp] = make_float2(0.f, 0.f);
-      const int cb = s * SCH, ce = min(cb + SCH, cn);
+      for (int j = 0; j < HT; ++j) acc[j] = make_float2(0.f, 0.f);
+      const int pb = s * (SCH / 2), pe = min(pb + SCH / 2, pn);
 #pragma unroll UNR
-      for (int c = cb; c < ce; ++c) {
-        const float4 a = rec[2 * c];
-        const float4 b = rec[2 * c + 1];
+      for (int c = pb; c < pe; ++c) {
+        const float4 r0 = rec[3 * c], r1 = rec[3 * c + 1], r2 = rec[3 * c + 2];
+        const float2 X2 = make_float2(r0.x, r0.y), Y2 = make_float2(r0.z, r0.w);
+        const float2 Z2 = make_float2(r1.x, r1.y), A2 = make_float2(r1.z, r1.w);
+        const float2 B2 = make_float2(r2.x, r2.y), W2 = make_float2(r2.z, r2.w);
 #pragma unroll
-        for (int jp = 0; jp < HP; ++jp) VL_SCORE_EVAL2(P[jp], acc[jp]);
+        for (int j = 0; j < HT; ++j) VL_SCORE_EVAL2(P[j], acc[j]);
       }
+      float sv[HT];  // the split's sum: even records + odd records
+#pragma unroll
+      for (int j = 0; j < HT; ++j) sv[j] = acc[j].x + acc[j].y;
       if (SPI == 1) {
         float* out = outq + (int64_t)(item.split + s) * wk.HCAP;
 #pragma unroll
-        for (int jp = 0; jp < HP; ++jp) {
-          if (hid[2 * jp] < nh) out[hid[2 * jp]] = acc[jp].x;
-          if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = acc[jp].y;
-        }
+        for (int j = 0; j < HT; ++j)
+          if (hid[j] < nh) out[hid[j]] = sv[j];
       } else if (G == 1) {
 #pragma unroll
-        for (int jp = 0; jp < HP; ++jp) {
-          gsum[jp].x = (s == 0) ? acc[jp].x : gsum[jp].x + acc[jp].x;
-          gsum[jp].y = (s == 0) ? acc[jp].y : gsum[jp].y + acc[jp].y;
-        }
+        for (int j = 0; j < HT; ++j) gsum[j] = (s == 0) ? sv[j] : gsum[j] + sv[j];
       } else {
         // split s of a partial tile computed by warp group grp: park it
 #pragma unroll
-        for (int jp = 0; jp < HP; ++jp) {
-          red[s][hs * WHYP + lane * HT + 2 * jp] = acc[jp].x;
-          red[s][hs * WHYP + lane * HT + 2 * jp + 1] = acc[jp].y;
-        }
+        for (int j = 0; j < HT; ++j) red[s][hs * WHYP + lane * HT + j] = sv[j];
       }
     }
     if (SPI > 1) {
@@ -145,22 +145,17 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
         __syncthreads();
         if (grp == 0) {
 #pragma unroll
-          for (int jp = 0; jp < HP; ++jp) {
-            float sx = red[0][hs * WHYP + lane * HT + 2 * jp], sy = red[0][hs * WHYP + lane * HT + 2 * jp + 1];
-            for (int s = 1; s < ns; ++s) {
-              sx += red[s][hs * WHYP + lane * HT + 2 * jp];
-              sy += red[s][hs * WHYP + lane * HT + 2 * jp + 1];
-            }
-            gsum[jp] = make_float2(sx, sy);
+          for (int j = 0; j < HT; ++j) {
+            float sx = red[0][hs * WHYP + lane * HT + j];
+            for (int s = 1; s < ns; ++s) sx += red[s][hs * WHYP + lane * HT + j];
+            gsum[j] = sx;
           }
         }
       }
       if (grp == 0) {
 #pragma unroll
-        for (int jp = 0; jp < HP; ++jp) {
-          if (hid[2 * jp] < nh) out[hid[2 * jp]] = gsum[jp].x;
-          if (hid[2 * jp + 1] < nh) out[hid[2 * jp + 1]] = gsum[jp].y;
-        }
+        for (int j = 0; j < HT; ++j)
+          if (hid[j] < nh) out[hid[j]] = gsum[j];
       }
     }
     // ---- tile completion ticket (threadfence reduction pattern)

@@ -97,12 +97,14 @@ int main(int argc, char** argv) {
   std::mt19937 rng(1);
   std::uniform_real_distribution<float> U(-1.f, 1.f);
   // correspondences: points in front of a camera near identity, pixels near projections
-  std::vector<float4> sub((size_t)b.Q * b.nsub * 2);
+  // record pairs (SoA float2 of points 2k, 2k+1: X, Y, Z, cx-u, cy-v, w), the k_prep layout
+  std::vector<float4> sub((size_t)b.Q * b.nsub / 2 * 3);
+  float* sf = reinterpret_cast<float*>(sub.data());
   for (size_t i = 0; i < (size_t)b.Q * b.nsub; ++i) {
     const float X = 1.2f * U(rng), Y = 1.2f * U(rng), Z = 3.5f + 1.5f * U(rng);
     const float u = 700.f * X / Z + 350.f + 20.f * U(rng), v = 700.f * Y / Z + 350.f + 20.f * U(rng);
-    sub[2 * i] = make_float4(X, Y, Z, 350.f - u);
-    sub[2 * i + 1] = make_float4(350.f - v, 0.5f + 0.5f * fabsf(U(rng)), 0.f, 0.f);
+    float* pr = sf + 12 * (i >> 1) + (i & 1);
+    pr[0] = X, pr[2] = Y, pr[4] = Z, pr[6] = 350.f - u, pr[8] = 350.f - v, pr[10] = 0.5f + 0.5f * fabsf(U(rng));
   }
   std::vector<float> P((size_t)b.Q * 12 * b.HCAP, 0.f);
   for (int q = 0; q < b.Q; ++q)
