@@ -233,8 +233,12 @@ __device__ __forceinline__ void lm_point(const double* R, const double* t, const
   if (GRAD) {
     const double wr = dmul(w, wt);
     if (wr != 0.0) {
-      const double p00 = in.fx / z, p02 = -in.fx * x / (z * z);
-      const double p11 = in.fy / z, p12 = -in.fy * y / (z * z);
+      // dpi/dX_cam (refine.py:115-118) from one reciprocal: the normal
+      // equations only steer the step (the cost above keeps the reference's
+      // exact divisions), so 1 ulp here changes nothing the schedule compares
+      const double iz = __drcp_rn(z);
+      const double p00 = in.fx * iz, p02 = -(in.fx * x) * (iz * iz);
+      const double p11 = in.fy * iz, p12 = -(in.fy * y) * (iz * iz);
       double J0[6], J1[6];
       J0[0] = p02 * y;
       J0[1] = p00 * z + p02 * (-x);
