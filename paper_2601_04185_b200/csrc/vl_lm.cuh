@@ -215,8 +215,15 @@ __device__ __forceinline__ void lm_point(const double* R, const double* t, const
     if (kind == kTruncated) acc[0] += dmul(w, s2);
     return;
   }
-  const double u = dadd(__ddiv_rn(dmul(in.fx, x), z), in.cx);
-  const double v = dadd(__ddiv_rn(dmul(in.fy, y), z), in.cy);
+  // (fx x) / z and (fy y) / z from one correctly rounded reciprocal plus a
+  // remainder correction (the quotient is correctly rounded but for rare
+  // double-rounding ties; the LM cost only steers the schedule — classification
+  // flags come from msac_pass's exact divisions)
+  const double iz = __drcp_rn(z);
+  const double ax = dmul(in.fx, x), ay = dmul(in.fy, y);
+  const double qx = ax * iz, qy = ay * iz;
+  const double u = dadd(fma(fma(-qx, z, ax), iz, qx), in.cx);
+  const double v = dadd(fma(fma(-qy, z, ay), iz, qy), in.cy);
   const double ru = dsub(u, u_obs);
   const double rv = dsub(v, v_obs);
   const double e2 = dadd(dmul(ru, ru), dmul(rv, rv));
@@ -236,7 +243,6 @@ __device__ __forceinline__ void lm_point(const double* R, const double* t, const
       // dpi/dX_cam (refine.py:115-118) from one reciprocal: the normal
       // equations only steer the step (the cost above keeps the reference's
       // exact divisions), so 1 ulp here changes nothing the schedule compares
-      const double iz = __drcp_rn(z);
       const double p00 = in.fx * iz, p02 = -(in.fx * x) * (iz * iz);
       const double p11 = in.fy * iz, p12 = -(in.fy * y) * (iz * iz);
       double J0[6], J1[6];
