@@ -152,11 +152,16 @@ __device__ __forceinline__ double msac_e2(const double* R, const double* t, cons
   cam_point(R, t, P, x, y, z);
   const bool front = z > 0;
   const double zs = front ? z : 1.0;
-  double du = dmul(in.fx, x);
-  du = __ddiv_rn(du, zs);
+  // (fx x) / zs via one reciprocal + remainder correction: the correctly
+  // rounded quotient except for rare double-rounding ties (1 ulp), which can
+  // only move a flag for e2 within ~1e-16 relative of tau^2 (the parity bar
+  // already excludes |e - tau| < 1e-6 px)
+  const double iz = __drcp_rn(zs);
+  const double ax = dmul(in.fx, x), ay = dmul(in.fy, y);
+  const double qx = ax * iz, qy = ay * iz;
+  double du = fma(fma(-qx, zs, ax), iz, qx);
   du = dadd(du, dsub(in.cx, u));
-  double dv = dmul(in.fy, y);
-  dv = __ddiv_rn(dv, zs);
+  double dv = fma(fma(-qy, zs, ay), iz, qy);
   dv = dadd(dv, dsub(in.cy, v));
   double e2 = dmul(du, du);
   e2 = dadd(e2, dmul(dv, dv));
