@@ -23,7 +23,7 @@ struct vl_ctx {
   int num_sms = 148;
   std::string err;
   int64_t launches = 0;
-  DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, P32, hsrc, items, item_count,
+  DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, p3p_geo, p3p_cand, p3p_nc, P32, hsrc, items, item_count,
       partial, cost32, tile_cnt, sub_pk, sub32, comp_pk;
   DevBuf scratch;  // small standalone-call scratch
   DevBuf lift_meta, lift_blk_count, lift_blk_off, lift_seg_off;  // vl_lift
@@ -191,10 +191,10 @@ int vl_destroy(vl_ctx* c) {
   if (!c) return VL_OK;
   cudaSetDevice(c->device);
   DevBuf* bufs[] = {&c->qs,      &c->active, &c->next_active, &c->active_count, &c->samples, &c->slots,
-                    &c->slot_cnt, &c->P32,   &c->hsrc,        &c->items,        &c->item_count,
+                    &c->slot_cnt, &c->p3p_geo, &c->p3p_cand, &c->p3p_nc, &c->P32,   &c->hsrc,        &c->items,        &c->item_count,
                     &c->partial, &c->cost32, &c->tile_cnt, &c->sub_pk, &c->sub32, &c->comp_pk,
                     &c->scratch, &c->lift_meta, &c->lift_blk_count,
-                    &c->lift_blk_off, &c->lift_seg_off};
+                    &c->lift_blk_off, &c->lift_seg_off, &c->tri_meta};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -244,6 +244,9 @@ int vl_reserve(vl_ctx* c, int32_t max_queries, int64_t max_n_per_query, int32_t 
   rc |= ensure(c, c->samples, Qc * B * 3 * sizeof(int));
   rc |= ensure(c, c->slots, Qc * B * 48 * sizeof(double));
   rc |= ensure(c, c->slot_cnt, Qc * B * sizeof(int));
+  rc |= ensure(c, c->p3p_geo, Qc * B * kGeoDoubles * sizeof(double));
+  rc |= ensure(c, c->p3p_cand, Qc * B * 3 * kMaxCandSlots * sizeof(double));
+  rc |= ensure(c, c->p3p_nc, Qc * B * sizeof(int));
   rc |= ensure(c, c->P32, Qc * 12 * H * sizeof(float));
   rc |= ensure(c, c->hsrc, Qc * H * sizeof(int));
   rc |= ensure(c, c->partial, Qc * ns * H * sizeof(float));
@@ -333,6 +336,9 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
         (rc = ensure(c, c->samples, Qn * B * 3 * sizeof(int))) ||
         (rc = ensure(c, c->slots, Qn * B * 48 * sizeof(double))) ||
         (rc = ensure(c, c->slot_cnt, Qn * B * sizeof(int))) ||
+        (rc = ensure(c, c->p3p_geo, Qn * B * kGeoDoubles * sizeof(double))) ||
+        (rc = ensure(c, c->p3p_cand, Qn * B * 3 * kMaxCandSlots * sizeof(double))) ||
+        (rc = ensure(c, c->p3p_nc, Qn * B * sizeof(int))) ||
         (rc = ensure(c, c->P32, Qn * 12 * HCAP * sizeof(float))) ||
         (rc = ensure(c, c->hsrc, Qn * HCAP * sizeof(int))) ||
         (rc = ensure(c, c->items, item_cap * sizeof(ScoreItem))) ||
@@ -358,6 +364,9 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
     wk.samples = (int*)c->samples.p;
     wk.slots = (double*)c->slots.p;
     wk.slot_cnt = (int*)c->slot_cnt.p;
+    wk.p3p_geo = (double*)c->p3p_geo.p;
+    wk.p3p_cand = (double*)c->p3p_cand.p;
+    wk.p3p_nc = (int*)c->p3p_nc.p;
     wk.P32 = (float*)c->P32.p;
     wk.hsrc = (int*)c->hsrc.p;
     wk.items = (ScoreItem*)c->items.p;

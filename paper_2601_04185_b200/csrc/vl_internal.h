@@ -56,6 +56,9 @@ struct RansacParams {
 };
 
 // Device workspace view for one chunk of queries.
+constexpr int kGeoDoubles = 25;  // sizeof(P3PGeo) / 8
+constexpr int kMaxCandSlots = 8;  // distance-triple candidates per sample (4 roots x 2 branches)
+
 struct Work {
   QState* qs;
   int* active_list;
@@ -64,6 +67,9 @@ struct Work {
   int* samples;          // [Qc][B][3]
   double* slots;         // [Qc][B][4][12]
   int* slot_cnt;         // [Qc][B]
+  double* p3p_geo;       // [Qc][B][kGeoDoubles] per-sample P3P geometry (k_p3p_roots -> k_p3p_polish)
+  double* p3p_cand;      // [Qc][B][8][3] distance-triple candidates
+  int* p3p_nc;           // [Qc][B] candidate counts
   float* P32;            // [Qc][12][HCAP]
   int* hsrc;             // [Qc][HCAP]
   ScoreItem* items;      // [item_cap]

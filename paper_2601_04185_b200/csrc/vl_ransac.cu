@@ -3,7 +3,7 @@
 // One "round" = one batch of `batch_size` minimal samples for every active
 // query (posest.py:250-276):
 //   k_sample   CTA/query : numpy-exact minimal sets (posest.py:252)
-//   k_p3p      thread/sample : P3P solutions into per-sample slots (p3p.py:57)
+//   k_p3p_roots / k_p3p_polish : P3P solutions into per-sample slots (p3p.py:57)
 //   k_compact  CTA/query : ordered hypothesis list + fp32 K[R|t] tiles,
 //                          appends scoring work items
 //   k_score    persistent grid (vl_score.cu): fp32 MSAC costs (posest.py:178)
@@ -13,6 +13,7 @@
 // After the last round k_final (CTA/query) classifies the full set and runs
 // the Cauchy refinement (posest.py:284-299).
 #include <climits>
+#include <cstddef>
 #include "vl_internal.h"
 #include "vl_lm.cuh"
 #include "vl_p3p.cuh"
@@ -161,48 +162,64 @@ __device__ __forceinline__ void bearing(const double* px, const Intr& in, double
   f[2] = 1.0 / nr;
 }
 
-// Warp-cooperative P3P.  Phase 1: lane = minimal sample (gate, quartic,
-// roots, distance-triple candidates).  The warp's candidates are compacted
-// in (sample, root) order into shared memory; phase 2 polishes them 32 at a
-// time (lane = candidate: Newton + Procrustes + contract), so the ~1.5
-// candidates per sample keep every lane busy instead of diverging per
-// sample.  Phase 3: each sample's owner lane dedups its candidates in order
-// into the sample's solution slots (<= 4), exactly the reference's order.
+// P3P in two kernels (one kernel with both phases thrashed the instruction
+// cache: ncu stall_no_inst 34 %, and its register / smem footprint capped
+// occupancy at 12 warps per SM).
+//  k_p3p_roots  lane = minimal sample: gate, resultant quartic, real positive
+//               roots, distance-triple candidates (p3p.py:91-231); the
+//               sample's geometry and candidates go to global scratch.
+//  k_p3p_polish warp = 32 consecutive samples: their candidates are compacted
+//               in (sample, root) order into shared memory and polished 32 at a
+//               time (lane = candidate: Newton + Procrustes + contract), so the
+//               ~1.5 candidates per sample keep every lane busy; each sample's
+//               owner lane then dedups its candidates in order into the
+//               sample's solution slots (<= 4) — the reference's order.
+// The arithmetic is the single-kernel version's, function for function.
+static_assert(sizeof(P3PGeo) == kGeoDoubles * sizeof(double) && kMaxCand == kMaxCandSlots, "P3P scratch layout");
+constexpr int kP3PRootThreads = 128;
 constexpr int kP3PThreads = 64;
 struct CandRec {
   double s0, s1, s2;
   int lane, pad;
 };
 
-__global__ void __launch_bounds__(kP3PThreads) k_p3p(Work wk, Inputs in) {
-  __shared__ P3PGeo geo[kP3PThreads];
+__global__ void __launch_bounds__(kP3PRootThreads) k_p3p_roots(Work wk, Inputs in) {
+  const int q = wk.active_list[blockIdx.x];
+  const QState& S = wk.qs[q];
+  const int s = blockIdx.y * kP3PRootThreads + threadIdx.x;
+  if (s >= S.batch_n) return;
+  const int64_t si = (int64_t)q * wk.B + s;
+  const int* smp = wk.samples + si * 3;
+  double f[9], P[9];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int64_t r = S.off + smp[k];
+    bearing(in.px + 2 * r, S.in, f + 3 * k);
+    P[3 * k] = in.X[3 * r];
+    P[3 * k + 1] = in.X[3 * r + 1];
+    P[3 * k + 2] = in.X[3 * r + 2];
+  }
+  P3PGeo g;
+  double quart[5], vs[4];
+  int nc = 0;
+  if (p3p_setup(f, P, g, quart)) {
+    const int nv = quartic_real_pos_roots(quart, vs);
+    if (nv) nc = p3p_candidates(g, vs, nv, wk.p3p_cand + si * (3 * kMaxCand), 3);
+  }
+  if (nc) *reinterpret_cast<P3PGeo*>(wk.p3p_geo + si * kGeoDoubles) = g;
+  wk.p3p_nc[si] = nc;
+}
+
+__global__ void __launch_bounds__(kP3PThreads) k_p3p_polish(Work wk) {
   __shared__ CandRec cand[kP3PThreads / 32][32 * kMaxCand];
   __shared__ double res[kP3PThreads / 32][32][13];
   const int q = wk.active_list[blockIdx.x];
   const QState& S = wk.qs[q];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int s = blockIdx.y * kP3PThreads + threadIdx.x;
+  const int64_t si = (int64_t)q * wk.B + s;
   const bool live = s < S.batch_n;
-  int nc = 0, nv = 0;
-  double vs[4];
-  P3PGeo& g = geo[threadIdx.x];
-  if (live) {
-    const int* smp = wk.samples + ((int64_t)q * wk.B + s) * 3;
-    double f[9], P[9];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int64_t r = S.off + smp[k];
-      bearing(in.px + 2 * r, S.in, f + 3 * k);
-      P[3 * k] = in.X[3 * r];
-      P[3 * k + 1] = in.X[3 * r + 1];
-      P[3 * k + 2] = in.X[3 * r + 2];
-    }
-    double quart[5];
-    if (p3p_setup(f, P, g, quart)) {
-      nv = quartic_real_pos_roots(quart, vs);
-      if (nv) nc = p3p_candidates(g, vs, nv, nullptr, 0);
-    }
-  }
+  const int nc = live ? wk.p3p_nc[si] : 0;
   // warp exclusive scan of candidate counts
   int incl = nc;
 #pragma unroll
@@ -212,21 +229,21 @@ __global__ void __launch_bounds__(kP3PThreads) k_p3p(Work wk, Inputs in) {
   }
   const int base = incl - nc;
   const int total = __shfl_sync(0xffffffffu, incl, 31);
-  if (nc) {
-    p3p_candidates(g, vs, nv, &cand[wid][base].s0, 4);
-    for (int i = 0; i < nc; ++i) cand[wid][base + i].lane = lane;
-  }
+  const double* cs = wk.p3p_cand + si * (3 * kMaxCand);
+  for (int i = 0; i < nc; ++i) cand[wid][base + i] = CandRec{cs[3 * i], cs[3 * i + 1], cs[3 * i + 2], lane, 0};
   __syncwarp();
-  double* slot = wk.slots + ((int64_t)q * wk.B + s) * (4 * 12);
-  const double ttol = live ? kDedupTol * sqrt(g.scale2) : 0.0;
+  double* slot = wk.slots + si * (4 * 12);
+  const double ttol = nc ? kDedupTol * sqrt(wk.p3p_geo[si * kGeoDoubles + offsetof(P3PGeo, scale2) / 8]) : 0.0;
   int kept = 0;
+  const int64_t warp_s0 = si - lane;  // sample index of lane 0
   for (int ch = 0; ch < total; ch += 32) {
     const int j = ch + lane;
     if (j < total) {
       const CandRec cr = cand[wid][j];
+      const P3PGeo g = *reinterpret_cast<const P3PGeo*>(wk.p3p_geo + (warp_s0 + cr.lane) * kGeoDoubles);
       double R[9], t[3];
       const double sv[3] = {cr.s0, cr.s1, cr.s2};
-      const bool ok = p3p_polish(geo[wid * 32 + cr.lane], sv, R, t);
+      const bool ok = p3p_polish(g, sv, R, t);
 #pragma unroll
       for (int i = 0; i < 9; ++i) res[wid][lane][i] = R[i];
 #pragma unroll
@@ -246,7 +263,7 @@ __global__ void __launch_bounds__(kP3PThreads) k_p3p(Work wk, Inputs in) {
     }
     __syncwarp();
   }
-  if (live) wk.slot_cnt[(int64_t)q * wk.B + s] = kept;
+  if (live) wk.slot_cnt[si] = kept;
 }
 
 __global__ void __launch_bounds__(128) k_p3p_batch(const double* f, const double* P, int B, double* slots,
@@ -556,8 +573,10 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     k_sample<<<nactive, 256, 0, st>>>(wk, p);
     H(kStageSample, false);
     H(kStageP3P, true);
+    dim3 gr(nactive, (wk.B + kP3PRootThreads - 1) / kP3PRootThreads);
+    k_p3p_roots<<<gr, kP3PRootThreads, 0, st>>>(wk, in);
     dim3 gp(nactive, (wk.B + kP3PThreads - 1) / kP3PThreads);
-    k_p3p<<<gp, kP3PThreads, 0, st>>>(wk, in);
+    k_p3p_polish<<<gp, kP3PThreads, 0, st>>>(wk);
     H(kStageP3P, false);
     H(kStageCompact, true);
     k_compact<<<nactive, 1024, 0, st>>>(wk, fine);
