@@ -133,6 +133,7 @@ VL_HD bool ferrari_init(const double* b, double* zr, double* zi) {
       wi[0] = 0.5 * sqrt(-dsc);
       wi[1] = -wi[0];
     }
+#pragma unroll
     for (int k = 0; k < 2; ++k) {  // complex square roots of w
       const double mod = sqrt(wr[k] * wr[k] + wi[k] * wi[k]);
       double sr = sqrt(fmax(0.5 * (mod + wr[k]), 0.0));
@@ -149,6 +150,7 @@ VL_HD bool ferrari_init(const double* b, double* zr, double* zi) {
     // y^2 - s y + (h + g) = 0 and y^2 + s y + (h - g) = 0
     const double c0[2] = {h + g, h - g};
     const double sg[2] = {s, -s};
+#pragma unroll
     for (int k = 0; k < 2; ++k) {
       const double dsc = sg[k] * sg[k] - 4.0 * c0[k];
       if (dsc >= 0) {
@@ -165,14 +167,19 @@ VL_HD bool ferrari_init(const double* b, double* zr, double* zi) {
     }
   }
   bool ok = true;
+#pragma unroll
   for (int k = 0; k < 4; ++k) ok &= isfinite(zr[k]) && isfinite(zi[k]);
   // Aberth needs distinct starting points
-  for (int k = 0; k < 4 && ok; ++k)
-    for (int j = k + 1; j < 4; ++j)
-      if (zr[k] == zr[j] && zi[k] == zi[j]) {
-        const double bump = 1e-7 * (1.0 + fabs(zr[k]));
-        zi[j] += (j - k) * bump;
-      }
+  if (ok) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int j = k + 1; j < 4; ++j)
+        if (zr[k] == zr[j] && zi[k] == zi[j]) {
+          const double bump = 1e-7 * (1.0 + fabs(zr[k]));
+          zi[j] += (j - k) * bump;
+        }
+  }
   return ok;
 }
 
@@ -187,17 +194,33 @@ VL_HD_BIG int quartic_real_pos_roots(const double* c_in, double* out) {
   double c[5];
 #pragma unroll
   for (int k = 0; k < 5; ++k) c[k] = c_in[k] / mx;
-  int lead = 0;
-  while (lead < 4 && c[lead] == 0) ++lead;
-  int last = 4;
-  while (last > lead && c[last] == 0) --last;
+  // every array below is indexed with compile-time indices only, so it stays
+  // in registers (a runtime index moves the array to local memory)
+  int lead = 4;  // first nonzero of c[0..3], else 4
+#pragma unroll
+  for (int k = 3; k >= 0; --k)
+    if (c[k] != 0) lead = k;
+  int last = lead;  // last nonzero above lead
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+    if (k > lead && c[k] != 0) last = k;
   const int d = last - lead;
   if (d <= 0) return 0;
   // ascending monic coefficients b[k] of z^k (k <= d), zero-padded to 5
+  // b[k] = c[last - k] / c[lead]: one static-index branch per `last` (a
+  // select over j == last - k is turned back into an indexed local load)
+  const double clead = lead == 0 ? c[0] : lead == 1 ? c[1] : lead == 2 ? c[2] : c[3];
+  const double il = 1.0 / clead;
   double b[5];
-  const double il = 1.0 / c[lead];
-#pragma unroll
-  for (int k = 0; k < 5; ++k) b[k] = (k <= d) ? c[last - k] * il : 0.0;
+#define VL_P3P_SHIFT(L)                                                     \
+  _Pragma("unroll") for (int k = 0; k < 5; ++k) b[k] = (k <= d && k <= L) ? c[(L - k) < 0 ? 0 : (L - k)] * il : 0.0;
+  switch (last) {
+    case 4: VL_P3P_SHIFT(4) break;
+    case 3: VL_P3P_SHIFT(3) break;
+    case 2: VL_P3P_SHIFT(2) break;
+    default: VL_P3P_SHIFT(1) break;
+  }
+#undef VL_P3P_SHIFT
   double zr[4], zi[4];
   bool conv[4];
   if (d == 1) {
@@ -210,8 +233,9 @@ VL_HD_BIG int quartic_real_pos_roots(const double* c_in, double* out) {
     int hk[5];
     float hl[5];
     int nh = 0;
-    for (int k = 0; k <= d; ++k) {
-      if (b[k] == 0) continue;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (k > d || b[k] == 0) continue;
       const float lk = logf((float)fabs(b[k]));
       while (nh >= 2) {
         const float cr = (float)(hk[nh - 1] - hk[nh - 2]) * (lk - hl[nh - 2]) -
@@ -231,15 +255,21 @@ VL_HD_BIG int quartic_real_pos_roots(const double* c_in, double* out) {
         const float ang = 6.2831853f * (float)j / (float)m + 1.5707963f / (float)d + 0.4f * s + 0.3f;
         float sn, cs;
         sincosf(ang, &sn, &cs);
-        zr[zc] = (double)(r * cs);
-        zi[zc] = (double)(r * sn);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (t == zc) {
+            zr[t] = (double)(r * cs);
+            zi[t] = (double)(r * sn);
+          }
         ++zc;
       }
     }
-    for (; zc < d; ++zc) {  // defensive: the hull always covers degree d
-      zr[zc] = cos(1.0 + zc);
-      zi[zc] = sin(1.0 + zc);
-    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (t >= zc && t < d) {  // defensive: the hull always covers degree d
+        zr[t] = cos(1.0 + t);
+        zi[t] = sin(1.0 + t);
+      }
     }  // !seeded
 #pragma unroll
     for (int k = 0; k < 4; ++k) conv[k] = (k >= d);
@@ -300,18 +330,29 @@ VL_HD_BIG int quartic_real_pos_roots(const double* c_in, double* out) {
       if (all) break;
     }
   }
+  // ascending real positive roots: 4-element sorting network, rejected
+  // roots parked at +inf (equal values are interchangeable)
   int nr = 0;
+  double w[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    if (k < d && fabs(zi[k]) <= 1e-6 * (1.0 + fabs(zr[k])) && zr[k] > 0) {
-      int p = nr++;
-      while (p > 0 && out[p - 1] > zr[k]) {
-        out[p] = out[p - 1];
-        --p;
-      }
-      out[p] = zr[k];
-    }
+    const bool keep = k < d && fabs(zi[k]) <= 1e-6 * (1.0 + fabs(zr[k])) && zr[k] > 0;
+    w[k] = keep ? zr[k] : HUGE_VAL;
+    nr += keep ? 1 : 0;
   }
+  auto cswap = [](double& a, double& b) {
+    const double lo = fmin(a, b), hi = fmax(a, b);
+    a = lo;
+    b = hi;
+  };
+  cswap(w[0], w[1]);
+  cswap(w[2], w[3]);
+  cswap(w[0], w[2]);
+  cswap(w[1], w[3]);
+  cswap(w[1], w[2]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (k < nr) out[k] = w[k];
   return nr;
 }
 
@@ -328,7 +369,9 @@ VL_HD_BIG int p3p_candidates(const P3PGeo& g, const double* vs, int nv, double* 
     }
     ++nc;
   };
-  for (int iv = 0; iv < nv; ++iv) {
+#pragma unroll
+  for (int iv = 0; iv < 4; ++iv) {
+    if (iv >= nv) break;
     const double v = vs[iv];
     const double den = 1.0 + v * v - 2.0 * v * g.cb;
     if (den <= 0) continue;
