@@ -714,7 +714,7 @@ def main():
             traffic = {"dram_bytes_per_launch": tr["dram_bytes_per_launch"], "source": tr["source"],
                        "algorithmic_bytes_per_launch": int(evals_per_step / score_launches * args.steps
                                                            / 10_000 * (48 + 4 * 20)) +
-                       (Q * 10_000 * 32 if score_launches else 0)}
+                       (Q * 10_000 * 24 if score_launches else 0)}  # 24-B records (pair-packed f32)
     except Exception:
         traffic = None
     roof = {"bound": "fp32", "kernel": "k_score", "achieved": achieved, "peak": round(fp32_peak, 2),
