@@ -125,6 +125,91 @@ __device__ __forceinline__ void cluster_total(LMShared<NT>& sm) {
   __syncthreads();
 }
 
+// Packed points streamed through a shared-memory ring by TMA bulk copies
+// (cp.async.bulk global -> shared, mbarrier completion): the LM / MSAC
+// passes over the scoring subset and the compacted inliers re-read the same
+// 48-B records every pass, and the plain loads left the passes latency bound
+// (ncu: long_scoreboard 35 % of the k_scan stalls).  Each CTA walks its
+// contiguous share of the points in chunks of kStageCh records; chunk c lands
+// in ring slot c % kStageN while the CTA works on the earlier slots.  Within
+// a CTA, thread t still visits points t, t + NT, t + 2 NT, ... in order, so a
+// 1-CTA launch accumulates exactly as the unstaged loop does.
+constexpr int kStageCh = 512;  // records per chunk (24 KB)
+constexpr int kStageN = 3;     // ring depth
+constexpr size_t kStageBytes = (size_t)kStageN * kStageCh * 3 * sizeof(double2);
+
+struct StagedPts {
+  const double2* p;  // [3n] global
+  int n;
+  double2* ring;     // dynamic smem [kStageN][3 * kStageCh]
+  uint64_t* bar;     // smem mbarriers [kStageN]
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void stage_issue(const StagedPts& ps, int lo, int cnt, int c) {
+  const int slot = c % kStageN;
+  const int m = min(kStageCh, cnt - c * kStageCh);
+  const unsigned bytes = (unsigned)m * 48u;
+  const unsigned bar = smem_u32(ps.bar + slot);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(ps.ring + (size_t)slot * 3 * kStageCh)), "l"(ps.p + 3 * (int64_t)(lo + c * kStageCh)),
+               "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void stage_wait(const StagedPts& ps, int c) {
+  const unsigned bar = smem_u32(ps.bar + c % kStageN);
+  const unsigned parity = (unsigned)(c / kStageN) & 1u;
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// fn(P, u, v, w) for every point of this CTA's share (cluster rank r owns
+// [n r / cs, n (r+1) / cs)); all threads of the CTA must call it.
+template <int NT, typename F>
+__device__ __forceinline__ void staged_for_each(const StagedPts& ps, F&& fn) {
+  const int r = (int)cl_rank(), cs = (int)cl_size();
+  const int lo = (int)((int64_t)ps.n * r / cs), hi = (int)((int64_t)ps.n * (r + 1) / cs);
+  const int cnt = hi - lo;
+  const int nch = (cnt + kStageCh - 1) / kStageCh;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kStageN; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(ps.bar + b)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int c = 0; c < min(kStageN, nch); ++c) stage_issue(ps, lo, cnt, c);
+  for (int c = 0; c < nch; ++c) {
+    stage_wait(ps, c);
+    const double2* buf = ps.ring + (size_t)(c % kStageN) * 3 * kStageCh;
+    const int m = min(kStageCh, cnt - c * kStageCh);
+    for (int i = threadIdx.x; i < m; i += NT) {
+      const double2 a = buf[3 * i], b = buf[3 * i + 1], cc = buf[3 * i + 2];
+      const double P[3] = {a.x, a.y, b.x};
+      fn(P, b.y, cc.x, cc.y);
+    }
+    __syncthreads();  // every thread is done with the slot before it is refilled
+    if (threadIdx.x == 0 && c + kStageN < nch) stage_issue(ps, lo, cnt, c + kStageN);
+  }
+}
+
+template <typename PS>
+struct is_staged {
+  static constexpr bool value = false;
+};
+template <>
+struct is_staged<StagedPts> {
+  static constexpr bool value = true;
+};
+
 // Load rotation matrix + translation of `p` into shared memory (thread 0).
 template <int NT>
 __device__ __forceinline__ void set_eval_pose(LMShared<NT>& sm, const Pose& p) {
@@ -179,6 +264,16 @@ __device__ void msac_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, double
 #pragma unroll
   for (int k = 0; k < 3; ++k) t[k] = sm.t[k];
   double acc[2] = {0.0, 0.0};
+  if constexpr (is_staged<PS>::value) {
+    staged_for_each<NT>(ps, [&](const double* P0, double u0, double v0, double w0) {
+      const double e0 = msac_e2(R, t, in, P0, u0, v0);
+      acc[0] = acc[0] + dmul(w0, fmin(e0, t2));
+      acc[1] += e0 < t2 ? 1.0 : 0.0;
+    });
+    block_sum<NT, 2>(acc, sm.scratch, sm.red);
+    cluster_total<NT, 2>(sm);
+    return;
+  } else {
   const int step = NT * (int)cl_size();
   int i = threadIdx.x + NT * (int)cl_rank();
   // two points per trip: both loads in flight before the arithmetic
@@ -206,6 +301,7 @@ __device__ void msac_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, double
   }
   block_sum<NT, 2>(acc, sm.scratch, sm.red);
   cluster_total<NT, 2>(sm);
+  }
 }
 
 // Cost / gradient / normal-matrix contribution of one point.
@@ -289,19 +385,25 @@ __device__ void lm_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, int kind
 #pragma unroll
   for (int k = 0; k < kRed; ++k) acc[k] = 0.0;
   double behind = 0.0;
-  const int step = NT * (int)cl_size();
-  int i = threadIdx.x + NT * (int)cl_rank();
-  for (; i + step < ps.n; i += 2 * step) {
-    double P0[3], u0, v0, w0, P1[3], u1, v1, w1;
-    ps.load(i, P0, u0, v0, w0);
-    ps.load(i + step, P1, u1, v1, w1);
-    lm_point<GRAD>(R, t, in, kind, s2, P0, u0, v0, w0, acc, behind);
-    lm_point<GRAD>(R, t, in, kind, s2, P1, u1, v1, w1, acc, behind);
-  }
-  if (i < ps.n) {
-    double P0[3], u0, v0, w0;
-    ps.load(i, P0, u0, v0, w0);
-    lm_point<GRAD>(R, t, in, kind, s2, P0, u0, v0, w0, acc, behind);
+  if constexpr (is_staged<PS>::value) {
+    staged_for_each<NT>(ps, [&](const double* P0, double u0, double v0, double w0) {
+      lm_point<GRAD>(R, t, in, kind, s2, P0, u0, v0, w0, acc, behind);
+    });
+  } else {
+    const int step = NT * (int)cl_size();
+    int i = threadIdx.x + NT * (int)cl_rank();
+    for (; i + step < ps.n; i += 2 * step) {
+      double P0[3], u0, v0, w0, P1[3], u1, v1, w1;
+      ps.load(i, P0, u0, v0, w0);
+      ps.load(i + step, P1, u1, v1, w1);
+      lm_point<GRAD>(R, t, in, kind, s2, P0, u0, v0, w0, acc, behind);
+      lm_point<GRAD>(R, t, in, kind, s2, P1, u1, v1, w1, acc, behind);
+    }
+    if (i < ps.n) {
+      double P0[3], u0, v0, w0;
+      ps.load(i, P0, u0, v0, w0);
+      lm_point<GRAD>(R, t, in, kind, s2, P0, u0, v0, w0, acc, behind);
+    }
   }
   // slot kRed carries the behind-camera count (a deterministic OR)
   if (GRAD) {

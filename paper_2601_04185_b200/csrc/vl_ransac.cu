@@ -423,8 +423,13 @@ __device__ __forceinline__ int64_t required_iters_dev(double eps, double eta, in
 #endif
 constexpr int kScanThreads = VL_LO_NT;
 
-__global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, RansacParams p) {
-  extern __shared__ float costs[];
+// costs_smem: the round's fp32 costs are copied to shared memory (HCAP floats
+// after the staging ring) unless a huge batch_size would not fit, in which
+// case the scan reads them from L2.
+__global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, RansacParams p, int costs_smem) {
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  double2* ring = reinterpret_cast<double2*>(dyn_smem);  // kStageBytes (TMA staging ring)
+  __shared__ uint64_t stage_bar[kStageN];
   __shared__ LMShared<kScanThreads> sm;
   __shared__ Pose s_start;
   const int q = wk.active_list[blockIdx.x / cl_size()];
@@ -432,13 +437,15 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   const int nh = S.nh;
   // final fp32 costs (canonical order, reduced by the scorer's tile tickets)
   const float* cq = wk.cost32 + (int64_t)q * wk.HCAP;
-  for (int h = threadIdx.x; h < nh; h += kScanThreads) {
-    const float c = __ldcg(cq + h);
-    costs[h] = c;
+  const float* costs = cq;
+  if (costs_smem) {
+    float* cs = reinterpret_cast<float*>(dyn_smem + kStageBytes);  // [HCAP]
+    for (int h = threadIdx.x; h < nh; h += kScanThreads) cs[h] = __ldcg(cq + h);
+    costs = cs;
   }
   __syncthreads();
   const Intr in = S.in;
-  const PackedPts sub{wk.sub_pk + 3 * S.sub_off, S.nsub};
+  const StagedPts sub{wk.sub_pk + 3 * S.sub_off, S.nsub, ring, stage_bar};
   double best_cost = S.best_cost;
   int has_best = S.has_best;
   Pose best = S.best;
@@ -588,9 +595,19 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   }
   if (phase != 1) {
     H(kStageScan, true);
-    const size_t smem = (size_t)wk.HCAP * sizeof(float);
+    static int max_smem = 0;
+    if (max_smem == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      max_smem -= (int)(sizeof(LMShared<kScanThreads>) + 1024);  // static smem of the kernel
+      cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    }
+    const size_t with_costs = kStageBytes + (size_t)wk.HCAP * sizeof(float);
+    const int costs_smem = with_costs <= (size_t)max_smem ? 1 : 0;
+    const size_t smem = costs_smem ? with_costs : kStageBytes;
     launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, VL_LO_MINB * num_sms), st, wk,
-                     p);
+                     p, costs_smem);
     H(kStageScan, false);
     H(kStageActive, true);
     k_active<<<1, 1024, 0, st>>>(wk, nactive);
@@ -605,6 +622,8 @@ constexpr int kFinalThreads = VL_LO_NT;
 
 __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, Inputs in, Outputs out, RansacParams p,
                                                          int q_base) {
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  __shared__ uint64_t stage_bar[kStageN];
   __shared__ LMShared<kFinalThreads> sm;
   __shared__ int warp_tot[32];
   const unsigned cr = cl_rank(), cs = cl_size();
@@ -682,7 +701,7 @@ __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, In
   __threadfence();
   __syncthreads();
   if (cs > 1) cl_sync();  // compacted points of every CTA visible cluster-wide
-  const PackedPts inl{cpk, (int)cnt_full};
+  const StagedPts inl{cpk, (int)cnt_full, reinterpret_cast<double2*>(dyn_smem), stage_bar};
   lm_refine<kFinalThreads>(sm, inl, cin, best, kCauchy, p.cauchy, p.lm_max_iters, 1e-10, 1e-12, nullptr,
                            nullptr);
   const Pose fin = sm.cur;
@@ -693,7 +712,13 @@ __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, In
 
 int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
                  int q_base, cudaStream_t st) {
-  launch_clustered(k_final, Q, kFinalThreads, 0, pick_cluster(Q, VL_LO_MINB * 148), st, wk, in, out, p, q_base);
+  static bool attr = false;
+  if (!attr) {  // the staging ring needs more than the 48 KB default dynamic smem
+    cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes);
+    attr = true;
+  }
+  launch_clustered(k_final, Q, kFinalThreads, kStageBytes, pick_cluster(Q, VL_LO_MINB * 148), st, wk, in, out, p,
+                   q_base);
   return 1;
 }
 
