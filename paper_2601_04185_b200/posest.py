@@ -19,13 +19,16 @@ import math
 from dataclasses import dataclass, field
 
 import numpy as np
+import os
+import time
 
 from . import _lib
 from .geometry import CameraIntrinsics, Pose
 
 __all__ = [
     "Match2D3D", "PoseEstimate", "RansacConfig", "UnderConstrainedError", "msac_score",
-    "ransac_pnp", "ransac_pnp_batch", "ransac_pnp_device", "required_iterations",
+    "ransac_pnp", "ransac_pnp_batch", "ransac_pnp_device", "ransac_pnp_host", "ransac_pnp_stream",
+    "required_iterations",
 ]
 
 
@@ -333,6 +336,176 @@ def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chu
     h2d_bytes = sum(int(t.numel() * t.element_size()) for t in host_in)
     d2h_bytes = sum(int(v.nbytes) for v in host.values())
     return host, h2d_bytes, d2h_bytes
+
+
+_STREAM_DEBUG = bool(os.environ.get("VISLOC_STREAM_DEBUG"))
+
+
+def ransac_pnp_stream(batches, cfg: RansacConfig):
+    """Serve a sequence of query batches held in HOST memory (generator; the serving loop).
+
+    ``batches``: iterable of ``(px, X, w, offsets, intrinsics, seeds)`` — the
+    arguments of ``ransac_pnp_host`` (pinned torch CPU tensors for full PCIe
+    bandwidth).  Yields ``(results, h2d_bytes, d2h_bytes)`` per batch, in
+    order, ``results`` as ``ransac_pnp_host`` returns them.
+
+    Batch k+1's inputs are copied to HBM on a side stream while batch k is
+    estimated (two device input buffers), so after the first batch — which is
+    admitted stage by stage like ``ransac_pnp_host`` — a steady stream runs at
+    the estimator's device-resident rate whenever the PCIe copy of a batch is
+    shorter than its estimation.  Every batch's H2D and its results' D2H are
+    real copies; nothing is cached between batches.
+    """
+    import torch
+    _lib.context()
+    comp = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    bufs = [None, None]       # device input sets (px, X, w), alternating
+    freed = [None, None]      # event: the run that read the set has finished
+    copy.wait_stream(comp)
+
+    def prepare(b):
+        px, X, w, offsets, intrinsics, seeds = b
+        offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+        host_in = []
+        for a in (px, X, w):
+            t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+            if not t.is_pinned():
+                t = t.pin_memory()
+            host_in.append(t)
+        return host_in, offsets, list(intrinsics), list(seeds)
+
+    def h2d(k, host_in, offsets, staged):
+        """Enqueue batch k's copy into buffer set k % 2; returns (stage ends, events)."""
+        j = k % 2
+        if bufs[j] is None or any(bd.shape != hs.shape for bd, hs in zip(bufs[j], host_in)):
+            with torch.cuda.stream(copy):
+                if freed[j] is not None:
+                    copy.wait_event(freed[j])
+                bufs[j] = [torch.empty(t.shape, dtype=t.dtype, device=dev) for t in host_in]
+        Q = offsets.shape[0] - 1
+        ends = _stage_schedule(Q) if staged else [Q]
+        events = []
+        with torch.cuda.stream(copy):
+            if freed[j] is not None:
+                copy.wait_event(freed[j])  # the run that read this set (batch k-2) is done
+            q0 = 0
+            for q1 in ends:
+                r0, r1 = int(offsets[q0]), int(offsets[q1])
+                for dst, src in zip(bufs[j], host_in):
+                    dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+                events.append(ev)
+                q0 = q1
+        return ends, events
+
+    _t0 = time.perf_counter()
+    host_pool = _PINNED_POOL  # shared by streams: pinned allocations are slow
+    it = iter(batches)
+    try:
+        cur = prepare(next(it))
+    except StopIteration:
+        return
+    k = 0
+    cur_stage = h2d(0, cur[0], cur[1], staged=True)
+    if _STREAM_DEBUG:
+        print(f"[stream] first copies queued at {time.perf_counter() - _t0:.4f}", flush=True)
+    pending = None  # (host results, done event, h2d bytes) of the previous batch
+    while cur is not None:
+        host_in, offsets, intrinsics, seeds = cur
+        try:
+            nxt = prepare(next(it))
+        except StopIteration:
+            nxt = None
+        # batch k+1's copy is queued before batch k runs (its buffer set was
+        # read by batch k-1, already finished) so it streams during the run
+        nxt_stage = h2d(k + 1, nxt[0], nxt[1], staged=False) if nxt is not None else None
+        N = int(offsets[-1])
+        j = k % 2
+        if _STREAM_DEBUG:
+            print(f"[stream] batch {k}: launch run at {time.perf_counter() - _t0:.4f}", flush=True)
+        out = ransac_pnp_device(bufs[j][0], bufs[j][1], bufs[j][2], offsets, intrinsics, seeds, cfg,
+                                stages=cur_stage)
+        if _STREAM_DEBUG:
+            print(f"[stream] batch {k}: run returned at {time.perf_counter() - _t0:.4f}", flush=True)
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        freed[j] = ev
+        # results D2H on the copy stream (overlaps the next run); batch k is
+        # handed out once batch k+1 has been launched
+        host_out = host_pool.get({key: (tuple(v.shape) if key != "flags" else (N,), v.dtype)
+                                  for key, v in out.items()})
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev)
+            for key, v in out.items():
+                v.record_stream(copy)
+                host_out.tensors[key].copy_(v[:N] if key == "flags" else v, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(copy)
+        h2d_bytes = sum(int(t.numel() * t.element_size()) for t in host_in)
+        if _STREAM_DEBUG:
+            print(f"[stream] batch {k}: D2H queued at {time.perf_counter() - _t0:.4f}", flush=True)
+        if pending is not None:
+            r = _stream_result(*pending)
+            if _STREAM_DEBUG:
+                print(f"[stream] batch {k - 1}: results ready at {time.perf_counter() - _t0:.4f}", flush=True)
+            yield r
+        pending = (host_out, done, h2d_bytes)
+        cur, cur_stage = nxt, nxt_stage
+        k += 1
+    if pending is not None:
+        yield _stream_result(*pending)
+
+
+def _stream_result(host_out, done, h2d_bytes):
+    done.synchronize()
+    host = {key: v.numpy() for key, v in host_out.tensors.items()}
+    host_out.hand_out(host.values())
+    return host, h2d_bytes, sum(int(v.nbytes) for v in host.values())
+
+
+class _PinnedPool:
+    """Pinned host result buffers reused across the batches of a stream.
+
+    A buffer set is reused only once every numpy array handed out from it has
+    been released by the caller (weak references), so results stay valid for
+    as long as they are referenced; a fresh pinned allocation (slow: it can
+    cost tens of ms) is only made when no released set of the right shapes
+    exists."""
+
+    class _Set:
+        def __init__(self, spec):
+            import torch
+            self.spec = spec
+            self.tensors = {k: torch.empty(shape, dtype=dt, pin_memory=True) for k, (shape, dt) in spec.items()}
+            self.refs = []
+
+        def free(self):
+            return all(r() is None for r in self.refs)
+
+        def hand_out(self, arrays):
+            import weakref
+            self.refs = [weakref.ref(a) for a in arrays]
+
+    def __init__(self):
+        self.sets = []
+
+    def get(self, spec):
+        for st in self.sets:
+            if st.spec == spec and st.free():
+                st.refs = [lambda: True]  # busy until handed out
+                return st
+        st = _PinnedPool._Set(spec)
+        st.refs = [lambda: True]
+        self.sets.append(st)
+        if len(self.sets) > 8:  # drop the oldest released sets beyond a small cache
+            self.sets = [x for x in self.sets[:-8] if not x.free()] + self.sets[-8:]
+        return st
+
+
+_PINNED_POOL = _PinnedPool()
 
 
 def _host_pipeline_chunks(host_in, offsets, intrinsics, seeds, cfg, chunk_queries, out, host_out, comp, copy, dev):

@@ -216,6 +216,32 @@ def test_host_api_chunked_pipeline_equals_device(vl):
             assert np.array_equal(host[k], ref[k]), (chunk, k)
 
 
+def test_host_stream_equals_device(vl):
+    """ransac_pnp_stream (batch k+1's H2D overlapping batch k, first batch staged) == device calls."""
+    import torch
+    from paper_2601_04185_b200.posest import ransac_pnp_device, ransac_pnp_stream
+    cfg = vl.RansacConfig(max_iterations=2000, miss_probability=1e-300)
+    batches, refs = [], []
+    for b, Q in enumerate((5, 9, 5, 3)):  # sizes change between batches (buffer re-allocation)
+        pxs, Xs, ws = batch_a(Q, 900 + 100 * b, 0.5, 1.0, seed0=200 + 10 * b)
+        offsets = np.concatenate([[0], np.cumsum([p.shape[0] for p in pxs])]).astype(np.int64)
+        px, X, w = np.concatenate(pxs), np.concatenate(Xs), np.concatenate(ws)
+        intr = [vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)] * Q
+        seeds = [7 * i + b for i in range(Q)]
+        batches.append((torch.from_numpy(px).pin_memory(), torch.from_numpy(X).pin_memory(),
+                        torch.from_numpy(w).pin_memory(), offsets, intr, seeds))
+        r = ransac_pnp_device(torch.from_numpy(px).cuda(), torch.from_numpy(X).cuda(), torch.from_numpy(w).cuda(),
+                              offsets, intr, seeds, cfg)
+        refs.append(({k: v.cpu().numpy() for k, v in r.items()}, px.nbytes + X.nbytes + w.nbytes))
+    got = list(ransac_pnp_stream(batches, cfg))
+    assert len(got) == len(refs)
+    for (host, h2d, d2h), (ref, nbytes) in zip(got, refs):
+        assert h2d == nbytes and d2h > 0
+        for k in ("q", "t", "flags", "count", "score", "iterations", "converged", "stats"):
+            assert np.array_equal(host[k], ref[k]), k
+    assert list(ransac_pnp_stream([], cfg)) == []
+
+
 def test_randomized_parity_sweep(vl, intr):
     """40 seeded problems across inlier ratio / noise / size / config regimes:
     GPU ransac_pnp vs the CPU oracle (itself bit-identical to the reference)."""
