@@ -183,7 +183,13 @@ struct CandRec {
   int lane, pad;
 };
 
-__global__ void __launch_bounds__(kP3PRootThreads) k_p3p_roots(Work wk, Inputs in) {
+#ifndef VL_P3P_ROOT_MINB
+#define VL_P3P_ROOT_MINB 5  // measured: 5 resident CTAs (96 regs) beat 4 (112 regs)
+#endif
+#ifndef VL_P3P_POLISH_MINB
+#define VL_P3P_POLISH_MINB 8  // measured: 128-register cap, 8 CTAs
+#endif
+__global__ void __launch_bounds__(kP3PRootThreads, VL_P3P_ROOT_MINB) k_p3p_roots(Work wk, Inputs in) {
   const int q = wk.active_list[blockIdx.x];
   const QState& S = wk.qs[q];
   const int s = blockIdx.y * kP3PRootThreads + threadIdx.x;
@@ -210,7 +216,7 @@ __global__ void __launch_bounds__(kP3PRootThreads) k_p3p_roots(Work wk, Inputs i
   wk.p3p_nc[si] = nc;
 }
 
-__global__ void __launch_bounds__(kP3PThreads) k_p3p_polish(Work wk) {
+__global__ void __launch_bounds__(kP3PThreads, VL_P3P_POLISH_MINB) k_p3p_polish(Work wk) {
   __shared__ CandRec cand[kP3PThreads / 32][32 * kMaxCand];
   __shared__ double res[kP3PThreads / 32][32][13];
   const int q = wk.active_list[blockIdx.x];
