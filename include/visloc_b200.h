@@ -140,6 +140,16 @@ int vl_ransac_partial_bytes(vl_ctx* ctx, int64_t* bytes);
 int vl_ransac_step_score(vl_ctx* ctx, void* partial_out, void* stream);
 int vl_ransac_step_finish(vl_ctx* ctx, const void* partial_in, int32_t* nactive, void* stream);
 int vl_ransac_end(vl_ctx* ctx, const vl_ransac_out* out, void* stream);
+/* BASELINE's packed (score, index) variant of the hypothesis split — an
+ * APPROXIMATION of the reference (at most one LO per round, on the batch's
+ * best hypothesis, instead of the ordered first-better chain).  Per round:
+ *   vl_ransac_step_score(ctx, NULL)        -> this rank's owned costs
+ *   vl_ransac_step_argmin(ctx, keys)       -> keys DEVICE int64 [Q]: min over owned
+ *                                             hypotheses of float_bits(cost) << 32 | h
+ *   MIN all-reduce of keys across ranks    (8 B per query)
+ *   vl_ransac_step_finish_argmin(ctx, keys, &n) -> scan / LO / stop on the winner */
+int vl_ransac_step_argmin(vl_ctx* ctx, int64_t* keys, void* stream);
+int vl_ransac_step_finish_argmin(vl_ctx* ctx, const int64_t* keys, int32_t* nactive, void* stream);
 
 /* replaces visloc.posest.msac_score (posest.py:160).  pose q[4], t[3] HOST;
  * arrays DEVICE; cost -> *cost_out (HOST), flags -> DEVICE (may be NULL). */

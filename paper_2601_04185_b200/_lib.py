@@ -183,8 +183,11 @@ def lib():
         L.vl_ransac_step_score.argtypes = [vp, vp, vp]
         L.vl_ransac_step_finish.argtypes = [vp, vp, C.POINTER(C.c_int32), vp]
         L.vl_ransac_end.argtypes = [vp, C.POINTER(RansacOut), vp]
+        L.vl_ransac_step_argmin.argtypes = [vp, vp, vp]
+        L.vl_ransac_step_finish_argmin.argtypes = [vp, vp, C.POINTER(C.c_int32), vp]
         for name in ("vl_ransac_begin", "vl_ransac_partial_bytes", "vl_ransac_step_score",
-                     "vl_ransac_step_finish", "vl_ransac_end"):
+                     "vl_ransac_step_finish", "vl_ransac_end", "vl_ransac_step_argmin",
+                     "vl_ransac_step_finish_argmin"):
             getattr(L, name).restype = C.c_int
         L.vl_quantize_depth.argtypes = [vp, C.POINTER(DepthCodecJob), i32, vp, i32, vp]
         L.vl_reduce_depth_codes.argtypes = [vp, C.POINTER(DepthCodecJob), i32, i32, i32, vp]
@@ -212,7 +215,7 @@ EXPORTED_SYMBOLS = (
     "vl_decode_depth", "vl_robust_cost", "vl_pose_residuals", "vl_ransac_begin", "vl_ransac_partial_bytes",
     "vl_ransac_step_score", "vl_ransac_step_finish", "vl_ransac_end", "vl_imlc_parse",
     "vl_retrieval_topk", "vl_ransac_pnp_staged", "vl_quantize_depth", "vl_reduce_depth_codes",
-    "vl_build_depth_maps", "vl_triangulate_rays",
+    "vl_build_depth_maps", "vl_triangulate_rays", "vl_ransac_step_argmin", "vl_ransac_step_finish_argmin",
 )
 
 STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final", "lift")

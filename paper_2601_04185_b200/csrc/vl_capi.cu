@@ -588,6 +588,24 @@ int vl_ransac_step_finish(vl_ctx* c, const void* partial_in, int32_t* nactive, v
   return VL_OK;
 }
 
+int vl_ransac_step_argmin(vl_ctx* c, int64_t* keys, void* stream) {
+  if (!c || !c->step.open || !keys) return fail(c, VL_ERR_INVALID, "no open stepwise run");
+  if (c->step.nactive <= 0) return fail(c, VL_ERR_INVALID, "no active queries");
+  cudaStream_t st = (cudaStream_t)stream;
+  c->launches += launch_fill_i64((long long*)keys, c->step.Q, INT64_MAX, st);  // inactive queries: no candidate
+  c->launches += launch_split_argmin(c->step.wk, c->step.nactive, c->num_sms, (long long*)keys, st);
+  return check_launch(c);
+}
+
+int vl_ransac_step_finish_argmin(vl_ctx* c, const int64_t* keys, int32_t* nactive, void* stream) {
+  if (!c || !c->step.open || !keys || !nactive) return fail(c, VL_ERR_INVALID, "no open stepwise run");
+  cudaStream_t st = (cudaStream_t)stream;
+  c->launches += launch_split_apply_argmin(c->step.wk, c->step.nactive, (const long long*)keys, st);
+  int rc;
+  if ((rc = check_launch(c))) return rc;
+  return vl_ransac_step_finish(c, nullptr, nactive, stream);
+}
+
 int vl_ransac_end(vl_ctx* c, const vl_ransac_out* o, void* stream) {
   if (!c || !c->step.open || !o) return fail(c, VL_ERR_INVALID, "no open stepwise run");
   if (c->step.nactive != 0) return fail(c, VL_ERR_INVALID, "queries still active");

@@ -129,4 +129,9 @@ int launch_p3p_batch(const double* f, const double* P, int B, double* slots, int
 int launch_sample(const GenState& g, uint64_t pos0, int64_t n, int count, int* out, uint64_t* pos_out,
                   cudaStream_t st);
 
+// hypothesis-split packed (score, index) variant (vl_ransac.cu)
+int launch_split_argmin(const Work& wk, int nactive, int num_sms, long long* keys, cudaStream_t st);
+int launch_split_apply_argmin(const Work& wk, int nactive, const long long* keys, cudaStream_t st);
+int launch_fill_i64(long long* p, int n, long long v, cudaStream_t st);
+
 }  // namespace vl

@@ -570,6 +570,77 @@ static void launch_clustered(void (*k)(KArgs...), int nq, int block, size_t smem
   cudaLaunchKernelEx(&cfg, k, args...);
 }
 
+// coarse scoring items unless the whole batch would not fill ~3 waves of SMs
+static bool round_is_fine(const Work& wk, int nactive, int num_sms) {
+  const int coarse_items = nactive * 2 * ((wk.NSPLIT + kScoreItemSplits - 1) / kScoreItemSplits);
+  return coarse_items < 3 * num_sms;
+}
+
+// ---------------------------------------------------------- hypothesis-split argmin
+// BASELINE's packed (score, index) variant of the hypothesis split (SURVEY
+// §8e): per active query, the minimum over this rank's OWN hypotheses of
+// key = float_bits(cost) << 32 | h (costs are >= 0, so the bit pattern orders
+// like the value and ties go to the lowest index); other queries keep
+// INT64_MAX.  A MIN all-reduce of the keys (8 B per query) then selects the
+// batch's best hypothesis on every rank.
+__global__ void __launch_bounds__(256) k_split_argmin(Work wk, int tile_h, long long* keys) {
+  __shared__ long long s_min[8];
+  const int q = wk.active_list[blockIdx.x];
+  const QState& S = wk.qs[q];
+  const int nh = S.nh, size = wk.split_size;
+  const int t0 = size > 1 ? (int)((((int64_t)wk.split_rank - (int64_t)q * wk.TCAP) % size + size) % size) : 0;
+  const float* cq = wk.cost32 + (int64_t)q * wk.HCAP;
+  long long best = LLONG_MAX;
+  for (int h = threadIdx.x; h < nh; h += blockDim.x) {
+    if ((h / tile_h) % size != t0) continue;
+    const long long key = ((long long)__float_as_uint(__ldcg(cq + h)) << 32) | (long long)h;
+    best = min(best, key);
+  }
+  for (int o = 16; o > 0; o >>= 1) best = min(best, (long long)__shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long m = s_min[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = min(m, s_min[w]);
+    keys[q] = m;
+  }
+}
+
+// After the MIN all-reduce: the scan sees only the winning hypothesis (its
+// cost; +inf for the rest of the batch), so the round runs at most one LO.
+__global__ void __launch_bounds__(256) k_split_apply_argmin(Work wk, const long long* keys) {
+  const int q = wk.active_list[blockIdx.x];
+  const int nh = wk.qs[q].nh;
+  const long long key = keys[q];
+  const int hw = key == LLONG_MAX ? -1 : (int)(key & 0xffffffffLL);
+  const float cw = __uint_as_float((unsigned)((unsigned long long)key >> 32));
+  float* cq = wk.cost32 + (int64_t)q * wk.HCAP;
+  for (int h = threadIdx.x; h < nh; h += blockDim.x) cq[h] = h == hw ? cw : CUDART_INF_F;
+}
+
+__global__ void k_fill_i64(long long* p, int n, long long v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
+}
+
+int launch_fill_i64(long long* p, int n, long long v, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_fill_i64<<<(n + 255) / 256, 256, 0, st>>>(p, n, v);
+  return 1;
+}
+
+int launch_split_argmin(const Work& wk, int nactive, int num_sms, long long* keys, cudaStream_t st) {
+  if (nactive <= 0) return 0;
+  k_split_argmin<<<nactive, 256, 0, st>>>(wk, round_is_fine(wk, nactive, num_sms) ? kScoreTileHypsFine
+                                                                                  : kScoreTileHyps, keys);
+  return 1;
+}
+
+int launch_split_apply_argmin(const Work& wk, int nactive, const long long* keys, cudaStream_t st) {
+  if (nactive <= 0) return 0;
+  k_split_apply_argmin<<<nactive, 256, 0, st>>>(wk, keys);
+  return 1;
+}
+
 // One round, kernel by kernel; `hook(stage, begin)` lets the caller bracket
 // each launch with CUDA events (profiling) without touching the kernels.
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
@@ -578,9 +649,7 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     if (hook) hook(hook_arg, stage, begin);
   };
   int n = 0;
-  // coarse work items unless the whole batch would not fill ~3 waves of SMs
-  const int coarse_items = nactive * 2 * ((wk.NSPLIT + kScoreItemSplits - 1) / kScoreItemSplits);
-  const int fine = coarse_items < 3 * num_sms ? 1 : 0;
+  const int fine = round_is_fine(wk, nactive, num_sms) ? 1 : 0;
   if (phase != 2) {
     H(kStageSample, true);
     k_sample<<<nactive, 256, 0, st>>>(wk, p);

@@ -82,6 +82,26 @@ class SplitRun:
         self.ctx.check(self.L.vl_ransac_step_score(self.ctx.handle, self.partial.data_ptr(), _lib.stream_ptr()),
                        "vl_ransac_step_score")
 
+    def argmin(self):
+        """Packed (score, index) keys of this rank's owned hypotheses -> ``self.keys`` (int64 [Q])."""
+        import torch
+
+        from . import _lib
+        if getattr(self, "keys", None) is None:
+            self.keys = torch.empty((self.Q,), dtype=torch.int64, device=self.partial.device)
+        self.ctx.check(self.L.vl_ransac_step_argmin(self.ctx.handle, self.keys.data_ptr(), _lib.stream_ptr()),
+                       "vl_ransac_step_argmin")
+
+    def finish_argmin(self) -> int:
+        import ctypes as C
+
+        from . import _lib
+        n = C.c_int32()
+        self.ctx.check(self.L.vl_ransac_step_finish_argmin(self.ctx.handle, self.keys.data_ptr(), C.byref(n),
+                                                           _lib.stream_ptr()), "vl_ransac_step_finish_argmin")
+        self.nactive = int(n.value)
+        return self.nactive
+
     def finish(self) -> int:
         import ctypes as C
 
@@ -120,15 +140,21 @@ class SplitRun:
         return _estimates_from(out, self.offsets)
 
 
-def ransac_pnp_split(matches, intr, cfg, group=None):
+def ransac_pnp_split(matches, intr, cfg, group=None, mode: str = "sum"):
     """One query's hypotheses split across the ranks of `group` (one GPU each).
 
-    Every rank passes the same matches and config; per round, one NCCL SUM
-    all-reduce of the partial-cost buffer (SURVEY §8e "exact reference
-    semantics" variant: the full cost vector, so the ordered first-better
-    scan is unchanged).  Returns the same PoseEstimate on every rank,
-    bit-identical to ``ransac_pnp``.
+    Every rank passes the same matches and config.  ``mode="sum"`` (default):
+    per round, one NCCL SUM all-reduce of the partial-cost buffer (SURVEY §8e
+    "exact reference semantics" variant: the full cost vector, so the ordered
+    first-better scan is unchanged) — the same PoseEstimate on every rank,
+    bit-identical to ``ransac_pnp``.  ``mode="argmin"``: BASELINE's packed
+    (score, index) variant — one MIN all-reduce of an 8-byte key per query
+    per round; the scan then sees only the batch's best hypothesis (at most
+    one LO per round), an APPROXIMATION of the reference's ordered chain that
+    is identical on every rank and for every split size.
     """
+    if mode not in ("sum", "argmin"):
+        raise ValueError(f"mode must be 'sum' or 'argmin', got {mode!r}")
     import torch
     import torch.distributed as dist
 
@@ -145,6 +171,12 @@ def ransac_pnp_split(matches, intr, cfg, group=None):
     run = SplitRun(ctx, dpx, dX, dw, [0, px.shape[0]], [intr], [cfg.seed], cfg, rank, world)
     while run.nactive > 0:
         run.score()
+        if mode == "argmin":
+            run.argmin()
+            if world > 1:
+                dist.all_reduce(run.keys, op=dist.ReduceOp.MIN, group=group)
+            run.finish_argmin()
+            continue
         if world > 1:
             dist.all_reduce(run.partial, op=dist.ReduceOp.SUM, group=group)
         run.finish()

@@ -301,3 +301,46 @@ def test_hypothesis_split_emulated_ranks_bit_identical(vl, intr):
             e = r.end()[0]
             assert np.array_equal(e.pose.q, ref.pose.q) and np.array_equal(e.pose.t, ref.pose.t)
             assert np.array_equal(e.inlier_flags, ref.inlier_flags) and e.iterations == ref.iterations
+
+
+def test_hypothesis_split_argmin_variant(vl, intr):
+    """BASELINE's packed (score, index) split: one int64 MIN all-reduce per round
+    (emulated ranks on one GPU).  Identical on every rank and for every split
+    size; round 1 picks the argmin of the exact fp32 costs; the pose stays close
+    to the exact estimator's (it is an approximation of the reference chain)."""
+    import torch
+    from paper_2601_04185_b200 import _lib
+    from paper_2601_04185_b200.dist import SplitRun, ransac_pnp_split
+    from paper_2601_04185_b200.geometry import pose_error
+    px, X, w, _ = matches_a(6000, 0.6, 1.0, seed=78)
+    cfg = vl.RansacConfig(seed=13, max_iterations=4000, miss_probability=1e-300)
+    exact = vl.ransac_pnp((px, X, w), intr, cfg)
+    one = ransac_pnp_split((px, X, w), intr, cfg, mode="argmin")  # world = 1
+    err = pose_error(one.pose, exact.pose)
+    assert err.rotation_error_deg < 0.05 and one.converged
+    d = [torch.from_numpy(a).cuda() for a in (px, X, w)]
+    # round 1: the winning key is the argmin (first minimum) of the full fp32 cost vector
+    ref_run = SplitRun(_lib.Context(0), d[0], d[1], d[2], [0, px.shape[0]], [intr], [cfg.seed], cfg, 0, 1)
+    ref_run.score()
+    ref_run.argmin()
+    for G in (2, 3):
+        ctxs = [_lib.Context(0) for _ in range(G)]
+        runs = [SplitRun(ctxs[r], d[0], d[1], d[2], [0, px.shape[0]], [intr], [cfg.seed], cfg, r, G)
+                for r in range(G)]
+        first = True
+        while runs[0].nactive > 0:
+            for r in runs:
+                r.score()
+                r.argmin()
+            keys = torch.stack([r.keys for r in runs]).min(0).values
+            if first:
+                assert int(keys[0].item()) == int(ref_run.keys[0].item())
+                first = False
+            for r in runs:
+                r.keys.copy_(keys)
+            n = [r.finish_argmin() for r in runs]
+            assert len(set(n)) == 1
+        for r in runs:
+            e = r.end()[0]
+            assert np.array_equal(e.pose.q, one.pose.q) and np.array_equal(e.pose.t, one.pose.t)
+            assert np.array_equal(e.inlier_flags, one.inlier_flags)

@@ -19,7 +19,7 @@ def _port():
     return p
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, mode="sum"):
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parent.parent
@@ -34,14 +34,19 @@ def _worker(rank, port, q):
     px, X, w, _ = matches_a(5000, 0.6, 1.0, seed=31)
     intr = vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
     cfg = vl.RansacConfig(seed=8, max_iterations=3000, miss_probability=1e-300)
-    e = ransac_pnp_split((px, X, w), intr, cfg)
-    ref = vl.ransac_pnp((px, X, w), intr, cfg)
+    e = ransac_pnp_split((px, X, w), intr, cfg, mode=mode)
+    if mode == "sum":
+        ref = vl.ransac_pnp((px, X, w), intr, cfg)
+    else:  # the approximate variant must not depend on the split size
+        singles = [dist.new_group([0]), dist.new_group([1])]  # collective: every rank creates both
+        ref = ransac_pnp_split((px, X, w), intr, cfg, group=singles[rank], mode=mode)
     q.put((rank, np.array_equal(e.pose.q, ref.pose.q) and np.array_equal(e.inlier_flags, ref.inlier_flags),
            e.pose.q.tolist()))
     dist.destroy_process_group()
 
 
-def test_split_two_processes():
+@pytest.mark.parametrize("mode", ["sum", "argmin"])
+def test_split_two_processes(mode):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -49,7 +54,7 @@ def test_split_two_processes():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, port, q, mode)) for r in range(2)]
     for p in ps:
         p.start()
     res = sorted(q.get(timeout=300) for _ in ps)
