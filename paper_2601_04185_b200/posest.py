@@ -403,6 +403,17 @@ def ransac_pnp_stream(batches, cfg: RansacConfig):
 
     _t0 = time.perf_counter()
     host_pool = _PINNED_POOL  # shared by streams: pinned allocations are slow
+    try:
+        yield from _stream_loop(batches, cfg, prepare, h2d, bufs, freed, host_pool, comp, copy, _t0)
+    finally:
+        # a consumer may stop early: in-flight kernels and copies still use the
+        # device buffers this generator owns, so drain both streams first
+        copy.synchronize()
+        comp.synchronize()
+
+
+def _stream_loop(batches, cfg, prepare, h2d, bufs, freed, host_pool, comp, copy, _t0):
+    import torch
     it = iter(batches)
     try:
         cur = prepare(next(it))

@@ -240,6 +240,10 @@ def test_host_stream_equals_device(vl):
         for k in ("q", "t", "flags", "count", "score", "iterations", "converged", "stats"):
             assert np.array_equal(host[k], ref[k]), k
     assert list(ransac_pnp_stream([], cfg)) == []
+    g = ransac_pnp_stream(batches, cfg)  # a consumer that stops early
+    host, _, _ = next(g)
+    g.close()
+    assert np.array_equal(host["q"], refs[0][0]["q"])
 
 
 def test_randomized_parity_sweep(vl, intr):
