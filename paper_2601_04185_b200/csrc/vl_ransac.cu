@@ -14,6 +14,7 @@
 // the Cauchy refinement (posest.py:284-299).
 #include <climits>
 #include <cstddef>
+#include <cstdlib>
 #include "vl_internal.h"
 #include "vl_lm.cuh"
 #include "vl_p3p.cuh"
@@ -792,8 +793,9 @@ int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const Ran
     cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes);
     attr = true;
   }
-  launch_clustered(k_final, Q, kFinalThreads, kStageBytes, pick_cluster(Q, VL_LO_MINB * 148), st, wk, in, out, p,
-                   q_base);
+  int cs = pick_cluster(Q, VL_LO_MINB * 148);
+  if (const char* e = getenv("VISLOC_FINAL_CS")) cs = atoi(e);  // tuning knob
+  launch_clustered(k_final, Q, kFinalThreads, kStageBytes, cs, st, wk, in, out, p, q_base);
   return 1;
 }
 
