@@ -169,12 +169,55 @@ def _check_job(entry, covis, fields):
     return gh, gw
 
 
+_VIEW_DTYPE = np.dtype([("targets", "<u8"), ("confidence", "<u8"), ("rt", "<f8", 9), ("center", "<f8", 3),
+                        ("fx", "<f8"), ("fy", "<f8"), ("cx", "<f8"), ("cy", "<f8")])          # vl_tri_view
+_MAP_DTYPE = np.dtype([("grid_w", "<i4"), ("grid_h", "<i4"), ("view0", "<i4"), ("nview", "<i4"),
+                       ("fx", "<f8"), ("fy", "<f8"), ("cx", "<f8"), ("cy", "<f8"), ("sx", "<f8"), ("sy", "<f8"),
+                       ("R", "<f8", 9), ("center", "<f8", 3), ("depth", "<u8"), ("valid", "<u8")])  # vl_tri_map
+assert _VIEW_DTYPE.itemsize == 144 and _MAP_DTYPE.itemsize == 176
+
+
+class _Staging:
+    """Pinned host staging buffers reused across plans (a pinned allocation
+    costs tens of ms); a buffer is refilled only after its H2D has completed."""
+
+    def __init__(self):
+        self.bufs = []  # [tensor, event or None]
+
+    def get(self, nbytes: int):
+        import torch
+        for b in self.bufs:
+            if b[0].numel() >= nbytes and (b[1] is None or b[1].query()):
+                return b
+        b = [torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True), None]
+        self.bufs.append(b)
+        if len(self.bufs) > 4:
+            self.bufs = [x for x in self.bufs[:-4] if x[1] is not None and not x[1].query()] + self.bufs[-4:]
+        return b
+
+
+_STAGING = _Staging()
+
+
+def _cam_record(pose, intr, cache):
+    """(R^T row-major, centre, fx, fy, cx, cy) of a camera, computed once per pose object."""
+    key = id(pose)
+    r = cache.get(key)
+    if r is None:
+        r = (np.asarray(pose.R, dtype=np.float64).T.reshape(-1), np.asarray(pose.center(), dtype=np.float64),
+             float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy), pose)
+        cache[key] = r
+    return r
+
+
 class DepthBuildPlan:
     """Many entries' fields resident in HBM, ready to triangulate (the device-resident path).
 
-    Construction does the host work once (checks, field packing + one H2D,
-    map / view records); ``run()`` launches ``vl_build_depth_maps`` into the
-    plan's device outputs ``depth`` (f32) / ``valid`` (u8), packed map after map."""
+    Construction does the host work once (checks, field packing into a pooled
+    pinned buffer + one H2D, map / view records as numpy structured arrays
+    with per-camera values computed once per pose); ``run()`` launches
+    ``vl_build_depth_maps`` into the plan's device outputs ``depth`` (f32) /
+    ``valid`` (u8), packed map after map."""
 
     def __init__(self, jobs, cfg: TriangulationConfig):
         import torch
@@ -185,44 +228,56 @@ class DepthBuildPlan:
         fields = [f for _, _, fl in self.jobs for f in fl]
         self.f64 = any(np.asarray(f.confidence).dtype != np.float32 or np.asarray(f.targets).dtype != np.float32
                        for f in fields)
-        dt = np.float64 if self.f64 else np.float32
-        tg = [np.ascontiguousarray(f.targets, dtype=dt).reshape(-1) for f in fields]
-        cf = [np.ascontiguousarray(f.confidence, dtype=dt).reshape(-1) for f in fields]
-        t_off = np.concatenate([[0], np.cumsum([a.size for a in tg])]).astype(np.int64)
-        c_off = np.concatenate([[0], np.cumsum([a.size for a in cf])]).astype(np.int64)
-        self.T = torch.from_numpy(np.concatenate(tg) if tg else np.zeros(1, dt)).pin_memory().cuda(non_blocking=True)
-        self.C = torch.from_numpy(np.concatenate(cf) if cf else np.zeros(1, dt)).pin_memory().cuda(non_blocking=True)
-        self.field_bytes = int(self.T.numel() + self.C.numel()) * (8 if self.f64 else 4)
-        item = 8 if self.f64 else 4
+        dt = np.dtype(np.float64 if self.f64 else np.float32)
+        item = dt.itemsize
+        ncell = np.fromiter((f.grid_w * f.grid_h for f in fields), dtype=np.int64, count=len(fields))
+        c_off = np.concatenate([[0], np.cumsum(ncell)]).astype(np.int64)
+        tot_cells = int(c_off[-1])
+        # one pinned buffer: targets (2 values / cell) then confidences (1 / cell)
+        nbytes = 3 * tot_cells * item
+        stage = _STAGING.get(nbytes)
+        host = stage[0].numpy()[:nbytes].view(dt)
+        if fields:
+            np.concatenate([np.asarray(f.targets, dtype=dt).reshape(-1) for f in fields], out=host[:2 * tot_cells])
+            np.concatenate([np.asarray(f.confidence, dtype=dt).reshape(-1) for f in fields], out=host[2 * tot_cells:])
+        self.D = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
+        self.D[:nbytes].copy_(stage[0][:nbytes], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        stage[1] = ev
+        self.field_bytes = nbytes
+        base = self.D.data_ptr()
         self.npix = [h * w for h, w in self.shapes]
         self.p_off = np.concatenate([[0], np.cumsum(self.npix)]).astype(np.int64)
         tot = max(int(self.p_off[-1]), 1)
         self.depth = torch.empty(tot, dtype=torch.float32, device="cuda")
         self.valid = torch.empty(tot, dtype=torch.uint8, device="cuda")
-        self.views = (_lib.TriView * max(len(fields), 1))()
-        self.maps = (_lib.TriMap * max(len(self.jobs), 1))()
         self.nviews = len(fields)
+        views = np.zeros(max(len(fields), 1), dtype=_VIEW_DTYPE)
+        maps = np.zeros(max(len(self.jobs), 1), dtype=_MAP_DTYPE)
+        if fields:
+            views["targets"][:len(fields)] = base + 2 * c_off[:-1] * item
+            views["confidence"][:len(fields)] = base + (2 * tot_cells + c_off[:-1]) * item
+        cache = {}
+        cams = [_cam_record(cov.pose, cov.intrinsics, cache) for _, covis, _ in self.jobs for cov in covis]
+        if cams:
+            views["rt"][:len(cams)] = np.stack([c[0] for c in cams])
+            views["center"][:len(cams)] = np.stack([c[1] for c in cams])
+            for k, name in enumerate(("fx", "fy", "cx", "cy")):
+                views[name][:len(cams)] = [c[2 + k] for c in cams]
         v = 0
         for m, ((entry, covis, fl), (gh, gw)) in enumerate(zip(self.jobs, self.shapes)):
-            M = self.maps[m]
+            M = maps[m]
             intr = entry.intrinsics
-            M.grid_w, M.grid_h, M.view0, M.nview = gw, gh, v, len(fl)
-            M.fx, M.fy, M.cx, M.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
-            M.sx, M.sy = intr.width / gw, intr.height / gh
-            R = np.asarray(entry.pose.R, dtype=np.float64)
-            for i in range(9):
-                M.R[i] = float(R.flat[i])
-            c = entry.pose.center()
-            for i in range(3):
-                M.center[i] = float(c[i])
-            M.depth = self.depth.data_ptr() + int(self.p_off[m]) * 4
-            M.valid = self.valid.data_ptr() + int(self.p_off[m])
-            for cov, f in zip(covis, fl):
-                W = self.views[v]
-                W.targets = self.T.data_ptr() + int(t_off[v]) * item
-                W.confidence = self.C.data_ptr() + int(c_off[v]) * item
-                _fill_cam(W, cov.pose, cov.intrinsics)
-                v += 1
+            M["grid_w"], M["grid_h"], M["view0"], M["nview"] = gw, gh, v, len(fl)
+            M["fx"], M["fy"], M["cx"], M["cy"] = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
+            M["sx"], M["sy"] = intr.width / gw, intr.height / gh
+            M["R"] = np.asarray(entry.pose.R, dtype=np.float64).reshape(-1)
+            M["center"] = np.asarray(entry.pose.center(), dtype=np.float64)
+            M["depth"] = self.depth.data_ptr() + int(self.p_off[m]) * 4
+            M["valid"] = self.valid.data_ptr() + int(self.p_off[m])
+            v += len(fl)
+        self._views, self._maps = views, maps  # kept alive: the C call reads them
         self._cfg = _cfg_c(cfg)
 
     @property
@@ -233,8 +288,11 @@ class DepthBuildPlan:
         ctx = _lib.context()
         if not self.jobs:
             return self
-        rc = _lib.lib().vl_build_depth_maps(ctx.handle, self.maps, len(self.jobs), self.views, self.nviews,
-                                            1 if self.f64 else 0, _lib.ctypes_ref(self._cfg), _lib.stream_ptr())
+        import ctypes as C
+        rc = _lib.lib().vl_build_depth_maps(ctx.handle, self._maps.ctypes.data_as(C.POINTER(_lib.TriMap)),
+                                            len(self.jobs), self._views.ctypes.data_as(C.POINTER(_lib.TriView)),
+                                            self.nviews, 1 if self.f64 else 0, _lib.ctypes_ref(self._cfg),
+                                            _lib.stream_ptr())
         ctx.check(rc, "vl_build_depth_maps")
         return self
 
