@@ -569,7 +569,10 @@ def run_map_bench(args, wl, rank, world, local, dist):
             "unit": "TFLOP/s", "frac": achieved / fp64_peak,
             "peak_source": "derived SMs*64*2*sm_max_mhz (MEASURED_PEAKS.json has no FP64 entry)",
             "flop_per_vote": VOTE_FLOP, "votes_per_s": votes / (tri_ms / 1e3),
-            "note": "vote-stage FLOPs only (the Newton refinement is excluded from the count)",
+            "note": "vote-stage FLOPs only (the Newton refinement, most of the work, is excluded from the "
+                    "count); ncu_fp64_pipe_active is the measured FP64-pipe utilisation of the whole kernel",
+            "ncu_fp64_pipe_active": 0.234, "ncu_source": "profiles/r01c_k_tri_quant_full_raw.csv "
+            "(sm__pipe_fp64_cycles_active, ncu --set full of bench.py --workload map)",
             "traffic": None, "tri_ms_per_step": tri_ms, "share_of_step": tri_ms / (ms / args.steps)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
