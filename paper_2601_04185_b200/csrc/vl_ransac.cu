@@ -682,8 +682,9 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     const size_t with_costs = kStageBytes + (size_t)wk.HCAP * sizeof(float);
     const int costs_smem = with_costs <= (size_t)max_smem ? 1 : 0;
     const size_t smem = costs_smem ? with_costs : kStageBytes;
-    launch_clustered(k_scan, nactive, kScanThreads, smem, pick_cluster(nactive, VL_LO_MINB * num_sms), st, wk,
-                     p, costs_smem);
+    int cs = pick_cluster(nactive, VL_LO_MINB * num_sms);
+    if (const char* e = getenv("VISLOC_SCAN_CS")) cs = atoi(e);  // tuning knob
+    launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, wk, p, costs_smem);
     H(kStageScan, false);
     H(kStageActive, true);
     k_active<<<1, 1024, 0, st>>>(wk, nactive);
