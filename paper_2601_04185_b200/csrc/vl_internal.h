@@ -9,7 +9,10 @@ namespace vl {
 
 // Scoring tile geometry (vl_score.cu).
 constexpr int kScoreThreads = 128;
-constexpr int kScoreHypPerThread = 6;  // coarse items: 3 f32x2 pairs (tools/score_bench.cu sweep)
+#ifndef VL_SCORE_HT
+#define VL_SCORE_HT 6
+#endif
+constexpr int kScoreHypPerThread = VL_SCORE_HT;  // coarse items: hypotheses per thread (sweeps: tools/)
 constexpr int kScoreTileHyps = kScoreThreads * kScoreHypPerThread;  // 768
 constexpr int kScoreItemSplits = 4;    // coarse items: 4 splits = 512 correspondences
 // canonical cost = sum over split groups (in order) of the group sum

@@ -142,7 +142,7 @@ def _to_device(a: np.ndarray):
 
 
 # ----------------------------------------------------------------- device entry
-def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, out=None, stages=None):
+def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, out=None, stages=None, ctx=None):
     """Batched estimator on device-resident inputs (the HBM-resident hot path).
 
     ``px`` (N,2), ``X`` (N,3), ``w`` (N,) are fp64 CUDA tensors holding Q
@@ -152,7 +152,8 @@ def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, o
     CUDA tensors (q, t, flags, count, score, iterations, converged, stats).
     ``stages``: optional ``(stage_end, events)`` — the inputs of queries
     ``[stage_end[k-1], stage_end[k])`` are only valid once ``events[k]``
-    (``torch.cuda.Event``) completes (``vl_ransac_pnp_staged``).
+    (``torch.cuda.Event``) completes (``vl_ransac_pnp_staged``).  ``ctx``: an
+    explicit ``_lib.Context`` (default: the device's shared one).
     """
     import torch
     offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
@@ -167,7 +168,8 @@ def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, o
     for a, shape in ((px, (N, 2)), (X, (N, 3)), (w, (N,))):
         if not (a.is_cuda and a.dtype == torch.float64 and a.is_contiguous() and tuple(a.shape) == shape):
             raise ValueError(f"expected contiguous fp64 CUDA tensor of shape {shape}")
-    ctx = _lib.context(dev.index)
+    if ctx is None:  # an explicit context (own workspace) lets several runs proceed concurrently
+        ctx = _lib.context(dev.index)
     if out is None:
         out = {
             "q": torch.empty((Q, 4), dtype=torch.float64, device=dev),
