@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(1024) k_active(Work wk, int nactive) {
   }
 }
 
-int launch_score(const Work& wk, float tau2, int num_sms, int fine, cudaStream_t st);  // vl_score.cu
+int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st);  // vl_score.cu
 
 // Cluster size for a per-query kernel: spread few queries over up to 8 SMs
 // each (single-query latency), keep one CTA per query when the batch alone
@@ -665,7 +665,7 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     k_compact<<<nactive, 1024, 0, st>>>(wk, fine);
     H(kStageCompact, false);
     H(kStageScore, true);
-    launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, st);
+    launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, nactive, st);
     H(kStageScore, false);
     n += 4;
   }

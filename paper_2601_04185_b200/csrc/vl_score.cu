@@ -23,6 +23,8 @@
 // its own partial slot; k_scan adds the splits in order, so costs do not
 // depend on the tile shape, the item size or the launch geometry.
 // Variant sweep and ncu evidence: tools/score_bench.cu, profiles/.
+#include <algorithm>
+#include <cstdlib>
 #include "vl_score.cuh"
 
 namespace vl {
@@ -38,14 +40,29 @@ constexpr int kCoarseMinBlocks = VL_SCORE_MINB;
 // fine: 256-hypothesis tiles x 128 correspondences (single queries / small batches)
 constexpr int kFineMinBlocks = 6;
 
-int launch_score(const Work& wk, float tau2, int num_sms, int fine, cudaStream_t st) {
+// grid: persistent (SMs x resident CTAs, dynamic cursor) by default; the
+// VISLOC_SCORE_GRID=items knob launches an item-count upper bound of CTAs
+// instead (one item each) so that other streams' kernels can interleave.
+static int score_grid(const Work& wk, int persistent, int fine, int nactive) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("VISLOC_SCORE_GRID");
+    mode = (e && e[0] == 'i') ? 1 : 0;
+  }
+  if (!mode) return persistent;
+  const int tile = fine ? kScoreTileHypsFine : kScoreTileHyps, spi = fine ? 1 : kScoreItemSplits;
+  const int64_t ub = (int64_t)nactive * ((wk.HCAP + tile - 1) / tile) * ((wk.NSPLIT + spi - 1) / spi);
+  return (int)std::min<int64_t>(ub, 1 << 30);
+}
+
+int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st) {
   if (fine) {
     auto kern = k_score2_t<kScoreThreads, kScoreHypPerThreadFine, 1, kScoreChunk, kFineMinBlocks, 2>;
     static int occ = 0;
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kScoreThreads, 0) != cudaSuccess ||
                      occ < 1))
       occ = kFineMinBlocks;
-    kern<<<num_sms * occ, kScoreThreads, 0, st>>>(wk, tau2);
+    kern<<<score_grid(wk, num_sms * occ, 1, nactive), kScoreThreads, 0, st>>>(wk, tau2);
   } else {
     auto kern = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks,
                            VL_SCORE_UNR>;
@@ -53,7 +70,7 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, cudaStream_t
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kScoreThreads, 0) != cudaSuccess ||
                      occ < 1))
       occ = kCoarseMinBlocks;
-    kern<<<num_sms * occ, kScoreThreads, 0, st>>>(wk, tau2);
+    kern<<<score_grid(wk, num_sms * occ, 0, nactive), kScoreThreads, 0, st>>>(wk, tau2);
   }
   return 1;
 }
