@@ -126,13 +126,16 @@ __device__ void sample_batch(const GenState& g, uint64_t& pos, int64_t n, int bn
   }
 }
 
-__global__ void __launch_bounds__(256) k_sample(Work wk, RansacParams p) {
+// NT threads per query: 256 for big batches, 1024 when few queries are active
+// (single-query latency: one speculative draw per thread)
+template <int NT>
+__global__ void __launch_bounds__(NT) k_sample(Work wk, RansacParams p) {
   const int q = wk.active_list[blockIdx.x];
   QState& S = wk.qs[q];
   const int64_t rem = p.max_iterations - S.iters;
   const int bn = (int)(rem < p.batch_size ? rem : p.batch_size);
   uint64_t pos = S.rng_pos;
-  sample_batch<256>(S.gen, pos, S.n, bn, wk.samples + (int64_t)q * wk.B * 3);
+  sample_batch<NT>(S.gen, pos, S.n, bn, wk.samples + (int64_t)q * wk.B * 3);
   if (threadIdx.x == 0) {
     S.rng_pos = pos;
     S.batch_n = bn;
@@ -653,7 +656,8 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   const int fine = round_is_fine(wk, nactive, num_sms) ? 1 : 0;
   if (phase != 2) {
     H(kStageSample, true);
-    k_sample<<<nactive, 256, 0, st>>>(wk, p);
+    if (nactive * 4 <= num_sms) k_sample<1024><<<nactive, 1024, 0, st>>>(wk, p);
+    else k_sample<256><<<nactive, 256, 0, st>>>(wk, p);
     H(kStageSample, false);
     H(kStageP3P, true);
     dim3 gr(nactive, (wk.B + kP3PRootThreads - 1) / kP3PRootThreads);
