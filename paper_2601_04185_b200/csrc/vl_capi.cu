@@ -38,6 +38,7 @@ struct vl_ctx {
   double stage_ms[kNumStages] = {0};
   int64_t stage_launches[kNumStages] = {0};
   cudaStream_t prof_stream = nullptr;
+  cudaEvent_t round_ev[2] = {nullptr, nullptr};  // lookahead round loop
   // stepwise driver state (vl_ransac_begin / step_score / step_finish / end)
   struct {
     Work wk;
@@ -198,6 +199,8 @@ int vl_destroy(vl_ctx* c) {
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->round_ev)
+    if (e) cudaEventDestroy(e);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   delete c;
   return VL_OK;
@@ -417,6 +420,35 @@ static int read_active(vl_ctx* c, const Work& wk, cudaStream_t st, int* nactive)
 
 extern "C" {
 
+// Round loop with a one-round lookahead: round r+1 is queued (with the last
+// count the host has read, a superset of the active queries; kernels skip list
+// positions >= the device-side count) before the host waits for round r's
+// count, so the GPU never idles while the host reads it and launches.  The
+// round queued after the last one is a no-op.
+static int round_loop_lookahead(vl_ctx* c, const Work& wk, const Inputs& in, const RansacParams& p, int Qn,
+                                int64_t max_rounds, cudaStream_t st) {
+  if (!c->round_ev[0]) {
+    for (auto& e : c->round_ev) VL_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  volatile int* h_count = (volatile int*)((char*)c->h_pinned + c->h_pinned_cap - 16);
+  int nlaunch = Qn;
+  int64_t r = 0;
+  c->launches += launch_round(wk, in, p, nlaunch, c->num_sms, st, nullptr, nullptr, 0);
+  VL_CUDA(c, cudaEventRecord(c->round_ev[0], st));
+  while (true) {
+    c->launches += launch_round(wk, in, p, nlaunch, c->num_sms, st, nullptr, nullptr, 0);
+    int rc;
+    if ((rc = check_launch(c))) return rc;
+    VL_CUDA(c, cudaEventRecord(c->round_ev[(r + 1) & 1], st));
+    VL_CUDA(c, cudaEventSynchronize(c->round_ev[r & 1]));  // round r (not the queued one) is done
+    const int n = *h_count;  // k_active's mirror: the count after round r (or a later round)
+    if (n == 0) break;
+    nlaunch = n;
+    if (++r > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
+  }
+  return VL_OK;
+}
+
 int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, void* stream) {
   if (!c || !a || !o) return fail(c, VL_ERR_INVALID, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
@@ -436,11 +468,15 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     if ((rc = setup_chunk(c, a, q0, Qn, in, wk, st))) return rc;
     int nactive = Qn;
     int guard = 0;
-    while (nactive > 0) {
-      c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c, 0);
-      if ((rc = check_launch(c))) return rc;
-      if ((rc = read_active(c, wk, st, &nactive))) return rc;
-      if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
+    if (c->prof) {  // per-stage event brackets: one round in flight at a time
+      while (nactive > 0) {
+        c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c, 0);
+        if ((rc = check_launch(c))) return rc;
+        if ((rc = read_active(c, wk, st, &nactive))) return rc;
+        if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
+      }
+    } else if ((rc = round_loop_lookahead(c, wk, in, p, Qn, max_rounds, st))) {
+      return rc;
     }
     prof_hook(c, kStageFinal, true);
     c->launches += launch_final(wk, in, out, p, Qn, (int)q0, st);

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
     if (threadIdx.x == 0) {
       wk.active_list[list_pos + blockIdx.x] = q;
       if (list_pos + blockIdx.x == 0) wk.item_count[0] = wk.item_count[1] = 0;
+      if (blockIdx.x == 0) *wk.active_count = list_pos + (int)gridDim.x;  // admitted queries are active
     }
     __syncthreads();
   }
@@ -128,8 +129,12 @@ __device__ void sample_batch(const GenState& g, uint64_t& pos, int64_t n, int bn
 
 // NT threads per query: 256 for big batches, 1024 when few queries are active
 // (single-query latency: one speculative draw per thread)
+// Per-query kernels return for list positions >= *active_count: the host may
+// queue a round with a stale (larger) grid before it has read the previous
+// round's count (one-round lookahead, vl_ransac_pnp).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_sample(Work wk, RansacParams p) {
+  if ((int)blockIdx.x >= *wk.active_count) return;
   const int q = wk.active_list[blockIdx.x];
   QState& S = wk.qs[q];
   const int64_t rem = p.max_iterations - S.iters;
@@ -194,6 +199,7 @@ struct CandRec {
 #define VL_P3P_POLISH_MINB 8  // measured: 128-register cap, 8 CTAs
 #endif
 __global__ void __launch_bounds__(kP3PRootThreads, VL_P3P_ROOT_MINB) k_p3p_roots(Work wk, Inputs in) {
+  if ((int)blockIdx.x >= *wk.active_count) return;
   const int q = wk.active_list[blockIdx.x];
   const QState& S = wk.qs[q];
   const int s = blockIdx.y * kP3PRootThreads + threadIdx.x;
@@ -223,6 +229,7 @@ __global__ void __launch_bounds__(kP3PRootThreads, VL_P3P_ROOT_MINB) k_p3p_roots
 __global__ void __launch_bounds__(kP3PThreads, VL_P3P_POLISH_MINB) k_p3p_polish(Work wk) {
   __shared__ CandRec cand[kP3PThreads / 32][32 * kMaxCand];
   __shared__ double res[kP3PThreads / 32][32][13];
+  if ((int)blockIdx.x >= *wk.active_count) return;
   const int q = wk.active_list[blockIdx.x];
   const QState& S = wk.qs[q];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -346,6 +353,7 @@ int launch_p3p_batch(const double* f, const double* P, int B, double* slots, int
 __global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
   __shared__ int warp_tot[32];
   __shared__ int s_item0;
+  if ((int)blockIdx.x >= *wk.active_count) return;
   const int q = wk.active_list[blockIdx.x];
   QState& S = wk.qs[q];
   const int bn = S.batch_n;
@@ -442,6 +450,7 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   __shared__ uint64_t stage_bar[kStageN];
   __shared__ LMShared<kScanThreads> sm;
   __shared__ Pose s_start;
+  if ((int)(blockIdx.x / cl_size()) >= *wk.active_count) return;  // whole cluster
   const int q = wk.active_list[blockIdx.x / cl_size()];
   QState& S = wk.qs[q];
   const int nh = S.nh;
@@ -524,8 +533,11 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   }
 }
 
-__global__ void __launch_bounds__(1024) k_active(Work wk, int nactive) {
+__global__ void __launch_bounds__(1024) k_active(Work wk, int nlaunch) {
   __shared__ int warp_tot[32];
+  // the current count (a lookahead round is launched with a stale one)
+  const int nactive = min(nlaunch, *wk.active_count);
+  __syncthreads();
   int running = 0;
   for (int base = 0; base < nactive; base += 1024) {
     const int i = base + threadIdx.x;
