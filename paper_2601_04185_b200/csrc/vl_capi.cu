@@ -539,6 +539,10 @@ int vl_ransac_pnp_staged(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out
       ++admitted;
     }
     if (nactive == 0) break;
+    if (admitted == nstage && !c->prof) {  // everything admitted: finish with the lookahead loop
+      if ((rc = round_loop_lookahead(c, wk, in, p, nactive, max_rounds, st))) return rc;
+      break;
+    }
     c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c, 0);
     if ((rc = check_launch(c))) return rc;
     if ((rc = read_active(c, wk, st, &nactive))) return rc;
