@@ -16,7 +16,7 @@ import numpy as np
 import os
 
 # VISLOC_B200_LIB: alternative in-tree build of the same library (A/B kernel experiments)
-_LIB_PATH = Path(os.environ.get("VISLOC_B200_LIB", Path(__file__).resolve().parent / "_lib" / "libvisloc_b200.so"))
+_LIB_PATH = Path(os.environ.get("VISLOC_B200_LIB") or Path(__file__).resolve().parent / "_lib" / "libvisloc_b200.so")
 
 VL_OK = 0
 VL_ERR_INVALID = 1

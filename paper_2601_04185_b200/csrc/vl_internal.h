@@ -7,6 +7,8 @@
 
 namespace vl {
 
+constexpr int kMaxDevices = 64;  // per-device launch state (function attributes)
+
 // Scoring tile geometry (vl_score.cu).
 constexpr int kScoreThreads = 128;
 #ifndef VL_SCORE_HT

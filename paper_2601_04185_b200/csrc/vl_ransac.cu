@@ -687,10 +687,12 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   }
   if (phase != 1) {
     H(kStageScan, true);
-    static int max_smem = 0;
+    // function attributes are per device: set once for each device used
+    static int max_smem_dev[kMaxDevices] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& max_smem = max_smem_dev[dev < kMaxDevices ? dev : 0];
     if (max_smem == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
       max_smem -= (int)(sizeof(LMShared<kScanThreads>) + 1024);  // static smem of the kernel
       cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
@@ -805,8 +807,11 @@ __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, In
 
 int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
                  int q_base, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {  // the staging ring needs more than the 48 KB default dynamic smem
+  static bool attr_dev[kMaxDevices] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  bool& attr = attr_dev[dev < kMaxDevices ? dev : 0];
+  if (!attr) {  // the staging ring needs more than the 48 KB default dynamic smem (per device)
     cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes);
     attr = true;
   }
