@@ -310,8 +310,12 @@ template <bool GRAD>
 __device__ __forceinline__ void lm_point(const double* R, const double* t, const Intr& in, int kind, double s2,
                                          const double* P, double u_obs, double v_obs, double w, double* acc,
                                          double& behind) {
-  double x, y, z;
-  cam_point(R, t, P, x, y, z);
+  // camera point with FMAs (3 per row instead of 3 mul + 3 add): the LM
+  // cost only steers the schedule; classification keeps msac_pass's
+  // reference-order arithmetic
+  const double x = fma(P[2], R[2], fma(P[1], R[1], fma(P[0], R[0], t[0])));
+  const double y = fma(P[2], R[5], fma(P[1], R[4], fma(P[0], R[3], t[1])));
+  const double z = fma(P[2], R[8], fma(P[1], R[7], fma(P[0], R[6], t[2])));
   if (!(z > 0)) {
     behind = 1.0;
     if (kind == kTruncated) acc[0] += dmul(w, s2);
