@@ -348,3 +348,24 @@ def test_hypothesis_split_argmin_variant(vl, intr):
             e = r.end()[0]
             assert np.array_equal(e.pose.q, one.pose.q) and np.array_equal(e.pose.t, one.pose.t)
             assert np.array_equal(e.inlier_flags, one.inlier_flags)
+
+
+@pytest.mark.parametrize("n,kw", [
+    (60_000, dict(max_scoring=50_000, max_iterations=2000, miss_probability=1e-300)),  # stride 2, 391 splits
+    (3_000, dict(batch_size=1, max_iterations=40, miss_probability=1e-300)),          # one sample per round
+    (2_500, dict(batch_size=777, max_iterations=3000, miss_probability=1e-300)),      # odd batch
+    (4_000, dict(reproj_threshold=2.5, cauchy_scale=1.0, lm_max_iters=7, max_iterations=2000,
+                 miss_probability=1e-300)),
+    (3, dict(max_iterations=50, batch_size=50)),                                      # minimal input
+    (1_999, dict(max_scoring=997, max_iterations=3000)),                              # odd subset size
+])
+def test_config_edge_cases_vs_oracle(vl, intr, n, kw):
+    """Unusual RansacConfig values and sizes against the CPU oracle."""
+    px, X, w, _ = matches_a(n, 0.5 if n > 3 else 0.0, 1.0 if n > 3 else 0.0, seed=n + 5)
+    e = vl.ransac_pnp((px, X, w), intr, vl.RansacConfig(seed=4, **kw))
+    o = ransac(px, X, w, INTR_T, Config(seed=4, **kw))
+    assert e.iterations == o.iterations and e.converged == o.converged
+    if o.converged:
+        assert og.rot_err_deg(e.pose.q, o.q) < 0.01
+        assert np.linalg.norm(e.pose.t - o.t) <= 1e-4 * max(np.linalg.norm(o.t), 1e-9)
+        assert (e.inlier_flags != o.inlier_flags).sum() == 0
