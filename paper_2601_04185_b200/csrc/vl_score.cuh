@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   constexpr int WHYP = 32 * HT;  // hypotheses per warp slice
   static_assert(SPI == 1 || SPI == kGroupSplits, "coarse items are exactly one split group");
   __shared__ float4 rec[3 * SPI * SCH / 2];  // record pairs: (X2, Y2), (Z2, A2), (B2, W2)
-  __shared__ float red[SPI][SPI > 1 ? NT * HT : 1];
+  __shared__ float red[SPI][SPI > 1 ? NT * HT : 1];  // split sums of coarse items
   __shared__ int s_it, s_last;
   const int nitems = wk.item_count[0];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -94,20 +94,16 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     __syncthreads();
     for (int k = threadIdx.x; k < 3 * pn; k += NT) rec[k] = src[k];
     float P[HT][12];
-    int hid[HT];
+    // hypotheses hid0 .. hid0 + HT - 1 of this thread (thread-contiguous)
+    const int hid0 = tile0 + hs * WHYP + lane * HT;
     const float* Pq = wk.P32 + (int64_t)item.q * 12 * wk.HCAP;
 #pragma unroll
-    for (int j = 0; j < HT; ++j) hid[j] = tile0 + hs * WHYP + lane * HT + j;
-#pragma unroll
     for (int j = 0; j < HT; ++j) {
-      const int h = hid[j] < nh ? hid[j] : 0;
+      const int h = hid0 + j < nh ? hid0 + j : 0;
 #pragma unroll
       for (int c = 0; c < 12; ++c) P[j][c] = Pq[(int64_t)c * wk.HCAP + h];
     }
     __syncthreads();
-    float gsum[HT];
-#pragma unroll
-    for (int j = 0; j < HT; ++j) gsum[j] = 0.f;
     for (int s = grp; s < ns && grp < G; s += G) {
       float2 acc[HT];
 #pragma unroll
@@ -122,40 +118,29 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
 #pragma unroll
         for (int j = 0; j < HT; ++j) VL_SCORE_EVAL2(P[j], acc[j]);
       }
-      float sv[HT];  // the split's sum: even records + odd records
-#pragma unroll
-      for (int j = 0; j < HT; ++j) sv[j] = acc[j].x + acc[j].y;
+      // the split's sum: even records + odd records
       if (SPI == 1) {
         float* out = outq + (int64_t)(item.split + s) * wk.HCAP;
 #pragma unroll
         for (int j = 0; j < HT; ++j)
-          if (hid[j] < nh) out[hid[j]] = sv[j];
-      } else if (G == 1) {
-#pragma unroll
-        for (int j = 0; j < HT; ++j) gsum[j] = (s == 0) ? sv[j] : gsum[j] + sv[j];
+          if (hid0 + j < nh) out[hid0 + j] = acc[j].x + acc[j].y;
       } else {
-        // split s of a partial tile computed by warp group grp: park it
+        // park the split sum in smem (no per-thread group accumulator stays
+        // live across the record loop); the group sum is formed below
 #pragma unroll
-        for (int j = 0; j < HT; ++j) red[s][hs * WHYP + lane * HT + j] = sv[j];
+        for (int j = 0; j < HT; ++j) red[s][hs * WHYP + lane * HT + j] = acc[j].x + acc[j].y;
       }
     }
     if (SPI > 1) {
       float* out = outq + (int64_t)(item.split / kGroupSplits) * wk.HCAP;
-      if (G > 1) {
-        __syncthreads();
-        if (grp == 0) {
-#pragma unroll
-          for (int j = 0; j < HT; ++j) {
-            float sx = red[0][hs * WHYP + lane * HT + j];
-            for (int s = 1; s < ns; ++s) sx += red[s][hs * WHYP + lane * HT + j];
-            gsum[j] = sx;
-          }
-        }
-      }
+      if (G > 1) __syncthreads();  // splits of a partial tile came from other warp groups
       if (grp == 0) {
 #pragma unroll
-        for (int j = 0; j < HT; ++j)
-          if (hid[j] < nh) out[hid[j]] = gsum[j];
+        for (int j = 0; j < HT; ++j) {
+          float sx = red[0][hs * WHYP + lane * HT + j];  // ((p0 + p1) + p2) + p3, in split order
+          for (int s = 1; s < ns; ++s) sx += red[s][hs * WHYP + lane * HT + j];
+          if (hid0 + j < nh) out[hid0 + j] = sx;
+        }
       }
     }
     // ---- tile completion ticket (threadfence reduction pattern)
