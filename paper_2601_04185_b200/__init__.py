@@ -9,6 +9,9 @@ mirror the reference so ``visloc`` call sites keep working:
 * ``p3p``      — p3p_solve, p3p_solve_batch, sample_minimal_sets
 * ``refine``   — refine_pose, TruncatedLoss, CauchyLoss
 * ``geometry`` — CameraIntrinsics, Pose, pose_error
+* ``localizer`` / ``matchio`` / ``retrieval`` — lift, localize, IMLC fields, top-K retrieval
+* ``mapstore`` / ``depthbuild`` — depth codecs, dense depth triangulation (mapping side)
+* ``dist`` — query sharding and the hypothesis-split modes over torch.distributed
 """
 
 from .geometry import CameraIntrinsics, Pose, pose_error  # noqa: F401
@@ -21,6 +24,8 @@ from .posest import (  # noqa: F401
     ransac_pnp,
     ransac_pnp_batch,
     ransac_pnp_device,
+    ransac_pnp_host,
+    ransac_pnp_stream,
     required_iterations,
 )
 

@@ -25,8 +25,7 @@ from . import _lib
 from .geometry import CameraIntrinsics, Pose
 from .matchio import CorrespondenceField, FieldBlob, filter_matches_arrays  # noqa: F401
 from .retrieval import DescriptorIndex
-from .posest import (Match2D3D, PoseEstimate, RansacConfig, _estimates_from, _intr_c,
-                     ransac_pnp_device)
+from .posest import Match2D3D, PoseEstimate, RansacConfig, _estimates_from, ransac_pnp_device
 
 __all__ = [
     "CONFIDENCE_THRESHOLD", "CorrespondenceField", "DepthMap", "DescriptorIndex", "FieldPair",

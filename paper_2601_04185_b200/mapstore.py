@@ -25,7 +25,6 @@ built with the input objects' classes.
 
 from __future__ import annotations
 
-import ctypes as C
 import functools
 import io
 import math
