@@ -1,0 +1,95 @@
+"""Large randomized parity sweep: GPU ransac_pnp vs the CPU oracle (tools only).
+
+The oracle runs on every host core (one process per problem); each problem
+draws its size, inlier ratio, noise, outlier weights, ground-truth pose,
+seed and RansacConfig (iterations, eta, batch size, tau, subset size) from
+one generator.  Prints the summary counts that DESIGN.md quotes.  GPU only:
+    python tools/parity_sweep.py [N] [seed]
+"""
+import json
+import multiprocessing as mp
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+
+
+def draw(k, seed0):
+    rng = np.random.default_rng([seed0, k])
+    n = int(rng.choice([20, 200, 1000, 3000, 8000, 20000, 60000]))
+    cfg = dict(seed=int(rng.integers(0, 2**40)),
+               max_iterations=int(rng.choice([500, 2000, 5000, 20000])),
+               miss_probability=float(rng.choice([1e-4, 1e-2, 1e-300])),
+               reproj_threshold=float(rng.choice([4.0, 8.0, 12.0, 20.0])),
+               max_scoring=int(rng.choice([10_000, 10_000, 2_500])))
+    cfg["batch_size"] = int(min(cfg["max_iterations"], rng.choice([1000, 1000, 250, 999])))
+    return dict(n=n, outlier=float(rng.choice([0.0, 0.3, 0.5, 0.7, 0.85])),
+                sigma=float(rng.choice([0.0, 0.5, 1.0, 2.0])), data_seed=int(rng.integers(0, 2**31)),
+                pose_seed=int(rng.integers(0, 2**31)), cfg=cfg)
+
+
+def problem(p):
+    from synth_inputs import matches_a, random_pose
+    _, R, t = random_pose(np.random.default_rng(p["pose_seed"]), 0.3, 0.3)
+    px, X, w, _ = matches_a(p["n"], p["outlier"], p["sigma"], seed=p["data_seed"], R=R, t=t)
+    return px, X, w
+
+
+def oracle_worker(p):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle.posest import Config, ransac
+    px, X, w = problem(p)
+    o = ransac(px, X, w, (700.0, 700.0, 350.0, 350.0), Config(**p["cfg"]))
+    return dict(q=o.q.tolist(), t=o.t.tolist(), flags=np.packbits(o.inlier_flags).tobytes().hex(),
+                iterations=o.iterations, converged=bool(o.converged))
+
+
+def main():
+    N = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    seed0 = int(sys.argv[2]) if len(sys.argv) > 2 else 7
+    probs = [draw(k, seed0) for k in range(N)]
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(len(os.sched_getaffinity(0))) as pool:
+        async_res = pool.map_async(oracle_worker, probs, chunksize=1)
+        import paper_2601_04185_b200 as vl
+        from oracle import geometry as og
+        intr = vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
+        gpu = []
+        for p in probs:
+            px, X, w = problem(p)
+            gpu.append(vl.ransac_pnp((px, X, w), intr, vl.RansacConfig(**p["cfg"])))
+        ref = async_res.get()
+    stats = dict(problems=N, same_iterations=0, same_converged=0, pose_within_tol=0, masks_identical=0,
+                 max_rot_deg=0.0, max_rel_t=0.0, flag_mismatch_points=0, near_tau_only=0)
+    from oracle.posest import errors_sq
+    for p, e, o in zip(probs, gpu, ref):
+        stats["same_iterations"] += int(e.iterations == o["iterations"])
+        stats["same_converged"] += int(e.converged == o["converged"])
+        if not o["converged"]:
+            stats["pose_within_tol"] += 1
+            stats["masks_identical"] += 1
+            continue
+        oq, ot = np.array(o["q"]), np.array(o["t"])
+        rot = og.rot_err_deg(e.pose.q, oq)
+        rel = float(np.linalg.norm(e.pose.t - ot) / max(np.linalg.norm(ot), 1e-12))
+        stats["max_rot_deg"] = max(stats["max_rot_deg"], rot)
+        stats["max_rel_t"] = max(stats["max_rel_t"], rel)
+        stats["pose_within_tol"] += int(rot < 0.01 and rel < 1e-4)
+        of = np.unpackbits(np.frombuffer(bytes.fromhex(o["flags"]), np.uint8))[: p["n"]].astype(bool)
+        diff = np.nonzero(of != e.inlier_flags)[0]
+        stats["masks_identical"] += int(diff.size == 0)
+        stats["flag_mismatch_points"] += int(diff.size)
+        if diff.size:  # the parity bar exempts points within 1e-6 px of tau
+            px, X, w = problem(p)
+            e2 = errors_sq(og.q2R(oq), ot, X[diff], px[diff], (700.0, 700.0, 350.0, 350.0))
+            tau = p["cfg"]["reproj_threshold"]
+            stats["near_tau_only"] += int(np.all(np.abs(np.sqrt(e2) - tau) < 1e-6))
+    print(json.dumps(stats))
+
+
+if __name__ == "__main__":
+    main()
