@@ -622,9 +622,16 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the multi-rank path on a one-GPU box (never a
+    # measurement): VISLOC_BENCH_DEVICE=0 VISLOC_BENCH_BACKEND=gloo
+    local = int(os.environ.get("VISLOC_BENCH_DEVICE", local))
+    backend = os.environ.get("VISLOC_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2601_04185_b200 import _lib
     from paper_2601_04185_b200.geometry import CameraIntrinsics
     from paper_2601_04185_b200.posest import RansacConfig, ransac_pnp_device, ransac_pnp_stream
