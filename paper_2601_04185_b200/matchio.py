@@ -33,7 +33,8 @@ from . import _lib
 
 __all__ = [
     "CorrespondenceField", "FieldArena", "FieldBlob", "FieldFormatError", "FieldMagicError",
-    "FieldTruncatedError", "FieldVersionError", "MAGIC", "VERSION", "field_bytes", "filter_matches_arrays",
+    "FieldTruncatedError", "FieldVersionError", "FilteredMatch", "MAGIC", "VERSION", "field_bytes", "filter_matches",
+    "filter_matches_arrays",
     "parse_header", "read_field", "read_field_blob", "write_field",
 ]
 
@@ -363,3 +364,19 @@ def filter_matches_arrays(fld, threshold: float):
     px, X, w, _, _, _ = _run_lift([(0, 0, 0, 0, fld)], [], threshold, mode=1)
     Xh = X.cpu().numpy()
     return px.cpu().numpy(), Xh[:, :2].copy(), w.cpu().numpy(), Xh[:, 2].astype(np.int64)
+
+
+@dataclass
+class FilteredMatch:
+    """A confidence-gated match in source/target pixel coordinates (matchio.py:127-132)."""
+
+    source_px: np.ndarray
+    target_px: np.ndarray
+    confidence: float
+
+
+def filter_matches(fld, threshold: float) -> list[FilteredMatch]:
+    """Per-match view of ``filter_matches_arrays`` (matchio.py:221-228): cells with
+    confidence >= threshold and > 0, row-major, gated on the GPU."""
+    src, tgt, conf, _ = filter_matches_arrays(fld, threshold)
+    return [FilteredMatch(src[i], tgt[i], float(conf[i])) for i in range(len(conf))]

@@ -167,3 +167,30 @@ def test_gpu_gate_interp_decode(vl):
     assert np.array_equal(dm.values, rv) and np.array_equal(dm.valid, rvalid)
     with pytest.raises(ValueError):
         vl.filter_matches_arrays(f, 1.5)
+
+
+@pytest.mark.gpu
+def test_gpu_filter_matches_cases(vl):
+    """The reference's filter_matches cases (test_matchio.py:167-232) through the GPU gate."""
+    from paper_2601_04185_b200.matchio import filter_matches
+    f = vl.CorrespondenceField("a", "b", np.array([[[np.nan, np.nan], [5.0, 6.0]]]), np.array([[0.0, 0.3]]))
+    out = filter_matches(f, 0.0)  # confidence 0 is the no-match sentinel even at threshold 0
+    assert len(out) == 1 and np.array_equal(out[0].target_px, [5.0, 6.0])
+    f = vl.CorrespondenceField("a", "b", np.zeros((1, 3, 2)), np.array([[0.04, 0.05, 0.9]]))
+    assert len(filter_matches(f, 0.05)) == 2  # inclusive threshold
+    f = vl.CorrespondenceField("a", "b", np.zeros((2, 2, 2)), np.ones((2, 2)), scale_x=10.0, scale_y=4.0)
+    assert [tuple(m.source_px) for m in filter_matches(f, 0.5)] == [(5.0, 2.0), (15.0, 2.0), (5.0, 6.0), (15.0, 6.0)]
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        conf = rng.random((7, 5))
+        conf[rng.random((7, 5)) < 0.3] = 0
+        f = vl.CorrespondenceField("a", "b", rng.normal(size=(7, 5, 2)), conf)
+        thr = float(rng.random())
+        got = filter_matches(f, thr)
+        assert len(got) == int(np.sum((conf >= thr) & (conf > 0)))
+        _, _, _, cells = vl.filter_matches_arrays(f, thr)
+        assert np.all(np.diff(cells) > 0)  # row-major
+    with pytest.raises(ValueError):
+        filter_matches(f, -0.1)
+    with pytest.raises(ValueError):
+        filter_matches(f, 1.1)
