@@ -329,6 +329,15 @@ def timed_region(ctx, stream, sync_all, step, steps, profile):
 
 
 # ----------------------------------------------------------------------------- GPU arm: lifted
+def serving_batch_ends(Q):
+    """Micro-batch ends of the C5 serving loop (env VISLOC_C5_SIZES="a,b,..." overrides)."""
+    env = os.environ.get("VISLOC_C5_SIZES")
+    if env:
+        return sorted({min(int(c), Q) for c in np.cumsum([int(x) for x in env.split(",")])} | {Q})
+    from paper_2601_04185_b200.localizer import serving_schedule
+    return serving_schedule(Q)
+
+
 def run_lift_bench(args, wl, rank, world, local, dist):
     """C2 / C5: a step = lift (gate + depth decode + unproject) + batched LO-RANSAC
     for every query of the shard, device-resident fields/depth (value) or the
@@ -346,11 +355,10 @@ def run_lift_bench(args, wl, rank, world, local, dist):
     seed0 = LIFT_SEED + 1000 * rank
     vmap, jobs, dcache = lifted_scene(wl["K"], Q, wl["g"], seed=seed0, depth_kind=wl["depth"], fields="f32")
     # the queries' fields arrive as IMLC payloads (matchio.py:9-20), one pinned
-    # arena per micro-batch of queries (posest._stage_schedule sizes); the GPU
+    # arena per micro-batch of queries (localizer.serving_schedule sizes); the GPU
     # lift reads the 12-B records in place
     from paper_2601_04185_b200.localizer import localize_pipelined
-    from paper_2601_04185_b200.posest import _stage_schedule
-    ends = _stage_schedule(Q)
+    ends = serving_batch_ends(Q)
     batches, q0 = [], 0
     bjobs = []
     for q1 in ends:
@@ -411,7 +419,8 @@ def run_lift_bench(args, wl, rank, world, local, dist):
     e2e = None
     if not args.no_e2e:
         big = max(a.host.numel() for _, a in batches)
-        bufs = [torch.empty(big, dtype=torch.uint8, device="cuda") for _ in range(2)]
+        lanes = int(os.environ.get("VISLOC_PIPE_LANES", 2))
+        bufs = [torch.empty(big, dtype=torch.uint8, device="cuda") for _ in range(int(os.environ.get("VISLOC_PIPE_BUFS", lanes + 1)))]
 
         def e2e_step():
             # micro-batched serving loop: batch k+1's IMLC payloads (pinned) go
@@ -420,10 +429,12 @@ def run_lift_bench(args, wl, rank, world, local, dist):
             return localize_pipelined(batches, vmap, cfg, seeds=seeds, depth_cache=dcache, device_cache=dev_cache,
                                       retrieval="gpu", buffers=bufs)
 
-        e2e_step()
+        for _ in range(2):  # warm the pinned result pool the loop cycles through
+            res = e2e_step()
         sync_all()
         e0.record(stream)
         for _ in range(args.steps):
+            res = None  # the caller is done with the previous step's results
             res = e2e_step()
         e1.record(stream)
         sync_all()

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -25,13 +26,15 @@ from . import _lib
 from .geometry import CameraIntrinsics, Pose, pose_error
 from .matchio import CorrespondenceField, FieldBlob, filter_matches_arrays  # noqa: F401
 from .retrieval import DescriptorIndex
-from .posest import Match2D3D, PoseEstimate, RansacConfig, _estimates_from, ransac_pnp_device
+from .posest import (Match2D3D, PoseEstimate, RansacConfig, _estimates_from, _estimates_from_host, _stage_results,
+                     ransac_pnp_device)
 
 __all__ = [
     "CONFIDENCE_THRESHOLD", "CorrespondenceField", "DepthMap", "DescriptorIndex", "EvalResult", "EvalThresholds",
     "FieldPair", "evaluate",
     "QuantizedDepthMap", "QueryJob", "dequantize_depth", "filter_matches_arrays", "interp_depth",
     "interp_depth_many", "LiftPlan", "lift", "lift_arrays", "localize", "localize_batch", "localize_pipelined",
+    "serving_schedule",
 ]
 
 CONFIDENCE_THRESHOLD = 0.05
@@ -182,15 +185,14 @@ class _FieldUpload:
     comes from the arena's arrays, so big batches need no per-field work
     beyond one attribute read."""
 
-    def __init__(self, fields):
-        import torch
+    def __init__(self, fields, finish: bool = True):
         n = len(fields)
+        self.fields = fields
         blob = np.fromiter((type(f) is FieldBlob for f in fields), dtype=bool, count=n)
-        planar_idx = np.nonzero(~blob)[0]
-        planar = [fields[i] for i in planar_idx]
+        self.planar_idx = np.nonzero(~blob)[0]
+        planar = [fields[i] for i in self.planar_idx]
         self.f64 = any(np.asarray(f.confidence).dtype != np.float32 or np.asarray(f.targets).dtype != np.float32
                        for f in planar)
-        dt = np.float64 if self.f64 else np.float32
         self.item = 8 if self.f64 else 4
         self.layout = np.where(blob, _lib.LIFT_IMLC, _lib.LIFT_PLANAR).astype(np.int32)
         self.tptr = np.zeros(n, dtype=np.uint64)
@@ -201,37 +203,52 @@ class _FieldUpload:
         self.sy = np.zeros(n, dtype=np.float64)
         self.keep = []
         self.bytes = 0
+        self.groups = []  # (arena, field positions, record offsets inside the arena)
         blob_idx = np.nonzero(blob)[0]
         if blob_idx.size:
             arenas = {}
             for i in blob_idx:
                 f = fields[i]
-                arenas.setdefault(id(f.arena), (f.arena, [], []))[1].append(i)
-            for arena, pos, _ in arenas.values():
+                arenas.setdefault(id(f.arena), (f.arena, []))[1].append(i)
+            for arena, pos in arenas.values():
                 pos = np.asarray(pos)
                 fidx = np.fromiter((fields[i].index for i in pos), dtype=np.int64, count=pos.size)
-                dev = arena.device()
-                arena.wait()  # a side-stream upload must land before the lift reads it
-                self.keep.append(dev)
-                self.tptr[pos] = np.uint64(dev.data_ptr()) + arena.roff[fidx]
                 self.gw[pos], self.gh[pos] = arena.gw[fidx], arena.gh[fidx]
                 self.sx[pos], self.sy[pos] = arena.sx[fidx], arena.sy[fidx]
                 self.bytes += int(12 * (arena.gw[fidx] * arena.gh[fidx]).sum())
-        self.targets = self.conf = None
+                self.groups.append((arena, pos, arena.roff[fidx]))
         if planar:
+            self.gw[self.planar_idx] = [f.grid_w for f in planar]
+            self.gh[self.planar_idx] = [f.grid_h for f in planar]
+            self.sx[self.planar_idx] = [float(f.scale_x) for f in planar]
+            self.sy[self.planar_idx] = [float(f.scale_y) for f in planar]
+        self.targets = self.conf = None
+        if finish:
+            self.finish()
+
+    def finish(self):
+        """Device side: arena mirrors (waiting on side-stream uploads) and the
+        planar fields' upload.  Host-only construction (``finish=False``) can
+        run on a worker thread; this part runs on the launching thread."""
+        import torch
+        for arena, pos, roff in self.groups:
+            dev = arena.device()
+            arena.wait()  # a side-stream upload must land before the lift reads it
+            self.keep.append(dev)
+            self.tptr[pos] = np.uint64(dev.data_ptr()) + roff
+        if self.planar_idx.size:
+            dt = np.float64 if self.f64 else np.float32
+            planar = [self.fields[i] for i in self.planar_idx]
             tg = [np.ascontiguousarray(f.targets, dtype=dt).reshape(-1) for f in planar]
             cf = [np.ascontiguousarray(f.confidence, dtype=dt).reshape(-1) for f in planar]
             t_off = np.concatenate([[0], np.cumsum([a.size for a in tg])]).astype(np.uint64)
             c_off = np.concatenate([[0], np.cumsum([a.size for a in cf])]).astype(np.uint64)
             self.targets = torch.from_numpy(np.concatenate(tg)).cuda()
             self.conf = torch.from_numpy(np.concatenate(cf)).cuda()
-            self.tptr[planar_idx] = self.targets.data_ptr() + t_off[:-1] * self.item
-            self.cptr[planar_idx] = self.conf.data_ptr() + c_off[:-1] * self.item
-            self.gw[planar_idx] = [f.grid_w for f in planar]
-            self.gh[planar_idx] = [f.grid_h for f in planar]
-            self.sx[planar_idx] = [float(f.scale_x) for f in planar]
-            self.sy[planar_idx] = [float(f.scale_y) for f in planar]
+            self.tptr[self.planar_idx] = self.targets.data_ptr() + t_off[:-1] * self.item
+            self.cptr[self.planar_idx] = self.conf.data_ptr() + c_off[:-1] * self.item
             self.bytes += int(self.targets.numel() + self.conf.numel()) * self.item
+        return self
 
     @property
     def cells(self) -> int:
@@ -252,8 +269,8 @@ def _seg_table(q, e, d, dep, up: _FieldUpload) -> np.ndarray:
     return t
 
 
-def _call_lift(table, nseg, deps, ndep, f64, threshold, mode, px, X, w, ent, cap, offs, flags, fields):
-    ctx = _lib.context()
+def _call_lift(table, nseg, deps, ndep, f64, threshold, mode, px, X, w, ent, cap, offs, flags, fields, ctx=None):
+    ctx = ctx or _lib.context()
     rc = _lib.lib().vl_lift(ctx.handle, table.ctypes.data, nseg, deps, ndep, 1 if f64 else 0, float(threshold),
                             mode, px.data_ptr(), X.data_ptr(), w.data_ptr(), ent.data_ptr(), cap,
                             offs.ctypes.data_as(C.POINTER(C.c_int64)), flags.ctypes.data_as(C.POINTER(C.c_int32)),
@@ -404,42 +421,47 @@ def _retrieve(jobs, index, retrieval):
     return [row[: j.k_loc] for row, j in zip(ids, jobs)]
 
 
-def _plan(jobs, vmap, index, depth_cache, device_cache, retrieval="host"):
-    """Segment arrays + depth records for every query (sorted retrieved ids,
-    localizer.py:220-235), with the reference's per-entry checks in its order
-    (db->query span, query->db span, depth size; localizer.py:147-155)."""
-    if index is None:
-        index = DescriptorIndex.from_entries((e.id, e.descriptor) for e in vmap.entries)
-    by_id = {e.id: e for e in vmap.entries}
-    pq, pe, fields, spans, names, derr = [], [], [], [], [], []
-    recs, rec_of, err_of = [], {}, {}
-    for qi, (job, ranked) in enumerate(zip(jobs, _retrieve(jobs, index, retrieval))):
+def _pair_fields(jobs, ranked_ids, by_id):
+    """Host half of the plan (no device work; safe on a worker thread): every
+    (query, retrieved entry) pair with fields, in the reference's order
+    (sorted retrieved ids, localizer.py:220-235), and the fields' geometry."""
+    pq, peid, fields, spans = [], [], [], []
+    for qi, (job, ranked) in enumerate(zip(jobs, ranked_ids)):
         qI = job.intrinsics
         for eid in sorted(ranked):
             pair = job.fields.get(eid)
             if pair is None:
                 continue
-            entry = by_id[eid]
-            k = rec_of.get(eid)
-            if k is None:
-                if depth_cache is not None and eid in depth_cache:
-                    depth = depth_cache[eid]
-                else:
-                    if getattr(entry, "qdepth", None) is None:
-                        raise ValueError(f"entry {eid} has no stored depth")
-                    depth = entry.qdepth
-                dd = _device_depth(entry, depth, device_cache)
-                k = rec_of[eid] = len(recs)
-                recs.append(dd.record(entry.intrinsics, entry.pose))
-                err_of[eid] = _depth_mismatch(entry, dd)
-            eI = entry.intrinsics
+            eI = by_id[eid].intrinsics
             pq.append(qi)
-            pe.append(k)
+            peid.append(eid)
             fields += (pair.db_to_query, pair.query_to_db)
             spans += ((eI.width, eI.height), (qI.width, qI.height))
-            names.append(eid)
-            derr.append(err_of[eid])
-    up = _FieldUpload(fields)
+    return pq, peid, fields, spans, _FieldUpload(fields, finish=False)
+
+
+def _plan_finish(pairs, by_id, depth_cache, device_cache):
+    """Device half: depth records (decoded depth cached in HBM), arena
+    waits, and the reference's per-entry checks in its order (db->query
+    span, query->db span, depth size; localizer.py:147-155)."""
+    pq, peid, fields, spans, up = pairs
+    recs, rec_of, err_of, pe, derr = [], {}, {}, [], []
+    for eid in peid:
+        k = rec_of.get(eid)
+        if k is None:
+            entry = by_id[eid]
+            if depth_cache is not None and eid in depth_cache:
+                depth = depth_cache[eid]
+            else:
+                if getattr(entry, "qdepth", None) is None:
+                    raise ValueError(f"entry {eid} has no stored depth")
+                depth = entry.qdepth
+            dd = _device_depth(entry, depth, device_cache)
+            k = rec_of[eid] = len(recs)
+            recs.append(dd.record(entry.intrinsics, entry.pose))
+            err_of[eid] = _depth_mismatch(entry, dd)
+        pe.append(k)
+        derr.append(err_of[eid])
     n = len(pq)
     if n:
         WH = np.array(spans, dtype=np.float64).reshape(-1, 2)
@@ -451,13 +473,28 @@ def _plan(jobs, vmap, index, depth_cache, device_cache, retrieval="host"):
             for j, what in ((2 * k, "db->query"), (2 * k + 1, "query->db")):
                 if bad[j]:
                     f, (w, h) = fields[j], spans[j]
-                    raise ValueError(f"entry {names[k]} {what}: field grid {f.grid_w}x{f.grid_h} at scale "
+                    raise ValueError(f"entry {peid[k]} {what}: field grid {f.grid_w}x{f.grid_h} at scale "
                                      f"({f.scale_x}, {f.scale_y}) does not span image {w}x{h}")
             raise ValueError(derr[k])
+    up.finish()
     q = np.repeat(np.asarray(pq, dtype=np.int64), 2)
     e = np.repeat(np.asarray(pe, dtype=np.int64), 2)
     d = np.tile(np.array([0, 1], dtype=np.int64), n)
     return q, e, d, fields, up, recs
+
+
+def _index_of(vmap, index):
+    if index is None:
+        index = DescriptorIndex.from_entries((e.id, e.descriptor) for e in vmap.entries)
+    return index
+
+
+def _plan(jobs, vmap, index, depth_cache, device_cache, retrieval="host", ranked=None):
+    """Segment arrays + depth records for every query."""
+    by_id = {e.id: e for e in vmap.entries}
+    if ranked is None:
+        ranked = _retrieve(jobs, _index_of(vmap, index), retrieval)
+    return _plan_finish(_pair_fields(jobs, ranked, by_id), by_id, depth_cache, device_cache)
 
 
 class LiftPlan:
@@ -469,15 +506,20 @@ class LiftPlan:
     """
 
     def __init__(self, jobs, vmap, index=None, depth_cache=None, device_cache=None,
-                 threshold: float = CONFIDENCE_THRESHOLD, retrieval: str = "host"):
+                 threshold: float = CONFIDENCE_THRESHOLD, retrieval: str = "host", pairs=None, ctx=None):
         import torch
+        self.ctx = ctx  # explicit _lib.Context (own workspace) for concurrent lanes
         if not 0 <= threshold <= 1:
             raise ValueError(f"threshold must be in [0, 1], got {threshold}")
         self.jobs = list(jobs)
         self.threshold = float(threshold)
         self.device_cache = {} if device_cache is None else device_cache
-        q, e, d, self.fields, self.up, recs = _plan(self.jobs, vmap, index, depth_cache, self.device_cache,
-                                                     retrieval)
+        if pairs is None:  # ``pairs``: a precomputed ``_pair_fields`` (the pipelined loop's worker)
+            q, e, d, self.fields, self.up, recs = _plan(self.jobs, vmap, index, depth_cache, self.device_cache,
+                                                         retrieval)
+        else:
+            q, e, d, self.fields, self.up, recs = _plan_finish(pairs, {x.id: x for x in vmap.entries},
+                                                                depth_cache, self.device_cache)
         self.nseg = len(self.fields)
         self.seg_q = q
         self.table = _seg_table(q, e, d, e, self.up)
@@ -497,20 +539,21 @@ class LiftPlan:
     def lift(self):
         """Run the lift; returns per-query [start, end) match ranges (host)."""
         _call_lift(self.table, self.nseg, self.deps, self.ndep, self.up.f64, self.threshold, 0, self.px, self.X,
-                   self.w, self.ent, self.cap, self.offs, self.flags, self.fields)
+                   self.w, self.ent, self.cap, self.offs, self.flags, self.fields, self.ctx)
         qs = np.arange(len(self.jobs))
         # segments are in query order: first/last segment of every query
         start = self.offs[np.searchsorted(self.seg_q, qs, "left")]
         end = self.offs[np.searchsorted(self.seg_q, qs, "right")]
         return start, end
 
-    def run_device(self, cfg: RansacConfig, seeds=None, out=None):
-        """Lift + batched estimator, all on device.  Returns (out dict or None,
-        estimated query indices, their match offsets, per-query ranges)."""
+    def run_device(self, cfg: RansacConfig, seeds=None, out=None, ranges=None):
+        """Lift (unless ``ranges`` from an earlier ``lift()`` are given) + batched
+        estimator, all on device.  Returns (out dict or None, estimated query
+        indices, their match offsets, per-query ranges)."""
         import torch
         Q = len(self.jobs)
         seeds = [cfg.seed] * Q if seeds is None else list(seeds)
-        start, end = self.lift()
+        start, end = self.lift() if ranges is None else ranges
         run = [qi for qi in range(Q) if end[qi] - start[qi] >= 3]
         if not run:
             return None, run, None, (start, end)
@@ -524,17 +567,23 @@ class LiftPlan:
             dX = torch.cat([self.X[s] for s in sl]).contiguous()
             dw = torch.cat([self.w[s] for s in sl]).contiguous()
         res = ransac_pnp_device(dpx, dX, dw, offsets, [self.jobs[qi].intrinsics for qi in run],
-                                [seeds[qi] for qi in run], cfg, out=out)
+                                [seeds[qi] for qi in run], cfg, out=out, ctx=self.ctx)
         return res, run, offsets, (start, end)
 
     def localize(self, cfg: RansacConfig, seeds=None) -> list:
-        out, run, offsets, (start, end) = self.run_device(cfg, seeds)
+        return self.collect(*self.run_device(cfg, seeds))
+
+    def collect(self, out, run, offsets, ranges, host=None) -> list:
+        """PoseEstimates of a ``run_device`` result (``host``: its arrays
+        already copied out by ``_stage_results``)."""
+        start, end = ranges
         res: list = [None] * len(self.jobs)
         for qi in range(len(self.jobs)):
             if qi not in run:
                 res[qi] = _failure(int(end[qi] - start[qi]))
         if run:
-            for qi, est in zip(run, _estimates_from(out, offsets)):
+            ests = _estimates_from(out, offsets) if host is None else _estimates_from_host(*host)
+            for qi, est in zip(run, ests):
                 res[qi] = est
         return res
 
@@ -556,45 +605,148 @@ def localize_batch(jobs, vmap, cfg: RansacConfig, seeds=None, index=None, depth_
     return plan.localize(cfg, seeds)
 
 
+_LANE_CONTEXTS: dict = {}
+
+
+def serving_schedule(Q: int):
+    """Micro-batch ends for ``localize_pipelined`` when the fields' PCIe copy
+    dominates (C5: 0.84 GB of IMLC records per 256 queries, ~15 ms at
+    55 GB/s against ~10 ms of GPU work): a small first batch so the GPU
+    starts early, a small last batch so little work trails the last copy,
+    larger batches between (weights 1,3,4,4,3,1 / 16; tools/c5_host_breakdown.py
+    sweep).  Small query counts collapse to fewer batches."""
+    w = np.array([1, 3, 4, 4, 3, 1], dtype=np.float64)
+    ends = np.round(np.cumsum(w) / w.sum() * Q).astype(np.int64)
+    return sorted({int(e) for e in ends if e > 0} | {Q})
+
+
+def _lanes(device: int, n: int):
+    """``n`` (library context, stream) lanes of a device and a copy stream,
+    kept for reuse: fresh streams would start with empty allocator pools."""
+    import torch
+    lst = _LANE_CONTEXTS.setdefault(device, [])
+    with torch.cuda.device(device):
+        while len(lst) < n:
+            lst.append((_lib.Context(device), torch.cuda.Stream()))
+        copy = _LANE_CONTEXTS.get(("copy", device))
+        if copy is None:
+            copy = _LANE_CONTEXTS[("copy", device)] = torch.cuda.Stream()
+    return lst[:n], copy
+
+
 def localize_pipelined(batches, vmap, cfg: RansacConfig, seeds=None, index=None, depth_cache=None,
                        confidence_threshold: float = CONFIDENCE_THRESHOLD, device_cache=None,
-                       retrieval: str = "host", buffers=None):
+                       retrieval: str = "host", buffers=None, lanes: int | None = None):
     """Micro-batched serving loop: ``batches`` = [(jobs, arena), ...], each
-    batch's IMLC fields in its own ``FieldArena``.  Batch k+1's fields are
-    copied to HBM on a side stream while batch k is retrieved, lifted and
-    estimated (``localize_batch``), so PCIe time hides behind GPU work.
-    ``buffers`` (optional): two uint8 CUDA tensors large enough for any
-    arena, reused across calls.  ``seeds`` covers all jobs, in order.
-    Returns the flat list of PoseEstimates."""
+    batch's IMLC fields in its own ``FieldArena``.
+
+    Every query is retrieved up front (one ranking call) and the map depth
+    it needs is made resident; then ``lanes`` host threads (default 2, env
+    VISLOC_PIPE_LANES), each with its own stream and library context, take
+    batches round-robin: plan, lift, estimate, read back.  While one lane
+    sits in the library's round loop (GIL released) the other plans its
+    next batch and the GPU runs both lanes' kernels concurrently.  Batch k's
+    fields go to HBM on a copy stream into ``buffers[k % len(buffers)]``
+    once batch k - len(buffers) has been lifted.  Each query behaves like
+    ``localize(job, vmap, RansacConfig(seed=seeds[i]))``.
+    ``buffers`` (optional): uint8 CUDA tensors large enough for any arena,
+    reused across calls (default: one per lane + 1).  ``seeds`` covers all
+    jobs, in order.  Returns the flat list of PoseEstimates."""
+    import threading
+
     import torch
     batches = list(batches)
     if not batches:
         return []
+    if not 0 <= confidence_threshold <= 1:
+        raise ValueError(f"threshold must be in [0, 1], got {confidence_threshold}")
+    nb = len(batches)
+    L = max(1, min(int(lanes or os.environ.get("VISLOC_PIPE_LANES", 2)), nb))
     njobs = sum(len(j) for j, _ in batches)
     seeds = [cfg.seed] * njobs if seeds is None else list(seeds)
     if buffers is None:
         big = max(a.host.numel() for _, a in batches)
-        buffers = [torch.empty(big, dtype=torch.uint8, device="cuda") for _ in range(min(2, len(batches)))]
-    copy = torch.cuda.Stream()
+        buffers = [torch.empty(big, dtype=torch.uint8, device="cuda") for _ in range(min(L + 1, nb))]
+    B = len(buffers)
+    all_jobs = [j for jobs, _ in batches for j in jobs]
+    first = np.cumsum([0] + [len(j) for j, _ in batches])
+    dev = torch.cuda.current_device()
+    lanes_, copy = _lanes(dev, L)
+    ctxs, streams = [c for c, _ in lanes_], [st for _, st in lanes_]
     comp = torch.cuda.current_stream()
-    done = [torch.cuda.Event() for _ in batches]
     copy.wait_stream(comp)
+    lifted = [torch.cuda.Event() for _ in batches]
+    issued = [threading.Event() for _ in batches]
+    results, errors = [None] * nb, [None] * nb
+    lock = threading.Lock()
 
     def upload(k):
-        if k >= 2:
-            copy.wait_event(done[k - 2])  # buffer k % 2 was last read by batch k - 2
-        batches[k][1].upload(buffers[k % len(buffers)], stream=copy)
+        if k < nb:
+            with lock:
+                if k >= B:
+                    copy.wait_event(lifted[k - B])  # buffer k % B was last read by batch k - B
+                batches[k][1].upload(buffers[k % B], stream=copy)
+            issued[k].set()
 
-    upload(0)
-    res, s0 = [], 0
-    for k, (jobs, _) in enumerate(batches):
-        if k + 1 < len(batches):
-            upload(k + 1)
-        res += localize_batch(jobs, vmap, cfg, seeds[s0:s0 + len(jobs)], index, depth_cache, confidence_threshold,
-                              device_cache, retrieval)
-        done[k].record(comp)
-        s0 += len(jobs)
-    return res
+    for k in range(min(B, nb)):  # the first payloads cross PCIe while the queries are ranked
+        upload(k)
+    ranked = _retrieve(all_jobs, _index_of(vmap, index), retrieval)
+    by_id = {e.id: e for e in vmap.entries}
+    device_cache = {} if device_cache is None else device_cache
+    for job, ids in zip(all_jobs, ranked):  # depth the lanes will read, resident before they start
+        for eid in ids:
+            if eid in job.fields and eid not in device_cache:
+                entry = by_id[eid]
+                depth = depth_cache.get(eid) if depth_cache is not None else None
+                depth = depth if depth is not None else getattr(entry, "qdepth", None)
+                if depth is not None:
+                    _device_depth(entry, depth, device_cache)
+    for st in streams:
+        st.wait_stream(comp)
+
+    order = iter(range(nb))  # a free lane takes the next batch
+
+    def lane(i):
+        with torch.cuda.device(dev), torch.cuda.stream(streams[i]):
+            while True:
+                with lock:
+                    k = next(order, None)
+                if k is None:
+                    return
+                issued[k].wait()
+                if any(e is not None for e in errors):
+                    continue
+                try:
+                    jobs = batches[k][0]
+                    pk = _pair_fields(jobs, ranked[first[k]:first[k + 1]], by_id)
+                    plan = LiftPlan(jobs, vmap, None, depth_cache, device_cache, confidence_threshold, pairs=pk,
+                                    ctx=ctxs[i])
+                    ranges = plan.lift()
+                    lifted[k].record(streams[i])
+                    upload(k + B)
+                    out, run, offsets, ranges = plan.run_device(cfg, seeds[first[k]:first[k + 1]], ranges=ranges)
+                    host = _stage_results(out, offsets) if run else None
+                    results[k] = plan.collect(out, run, offsets, ranges, host)
+                except BaseException as exc:  # noqa: BLE001 - re-raised on the calling thread
+                    errors[k] = exc
+                    for j in range(k + 1, nb):  # release every lane still waiting on an upload
+                        issued[j].set()
+
+    if L == 1:
+        lane(0)
+    else:
+        threads = [threading.Thread(target=lane, args=(i,), daemon=True) for i in range(L)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    for st in streams:
+        comp.wait_stream(st)
+    comp.wait_stream(copy)
+    for exc in errors:
+        if exc is not None:
+            raise exc
+    return [est for r in results for est in r]
 
 
 def localize(query_job, vmap, cfg: RansacConfig, index=None, depth_cache=None,

@@ -208,19 +208,26 @@ def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, o
     return out
 
 
-def _estimates_from(out, offsets) -> list[PoseEstimate]:
-    """PoseEstimates from the device result dict: one pinned D2H per array
-    (flags viewed as bool without a host conversion pass), per-query masks are
-    views of the one host flag array."""
+def _stage_results(out, offsets):
+    """Enqueue the D2H copies of a device result dict into pinned host
+    tensors on the current stream; returns (host dict, ready event, offsets)."""
     import torch
-    keys = ("q", "t", "flags", "count", "score", "iterations", "converged", "stats")
     host = {}
-    for k in keys:
+    for k in ("q", "t", "flags", "count", "score", "iterations", "converged", "stats"):
         v = out[k]
         h = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
         h.copy_(v, non_blocking=True)
         host[k] = h
-    torch.cuda.current_stream().synchronize()
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream())
+    return host, ev, offsets
+
+
+def _estimates_from_host(host, ev, offsets) -> list[PoseEstimate]:
+    """PoseEstimates once ``_stage_results``' copies land (any thread): the
+    flags are viewed as bool without a conversion pass and per-query masks
+    are views of the one host flag array."""
+    ev.synchronize()
     q, t = host["q"].numpy(), host["t"].numpy()
     flags = host["flags"].numpy().view(np.bool_)
     cnt, score = host["count"].numpy().tolist(), host["score"].numpy().tolist()
@@ -235,6 +242,11 @@ def _estimates_from(out, offsets) -> list[PoseEstimate]:
             score=score[i], iterations=iters[i], converged=bool(conv[i]),
             stats={"lo_calls": st[0], "hypotheses": st[1], "evals": st[2], "rounds": st[3]}))
     return res
+
+
+def _estimates_from(out, offsets) -> list[PoseEstimate]:
+    """PoseEstimates from the device result dict (one pinned D2H per array)."""
+    return _estimates_from_host(*_stage_results(out, offsets))
 
 
 def _host_chunks(Q: int, chunk_queries=None):

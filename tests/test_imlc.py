@@ -178,8 +178,19 @@ def test_gpu_localize_pipelined_equals_batch(golden):
         batches.append((bj, arena))
     flat = [j for b, _ in batches for j in b]
     ref = L.localize_batch(flat, vmap, cfg, seeds=seeds, depth_cache={})
-    got = L.localize_pipelined(batches, vmap, cfg, seeds=seeds, depth_cache={})
-    assert len(got) == len(ref)
-    for a, b in zip(ref, got):
-        assert np.array_equal(a.pose.q, b.pose.q) and np.array_equal(a.inlier_flags, b.inlier_flags)
-        assert a.iterations == b.iterations and a.score == b.score
+    import torch
+    for lanes, nbuf in ((1, 1), (2, 2), (2, 3), (3, 1)):
+        bufs = [torch.empty(max(a.host.numel() for _, a in batches), dtype=torch.uint8, device="cuda")
+                for _ in range(nbuf)]
+        got = L.localize_pipelined(batches, vmap, cfg, seeds=seeds, depth_cache={}, buffers=bufs, lanes=lanes)
+        assert len(got) == len(ref)
+        for a, b in zip(ref, got):
+            assert np.array_equal(a.pose.q, b.pose.q) and np.array_equal(a.inlier_flags, b.inlier_flags)
+            assert a.iterations == b.iterations and a.score == b.score
+    # an error in one lane's batch surfaces on the caller (no lane left waiting)
+    bad = [(list(b), a) for b, a in batches]
+    j0 = bad[1][0][0]
+    bad[1][0][0] = L.QueryJob(j0.query_id, L.CameraIntrinsics(1.0, 1.0, 0.0, 0.0, 7, 7), j0.descriptor,
+                              j0.fields, j0.k_loc)
+    with pytest.raises(ValueError, match="does not span image 7x7"):
+        L.localize_pipelined(bad, vmap, cfg, seeds=seeds, depth_cache={}, lanes=2)
