@@ -12,6 +12,7 @@
 //   k_active   1 CTA     : compacts the active-query list for the next round
 // After the last round k_final (CTA/query) classifies the full set and runs
 // the Cauchy refinement (posest.py:284-299).
+#include <mutex>
 #include <climits>
 #include <cstddef>
 #include <cstdlib>
@@ -688,14 +689,23 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   if (phase != 1) {
     H(kStageScan, true);
     // function attributes are per device: set once for each device used
+    // (host threads driving separate contexts may get here together)
     static int max_smem_dev[kMaxDevices] = {0};
+    static std::mutex mu;
     int dev = 0;
     cudaGetDevice(&dev);
-    int& max_smem = max_smem_dev[dev < kMaxDevices ? dev : 0];
-    if (max_smem == 0) {
-      cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-      max_smem -= (int)(sizeof(LMShared<kScanThreads>) + 1024);  // static smem of the kernel
-      cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    int max_smem;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      int& ms = max_smem_dev[dev < kMaxDevices ? dev : 0];
+      if (ms == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        v -= (int)(sizeof(LMShared<kScanThreads>) + 1024);  // static smem of the kernel
+        cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+        ms = v;
+      }
+      max_smem = ms;
     }
     const size_t with_costs = kStageBytes + (size_t)wk.HCAP * sizeof(float);
     const int costs_smem = with_costs <= (size_t)max_smem ? 1 : 0;
@@ -808,12 +818,16 @@ __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, In
 int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
                  int q_base, cudaStream_t st) {
   static bool attr_dev[kMaxDevices] = {false};
+  static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
-  bool& attr = attr_dev[dev < kMaxDevices ? dev : 0];
-  if (!attr) {  // the staging ring needs more than the 48 KB default dynamic smem (per device)
-    cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes);
-    attr = true;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    bool& attr = attr_dev[dev < kMaxDevices ? dev : 0];
+    if (!attr) {  // the staging ring needs more than the 48 KB default dynamic smem (per device)
+      cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes);
+      attr = true;
+    }
   }
   int cs = pick_cluster(Q, VL_LO_MINB * 148);
   if (const char* e = getenv("VISLOC_FINAL_CS")) cs = atoi(e);  // tuning knob

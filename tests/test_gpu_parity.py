@@ -369,3 +369,48 @@ def test_config_edge_cases_vs_oracle(vl, intr, n, kw):
         assert og.rot_err_deg(e.pose.q, o.q) < 0.01
         assert np.linalg.norm(e.pose.t - o.t) <= 1e-4 * max(np.linalg.norm(o.t), 1e-9)
         assert (e.inlier_flags != o.inlier_flags).sum() == 0
+
+
+def test_gpu_concurrent_contexts_from_threads(vl):
+    """Two host threads, each with its own library context and stream, estimate
+    different query groups at the same time (the serving lanes of
+    localize_pipelined): results equal the single-threaded run."""
+    import threading
+
+    import torch
+    from paper_2601_04185_b200 import _lib
+    from paper_2601_04185_b200.posest import ransac_pnp_device
+    Q, n = 12, 3000
+    qs = [matches_a(n, 0.6, 1.0, seed=900 + i) for i in range(Q)]
+    d = [torch.from_numpy(np.concatenate([q[k] for q in qs])).cuda() for k in range(3)]
+    offsets = np.arange(Q + 1, dtype=np.int64) * n
+    intr = [vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)] * Q
+    seeds = [77 + i for i in range(Q)]
+    cfg = vl.RansacConfig(max_iterations=2000)
+    ref = {k: v.cpu() for k, v in ransac_pnp_device(d[0], d[1], d[2], offsets, intr, seeds, cfg).items()}
+    halves = [(0, Q // 2), (Q // 2, Q)]
+    ctxs = [_lib.Context(torch.cuda.current_device()) for _ in halves]
+    streams = [torch.cuda.Stream() for _ in halves]
+    outs, errs = [None, None], []
+
+    def run(g):
+        try:
+            a, b = halves[g]
+            r0, r1 = int(offsets[a]), int(offsets[b])
+            with torch.cuda.stream(streams[g]):
+                for _ in range(3):
+                    o = ransac_pnp_device(d[0][r0:r1], d[1][r0:r1], d[2][r0:r1], offsets[a:b + 1] - offsets[a],
+                                          intr[a:b], seeds[a:b], cfg, ctx=ctxs[g])
+                streams[g].synchronize()
+                outs[g] = {k: v.cpu() for k, v in o.items()}
+        except BaseException as exc:  # noqa: BLE001
+            errs.append(exc)
+    th = [threading.Thread(target=run, args=(g,)) for g in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for g, (a, b) in enumerate(halves):
+        assert torch.equal(outs[g]["q"], ref["q"][a:b]) and torch.equal(outs[g]["count"], ref["count"][a:b])
+        assert torch.equal(outs[g]["flags"], ref["flags"][int(offsets[a]):int(offsets[b])])
