@@ -814,7 +814,7 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
   const size_t meta = seg_bytes + dep_bytes + nseg * sizeof(int64_t);  // all multiples of 8
   const size_t host_bytes = meta + (nseg + 1) * sizeof(int64_t) + nseg * sizeof(int) + 64;
   int rc;
-  if ((rc = ensure(c, c->lift_meta, meta + nseg * sizeof(int))) || (rc = ensure(c, c->lift_blk_count, nblk * sizeof(int))) ||
+  if ((rc = ensure(c, c->lift_meta, meta + nseg * sizeof(int))) || (rc = ensure(c, c->lift_blk_count, nblk * 9 * sizeof(int))) ||
       (rc = ensure(c, c->lift_blk_off, nblk * sizeof(int64_t))) || (rc = ensure(c, c->lift_seg_off, (nseg + 1) * sizeof(int64_t))) ||
       (rc = ensure_host(c, host_bytes)))
     return rc;
@@ -839,6 +839,7 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
   a.seg_blk0 = (const int64_t*)(d + seg_bytes + dep_bytes);
   a.nblk = nblk;
   a.blk_count = (int*)c->lift_blk_count.p;
+  a.warp_count = a.blk_count + nblk;
   a.blk_off = (int64_t*)c->lift_blk_off.p;
   a.seg_off = (int64_t*)c->lift_seg_off.p;
   a.seg_flags = (int*)(d + meta);

@@ -210,38 +210,52 @@ __device__ __forceinline__ int find_seg(const int64_t* seg_blk0, int nseg, int64
   return lo;
 }
 
-// A block covers kLiftBlockCells consecutive cells of one segment; iteration
-// i handles cells [i*NT, (i+1)*NT) of it, one per thread, so every load and
-// every output store of a warp touches consecutive addresses.
+// A block covers kLiftBlockCells consecutive cells of one segment; warp w owns
+// the contiguous run [w*256, (w+1)*256) of them and iteration i handles cells
+// w*256 + i*32 + lane, so every load and output store of a warp touches
+// consecutive addresses and the write pass can rank cells inside each warp
+// with no block barrier (per-warp counts come from this pass).
+#ifndef VL_LIFT_CMINB
+#define VL_LIFT_CMINB 8  // min resident CTAs of the count pass (register cap; 8 measured best)
+#endif
+#ifndef VL_LIFT_WMINB
+#define VL_LIFT_WMINB 5  // same for the write pass (5 measured best; small spills cost less than the occupancy)
+#endif
+constexpr int kLiftWarps = kLiftThreads / 32;
+constexpr int kLiftWarpCells = kLiftBlockCells / kLiftWarps;  // 256
+
 template <typename T>
-__global__ void __launch_bounds__(kLiftThreads) k_lift_count(LiftArgs a, int mode) {
+__global__ void __launch_bounds__(kLiftThreads, VL_LIFT_CMINB) k_lift_count(LiftArgs a, int mode) {
   const int64_t b = blockIdx.x;
   const int s = find_seg(a.seg_blk0, a.nseg, b);
   const LiftSeg S = a.segs[s];
   const int cells = S.gw * S.gh;
-  const int cb = (int)(b - a.seg_blk0[s]) * kLiftBlockCells;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int cw = (int)(b - a.seg_blk0[s]) * kLiftBlockCells + wid * kLiftWarpCells;
   const T thr = (T)a.threshold;
   int cnt = 0, flags = 0;
-#pragma unroll 2
+#pragma unroll 4
   for (int i = 0; i < kLiftPerThread; ++i) {
-    const int cell = cb + i * kLiftThreads + threadIdx.x;
-    if (cell >= cells) break;
-    const CellIn<T> in = load_cell<T>(S, cell);
-    if (S.layout == kLayoutImlc) flags |= content_flags((float)in.c, in.tx, in.ty);
-    if (gate<T>(in.c, thr) && cell_keep<T>(S, a.depths, cell, in, mode)) ++cnt;
+    const int cell = cw + i * 32 + lane;
+    if (cell < cells) {
+      const CellIn<T> in = load_cell<T>(S, cell);
+      if (S.layout == kLayoutImlc) flags |= content_flags((float)in.c, in.tx, in.ty);
+      if (gate<T>(in.c, thr) && cell_keep<T>(S, a.depths, cell, in, mode)) ++cnt;
+    }
   }
-  __shared__ int wsum[kLiftThreads / 32];
-  __shared__ int wflag[kLiftThreads / 32];
+  __shared__ int wsum[kLiftWarps];
+  __shared__ int wflag[kLiftWarps];
   cnt = warp_sum(cnt);
   flags = __reduce_or_sync(0xffffffffu, (unsigned)flags);
-  if ((threadIdx.x & 31) == 0) {
-    wsum[threadIdx.x >> 5] = cnt;
-    wflag[threadIdx.x >> 5] = flags;
+  if (lane == 0) {
+    wsum[wid] = cnt;
+    wflag[wid] = flags;
+    a.warp_count[b * kLiftWarps + wid] = cnt;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     int t = 0, f = 0;
-    for (int w = 0; w < kLiftThreads / 32; ++w) {
+    for (int w = 0; w < kLiftWarps; ++w) {
       t += wsum[w];
       f |= wflag[w];
     }
@@ -305,49 +319,44 @@ int launch_lift_prep(void* dst, const void* src_host, size_t bytes, int* zero, i
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kLiftThreads) k_lift_write(LiftArgs a, int mode) {
-  __shared__ int wcnt[2][kLiftThreads / 32];
+__global__ void __launch_bounds__(kLiftThreads, VL_LIFT_WMINB) k_lift_write(LiftArgs a, int mode) {
   const int64_t b = blockIdx.x;
   const int s = find_seg(a.seg_blk0, a.nseg, b);
   const LiftSeg S = a.segs[s];
   const int cells = S.gw * S.gh;
-  const int cb = (int)(b - a.seg_blk0[s]) * kLiftBlockCells;
-  const T thr = (T)a.threshold;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int cw = (int)(b - a.seg_blk0[s]) * kLiftBlockCells + wid * kLiftWarpCells;
+  if (cw >= cells) return;  // whole warp past the segment end
+  const T thr = (T)a.threshold;
   const unsigned lt = (1u << lane) - 1u;
-  int64_t pos0 = a.blk_off[b];
+  // this warp's first output row: block offset + the block's earlier warps
+  int64_t pos = a.blk_off[b];
+  {
+    const int c = lane < wid ? a.warp_count[b * kLiftWarps + lane] : 0;
+    pos += warp_sum(c);
+  }
   for (int i = 0; i < kLiftPerThread; ++i) {
-    if (cb + i * kLiftThreads >= cells) break;  // uniform across the block
-    const int cell = cb + i * kLiftThreads + threadIdx.x;
+    const int cell = cw + i * 32 + lane;
+    if (cw + i * 32 >= cells) break;  // uniform across the warp
     CellResult r;
     bool keep = false;
     if (cell < cells) {
       const CellIn<T> in = load_cell<T>(S, cell);
       keep = gate<T>(in.c, thr) && cell_eval<T>(S, a.depths, cell, in, mode, r);
     }
-    // order-preserving rank inside iteration i (row-major cell order)
     const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) wcnt[i & 1][wid] = __popc(m);
-    __syncthreads();
-    int before = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kLiftThreads / 32; ++w) {
-      const int c = wcnt[i & 1][w];
-      before += w < wid ? c : 0;
-      tot += c;
-    }
     if (keep) {
-      const int64_t pos = pos0 + before + __popc(m & lt);
-      if (pos < a.capacity) {
-        reinterpret_cast<double2*>(a.px_out)[pos] = make_double2(r.px[0], r.px[1]);
-        a.X_out[3 * pos] = r.X[0];
-        a.X_out[3 * pos + 1] = r.X[1];
-        a.X_out[3 * pos + 2] = r.X[2];
-        a.w_out[pos] = r.w;
-        if (a.entry_out) a.entry_out[pos] = S.entry;
+      const int64_t p = pos + __popc(m & lt);
+      if (p < a.capacity) {
+        reinterpret_cast<double2*>(a.px_out)[p] = make_double2(r.px[0], r.px[1]);
+        a.X_out[3 * p] = r.X[0];
+        a.X_out[3 * p + 1] = r.X[1];
+        a.X_out[3 * p + 2] = r.X[2];
+        a.w_out[p] = r.w;
+        if (a.entry_out) a.entry_out[p] = S.entry;
       }
     }
-    pos0 += tot;
+    pos += __popc(m);
   }
 }
 

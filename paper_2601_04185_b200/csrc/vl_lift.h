@@ -38,6 +38,7 @@ struct LiftArgs {
   const int64_t* seg_blk0;  // [nseg] first block of each segment
   int64_t nblk;
   int* blk_count;           // [nblk]
+  int* warp_count;          // [nblk * 8] kept cells of every warp's 256-cell run
   int* seg_flags;           // [nseg] IMLC content verdicts (VL_FIELD_*), zeroed by the caller
   int64_t* blk_off;         // [nblk]
   int64_t* seg_off;         // [nseg+1]
