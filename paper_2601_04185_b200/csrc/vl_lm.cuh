@@ -159,6 +159,16 @@ __device__ __forceinline__ void stage_issue(const StagedPts& ps, int lo, int cnt
                : "memory");
 }
 
+// Invalidate the ring's mbarriers once every thread is past its last wait, so
+// the next pass's mbarrier.init does not act on a live barrier.
+__device__ __forceinline__ void stage_inval(uint64_t* bars) {
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int b = 0; b < kStageN; ++b)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bars + b)) : "memory");
+  __syncthreads();
+}
+
 __device__ __forceinline__ void stage_wait(const StagedPts& ps, int c) {
   const unsigned bar = smem_u32(ps.bar + c % kStageN);
   const unsigned parity = (unsigned)(c / kStageN) & 1u;
@@ -199,6 +209,7 @@ __device__ __forceinline__ void staged_for_each(const StagedPts& ps, F&& fn) {
     __syncthreads();  // every thread is done with the slot before it is refilled
     if (threadIdx.x == 0 && c + kStageN < nch) stage_issue(ps, lo, cnt, c + kStageN);
   }
+  stage_inval(ps.bar);  // the next pass re-initialises them
 }
 
 template <typename PS>

@@ -725,8 +725,132 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
 // ------------------------------------------------------------------ final stage
 constexpr int kFinalThreads = VL_LO_NT;
 
+// Full-set MSAC pass (posest.py:160-175 / 284-299) of a one-CTA query with
+// the caller's px / X / w arrays streamed through the TMA ring: chunk c is
+// the 512 points [a0 + 512 c, ...) of the global arrays, a0 = S.off rounded
+// down to even so every bulk copy (px 16 B, X 24 B, w 8 B per point) starts
+// and ends on a 16-B boundary; a trailing odd point is read directly.  The
+// plain-load pass was latency bound (ncu, C5: long_scoreboard 42 % of the
+// k_final stalls at 13 warps/SM).  With COMPACT the ordered inlier
+// compaction X[flags_full] (posest.py:291-294) is done in the same pass from
+// the staged records: one block scan of (first-half, second-half) flag
+// counts packed into an int per chunk, so the inliers are not re-read.
+// Returns cost / count in sm.red[0..1] like msac_pass.
+constexpr int kAosSlotPx = 0, kAosSlotX = kStageCh * 16, kAosSlotW = kStageCh * 40;  // byte offsets in a slot
+
+__device__ __forceinline__ void aos_issue(const double* px, const double* X, const double* w, int64_t a0, int64_t e,
+                                          unsigned char* ring, uint64_t* bars, int c) {
+  const int slot = c % kStageN;
+  const int64_t s = a0 + (int64_t)c * kStageCh;
+  const unsigned m = (unsigned)(e - s < kStageCh ? e - s : kStageCh);
+  unsigned char* dst = ring + (size_t)slot * kStageCh * 48;
+  const unsigned bar = smem_u32(bars + slot);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(m * 48u) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst + kAosSlotPx)), "l"(px + 2 * s), "r"(m * 16u), "r"(bar) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst + kAosSlotX)), "l"(X + 3 * s), "r"(m * 24u), "r"(bar) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst + kAosSlotW)), "l"(w + s), "r"(m * 8u), "r"(bar) : "memory");
+}
+
+template <int NT, bool COMPACT>
+__device__ void msac_full_staged(LMShared<NT>& sm, const Inputs& in, int64_t g0, int n, const Intr& cin, double tau,
+                                 uint8_t* flags, double2* cpk, unsigned char* ring, uint64_t* bars, int* warp_tot,
+                                 int direct) {
+  static_assert(kStageCh == 2 * NT, "two points per thread per chunk");
+  const double t2 = dmul(tau, tau);
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = sm.R[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = sm.t[k];
+  const int64_t g1 = g0 + n, a0 = g0 & ~(int64_t)1, e = g1 & ~(int64_t)1;
+  const int nch = (int)((e - a0 + kStageCh - 1) / kStageCh);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kStageN; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + b)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int c = 0; c < min(kStageN, nch); ++c) aos_issue(in.px, in.X, in.w, a0, e, ring, bars, c);
+  double acc[2] = {0.0, 0.0};
+  int running = 0;
+  auto point = [&](int64_t gi, const double* P, double u, double v, double w, int& f) {
+    const double e2 = msac_e2(R, t, cin, P, u, v);
+    acc[0] = acc[0] + dmul(w, fmin(e2, t2));
+    f = e2 < t2 ? 1 : 0;
+    acc[1] += (double)f;
+    flags[gi - g0] = (uint8_t)f;
+  };
+  for (int c = 0; c < nch; ++c) {
+    const unsigned bar = smem_u32(bars + c % kStageN);
+    const unsigned parity = (unsigned)(c / kStageN) & 1u;
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITA_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITA_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+    const unsigned char* buf = ring + (size_t)(c % kStageN) * kStageCh * 48;
+    const double2* spx = reinterpret_cast<const double2*>(buf + kAosSlotPx);
+    const double* sX = reinterpret_cast<const double*>(buf + kAosSlotX);
+    const double* sw = reinterpret_cast<const double*>(buf + kAosSlotW);
+    const int64_t s = a0 + (int64_t)c * kStageCh;
+    const int m = (int)(e - s < kStageCh ? e - s : kStageCh);
+    double P[2][3], u[2], v[2], w[2];
+    int f[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = threadIdx.x + h * NT;
+      if (j < m && s + j >= g0) {
+        if (direct) {
+          const int64_t gi = s + j;
+          P[h][0] = in.X[3 * gi];
+          P[h][1] = in.X[3 * gi + 1];
+          P[h][2] = in.X[3 * gi + 2];
+          u[h] = in.px[2 * gi];
+          v[h] = in.px[2 * gi + 1];
+          w[h] = in.w[gi];
+        } else {
+        const double2 q = spx[j];
+        P[h][0] = sX[3 * j];
+        P[h][1] = sX[3 * j + 1];
+        P[h][2] = sX[3 * j + 2];
+        u[h] = q.x;
+        v[h] = q.y;
+        w[h] = sw[j];
+        }
+        point(s + j, P[h], u[h], v[h], w[h], f[h]);
+      }
+    }
+    if constexpr (COMPACT) {
+      int total;
+      const int ex = block_excl_scan<NT>(f[0] | (f[1] << 16), warp_tot, total);
+      const int t0 = total & 0xffff;
+      if (f[0]) pack_point(cpk, running + (ex & 0xffff), P[0], u[0], v[0], w[0]);
+      if (f[1]) pack_point(cpk, running + t0 + (ex >> 16), P[1], u[1], v[1], w[1]);
+      running += t0 + (total >> 16);
+    } else {
+      __syncthreads();  // every thread is done with the slot before it is refilled
+    }
+    if (threadIdx.x == 0 && c + kStageN < nch) aos_issue(in.px, in.X, in.w, a0, e, ring, bars, c + kStageN);
+  }
+  stage_inval(bars);
+  if (g1 != e && threadIdx.x == 0) {  // odd end: the last point, after every staged one
+    const int64_t gi = g1 - 1;
+    double P[3] = {in.X[3 * gi], in.X[3 * gi + 1], in.X[3 * gi + 2]};
+    int f = 0;
+    point(gi, P, in.px[2 * gi], in.px[2 * gi + 1], in.w[gi], f);
+    if (COMPACT && f) pack_point(cpk, running, P, in.px[2 * gi], in.px[2 * gi + 1], in.w[gi]);
+  }
+  block_sum<NT, 2>(acc, sm.scratch, sm.red);
+}
+
 __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, Inputs in, Outputs out, RansacParams p,
-                                                         int q_base) {
+                                                         int q_base, int staged) {
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ uint64_t stage_bar[kStageN];
   __shared__ LMShared<kFinalThreads> sm;
@@ -766,13 +890,19 @@ __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, In
   }
   const Pose best = S.best;
   set_eval_pose(sm, best);
-  msac_pass<kFinalThreads>(sm, full, cin, p.tau, flags);  // cluster-wide; flags visible after its cluster barrier
+  double2* cpk = wk.comp_pk + 3 * S.coff;
+  if (staged & 1)  // one CTA per query: TMA-streamed pass with the inlier compaction fused
+    msac_full_staged<kFinalThreads, true>(sm, in, S.off, n, cin, p.tau, flags, cpk, dyn_smem, stage_bar, warp_tot,
+                                          staged & 4);
+  else
+    msac_pass<kFinalThreads>(sm, full, cin, p.tau, flags);  // cluster-wide; flags visible after its cluster barrier
   const double cost_full = sm.red[0];
   const int64_t cnt_full = (int64_t)sm.red[1];
   if (cnt_full < 3) {
     write_small(best, cnt_full, cost_full, 0);
     return;
   }
+  if (!(staged & 1)) {
   // ordered compaction of the full-set inliers (X[flags_full], posest.py:291-294):
   // CTA r of the cluster owns the contiguous range [lo, hi) of the point list
   __syncthreads();
@@ -789,7 +919,6 @@ __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, In
     cl_sync();
     for (unsigned r = 0; r < cr; ++r) start += (int)cl_load_ll(&sm.cnt[0], r);
   }
-  double2* cpk = wk.comp_pk + 3 * S.coff;
   int running = start;
   for (int base = lo; base < hi; base += kFinalThreads) {
     const int i = base + threadIdx.x;
@@ -803,7 +932,9 @@ __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, In
     }
     running += total;
   }
+  }
   __threadfence();
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // compacted records are read back by TMA
   __syncthreads();
   if (cs > 1) cl_sync();  // compacted points of every CTA visible cluster-wide
   const StagedPts inl{cpk, (int)cnt_full, reinterpret_cast<double2*>(dyn_smem), stage_bar};
@@ -811,7 +942,11 @@ __global__ void __launch_bounds__(kFinalThreads, VL_LO_MINB) k_final(Work wk, In
                            nullptr);
   const Pose fin = sm.cur;
   set_eval_pose(sm, fin);
-  msac_pass<kFinalThreads>(sm, full, cin, p.tau, flags);
+  if (staged & 2)
+    msac_full_staged<kFinalThreads, false>(sm, in, S.off, n, cin, p.tau, flags, nullptr, dyn_smem, stage_bar, warp_tot,
+                                           staged & 4);
+  else
+    msac_pass<kFinalThreads>(sm, full, cin, p.tau, flags);
   write_small(fin, (int64_t)sm.red[1], sm.red[0], 1);
 }
 
@@ -831,7 +966,12 @@ int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const Ran
   }
   int cs = pick_cluster(Q, VL_LO_MINB * 148);
   if (const char* e = getenv("VISLOC_FINAL_CS")) cs = atoi(e);  // tuning knob
-  launch_clustered(k_final, Q, kFinalThreads, kStageBytes, cs, st, wk, in, out, p, q_base);
+  // TMA-streamed full-set passes need one CTA per query and 16-B aligned arrays
+  int staged = cs == 1 && ((reinterpret_cast<uintptr_t>(in.px) | reinterpret_cast<uintptr_t>(in.X) |
+                            reinterpret_cast<uintptr_t>(in.w)) & 15) == 0;
+  if (staged) staged = 3;  // bit 0: first pass + fused compaction, bit 1: final pass, bit 2: debug (global reads)
+  if (const char* e = getenv("VISLOC_FINAL_STAGED")) staged = staged ? atoi(e) : 0;  // A/B knob
+  launch_clustered(k_final, Q, kFinalThreads, kStageBytes, cs, st, wk, in, out, p, q_base, staged);
   return 1;
 }
 
