@@ -4,7 +4,10 @@ The oracle runs on every host core (one process per problem); each problem
 draws its size, inlier ratio, noise, outlier weights, ground-truth pose,
 seed and RansacConfig (iterations, eta, batch size, tau, subset size) from
 one generator.  Prints the summary counts that DESIGN.md quotes.  GPU only:
-    python tools/parity_sweep.py [N] [seed]
+    python tools/parity_sweep.py [N] [seed] [batch]
+With "batch" every problem shares one RansacConfig (own seed, n <= 20001)
+and the GPU side is ONE ransac_pnp_batch call, so batches of more than 74
+problems run k_final one CTA per query (TMA-streamed full-set passes).
 """
 import json
 import multiprocessing as mp
@@ -51,7 +54,13 @@ def oracle_worker(p):
 def main():
     N = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     seed0 = int(sys.argv[2]) if len(sys.argv) > 2 else 7
+    batched = len(sys.argv) > 3 and sys.argv[3] == "batch"
     probs = [draw(k, seed0) for k in range(N)]
+    if batched:
+        for k, p in enumerate(probs):
+            p["n"] = int(np.random.default_rng([seed0, k, 1]).choice([20, 201, 1000, 3001, 8000, 20001]))
+            p["cfg"] = dict(seed=p["cfg"]["seed"], max_iterations=2000, miss_probability=1e-2,
+                            reproj_threshold=12.0, max_scoring=10_000, batch_size=1000)
     ctx = mp.get_context("spawn")
     with ctx.Pool(len(os.sched_getaffinity(0))) as pool:
         async_res = pool.map_async(oracle_worker, probs, chunksize=1)
@@ -59,11 +68,16 @@ def main():
         from oracle import geometry as og
         intr = vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
         gpu = []
-        for p in probs:
+        if batched:
+            cfg = dict(probs[0]["cfg"])
+            cfg.pop("seed")
+            gpu = vl.ransac_pnp_batch([problem(p) for p in probs], intr, vl.RansacConfig(**cfg),
+                                      seeds=[p["cfg"]["seed"] for p in probs])
+        for p in ([] if batched else probs):
             px, X, w = problem(p)
             gpu.append(vl.ransac_pnp((px, X, w), intr, vl.RansacConfig(**p["cfg"])))
         ref = async_res.get()
-    stats = dict(problems=N, same_iterations=0, same_converged=0, pose_within_tol=0, masks_identical=0,
+    stats = dict(mode="batch" if batched else "single", problems=N, same_iterations=0, same_converged=0, pose_within_tol=0, masks_identical=0,
                  max_rot_deg=0.0, max_rel_t=0.0, flag_mismatch_points=0, near_tau_only=0)
     from oracle.posest import errors_sq
     for p, e, o in zip(probs, gpu, ref):
