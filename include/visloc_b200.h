@@ -118,7 +118,9 @@ int vl_ransac_pnp(vl_ctx* ctx, const vl_ransac_args* args, const vl_ransac_out* 
  * stage_events[k] (a cudaEvent_t recorded after that stage's host-to-device
  * copy, on any stream) has completed.  All stages share one round loop, so
  * later copies overlap the rounds of admitted queries.  Results equal
- * vl_ransac_pnp's.  One workspace chunk of queries. */
+ * vl_ransac_pnp's.  A run larger than one workspace chunk (4096 queries at
+ * batch_size 1000, fewer for larger batches) runs its chunks in order, each
+ * admitting the stages that overlap it. */
 int vl_ransac_pnp_staged(vl_ctx* ctx, const vl_ransac_args* args, const vl_ransac_out* out, int32_t nstage,
                          const int32_t* stage_end, void* const* stage_events, void* stream);
 
@@ -156,6 +158,16 @@ int vl_ransac_step_finish_argmin(vl_ctx* ctx, const int64_t* keys, int32_t* nact
 int vl_msac_score(vl_ctx* ctx, const double* q, const double* t, const double* px,
                   const double* X, const double* w, int64_t n, vl_intrinsics intr, double tau,
                   double* cost_out, uint8_t* flags, void* stream);
+
+/* replaces visloc.posest._score_hypotheses (posest.py:178-220): the fp32
+ * ranking costs of H hypotheses (R DEVICE [H,3,3] row-major, t DEVICE [H,3])
+ * against one scoring set (px/X/w DEVICE, n rows) through the estimator's own
+ * k_score kernel (records, fx/fy-folded rows, canonical split sums).
+ * shape: 0 = the estimator's single-query tiles, 1 = fine, 2 = coarse tiles
+ * (same bits by construction).  costs DEVICE [H] f32. */
+int vl_score_hypotheses(vl_ctx* ctx, const double* R, const double* t, int32_t H, const double* px,
+                        const double* X, const double* w, int64_t n, vl_intrinsics intr, double tau,
+                        int32_t shape, float* costs, void* stream);
 
 /* replaces visloc.refine.refine_pose (refine.py:164).  loss: 0 truncated
  * (TruncatedLoss(scale)), 1 Cauchy (CauchyLoss(scale)).  q_io/t_io HOST

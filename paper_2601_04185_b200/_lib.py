@@ -161,6 +161,8 @@ def lib():
         L.vl_profile_read.argtypes = [vp, dp, C.POINTER(C.c_int64), i32]
         L.vl_ransac_pnp.argtypes = [vp, C.POINTER(RansacArgs), C.POINTER(RansacOut), vp]
         L.vl_msac_score.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, dbl, dp, vp, vp]
+        L.vl_score_hypotheses.argtypes = [vp, vp, vp, i32, vp, vp, vp, i64, Intrinsics, dbl, i32, vp, vp]
+        L.vl_score_hypotheses.restype = C.c_int
         L.vl_refine_pose.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, i32, dbl, i32, dbl, dbl,
                                      ip, ip, dp, ip, vp]
         L.vl_p3p_solve_batch.argtypes = [vp, vp, vp, i32, vp, vp, vp, ip, vp]
@@ -216,6 +218,7 @@ EXPORTED_SYMBOLS = (
     "vl_ransac_step_score", "vl_ransac_step_finish", "vl_ransac_end", "vl_imlc_parse",
     "vl_retrieval_topk", "vl_ransac_pnp_staged", "vl_quantize_depth", "vl_reduce_depth_codes",
     "vl_build_depth_maps", "vl_triangulate_rays", "vl_ransac_step_argmin", "vl_ransac_step_finish_argmin",
+    "vl_score_hypotheses",
 )
 
 STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final", "lift")

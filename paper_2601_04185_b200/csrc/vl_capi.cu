@@ -498,44 +498,35 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
 // without the tail cost of separate per-chunk runs.  Per-query results are
 // identical to vl_ransac_pnp (each query's computation is independent of
 // which others share its rounds).
-int vl_ransac_pnp_staged(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, int32_t nstage,
-                         const int32_t* stage_end, void* const* stage_events, void* stream) {
-  if (!c || !a || !o || nstage < 1 || !stage_end || !stage_events) return fail(c, VL_ERR_INVALID, "null argument");
-  cudaStream_t st = (cudaStream_t)stream;
-  RansacParams p;
-  int rc;
-  if ((rc = ransac_params(c, a, p))) return rc;
-  const int Q = a->num_queries;
-  for (int k = 0; k < nstage; ++k)
-    if (stage_end[k] <= (k ? stage_end[k - 1] : 0) || !stage_events[k])
-      return fail(c, VL_ERR_INVALID, "stages must be non-empty, increasing, with an event each");
-  if (stage_end[nstage - 1] != Q) return fail(c, VL_ERR_INVALID, "last stage must end at num_queries");
-  if (ransac_chunk(Q, a->cfg.batch_size) < Q) return fail(c, VL_ERR_INVALID, "staged run takes one workspace chunk");
-  VL_CUDA(c, cudaSetDevice(c->device));
+// One workspace chunk [q0, q0 + Qn) of a staged run; `ends` (chunk-relative)
+// and `evs` are the stages clipped to the chunk.
+static int staged_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, const std::vector<int>& ends,
+                        const std::vector<cudaEvent_t>& evs, const Inputs& in, const Outputs& out,
+                        const RansacParams& p, cudaStream_t st) {
   const int64_t B = a->cfg.batch_size;
-  Inputs in{a->px, a->X, a->w};
-  Outputs out{o->q, o->t, o->inlier_flags, o->inlier_count, o->score, o->iterations, o->converged, o->stats};
+  const int nstage = (int)ends.size();
   Work wk;
   QState* d_hqs = nullptr;
-  if ((rc = setup_chunk(c, a, 0, Q, in, wk, st, &d_hqs))) return rc;
+  int rc;
+  if ((rc = setup_chunk(c, a, q0, Qn, in, wk, st, &d_hqs))) return rc;
   const int64_t max_rounds = ((a->cfg.max_iterations + B - 1) / B + 1) * (int64_t)nstage + nstage;
   int admitted = 0, nactive = 0, guard = 0;
   while (true) {
     // admit every stage whose copy has landed (block on the next one only when idle)
     while (admitted < nstage) {
-      cudaEvent_t ev = (cudaEvent_t)stage_events[admitted];
+      cudaEvent_t ev = evs[admitted];
       if (nactive > 0) {
         const cudaError_t e = cudaEventQuery(ev);
         if (e == cudaErrorNotReady) break;
         if (e != cudaSuccess) return fail(c, VL_ERR_CUDA, std::string("cudaEventQuery: ") + cudaGetErrorString(e));
       }
       VL_CUDA(c, cudaStreamWaitEvent(st, ev, 0));
-      const int q0 = admitted ? stage_end[admitted - 1] : 0, q1 = stage_end[admitted];
+      const int s0 = admitted ? ends[admitted - 1] : 0, s1 = ends[admitted];
       prof_hook(c, kStagePrep, true);
-      c->launches += launch_prep(wk, in, q0, q1 - q0, nactive, d_hqs, st);
+      c->launches += launch_prep(wk, in, s0, s1 - s0, nactive, d_hqs, st);
       prof_hook(c, kStagePrep, false);
       if ((rc = check_launch(c))) return rc;
-      nactive += q1 - q0;
+      nactive += s1 - s0;
       ++admitted;
     }
     if (nactive == 0) break;
@@ -549,12 +540,46 @@ int vl_ransac_pnp_staged(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out
     if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
   }
   prof_hook(c, kStageFinal, true);
-  c->launches += launch_final(wk, in, out, p, Q, 0, st);
+  c->launches += launch_final(wk, in, out, p, Qn, (int)q0, st);
   prof_hook(c, kStageFinal, false);
-  if ((rc = check_launch(c))) return rc;
-  if (c->prof) {
-    VL_CUDA(c, cudaStreamSynchronize(st));
-    prof_collect(c);
+  return check_launch(c);
+}
+
+int vl_ransac_pnp_staged(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, int32_t nstage,
+                         const int32_t* stage_end, void* const* stage_events, void* stream) {
+  if (!c || !a || !o || nstage < 1 || !stage_end || !stage_events) return fail(c, VL_ERR_INVALID, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  RansacParams p;
+  int rc;
+  if ((rc = ransac_params(c, a, p))) return rc;
+  const int Q = a->num_queries;
+  for (int k = 0; k < nstage; ++k)
+    if (stage_end[k] <= (k ? stage_end[k - 1] : 0) || !stage_events[k])
+      return fail(c, VL_ERR_INVALID, "stages must be non-empty, increasing, with an event each");
+  if (stage_end[nstage - 1] != Q) return fail(c, VL_ERR_INVALID, "last stage must end at num_queries");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  Inputs in{a->px, a->X, a->w};
+  Outputs out{o->q, o->t, o->inlier_flags, o->inlier_count, o->score, o->iterations, o->converged, o->stats};
+  // a run larger than one workspace chunk: the chunks run one after another,
+  // each admitting the stages that overlap it as their copies land
+  const int64_t Qc = ransac_chunk(Q, a->cfg.batch_size);
+  for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
+    const int Qn = (int)std::min<int64_t>(Qc, Q - q0);
+    std::vector<int> ends;
+    std::vector<cudaEvent_t> evs;
+    for (int k = 0; k < nstage; ++k) {
+      const int64_t lo = std::max<int64_t>(k ? stage_end[k - 1] : 0, q0);
+      const int64_t hi = std::min<int64_t>(stage_end[k], q0 + Qn);
+      if (lo < hi) {
+        ends.push_back((int)(hi - q0));
+        evs.push_back((cudaEvent_t)stage_events[k]);
+      }
+    }
+    if ((rc = staged_chunk(c, a, q0, Qn, ends, evs, in, out, p, st))) return rc;
+    if (q0 + Qc < Q || c->prof) {
+      VL_CUDA(c, cudaStreamSynchronize(st));  // staging buffer reuse / event readout
+      prof_collect(c);
+    }
   }
   return VL_OK;
 }
@@ -681,6 +706,62 @@ int vl_msac_score(vl_ctx* c, const double* q, const double* t, const double* px,
   VL_CUDA(c, cudaMemcpyAsync(h, dred, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
   VL_CUDA(c, cudaStreamSynchronize(st));
   *cost_out = h[0];
+  return VL_OK;
+}
+
+int vl_score_hypotheses(vl_ctx* c, const double* R, const double* t, int32_t H, const double* px,
+                        const double* X, const double* w, int64_t n, vl_intrinsics intr, double tau,
+                        int32_t shape, float* costs, void* stream) {
+  if (!c || !R || !t || !px || !X || !w || !costs || H < 0 || n < 1 || shape < 0 || shape > 2)
+    return fail(c, VL_ERR_INVALID, "bad argument");
+  if (!(tau > 0)) return fail(c, VL_ERR_INVALID, "tau must be positive");
+  if (n > 0x7FFFFFFF || H > (1 << 28)) return fail(c, VL_ERR_INVALID, "n or H too large");
+  if (H == 0) return VL_OK;
+  VL_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  QState S;
+  std::memset(&S, 0, sizeof(QState));
+  S.n = S.nsub = (int)n;
+  S.stride = 1;
+  S.nsplit = (int)((n + kScoreChunk - 1) / kScoreChunk);
+  S.in = Intr{intr.fx, intr.fy, intr.cx, intr.cy};
+  S.nh = H;
+  // tile shape: the one the estimator picks for a lone query (fine), or forced
+  const int fine = shape == 2 ? 0 : 1;
+  const int64_t HCAP = H, ntile = (H + kScoreTileHypsFine - 1) / kScoreTileHypsFine;
+  const int64_t nsub_pad = n + (n & 1);
+  int rc;
+  if ((rc = ensure(c, c->qs, sizeof(QState))) || (rc = ensure(c, c->items, ntile * S.nsplit * sizeof(ScoreItem))) ||
+      (rc = ensure(c, c->item_count, 2 * sizeof(int))) || (rc = ensure(c, c->P32, 12 * HCAP * sizeof(float))) ||
+      (rc = ensure(c, c->partial, (size_t)S.nsplit * HCAP * sizeof(float))) ||
+      (rc = ensure(c, c->cost32, HCAP * sizeof(float))) || (rc = ensure(c, c->tile_cnt, ntile * sizeof(int))) ||
+      (rc = ensure(c, c->sub_pk, nsub_pad * 3 * sizeof(double2))) ||
+      (rc = ensure(c, c->sub32, (nsub_pad / 2) * 3 * sizeof(float4))))
+    return rc;
+  Work wk;
+  wk.qs = (QState*)c->qs.p;
+  wk.items = (ScoreItem*)c->items.p;
+  wk.item_count = (int*)c->item_count.p;
+  wk.P32 = (float*)c->P32.p;
+  wk.partial = (float*)c->partial.p;
+  wk.cost32 = (float*)c->cost32.p;
+  wk.tile_cnt = (int*)c->tile_cnt.p;
+  wk.sub_pk = (double2*)c->sub_pk.p;
+  wk.sub32 = (float4*)c->sub32.p;
+  wk.HCAP = (int)HCAP;
+  wk.TCAP = (int)ntile;
+  wk.NSPLIT = S.nsplit;
+  wk.item_cap = ntile * S.nsplit;
+  wk.split_rank = 0;
+  wk.split_size = 1;
+  VL_CUDA(c, cudaMemcpyAsync(wk.qs, &S, sizeof(QState), cudaMemcpyHostToDevice, st));
+  Inputs in{px, X, w};
+  c->launches += launch_prep(wk, in, 0, 1, 0, nullptr, st);  // scoring records, as every round reads them
+  c->launches += launch_hyp_rows(wk, R, t, H, fine, st);
+  c->launches += launch_score(wk, (float)(tau * tau), c->num_sms, fine, 1, st);
+  if ((rc = check_launch(c))) return rc;
+  VL_CUDA(c, cudaMemcpyAsync(costs, wk.cost32, H * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  VL_CUDA(c, cudaStreamSynchronize(st));  // the host-side state above is stack memory
   return VL_OK;
 }
 

@@ -134,6 +134,10 @@ int launch_p3p_batch(const double* f, const double* P, int B, double* slots, int
 int launch_sample(const GenState& g, uint64_t pos0, int64_t n, int count, int* out, uint64_t* pos_out,
                   cudaStream_t st);
 
+// standalone scoring: fp32 rows + score items of H caller hypotheses (query 0)
+int launch_hyp_rows(const Work& wk, const double* R, const double* t, int H, int fine, cudaStream_t st);
+int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st);
+
 // hypothesis-split packed (score, index) variant (vl_ransac.cu)
 int launch_split_argmin(const Work& wk, int nactive, int num_sms, long long* keys, cudaStream_t st);
 int launch_split_apply_argmin(const Work& wk, int nactive, const long long* keys, cudaStream_t st);

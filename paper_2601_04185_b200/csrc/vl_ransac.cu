@@ -12,6 +12,7 @@
 //   k_active   1 CTA     : compacts the active-query list for the next round
 // After the last round k_final (CTA/query) classifies the full set and runs
 // the Cauchy refinement (posest.py:284-299).
+#include <algorithm>
 #include <mutex>
 #include <climits>
 #include <cstddef>
@@ -351,6 +352,58 @@ int launch_p3p_batch(const double* f, const double* P, int B, double* slots, int
   return 2;
 }
 
+// fp32 scoring row of one hypothesis: diag(fx, fy, 1) [R | t] (R row-major,
+// t in sl[9..11]), folded in fp64 and rounded once, stored SoA with column
+// stride cs (k_score reads entry c of hypothesis h at P[c * cs + h]).
+__device__ __forceinline__ void store_p32(float* P, int64_t cs, double fx, double fy, const double* sl) {
+  P[0 * cs] = (float)(fx * sl[0]);
+  P[1 * cs] = (float)(fx * sl[1]);
+  P[2 * cs] = (float)(fx * sl[2]);
+  P[3 * cs] = (float)(fx * sl[9]);
+  P[4 * cs] = (float)(fy * sl[3]);
+  P[5 * cs] = (float)(fy * sl[4]);
+  P[6 * cs] = (float)(fy * sl[5]);
+  P[7 * cs] = (float)(fy * sl[10]);
+  P[8 * cs] = (float)sl[6];
+  P[9 * cs] = (float)sl[7];
+  P[10 * cs] = (float)sl[8];
+  P[11 * cs] = (float)sl[11];
+}
+
+// Standalone scoring (vl_score_hypotheses): rows of caller-given hypotheses
+// for query 0 of a one-query workspace, plus that round's score items.
+__global__ void k_hyp_rows(Work wk, const double* R, const double* t, int H, int fine) {
+  const QState& S = wk.qs[0];
+  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
+    double sl[12];
+    for (int i = 0; i < 9; ++i) sl[i] = R[9 * (int64_t)h + i];
+    for (int i = 0; i < 3; ++i) sl[9 + i] = t[3 * (int64_t)h + i];
+    store_p32(wk.P32 + h, wk.HCAP, S.in.fx, S.in.fy, sl);
+  }
+  const int tile_h = fine ? kScoreTileHypsFine : kScoreTileHyps;
+  const int spi = fine ? 1 : kScoreItemSplits;
+  const int ntile = (H + tile_h - 1) / tile_h, ngroups = (S.nsplit + spi - 1) / spi;
+  const int nitems = ntile * ngroups;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
+    ScoreItem it;
+    it.q = 0;
+    it.tile = i / ngroups;
+    it.split = (i % ngroups) * spi;
+    it.nsplit = min(spi, S.nsplit - it.split);
+    wk.items[i] = it;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < wk.TCAP; i += gridDim.x * blockDim.x) wk.tile_cnt[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    wk.item_count[0] = nitems;
+    wk.item_count[1] = 0;
+  }
+}
+
+int launch_hyp_rows(const Work& wk, const double* R, const double* t, int H, int fine, cudaStream_t st) {
+  k_hyp_rows<<<std::max(1, std::min(148, (H + 255) / 256)), 256, 0, st>>>(wk, R, t, H, fine);
+  return 1;
+}
+
 __global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
   __shared__ int warp_tot[32];
   __shared__ int s_item0;
@@ -368,21 +421,8 @@ __global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
     for (int k = 0; k < c; ++k) {
       const int h = running + ex + k;
       wk.hsrc[(int64_t)q * wk.HCAP + h] = s * 4 + k;
-      const double* sl = wk.slots + ((int64_t)q * wk.B + s) * 48 + 12 * k;
-      float* P = wk.P32 + (int64_t)q * 12 * wk.HCAP + h;
-      const int64_t cs = wk.HCAP;
-      P[0 * cs] = (float)(fx * sl[0]);
-      P[1 * cs] = (float)(fx * sl[1]);
-      P[2 * cs] = (float)(fx * sl[2]);
-      P[3 * cs] = (float)(fx * sl[9]);
-      P[4 * cs] = (float)(fy * sl[3]);
-      P[5 * cs] = (float)(fy * sl[4]);
-      P[6 * cs] = (float)(fy * sl[5]);
-      P[7 * cs] = (float)(fy * sl[10]);
-      P[8 * cs] = (float)sl[6];
-      P[9 * cs] = (float)sl[7];
-      P[10 * cs] = (float)sl[8];
-      P[11 * cs] = (float)sl[11];
+      store_p32(wk.P32 + (int64_t)q * 12 * wk.HCAP + h, wk.HCAP, fx, fy,
+                wk.slots + ((int64_t)q * wk.B + s) * 48 + 12 * k);
     }
     running += total;
   }

@@ -627,3 +627,25 @@ def msac_score(pose: Pose, matches, intr: CameraIntrinsics, tau: float):
                                   float(tau), C.byref(cost), flags.data_ptr(), _lib.stream_ptr())
     ctx.check(rc, "vl_msac_score")
     return float(cost.value), flags[:n].cpu().numpy().astype(bool)
+
+
+def score_hypotheses(Rs, ts, X, px, w, intr: CameraIntrinsics, tau: float, shape: int = 0) -> np.ndarray:
+    """fp32 MSAC ranking costs of many hypotheses against one correspondence set
+    (``_score_hypotheses``, posest.py:178-220), computed by the estimator's own
+    k_score kernel.  Returns float64 like the reference (the values are fp32).
+    ``shape`` selects the scoring tiles (0 single-query default, 1 fine, 2
+    coarse); every shape gives the same bits."""
+    import torch
+    Rs = np.ascontiguousarray(Rs, dtype=np.float64).reshape(-1, 3, 3)
+    ts = np.ascontiguousarray(ts, dtype=np.float64).reshape(-1, 3)
+    px, X, w = _host_arrays((px, X, w))
+    H, n = Rs.shape[0], px.shape[0]
+    ctx = _lib.context()
+    dR, dt = _to_device(Rs), _to_device(ts)
+    dpx, dX, dw = _to_device(px), _to_device(X), _to_device(w)
+    out = torch.empty((max(H, 1),), dtype=torch.float32, device=dpx.device)
+    rc = _lib.lib().vl_score_hypotheses(ctx.handle, dR.data_ptr(), dt.data_ptr(), H, dpx.data_ptr(),
+                                        dX.data_ptr(), dw.data_ptr(), n, _intr_c(intr), float(tau), int(shape),
+                                        out.data_ptr(), _lib.stream_ptr())
+    ctx.check(rc, "vl_score_hypotheses")
+    return out[:H].cpu().numpy().astype(np.float64)

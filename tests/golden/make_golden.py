@@ -26,6 +26,7 @@ from visloc.posest import (RansacConfig, _bearings, _score_hypotheses, msac_scor
 from visloc.refine import CauchyLoss, TruncatedLoss, refine_pose  # noqa: E402
 
 sys.path.insert(0, str(OUT.parent))
+sys.path.append(str(OUT.parent.parent))  # repo root (oracle / package types for the synthetic scenes)
 from synth_inputs import INTR_A, GT_A, matches_a, refine_problem  # noqa: E402
 
 
@@ -414,6 +415,150 @@ def depthbuild_vectors():
     np.savez_compressed(OUT / "depthbuild.npz", **out)
 
 
+class _LOCounter:
+    """Counts the reference's LO calls: refine_pose with a TruncatedLoss inside
+    ransac_pnp (posest.py:261-264; the final stage uses a CauchyLoss)."""
+
+    def __enter__(self):
+        import visloc.posest as P
+        self.P, self.orig, self.n = P, P.refine_pose, 0
+
+        def wrapped(*a, **k):
+            loss = a[4] if len(a) > 4 else k.get("loss")
+            if isinstance(loss, TruncatedLoss):
+                self.n += 1
+            return self.orig(*a, **k)
+
+        P.refine_pose = wrapped
+        return self
+
+    def __exit__(self, *exc):
+        self.P.refine_pose = self.orig
+
+
+def _est_record(out, p, e, lo_calls):
+    out[p + "q"], out[p + "t"] = e.pose.q, e.pose.t
+    out[p + "flags"] = np.packbits(e.inlier_flags)
+    out[p + "n"] = np.array(e.inlier_flags.size)
+    out[p + "score"] = np.array(e.score)
+    out[p + "iters"] = np.array(e.iterations)
+    out[p + "conv"] = np.array(e.converged)
+    out[p + "count"] = np.array(e.inlier_count)
+    out[p + "lo_calls"] = np.array(lo_calls)
+
+
+def baseline_vectors():
+    """Reference ransac_pnp at the BASELINE single-query shapes:
+    C1 (n=2k, eps=0.3, 10k fixed samples) and C4 (n=10k, eps=0.05, 100k fixed
+    samples and the adaptive default), with the reference's LO-call counts."""
+    cases = [
+        # (name, n, outlier_frac, sigma, data seed, ransac seed, max_iterations, eta)
+        ("c1", 2000, 0.7, 1.0, 41, 1, 10_000, 1e-300),
+        ("c4", 10_000, 0.95, 1.0, 42, 2, 100_000, 1e-300),
+        ("c4a", 10_000, 0.95, 1.0, 43, 3, 100_000, 1e-4),
+    ]
+    out = {"names": np.array([c[0] for c in cases]),
+           "cases": np.array([c[1:] for c in cases], dtype=np.float64)}
+    for name, n, of, sg, ds, rs, mi, eta in cases:
+        px, X, w, _ = matches_a(n, of, sg, seed=ds)
+        with _LOCounter() as lc:
+            e = ransac_pnp((px, X, w), INTR_A, RansacConfig(seed=rs, max_iterations=mi, miss_probability=eta))
+        _est_record(out, name + "_", e, lc.n)
+        print(name, e.iterations, lc.n, e.inlier_count, e.converged, flush=True)
+    np.savez_compressed(OUT / "baseline.npz", **out)
+
+
+def _ref_scene(vmap, jobs, dcache):
+    """Reference-typed copies of a generator-B scene (tests/synth_inputs.lifted_scene)."""
+    from visloc.depthbuild import DepthMap
+    from visloc.localizer import FieldPair, QueryJob
+    from visloc.mapstore import QuantizedDepthMap
+    from visloc.matchio import CorrespondenceField
+
+    def intr(i):
+        return CameraIntrinsics(i.fx, i.fy, i.cx, i.cy, i.width, i.height)
+
+    class Entry:
+        pass
+
+    class Map:
+        pass
+
+    ents, depth = [], {}
+    for e in vmap.entries:
+        r = Entry()
+        r.id, r.pose, r.intrinsics, r.descriptor = e.id, Pose(e.pose.q, e.pose.t), intr(e.intrinsics), e.descriptor
+        r.qdepth = None
+        if e.qdepth is not None:
+            q = e.qdepth
+            r.qdepth = QuantizedDepthMap(q.codes, q.d_min, q.d_max, q.levels, r.intrinsics)
+        if dcache is not None and e.id in dcache:
+            # the reference has no fp16 depth: its oracle is DepthMap(values=fp16.astype(f32)) (SURVEY §8d)
+            depth[e.id] = DepthMap(np.asarray(dcache[e.id].values).astype(np.float32), dcache[e.id].valid,
+                                   r.intrinsics)
+        ents.append(r)
+    m = Map()
+    m.entries = ents
+
+    def cf(f):
+        return CorrespondenceField(f.source_id, f.target_id, f.targets, f.confidence, f.scale_x, f.scale_y)
+
+    rjobs = [QueryJob(j.query_id, intr(j.intrinsics), np.asarray(j.descriptor),
+                      {k: FieldPair(cf(v.query_to_db), cf(v.db_to_query)) for k, v in j.fields.items()}, j.k_loc)
+             for j in jobs]
+    return m, rjobs, depth
+
+
+def lift_full_vectors():
+    """Reference lift + localize at the BASELINE lifted shapes on generator B
+    (tests/synth_inputs.lifted_scene, f32 fields as a file-backed IMLC field):
+    C5 (K=10, 117^2 fields, u8 log codes, and the fp16-depth variant, default
+    config) and C2 (K=20, 83^2, f32 depth, 10k fixed samples).  Per (query,
+    entry): the match count, sha256 of the pixel and weight bytes (bit-exact),
+    every 61st world point and the per-coordinate sum of X; per query the
+    localize estimate and the reference's LO-call count."""
+    import hashlib
+    from visloc.localizer import lift, localize
+    from visloc.mapstore import dequantize_depth
+    from synth_inputs import lifted_scene
+
+    cases = [  # (name, K, g, depth, seed0, queries, max_iterations, eta)
+        ("c5u8", 10, 117, "u8", 77, (0, 1), 100_000, 1e-4),
+        ("c5f16", 10, 117, "f16", 77, (0, 1), 100_000, 1e-4),
+        ("c2", 20, 83, "f32", 78, (0,), 10_000, 1e-300),
+    ]
+    out = {"names": np.array([c[0] for c in cases])}
+    for name, K, g, dk, seed0, qs, mi, eta in cases:
+        vmap, jobs, dc = lifted_scene(K, 0, g, seed=seed0, depth_kind=dk, fields="f32", only=list(qs))
+        rmap, rjobs, rdepth = _ref_scene(vmap, jobs, dc)
+        out[name + "_meta"] = np.array([K, g, seed0, mi], dtype=np.float64)
+        out[name + "_eta"] = np.array(eta)
+        out[name + "_queries"] = np.array(qs)
+        for qi, rj in zip(qs, rjobs):
+            p = f"{name}_q{qi}_"
+            cnt, hpx, hw, xs, xsum = [], [], [], [], []
+            for e in sorted(rmap.entries, key=lambda e: e.id):
+                d = rdepth[e.id] if e.id in rdepth else dequantize_depth(e.qdepth)
+                ms = lift(rj, e, d, 0.05)
+                px = np.array([m.query_px for m in ms], dtype=np.float64).reshape(-1, 2)
+                X = np.array([m.world_point for m in ms], dtype=np.float64).reshape(-1, 3)
+                w = np.array([m.weight for m in ms], dtype=np.float64)
+                cnt.append(len(ms))
+                hpx.append(hashlib.sha256(np.ascontiguousarray(px).tobytes()).hexdigest())
+                hw.append(hashlib.sha256(np.ascontiguousarray(w).tobytes()).hexdigest())
+                xs.append(X[::61])
+                xsum.append(X.sum(axis=0))
+            out[p + "count"], out[p + "hpx"], out[p + "hw"] = np.array(cnt), np.array(hpx), np.array(hw)
+            out[p + "Xs"], out[p + "Xsum"] = np.concatenate(xs), np.array(xsum)
+            seed = 1_000_003 * seed0 + qi  # bench.query_seed
+            with _LOCounter() as lc:
+                est = localize(rj, rmap, RansacConfig(seed=seed, max_iterations=mi, miss_probability=eta),
+                               depth_cache=dict(rdepth))
+            _est_record(out, p + "loc_", est, lc.n)
+            print(name, qi, sum(cnt), est.iterations, lc.n, est.inlier_count, est.converged, flush=True)
+    np.savez_compressed(OUT / "lift_full.npz", **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `make_golden.py mapstore`
         for name in sys.argv[1:]:
@@ -430,5 +575,7 @@ if __name__ == "__main__":
     msac_vectors()
     refine_vectors()
     ransac_vectors()
+    baseline_vectors()
+    lift_full_vectors()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -14,7 +14,6 @@ import os
 import numpy as np
 import pytest
 
-from oracle import geometry as og
 from oracle.posest import Config, ransac
 from synth_inputs import batch_a
 
@@ -42,14 +41,29 @@ def _run(vl, mode, qs, cfg, intr):
             os.environ["VISLOC_FINAL_STAGED"] = old
 
 
-@pytest.mark.parametrize("n", [777, 1024, 3001])
-def test_staged_final_equals_plain(vl, n):
+_PLAIN = {}
+
+
+def _case(vl, n):
     intr = vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
     pxs, Xs, ws = batch_a(160, n, 0.5, 1.0, seed0=n)
     qs = list(zip(pxs, Xs, ws))
     cfg = vl.RansacConfig(max_iterations=2000, miss_probability=1e-300)
-    plain = _run(vl, "0", qs, cfg, intr)
-    staged = _run(vl, "1", qs, cfg, intr)
+    if n not in _PLAIN:
+        _PLAIN[n] = _run(vl, "0", qs, cfg, intr)
+    return qs, cfg, intr, _PLAIN[n]
+
+
+# modes (VISLOC_FINAL_STAGED bits): 1 = first pass staged + fused compaction,
+# 2 = final pass staged (writes the returned flags / count / score), 3 = both
+# (the production default), 7 = both with the debug direct-read path.  n odd
+# gives odd per-query offsets (the a0 = even-rounded start); n = 1, 2 mod 512
+# leave a 1- or 2-point last chunk.
+@pytest.mark.parametrize("mode", ["1", "2", "3", "7"])
+@pytest.mark.parametrize("n", [777, 1024, 3001, 513, 1026])
+def test_staged_final_equals_plain(vl, n, mode):
+    qs, cfg, intr, plain = _case(vl, n)
+    staged = _run(vl, mode, qs, cfg, intr)
     for a, b in zip(plain, staged):
         assert a.converged == b.converged
         assert a.inlier_count == b.inlier_count
@@ -57,9 +71,21 @@ def test_staged_final_equals_plain(vl, n):
         assert np.allclose(a.pose.q, b.pose.q, rtol=0, atol=1e-12)
         assert np.allclose(a.pose.t, b.pose.t, rtol=0, atol=1e-12)
         assert abs(a.score - b.score) <= 1e-12 * abs(a.score)
-    # default launch (staged) against the CPU oracle on one query
-    i = 7
+
+
+@pytest.mark.parametrize("i", [7, 8])
+def test_default_final_vs_oracle(vl, i):
+    """The production launch (no knob: mode 3 for a > 74-query batch) against the CPU oracle."""
+    from parity_util import check_mask, check_pose
+    intr = vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
+    pxs, Xs, ws = batch_a(160, 777, 0.5, 1.0, seed0=777)
+    assert "VISLOC_FINAL_STAGED" not in os.environ
+    est = vl.ransac_pnp_batch(list(zip(pxs, Xs, ws)), intr, vl.RansacConfig(max_iterations=2000,
+                                                                            miss_probability=1e-300),
+                              seeds=list(range(160)))[i]
     ref = ransac(pxs[i], Xs[i], ws[i], (700.0, 700.0, 350.0, 350.0),
                  Config(seed=i, max_iterations=2000, miss_probability=1e-300))
-    assert og.rot_err_deg(staged[i].pose.q, ref.q) < 0.01
-    assert np.linalg.norm(staged[i].pose.t - ref.t) < 1e-4 * np.linalg.norm(ref.t)
+    check_pose(est.pose.q, est.pose.t, ref.q, ref.t)
+    check_mask(est.inlier_flags, ref.inlier_flags, est.pose.q, est.pose.t, pxs[i], Xs[i],
+               (700.0, 700.0, 350.0, 350.0), 12.0, q_ref=ref.q, t_ref=ref.t)
+    assert est.iterations == ref.iterations and est.stats["lo_calls"] == ref.lo_calls

@@ -109,6 +109,48 @@ def test_msac_matches_reference_golden(vl, intr, golden):
         _check_mask(f, g["flags"][k], g["q"][k], g["t"][k], g["px"], g["X"])
 
 
+def test_fp32_costs_match_reference_golden(vl, intr, golden):
+    """K4 (posest.py:178-220): the estimator's k_score costs of the reference's
+    600 golden hypotheses vs the reference's own fp32 costs (score.npz),
+    <= 1e-5 relative; every tile shape gives the same bits."""
+    from paper_2601_04185_b200.posest import score_hypotheses
+    g = golden("score")
+    ref = g["costs"]
+    got = [score_hypotheses(g["R"], g["t"], g["X"], g["px"], g["w"], intr, float(g["tau"]), shape=s)
+           for s in (0, 1, 2)]
+    assert np.array_equal(got[0], got[1]) and np.array_equal(got[0], got[2])
+    rel = np.abs(got[0] - ref) / np.maximum(np.abs(ref), 1e-30)
+    print(f"k_score vs reference fp32 costs: max rel {rel.max():.3e}, median {np.median(rel):.3e}")
+    assert rel.max() <= 1e-5, rel.max()
+    # ranking: the reference's best hypothesis is the GPU's best too
+    assert int(np.argmin(got[0])) == int(np.argmin(ref))
+
+
+@pytest.mark.parametrize("n,outl", [(10_000, 0.7), (9_999, 0.3), (129, 0.5), (3, 0.0)])
+def test_fp32_costs_full_round_vs_oracle(vl, intr, n, outl):
+    """One full round's hypotheses (P3P of 1000 samples) over an n_sub-point set
+    against the oracle's restatement of _score_hypotheses (pinned to the
+    reference by score.npz): <= 1e-5 relative, odd n and single-split sets."""
+    from oracle.posest import score_fp32
+    from oracle.p3p import p3p_batch
+    from oracle.posest import bearings
+    from paper_2601_04185_b200.posest import score_hypotheses
+    px, X, w, _ = matches_a(n, outl, 1.0, seed=n)
+    rng = np.random.default_rng(n)
+    smp = np.stack([rng.choice(n, 3, replace=False) for _ in range(300 if n > 3 else 1)])
+    f = bearings(px, INTR_T)
+    R, t, _ = p3p_batch(f[smp], X[smp])
+    if R.shape[0] == 0:
+        pytest.skip("degenerate draw")
+    ref = score_fp32(R, t, X, px, w, INTR_T, TAU)
+    got = score_hypotheses(R, t, X, px, w, intr, TAU)
+    assert np.array_equal(got, score_hypotheses(R, t, X, px, w, intr, TAU, shape=2))
+    # relative, with a floor of 1e-3 px^2 per unit weight: an exact minimal
+    # set (n = 3) has a cost that is pure fp32 rounding noise in both
+    rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-3 * w.sum())
+    assert rel.max() <= 1e-5, rel.max()
+
+
 def test_msac_kats(vl, intr):
     pose = vl.Pose.identity()
     xw = np.array([[0.0, 0.0, 2.0], [0.0, 0.0, 3.0]])
@@ -214,6 +256,37 @@ def test_host_api_chunked_pipeline_equals_device(vl):
         assert h2d == px.nbytes + X.nbytes + w.nbytes
         for k in ("q", "t", "flags", "count", "score", "iterations", "converged", "stats"):
             assert np.array_equal(host[k], ref[k]), (chunk, k)
+
+
+@pytest.mark.parametrize("Q,n,batch", [(5000, 24, 1000), (1500, 40, 10_000)])
+def test_host_api_above_one_workspace_chunk(vl, Q, n, batch):
+    """ransac_pnp_host / ransac_pnp_stream with more queries than one workspace
+    chunk (4096 at batch_size 1000, ~646 at 10k) equal ransac_pnp_device
+    (which loops over chunks) field by field (vl_capi.cu staged chunks)."""
+    import torch
+    from paper_2601_04185_b200.posest import ransac_pnp_device, ransac_pnp_host, ransac_pnp_stream
+    rng = np.random.default_rng(Q)
+    pxs, Xs, ws = [], [], []
+    for qi in range(Q):
+        px, X, w, _ = matches_a(n, 0.3, 1.0, seed=int(rng.integers(1 << 30)))
+        pxs.append(px)
+        Xs.append(X)
+        ws.append(w)
+    offsets = np.arange(Q + 1, dtype=np.int64) * n
+    px, X, w = np.concatenate(pxs), np.concatenate(Xs), np.concatenate(ws)
+    intr = [vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)] * Q
+    seeds = list(range(Q))
+    cfg = vl.RansacConfig(max_iterations=batch, batch_size=batch, miss_probability=1e-300)
+    ref = ransac_pnp_device(torch.from_numpy(px).cuda(), torch.from_numpy(X).cuda(), torch.from_numpy(w).cuda(),
+                            offsets, intr, seeds, cfg)
+    ref = {k: v.cpu().numpy() for k, v in ref.items()}
+    host, _, _ = ransac_pnp_host(px, X, w, offsets, intr, seeds, cfg)
+    (shost, _, _), = list(ransac_pnp_stream([(torch.from_numpy(px).pin_memory(), torch.from_numpy(X).pin_memory(),
+                                              torch.from_numpy(w).pin_memory(), offsets, intr, seeds)], cfg))
+    for k in ("q", "t", "flags", "count", "score", "iterations", "converged", "stats"):
+        assert np.array_equal(host[k], ref[k]), k
+        assert np.array_equal(shost[k], ref[k]), k
+    assert ref["converged"].mean() > 0.9
 
 
 def test_host_stream_equals_device(vl):

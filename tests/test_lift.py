@@ -125,7 +125,10 @@ def test_gpu_localize_matches_reference(vl, golden):
     from paper_2601_04185_b200.posest import RansacConfig
     z = golden("lift")
     vmap, jobs = unpack_scene(z)
+    from parity_util import check_mask
     res = vl.localize_batch(jobs, vmap, RansacConfig(), seeds=[100 + j for j in range(len(jobs))])
+    plan = vl.LiftPlan(jobs, vmap)  # the lifted correspondences localize estimated from
+    start, end = plan.lift()
     for j, est in enumerate(res):
         assert est.converged == bool(z[f"loc{j}_conv"])
         assert est.iterations == int(z[f"loc{j}_iters"])
@@ -133,8 +136,11 @@ def test_gpu_localize_matches_reference(vl, golden):
         assert np.linalg.norm(est.pose.t - z[f"loc{j}_t"]) < 1e-4 * max(1e-9, np.linalg.norm(z[f"loc{j}_t"]))
         ref = z[f"loc{j}_flags"]
         assert est.inlier_flags.shape == ref.shape
-        mism = est.inlier_flags != ref
-        assert mism.sum() <= max(1, int(1e-3 * ref.size)), int(mism.sum())
+        px = plan.px[int(start[j]):int(end[j])].cpu().numpy()
+        X = plan.X[int(start[j]):int(end[j])].cpu().numpy()
+        I = jobs[j].intrinsics
+        check_mask(est.inlier_flags, ref, est.pose.q, est.pose.t, px, X, (I.fx, I.fy, I.cx, I.cy), 12.0,
+                   q_ref=z[f"loc{j}_q"], t_ref=z[f"loc{j}_t"])
         assert math.isclose(est.score, float(z[f"loc{j}_score"]), rel_tol=1e-6, abs_tol=1e-9)
     single = vl.localize(jobs[1], vmap, RansacConfig(seed=101))
     assert np.array_equal(single.inlier_flags, res[1].inlier_flags)
