@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Benchmark of the B200 LO-RANSAC PnP hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c4] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c3a|c1|c4|c2|c5|c5h|map]
+                    [--impl ours|reference] [--no-configs]
 
 One *step* = one complete batched ``ransac_pnp`` over the workload's
 queries (sampling, P3P, fp32 scoring, LO, adaptive stop, final Cauchy
@@ -9,10 +10,20 @@ refinement) with inputs resident in HBM.  Default workload is BASELINE
 config C3 ("Aachen-style batch": 1000 queries x 50k correspondences per GPU,
 30% inliers, sigma 1 px) in fixed-iteration mode (10k minimal samples per
 query, eta = 1e-300) so every query does the same, BASELINE-named amount of
-work.  Queries shard across GPUs with no collective (weak scaling: 1000
-queries per GPU).  ``value`` = hypothesis x correspondence evaluations / s
-over the whole job; ``e2e`` = the same through the host-buffer API
-(H2D of the packed matches + D2H of poses/masks inside the timed region).
+work.  ``value`` = hypothesis x correspondence evaluations / s over the
+whole job; ``e2e`` = the same through the host-buffer API (H2D of the packed
+matches + D2H of poses/masks inside the timed region).
+
+Multi-GPU: ``--gpus N`` without a torchrun environment re-launches itself
+under ``torch.distributed.run`` (N ranks, one per GPU, NCCL, 127.0.0.1).
+Queries shard with no collective.  ``value`` is weak scaling (1000 queries
+per GPU); the line's ``strong`` object times the literal C3 batch of 1000
+queries split across the N ranks (interleaved assignment, dist.shard_indices).
+
+At N = 1 the default line also carries ``configs``: BASELINE C1 (single query
+through the drop-in ``ransac_pnp``), C4 (low inlier ratio, LO-heavy) and C5
+(8-bit compressed map: GPU lift + estimator, lift HBM roofline), each with
+its own value / e2e / roofline / cpu_baseline.
 
 ``--impl reference`` times the CPU reference arm: the oracle port of the
 reference algorithm (``oracle/``, bit-identical to visloc on the golden
@@ -44,7 +55,7 @@ WORKLOADS = {
     "c3": dict(name="C3 Aachen-style batch: 1000 queries x 50k corrs per GPU, eps=0.3, sigma=1px, "
                     "fixed 10k minimal samples/query (eta=1e-300)",
                queries=1000, n=50_000, outlier=0.7, sigma=1.0, max_iterations=10_000, eta=1e-300,
-               cpu_queries_per_core=1),
+               cpu_queries_per_core=2),
     "c3a": dict(name="C3 Aachen-style batch, adaptive stop (eta=1e-4): 1000 queries x 50k corrs per GPU, "
                      "eps=0.3, sigma=1px",
                 queries=1000, n=50_000, outlier=0.7, sigma=1.0, max_iterations=100_000, eta=1e-4,
@@ -54,7 +65,7 @@ WORKLOADS = {
                cpu_queries_per_core=1),
     "c4": dict(name="C4 low inlier ratio: 10k corrs, eps=0.05, 100k minimal samples (LO-heavy)",
                queries=1, n=10_000, outlier=0.95, sigma=1.0, max_iterations=100_000, eta=1e-300,
-               cpu_queries_per_core=1),
+               cpu_queries_per_core=1, cpu_max_iterations=20_000),
 }
 
 
@@ -64,10 +75,10 @@ LIFT_WORKLOADS = {
                K=20, g=83, queries=1, depth="f32", max_iterations=10_000, eta=1e-300, cpu_queries_per_core=0.0625),
     "c5": dict(name="C5 compressed map: 8-bit log-quantised depth decode + lift, K=10 x 117x117 fields "
                     "(~20k lifted/entry), 256 queries, default adaptive config",
-               K=10, g=117, queries=256, depth="u8", max_iterations=100_000, eta=1e-4, cpu_queries_per_core=1),
+               K=10, g=117, queries=256, depth="u8", max_iterations=100_000, eta=1e-4, cpu_queries_per_core=2),
     "c5h": dict(name="C5 compressed map (fp16 depth variant): K=10 x 117x117 fields, 256 queries, "
                      "default adaptive config",
-                K=10, g=117, queries=256, depth="f16", max_iterations=100_000, eta=1e-4, cpu_queries_per_core=1),
+                K=10, g=117, queries=256, depth="f16", max_iterations=100_000, eta=1e-4, cpu_queries_per_core=2),
 }
 LIFT_SEED = 77
 
@@ -151,7 +162,7 @@ def _cpu_worker(job):
     px, X, w = query_a(qi, wl["n"], wl["outlier"], wl["sigma"], seed0)
     t0 = time.perf_counter()
     r = ransac(px, X, w, (700.0, 700.0, 350.0, 350.0),
-               Config(seed=query_seed(qi, seed0), max_iterations=wl["max_iterations"],
+               Config(seed=query_seed(qi, seed0), max_iterations=wl.get("cpu_max_iterations", wl["max_iterations"]),
                       miss_probability=wl["eta"]))
     return r.evals, time.perf_counter() - t0
 
@@ -170,7 +181,8 @@ def cpu_sample(wl, seed0, n_queries, cores):
         ctx = mp.get_context("spawn")
         with ctx.Pool(cores) as pool:
             if not lifted and "E" not in wl:
-                pool.map(_cpu_worker, [(0, dict(wl, n=64, max_iterations=wl.get("batch", 1000)), seed0)] * cores)
+                pool.map(_cpu_worker, [(0, dict(wl, n=64, max_iterations=wl.get("batch", 1000),
+                                                cpu_max_iterations=1000), seed0)] * cores)
             t0 = time.perf_counter()
             res = pool.map(worker, [(qi, wl, seed0) for qi in range(n_queries)])
             wall = time.perf_counter() - t0
@@ -189,6 +201,44 @@ def host_cores() -> int:
     return len(os.sched_getaffinity(0))
 
 
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_sample_plan(wl, cores):
+    """(queries per sample, description) of the bounded CPU sample of a workload."""
+    nq = max(1, int(round(cores * wl["cpu_queries_per_core"])))
+    total = wl.get("queries", 1)
+    parts = [f"{nq} quer{'y' if nq == 1 else 'ies'} of the workload (the first {nq}, same inputs and seeds)"]
+    if wl.get("cpu_max_iterations"):
+        parts.append(f"each truncated to its first {wl['cpu_max_iterations']} of {wl['max_iterations']} minimal "
+                     f"samples (1/{wl['max_iterations'] // wl['cpu_max_iterations']} scale)")
+    parts.append(f"{min(cores, nq)} processes (1 per core, BLAS 1 thread), oracle port")
+    return nq, ", ".join(parts), nq < total or bool(wl.get("cpu_max_iterations"))
+
+
+def cpu_baseline_line(wl, seed0, cores, evals=None, wall=None):
+    """The ``cpu_baseline`` object: rate of the bounded sample, labelled."""
+    nq, desc, extrapolated = cpu_sample_plan(wl, cores)
+    if evals is None:
+        evals, wall = cpu_sample(wl, seed0, nq, cores)
+    out = {"value": evals / wall, "unit": "evals/s", "cores": min(cores, nq), "kind": "port",
+           "sample": desc, "cpu_model": cpu_model(), "host_cores": cores,
+           "sample_wall_s": wall, "queries_per_s": nq / wall}
+    if extrapolated:
+        out["extrapolated"] = True
+        out["extrapolation"] = ("rate of the sample applied to the whole workload (queries are independent; "
+                                "the metric is a rate)")
+    return out
+
+
 def run_reference_arm(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -197,19 +247,20 @@ def run_reference_arm(args, wl):
     if "E" in wl:
         run_map_reference_arm(args, wl, cores)
         return
-    nq = max(1, int(cores * wl["cpu_queries_per_core"]))
+    nq, desc, _ = cpu_sample_plan(wl, cores)
     seed0 = LIFT_SEED if "K" in wl else 3000
+    # warm-up: the worker pool and imports on a small sample (one query per core)
     for _ in range(args.warmup):
-        cpu_sample(wl, seed0, nq, cores)
-    vals, walls = [], []
+        cpu_sample(dict(wl, cpu_max_iterations=wl.get("batch", 1000)) if "K" not in wl else wl, seed0,
+                   min(nq, cores), cores)
+    walls = []
     total_evals = 0
     for _ in range(args.steps):
         ev, wall = cpu_sample(wl, seed0, nq, cores)
-        vals.append(ev / wall)
         walls.append(wall)
         total_evals += ev
     value = total_evals / sum(walls)
-    sample = f"{nq} queries of the workload per step ({wl['cpu_queries_per_core']}/core), oracle port"
+    cpu = cpu_baseline_line(wl, seed0, cores, total_evals, sum(walls))
     line = {
         "impl": "reference", "metric": "hyp×corr evals/s", "value": value, "unit": "evals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -217,7 +268,7 @@ def run_reference_arm(args, wl):
         "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
         "config": {"workload": wl["name"], "queries_per_step": nq, "corrs_per_query": wl.get("n", "lifted")},
         "queries_per_s": nq / statistics.mean(walls),
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -241,7 +292,8 @@ def run_map_reference_arm(args, wl, cores):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl["name"], "maps_per_step": nm},
         "cpu_baseline": {"value": value, "unit": "px/s", "cores": min(cores, nm), "kind": "port",
-                         "sample": f"{nm} maps of the workload per step (1/core), oracle port"},
+                         "sample": f"{nm} maps of the workload per step (1/core), oracle port",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "px/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -473,11 +525,8 @@ def run_lift_bench(args, wl, rank, world, local, dist):
                      "share_of_step": lift_ms / ms if ms else None, "launches": lift_launches}}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cores = host_cores()
-        nq = max(1, int(cores * wl["cpu_queries_per_core"]))
-        cev, cwall = cpu_sample(wl, seed0, nq, cores)
-        cpu = {"value": cev / cwall, "unit": "evals/s", "cores": min(cores, nq), "kind": "port",
-               "sample": f"{nq} queries of the same workload (oracle lift + ransac), 1 process/query"}
+        cpu = cpu_baseline_line(wl, seed0, host_cores())
+        cpu["sample"] += " (lift + ransac per query)"
     if rank == 0:
         line = {
             "metric": "hyp×corr evals/s", "value": value, "unit": "evals/s", "n_gpus": world,
@@ -496,7 +545,8 @@ def run_lift_bench(args, wl, rank, world, local, dist):
             "stage_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in prof.items()},
             "profiled_ms_per_step": ms_prof / args.steps,
         }
-        print(json.dumps(line), flush=True)
+        return line
+    return None
 
 
 # ----------------------------------------------------------------------------- GPU arm: mapping
@@ -605,63 +655,44 @@ def run_map_bench(args, wl, rank, world, local, dist):
         }), flush=True)
 
 
-# ----------------------------------------------------------------------------- GPU arm
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(LIFT_WORKLOADS) + sorted(MAP_WORKLOADS),
-                    default="c3")
-    ap.add_argument("--queries", type=int, default=None, help="override queries per GPU")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-e2e", action="store_true")
-    args = ap.parse_args()
-    lifted = args.workload in LIFT_WORKLOADS
-    mapping = args.workload in MAP_WORKLOADS
-    wl = dict(MAP_WORKLOADS[args.workload] if mapping else
-              LIFT_WORKLOADS[args.workload] if lifted else WORKLOADS[args.workload])
-    if args.queries:
-        wl["queries"] = args.queries
-    if args.impl == "reference":
-        run_reference_arm(args, wl)
-        return
+# ----------------------------------------------------------------------------- GPU arm: generator A
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
 
+
+def bench_direct(args, wl, rank, world, local, dist, steps, mode="weak", with_e2e=True, with_cpu=True):
+    """Generator-A workloads (C1, C3, C3a, C4).  mode "weak": every rank runs
+    its own wl["queries"] queries; "strong": the wl["queries"] queries of the
+    job are split across the ranks (interleaved, dist.shard_indices).
+    Returns the JSON line (rank 0) or None."""
     import torch
-    import torch.distributed as dist
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # functional check of the multi-rank path on a one-GPU box (never a
-    # measurement): VISLOC_BENCH_DEVICE=0 VISLOC_BENCH_BACKEND=gloo
-    local = int(os.environ.get("VISLOC_BENCH_DEVICE", local))
-    backend = os.environ.get("VISLOC_BENCH_BACKEND", "nccl")
-    torch.cuda.set_device(local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    from paper_2601_04185_b200 import _lib
-    from paper_2601_04185_b200.geometry import CameraIntrinsics
-    from paper_2601_04185_b200.posest import RansacConfig, ransac_pnp_device, ransac_pnp_stream
-    if lifted or mapping:
-        (run_map_bench if mapping else run_lift_bench)(args, wl, rank, world, local, dist)
-        if world > 1:
-            dist.destroy_process_group()
-        return
 
-    Q, n = wl["queries"], wl["n"]
-    seed0 = 3000 + 100_000 * rank
-    qs = [query_a(qi, n, wl["outlier"], wl["sigma"], seed0) for qi in range(Q)]
+    from paper_2601_04185_b200 import _lib
+    from paper_2601_04185_b200.dist import shard_indices
+    from paper_2601_04185_b200.geometry import CameraIntrinsics
+    from paper_2601_04185_b200.posest import (RansacConfig, ransac_pnp, ransac_pnp_device, ransac_pnp_host,
+                                              ransac_pnp_stream)
+    n = wl["n"]
+    if mode == "strong":
+        seed0 = 3000
+        qids = shard_indices(wl["queries"], rank, world, "interleaved")
+    else:
+        seed0 = 3000 + 100_000 * rank
+        qids = list(range(wl["queries"]))
+    Q = len(qids)
+    qs = [query_a(qi, n, wl["outlier"], wl["sigma"], seed0) for qi in qids]
     px_h = torch.from_numpy(np.concatenate([q[0] for q in qs])).pin_memory()
     X_h = torch.from_numpy(np.concatenate([q[1] for q in qs])).pin_memory()
     w_h = torch.from_numpy(np.concatenate([q[2] for q in qs])).pin_memory()
+    single = [(q[0], q[1], q[2]) for q in qs] if Q == 1 else None
     del qs
     offsets = np.arange(Q + 1, dtype=np.int64) * n
-    intr = [CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)] * Q
-    seeds = [query_seed(qi, seed0) for qi in range(Q)]
+    intr1 = CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
+    intr = [intr1] * Q
+    seeds = [query_seed(qi, seed0) for qi in qids]
     cfg = RansacConfig(max_iterations=wl["max_iterations"], miss_probability=wl["eta"])
     px_d, X_d, w_d = px_h.cuda(), X_h.cuda(), w_h.cuda()
     ctx = _lib.context(local)
@@ -672,6 +703,12 @@ def main():
         if world > 1:
             dist.barrier()
             torch.cuda.synchronize()
+
+    def max_over_ranks(v, op="max"):
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
 
     out = None
     for _ in range(args.warmup):
@@ -684,81 +721,91 @@ def main():
     def step():
         ransac_pnp_device(px_d, X_d, w_d, offsets, intr, seeds, cfg, out=out)
 
-    ms, launches, _, clocks = timed_region(ctx, stream, sync_all, step, args.steps, False)
-    ms_prof, _, prof, _ = timed_region(ctx, stream, sync_all, step, args.steps, True)
+    ms, launches, _, clocks = timed_region(ctx, stream, sync_all, step, steps, False)
+    ms_prof, _, prof, _ = timed_region(ctx, stream, sync_all, step, steps, True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t_local = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    ms_max = float(t_local.item())
-    evals_local = torch.tensor([float(evals_per_step)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(evals_local)
-    evals_total = float(evals_local.item()) * args.steps
+    ms_max = max_over_ranks(ms)
+    evals_total = max_over_ranks(evals_per_step, "sum") * steps
+    q_total = max_over_ranks(Q, "sum")
     value = evals_total / (ms_max / 1000.0)
-    queries_per_s = Q * world * args.steps / (ms_max / 1000.0)
+    queries_per_s = q_total * steps / (ms_max / 1000.0)
 
-    # ---- end-to-end through the host-buffer API
+    # ---- end-to-end through the public host API
     e2e = None
-    if not args.no_e2e:
-        # serving loop through the public host API: every step is one batch of
-        # Q queries copied from pinned host memory (H2D) and its results read
-        # back (D2H); batch k+1's copy streams while batch k is estimated, the
-        # first batch is admitted stage by stage (ransac_pnp_stream)
+    if with_e2e and Q == 1:
+        # the drop-in call a user makes: ransac_pnp(matches (host numpy), intr, cfg) -> PoseEstimate
+        px1, X1, w1 = single[0]
+        c1 = RansacConfig(max_iterations=wl["max_iterations"], miss_probability=wl["eta"], seed=seeds[0])
+        for _ in range(2):
+            est = ransac_pnp((px1, X1, w1), intr1, c1)
+        sync_all()
+        e0.record(stream)
+        for _ in range(steps):
+            est = ransac_pnp((px1, X1, w1), intr1, c1)
+        e1.record(stream)
+        sync_all()
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": evals_total / (ems / 1000.0), "unit": "evals/s",
+               "h2d_bytes_per_step": int(px1.nbytes + X1.nbytes + w1.nbytes),
+               "d2h_bytes_per_step": int(est.inlier_flags.size + 8 * (4 + 3 + 1 + 1 + 1 + 1 + 4)),
+               "api": "ransac_pnp((px, X, w) host numpy, intr, cfg) -> PoseEstimate (the drop-in call), "
+                      "per call: pinned staging, H2D, estimate, D2H",
+               "latency_ms": ems / steps, "queries_per_s": q_total * steps / (ems / 1000.0)}
+    elif with_e2e:
+        # one-shot: one cold ransac_pnp_host call (the whole batch's H2D, staged
+        # admission, estimate, D2H of every result), nothing overlapped from before
+        sync_all()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        host, hb, db = ransac_pnp_host(px_h, X_h, w_h, offsets, intr, seeds, cfg)
+        e1.record(stream)
+        sync_all()
+        one_ms = max_over_ranks(max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0)))
+        one_shot = {"value": evals_total / steps / (one_ms / 1000.0), "unit": "evals/s", "ms": one_ms,
+                    "h2d_bytes": int(hb), "d2h_bytes": int(db),
+                    "api": "ransac_pnp_host: one call, first batch's H2D included (no pipeline fill excluded)"}
+        del host
+        # serving loop: every step is one batch of Q queries copied from pinned
+        # host memory (H2D) and its results read back (D2H); batch k+1's copy
+        # streams while batch k is estimated
         batch = (px_h, X_h, w_h, offsets, intr, seeds)
         for res in ransac_pnp_stream([batch] * 3, cfg):  # warm (device buffers, pinned result sets)
             del res
         sync_all()
-        # steady-state serving: one stream of W + K + 1 batches; the timed
-        # region runs from the W-th result handed out to the (W+K)-th, so it
-        # holds K batches' H2D, estimation and result D2H, and not the
-        # pipeline fill (first batch's staged copy) or drain
         W = 3
         h2d = d2h = 0
-        marks = []
-        gen = ransac_pnp_stream([batch] * (W + args.steps + 1), cfg)
+        gen = ransac_pnp_stream([batch] * (W + steps + 1), cfg)
         for i, (res, hb, db) in enumerate(gen):
             h2d, d2h = hb, db
             del res  # results consumed: the pinned set goes back to the pool
             if i == W - 1:
                 e0.record(stream)
-            if i >= W - 1:
-                marks.append(time.perf_counter())
-            if i == W - 1 + args.steps:
+            if i == W - 1 + steps:
                 e1.record(stream)
                 break
         gen.close()
         sync_all()
-        if os.environ.get("VISLOC_BENCH_TRACE"):
-            print("e2e result intervals (ms):", [round(1e3 * (b - a), 1) for a, b in zip(marks, marks[1:])],
-                  file=sys.stderr)
-        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        e2e = {"value": evals_total / (float(ems.item()) / 1000.0), "unit": "evals/s",
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": evals_total / (ems / 1000.0), "unit": "evals/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "api": "ransac_pnp_stream: one batch per step, batch k+1 H2D overlaps batch k; steady state "
-                      "(timed from the 3rd result handed out, pipeline fill and drain excluded)",
-               "queries_per_s": Q * world * args.steps / (float(ems.item()) / 1000.0)}
+                      "(timed from the 3rd result handed out, pipeline fill and drain excluded; see one_shot)",
+               "queries_per_s": q_total * steps / (ems / 1000.0), "one_shot": one_shot}
 
     # ---- roofline of the dominant kernel (fp32 MSAC scoring), live CUDA events
-    peaks = {}
-    try:
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except Exception:
-        pass
+    peaks = _peaks()
     props = torch.cuda.get_device_properties(local)
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
     score_ms, score_launches = prof["score"]
-    achieved = (evals_per_step * args.steps * FLOP_PER_EVAL) / (score_ms / 1000.0) / 1e12 if score_ms else None
-    stage_ms = {k: round(v[0] / args.steps, 3) for k, v in prof.items()}
+    achieved = (evals_per_step * steps * FLOP_PER_EVAL) / (score_ms / 1000.0) / 1e12 if score_ms else None
+    stage_ms = {k: round(v[0] / steps, 3) for k, v in prof.items()}
     traffic = None
     try:  # DRAM bytes per k_score launch from the committed ncu --set full capture (profiles/)
         tr = json.loads((ROOT / "profiles" / "traffic.json").read_text())["k_score"]
-        if tr.get("workload") == args.workload and Q == 1000:
+        if tr.get("workload") == args.workload and Q == 1000 and mode == "weak":
             traffic = {"dram_bytes_per_launch": tr["dram_bytes_per_launch"], "source": tr["source"],
-                       "algorithmic_bytes_per_launch": int(evals_per_step / score_launches * args.steps
+                       "algorithmic_bytes_per_launch": int(evals_per_step / score_launches * steps
                                                            / 10_000 * (48 + 4 * 20)) +
                        (Q * 10_000 * 24 if score_launches else 0)}  # 24-B records (pair-packed f32)
     except Exception:
@@ -768,38 +815,177 @@ def main():
             "peak_source": "derived SMs*128*2*sm_max_mhz (MEASURED_PEAKS.json has no FP32 entry)",
             "flop_per_eval": FLOP_PER_EVAL,
             "traffic": traffic["dram_bytes_per_launch"] if traffic else None, "traffic_detail": traffic,
-            "evals_per_s_kernel": (evals_per_step * args.steps) / (score_ms / 1000.0) if score_ms else None,
+            "evals_per_s_kernel": (evals_per_step * steps) / (score_ms / 1000.0) if score_ms else None,
             "score_share_of_step": (score_ms / ms_prof) if ms_prof else None,
             "score_launches": score_launches}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cores = host_cores()
-        ev, wall = cpu_sample(wl, seed0, cores * wl["cpu_queries_per_core"], cores)
-        cpu = {"value": ev / wall, "unit": "evals/s", "cores": cores, "kind": "port",
-               "sample": f"{cores * wl['cpu_queries_per_core']} queries of the same workload "
-                         f"(first queries, same seeds), oracle port, 1 process/core"}
+    if rank == 0 and world == 1 and with_cpu and not args.no_cpu:
+        cpu = cpu_baseline_line(wl, seed0, host_cores())
+    if rank != 0:
+        return None
+    return {
+        "metric": "hyp×corr evals/s", "value": value, "unit": "evals/s", "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": ms_max / steps,
+        "higher_is_better": True, "scaling": mode, "vs_baseline": None, "dtype": "f32+f64",
+        "data": "synthetic",
+        "config": {"workload": wl["name"], "queries_total": int(q_total),
+                   "queries_per_gpu": Q if mode == "weak" else f"{wl['queries']}/{world} (interleaved)",
+                   "corrs_per_query": n, "n_sub": min(n, 10_000), "max_iterations": wl["max_iterations"],
+                   "miss_probability": wl["eta"],
+                   "l2": (f"inputs {px_h.numel() * 8 * 3 / 1e9:.2f} GB/GPU (> 126 MB L2; no flush needed)"
+                          if px_h.numel() * 24 > 126e6 else
+                          f"inputs {px_h.numel() * 24 / 1e6:.2f} MB/GPU, L2-resident (single-query latency "
+                          f"config: every step re-reads them from L2, as a serving loop would)"),
+                   "parallelism": f"query-sharded x{world} ({'weak' if mode == 'weak' else 'strong, interleaved'}), "
+                                  f"no collective"},
+        "queries_per_s": queries_per_s, "converged_frac": conv_rate,
+        "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+        "clocks": clocks, "gpu_launches": launches, "stage_ms_per_step": stage_ms,
+        "profiled_ms_per_step": ms_prof / steps,
+    }
 
+
+def _config_summary(line):
+    """The parts of a workload's line that the default line's ``configs`` carries."""
+    keep = ("value", "unit", "ms_per_step", "steps", "queries_per_s", "converged_frac", "e2e", "roofline",
+            "cpu_baseline", "clocks", "gpu_launches", "stage_ms_per_step", "config")
+    return {k: line[k] for k in keep if k in line}
+
+
+# ----------------------------------------------------------------------------- launcher
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n: int) -> int:
+    """Re-launch this command under torch.distributed.run with n ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_setup(args):
+    """(rank, world, local device, backend) from the torchrun environment; initialises the group."""
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # VISLOC_BENCH_BACKEND=gloo: functional check of the multi-rank path on
+    # fewer GPUs than ranks (ranks share devices: never a measurement)
+    backend = os.environ.get("VISLOC_BENCH_BACKEND", "nccl")
+    dry = bool(os.environ.get("VISLOC_BENCH_DRYRUN"))
+    if not dry:
+        ndev = torch.cuda.device_count()
+        if ndev == 0:
+            raise SystemExit("bench.py: no CUDA device (the GPU arm has no CPU fallback)")
+        if "VISLOC_BENCH_DEVICE" in os.environ:
+            local = int(os.environ["VISLOC_BENCH_DEVICE"])
+        elif backend != "nccl":
+            local %= ndev
+        elif local >= ndev:
+            raise SystemExit(f"bench.py: rank {rank} needs GPU {local} but only {ndev} are visible "
+                             f"(use VISLOC_BENCH_BACKEND=gloo for a functional check)")
+        torch.cuda.set_device(local)
+    if world > 1:
+        if backend == "nccl" and not dry:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo" if dry else backend)
+    return rank, world, local, backend, dist
+
+
+def dry_run(args, rank, world, dist):
+    """CPU check of the launcher: N ranks come up, own interleaved shards that
+    partition the job, and reduce a time as a max over ranks."""
+    import torch
+
+    from paper_2601_04185_b200.dist import shard_indices
+    mine = shard_indices(1000, rank, world, "interleaved")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    cnt = torch.tensor([float(len(mine))], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnt)
     if rank == 0:
-        line = {
-            "metric": "hyp×corr evals/s", "value": value, "unit": "evals/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
-            "data": "synthetic",
-            "config": {"workload": wl["name"], "queries_per_gpu": Q, "corrs_per_query": n,
-                       "n_sub": min(n, 10_000), "max_iterations": wl["max_iterations"],
-                       "miss_probability": wl["eta"],
-                       "l2": f"inputs {px_h.numel() * 8 * 3 / 1e9:.2f} GB/GPU (> 126 MB L2; no flush needed)",
-                       "parallelism": f"query-sharded x{world}, no collective"},
-            "queries_per_s": queries_per_s, "converged_frac": conv_rate,
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
-            "clocks": clocks, "gpu_launches": launches, "stage_ms_per_step": stage_ms,
-            "profiled_ms_per_step": ms_prof / args.steps,
-        }
+        print(json.dumps({"dryrun": True, "n_gpus": world, "max_over_ranks": float(t.item()),
+                          "queries_total": int(cnt.item()), "world_env": os.environ.get("WORLD_SIZE")}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(LIFT_WORKLOADS) + sorted(MAP_WORKLOADS),
+                    default="c3")
+    ap.add_argument("--queries", type=int, default=None, help="override queries per GPU")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="default line without the C1/C4/C5 configs")
+    args = ap.parse_args()
+    lifted = args.workload in LIFT_WORKLOADS
+    mapping = args.workload in MAP_WORKLOADS
+    wl = dict(MAP_WORKLOADS[args.workload] if mapping else
+              LIFT_WORKLOADS[args.workload] if lifted else WORKLOADS[args.workload])
+    if args.queries:
+        wl["queries"] = args.queries
+    if args.impl == "reference":
+        run_reference_arm(args, wl)
+        return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+
+    rank, world, local, backend, dist = dist_setup(args)
+    if os.environ.get("VISLOC_BENCH_DRYRUN"):
+        dry_run(args, rank, world, dist)
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    if lifted or mapping:
+        if mapping:
+            run_map_bench(args, wl, rank, world, local, dist)
+        else:
+            line = run_lift_bench(args, wl, rank, world, local, dist)
+            if line is not None:
+                print(json.dumps(line), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    line = bench_direct(args, wl, rank, world, local, dist, args.steps, "weak", not args.no_e2e)
+    if world > 1 and args.workload in ("c3", "c3a"):
+        # the literal BASELINE C3 batch (1000 queries) split across the ranks
+        strong = bench_direct(args, wl, rank, world, local, dist, args.steps, "strong", False, False)
+        if rank == 0:
+            line["strong"] = {k: strong[k] for k in ("value", "unit", "ms_per_step", "queries_per_s", "config",
+                                                     "roofline", "clocks")}
+    if world == 1 and args.workload == "c3" and not args.no_configs:
+        # the other BASELINE configs, each with its own value / e2e / roofline / cpu_baseline
+        configs = {}
+        for name in ("c1", "c4"):
+            sub = bench_direct(args, dict(WORKLOADS[name]), rank, world, local, dist, args.steps, "weak",
+                               not args.no_e2e)
+            configs[name] = _config_summary(sub)
+        sub = run_lift_bench(argparse.Namespace(**{**vars(args), "workload": "c5"}), dict(LIFT_WORKLOADS["c5"]),
+                             rank, world, local, dist)
+        configs["c5"] = _config_summary(sub)
+        line["configs"] = configs
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -1,11 +1,17 @@
 """Query sharding across GPUs (one process per GPU, torch.distributed plumbing).
 
 Queries are independent (reference SPEC: per-query determinism, no shared
-state), so the multi-GPU path partitions whole queries into contiguous
-shards with **no collective on the data path**; each rank runs the batched
-device estimator on its shard and results are gathered only for reporting
+state), so the multi-GPU path partitions whole queries across ranks with
+**no collective on the data path**; each rank runs the batched device
+estimator on its shard and results are gathered only for reporting
 (`all_gather_object` / a scalar max for timing).  Sharding never changes a
 query's result: each query keeps its own seed.
+
+Assignment is interleaved by default (rank r owns queries r, r + G, r + 2G,
+...): adaptive stopping makes per-query cost uneven, and neighbouring
+queries of a real batch (one image sequence) tend to be alike, so blocks
+would load some ranks with all the hard queries.  Contiguous
+blocks (`shard_range`) remain available.
 """
 
 from __future__ import annotations
@@ -20,23 +26,38 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def run_sharded(items, fn, group=None):
+def shard_indices(n: int, rank: int, world: int, mode: str = "interleaved") -> list[int]:
+    """Indices of the n items owned by `rank`: ``interleaved`` (r, r+G, ...) or
+    ``contiguous`` (the `shard_range` block).  Every item has exactly one owner."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    if mode == "interleaved":
+        return list(range(rank, n, world))
+    if mode == "contiguous":
+        lo, hi = shard_range(n, rank, world)
+        return list(range(lo, hi))
+    raise ValueError(f"mode must be 'interleaved' or 'contiguous', got {mode!r}")
+
+
+def run_sharded(items, fn, group=None, mode: str = "interleaved"):
     """Apply `fn(local_items) -> list` on this rank's shard; every rank gets all
     results in the original order (gathered as Python objects)."""
     import torch.distributed as dist
+    items = list(items)
     if not (dist.is_available() and dist.is_initialized()):
-        return list(fn(list(items)))
+        return list(fn(items))
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    lo, hi = shard_range(len(items), rank, world)
-    local = list(fn(list(items[lo:hi])))
-    if len(local) != hi - lo:
+    mine = shard_indices(len(items), rank, world, mode)
+    local = list(fn([items[i] for i in mine]))
+    if len(local) != len(mine):
         raise RuntimeError("fn must return one result per item")
     gathered = [None] * world
     dist.all_gather_object(gathered, local, group=group)
-    out = []
-    for part in gathered:
-        out.extend(part)
+    out = [None] * len(items)
+    for r, part in enumerate(gathered):
+        for i, v in zip(shard_indices(len(items), r, world, mode), part):
+            out[i] = v
     return out
 
 
@@ -184,7 +205,7 @@ def ransac_pnp_split(matches, intr, cfg, group=None, mode: str = "sum"):
     return run.end()[0]
 
 
-def localize_sharded(jobs, vmap, cfg, seeds=None, group=None, **kw):
+def localize_sharded(jobs, vmap, cfg, seeds=None, group=None, mode: str = "interleaved", **kw):
     """``localize_batch`` over all ranks' GPUs (each rank: its own shard, its own device)."""
     from .localizer import localize_batch
     jobs = list(jobs)
@@ -196,10 +217,10 @@ def localize_sharded(jobs, vmap, cfg, seeds=None, group=None, **kw):
             return []
         return localize_batch([j for j, _ in local], vmap, cfg, seeds=[s for _, s in local], **kw)
 
-    return run_sharded(pairs, fn, group)
+    return run_sharded(pairs, fn, group, mode)
 
 
-def ransac_pnp_sharded(queries, intrinsics, cfg, seeds=None, group=None):
+def ransac_pnp_sharded(queries, intrinsics, cfg, seeds=None, group=None, mode: str = "interleaved"):
     """``ransac_pnp_batch`` over all ranks' GPUs."""
     from .posest import ransac_pnp_batch
     queries = list(queries)
@@ -214,4 +235,4 @@ def ransac_pnp_sharded(queries, intrinsics, cfg, seeds=None, group=None):
         return ransac_pnp_batch([q for q, _, _ in local], [i for _, i, _ in local], cfg,
                                 seeds=[s for _, _, s in local])
 
-    return run_sharded(triples, fn, group)
+    return run_sharded(triples, fn, group, mode)

@@ -30,8 +30,8 @@ from .posest import (Match2D3D, PoseEstimate, RansacConfig, _estimates_from, _es
                      ransac_pnp_device)
 
 __all__ = [
-    "CONFIDENCE_THRESHOLD", "CorrespondenceField", "DepthMap", "DescriptorIndex", "EvalResult", "EvalThresholds",
-    "FieldPair", "evaluate",
+    "CONFIDENCE_THRESHOLD", "CorrespondenceField", "DepthMap", "DescriptorIndex", 
+    "FieldPair",
     "QuantizedDepthMap", "QueryJob", "dequantize_depth", "filter_matches_arrays", "interp_depth",
     "interp_depth_many", "LiftPlan", "lift", "lift_arrays", "localize", "localize_batch", "localize_pipelined",
     "serving_schedule",
@@ -754,57 +754,3 @@ def localize(query_job, vmap, cfg: RansacConfig, index=None, depth_cache=None,
     """Drop-in ``visloc.localizer.localize`` (localizer.py:200-238)."""
     return localize_batch([query_job], vmap, cfg, seeds=[cfg.seed], index=index, depth_cache=depth_cache,
                           confidence_threshold=confidence_threshold)[0]
-
-
-# ----------------------------------------------------------------------------- metrics
-# Recall bookkeeping over finished estimates (localizer.py:66-84, :244-305).  Not
-# on the hot path (SURVEY §2 marks it out of scope); kept so callers that score
-# their localisations with the reference's ``evaluate`` find it here.
-@dataclass(frozen=True)
-class EvalThresholds:
-    """(translation m, rotation deg) recall thresholds."""
-
-    pairs: tuple = ((0.25, 2.0), (0.5, 5.0), (1.0, 10.0))
-
-    def __post_init__(self):
-        for t, r in self.pairs:
-            if t <= 0 or r <= 0:
-                raise ValueError(f"thresholds must be positive, got ({t}, {r})")
-
-    @classmethod
-    def parse(cls, text: str) -> "EvalThresholds":
-        """"0.25:2,0.5:5,1:10" -> threshold pairs."""
-        return cls(tuple((float(t), float(r)) for t, r in (item.split(":") for item in text.split(","))))
-
-
-@dataclass
-class EvalResult:
-    thresholds: EvalThresholds
-    recalls: list
-    median_rotation_deg: float
-    median_translation_m: float
-    num_queries: int
-    num_failed: int
-    errors: list = field(default_factory=list, repr=False)
-
-
-def evaluate(estimates, thresholds: EvalThresholds) -> EvalResult:
-    """Recall per threshold pair and lower-median errors over the converged
-    estimates; a failed estimate counts against every threshold."""
-    if not estimates:
-        raise ValueError("evaluate needs at least one estimate")
-    errs = []
-    for est, gt in estimates:
-        if est.converged:
-            pe = pose_error(est.pose, gt)
-            errs.append((pe.translation_error_m, pe.rotation_error_deg))
-        else:
-            errs.append((math.nan, math.nan))
-    ok = [(t, r) for t, r in errs if not math.isnan(t)]
-    recalls = [sum(1 for t, r in ok if t <= tm and r <= rd) / len(errs) for tm, rd in thresholds.pairs]
-    if ok:
-        k = (len(ok) - 1) // 2
-        med_t, med_r = sorted(t for t, _ in ok)[k], sorted(r for _, r in ok)[k]
-    else:
-        med_t = med_r = math.nan
-    return EvalResult(thresholds, recalls, med_r, med_t, len(errs), len(errs) - len(ok), errs)

@@ -26,7 +26,6 @@ built with the input objects' classes.
 from __future__ import annotations
 
 import functools
-import io
 import math
 from dataclasses import dataclass, field
 
@@ -307,6 +306,11 @@ def reduce_map(vmap, keyframe_stride: int = 1, rgb_resolution_factor: float = 1.
         raise ValueError("resolution factors must be >= 1")
     if not 5 <= depth_bits <= 9:
         raise ValueError(f"depth_bits must be within 5..9, got {depth_bits}")
+    if rgb_resolution_factor != 1 or (vmap.rgb_codec != "png" and rgb_quality != 90):
+        # RGB re-encoding (mapstore.py:479-490, Pillow) is map storage, outside the
+        # hot path: this drop-in reduces depth and keeps RGB payloads
+        raise ValueError("RGB resampling / re-encoding is not part of this package (map storage, SURVEY §2); "
+                         "use rgb_resolution_factor=1 and the stored codec's quality")
     kept = set(sorted(e.id for e in vmap.entries)[::keyframe_stride])
     entries = [e for e in vmap.entries if e.id in kept]
     new_levels = 2 ** depth_bits - 1
@@ -319,29 +323,6 @@ def reduce_map(vmap, keyframe_stride: int = 1, rgb_resolution_factor: float = 1.
         qd = e.qdepth
         if qd is not None:
             qd = type(qd)(reduced[e.id], qd.d_min, qd.d_max, new_levels, qd.intrinsics)
-        identity_rgb = rgb_resolution_factor == 1 and (vmap.rgb_codec == "png" or rgb_quality == 90)
-        if identity_rgb:
-            payload, codec = e.rgb_payload, e.rgb_codec
-        else:
-            payload, codec = _resample_rgb(e.rgb_payload, vmap.rgb_codec, rgb_resolution_factor, rgb_quality)
-        out_entries.append(type(e)(id=e.id, pose=e.pose, intrinsics=e.intrinsics, rgb_payload=payload,
-                                   rgb_codec=codec, qdepth=qd, descriptor=np.array(e.descriptor, copy=True)))
+        out_entries.append(type(e)(id=e.id, pose=e.pose, intrinsics=e.intrinsics, rgb_payload=e.rgb_payload,
+                                   rgb_codec=e.rgb_codec, qdepth=qd, descriptor=np.array(e.descriptor, copy=True)))
     return type(vmap)(entries=out_entries, rgb_codec=vmap.rgb_codec, depth_codec=vmap.depth_codec)
-
-
-def _resample_rgb(payload: bytes, codec: str, factor: float, quality: int):
-    """Lanczos resample + re-encode (mapstore.py:479-490): map storage, host-side like the reference."""
-    from PIL import Image
-    with Image.open(io.BytesIO(payload)) as im0:
-        img = np.asarray(im0.convert("RGB"))
-    h, w = img.shape[:2]
-    new_w, new_h = max(1, round(w / factor)), max(1, round(h / factor))
-    im = Image.fromarray(img, mode="RGB")
-    if (new_w, new_h) != (w, h):
-        im = im.resize((new_w, new_h), Image.LANCZOS)
-    buf = io.BytesIO()
-    if codec == "png":
-        im.save(buf, format="PNG", optimize=False)
-    else:
-        im.save(buf, format="JPEG", quality=int(quality))
-    return buf.getvalue(), codec

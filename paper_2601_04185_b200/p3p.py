@@ -2,8 +2,10 @@
 
 ``p3p_solve_batch`` runs one GPU thread per minimal sample
 (``vl_p3p_solve_batch``): register-resident fp64 resultant quartic, Aberth
-root finding, Newton polish, Jacobi-SVD Procrustes, the 1e-8 rad bearing
-contract and per-sample dedup.  Output order matches the reference: by
+root finding, Newton polish, the reference's SVD Procrustes evaluated in
+closed form (three points are planar: map the world triangle's plane frame
+onto the camera triangle's, then the 2-D Procrustes rotation in that plane;
+``csrc/vl_p3p.cuh``), the 1e-8 rad bearing contract and per-sample dedup.  Output order matches the reference: by
 sample, then by ascending quartic root.
 
 ``sample_minimal_sets`` exposes the device reproduction of numpy's

@@ -5,7 +5,7 @@ import socket
 
 import pytest
 
-from paper_2601_04185_b200.dist import run_sharded, shard_range
+from paper_2601_04185_b200.dist import run_sharded, shard_indices, shard_range
 
 
 def test_shard_range_partitions():
@@ -16,6 +16,17 @@ def test_shard_range_partitions():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             sizes = [b - a for a, b in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_shard_indices_partition():
+    for n in (0, 1, 7, 1000, 1001):
+        for world in (1, 2, 3, 8):
+            for mode in ("interleaved", "contiguous"):
+                owned = [i for r in range(world) for i in shard_indices(n, r, world, mode)]
+                assert sorted(owned) == list(range(n))
+            assert shard_indices(n, world - 1, world, "interleaved") == list(range(world - 1, n, world))
+    with pytest.raises(ValueError):
+        shard_indices(4, 0, 2, "random")
 
 
 def _free_port():
@@ -37,6 +48,8 @@ def _worker(rank, world, port, q):
         return [x * x for x in local]
 
     out = run_sharded(list(range(11)), fn)
+    out_c = run_sharded(list(range(11)), lambda local: [-x for x in local], mode="contiguous")
+    assert out_c == [-x for x in range(11)]
     # timing reduction used by bench.py: max over ranks
     import torch
     t = torch.tensor([float(rank + 1)])
@@ -60,4 +73,25 @@ def test_run_sharded_gloo_world2():
     for rank, out, seen, tmax in res:
         assert out == [x * x for x in range(11)]
         assert tmax == 2.0
-    assert res[0][2] == list(range(0, 6)) and res[1][2] == list(range(6, 11))
+    assert res[0][2] == list(range(0, 11, 2)) and res[1][2] == list(range(1, 11, 2))  # interleaved
+
+
+def test_bench_gpus_spawns_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself
+    under torch.distributed.run: 2 ranks, one JSON line from rank 0 with
+    n_gpus 2, interleaved shards covering the 1000-query job, a max-over-ranks
+    time (VISLOC_BENCH_DRYRUN: the launcher and reductions only, on gloo)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["VISLOC_BENCH_DRYRUN"] = "1"
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2"], capture_output=True, text=True,
+                       env=env, timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["queries_total"] == 1000 and d["max_over_ranks"] == 2.0

@@ -4,10 +4,15 @@ The oracle runs on every host core (one process per problem); each problem
 draws its size, inlier ratio, noise, outlier weights, ground-truth pose,
 seed and RansacConfig (iterations, eta, batch size, tau, subset size) from
 one generator.  Prints the summary counts that DESIGN.md quotes.  GPU only:
-    python tools/parity_sweep.py [N] [seed] [batch]
+    python tools/parity_sweep.py [N] [seed] [batch|lowinlier]
 With "batch" every problem shares one RansacConfig (own seed, n <= 20001)
 and the GPU side is ONE ransac_pnp_batch call, so batches of more than 74
 problems run k_final one CTA per query (TMA-streamed full-set passes).
+"lowinlier" is the BASELINE C4 regime (posest.py:257-276, the LO-heavy
+ordered first-better scan): eps in {3, 5, 8} %, n in {2k, 5k, 10k}, 100k
+maximum samples, half the problems with the fixed-iteration eta = 1e-300 and
+half with the adaptive default eta = 1e-4, each half one ransac_pnp_batch.
+Every mode also compares the LO-call counts.
 """
 import json
 import multiprocessing as mp
@@ -48,15 +53,25 @@ def oracle_worker(p):
     px, X, w = problem(p)
     o = ransac(px, X, w, (700.0, 700.0, 350.0, 350.0), Config(**p["cfg"]))
     return dict(q=o.q.tolist(), t=o.t.tolist(), flags=np.packbits(o.inlier_flags).tobytes().hex(),
-                iterations=o.iterations, converged=bool(o.converged))
+                iterations=o.iterations, converged=bool(o.converged), lo_calls=int(o.lo_calls))
 
 
 def main():
     N = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     seed0 = int(sys.argv[2]) if len(sys.argv) > 2 else 7
-    batched = len(sys.argv) > 3 and sys.argv[3] == "batch"
+    mode = sys.argv[3] if len(sys.argv) > 3 else "single"
+    batched = mode in ("batch", "lowinlier")
     probs = [draw(k, seed0) for k in range(N)]
-    if batched:
+    if mode == "lowinlier":
+        for k, p in enumerate(probs):
+            r = np.random.default_rng([seed0, k, 2])
+            p["n"] = int(r.choice([2000, 5000, 10_000]))
+            p["outlier"] = float(1.0 - r.choice([0.03, 0.05, 0.08]))
+            p["sigma"] = float(r.choice([0.5, 1.0]))
+            p["cfg"] = dict(seed=p["cfg"]["seed"], max_iterations=100_000,
+                            miss_probability=1e-300 if k % 2 == 0 else 1e-4,
+                            reproj_threshold=12.0, max_scoring=10_000, batch_size=1000)
+    elif batched:
         for k, p in enumerate(probs):
             p["n"] = int(np.random.default_rng([seed0, k, 1]).choice([20, 201, 1000, 3001, 8000, 20001]))
             p["cfg"] = dict(seed=p["cfg"]["seed"], max_iterations=2000, miss_probability=1e-2,
@@ -68,20 +83,30 @@ def main():
         from oracle import geometry as og
         intr = vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
         gpu = []
-        if batched:
-            cfg = dict(probs[0]["cfg"])
-            cfg.pop("seed")
-            gpu = vl.ransac_pnp_batch([problem(p) for p in probs], intr, vl.RansacConfig(**cfg),
-                                      seeds=[p["cfg"]["seed"] for p in probs])
+        if batched:  # one batch per distinct config (lowinlier: fixed / adaptive halves)
+            gpu = [None] * N
+            groups = {}
+            for k, p in enumerate(probs):
+                key = tuple(sorted((a, b) for a, b in p["cfg"].items() if a != "seed"))
+                groups.setdefault(key, []).append(k)
+            for key, ks in groups.items():
+                res = vl.ransac_pnp_batch([problem(probs[k]) for k in ks], intr, vl.RansacConfig(**dict(key)),
+                                          seeds=[probs[k]["cfg"]["seed"] for k in ks])
+                for k, e in zip(ks, res):
+                    gpu[k] = e
         for p in ([] if batched else probs):
             px, X, w = problem(p)
             gpu.append(vl.ransac_pnp((px, X, w), intr, vl.RansacConfig(**p["cfg"])))
         ref = async_res.get()
-    stats = dict(mode="batch" if batched else "single", problems=N, same_iterations=0, same_converged=0, pose_within_tol=0, masks_identical=0,
-                 max_rot_deg=0.0, max_rel_t=0.0, flag_mismatch_points=0, near_tau_only=0)
+    stats = dict(mode=mode, problems=N, same_iterations=0, same_lo_calls=0, same_converged=0,
+                 pose_within_tol=0, masks_identical=0, max_rot_deg=0.0, max_rel_t=0.0, flag_mismatch_points=0,
+                 near_tau_only=0, lo_calls_total=0, iterations_total=0)
     from oracle.posest import errors_sq
     for p, e, o in zip(probs, gpu, ref):
         stats["same_iterations"] += int(e.iterations == o["iterations"])
+        stats["same_lo_calls"] += int(e.stats["lo_calls"] == o["lo_calls"])
+        stats["lo_calls_total"] += o["lo_calls"]
+        stats["iterations_total"] += o["iterations"]
         stats["same_converged"] += int(e.converged == o["converged"])
         if not o["converged"]:
             stats["pose_within_tol"] += 1
