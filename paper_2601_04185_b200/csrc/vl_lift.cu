@@ -335,6 +335,11 @@ __global__ void __launch_bounds__(kLiftThreads, VL_LIFT_WMINB) k_lift_write(Lift
     const int c = lane < wid ? a.warp_count[b * kLiftWarps + lane] : 0;
     pos += warp_sum(c);
   }
+  // X rows (24 B) of the warp's kept cells are staged in shared memory and
+  // stored as one contiguous run of doubles (3 fully coalesced stores per
+  // iteration instead of three 8-B stores at a 24-B stride)
+  __shared__ double sX[kLiftWarps][3 * 32];
+  double* xs = sX[wid];
   for (int i = 0; i < kLiftPerThread; ++i) {
     const int cell = cw + i * 32 + lane;
     if (cw + i * 32 >= cells) break;  // uniform across the warp
@@ -345,18 +350,25 @@ __global__ void __launch_bounds__(kLiftThreads, VL_LIFT_WMINB) k_lift_write(Lift
       keep = gate<T>(in.c, thr) && cell_eval<T>(S, a.depths, cell, in, mode, r);
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const int nk = __popc(m);
     if (keep) {
-      const int64_t p = pos + __popc(m & lt);
+      const int k = __popc(m & lt);
+      const int64_t p = pos + k;
+      xs[3 * k] = r.X[0];
+      xs[3 * k + 1] = r.X[1];
+      xs[3 * k + 2] = r.X[2];
       if (p < a.capacity) {
         reinterpret_cast<double2*>(a.px_out)[p] = make_double2(r.px[0], r.px[1]);
-        a.X_out[3 * p] = r.X[0];
-        a.X_out[3 * p + 1] = r.X[1];
-        a.X_out[3 * p + 2] = r.X[2];
         a.w_out[p] = r.w;
         if (a.entry_out) a.entry_out[p] = S.entry;
       }
     }
-    pos += __popc(m);
+    __syncwarp();
+    const int64_t lim = 3 * (a.capacity - pos);  // doubles of X_out still inside the capacity
+    for (int j = lane; j < 3 * nk; j += 32)
+      if (j < lim) a.X_out[3 * pos + j] = xs[j];
+    __syncwarp();
+    pos += nk;
   }
 }
 
