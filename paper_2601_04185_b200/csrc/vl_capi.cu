@@ -892,17 +892,28 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
         return fail(c, VL_ERR_INVALID, "depth " + std::to_string(d) + ": bad map");
     }
   const size_t seg_bytes = nseg * sizeof(vl_lift_segment), dep_bytes = (mode == 0 ? ndepth : 0) * sizeof(vl_lift_depth);
-  const size_t meta = seg_bytes + dep_bytes + nseg * sizeof(int64_t);  // all multiples of 8
+  const size_t sob_bytes = ((size_t)nblk * sizeof(int) + 7) & ~(size_t)7;  // tile -> segment table
+  const size_t meta = seg_bytes + dep_bytes + nseg * sizeof(int64_t) + sob_bytes;  // all multiples of 8
+  // zeroed by k_lift_prep: seg_flags [nseg] int, the scan's ticket
+  const size_t zflags = meta, zend = zflags + (size_t)(nseg + 1) * sizeof(int);
+  const int64_t nchunk = (nblk + 1023) / 1024;
   const size_t host_bytes = meta + (nseg + 1) * sizeof(int64_t) + nseg * sizeof(int) + 64;
   int rc;
-  if ((rc = ensure(c, c->lift_meta, meta + nseg * sizeof(int))) || (rc = ensure(c, c->lift_blk_count, nblk * 9 * sizeof(int))) ||
-      (rc = ensure(c, c->lift_blk_off, nblk * sizeof(int64_t))) || (rc = ensure(c, c->lift_seg_off, (nseg + 1) * sizeof(int64_t))) ||
+  if ((rc = ensure(c, c->lift_meta, zend)) || (rc = ensure(c, c->lift_blk_count, nblk * 9 * sizeof(int))) ||
+      (rc = ensure(c, c->lift_blk_off, (nblk + nchunk) * sizeof(int64_t))) || (rc = ensure(c, c->lift_seg_off, (nseg + 1) * sizeof(int64_t))) ||
       (rc = ensure_host(c, host_bytes)))
     return rc;
   char* h = (char*)c->h_pinned;
   std::memcpy(h, segs, seg_bytes);
   if (dep_bytes) std::memcpy(h + seg_bytes, depths, dep_bytes);
   std::memcpy(h + seg_bytes + dep_bytes, blk0.data(), nseg * sizeof(int64_t));
+  {
+    int* sob = (int*)(h + seg_bytes + dep_bytes + nseg * sizeof(int64_t));
+    for (int s = 0; s < nseg; ++s) {
+      const int64_t e = s + 1 < nseg ? blk0[s + 1] : nblk;
+      for (int64_t k = blk0[s]; k < e; ++k) sob[k] = s;
+    }
+  }
   char* d = (char*)c->lift_meta.p;
   int64_t* hoff = (int64_t*)(h + meta);
   int* hflags = (int*)(h + meta + (nseg + 1) * sizeof(int64_t));
@@ -912,18 +923,21 @@ extern "C" int vl_lift(vl_ctx* c, const vl_lift_segment* segs, int32_t nseg, con
   VL_CUDA(c, cudaHostGetDevicePointer(&d_hflags, hflags, 0));
   // metadata pulled by a kernel from mapped pinned memory and results pushed
   // back the same way: no copy-engine transfers queued on this stream
-  c->launches += launch_lift_prep(d, d_h, meta, (int*)(d + meta), nseg, st);
+  c->launches += launch_lift_prep(d, d_h, meta, (int*)(d + zflags), (int)((zend - zflags) / sizeof(int)), st);
   LiftArgs a;
   a.segs = (const LiftSeg*)d;
   a.nseg = nseg;
   a.depths = (const LiftDepth*)(d + seg_bytes);
   a.seg_blk0 = (const int64_t*)(d + seg_bytes + dep_bytes);
+  a.seg_of_blk = (const int*)(d + seg_bytes + dep_bytes + nseg * sizeof(int64_t));
   a.nblk = nblk;
   a.blk_count = (int*)c->lift_blk_count.p;
   a.warp_count = a.blk_count + nblk;
   a.blk_off = (int64_t*)c->lift_blk_off.p;
   a.seg_off = (int64_t*)c->lift_seg_off.p;
-  a.seg_flags = (int*)(d + meta);
+  a.seg_flags = (int*)(d + zflags);
+  a.scan_ticket = (int*)(d + zflags) + nseg;
+  a.chunk_off = (int64_t*)c->lift_blk_off.p + nblk;
   a.seg_off_host = (int64_t*)d_hoff;
   a.seg_flags_host = (int*)d_hflags;
   a.threshold = threshold;

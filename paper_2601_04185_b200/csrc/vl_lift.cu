@@ -84,35 +84,175 @@ __device__ __forceinline__ void lift_point(const LiftDepth& D, double u, double 
   for (int j = 0; j < 3; ++j) X[j] = dadd(dadd(dmul(v0, D.R[j]), dmul(v1, D.R[3 + j])), dmul(v2, D.R[6 + j]));
 }
 
-struct CellResult {
-  double px[2];
-  double X[3];
-  double w;
+// Block-uniform parameters of a segment and of its depth map, held in
+// registers for the whole block (loaded once with uniform __ldg: the
+// generic-pointer struct copies of the first version went through local
+// memory and cost an LD per use).
+struct SegP {
+  int gw, cells, entry, direction, layout, depth;
+  double scale_x, scale_y;
+  const void* targets;
+  const void* conf;
 };
 
-// One field cell: confidence + target, in the field's own dtype for the gate.
-template <typename T>
-struct CellIn {
-  T c;
-  double tx, ty;
+struct DepP {
+  int w, h;
+  double wm1, hm1, wm2, hm2;  // w - 1, h - 1, w - 2, h - 2 as doubles (clamp bounds)
+  const void* values;
+  const uint8_t* valid;
+  const float* lut;
+  double fx, fy, cx, cy, sxd, syd;
 };
 
+__device__ __forceinline__ SegP load_seg(const LiftSeg* g) {
+  SegP S;
+  S.gw = __ldg(&g->gw);
+  S.cells = S.gw * __ldg(&g->gh);
+  S.entry = __ldg(&g->entry);
+  S.direction = __ldg(&g->direction);
+  S.layout = __ldg(&g->layout);
+  S.depth = __ldg(&g->depth);
+  S.scale_x = __ldg(&g->scale_x);
+  S.scale_y = __ldg(&g->scale_y);
+  S.targets = (const void*)__ldg((const unsigned long long*)&g->targets);
+  S.conf = (const void*)__ldg((const unsigned long long*)&g->confidence);
+  return S;
+}
+
+__device__ __forceinline__ DepP load_dep(const LiftDepth* g) {
+  DepP D;
+  D.w = __ldg(&g->w);
+  D.h = __ldg(&g->h);
+  D.wm1 = (double)(D.w - 1);
+  D.hm1 = (double)(D.h - 1);
+  D.wm2 = (double)(D.w - 2);
+  D.hm2 = (double)(D.h - 2);
+  D.values = (const void*)__ldg((const unsigned long long*)&g->values);
+  D.valid = (const uint8_t*)__ldg((const unsigned long long*)&g->valid);
+  D.lut = (const float*)__ldg((const unsigned long long*)&g->lut);
+  D.fx = __ldg(&g->fx);
+  D.fy = __ldg(&g->fy);
+  D.cx = __ldg(&g->cx);
+  D.cy = __ldg(&g->cy);
+  D.sxd = __ldg(&g->sx_depth);
+  D.syd = __ldg(&g->sy_depth);
+  return D;
+}
+
+// Depth taps per stored kind (kind is a template parameter: the inner loops
+// carry no switch).  tap_ok: validity only (count pass: no value / LUT load).
+template <int KIND>
+__device__ __forceinline__ bool tap_ok(const DepP& D, int idx) {
+  if (KIND == kDepthF32 || KIND == kDepthF16) return __ldg(D.valid + idx) != 0;
+  if (KIND == kDepthCode8) return __ldg((const uint8_t*)D.values + idx) != 0;
+  return __ldg((const uint16_t*)D.values + idx) != 0;
+}
+
+template <int KIND>
+__device__ __forceinline__ float tap_val(const DepP& D, int idx, bool& ok) {
+  if (KIND == kDepthF32) {
+    ok = __ldg(D.valid + idx) != 0;
+    return __ldg((const float*)D.values + idx);
+  }
+  if (KIND == kDepthF16) {
+    ok = __ldg(D.valid + idx) != 0;
+    return __half2float(__ldg((const __half*)D.values + idx));
+  }
+  const int c = KIND == kDepthCode8 ? (int)__ldg((const uint8_t*)D.values + idx)
+                                    : (int)__ldg((const uint16_t*)D.values + idx);
+  ok = c > 0;
+  return __ldg(D.lut + c);
+}
+
+// Bilinear sample position (localizer.py:97-105): clamped base tap and
+// fractions, `inside` = the reference's inside test.
+struct Bilin {
+  int i00;
+  double fx, fy;
+  bool inside;
+};
+
+__device__ __forceinline__ Bilin bilin(const DepP& D, double px, double py) {
+  const double x = dsub(px, 0.5), y = dsub(py, 0.5);
+  Bilin b;
+  b.inside = (x >= 0) && (x <= D.wm1) && (y >= 0) && (y <= D.hm1);
+  // x0 = clip(floor(x), 0, w - 2) kept as a double: x - x0 needs no int -> double conversion
+  const double xf = fmin(fmax(floor(x), 0.0), D.wm2);
+  const double yf = fmin(fmax(floor(y), 0.0), D.hm2);
+  b.fx = fmin(fmax(dsub(x, xf), 0.0), 1.0);
+  b.fy = fmin(fmax(dsub(y, yf), 0.0), 1.0);
+  b.i00 = (int)yf * D.w + (int)xf;
+  return b;
+}
+
+template <int KIND>
+__device__ __forceinline__ bool interp_ok(const DepP& D, double px, double py) {
+  const Bilin b = bilin(D, px, py);
+  if (!b.inside) return false;
+  return tap_ok<KIND>(D, b.i00) && tap_ok<KIND>(D, b.i00 + 1) && tap_ok<KIND>(D, b.i00 + D.w) &&
+         tap_ok<KIND>(D, b.i00 + D.w + 1);
+}
+
+// value: d00(1-fx)(1-fy) + d10 fx(1-fy) + d01(1-fx)fy + d11 fx fy, left to right (localizer.py:106-112)
+template <int KIND>
+__device__ __forceinline__ bool interp_val(const DepP& D, double px, double py, double& d) {
+  const Bilin b = bilin(D, px, py);
+  if (!b.inside) return false;
+  bool v00, v10, v01, v11;
+  const double d00 = tap_val<KIND>(D, b.i00, v00);
+  const double d10 = tap_val<KIND>(D, b.i00 + 1, v10);
+  const double d01 = tap_val<KIND>(D, b.i00 + D.w, v01);
+  const double d11 = tap_val<KIND>(D, b.i00 + D.w + 1, v11);
+  if (!(v00 && v10 && v01 && v11)) return false;
+  const double gx = dsub(1.0, b.fx), gy = dsub(1.0, b.fy);
+  double s = dmul(dmul(d00, gx), gy);
+  s = dadd(s, dmul(dmul(d10, b.fx), gy));
+  s = dadd(s, dmul(dmul(d01, gx), b.fy));
+  s = dadd(s, dmul(dmul(d11, b.fx), b.fy));
+  d = s;
+  return true;
+}
+
+// db -> query direct lookup index: int(src * depth/image) clipped (localizer.py:164-165)
+__device__ __forceinline__ int direct_idx(const DepP& D, double sx, double sy) {
+  const double fxi = floor(dmul(sx, D.sxd)), fyi = floor(dmul(sy, D.syd));
+  const int ix = (int)fmin(fmax(fxi, 0.0), D.wm1);
+  const int iy = (int)fmin(fmax(fyi, 0.0), D.hm1);
+  return iy * D.w + ix;
+}
+
+// world point (xc - t) @ R for pixel (u, v) at depth d in the db camera
+__device__ __forceinline__ void lift_point(const DepP& D, const double* R, const double* t, double u, double v,
+                                           double d, double* X) {
+  const double xc0 = dmul(__ddiv_rn(dsub(u, D.cx), D.fx), d);
+  const double xc1 = dmul(__ddiv_rn(dsub(v, D.cy), D.fy), d);
+  const double v0 = dsub(xc0, t[0]), v1 = dsub(xc1, t[1]), v2 = dsub(d, t[2]);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) X[j] = dadd(dadd(dmul(v0, R[j]), dmul(v1, R[3 + j])), dmul(v2, R[6 + j]));
+}
+
+// One field cell in the field's own dtype (IMLC records are f32).  `srec`:
+// the block's records staged in shared memory (cell c0 first), or null.
 template <typename T>
-__device__ __forceinline__ CellIn<T> load_cell(const LiftSeg& S, int cell) {
-  CellIn<T> in;
-  if (S.layout == kLayoutImlc) {
+__device__ __forceinline__ void load_cell(const SegP& S, int cell, T& c, double& tx, double& ty,
+                                          const float* srec = nullptr, int c0 = 0) {
+  if (srec) {
+    const float* r = srec + 3 * (cell - c0);
+    c = (T)r[2];
+    tx = (double)r[0];
+    ty = (double)r[1];
+  } else if (S.layout == kLayoutImlc) {
     // IMLC record (x f32, y f32, conf f32), matchio.py:18-19
     const float* r = (const float*)S.targets + 3 * (int64_t)cell;
-    in.c = (T)r[2];
-    in.tx = (double)r[0];
-    in.ty = (double)r[1];
+    c = (T)__ldg(r + 2);
+    tx = (double)__ldg(r);
+    ty = (double)__ldg(r + 1);
   } else {
     const T* tg = (const T*)S.targets;
-    in.c = ((const T*)S.confidence)[cell];
-    in.tx = (double)tg[2 * (int64_t)cell];
-    in.ty = (double)tg[2 * (int64_t)cell + 1];
+    c = __ldg((const T*)S.conf + cell);
+    tx = (double)__ldg(tg + 2 * (int64_t)cell);
+    ty = (double)__ldg(tg + 2 * (int64_t)cell + 1);
   }
-  return in;
 }
 
 // gate (matchio.py:211): (conf >= thr) & (conf > 0), compared in the field
@@ -120,76 +260,6 @@ __device__ __forceinline__ CellIn<T> load_cell(const LiftSeg& S, int cell) {
 template <typename T>
 __device__ __forceinline__ bool gate(T c, T thr) {
   return (c >= thr) && (c > (T)0);
-}
-
-__device__ __forceinline__ void source_px(const LiftSeg& S, int cell, double& sx, double& sy) {
-  const int row = cell / S.gw, col = cell - row * S.gw;
-  sx = dmul((double)col + 0.5, S.scale_x);
-  sy = dmul((double)row + 0.5, S.scale_y);
-}
-
-__device__ __forceinline__ void direct_tap(const LiftDepth& D, double sx, double sy, int64_t& idx) {
-  const double fxi = floor(dmul(sx, D.sx_depth)), fyi = floor(dmul(sy, D.sy_depth));
-  const int ix = (int)fmin(fmax(fxi, 0.0), (double)(D.w - 1));
-  const int iy = (int)fmin(fmax(fyi, 0.0), (double)(D.h - 1));
-  idx = (int64_t)iy * D.w + ix;
-}
-
-// Evaluate one gated cell.  mode 0: lift (false when the depth is invalid);
-// mode 1: gate only (px = source, X[0..1] = target, X[2] = flat cell index).
-template <typename T>
-__device__ __forceinline__ bool cell_eval(const LiftSeg& S, const LiftDepth* depths, int cell, const CellIn<T>& in,
-                                          int mode, CellResult& r) {
-  double sx, sy;
-  source_px(S, cell, sx, sy);
-  r.w = (double)in.c;
-  if (mode == 1) {
-    r.px[0] = sx;
-    r.px[1] = sy;
-    r.X[0] = in.tx;
-    r.X[1] = in.ty;
-    r.X[2] = (double)cell;
-    return true;
-  }
-  const LiftDepth& D = depths[S.depth];
-  double d;
-  if (S.direction == 0) {
-    // db -> query: direct lookup at the db cell (localizer.py:164-168)
-    int64_t idx;
-    direct_tap(D, sx, sy, idx);
-    bool ok;
-    d = (double)depth_value(D, idx, ok);
-    if (!ok) return false;
-    lift_point(D, sx, sy, d, r.X);
-    r.px[0] = in.tx;
-    r.px[1] = in.ty;
-  } else {
-    // query -> db: bilinear at the subpixel target (localizer.py:181-196)
-    if (!interp_depth(D, dmul(in.tx, D.sx_depth), dmul(in.ty, D.sy_depth), d)) return false;
-    lift_point(D, in.tx, in.ty, d, r.X);
-    r.px[0] = sx;
-    r.px[1] = sy;
-  }
-  return true;
-}
-
-// Keep decision only (count pass): gate + depth validity, no lift arithmetic.
-template <typename T>
-__device__ __forceinline__ bool cell_keep(const LiftSeg& S, const LiftDepth* depths, int cell, const CellIn<T>& in,
-                                          int mode) {
-  if (mode == 1) return true;
-  const LiftDepth& D = depths[S.depth];
-  double sx, sy;
-  if (S.direction == 0) {
-    source_px(S, cell, sx, sy);
-    int64_t idx;
-    direct_tap(D, sx, sy, idx);
-    bool ok;
-    (void)depth_value(D, idx, ok);
-    return ok;
-  }
-  double d;
-  return interp_depth(D, dmul(in.tx, D.sx_depth), dmul(in.ty, D.sy_depth), d);
 }
 
 // IMLC content rules of CorrespondenceField.__post_init__ (matchio.py:99-109)
@@ -200,15 +270,121 @@ __device__ __forceinline__ int content_flags(float c, double tx, double ty) {
   return f;
 }
 
-__device__ __forceinline__ int find_seg(const int64_t* seg_blk0, int nseg, int64_t b) {
-  int lo = 0, hi = nseg - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (seg_blk0[mid] <= b) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
+// Source pixel of a cell: ((col + 0.5) sx, (row + 0.5) sy) (matchio.py:215-216)
+__device__ __forceinline__ void source_px(const SegP& S, int row, int col, double& sx, double& sy) {
+  sx = dmul((double)col + 0.5, S.scale_x);
+  sy = dmul((double)row + 0.5, S.scale_y);
 }
+
+// Lane's (row, col) walk: cell advances by 32 per iteration.
+struct CellWalk {
+  int cell, row, col;
+  __device__ __forceinline__ CellWalk(int c0, int gw) : cell(c0), row(c0 / gw), col(c0 - (c0 / gw) * gw) {}
+  __device__ __forceinline__ void next(int gw) {
+    cell += 32;
+    col += 32;
+    while (col >= gw) {
+      col -= gw;
+      ++row;
+    }
+  }
+};
+
+// KIND = kGateOnly: mode 1 (gate only, no depth)
+constexpr int kGateOnly = 4;
+
+// db -> query segments: the depth tap and the normalised ray of a cell
+// depend only on its column and row (localizer.py:164-176), so a block
+// computes them once per column / row — the same fp64 operations, cached —
+// instead of once per cell: ix = clip(int(sx * dw / W)), xn = (sx - cx) / fx
+// (the division), likewise for rows.  Used when the grid is at most
+// kTabCols wide and the block spans at most kTabRows rows.
+constexpr int kTabCols = 512, kTabRows = 72;
+
+struct Dir0Tab {
+  const int* ix;       // [gw]
+  const int* iy;       // [rows of the block], row0 first
+  const double* xn;    // [gw]  (write pass)
+  const double* yn;    // [rows]
+  int row0;
+  bool on;             // tables filled (else the per-cell path)
+};
+
+// All threads call it; the caller's next __syncthreads publishes the tables.
+// Returns false (tables unused) when the segment does not qualify.
+__device__ __forceinline__ bool fill_dir0_tab(const SegP& S, const DepP& D, int c0, bool with_n, int* ix, int* iy,
+                                              double* xn, double* yn, Dir0Tab& tab) {
+  const int row0 = c0 / S.gw, row1 = (min(S.cells, c0 + kLiftBlockCells) - 1) / S.gw;
+  tab.on = false;
+  if (S.direction != 0 || S.gw > kTabCols || row1 - row0 + 1 > kTabRows) return false;
+  for (int col = threadIdx.x; col < S.gw; col += blockDim.x) {
+    const double sx = dmul((double)col + 0.5, S.scale_x);
+    ix[col] = (int)fmin(fmax(floor(dmul(sx, D.sxd)), 0.0), (double)(D.w - 1));
+    if (with_n) xn[col] = __ddiv_rn(dsub(sx, D.cx), D.fx);
+  }
+  for (int r = threadIdx.x; r <= row1 - row0; r += blockDim.x) {
+    const double sy = dmul((double)(row0 + r) + 0.5, S.scale_y);
+    iy[r] = (int)fmin(fmax(floor(dmul(sy, D.syd)), 0.0), (double)(D.h - 1));
+    if (with_n) yn[r] = __ddiv_rn(dsub(sy, D.cy), D.fy);
+  }
+  tab.ix = ix;
+  tab.iy = iy;
+  tab.xn = xn;
+  tab.yn = yn;
+  tab.row0 = row0;
+  tab.on = true;
+  return true;
+}
+
+// world point from the normalised ray (xn, yn) at depth d: identical to
+// lift_point's arithmetic with the quotients precomputed
+__device__ __forceinline__ void lift_point_n(const double* R, const double* t, double xn, double yn, double d,
+                                             double* X) {
+  const double xc0 = dmul(xn, d), xc1 = dmul(yn, d);
+  const double v0 = dsub(xc0, t[0]), v1 = dsub(xc1, t[1]), v2 = dsub(d, t[2]);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) X[j] = dadd(dadd(dmul(v0, R[j]), dmul(v1, R[3 + j])), dmul(v2, R[6 + j]));
+}
+
+// The block's 2048 IMLC records (24 KB, 12 B each) are pulled into shared
+// memory by ONE bulk async copy (cp.async.bulk, TMA engine, mbarrier
+// completion) instead of 3 dependent 4-B loads per lane per iteration: the
+// count pass was latency bound (ncu: 1.8 TB/s, 22 % of DRAM peak, IPC 2.3).
+// Records of a 16-B aligned segment start 16-B aligned for every block
+// (2048 x 12 B = 24576 B); a sub-16-B tail of the last block is copied by
+// plain loads.  Returns srec, or null (planar fields / unaligned records:
+// the global path).  Every thread of the block must call it; it ends with a
+// block barrier on both paths.
+__device__ __forceinline__ unsigned lift_smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ const float* stage_records(const SegP& S, int c0, float* srec, uint64_t* bar) {
+  if (S.layout != kLayoutImlc || (reinterpret_cast<uintptr_t>(S.targets) & 15) || c0 >= S.cells) {
+    __syncthreads();  // block-uniform: callers rely on this barrier either way
+    return nullptr;
+  }
+  const int ncell = min(kLiftBlockCells, S.cells - c0);
+  const float* src = (const float*)S.targets + 3 * (int64_t)c0;
+  const unsigned bytes = (unsigned)ncell * 12u, bulk = bytes & ~15u;
+  const unsigned b = lift_smem_u32(bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bulk) : "memory");
+    if (bulk)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(lift_smem_u32(srec)), "l"(src), "r"(bulk), "r"(b) : "memory");
+  }
+  for (unsigned k = bulk / 4 + threadIdx.x; k < bytes / 4; k += blockDim.x) srec[k] = __ldg(src + k);
+  __syncthreads();  // barrier initialised, tail stored
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "LIFT_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra LIFT_WAIT_%=;\n}" ::"r"(b)
+      : "memory");
+  return srec;
+}
+
 
 // A block covers kLiftBlockCells consecutive cells of one segment; warp w owns
 // the contiguous run [w*256, (w+1)*256) of them and iteration i handles cells
@@ -216,32 +392,88 @@ __device__ __forceinline__ int find_seg(const int64_t* seg_blk0, int nseg, int64
 // consecutive addresses and the write pass can rank cells inside each warp
 // with no block barrier (per-warp counts come from this pass).
 #ifndef VL_LIFT_CMINB
-#define VL_LIFT_CMINB 8  // min resident CTAs of the count pass (register cap; 8 measured best)
+#define VL_LIFT_CMINB 6  // min resident CTAs of the count pass (40 registers: no spills)
 #endif
 #ifndef VL_LIFT_WMINB
-#define VL_LIFT_WMINB 5  // same for the write pass (5 measured best; small spills cost less than the occupancy)
+#define VL_LIFT_WMINB 5  // same for the write pass
 #endif
 constexpr int kLiftWarps = kLiftThreads / 32;
 constexpr int kLiftWarpCells = kLiftBlockCells / kLiftWarps;  // 256
 
+// A block covers kLiftBlockCells consecutive cells of one segment; warp w owns
+// the contiguous run [w*256, (w+1)*256) of them and iteration i handles cells
+// w*256 + i*32 + lane, so every load and output store of a warp touches
+// consecutive addresses and the write pass can rank cells inside each warp
+// with no block barrier (per-warp counts come from the count pass).
+template <typename T, int DIR, int KIND>
+__device__ __forceinline__ int count_run(const SegP& S, const DepP& D, T thr, int cw, int lane, int& flags,
+                                         const float* srec, int c0, const Dir0Tab tab) {
+  int cnt = 0;
+  CellWalk cwk(cw + lane, S.gw);
+#pragma unroll 2
+  for (int i = 0; i < kLiftPerThread; ++i, cwk.next(S.gw)) {
+    if (cwk.cell >= S.cells) break;
+    T c;
+    double tx, ty;
+    load_cell<T>(S, cwk.cell, c, tx, ty, srec, c0);
+    if (S.layout == kLayoutImlc) flags |= content_flags((float)c, tx, ty);
+    bool keep = gate<T>(c, thr);
+    if (keep && KIND != kGateOnly) {
+      if (DIR == 0) {
+        if (tab.on) {
+          keep = tap_ok<KIND>(D, tab.iy[cwk.row - tab.row0] * D.w + tab.ix[cwk.col]);
+        } else {
+          double sx, sy;
+          source_px(S, cwk.row, cwk.col, sx, sy);
+          keep = tap_ok<KIND>(D, direct_idx(D, sx, sy));
+        }
+      } else {
+        keep = interp_ok<KIND>(D, dmul(tx, D.sxd), dmul(ty, D.syd));
+      }
+    }
+    cnt += keep ? 1 : 0;
+  }
+  return cnt;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kLiftThreads, VL_LIFT_CMINB) k_lift_count(LiftArgs a, int mode) {
   const int64_t b = blockIdx.x;
-  const int s = find_seg(a.seg_blk0, a.nseg, b);
-  const LiftSeg S = a.segs[s];
-  const int cells = S.gw * S.gh;
+  const int s = __ldg(a.seg_of_blk + b);  // host-built tile -> segment table (no per-thread binary search)
+  const SegP S = load_seg(a.segs + s);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int cw = (int)(b - a.seg_blk0[s]) * kLiftBlockCells + wid * kLiftWarpCells;
+  const int c0 = (int)(b - a.seg_blk0[s]) * kLiftBlockCells;
+  const int cw = c0 + wid * kLiftWarpCells;
   const T thr = (T)a.threshold;
+  __shared__ __align__(16) float srec_buf[3 * kLiftBlockCells];
+  __shared__ __align__(8) uint64_t sbar;
+  __shared__ int s_ix[kTabCols], s_iy[kTabRows];
+  DepP D{};
+  int kind = kGateOnly;
+  Dir0Tab tab;
+  tab.on = false;
+  if (mode == 0) {
+    const LiftDepth* gd = a.depths + S.depth;
+    D = load_dep(gd);
+    kind = __ldg(&gd->kind);
+    fill_dir0_tab(S, D, c0, false, s_ix, s_iy, nullptr, nullptr, tab);
+  }
+  const float* srec = stage_records(S, c0, srec_buf, &sbar);  // its barrier also publishes the tables
+  Dir0Tab notab = tab;
+  notab.on = false;
   int cnt = 0, flags = 0;
-#pragma unroll 4
-  for (int i = 0; i < kLiftPerThread; ++i) {
-    const int cell = cw + i * 32 + lane;
-    if (cell < cells) {
-      const CellIn<T> in = load_cell<T>(S, cell);
-      if (S.layout == kLayoutImlc) flags |= content_flags((float)in.c, in.tx, in.ty);
-      if (gate<T>(in.c, thr) && cell_keep<T>(S, a.depths, cell, in, mode)) ++cnt;
+  if (cw < S.cells) {
+#define VL_LIFT_COUNT(K)                                                                         \
+  cnt = S.direction == 0 ? count_run<T, 0, K>(S, D, thr, cw, lane, flags, srec, c0, tab)         \
+                         : count_run<T, 1, K>(S, D, thr, cw, lane, flags, srec, c0, notab);
+    switch (kind) {
+      case kDepthF32: VL_LIFT_COUNT(kDepthF32) break;
+      case kDepthF16: VL_LIFT_COUNT(kDepthF16) break;
+      case kDepthCode8: VL_LIFT_COUNT(kDepthCode8) break;
+      case kDepthCode16: VL_LIFT_COUNT(kDepthCode16) break;
+      default: cnt = count_run<T, 0, kGateOnly>(S, D, thr, cw, lane, flags, srec, c0, notab); break;
     }
+#undef VL_LIFT_COUNT
   }
   __shared__ int wsum[kLiftWarps];
   __shared__ int wflag[kLiftWarps];
@@ -264,43 +496,76 @@ __global__ void __launch_bounds__(kLiftThreads, VL_LIFT_CMINB) k_lift_count(Lift
   }
 }
 
-// One CTA: exclusive scan of block counts, segment offsets, total.
-__global__ void __launch_bounds__(1024) k_lift_scan(LiftArgs a) {
+// Exclusive scan of the block counts: one 1024-thread CTA per chunk of 1024
+// blocks writes chunk-relative offsets and the chunk total; the last CTA to
+// finish (atomic ticket) scans the chunk totals and writes the segment
+// offsets, the total and the host mirrors.  (A single CTA walking 35840
+// blocks took 43-85 us at C5.)
+constexpr int kScanChunk = 1024;
+
+__global__ void __launch_bounds__(kScanChunk) k_lift_scan(LiftArgs a) {
   __shared__ int64_t wtot[32];
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
+  __shared__ int s_last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int64_t base = 0; base < a.nblk; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const int64_t v = i < a.nblk ? a.blk_count[i] : 0;
-    int64_t x = v;
+  const int64_t i = (int64_t)blockIdx.x * kScanChunk + threadIdx.x;
+  const int64_t v = i < a.nblk ? a.blk_count[i] : 0;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wtot[wid] = x;
+  __syncthreads();
+  int64_t wb = 0, tot = 0;
+  for (int w = 0; w < 32; ++w) {
+    const int64_t t = wtot[w];
+    if (w < wid) wb += t;
+    tot += t;
+  }
+  if (i < a.nblk) a.blk_off[i] = wb + x - v;
+  if (threadIdx.x == 0) a.chunk_off[blockIdx.x] = tot;  // the chunk total for now
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.scan_ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // chunk totals -> exclusive chunk offsets: one block-wide scan per 1024 chunks
+  int64_t carry = 0;
+  for (unsigned k0 = 0; k0 < gridDim.x; k0 += kScanChunk) {
+    const unsigned k = k0 + threadIdx.x;
+    const int64_t cv = k < gridDim.x ? __ldcg(a.chunk_off + k) : 0;
+    int64_t cx = cv;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int64_t y = __shfl_up_sync(0xffffffffu, cx, o);
+      if (lane >= o) cx += y;
     }
-    if (lane == 31) wtot[wid] = x;
     __syncthreads();
-    int64_t wb = 0, tot = 0;
+    if (lane == 31) wtot[wid] = cx;
+    __syncthreads();
+    int64_t cb = 0, ct = 0;
     for (int w = 0; w < 32; ++w) {
-      if (w < wid) wb += wtot[w];
-      tot += wtot[w];
+      const int64_t t = wtot[w];
+      if (w < wid) cb += t;
+      ct += t;
     }
-    if (i < a.nblk) a.blk_off[i] = carry + wb + x - v;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-  for (int s = threadIdx.x; s < a.nseg; s += 1024) {
-    const int64_t o = a.blk_off[a.seg_blk0[s]];
-    a.seg_off[s] = o;
-    if (a.seg_off_host) a.seg_off_host[s] = o;
-    if (a.seg_flags_host) a.seg_flags_host[s] = a.seg_flags ? a.seg_flags[s] : 0;
+    if (k < gridDim.x) a.chunk_off[k] = carry + cb + cx - cv;
+    carry += ct;
   }
   if (threadIdx.x == 0) {
     a.seg_off[a.nseg] = carry;
     if (a.seg_off_host) a.seg_off_host[a.nseg] = carry;
+  }
+  __threadfence_block();
+  __syncthreads();
+  for (int s = threadIdx.x; s < a.nseg; s += kScanChunk) {
+    const int64_t b0 = a.seg_blk0[s];
+    const int64_t o = __ldcg(a.chunk_off + b0 / kScanChunk) + __ldcg(a.blk_off + b0);
+    a.seg_off[s] = o;
+    if (a.seg_off_host) a.seg_off_host[s] = o;
+    if (a.seg_flags_host) a.seg_flags_host[s] = a.seg_flags ? __ldcg(a.seg_flags + s) : 0;
   }
 }
 
@@ -318,65 +583,152 @@ int launch_lift_prep(void* dst, const void* src_host, size_t bytes, int* zero, i
   return 1;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kLiftThreads, VL_LIFT_WMINB) k_lift_write(LiftArgs a, int mode) {
-  const int64_t b = blockIdx.x;
-  const int s = find_seg(a.seg_blk0, a.nseg, b);
-  const LiftSeg S = a.segs[s];
-  const int cells = S.gw * S.gh;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int cw = (int)(b - a.seg_blk0[s]) * kLiftBlockCells + wid * kLiftWarpCells;
-  if (cw >= cells) return;  // whole warp past the segment end
-  const T thr = (T)a.threshold;
+// Write pass: recompute the keep decision, lift the kept cells and store
+// them at their ranked rows.  X rows (24 B) of the warp's kept cells are
+// staged in shared memory and stored as one contiguous run of doubles (3
+// fully coalesced stores per iteration instead of three 8-B stores at a
+// 24-B stride).
+template <typename T, int DIR, int KIND>
+__device__ __forceinline__ void write_run(const LiftArgs& a, const SegP& S, const DepP& D, const double* R,
+                                          const double* t, T thr, int cw, int lane, int64_t pos, double* xs,
+                                          const float* srec, int c0, const Dir0Tab tab) {
   const unsigned lt = (1u << lane) - 1u;
-  // this warp's first output row: block offset + the block's earlier warps
-  int64_t pos = a.blk_off[b];
-  {
-    const int c = lane < wid ? a.warp_count[b * kLiftWarps + lane] : 0;
-    pos += warp_sum(c);
-  }
-  // X rows (24 B) of the warp's kept cells are staged in shared memory and
-  // stored as one contiguous run of doubles (3 fully coalesced stores per
-  // iteration instead of three 8-B stores at a 24-B stride)
-  __shared__ double sX[kLiftWarps][3 * 32];
-  double* xs = sX[wid];
-  for (int i = 0; i < kLiftPerThread; ++i) {
-    const int cell = cw + i * 32 + lane;
-    if (cw + i * 32 >= cells) break;  // uniform across the warp
-    CellResult r;
+  CellWalk cwk(cw + lane, S.gw);
+  for (int i = 0; i < kLiftPerThread; ++i, cwk.next(S.gw)) {
+    if (cw + i * 32 >= S.cells) break;  // uniform across the warp
     bool keep = false;
-    if (cell < cells) {
-      const CellIn<T> in = load_cell<T>(S, cell);
-      keep = gate<T>(in.c, thr) && cell_eval<T>(S, a.depths, cell, in, mode, r);
+    double px0 = 0, px1 = 0, X0 = 0, X1 = 0, X2 = 0, wv = 0;
+    if (cwk.cell < S.cells) {
+      T c;
+      double tx, ty;
+      load_cell<T>(S, cwk.cell, c, tx, ty, srec, c0);
+      keep = gate<T>(c, thr);
+      wv = (double)c;
+      if (keep) {
+        if (KIND == kGateOnly) {
+          source_px(S, cwk.row, cwk.col, px0, px1);
+          X0 = tx;
+          X1 = ty;
+          X2 = (double)cwk.cell;
+        } else if (DIR == 0) {
+          // db -> query: direct lookup at the db cell (localizer.py:164-177)
+          bool ok;
+          double X[3];
+          if (tab.on) {
+            const int r = cwk.row - tab.row0;
+            const double d = (double)tap_val<KIND>(D, tab.iy[r] * D.w + tab.ix[cwk.col], ok);
+            if (ok) lift_point_n(R, t, tab.xn[cwk.col], tab.yn[r], d, X);
+          } else {
+            double sx, sy;
+            source_px(S, cwk.row, cwk.col, sx, sy);
+            const double d = (double)tap_val<KIND>(D, direct_idx(D, sx, sy), ok);
+            if (ok) lift_point(D, R, t, sx, sy, d, X);
+          }
+          keep = ok;
+          if (ok) {
+            X0 = X[0];
+            X1 = X[1];
+            X2 = X[2];
+            px0 = tx;
+            px1 = ty;
+          }
+        } else {
+          // query -> db: bilinear at the subpixel target (localizer.py:181-196)
+          double d;
+          keep = interp_val<KIND>(D, dmul(tx, D.sxd), dmul(ty, D.syd), d);
+          if (keep) {
+            double X[3];
+            lift_point(D, R, t, tx, ty, d, X);
+            X0 = X[0];
+            X1 = X[1];
+            X2 = X[2];
+            source_px(S, cwk.row, cwk.col, px0, px1);
+          }
+        }
+      }
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     const int nk = __popc(m);
     if (keep) {
       const int k = __popc(m & lt);
       const int64_t p = pos + k;
-      xs[3 * k] = r.X[0];
-      xs[3 * k + 1] = r.X[1];
-      xs[3 * k + 2] = r.X[2];
+      xs[3 * k] = X0;
+      xs[3 * k + 1] = X1;
+      xs[3 * k + 2] = X2;
       if (p < a.capacity) {
-        reinterpret_cast<double2*>(a.px_out)[p] = make_double2(r.px[0], r.px[1]);
-        a.w_out[p] = r.w;
+        reinterpret_cast<double2*>(a.px_out)[p] = make_double2(px0, px1);
+        a.w_out[p] = wv;
         if (a.entry_out) a.entry_out[p] = S.entry;
       }
     }
     __syncwarp();
-    const int64_t lim = 3 * (a.capacity - pos);  // doubles of X_out still inside the capacity
-    for (int j = lane; j < 3 * nk; j += 32)
-      if (j < lim) a.X_out[3 * pos + j] = xs[j];
+    // the iteration's 3 nk doubles of X, lanes consecutive (capacity-clipped)
+    const int n3 = (int)min((int64_t)(3 * nk), max((int64_t)0, 3 * (a.capacity - pos)));
+    double* xo = a.X_out + 3 * pos;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (lane + 32 * k < n3) xo[lane + 32 * k] = xs[lane + 32 * k];
     __syncwarp();
     pos += nk;
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kLiftThreads, VL_LIFT_WMINB) k_lift_write(LiftArgs a, int mode) {
+  __shared__ double sX[kLiftWarps][3 * 32];
+  __shared__ __align__(16) float srec_buf[3 * kLiftBlockCells];
+  __shared__ __align__(8) uint64_t sbar;
+  __shared__ double sRt[12];  // the database pose (block-uniform broadcast reads)
+  __shared__ int s_ix[kTabCols], s_iy[kTabRows];
+  __shared__ double s_xn[kTabCols], s_yn[kTabRows];
+  const int64_t b = blockIdx.x;
+  const int s = __ldg(a.seg_of_blk + b);  // host-built tile -> segment table (no per-thread binary search)
+  const SegP S = load_seg(a.segs + s);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c0 = (int)(b - a.seg_blk0[s]) * kLiftBlockCells;
+  const int cw = c0 + wid * kLiftWarpCells;
+  const T thr = (T)a.threshold;
+  DepP D{};
+  int kind = kGateOnly;
+  Dir0Tab tab;
+  tab.on = false;
+  if (mode == 0) {
+    const LiftDepth* gd = a.depths + S.depth;
+    D = load_dep(gd);
+    kind = __ldg(&gd->kind);
+    if (threadIdx.x < 12) sRt[threadIdx.x] = threadIdx.x < 9 ? __ldg(gd->R + threadIdx.x) : __ldg(gd->t + threadIdx.x - 9);
+    fill_dir0_tab(S, D, c0, true, s_ix, s_iy, s_xn, s_yn, tab);
+  }
+  const float* srec = stage_records(S, c0, srec_buf, &sbar);  // its barrier also publishes sRt and the tables
+  if (cw >= S.cells) return;  // whole warp past the segment end
+  // this warp's first output row: block offset + the block's earlier warps
+  int64_t pos = a.blk_off[b] + a.chunk_off[b / kScanChunk];
+  {
+    const int c = lane < wid ? a.warp_count[b * kLiftWarps + lane] : 0;
+    pos += warp_sum(c);
+  }
+  Dir0Tab notab = tab;
+  notab.on = false;
+  const double* R = sRt;
+  const double* t = sRt + 9;
+#define VL_LIFT_WRITE(K)                                                                                 \
+  if (S.direction == 0) write_run<T, 0, K>(a, S, D, R, t, thr, cw, lane, pos, sX[wid], srec, c0, tab);    \
+  else write_run<T, 1, K>(a, S, D, R, t, thr, cw, lane, pos, sX[wid], srec, c0, notab);
+  switch (kind) {
+    case kDepthF32: VL_LIFT_WRITE(kDepthF32) break;
+    case kDepthF16: VL_LIFT_WRITE(kDepthF16) break;
+    case kDepthCode8: VL_LIFT_WRITE(kDepthCode8) break;
+    case kDepthCode16: VL_LIFT_WRITE(kDepthCode16) break;
+    default: write_run<T, 0, kGateOnly>(a, S, D, nullptr, nullptr, thr, cw, lane, pos, sX[wid], srec, c0, notab); break;
+  }
+#undef VL_LIFT_WRITE
 }
 
 int launch_lift(const LiftArgs& a, int field_f64, int mode, cudaStream_t st) {
   if (a.nblk <= 0) return 0;
   if (field_f64) k_lift_count<double><<<(unsigned)a.nblk, kLiftThreads, 0, st>>>(a, mode);
   else k_lift_count<float><<<(unsigned)a.nblk, kLiftThreads, 0, st>>>(a, mode);
-  k_lift_scan<<<1, 1024, 0, st>>>(a);
+  k_lift_scan<<<(unsigned)((a.nblk + kScanChunk - 1) / kScanChunk), kScanChunk, 0, st>>>(a);
   return 2;
 }
 

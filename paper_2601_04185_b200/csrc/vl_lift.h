@@ -50,6 +50,9 @@ struct LiftArgs {
   double* w_out;
   int32_t* entry_out;
   int64_t capacity;
+  const int* seg_of_blk;    // [nblk] segment of every 2048-cell block (host-built)
+  int64_t* chunk_off;       // [nchunk] offsets of the scan's 1024-block chunks (blk_off is chunk-relative)
+  int* scan_ticket;         // zeroed by the caller
 };
 
 // copies `bytes` (multiple of 8) from mapped pinned host memory and zeroes
