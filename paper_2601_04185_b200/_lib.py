@@ -317,3 +317,14 @@ def state_to_dict(st: PCG64State) -> dict:
 def stream_ptr():
     import torch
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def nvtx(name: str):
+    """NVTX range around a host API stage (visible in Nsight Systems / ncu
+    --nvtx); a no-op context when NVTX is unavailable."""
+    import contextlib
+    try:
+        import torch
+        return torch.cuda.nvtx.range(name)
+    except Exception:  # pragma: no cover
+        return contextlib.nullcontext()

@@ -538,8 +538,9 @@ class LiftPlan:
 
     def lift(self):
         """Run the lift; returns per-query [start, end) match ranges (host)."""
-        _call_lift(self.table, self.nseg, self.deps, self.ndep, self.up.f64, self.threshold, 0, self.px, self.X,
-                   self.w, self.ent, self.cap, self.offs, self.flags, self.fields, self.ctx)
+        with _lib.nvtx(f"visloc.lift segments={self.nseg}"):
+            _call_lift(self.table, self.nseg, self.deps, self.ndep, self.up.f64, self.threshold, 0, self.px, self.X,
+                       self.w, self.ent, self.cap, self.offs, self.flags, self.fields, self.ctx)
         qs = np.arange(len(self.jobs))
         # segments are in query order: first/last segment of every query
         start = self.offs[np.searchsorted(self.seg_q, qs, "left")]

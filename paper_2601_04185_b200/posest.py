@@ -195,7 +195,7 @@ def ransac_pnp_device(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, o
     o.inlier_count, o.score = out["count"].data_ptr(), out["score"].data_ptr()
     o.iterations, o.converged = out["iterations"].data_ptr(), out["converged"].data_ptr()
     o.stats = out["stats"].data_ptr()
-    with torch.cuda.device(dev):
+    with torch.cuda.device(dev), _lib.nvtx(f"visloc.ransac_pnp_device Q={Q}"):
         if stages is None:
             rc = _lib.lib().vl_ransac_pnp(ctx.handle, C.byref(args), C.byref(o), _lib.stream_ptr())
         else:
@@ -324,25 +324,26 @@ def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chu
     }
     host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()}
     if not chunk_queries:
-        ends = list(stage_ends) if stage_ends is not None else _stage_schedule(Q)
-        bufs = [torch.empty(t.shape, dtype=t.dtype, device=dev) for t in host_in]
-        events = []
-        copy.wait_stream(comp)  # the device buffers are fresh allocations on the compute stream
-        with torch.cuda.stream(copy):
-            q0 = 0
-            for q1 in ends:
-                r0, r1 = int(offsets[q0]), int(offsets[q1])
-                for dst, src in zip(bufs, host_in):
-                    dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-                events.append(ev)
-                q0 = q1
-        ransac_pnp_device(bufs[0], bufs[1], bufs[2], offsets, intrinsics, seeds, cfg, out=out,
-                          stages=(ends, events))
-        for key, v in out.items():
-            host_out[key].copy_(v[:N] if key == "flags" else v, non_blocking=True)
-        comp.synchronize()
+        with _lib.nvtx(f"visloc.ransac_pnp_host Q={Q}"):
+            ends = list(stage_ends) if stage_ends is not None else _stage_schedule(Q)
+            bufs = [torch.empty(t.shape, dtype=t.dtype, device=dev) for t in host_in]
+            events = []
+            copy.wait_stream(comp)  # the device buffers are fresh allocations on the compute stream
+            with torch.cuda.stream(copy):
+                q0 = 0
+                for q1 in ends:
+                    r0, r1 = int(offsets[q0]), int(offsets[q1])
+                    for dst, src in zip(bufs, host_in):
+                        dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                    events.append(ev)
+                    q0 = q1
+            ransac_pnp_device(bufs[0], bufs[1], bufs[2], offsets, intrinsics, seeds, cfg, out=out,
+                              stages=(ends, events))
+            for key, v in out.items():
+                host_out[key].copy_(v[:N] if key == "flags" else v, non_blocking=True)
+            comp.synchronize()
     else:
         _host_pipeline_chunks(host_in, offsets, intrinsics, seeds, cfg, chunk_queries, out, host_out, comp, copy,
                               dev)
