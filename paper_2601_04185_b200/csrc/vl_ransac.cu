@@ -404,7 +404,8 @@ int launch_hyp_rows(const Work& wk, const double* R, const double* t, int H, int
   return 1;
 }
 
-__global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
   __shared__ int warp_tot[32];
   __shared__ int s_item0;
   if ((int)blockIdx.x >= *wk.active_count) return;
@@ -413,11 +414,11 @@ __global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
   const int bn = S.batch_n;
   const double fx = S.in.fx, fy = S.in.fy;
   int running = 0;
-  for (int base = 0; base < bn; base += 1024) {
+  for (int base = 0; base < bn; base += NT) {
     const int s = base + threadIdx.x;
     const int c = s < bn ? wk.slot_cnt[(int64_t)q * wk.B + s] : 0;
     int total;
-    const int ex = block_excl_scan<1024>(c, warp_tot, total);
+    const int ex = block_excl_scan<NT>(c, warp_tot, total);
     for (int k = 0; k < c; ++k) {
       const int h = running + ex + k;
       wk.hsrc[(int64_t)q * wk.HCAP + h] = s * 4 + k;
@@ -439,9 +440,9 @@ __global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
   const int t0 = size > 1 ? (int)((((int64_t)wk.split_rank - (int64_t)q * wk.TCAP) % size + size) % size) : 0;
   const int nown = t0 < ntile ? (ntile - 1 - t0) / size + 1 : 0;
   const int nitems = nown * ngroups;
-  for (int t = threadIdx.x; t < ntile; t += 1024) wk.tile_cnt[(int64_t)q * wk.TCAP + t] = 0;
+  for (int t = threadIdx.x; t < ntile; t += NT) wk.tile_cnt[(int64_t)q * wk.TCAP + t] = 0;
   if (size > 1)
-    for (int h = threadIdx.x; h < nh; h += 1024)
+    for (int h = threadIdx.x; h < nh; h += NT)
       if ((h / tile_h) % size != t0) wk.cost32[(int64_t)q * wk.HCAP + h] = 0.f;
   if (threadIdx.x == 0) {
     S.nh = nh;
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(1024) k_compact(Work wk, int fine) {
     s_item0 = nitems > 0 ? atomicAdd(wk.item_count, nitems) : 0;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nitems; i += 1024) {
+  for (int i = threadIdx.x; i < nitems; i += NT) {
     ScoreItem it;
     it.q = q;
     it.tile = t0 + (i / ngroups) * size;
@@ -719,7 +720,18 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     k_p3p_polish<<<gp, kP3PThreads, 0, st>>>(wk);
     H(kStageP3P, false);
     H(kStageCompact, true);
-    k_compact<<<nactive, 1024, 0, st>>>(wk, fine);
+    {
+      // threads per CTA (A/B knob VISLOC_COMPACT_NT: 256 / 512 / 1024); C3:
+      // 256 -> 1.39 ms/step, 512 -> 1.63, 1024 -> 1.47 (spills at the 64-register cap)
+      static int cnt = -1;
+      if (cnt < 0) {
+        const char* e = getenv("VISLOC_COMPACT_NT");
+        cnt = e ? atoi(e) : 256;
+      }
+      if (cnt == 256) k_compact<256><<<nactive, 256, 0, st>>>(wk, fine);
+      else if (cnt == 512) k_compact<512><<<nactive, 512, 0, st>>>(wk, fine);
+      else k_compact<1024><<<nactive, 1024, 0, st>>>(wk, fine);
+    }
     H(kStageCompact, false);
     H(kStageScore, true);
     launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, nactive, st);
