@@ -593,6 +593,9 @@ __device__ __forceinline__ void write_run(const LiftArgs& a, const SegP& S, cons
                                           const double* t, T thr, int cw, int lane, int64_t pos, double* xs,
                                           const float* srec, int c0, const Dir0Tab tab) {
   const unsigned lt = (1u << lane) - 1u;
+  // the capacity clip only matters when the caller's arrays are too small
+  const bool room = pos + kLiftWarpCells <= a.capacity;
+  double* xo = a.X_out + 3 * pos;
   CellWalk cwk(cw + lane, S.gw);
   for (int i = 0; i < kLiftPerThread; ++i, cwk.next(S.gw)) {
     if (cw + i * 32 >= S.cells) break;  // uniform across the warp
@@ -655,21 +658,21 @@ __device__ __forceinline__ void write_run(const LiftArgs& a, const SegP& S, cons
       xs[3 * k] = X0;
       xs[3 * k + 1] = X1;
       xs[3 * k + 2] = X2;
-      if (p < a.capacity) {
+      if (room || p < a.capacity) {
         reinterpret_cast<double2*>(a.px_out)[p] = make_double2(px0, px1);
         a.w_out[p] = wv;
         if (a.entry_out) a.entry_out[p] = S.entry;
       }
     }
     __syncwarp();
-    // the iteration's 3 nk doubles of X, lanes consecutive (capacity-clipped)
-    const int n3 = (int)min((int64_t)(3 * nk), max((int64_t)0, 3 * (a.capacity - pos)));
-    double* xo = a.X_out + 3 * pos;
+    // the iteration's 3 nk doubles of X, lanes consecutive
+    const int n3 = room ? 3 * nk : (int)min((int64_t)(3 * nk), max((int64_t)0, 3 * (a.capacity - pos)));
 #pragma unroll
     for (int k = 0; k < 3; ++k)
       if (lane + 32 * k < n3) xo[lane + 32 * k] = xs[lane + 32 * k];
     __syncwarp();
     pos += nk;
+    xo += 3 * nk;
   }
 }
 
