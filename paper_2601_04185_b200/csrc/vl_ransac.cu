@@ -83,18 +83,35 @@ int launch_prep(const Work& wk, const Inputs& in, int q0, int nq, int list_pos, 
 // Speculative parallel generation: sample i assumes no Lemire rejection
 // happened in samples [i0, i); the first sample that would reject is redone
 // exactly by one thread and speculation restarts after it.
+// Speculation rounds start from a base state computed once by thread 0 (one
+// O(log n) pcg_advance); each thread then jumps only its own offset within
+// the batch through the block's 2^k jump table (a few affine compositions
+// instead of a full O(log n) advance per thread).
 template <int NT>
 __device__ void sample_batch(const GenState& g, uint64_t& pos, int64_t n, int bn, int* out) {
   __shared__ int s_first;
   __shared__ unsigned long long s_pos;
+  __shared__ u128 s_tmul[kJumpBits], s_tplus[kJumpBits], s_base;
+  __shared__ unsigned long long s_m0;
   const int D = draws_per_sample(n);
+  if (threadIdx.x == 0) pcg_jump_table(g.inc, s_tmul, s_tplus);
   int i0 = 0;
   while (i0 < bn) {
-    if (threadIdx.x == 0) s_first = INT_MAX;
+    if (threadIdx.x == 0) {
+      s_first = INT_MAX;
+      const uint64_t q0 = pos >= (uint64_t)g.has0 ? pos - g.has0 : 0;  // first non-buffered word
+      s_m0 = q0 >> 1;
+      s_base = pcg_advance(g.state, g.inc, s_m0 + 1);
+    }
     __syncthreads();
+    // the speculative window spans at most NT samples at a time: offsets < 2^kJumpBits words
     for (int i = i0 + threadIdx.x; i < bn; i += NT) {
       WordReader rd;
-      rd.init(g, pos + (uint64_t)D * (uint64_t)(i - i0));
+      const uint64_t off = (uint64_t)D * (uint64_t)(i - i0);
+      if (off < (1ull << (kJumpBits - 1)))
+        reader_init_from(rd, g, pos + off, s_base, s_m0, s_tmul, s_tplus);
+      else
+        rd.init(g, pos + off);
       int64_t v[3];
       if (choice3(rd, (uint32_t)n, false, v, nullptr)) {
         out[3 * i] = (int)v[0];

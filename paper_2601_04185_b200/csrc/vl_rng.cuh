@@ -92,6 +92,57 @@ struct WordReader {
   }
 };
 
+// Jump table for a block: tmul[k], tplus[k] advance the LCG by 2^k steps
+// (the squarings pcg_advance repeats for every call, done once).
+constexpr int kJumpBits = 16;
+
+VL_HD void pcg_jump_table(u128 inc, u128* tmul, u128* tplus) {
+  u128 m = pcg_mult(), c = inc;
+  for (int k = 0; k < kJumpBits; ++k) {
+    tmul[k] = m;
+    tplus[k] = c;
+    c = (m + 1) * c;
+    m *= m;
+  }
+}
+
+// state after `delta` (< 2^kJumpBits) more LCG steps, from the table: one
+// affine composition per set bit of delta (same result as pcg_advance).
+VL_HD u128 pcg_advance_tab(u128 state, uint64_t delta, const u128* tmul, const u128* tplus) {
+  u128 acc_mult = 1, acc_plus = 0;
+  for (int k = 0; delta; ++k, delta >>= 1)
+    if (delta & 1) {
+      acc_mult *= tmul[k];
+      acc_plus = acc_plus * tmul[k] + tplus[k];
+    }
+  return acc_mult * state + acc_plus;
+}
+
+// WordReader positioned at word `pos` from a shared base: base_st is the
+// state after 64-bit output m0 + 1 steps, i.e. pcg_advance(g.state, g.inc,
+// m0 + 1) with m0 = word index of the batch's first (non-buffered) word >> 1;
+// the reader's own output index m >= m0 is then at most a few thousand
+// outputs ahead (pos - batch start < 2^kJumpBits words).
+VL_HD void reader_init_from(WordReader& rd, const GenState& g, uint64_t pos, u128 base_st, uint64_t m0,
+                            const u128* tmul, const u128* tplus) {
+  rd.inc = g.inc;
+  rd.pending0 = 0;
+  rd.buf0 = g.uint0;
+  if (g.has0) {
+    if (pos == 0) {
+      rd.pending0 = 1;
+      rd.st = g.state;
+      rd.half = 2;
+      return;
+    }
+    pos -= 1;
+  }
+  const uint64_t m = pos >> 1;
+  rd.st = pcg_advance_tab(base_st, m - m0, tmul, tplus);
+  rd.cur = pcg_out(rd.st);
+  rd.half = (int)(pos & 1);
+}
+
 // Number of 32-bit draws one choice(n,3) takes when no rejection happens.
 VL_HD int draws_per_sample(int64_t n) { return n == 3 ? 4 : 5; }
 
