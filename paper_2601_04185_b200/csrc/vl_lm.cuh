@@ -201,6 +201,9 @@ __device__ __forceinline__ void staged_for_each(const StagedPts& ps, F&& fn) {
     stage_wait(ps, c);
     const double2* buf = ps.ring + (size_t)(c % kStageN) * 3 * kStageCh;
     const int m = min(kStageCh, cnt - c * kStageCh);
+#ifdef VL_STAGE_UNROLL2
+#pragma unroll 2
+#endif
     for (int i = threadIdx.x; i < m; i += NT) {
       const double2 a = buf[3 * i], b = buf[3 * i + 1], cc = buf[3 * i + 2];
       const double P[3] = {a.x, a.y, b.x};
@@ -454,10 +457,25 @@ __device__ void lm_pass(LMShared<NT>& sm, const PS& ps, const Intr& in, int kind
 
 // 6x6 LU with partial pivoting in shared memory (np.linalg.solve / LAPACK
 // gesv semantics: fails only on an exactly zero pivot).  One thread.
-__device__ __forceinline__ bool solve6_smem(double* A, double* b) {
+// 6x6 solve with partial pivoting (the damped normal equations), on one
+// thread.  The matrix is copied into registers and the elimination fully
+// unrolled — every index static, pivot row swaps as predicated selects — so
+// the serial section the other warps wait for is register latency, not ~200
+// dependent shared-memory round trips (ncu: that barrier was 15.6 % of the C5
+// k_scan stall samples).  Same operations in the same order as the smem
+// version, hence the same bits.
+__device__ __noinline__ bool solve6_smem(double* As, double* bs) {
+  double A[36], b[6];
+#pragma unroll
+  for (int i = 0; i < 36; ++i) A[i] = As[i];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) b[i] = bs[i];
+  bool ok = true;
+#pragma unroll
   for (int k = 0; k < 6; ++k) {
     int p = k;
     double pv = fabs(A[6 * k + k]);
+#pragma unroll
     for (int i = k + 1; i < 6; ++i) {
       const double v = fabs(A[6 * i + k]);
       if (v > pv) {
@@ -465,29 +483,43 @@ __device__ __forceinline__ bool solve6_smem(double* A, double* b) {
         p = i;
       }
     }
-    if (A[6 * p + k] == 0.0) return false;
-    if (p != k) {
-      for (int j = 0; j < 6; ++j) {
-        const double tmp = A[6 * k + j];
-        A[6 * k + j] = A[6 * p + j];
-        A[6 * p + j] = tmp;
+    double piv = A[6 * k + k];
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) piv = p == i ? A[6 * i + k] : piv;
+    if (piv == 0.0) ok = false;
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) {
+      if (p == i) {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const double tmp = A[6 * k + j];
+          A[6 * k + j] = A[6 * i + j];
+          A[6 * i + j] = tmp;
+        }
+        const double tb = b[k];
+        b[k] = b[i];
+        b[i] = tb;
       }
-      const double tb = b[k];
-      b[k] = b[p];
-      b[p] = tb;
     }
     const double inv = A[6 * k + k];
+#pragma unroll
     for (int i = k + 1; i < 6; ++i) {
       const double f = A[6 * i + k] / inv;
+#pragma unroll
       for (int j = k + 1; j < 6; ++j) A[6 * i + j] -= f * A[6 * k + j];
       b[i] -= f * b[k];
     }
   }
+  if (!ok) return false;
+#pragma unroll
   for (int i = 5; i >= 0; --i) {
     double s = b[i];
+#pragma unroll
     for (int j = i + 1; j < 6; ++j) s -= A[6 * i + j] * b[j];
     b[i] = s / A[6 * i + i];
   }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) bs[i] = b[i];
   return true;
 }
 

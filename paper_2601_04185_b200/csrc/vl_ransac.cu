@@ -739,13 +739,15 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     H(kStageCompact, true);
     {
       // threads per CTA (A/B knob VISLOC_COMPACT_NT: 256 / 512 / 1024); C3:
-      // 256 -> 1.39 ms/step, 512 -> 1.63, 1024 -> 1.47 (spills at the 64-register cap)
+      // 256 -> 1.39 ms/step, 512 -> 1.63, 1024 -> 1.47 (spills at the 64-register
+      // cap); a few queries (C4) take one 1024-thread pass: 2.3 vs 2.8 ms at 256
       static int cnt = -1;
       if (cnt < 0) {
         const char* e = getenv("VISLOC_COMPACT_NT");
         cnt = e ? atoi(e) : 256;
       }
-      if (cnt == 256) k_compact<256><<<nactive, 256, 0, st>>>(wk, fine);
+      if (nactive * 4 <= num_sms) k_compact<1024><<<nactive, 1024, 0, st>>>(wk, fine);  // few queries: one pass
+      else if (cnt == 256) k_compact<256><<<nactive, 256, 0, st>>>(wk, fine);
       else if (cnt == 512) k_compact<512><<<nactive, 512, 0, st>>>(wk, fine);
       else k_compact<1024><<<nactive, 1024, 0, st>>>(wk, fine);
     }
