@@ -72,8 +72,12 @@ struct Work {
   int* samples;          // [Qc][B][3]
   double* slots;         // [Qc][B][4][12]
   int* slot_cnt;         // [Qc][B]
-  double* p3p_geo;       // [Qc][B][kGeoDoubles] per-sample P3P geometry (k_p3p_roots -> k_p3p_polish)
-  double* p3p_cand;      // [Qc][B][8][3] distance-triple candidates
+  // P3P scratch (k_p3p_roots -> k_p3p_polish), warp-blocked SoA: samples are
+  // grouped 32 per block (group = q * ceil(B/32) + s/32, lane = s % 32) and
+  // field f of a sample lives at [group][f][lane], so a warp's stores and
+  // loads of one field are 256 contiguous bytes
+  double* p3p_geo;       // [Qc][ceil(B/32)][kGeoDoubles][32] per-sample geometry
+  double* p3p_cand;      // [Qc][ceil(B/32)][8 * 3][32] distance-triple candidates
   int* p3p_nc;           // [Qc][B] candidate counts
   float* P32;            // [Qc][12][HCAP]
   int* hsrc;             // [Qc][HCAP]

@@ -357,15 +357,16 @@ VL_HD_BIG int quartic_real_pos_roots(const double* c_in, double* out) {
 }
 
 // Distance-triple candidates (s1, s2, s3) from the roots (p3p.py:206-231),
-// in reference order.  Returns the count (<= 8); candidate k is written to
-// cand[k*stride + 0..2] unless cand is null (count only).
-VL_HD_BIG int p3p_candidates(const P3PGeo& g, const double* vs, int nv, double* cand, int stride) {
+// in reference order.  Returns the count (<= 8); component j of candidate k
+// is written to cand[k*stride + j*estride] unless cand is null (count only).
+VL_HD_BIG int p3p_candidates(const P3PGeo& g, const double* vs, int nv, double* cand, int stride,
+                             int estride = 1) {
   int nc = 0;
   auto put = [&](double a, double b, double c) {
     if (cand) {
       cand[stride * nc] = a;
-      cand[stride * nc + 1] = b;
-      cand[stride * nc + 2] = c;
+      cand[stride * nc + estride] = b;
+      cand[stride * nc + 2 * estride] = c;
     }
     ++nc;
   };

@@ -237,11 +237,18 @@ __global__ void __launch_bounds__(kP3PRootThreads, VL_P3P_ROOT_MINB) k_p3p_roots
   P3PGeo g;
   double quart[5], vs[4];
   int nc = 0;
+  const int64_t grp = (int64_t)q * ((wk.B + 31) / 32) + s / 32;  // warp-blocked SoA scratch
+  const int ln = s & 31;
   if (p3p_setup(f, P, g, quart)) {
     const int nv = quartic_real_pos_roots(quart, vs);
-    if (nv) nc = p3p_candidates(g, vs, nv, wk.p3p_cand + si * (3 * kMaxCand), 3);
+    if (nv) nc = p3p_candidates(g, vs, nv, wk.p3p_cand + grp * (3 * kMaxCand * 32) + ln, 3 * 32, 32);
   }
-  if (nc) *reinterpret_cast<P3PGeo*>(wk.p3p_geo + si * kGeoDoubles) = g;
+  if (nc) {
+    const double* gd = reinterpret_cast<const double*>(&g);
+    double* dst = wk.p3p_geo + grp * (kGeoDoubles * 32) + ln;
+#pragma unroll
+    for (int k = 0; k < kGeoDoubles; ++k) dst[32 * k] = gd[k];
+  }
   wk.p3p_nc[si] = nc;
 }
 
@@ -265,18 +272,26 @@ __global__ void __launch_bounds__(kP3PThreads, VL_P3P_POLISH_MINB) k_p3p_polish(
   }
   const int base = incl - nc;
   const int total = __shfl_sync(0xffffffffu, incl, 31);
-  const double* cs = wk.p3p_cand + si * (3 * kMaxCand);
-  for (int i = 0; i < nc; ++i) cand[wid][base + i] = CandRec{cs[3 * i], cs[3 * i + 1], cs[3 * i + 2], lane, 0};
+  // this warp's 32 samples are one block of the SoA scratch (s is a multiple of 32 at lane 0)
+  const int64_t grp = (int64_t)q * ((wk.B + 31) / 32) + s / 32;
+  const double* cs = wk.p3p_cand + grp * (3 * kMaxCand * 32) + lane;
+  for (int i = 0; i < nc; ++i)
+    cand[wid][base + i] = CandRec{cs[32 * (3 * i)], cs[32 * (3 * i + 1)], cs[32 * (3 * i + 2)], lane, 0};
   __syncwarp();
   double* slot = wk.slots + si * (4 * 12);
-  const double ttol = nc ? kDedupTol * sqrt(wk.p3p_geo[si * kGeoDoubles + offsetof(P3PGeo, scale2) / 8]) : 0.0;
+  const double* geo = wk.p3p_geo + grp * (kGeoDoubles * 32);
+  const double ttol = nc ? kDedupTol * sqrt(geo[32 * (offsetof(P3PGeo, scale2) / 8) + lane]) : 0.0;
   int kept = 0;
-  const int64_t warp_s0 = si - lane;  // sample index of lane 0
   for (int ch = 0; ch < total; ch += 32) {
     const int j = ch + lane;
     if (j < total) {
       const CandRec cr = cand[wid][j];
-      const P3PGeo g = *reinterpret_cast<const P3PGeo*>(wk.p3p_geo + (warp_s0 + cr.lane) * kGeoDoubles);
+      P3PGeo g;
+      {
+        double* gd = reinterpret_cast<double*>(&g);
+#pragma unroll
+        for (int k = 0; k < kGeoDoubles; ++k) gd[k] = geo[32 * k + cr.lane];
+      }
       double R[9], t[3];
       const double sv[3] = {cr.s0, cr.s1, cr.s2};
       const bool ok = p3p_polish(g, sv, R, t);
