@@ -245,7 +245,7 @@ int vl_reserve(vl_ctx* c, int32_t max_queries, int64_t max_n_per_query, int32_t 
   const int64_t ns = (nsub + kScoreChunk - 1) / kScoreChunk;
   int rc = VL_OK;
   rc |= ensure(c, c->samples, Qc * B * 3 * sizeof(int));
-  rc |= ensure(c, c->slots, Qc * B * 48 * sizeof(double));
+  rc |= ensure(c, c->slots, Qc * ((B + 31) / 32 * 32) * 48 * sizeof(double));
   rc |= ensure(c, c->slot_cnt, Qc * B * sizeof(int));
   const int64_t B32 = (B + 31) / 32 * 32;  // P3P scratch is blocked by 32 samples
   rc |= ensure(c, c->p3p_geo, Qc * B32 * kGeoDoubles * sizeof(double));
@@ -338,7 +338,7 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
         (rc = ensure(c, c->active, Qn * sizeof(int))) ||
         (rc = ensure(c, c->active_count, 2 * sizeof(int))) ||
         (rc = ensure(c, c->samples, Qn * B * 3 * sizeof(int))) ||
-        (rc = ensure(c, c->slots, Qn * B * 48 * sizeof(double))) ||
+        (rc = ensure(c, c->slots, Qn * ((B + 31) / 32 * 32) * 48 * sizeof(double))) ||
         (rc = ensure(c, c->slot_cnt, Qn * B * sizeof(int))) ||
         (rc = ensure(c, c->p3p_geo, Qn * ((B + 31) / 32 * 32) * kGeoDoubles * sizeof(double))) ||
         (rc = ensure(c, c->p3p_cand, Qn * ((B + 31) / 32 * 32) * 3 * kMaxCandSlots * sizeof(double))) ||

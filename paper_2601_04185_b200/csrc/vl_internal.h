@@ -70,7 +70,7 @@ struct Work {
   int* active_count;     // device scalar
   int* next_active;      // [Qc]
   int* samples;          // [Qc][B][3]
-  double* slots;         // [Qc][B][4][12]
+  double* slots;         // [Qc][ceil(B/32)][4 * 12][32] solution slots (R row-major + t), warp-blocked SoA
   int* slot_cnt;         // [Qc][B]
   // P3P scratch (k_p3p_roots -> k_p3p_polish), warp-blocked SoA: samples are
   // grouped 32 per block (group = q * ceil(B/32) + s/32, lane = s % 32) and
@@ -94,6 +94,12 @@ struct Work {
   int split_rank, split_size;  // hypothesis-split mode: scoring tiles dealt round-robin
   int* host_count;       // mapped pinned mirror of *active_count (nullable)
 };
+
+// Element e (0..11: R row-major, t) of solution k of sample s of query q in
+// the warp-blocked slot layout: slot_ptr(...)[32 * e].
+__device__ __forceinline__ double* slot_ptr(const Work& wk, int q, int s, int k) {
+  return wk.slots + (((int64_t)q * ((wk.B + 31) / 32) + s / 32) * 48 + 12 * k) * 32 + (s & 31);
+}
 
 struct Inputs {
   const double* px;

@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kP3PThreads, VL_P3P_POLISH_MINB) k_p3p_polish(
   for (int i = 0; i < nc; ++i)
     cand[wid][base + i] = CandRec{cs[32 * (3 * i)], cs[32 * (3 * i + 1)], cs[32 * (3 * i + 2)], lane, 0};
   __syncwarp();
-  double* slot = wk.slots + si * (4 * 12);
+  double* slot = slot_ptr(wk, q, s, 0);  // element e of kept solution k: slot[32 * (12 k + e)]
   const double* geo = wk.p3p_geo + grp * (kGeoDoubles * 32);
   const double ttol = nc ? kDedupTol * sqrt(geo[32 * (offsetof(P3PGeo, scale2) / 8) + lane]) : 0.0;
   int kept = 0;
@@ -307,9 +307,14 @@ __global__ void __launch_bounds__(kP3PThreads, VL_P3P_POLISH_MINB) k_p3p_polish(
       const double* rr = res[wid][e - ch];
       if (rr[12] == 0.0 || kept >= kMaxSolPerSample) continue;
       bool dup = false;
-      for (int k = 0; k < kept && !dup; ++k) dup = p3p_is_dup(rr, rr + 9, slot + 12 * k, slot + 12 * k + 9, ttol);
+      for (int k = 0; k < kept && !dup; ++k) {
+        double sk[12];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) sk[i] = slot[32 * (12 * k + i)];
+        dup = p3p_is_dup(rr, rr + 9, sk, sk + 9, ttol);
+      }
       if (dup) continue;
-      for (int i = 0; i < 12; ++i) slot[12 * kept + i] = rr[i];
+      for (int i = 0; i < 12; ++i) slot[32 * (12 * kept + i)] = rr[i];
       ++kept;
     }
     __syncwarp();
@@ -387,19 +392,19 @@ int launch_p3p_batch(const double* f, const double* P, int B, double* slots, int
 // fp32 scoring row of one hypothesis: diag(fx, fy, 1) [R | t] (R row-major,
 // t in sl[9..11]), folded in fp64 and rounded once, stored SoA with column
 // stride cs (k_score reads entry c of hypothesis h at P[c * cs + h]).
-__device__ __forceinline__ void store_p32(float* P, int64_t cs, double fx, double fy, const double* sl) {
-  P[0 * cs] = (float)(fx * sl[0]);
-  P[1 * cs] = (float)(fx * sl[1]);
-  P[2 * cs] = (float)(fx * sl[2]);
-  P[3 * cs] = (float)(fx * sl[9]);
-  P[4 * cs] = (float)(fy * sl[3]);
-  P[5 * cs] = (float)(fy * sl[4]);
-  P[6 * cs] = (float)(fy * sl[5]);
-  P[7 * cs] = (float)(fy * sl[10]);
-  P[8 * cs] = (float)sl[6];
-  P[9 * cs] = (float)sl[7];
-  P[10 * cs] = (float)sl[8];
-  P[11 * cs] = (float)sl[11];
+__device__ __forceinline__ void store_p32(float* P, int64_t cs, double fx, double fy, const double* sl, int es = 1) {
+  P[0 * cs] = (float)(fx * sl[0 * es]);
+  P[1 * cs] = (float)(fx * sl[1 * es]);
+  P[2 * cs] = (float)(fx * sl[2 * es]);
+  P[3 * cs] = (float)(fx * sl[9 * es]);
+  P[4 * cs] = (float)(fy * sl[3 * es]);
+  P[5 * cs] = (float)(fy * sl[4 * es]);
+  P[6 * cs] = (float)(fy * sl[5 * es]);
+  P[7 * cs] = (float)(fy * sl[10 * es]);
+  P[8 * cs] = (float)sl[6 * es];
+  P[9 * cs] = (float)sl[7 * es];
+  P[10 * cs] = (float)sl[8 * es];
+  P[11 * cs] = (float)sl[11 * es];
 }
 
 // Standalone scoring (vl_score_hypotheses): rows of caller-given hypotheses
@@ -454,8 +459,7 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
     for (int k = 0; k < c; ++k) {
       const int h = running + ex + k;
       wk.hsrc[(int64_t)q * wk.HCAP + h] = s * 4 + k;
-      store_p32(wk.P32 + (int64_t)q * 12 * wk.HCAP + h, wk.HCAP, fx, fy,
-                wk.slots + ((int64_t)q * wk.B + s) * 48 + 12 * k);
+      store_p32(wk.P32 + (int64_t)q * 12 * wk.HCAP + h, wk.HCAP, fx, fy, slot_ptr(wk, q, s, k), 32);
     }
     running += total;
   }
@@ -566,7 +570,10 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     has_best = 1;
     if (threadIdx.x == 0) {
       const int src = wk.hsrc[(int64_t)q * wk.HCAP + found];
-      const double* sl = wk.slots + ((int64_t)q * wk.B + (src >> 2)) * 48 + 12 * (src & 3);
+      const double* sp = slot_ptr(wk, q, src >> 2, src & 3);
+      double sl[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) sl[i] = sp[32 * i];
       pose_from_Rt(sl, sl + 9, s_start);
     }
     __syncthreads();
