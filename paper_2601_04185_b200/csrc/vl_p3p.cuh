@@ -535,18 +535,26 @@ VL_HD_BIG bool p3p_polish(const P3PGeo& g, const double* s_in, double* R, double
     double pr[3];
     for (int i = 0; i < 3; ++i)
       pr[i] = (R[3 * i] * P[3 * k] + R[3 * i + 1] * P[3 * k + 1] + R[3 * i + 2] * P[3 * k + 2]) + t[i];
-    const double nr = nrm3(pr);
-    if (!(nr > 0)) return false;
-    const double inr = 1.0 / nr;
+    // positive norm (sqrt(n2) > 0 <=> n2 > 0, NaN fails both)
+    if (!(dot3(pr, pr) > 0)) return false;
+    // ang = atan2(|pr x f|, pr . f) <= tol on the normalised pr.  Away from the
+    // threshold the decision is taken on the unnormalised pr: the ratio |c| / d
+    // does not depend on |pr| and the 1 % band dwarfs the rounding, so the
+    // decision is identical; within the band the reference's normalised atan2
+    // decides (atan is monotone and atan(x) <= x)
+    {
+      double cx[3];
+      cross3(pr, f + 3 * k, cx);
+      const double c = nrm3(cx), d = dot3(pr, f + 3 * k);
+      if (d > 0.0 && c <= 0.99 * kBearingTol * d) continue;
+      if (!(d > 0.0) || c >= 1.01 * kBearingTol * d) return false;
+    }
+    const double inr = 1.0 / nrm3(pr);
     for (int i = 0; i < 3; ++i) pr[i] *= inr;
     double cx[3];
     cross3(pr, f + 3 * k, cx);
-    // ang = atan2(|c|, d) <= tol, decided without atan2 outside a narrow band
-    // around the threshold (atan is monotone and atan(x) <= x): identical
-    // decisions, the fp64 atan2 only runs for |c|/d within 1 % of tol
     const double c = nrm3(cx), d = dot3(pr, f + 3 * k);
-    if (d > 0.0 && c <= 0.99 * kBearingTol * d) continue;
-    if (!(d > 0.0) || c >= 1.01 * kBearingTol * d) return false;
+    if (!(d > 0.0)) return false;
     const double ang = atan2(c, d);
     if (!(ang <= kBearingTol)) return false;
   }
