@@ -164,7 +164,8 @@ int vl_msac_score(vl_ctx* ctx, const double* q, const double* t, const double* p
  * against one scoring set (px/X/w DEVICE, n rows) through the estimator's own
  * k_score kernel (records, fx/fy-folded rows, canonical split sums).
  * shape: 0 = the estimator's single-query tiles, 1 = fine, 2 = coarse tiles
- * (same bits by construction).  costs DEVICE [H] f32. */
+ * (same bits by construction).  costs DEVICE [H] f32.  Uses the context's
+ * estimator workspace: VL_ERR_INVALID while a stepwise run is open. */
 int vl_score_hypotheses(vl_ctx* ctx, const double* R, const double* t, int32_t H, const double* px,
                         const double* X, const double* w, int64_t n, vl_intrinsics intr, double tau,
                         int32_t shape, float* costs, void* stream);

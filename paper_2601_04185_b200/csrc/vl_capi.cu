@@ -717,6 +717,8 @@ int vl_score_hypotheses(vl_ctx* c, const double* R, const double* t, int32_t H, 
     return fail(c, VL_ERR_INVALID, "bad argument");
   if (!(tau > 0)) return fail(c, VL_ERR_INVALID, "tau must be positive");
   if (n > 0x7FFFFFFF || H > (1 << 28)) return fail(c, VL_ERR_INVALID, "n or H too large");
+  // it scores in the estimator's workspace: not while a stepwise run holds it
+  if (c->step.open) return fail(c, VL_ERR_INVALID, "context has an open stepwise run (vl_ransac_begin)");
   if (H == 0) return VL_OK;
   VL_CUDA(c, cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;

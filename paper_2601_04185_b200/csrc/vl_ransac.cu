@@ -804,6 +804,10 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     const int costs_smem = with_costs <= (size_t)max_smem ? 1 : 0;
     const size_t smem = costs_smem ? with_costs : kStageBytes;
     int cs = pick_cluster(nactive, VL_LO_MINB * num_sms);
+    // a batch that fits the resident slots once but not twice (C5: 256 queries)
+    // still gains from 2-CTA clusters: 1.97 -> 1.87 ms per C5 step (the
+    // 1000-query C3 scan stays one CTA per query: clusters measured slower)
+    if (cs == 1 && nactive <= VL_LO_MINB * num_sms) cs = 2;
     if (const char* e = getenv("VISLOC_SCAN_CS")) cs = atoi(e);  // tuning knob
     launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, wk, p, costs_smem);
     H(kStageScan, false);

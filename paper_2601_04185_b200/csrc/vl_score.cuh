@@ -158,31 +158,41 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
       const int h1 = min(nh, tile0 + NT * HT);
       float* costq = wk.cost32 + (int64_t)item.q * wk.HCAP;
       for (int h = tile0 + threadIdx.x; h < h1; h += NT) {
+        // the partials of 4 groups (fine: 16 splits) / 8 groups (coarse) are
+        // loaded before they are added, in the canonical order, so the
+        // closing item waits for a few L2 round trips instead of one per group
         float c = 0.f;
         if (SPI == 1) {
-          for (int g = 0; g < NG; ++g) {
-            float v[kGroupSplits];
+          for (int g0 = 0; g0 < NG; g0 += 4) {
+            float v[4][kGroupSplits];
 #pragma unroll
-            for (int k = 0; k < kGroupSplits; ++k) {
-              const int sp = g * kGroupSplits + k;
-              v[k] = sp < NS ? __ldcg(outq + (int64_t)sp * wk.HCAP + h) : 0.f;
+            for (int gg = 0; gg < 4; ++gg)
+#pragma unroll
+              for (int k = 0; k < kGroupSplits; ++k) {
+                const int sp = (g0 + gg) * kGroupSplits + k;
+                v[gg][k] = sp < NS ? __ldcg(outq + (int64_t)sp * wk.HCAP + h) : 0.f;
+              }
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) {
+              const int g = g0 + gg;
+              if (g < NG) {
+                float gs = v[gg][0];
+#pragma unroll
+                for (int k = 1; k < kGroupSplits; ++k)
+                  if (g * kGroupSplits + k < NS) gs += v[gg][k];
+                c += gs;
+              }
             }
-            float gs = v[0];
-#pragma unroll
-            for (int k = 1; k < kGroupSplits; ++k)
-              if (g * kGroupSplits + k < NS) gs += v[k];
-            c += gs;
           }
         } else {
-          int g = 0;
-          for (; g + 4 <= NG; g += 4) {
-            float v[4];
+          for (int g0 = 0; g0 < NG; g0 += 8) {
+            float v[8];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = __ldcg(outq + (int64_t)(g + k) * wk.HCAP + h);
+            for (int k = 0; k < 8; ++k) v[k] = g0 + k < NG ? __ldcg(outq + (int64_t)(g0 + k) * wk.HCAP + h) : 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) c += v[k];
+            for (int k = 0; k < 8; ++k)
+              if (g0 + k < NG) c += v[k];
           }
-          for (; g < NG; ++g) c += __ldcg(outq + (int64_t)g * wk.HCAP + h);
         }
         costq[h] = c;
       }

@@ -322,7 +322,10 @@ def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chu
         "converged": torch.empty((Q,), dtype=torch.int32, device=dev),
         "stats": torch.empty((Q, 4), dtype=torch.int64, device=dev),
     }
-    host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()}
+    # pinned result buffers from the pool (a fresh pinned allocation costs up
+    # to tens of ms; a set is reused once the caller has dropped its arrays)
+    pset = _PINNED_POOL.get({k: (tuple(v.shape), v.dtype) for k, v in out.items()})
+    host_out = pset.tensors
     if not chunk_queries:
         with _lib.nvtx(f"visloc.ransac_pnp_host Q={Q}"):
             ends = list(stage_ends) if stage_ends is not None else _stage_schedule(Q)
@@ -347,7 +350,9 @@ def ransac_pnp_host(px, X, w, offsets, intrinsics, seeds, cfg: RansacConfig, chu
     else:
         _host_pipeline_chunks(host_in, offsets, intrinsics, seeds, cfg, chunk_queries, out, host_out, comp, copy,
                               dev)
-    host = {k: v.numpy()[:N] if k == "flags" else v.numpy() for k, v in host_out.items()}
+    full = {k: v.numpy() for k, v in host_out.items()}
+    pset.hand_out(full.values())  # views below keep these alive while the caller holds them
+    host = {k: v[:N] if k == "flags" else v for k, v in full.items()}
     h2d_bytes = sum(int(t.numel() * t.element_size()) for t in host_in)
     d2h_bytes = sum(int(v.nbytes) for v in host.values())
     return host, h2d_bytes, d2h_bytes
