@@ -380,20 +380,35 @@ __device__ __forceinline__ void lm_point(const double* R, const double* t, const
       J1[3] = 0.0;
       J1[4] = p11;
       J1[5] = p12;
-      // weighted rows once, then g += Jw^T r and H += Jw^T J: 2 FMA per entry
+      // weighted rows once, then g += Jw^T r and H += Jw^T J: 2 FMA per entry.
+      // J0[4] = J1[3] = 0 exactly, so every product with one of them is an
+      // exact zero: those entries keep only their other term, as a rounded
+      // product added to the accumulator — the bits the two-term expression
+      // gives (fma(x, y, +-0) = round(x y); fma(0, y, p) = p) — and H[3][4]
+      // stays 0.  Same results, 16 fewer fp64 operations per point.
       double W0[6], W1[6];
 #pragma unroll
       for (int a = 0; a < 6; ++a) {
-        W0[a] = wr * J0[a];
-        W1[a] = wr * J1[a];
+        W0[a] = a == 4 ? 0.0 : wr * J0[a];
+        W1[a] = a == 3 ? 0.0 : wr * J1[a];
       }
 #pragma unroll
-      for (int a = 0; a < 6; ++a) acc[1 + a] += W0[a] * ru + W1[a] * rv;
+      for (int a = 0; a < 6; ++a) {
+        if (a == 3) acc[1 + a] += dmul(W0[a], ru);
+        else if (a == 4) acc[1 + a] += dmul(W1[a], rv);
+        else acc[1 + a] += W0[a] * ru + W1[a] * rv;
+      }
       int k = 7;
 #pragma unroll
       for (int a = 0; a < 6; ++a)
 #pragma unroll
-        for (int b = a; b < 6; ++b) acc[k++] += W0[a] * J0[b] + W1[a] * J1[b];
+        for (int b = a; b < 6; ++b, ++k) {
+          const bool z0 = a == 4 || b == 4, z1 = a == 3 || b == 3;
+          if (z0 && z1) continue;  // H[3][4]: both terms exactly zero
+          if (z0) acc[k] += dmul(W1[a], J1[b]);
+          else if (z1) acc[k] += dmul(W0[a], J0[b]);
+          else acc[k] += W0[a] * J0[b] + W1[a] * J1[b];
+        }
     }
   }
 }
