@@ -20,10 +20,11 @@ Queries shard with no collective.  ``value`` is weak scaling (1000 queries
 per GPU); the line's ``strong`` object times the literal C3 batch of 1000
 queries split across the N ranks (interleaved assignment, dist.shard_indices).
 
-At N = 1 the default line also carries ``configs``: BASELINE C1 (single query
-through the drop-in ``ransac_pnp``), C4 (low inlier ratio, LO-heavy) and C5
-(8-bit compressed map: GPU lift + estimator, lift HBM roofline), each with
-its own value / e2e / roofline / cpu_baseline.
+At N = 1 the default line also carries ``configs``: C3a (the same batch with
+the adaptive default stop, whose serving e2e is PCIe-bound), BASELINE C1
+(single query through the drop-in ``ransac_pnp``), C4 (low inlier ratio,
+LO-heavy) and C5 (8-bit compressed map: GPU lift + estimator, lift HBM
+roofline), each with its own value / e2e / roofline / cpu_baseline.
 
 ``--impl reference`` times the CPU reference arm: the oracle port of the
 reference algorithm (``oracle/``, bit-identical to visloc on the golden
@@ -976,7 +977,7 @@ def main():
     if world == 1 and args.workload == "c3" and not args.no_configs:
         # the other BASELINE configs, each with its own value / e2e / roofline / cpu_baseline
         configs = {}
-        for name in ("c1", "c4"):
+        for name in ("c3a", "c1", "c4"):
             sub = bench_direct(args, dict(WORKLOADS[name]), rank, world, local, dist, args.steps, "weak",
                                not args.no_e2e)
             configs[name] = _config_summary(sub)

@@ -30,14 +30,26 @@ __device__ __forceinline__ float rcp_approx_ftz(float x) {
 // clamp runs on the ALU pipe, the reciprocal on the MUFU pipe: the FMA pipe
 // only sees the 14 FFMA2/FMUL2 of the evaluation pair.  A padding record
 // (odd subset size) has w = 0 and adds +0.
+#ifdef VL_SCORE_DIV_RN
+// A/B variant (not the product): IEEE-rounded quotients x / z, y / z as the
+// reference computes them (posest.py:209-211), for the cost / speed comparison
+// quoted in DESIGN.md
+#define VL_SCORE_DU_DV(x_, y_, z_)                                                                \
+  const float2 zc_ = make_float2(fmaxf(z_.x, 0.f), fmaxf(z_.y, 0.f));                             \
+  const float2 du_ = make_float2(__fadd_rn(__fdiv_rn(x_.x, zc_.x), A2.x), __fadd_rn(__fdiv_rn(x_.y, zc_.y), A2.y)); \
+  const float2 dv_ = make_float2(__fadd_rn(__fdiv_rn(y_.x, zc_.x), B2.x), __fadd_rn(__fdiv_rn(y_.y, zc_.y), B2.y));
+#else
+#define VL_SCORE_DU_DV(x_, y_, z_)                                                                \
+  const float2 r_ = make_float2(rcp_approx_ftz(fmaxf(z_.x, 0.f)), rcp_approx_ftz(fmaxf(z_.y, 0.f))); \
+  const float2 du_ = fma2(x_, r_, A2);                                                            \
+  const float2 dv_ = fma2(y_, r_, B2);
+#endif
 #define VL_SCORE_EVAL2(Ph, acch)                                                                  \
   {                                                                                               \
     const float2 x_ = fma2(X2, f2(Ph[0]), fma2(Y2, f2(Ph[1]), fma2(Z2, f2(Ph[2]), f2(Ph[3]))));   \
     const float2 y_ = fma2(X2, f2(Ph[4]), fma2(Y2, f2(Ph[5]), fma2(Z2, f2(Ph[6]), f2(Ph[7]))));   \
     const float2 z_ = fma2(X2, f2(Ph[8]), fma2(Y2, f2(Ph[9]), fma2(Z2, f2(Ph[10]), f2(Ph[11])))); \
-    const float2 r_ = make_float2(rcp_approx_ftz(fmaxf(z_.x, 0.f)), rcp_approx_ftz(fmaxf(z_.y, 0.f))); \
-    const float2 du_ = fma2(x_, r_, A2);                                                          \
-    const float2 dv_ = fma2(y_, r_, B2);                                                          \
+    VL_SCORE_DU_DV(x_, y_, z_)                                                                    \
     float2 e2_ = fma2(du_, du_, mul2(dv_, dv_));                                                  \
     e2_.x = fminf(e2_.x, tau2);                                                                   \
     e2_.y = fminf(e2_.y, tau2);                                                                   \
