@@ -45,6 +45,10 @@ struct __align__(16) QState {
   double best_cost;
   Pose best;
   int64_t lo_calls, hyps, evals, rounds;
+  // subset inlier count of `best` (the stop rule's msac_score, posest.py:269-273),
+  // kept while `best` is unchanged: the next rounds' stop checks reuse it
+  int64_t best_sub_cnt;
+  int best_cnt_valid, pad_;
 };
 
 struct ScoreItem {

@@ -547,6 +547,7 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   int has_best = S.has_best;
   Pose best = S.best;
   int64_t lo_calls = 0;
+  int64_t best_cnt = S.best_cnt_valid ? S.best_sub_cnt : -1;  // -1: not known for `best`
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int h0 = 0;
   while (h0 < nh) {
@@ -587,8 +588,10 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     if (lo_cost < best_cost) {
       best_cost = lo_cost;
       best = lo;
+      best_cnt = (int64_t)sm.red[1];  // this pass is the stop rule's msac_score of the new best
     } else {
       best = start;
+      best_cnt = -1;
     }
     ++lo_calls;
     h0 = found + 1;
@@ -596,10 +599,16 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   }
   int active = 1;
   if (has_best) {
-    set_eval_pose(sm, best);
-    msac_pass<kScanThreads>(sm, sub, in, p.tau, nullptr);
-    const int64_t cnt = (int64_t)sm.red[1];
-    const int64_t need = required_iters_dev((double)cnt / (double)S.nsub, p.eta, p.max_iterations);
+    // the stop rule's subset inlier count (posest.py:269-273): computed once
+    // per best pose — an unchanged best (most rounds after the first) or a
+    // best just set by an accepted LO (its msac pass above) reuses the count,
+    // which is the same pass over the same pose and subset, hence identical
+    if (best_cnt < 0) {
+      set_eval_pose(sm, best);
+      msac_pass<kScanThreads>(sm, sub, in, p.tau, nullptr);
+      best_cnt = (int64_t)sm.red[1];
+    }
+    const int64_t need = required_iters_dev((double)best_cnt / (double)S.nsub, p.eta, p.max_iterations);
     if (S.iters >= need) active = 0;
   }
   if (S.iters >= p.max_iterations) active = 0;
@@ -611,6 +620,8 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     S.best = best;
     S.lo_calls += lo_calls;
     S.active = active;
+    S.best_sub_cnt = best_cnt;
+    S.best_cnt_valid = has_best ? 1 : 0;
   }
 }
 
