@@ -346,7 +346,7 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
         (rc = ensure(c, c->P32, Qn * 12 * HCAP * sizeof(float))) ||
         (rc = ensure(c, c->hsrc, Qn * HCAP * sizeof(int))) ||
         (rc = ensure(c, c->items, item_cap * sizeof(ScoreItem))) ||
-        (rc = ensure(c, c->item_count, 2 * sizeof(int))) ||
+        (rc = ensure(c, c->item_count, 4 * sizeof(int))) ||
         (rc = ensure(c, c->partial, (size_t)Qn * max_split * HCAP * sizeof(float))) ||
         (rc = ensure(c, c->cost32, (size_t)Qn * HCAP * sizeof(float))) ||
         (rc = ensure(c, c->tile_cnt, (size_t)Qn * ntile * sizeof(int))) ||
@@ -410,7 +410,7 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
 
 // Reads back the active-query count after a round (the one host sync per round).
 static int read_active(vl_ctx* c, const Work& wk, cudaStream_t st, int* nactive) {
-  // k_active mirrors the count into this mapped pinned word
+  // k_scan's closing cluster mirrors the count into this mapped pinned word
   volatile int* h_count = (volatile int*)((char*)c->h_pinned + c->h_pinned_cap - 16);
   if (!wk.host_count) VL_CUDA(c, cudaMemcpyAsync((void*)h_count, wk.active_count, sizeof(int), cudaMemcpyDeviceToHost, st));
   VL_CUDA(c, cudaStreamSynchronize(st));
@@ -442,7 +442,7 @@ static int round_loop_lookahead(vl_ctx* c, const Work& wk, const Inputs& in, con
     if ((rc = check_launch(c))) return rc;
     VL_CUDA(c, cudaEventRecord(c->round_ev[(r + 1) & 1], st));
     VL_CUDA(c, cudaEventSynchronize(c->round_ev[r & 1]));  // round r (not the queued one) is done
-    const int n = *h_count;  // k_active's mirror: the count after round r (or a later round)
+    const int n = *h_count;  // the mirror of the count after round r (or a later round)
     if (n == 0) break;
     nlaunch = n;
     if (++r > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
@@ -735,7 +735,7 @@ int vl_score_hypotheses(vl_ctx* c, const double* R, const double* t, int32_t H, 
   const int64_t nsub_pad = n + (n & 1);
   int rc;
   if ((rc = ensure(c, c->qs, sizeof(QState))) || (rc = ensure(c, c->items, ntile * S.nsplit * sizeof(ScoreItem))) ||
-      (rc = ensure(c, c->item_count, 2 * sizeof(int))) || (rc = ensure(c, c->P32, 12 * HCAP * sizeof(float))) ||
+      (rc = ensure(c, c->item_count, 4 * sizeof(int))) || (rc = ensure(c, c->P32, 12 * HCAP * sizeof(float))) ||
       (rc = ensure(c, c->partial, (size_t)S.nsplit * HCAP * sizeof(float))) ||
       (rc = ensure(c, c->cost32, HCAP * sizeof(float))) || (rc = ensure(c, c->tile_cnt, ntile * sizeof(int))) ||
       (rc = ensure(c, c->sub_pk, nsub_pad * 3 * sizeof(double2))) ||

@@ -86,7 +86,7 @@ struct Work {
   float* P32;            // [Qc][12][HCAP]
   int* hsrc;             // [Qc][HCAP]
   ScoreItem* items;      // [item_cap]
-  int* item_count;       // [0] items appended this round, [1] scoring work cursor
+  int* item_count;       // [0] items appended this round, [1] scoring work cursor, [2] k_scan completion ticket
   float* partial;        // [Qc][NSPLIT][HCAP] split / group partial sums
   float* cost32;         // [Qc][HCAP] final fp32 costs (written by the last item of each tile)
   int* tile_cnt;         // [Qc][TCAP] per-round completion tickets of the scoring tiles

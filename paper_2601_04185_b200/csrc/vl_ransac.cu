@@ -9,7 +9,8 @@
 //   k_score    persistent grid (vl_score.cu): fp32 MSAC costs (posest.py:178)
 //   k_scan     CTA/query : ordered first-better scan with LM local
 //                          optimisation + adaptive stop (posest.py:257-276)
-//   k_active   1 CTA     : compacts the active-query list for the next round
+//              (its closing cluster also compacts the active-query list for
+//              the next round: compact_active)
 // After the last round k_final (CTA/query) classifies the full set and runs
 // the Cauchy refinement (posest.py:284-299).
 #include <algorithm>
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
     for (int i = threadIdx.x; i < kWords; i += blockDim.x) dst[i] = src[i];
     if (threadIdx.x == 0) {
       wk.active_list[list_pos + blockIdx.x] = q;
-      if (list_pos + blockIdx.x == 0) wk.item_count[0] = wk.item_count[1] = 0;
+      if (list_pos + blockIdx.x == 0) wk.item_count[0] = wk.item_count[1] = wk.item_count[2] = 0;
       if (blockIdx.x == 0) *wk.active_count = list_pos + (int)gridDim.x;  // admitted queries are active
     }
     __syncthreads();
@@ -519,6 +520,33 @@ __device__ __forceinline__ int64_t required_iters_dev(double eps, double eta, in
 #endif
 constexpr int kScanThreads = VL_LO_NT;
 
+// Active-list compaction after a round (the loop condition of posest.py:250):
+// queries still active keep their order.  Run by one CTA once every query's
+// scan has finished (the closing cluster of k_scan, after an atomic ticket);
+// the other CTAs' QState writes are read through L2.
+template <int NT>
+__device__ void compact_active(Work wk, int nactive) {
+  __shared__ int warp_tot[32];
+  int running = 0;
+  for (int base = 0; base < nactive; base += NT) {
+    const int i = base + threadIdx.x;
+    const int q = i < nactive ? __ldcg(wk.active_list + i) : -1;
+    const int a = (q >= 0 && __ldcg(&wk.qs[q].active)) ? 1 : 0;
+    int total;
+    const int ex = block_excl_scan<NT>(a, warp_tot, total);
+    if (a) wk.active_list[running + ex] = q;  // in place: write index <= read index
+    running += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *wk.active_count = running;
+    if (wk.host_count) *(volatile int*)wk.host_count = running;  // mapped pinned: read after the stream sync
+    wk.item_count[0] = 0;  // items appended next round
+    wk.item_count[1] = 0;  // scoring work cursor
+    wk.item_count[2] = 0;  // k_scan completion ticket
+  }
+}
+
 // costs_smem: the round's fp32 costs are copied to shared memory (HCAP floats
 // after the staging ring) unless a huge batch_size would not fit, in which
 // case the scan reads them from L2.
@@ -528,7 +556,12 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   __shared__ uint64_t stage_bar[kStageN];
   __shared__ LMShared<kScanThreads> sm;
   __shared__ Pose s_start;
-  if ((int)(blockIdx.x / cl_size()) >= *wk.active_count) return;  // whole cluster
+  __shared__ int s_last;
+  // the active count of this round (the grid may be a stale superset, see
+  // vl_ransac_pnp's lookahead); read once: the closing cluster rewrites it
+  const int nact = *wk.active_count;
+  const int nlist = min((int)(gridDim.x / cl_size()), nact);
+  if ((int)(blockIdx.x / cl_size()) >= nlist) return;  // whole cluster
   const int q = wk.active_list[blockIdx.x / cl_size()];
   QState& S = wk.qs[q];
   const int nh = S.nh;
@@ -623,31 +656,22 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     S.best_sub_cnt = best_cnt;
     S.best_cnt_valid = has_best ? 1 : 0;
   }
+  // the last cluster to finish compacts the active list for the next round
+  // (was a separate one-CTA kernel per round: ~8.6 us of launch + drain per
+  // round on single-query configs)
+  if (cl_rank() == 0) {
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(wk.item_count + 2, 1) == nlist - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      compact_active<kScanThreads>(wk, nlist);
+    }
+  }
 }
 
-__global__ void __launch_bounds__(1024) k_active(Work wk, int nlaunch) {
-  __shared__ int warp_tot[32];
-  // the current count (a lookahead round is launched with a stale one)
-  const int nactive = min(nlaunch, *wk.active_count);
-  __syncthreads();
-  int running = 0;
-  for (int base = 0; base < nactive; base += 1024) {
-    const int i = base + threadIdx.x;
-    const int q = i < nactive ? wk.active_list[i] : -1;
-    const int a = (q >= 0 && wk.qs[q].active) ? 1 : 0;
-    int total;
-    const int ex = block_excl_scan<1024>(a, warp_tot, total);
-    if (a) wk.active_list[running + ex] = q;  // in place: write index <= read index
-    running += total;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    *wk.active_count = running;
-    if (wk.host_count) *(volatile int*)wk.host_count = running;  // mapped pinned: read after the stream sync
-    wk.item_count[0] = 0;  // items appended next round
-    wk.item_count[1] = 0;  // scoring work cursor
-  }
-}
 
 int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st);  // vl_score.cu
 
@@ -822,12 +846,9 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     // 1000-query C3 scan stays one CTA per query: clusters measured slower)
     if (cs == 1 && nactive <= VL_LO_MINB * num_sms) cs = 2;
     if (const char* e = getenv("VISLOC_SCAN_CS")) cs = atoi(e);  // tuning knob
-    launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, wk, p, costs_smem);
+    launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, wk, p, costs_smem);  // + active-list compaction
     H(kStageScan, false);
-    H(kStageActive, true);
-    k_active<<<1, 1024, 0, st>>>(wk, nactive);
-    H(kStageActive, false);
-    n += 2;
+    n += 1;
   }
   return n;
 }
