@@ -16,7 +16,10 @@ constexpr int kScoreThreads = 128;
 #endif
 constexpr int kScoreHypPerThread = VL_SCORE_HT;  // coarse items: hypotheses per thread (sweeps: tools/)
 constexpr int kScoreTileHyps = kScoreThreads * kScoreHypPerThread;  // 768
-constexpr int kScoreItemSplits = 4;    // coarse items: 4 splits = 512 correspondences
+#ifndef VL_SCORE_SPI
+#define VL_SCORE_SPI 4
+#endif
+constexpr int kScoreItemSplits = VL_SCORE_SPI;  // coarse items: 4 splits = 512 correspondences
 // canonical cost = sum over split groups (in order) of the group sum
 // ((p0 + p1) + p2) + p3 over its splits; coarse items produce one group
 constexpr int kGroupSplits = kScoreItemSplits;

@@ -25,6 +25,7 @@
 // Variant sweep and ncu evidence: tools/score_bench.cu, profiles/.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include "vl_score.cuh"
 
 namespace vl {
@@ -56,21 +57,38 @@ static int score_grid(const Work& wk, int persistent, int fine, int nactive) {
 }
 
 int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st) {
+  // dynamic smem: the attribute is set once per device (host threads driving
+  // separate contexts may get here together)
+  static std::mutex mu;
+  static bool attr_dev[kMaxDevices] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  constexpr size_t kFineSmem = score_smem_bytes<kScoreThreads, kScoreHypPerThreadFine, 1, kScoreChunk>();
+  constexpr size_t kCoarseSmem = score_smem_bytes<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk>();
+  auto fkern = k_score2_t<kScoreThreads, kScoreHypPerThreadFine, 1, kScoreChunk, kFineMinBlocks, 2>;
+  auto ckern = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks,
+                          VL_SCORE_UNR>;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    bool& a = attr_dev[dev < kMaxDevices ? dev : 0];
+    if (!a) {
+      cudaFuncSetAttribute(fkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFineSmem);
+      cudaFuncSetAttribute(ckern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoarseSmem);
+      a = true;
+    }
+  }
   if (fine) {
-    auto kern = k_score2_t<kScoreThreads, kScoreHypPerThreadFine, 1, kScoreChunk, kFineMinBlocks, 2>;
     static int occ = 0;
-    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kScoreThreads, 0) != cudaSuccess ||
-                     occ < 1))
+    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fkern, kScoreThreads, kFineSmem) !=
+                         cudaSuccess || occ < 1))
       occ = kFineMinBlocks;
-    kern<<<score_grid(wk, num_sms * occ, 1, nactive), kScoreThreads, 0, st>>>(wk, tau2);
+    fkern<<<score_grid(wk, num_sms * occ, 1, nactive), kScoreThreads, kFineSmem, st>>>(wk, tau2);
   } else {
-    auto kern = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks,
-                           VL_SCORE_UNR>;
     static int occ = 0;
-    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kScoreThreads, 0) != cudaSuccess ||
-                     occ < 1))
+    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ckern, kScoreThreads, kCoarseSmem) !=
+                         cudaSuccess || occ < 1))
       occ = kCoarseMinBlocks;
-    kern<<<score_grid(wk, num_sms * occ, 0, nactive), kScoreThreads, 0, st>>>(wk, tau2);
+    ckern<<<score_grid(wk, num_sms * occ, 0, nactive), kScoreThreads, kCoarseSmem, st>>>(wk, tau2);
   }
   return 1;
 }

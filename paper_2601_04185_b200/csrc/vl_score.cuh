@@ -65,14 +65,23 @@ __device__ __forceinline__ float rcp_approx_ftz(float x) {
 // tile shape (HT), the splits per item (SPI) nor the grid changes a single
 // bit.  The last item to finish a (query, tile) — atomic ticket per tile —
 // reduces the tile's partial slots in that order and writes the final costs.
+template <int NT, int HT, int SPI, int SCH>
+constexpr size_t score_smem_bytes() {
+  return sizeof(float4) * (3 * SPI * SCH / 2) + sizeof(float) * SPI * (SPI > 1 ? NT * HT : 1);
+}
+
 template <int NT, int HT, int SPI, int SCH, int MINB, int UNR>
 __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   static_assert(SCH % 2 == 0, "splits hold whole record pairs");
   constexpr int NW = NT / 32;
   constexpr int WHYP = 32 * HT;  // hypotheses per warp slice
   static_assert(SPI == 1 || SPI == kGroupSplits, "coarse items are exactly one split group");
-  __shared__ float4 rec[3 * SPI * SCH / 2];  // record pairs: (X2, Y2), (Z2, A2), (B2, W2)
-  __shared__ float red[SPI][SPI > 1 ? NT * HT : 1];  // split sums of coarse items
+  // record pairs (X2, Y2), (Z2, A2), (B2, W2) in dynamic smem (can exceed the
+  // 48 KB static limit for 8-split items), split sums of coarse items after them
+  extern __shared__ __align__(16) unsigned char score_dyn[];
+  float4* rec = reinterpret_cast<float4*>(score_dyn);                                   // [3 * SPI * SCH / 2]
+  float (*red)[SPI > 1 ? NT * HT : 1] = reinterpret_cast<float (*)[SPI > 1 ? NT * HT : 1]>(
+      score_dyn + sizeof(float4) * (3 * SPI * SCH / 2));                                // [SPI][NT * HT]
   __shared__ int s_it, s_last;
   const int nitems = wk.item_count[0];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
