@@ -512,9 +512,10 @@ def run_lift_bench(args, wl, rank, world, local, dist):
     lift_ms, lift_launches = prof["lift"]
     achieved = (evals_per_step * args.steps * FLOP_PER_EVAL) / (score_ms / 1e3) / 1e12 if score_ms else None
     ms = ms_prof  # shares below are of the profiled region
-    # lift algorithmic bytes per step: IMLC record 12 B/cell (f32 fields), depth taps, 52 B per match out
+    # lift algorithmic bytes per step: IMLC record 12 B/cell (f32 fields), depth taps, 48 B per match out
+    # (px 2 f64, X 3 f64, w f64 — the rows the estimator reads; no per-match entry ids are written)
     tap_bytes = {"f32": 5, "f16": 3, "u8": 1}[wl["depth"]]
-    lift_bytes = 12 * plan.cells + matches * (52 + 2.5 * tap_bytes)
+    lift_bytes = 12 * plan.cells + matches * (48 + 2.5 * tap_bytes)
     hbm = float(peaks.get("hbm_gbs", 6548.8))
     lift_gbs = lift_bytes * args.steps / (lift_ms / 1e3) / 1e9 if lift_ms else None
     roof = {"bound": "fp32", "kernel": "k_score", "achieved": achieved, "peak": round(fp32_peak, 2),

@@ -287,7 +287,8 @@ typedef struct {
  * Outputs DEVICE (capacity rows); seg_offsets HOST [nseg+1] receives the
  * exclusive output offset of every segment (last = total matches);
  * seg_flags HOST [nseg] (nullable) receives the VL_FIELD_* content verdict
- * of every IMLC segment (0 = valid; always 0 for planar segments). */
+ * of every IMLC segment (0 = valid; always 0 for planar segments);
+ * entry_out DEVICE (nullable): the segment's `entry` index per output row. */
 int vl_lift(vl_ctx* ctx, const vl_lift_segment* segs, int32_t nseg, const vl_lift_depth* depths,
             int32_t ndepth, int32_t field_f64, double threshold, int32_t mode, double* px_out,
             double* X_out, double* w_out, int32_t* entry_out, int64_t capacity, int64_t* seg_offsets,

@@ -272,7 +272,8 @@ def _seg_table(q, e, d, dep, up: _FieldUpload) -> np.ndarray:
 def _call_lift(table, nseg, deps, ndep, f64, threshold, mode, px, X, w, ent, cap, offs, flags, fields, ctx=None):
     ctx = ctx or _lib.context()
     rc = _lib.lib().vl_lift(ctx.handle, table.ctypes.data, nseg, deps, ndep, 1 if f64 else 0, float(threshold),
-                            mode, px.data_ptr(), X.data_ptr(), w.data_ptr(), ent.data_ptr(), cap,
+                            mode, px.data_ptr(), X.data_ptr(), w.data_ptr(), ent.data_ptr() if ent is not None else None,
+                            cap,
                             offs.ctypes.data_as(C.POINTER(C.c_int64)), flags.ctypes.data_as(C.POINTER(C.c_int32)),
                             _lib.stream_ptr())
     ctx.check(rc, "vl_lift")
@@ -283,7 +284,7 @@ def _call_lift(table, nseg, deps, ndep, f64, threshold, mode, px, X, w, ent, cap
 
 def _run_lift(segs_spec, depth_records, threshold, mode=0):
     """segs_spec: list of (query, entry, direction, depth_index, field).  Returns
-    (px, X, w, entry) CUDA tensors and host segment offsets."""
+    (px, X, w, None) CUDA tensors and host segment offsets."""
     import torch
     if not 0 <= threshold <= 1:
         raise ValueError(f"threshold must be in [0, 1], got {threshold}")
@@ -297,13 +298,14 @@ def _run_lift(segs_spec, depth_records, threshold, mode=0):
     px = torch.empty((cap, 2), dtype=torch.float64, device="cuda")
     X = torch.empty((cap, 3), dtype=torch.float64, device="cuda")
     w = torch.empty((cap,), dtype=torch.float64, device="cuda")
-    ent = torch.empty((cap,), dtype=torch.int32, device="cuda")
     offs = np.zeros(n + 1, dtype=np.int64)
     flags = np.zeros(max(n, 1), dtype=np.int32)
-    _call_lift(table, n, deps, len(depth_records), up.f64, threshold, mode, px, X, w, ent, cap, offs, flags,
+    # no per-match entry ids: every caller knows the entry of a segment (the
+    # estimator never reads them), so the lift skips those 4 B per match
+    _call_lift(table, n, deps, len(depth_records), up.f64, threshold, mode, px, X, w, None, cap, offs, flags,
                fields)
     tot = int(offs[-1])
-    return px[:tot], X[:tot], w[:tot], ent[:tot], offs, up
+    return px[:tot], X[:tot], w[:tot], None, offs, up
 
 
 # ----------------------------------------------------------------------------- API
@@ -530,7 +532,6 @@ class LiftPlan:
         self.px = torch.empty((self.cap, 2), dtype=torch.float64, device="cuda")
         self.X = torch.empty((self.cap, 3), dtype=torch.float64, device="cuda")
         self.w = torch.empty((self.cap,), dtype=torch.float64, device="cuda")
-        self.ent = torch.empty((self.cap,), dtype=torch.int32, device="cuda")
         self.offs = np.zeros(self.nseg + 1, dtype=np.int64)
         self.flags = np.zeros(max(self.nseg, 1), dtype=np.int32)
         self.cells = cap
@@ -540,7 +541,7 @@ class LiftPlan:
         """Run the lift; returns per-query [start, end) match ranges (host)."""
         with _lib.nvtx(f"visloc.lift segments={self.nseg}"):
             _call_lift(self.table, self.nseg, self.deps, self.ndep, self.up.f64, self.threshold, 0, self.px, self.X,
-                       self.w, self.ent, self.cap, self.offs, self.flags, self.fields, self.ctx)
+                       self.w, None, self.cap, self.offs, self.flags, self.fields, self.ctx)
         qs = np.arange(len(self.jobs))
         # segments are in query order: first/last segment of every query
         start = self.offs[np.searchsorted(self.seg_q, qs, "left")]
