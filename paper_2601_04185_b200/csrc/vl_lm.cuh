@@ -201,9 +201,6 @@ __device__ __forceinline__ void staged_for_each(const StagedPts& ps, F&& fn) {
     stage_wait(ps, c);
     const double2* buf = ps.ring + (size_t)(c % kStageN) * 3 * kStageCh;
     const int m = min(kStageCh, cnt - c * kStageCh);
-#ifdef VL_STAGE_UNROLL2
-#pragma unroll 2
-#endif
     for (int i = threadIdx.x; i < m; i += NT) {
       const double2 a = buf[3 * i], b = buf[3 * i + 1], cc = buf[3 * i + 2];
       const double P[3] = {a.x, a.y, b.x};
