@@ -120,3 +120,45 @@ def test_c4_scale_low_inlier_lo_heavy(vl):
     assert a.converged and a.iterations <= 100_000
     assert og.rot_err_deg(a.pose.q, gq) < 0.1
     assert need > 10_000  # the low-inlier regime the config is about
+
+
+def test_million_point_query_vs_oracle(vl):
+    """One query with 1M correspondences (subset stride 100, final refinement
+    over ~300k inliers, one CTA streaming the full set) against the oracle."""
+    from parity_util import check_mask, check_pose
+    px, X, w, _ = matches_a(1_000_000, 0.7, 1.0, seed=1234)
+    intr = vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
+    est = vl.ransac_pnp((px, X, w), intr, vl.RansacConfig(seed=5, max_iterations=2000, miss_probability=1e-300))
+    ref = ransac(px, X, w, INTR_T, Config(seed=5, max_iterations=2000, miss_probability=1e-300))
+    assert est.converged and est.iterations == ref.iterations == 2000
+    assert est.stats["lo_calls"] == ref.lo_calls
+    check_pose(est.pose.q, est.pose.t, ref.q, ref.t)
+    check_mask(est.inlier_flags, ref.inlier_flags, est.pose.q, est.pose.t, px, X, INTR_T, 12.0, q_ref=ref.q,
+               t_ref=ref.t)
+
+
+def test_mixed_batch_edge_queries_vs_oracle(vl):
+    """One batch mixing minimal (n = 3, 4), all-outlier, small and large
+    queries: every query behaves as it does alone in the oracle (including the
+    in-band failures: converged False, identity pose, inf score)."""
+    import math
+    from parity_util import check_mask, check_pose
+    rng = np.random.default_rng(77)
+    qs = []
+    for n, outl in ((3, 0.0), (4, 0.0), (500, 1.0), (2000, 0.5), (30_000, 0.7), (7, 0.0), (1200, 0.95)):
+        px, X, w, _ = matches_a(n, outl, 0.5, seed=int(rng.integers(1 << 30)))
+        qs.append((px, X, w))
+    intr = vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)
+    cfg = vl.RansacConfig(max_iterations=3000, miss_probability=1e-300)
+    seeds = list(range(11, 11 + len(qs)))
+    ests = vl.ransac_pnp_batch(qs, intr, cfg, seeds=seeds)
+    for (px, X, w), est, sd in zip(qs, ests, seeds):
+        ref = ransac(px, X, w, INTR_T, Config(seed=sd, max_iterations=3000, miss_probability=1e-300))
+        assert est.converged == ref.converged and est.iterations == ref.iterations
+        assert est.inlier_count == ref.inlier_count
+        if math.isinf(ref.score):
+            assert math.isinf(est.score) and np.array_equal(est.pose.q, [1.0, 0.0, 0.0, 0.0])
+            continue
+        check_pose(est.pose.q, est.pose.t, ref.q, ref.t)
+        check_mask(est.inlier_flags, ref.inlier_flags, est.pose.q, est.pose.t, px, X, INTR_T, 12.0, q_ref=ref.q,
+                   t_ref=ref.t)
