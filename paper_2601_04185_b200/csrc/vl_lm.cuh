@@ -135,7 +135,10 @@ __device__ __forceinline__ void cluster_total(LMShared<NT>& sm) {
 // a CTA, thread t still visits points t, t + NT, t + 2 NT, ... in order, so a
 // 1-CTA launch accumulates exactly as the unstaged loop does.
 constexpr int kStageCh = 512;  // records per chunk (24 KB)
-constexpr int kStageN = 3;     // ring depth
+#ifndef VL_STAGE_N
+#define VL_STAGE_N 3
+#endif
+constexpr int kStageN = VL_STAGE_N;  // ring depth
 constexpr size_t kStageBytes = (size_t)kStageN * kStageCh * 3 * sizeof(double2);
 
 struct StagedPts {
