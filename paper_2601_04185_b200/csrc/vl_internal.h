@@ -102,6 +102,16 @@ struct Work {
   int* host_count;       // mapped pinned mirror of *active_count (nullable)
 };
 
+// Programmatic dependent launch (PDL): every kernel of the round loop waits
+// for its predecessor grid's completion + memory flush at entry (a no-op when
+// launched without the PDL attribute) and immediately lets its own dependent
+// launch: for latency-bound small batches the next kernel's launch and CTA
+// scheduling then overlap this kernel instead of following it.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Element e (0..11: R row-major, t) of solution k of sample s of query q in
 // the warp-blocked slot layout: slot_ptr(...)[32 * e].
 __device__ __forceinline__ double* slot_ptr(const Work& wk, int q, int s, int k) {
@@ -153,7 +163,8 @@ int launch_sample(const GenState& g, uint64_t pos0, int64_t n, int count, int* o
 
 // standalone scoring: fp32 rows + score items of H caller hypotheses (query 0)
 int launch_hyp_rows(const Work& wk, const double* R, const double* t, int H, int fine, cudaStream_t st);
-int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st);
+int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st,
+                 bool pdl = false);
 
 // hypothesis-split packed (score, index) variant (vl_ransac.cu)
 int launch_split_argmin(const Work& wk, int nactive, int num_sms, long long* keys, cudaStream_t st);

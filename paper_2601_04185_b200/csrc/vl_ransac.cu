@@ -154,6 +154,7 @@ __device__ void sample_batch(const GenState& g, uint64_t& pos, int64_t n, int bn
 // round's count (one-round lookahead, vl_ransac_pnp).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_sample(Work wk, RansacParams p) {
+  pdl_enter();
   if ((int)blockIdx.x >= *wk.active_count) return;
   const int q = wk.active_list[blockIdx.x];
   QState& S = wk.qs[q];
@@ -219,6 +220,7 @@ struct CandRec {
 #define VL_P3P_POLISH_MINB 8  // measured: 128-register cap, 8 CTAs
 #endif
 __global__ void __launch_bounds__(kP3PRootThreads, VL_P3P_ROOT_MINB) k_p3p_roots(Work wk, Inputs in) {
+  pdl_enter();
   if ((int)blockIdx.x >= *wk.active_count) return;
   const int q = wk.active_list[blockIdx.x];
   const QState& S = wk.qs[q];
@@ -254,6 +256,7 @@ __global__ void __launch_bounds__(kP3PRootThreads, VL_P3P_ROOT_MINB) k_p3p_roots
 }
 
 __global__ void __launch_bounds__(kP3PThreads, VL_P3P_POLISH_MINB) k_p3p_polish(Work wk) {
+  pdl_enter();
   __shared__ CandRec cand[kP3PThreads / 32][32 * kMaxCand];
   __shared__ double res[kP3PThreads / 32][32][13];
   if ((int)blockIdx.x >= *wk.active_count) return;
@@ -444,6 +447,7 @@ int launch_hyp_rows(const Work& wk, const double* R, const double* t, int H, int
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
+  pdl_enter();
   __shared__ int warp_tot[32];
   __shared__ int s_item0;
   if ((int)blockIdx.x >= *wk.active_count) return;
@@ -551,6 +555,7 @@ __device__ void compact_active(Work wk, int nactive) {
 // after the staging ring) unless a huge batch_size would not fit, in which
 // case the scan reads them from L2.
 __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, RansacParams p, int costs_smem) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   double2* ring = reinterpret_cast<double2*>(dyn_smem);  // kStageBytes (TMA staging ring)
   __shared__ uint64_t stage_bar[kStageN];
@@ -673,7 +678,7 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
 }
 
 
-int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st);  // vl_score.cu
+
 
 // Cluster size for a per-query kernel: spread few queries over up to 8 SMs
 // each (single-query latency), keep one CTA per query when the batch alone
@@ -686,20 +691,48 @@ static int pick_cluster(int nq, int slots) {
 
 template <typename... KArgs, typename... Args>
 static void launch_clustered(void (*k)(KArgs...), int nq, int block, size_t smem, int cs, cudaStream_t st,
-                             Args... args) {
+                             bool pdl, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nq * cs, 1, 1);
   cfg.blockDim = dim3(block, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// A plain launch, optionally as a programmatic dependent launch (see pdl_enter).
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*k)(KArgs...), dim3 grid, int block, cudaStream_t st, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// PDL for small (latency-bound) batches; VISLOC_PDL=0/1 forces it off/on
+static bool use_pdl(int nactive) {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("VISLOC_PDL");
+    mode = e ? atoi(e) : -1;
+  }
+  return mode >= 0 ? mode != 0 : nactive <= 8;
 }
 
 // coarse scoring items unless the whole batch would not fill ~3 waves of SMs
@@ -782,16 +815,17 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
   };
   int n = 0;
   const int fine = round_is_fine(wk, nactive, num_sms) ? 1 : 0;
+  const bool pdl = use_pdl(nactive) && !hook;  // (profiling brackets every launch with events)
   if (phase != 2) {
     H(kStageSample, true);
-    if (nactive * 4 <= num_sms) k_sample<1024><<<nactive, 1024, 0, st>>>(wk, p);
-    else k_sample<256><<<nactive, 256, 0, st>>>(wk, p);
+    if (nactive * 4 <= num_sms) launch_k(k_sample<1024>, dim3(nactive), 1024, st, pdl, wk, p);
+    else launch_k(k_sample<256>, dim3(nactive), 256, st, pdl, wk, p);
     H(kStageSample, false);
     H(kStageP3P, true);
     dim3 gr(nactive, (wk.B + kP3PRootThreads - 1) / kP3PRootThreads);
-    k_p3p_roots<<<gr, kP3PRootThreads, 0, st>>>(wk, in);
+    launch_k(k_p3p_roots, gr, kP3PRootThreads, st, pdl, wk, in);
     dim3 gp(nactive, (wk.B + kP3PThreads - 1) / kP3PThreads);
-    k_p3p_polish<<<gp, kP3PThreads, 0, st>>>(wk);
+    launch_k(k_p3p_polish, gp, kP3PThreads, st, pdl, wk);
     H(kStageP3P, false);
     H(kStageCompact, true);
     {
@@ -805,14 +839,14 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
       }
       // up to 2 queries per SM (C5: 256, C4: 1): one 1024-thread pass per query
       // (C5 compact 0.096 -> 0.037 ms); big batches (C3: 1000) at 256 threads
-      if (nactive <= 2 * num_sms) k_compact<1024><<<nactive, 1024, 0, st>>>(wk, fine);
-      else if (cnt == 256) k_compact<256><<<nactive, 256, 0, st>>>(wk, fine);
-      else if (cnt == 512) k_compact<512><<<nactive, 512, 0, st>>>(wk, fine);
-      else k_compact<1024><<<nactive, 1024, 0, st>>>(wk, fine);
+      if (nactive <= 2 * num_sms) launch_k(k_compact<1024>, dim3(nactive), 1024, st, pdl, wk, fine);
+      else if (cnt == 256) launch_k(k_compact<256>, dim3(nactive), 256, st, pdl, wk, fine);
+      else if (cnt == 512) launch_k(k_compact<512>, dim3(nactive), 512, st, pdl, wk, fine);
+      else launch_k(k_compact<1024>, dim3(nactive), 1024, st, pdl, wk, fine);
     }
     H(kStageCompact, false);
     H(kStageScore, true);
-    launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, nactive, st);
+    launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, nactive, st, pdl);
     H(kStageScore, false);
     n += 4;
   }
@@ -846,7 +880,7 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     // 1000-query C3 scan stays one CTA per query: clusters measured slower)
     if (cs == 1 && nactive <= VL_LO_MINB * num_sms) cs = 2;
     if (const char* e = getenv("VISLOC_SCAN_CS")) cs = atoi(e);  // tuning knob
-    launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, wk, p, costs_smem);  // + active-list compaction
+    launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, pdl, wk, p, costs_smem);  // + active-list compaction
     H(kStageScan, false);
     n += 1;
   }
@@ -1102,7 +1136,7 @@ int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const Ran
                             reinterpret_cast<uintptr_t>(in.w)) & 15) == 0;
   if (staged) staged = 3;  // bit 0: first pass + fused compaction, bit 1: final pass, bit 2: debug (global reads)
   if (const char* e = getenv("VISLOC_FINAL_STAGED")) staged = staged ? atoi(e) : 0;  // A/B knob
-  launch_clustered(k_final, Q, kFinalThreads, kStageBytes, cs, st, wk, in, out, p, q_base, staged);
+  launch_clustered(k_final, Q, kFinalThreads, kStageBytes, cs, st, false, wk, in, out, p, q_base, staged);
   return 1;
 }
 

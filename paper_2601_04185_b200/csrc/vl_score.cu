@@ -56,7 +56,7 @@ static int score_grid(const Work& wk, int persistent, int fine, int nactive) {
   return (int)std::min<int64_t>(ub, 1 << 30);
 }
 
-int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st) {
+int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive, cudaStream_t st, bool pdl) {
   // dynamic smem: the attribute is set once per device (host threads driving
   // separate contexts may get here together)
   static std::mutex mu;
@@ -77,18 +77,30 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive,
       a = true;
     }
   }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kScoreThreads, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see pdl_enter (vl_internal.h)
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
   if (fine) {
     static int occ = 0;
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fkern, kScoreThreads, kFineSmem) !=
                          cudaSuccess || occ < 1))
       occ = kFineMinBlocks;
-    fkern<<<score_grid(wk, num_sms * occ, 1, nactive), kScoreThreads, kFineSmem, st>>>(wk, tau2);
+    cfg.gridDim = dim3(score_grid(wk, num_sms * occ, 1, nactive), 1, 1);
+    cfg.dynamicSmemBytes = kFineSmem;
+    cudaLaunchKernelEx(&cfg, fkern, wk, tau2);
   } else {
     static int occ = 0;
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ckern, kScoreThreads, kCoarseSmem) !=
                          cudaSuccess || occ < 1))
       occ = kCoarseMinBlocks;
-    ckern<<<score_grid(wk, num_sms * occ, 0, nactive), kScoreThreads, kCoarseSmem, st>>>(wk, tau2);
+    cfg.gridDim = dim3(score_grid(wk, num_sms * occ, 0, nactive), 1, 1);
+    cfg.dynamicSmemBytes = kCoarseSmem;
+    cudaLaunchKernelEx(&cfg, ckern, wk, tau2);
   }
   return 1;
 }

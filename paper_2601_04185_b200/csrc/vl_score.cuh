@@ -72,6 +72,7 @@ constexpr size_t score_smem_bytes() {
 
 template <int NT, int HT, int SPI, int SCH, int MINB, int UNR>
 __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
+  pdl_enter();
   static_assert(SCH % 2 == 0, "splits hold whole record pairs");
   constexpr int NW = NT / 32;
   constexpr int WHYP = 32 * HT;  // hypotheses per warp slice
