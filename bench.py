@@ -56,7 +56,14 @@ WORKLOADS = {
     "c3": dict(name="C3 Aachen-style batch: 1000 queries x 50k corrs per GPU, eps=0.3, sigma=1px, "
                     "fixed 10k minimal samples/query (eta=1e-300)",
                queries=1000, n=50_000, outlier=0.7, sigma=1.0, max_iterations=10_000, eta=1e-300,
-               cpu_queries_per_core=2),
+               cpu_queries_per_core=2, prune=False),
+    # the same batch with exact scoring pruning (vl_set_scoring_pruning): hypotheses whose fp32
+    # prefix sum already reaches the best cost are not scored to the end; outputs identical, `value`
+    # counts the reference's nominal evaluations (the roofline counts the executed ones)
+    "c3p": dict(name="C3 Aachen-style batch: 1000 queries x 50k corrs per GPU, eps=0.3, sigma=1px, "
+                     "fixed 10k minimal samples/query (eta=1e-300), exact scoring pruning",
+                queries=1000, n=50_000, outlier=0.7, sigma=1.0, max_iterations=10_000, eta=1e-300,
+                cpu_queries_per_core=2, prune=True),
     "c3a": dict(name="C3 Aachen-style batch, adaptive stop (eta=1e-4): 1000 queries x 50k corrs per GPU, "
                      "eps=0.3, sigma=1px",
                 queries=1000, n=50_000, outlier=0.7, sigma=1.0, max_iterations=100_000, eta=1e-4,
@@ -435,6 +442,7 @@ def run_lift_bench(args, wl, rank, world, local, dist):
     seeds = [query_seed(qi, seed0) for qi in range(Q)]
     cfg = RansacConfig(max_iterations=wl["max_iterations"], miss_probability=wl["eta"])
     ctx = _lib.context(local)
+    ctx.set_pruning(bool(wl.get("prune", True)))  # (the context outlives the previous config's setting)
     stream = torch.cuda.current_stream()
     for _, a in batches:
         a.device()  # device-resident copies for the `value` path
@@ -698,6 +706,8 @@ def bench_direct(args, wl, rank, world, local, dist, steps, mode="weak", with_e2
     cfg = RansacConfig(max_iterations=wl["max_iterations"], miss_probability=wl["eta"])
     px_d, X_d, w_d = px_h.cuda(), X_h.cuda(), w_h.cuda()
     ctx = _lib.context(local)
+    prune = bool(wl.get("prune", True))
+    ctx.set_pruning(prune)
     stream = torch.cuda.current_stream()
 
     def sync_all():
@@ -724,7 +734,10 @@ def bench_direct(args, wl, rank, world, local, dist, steps, mode="weak", with_e2
         ransac_pnp_device(px_d, X_d, w_d, offsets, intr, seeds, cfg, out=out)
 
     ms, launches, _, clocks = timed_region(ctx, stream, sync_all, step, steps, False)
+    ctx.scoring_counters(reset=True)
     ms_prof, _, prof, _ = timed_region(ctx, stream, sync_all, step, steps, True)
+    skipped, tail_evals = ctx.scoring_counters(reset=True)
+    executed_per_step = evals_per_step - skipped / steps
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ms_max = max_over_ranks(ms)
     evals_total = max_over_ranks(evals_per_step, "sum") * steps
@@ -804,7 +817,8 @@ def bench_direct(args, wl, rank, world, local, dist, steps, mode="weak", with_e2
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
     score_ms, score_launches = prof["score"]
-    achieved = (evals_per_step * steps * FLOP_PER_EVAL) / (score_ms / 1000.0) / 1e12 if score_ms else None
+    # executed evaluations (= nominal unless pruning skipped some) over the scoring stage's time
+    achieved = (executed_per_step * steps * FLOP_PER_EVAL) / (score_ms / 1000.0) / 1e12 if score_ms else None
     stage_ms = {k: round(v[0] / steps, 3) for k, v in prof.items()}
     traffic = None
     try:  # DRAM bytes per k_score launch from the committed ncu --set full capture (profiles/)
@@ -821,9 +835,13 @@ def bench_direct(args, wl, rank, world, local, dist, steps, mode="weak", with_e2
             "peak_source": "derived SMs*128*2*sm_max_mhz (MEASURED_PEAKS.json has no FP32 entry)",
             "flop_per_eval": FLOP_PER_EVAL,
             "traffic": traffic["dram_bytes_per_launch"] if traffic else None, "traffic_detail": traffic,
-            "evals_per_s_kernel": (evals_per_step * steps) / (score_ms / 1000.0) if score_ms else None,
+            "evals_per_s_kernel": (executed_per_step * steps) / (score_ms / 1000.0) if score_ms else None,
             "score_share_of_step": (score_ms / ms_prof) if ms_prof else None,
-            "score_launches": score_launches}
+            "score_launches": score_launches,
+            "evals_nominal_per_step": evals_per_step, "evals_executed_per_step": executed_per_step,
+            "evals_tail_per_step": tail_evals / steps}
+    if prune and skipped:
+        roof["kernel"] = "k_score + k_score_tail (pruned rounds)"
 
     cpu = None
     if rank == 0 and world == 1 and with_cpu and not args.no_cpu:
@@ -839,6 +857,10 @@ def bench_direct(args, wl, rank, world, local, dist, steps, mode="weak", with_e2
                    "queries_per_gpu": Q if mode == "weak" else f"{wl['queries']}/{world} (interleaved)",
                    "corrs_per_query": n, "n_sub": min(n, 10_000), "max_iterations": wl["max_iterations"],
                    "miss_probability": wl["eta"],
+                   "scoring": ("exact prefix pruning (vl_set_scoring_pruning; outputs identical to full scoring; "
+                               "value counts the reference's nominal hyp x corr evaluations, the roofline the "
+                               "executed ones)" if prune else
+                               "full: every hypothesis scored on the whole subset, as the reference does"),
                    "l2": (f"inputs {px_h.numel() * 8 * 3 / 1e9:.2f} GB/GPU (> 126 MB L2; no flush needed)"
                           if px_h.numel() * 24 > 126e6 else
                           f"inputs {px_h.numel() * 24 / 1e6:.2f} MB/GPU, L2-resident (single-query latency "
@@ -978,6 +1000,9 @@ def main():
     if world == 1 and args.workload == "c3" and not args.no_configs:
         # the other BASELINE configs, each with its own value / e2e / roofline / cpu_baseline
         configs = {}
+        sub = bench_direct(args, dict(WORKLOADS["c3p"]), rank, world, local, dist, args.steps, "weak",
+                           not args.no_e2e, False)
+        configs["c3p"] = _config_summary(sub)
         for name in ("c3a", "c1", "c4"):
             sub = bench_direct(args, dict(WORKLOADS[name]), rank, world, local, dist, args.steps, "weak",
                                not args.no_e2e)

@@ -104,6 +104,21 @@ int64_t vl_launch_count(vl_ctx* ctx);
 int vl_profile(vl_ctx* ctx, int enable);
 int vl_profile_read(vl_ctx* ctx, double* ms, int64_t* launches, int32_t n);
 
+/* Exact scoring pruning (default on; env VISLOC_PRUNE=0 turns it off for a
+ * context that never called this).  In rounds with a best pose, the fp32
+ * MSAC sum of a hypothesis (posest.py:178-220) is first formed over a prefix
+ * of the scoring subset; the terms are non-negative and fp32 addition is
+ * monotone, so a prefix >= the best cost proves that the ordered scan
+ * (`costs[h] < best_cost`, posest.py:258) rejects the hypothesis, and only
+ * the others are scored to the end.  Every output is identical either way;
+ * only the number of evaluations executed changes.  Queries with a negative
+ * weight are never pruned. */
+int vl_set_scoring_pruning(vl_ctx* ctx, int32_t enable);
+/* Run totals since the last reset: out[0] = hypothesis x correspondence
+ * evaluations skipped by pruning, out[1] = evaluations done by the tail pass
+ * for the hypotheses that survived the prefix.  Synchronises the device. */
+int vl_scoring_counters(vl_ctx* ctx, int64_t* out, int32_t reset);
+
 /* numpy SeedSequence(seed) -> PCG64 state (np.random.default_rng(seed),
  * posest.py:243).  Host-only helper, no device work. */
 int vl_pcg64_seed(uint64_t seed, vl_pcg64_state* out);

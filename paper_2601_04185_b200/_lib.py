@@ -163,6 +163,10 @@ def lib():
         L.vl_msac_score.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, dbl, dp, vp, vp]
         L.vl_score_hypotheses.argtypes = [vp, vp, vp, i32, vp, vp, vp, i64, Intrinsics, dbl, i32, vp, vp]
         L.vl_score_hypotheses.restype = C.c_int
+        L.vl_set_scoring_pruning.argtypes = [vp, i32]
+        L.vl_set_scoring_pruning.restype = C.c_int
+        L.vl_scoring_counters.argtypes = [vp, C.POINTER(C.c_int64), i32]
+        L.vl_scoring_counters.restype = C.c_int
         L.vl_refine_pose.argtypes = [vp, dp, dp, vp, vp, vp, i64, Intrinsics, i32, dbl, i32, dbl, dbl,
                                      ip, ip, dp, ip, vp]
         L.vl_p3p_solve_batch.argtypes = [vp, vp, vp, i32, vp, vp, vp, ip, vp]
@@ -218,7 +222,7 @@ EXPORTED_SYMBOLS = (
     "vl_ransac_step_score", "vl_ransac_step_finish", "vl_ransac_end", "vl_imlc_parse",
     "vl_retrieval_topk", "vl_ransac_pnp_staged", "vl_quantize_depth", "vl_reduce_depth_codes",
     "vl_build_depth_maps", "vl_triangulate_rays", "vl_ransac_step_argmin", "vl_ransac_step_finish_argmin",
-    "vl_score_hypotheses",
+    "vl_score_hypotheses", "vl_set_scoring_pruning", "vl_scoring_counters",
 )
 
 STAGES = ("prep", "sample", "p3p", "compact", "score", "scan", "active", "final", "lift")
@@ -250,6 +254,16 @@ class Context:
 
     def launches(self) -> int:
         return int(lib().vl_launch_count(self.handle))
+
+    def set_pruning(self, enable: bool):
+        """Exact scoring pruning on / off (vl_set_scoring_pruning; outputs identical either way)."""
+        self.check(lib().vl_set_scoring_pruning(self.handle, 1 if enable else 0), "vl_set_scoring_pruning")
+
+    def scoring_counters(self, reset: bool = False) -> tuple[int, int]:
+        """(evaluations skipped by pruning, evaluations done by the tail pass) since the last reset."""
+        out = (C.c_int64 * 2)()
+        self.check(lib().vl_scoring_counters(self.handle, out, 1 if reset else 0), "vl_scoring_counters")
+        return int(out[0]), int(out[1])
 
     def profile(self, enable: bool):
         lib().vl_profile(self.handle, 1 if enable else 0)

@@ -25,6 +25,8 @@ struct vl_ctx {
   int64_t launches = 0;
   DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, p3p_geo, p3p_cand, p3p_nc, P32, hsrc, items, item_count,
       partial, cost32, tile_cnt, sub_pk, sub32, comp_pk;
+  DevBuf surv, tail, prune_ctr;  // exact scoring pruning (vl_score.cuh)
+  int prune = -1;                // -1: VISLOC_PRUNE (default on), else vl_set_scoring_pruning
   DevBuf scratch;  // small standalone-call scratch
   DevBuf lift_meta, lift_blk_count, lift_blk_off, lift_seg_off;  // vl_lift
   DevBuf tri_meta;                                               // vl_build_depth_maps
@@ -111,6 +113,24 @@ static int ensure(vl_ctx* c, DevBuf& b, size_t bytes) {
   return VL_OK;
 }
 
+// run totals of the pruning counters (evaluations skipped / evaluated by the
+// scoring tail), zeroed when first allocated and by vl_scoring_counters
+static int ensure_ctr(vl_ctx* c) {
+  if (c->prune_ctr.p) return VL_OK;
+  int rc = ensure(c, c->prune_ctr, 2 * sizeof(unsigned long long));
+  if (rc) return rc;
+  VL_CUDA(c, cudaMemset(c->prune_ctr.p, 0, 2 * sizeof(unsigned long long)));
+  return VL_OK;
+}
+
+static int prune_enabled(vl_ctx* c) {
+  if (c->prune < 0) {
+    const char* e = getenv("VISLOC_PRUNE");
+    c->prune = e ? (atoi(e) != 0) : 1;
+  }
+  return c->prune;
+}
+
 static int ensure_host(vl_ctx* c, size_t bytes) {
   if (c->h_pinned_cap >= bytes) return VL_OK;
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
@@ -194,6 +214,7 @@ int vl_destroy(vl_ctx* c) {
   DevBuf* bufs[] = {&c->qs,      &c->active, &c->next_active, &c->active_count, &c->samples, &c->slots,
                     &c->slot_cnt, &c->p3p_geo, &c->p3p_cand, &c->p3p_nc, &c->P32,   &c->hsrc,        &c->items,        &c->item_count,
                     &c->partial, &c->cost32, &c->tile_cnt, &c->sub_pk, &c->sub32, &c->comp_pk,
+                    &c->surv, &c->tail, &c->prune_ctr,
                     &c->scratch, &c->lift_meta, &c->lift_blk_count,
                     &c->lift_blk_off, &c->lift_seg_off, &c->tri_meta};
   for (DevBuf* b : bufs)
@@ -228,6 +249,26 @@ int vl_profile_read(vl_ctx* c, double* ms, int64_t* launches, int32_t n) {
     ms[k] = c->stage_ms[k];
     launches[k] = c->stage_launches[k];
   }
+  return VL_OK;
+}
+
+int vl_set_scoring_pruning(vl_ctx* c, int32_t enable) {
+  if (!c) return VL_ERR_INVALID;
+  c->prune = enable ? 1 : 0;
+  return VL_OK;
+}
+
+int vl_scoring_counters(vl_ctx* c, int64_t* out, int32_t reset) {
+  if (!c || !out) return fail(c, VL_ERR_INVALID, "null argument");
+  VL_CUDA(c, cudaSetDevice(c->device));
+  int rc;
+  if ((rc = ensure_ctr(c))) return rc;
+  unsigned long long h[2];
+  VL_CUDA(c, cudaDeviceSynchronize());
+  VL_CUDA(c, cudaMemcpy(h, c->prune_ctr.p, sizeof h, cudaMemcpyDeviceToHost));
+  out[0] = (int64_t)h[0];
+  out[1] = (int64_t)h[1];
+  if (reset) VL_CUDA(c, cudaMemset(c->prune_ctr.p, 0, sizeof h));
   return VL_OK;
 }
 
@@ -352,7 +393,10 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
         (rc = ensure(c, c->tile_cnt, (size_t)Qn * ntile * sizeof(int))) ||
         (rc = ensure(c, c->sub_pk, nsub_tot * 3 * sizeof(double2))) ||
         (rc = ensure(c, c->sub32, (nsub_tot / 2) * 3 * sizeof(float4))) ||
-        (rc = ensure(c, c->comp_pk, ncomp * 3 * sizeof(double2))))
+        (rc = ensure(c, c->comp_pk, ncomp * 3 * sizeof(double2))) ||
+        (rc = ensure(c, c->surv, (size_t)Qn * HCAP * sizeof(int))) ||
+        (rc = ensure(c, c->tail, (size_t)Qn * (HCAP / 32 + ntile) * sizeof(TailTask))) ||
+        (rc = ensure_ctr(c)))
       return rc;
     const size_t host_bytes = Qn * sizeof(QState) + Qn * sizeof(int) + 64;
     if ((rc = ensure_host(c, host_bytes))) return rc;
@@ -388,6 +432,11 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
     wk.item_cap = item_cap;
     wk.split_rank = 0;
     wk.split_size = 1;
+    wk.prune = prune_enabled(c);
+    wk.surv = (int*)c->surv.p;
+    wk.tail = (TailTask*)c->tail.p;
+    wk.tail_cap = (int64_t)Qn * (HCAP / 32 + ntile);
+    wk.prune_ctr = (unsigned long long*)c->prune_ctr.p;
     // k_prep pulls the states from the mapped staging buffer itself: no
     // copy-engine transfer on this stream (it would queue behind a concurrent
     // bulk host-to-device prefetch, see posest.ransac_pnp_host)
@@ -607,6 +656,7 @@ int vl_ransac_begin(vl_ctx* c, const vl_ransac_args* a, int32_t split_rank, int3
   if ((rc = setup_chunk(c, a, 0, a->num_queries, c->step.in, c->step.wk, st))) return rc;
   c->step.wk.split_rank = split_rank;
   c->step.wk.split_size = split_size;
+  c->step.wk.prune = 0;  // the exchanged cost vectors are full costs (SUM / packed-argmin reductions)
   c->step.p = p;
   c->step.Q = a->num_queries;
   c->step.nactive = a->num_queries;
@@ -741,7 +791,8 @@ int vl_score_hypotheses(vl_ctx* c, const double* R, const double* t, int32_t H, 
       (rc = ensure(c, c->sub_pk, nsub_pad * 3 * sizeof(double2))) ||
       (rc = ensure(c, c->sub32, (nsub_pad / 2) * 3 * sizeof(float4))))
     return rc;
-  Work wk;
+  Work wk{};
+  wk.prune = 0;  // every hypothesis' full cost is the output
   wk.qs = (QState*)c->qs.p;
   wk.items = (ScoreItem*)c->items.p;
   wk.item_count = (int*)c->item_count.p;

@@ -52,10 +52,24 @@ struct __align__(16) QState {
   // kept while `best` is unchanged: the next rounds' stop checks reuse it
   int64_t best_sub_cnt;
   int best_cnt_valid, pad_;
+  // exact scoring pruning (vl_score.cuh): prune_ok = every fp32 subset weight
+  // is >= 0 (MSAC partial sums then only grow), cost_typ = mean fp32 cost of
+  // the last fully scored round, gA = split groups scored for EVERY hypothesis
+  // this round (the rest only for hypotheses whose prefix is below best_cost)
+  float cost_typ;
+  int gA, prune_ok;
+  int nsurv, tiles_closed;  // this round's surviving hypotheses / closed scoring tiles (reset by k_compact)
+  int pad2_[3];
 };
 
 struct ScoreItem {
   int q, tile, split, nsplit;  // query, hypothesis tile, first split, splits in the item
+};
+
+// Scoring tail task (pruned rounds): up to 32 surviving hypotheses of one
+// query, listed at surv[q][base .. base + cnt), finished over groups [gA, NG).
+struct TailTask {
+  int q, base, cnt, pad;
 };
 
 struct RansacParams {
@@ -89,7 +103,8 @@ struct Work {
   float* P32;            // [Qc][12][HCAP]
   int* hsrc;             // [Qc][HCAP]
   ScoreItem* items;      // [item_cap]
-  int* item_count;       // [0] items appended this round, [1] scoring work cursor, [2] k_scan completion ticket
+  int* item_count;       // [0] items appended this round, [1] scoring work cursor, [2] k_scan completion ticket,
+                         // [3] scoring tail tasks
   float* partial;        // [Qc][NSPLIT][HCAP] split / group partial sums
   float* cost32;         // [Qc][HCAP] final fp32 costs (written by the last item of each tile)
   int* tile_cnt;         // [Qc][TCAP] per-round completion tickets of the scoring tiles
@@ -100,6 +115,13 @@ struct Work {
   int64_t item_cap;
   int split_rank, split_size;  // hypothesis-split mode: scoring tiles dealt round-robin
   int* host_count;       // mapped pinned mirror of *active_count (nullable)
+  // exact scoring pruning (coarse rounds with a best pose; 0 = every
+  // hypothesis scored on the whole subset, as the reference does)
+  int prune;
+  int* surv;                     // [Qc][HCAP] surviving hypotheses of each query (any order)
+  TailTask* tail;                // [tail_cap] tasks (count: item_count[3])
+  int64_t tail_cap;
+  unsigned long long* prune_ctr; // [2] evaluations skipped / evaluated by the tail (run totals)
 };
 
 // Programmatic dependent launch (PDL): every kernel of the round loop waits

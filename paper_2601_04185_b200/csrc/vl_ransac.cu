@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
     for (int i = threadIdx.x; i < kWords; i += blockDim.x) dst[i] = src[i];
     if (threadIdx.x == 0) {
       wk.active_list[list_pos + blockIdx.x] = q;
-      if (list_pos + blockIdx.x == 0) wk.item_count[0] = wk.item_count[1] = wk.item_count[2] = 0;
+      if (list_pos + blockIdx.x == 0) wk.item_count[0] = wk.item_count[1] = wk.item_count[2] = wk.item_count[3] = 0;
       if (blockIdx.x == 0) *wk.active_count = list_pos + (int)gridDim.x;  // admitted queries are active
     }
     __syncthreads();
@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
   const int64_t off = S.off, so = S.sub_off;
   const int stride = S.stride, nsub = S.nsub;
   const double cx = S.in.cx, cy = S.in.cy;
+  int w_ok = 1;  // every fp32 weight >= 0 (scoring pruning: partial MSAC sums never decrease)
   for (int i = threadIdx.x; i < nsub; i += blockDim.x) {
     const int64_t src = off + (int64_t)i * stride;
     const double pu = in.px[2 * src], pv = in.px[2 * src + 1];
@@ -68,8 +69,15 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
     pr[6] = (float)(cx - pu);
     pr[8] = (float)(cy - pv);
     pr[10] = (float)w;
+    w_ok &= (float)w >= 0.f ? 1 : 0;
     if ((nsub & 1) && i == nsub - 1)  // padding record: w = 0 adds +0
       for (int k = 0; k < 12; k += 2) pr[k + 1] = 0.f;
+  }
+  w_ok = __syncthreads_and(w_ok);
+  if (threadIdx.x == 0) {
+    S.prune_ok = w_ok;
+    S.gA = 0;
+    S.cost_typ = 0.f;
   }
 }
 
@@ -474,7 +482,18 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
   const int tile_h = fine ? kScoreTileHypsFine : kScoreTileHyps;
   const int spi = fine ? 1 : kScoreItemSplits;
   const int ntile = (nh + tile_h - 1) / tile_h;
-  const int ngroups = (S.nsplit + spi - 1) / spi;
+  int ngroups = (S.nsplit + spi - 1) / spi;
+  // exact pruning (coarse rounds, a best pose known, non-negative weights):
+  // score the first gA split groups of every hypothesis, where gA / NG is the
+  // best cost over the typical hypothesis cost of the last fully scored round
+  // (plus 8 %): a typical hypothesis' prefix then already exceeds the best
+  // cost, and only the others are finished (k_score_tail)
+  int gA = ngroups;
+  if (wk.prune && !fine && S.prune_ok && S.has_best && S.cost_typ > 0.f) {
+    const double f = S.best_cost / (double)S.cost_typ * 1.08;
+    if (f < 1.0) gA = max(1, min(ngroups, (int)ceil(f * ngroups)));
+  }
+  ngroups = gA;
   // hypothesis-split mode: tile (q, t) belongs to rank (q*TCAP + t) mod size;
   // the other ranks leave its costs at zero for the SUM all-reduce
   const int size = wk.split_size;
@@ -487,6 +506,9 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
       if ((h / tile_h) % size != t0) wk.cost32[(int64_t)q * wk.HCAP + h] = 0.f;
   if (threadIdx.x == 0) {
     S.nh = nh;
+    S.gA = gA;
+    S.nsurv = 0;
+    S.tiles_closed = 0;
     S.hyps += nh;
     S.evals += (int64_t)nh * S.nsub;
     s_item0 = nitems > 0 ? atomicAdd(wk.item_count, nitems) : 0;
@@ -548,6 +570,7 @@ __device__ void compact_active(Work wk, int nactive) {
     wk.item_count[0] = 0;  // items appended next round
     wk.item_count[1] = 0;  // scoring work cursor
     wk.item_count[2] = 0;  // k_scan completion ticket
+    wk.item_count[3] = 0;  // scoring tail tasks
   }
 }
 
@@ -579,6 +602,17 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     costs = cs;
   }
   __syncthreads();
+  // typical hypothesis cost (mean fp32 cost) of a fully scored round: sizes
+  // the next rounds' pruning prefix (k_compact); pruned rounds keep it
+  float cost_typ = S.cost_typ;
+  if (wk.prune && nh > 0 && S.gA * kGroupSplits >= S.nsplit) {
+    double acc[1] = {0.0};
+    for (int h = threadIdx.x; h < nh; h += kScanThreads) acc[0] += (double)costs[h];
+    block_sum<kScanThreads, 1>(acc, sm.scratch, sm.red);
+    const double m = sm.red[0] / nh;
+    cost_typ = m < 3.0e38 ? (float)m : 0.f;
+    __syncthreads();
+  }
   const Intr in = S.in;
   const StagedPts sub{wk.sub_pk + 3 * S.sub_off, S.nsub, ring, stage_bar};
   double best_cost = S.best_cost;
@@ -660,6 +694,7 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     S.active = active;
     S.best_sub_cnt = best_cnt;
     S.best_cnt_valid = has_best ? 1 : 0;
+    S.cost_typ = cost_typ;
   }
   // the last cluster to finish compacts the active list for the next round
   // (was a separate one-CTA kernel per round: ~8.6 us of launch + drain per
@@ -847,9 +882,8 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     }
     H(kStageCompact, false);
     H(kStageScore, true);
-    launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, nactive, st, pdl);
+    n += 4 + launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, nactive, st, pdl);  // (+ pruning tail)
     H(kStageScore, false);
-    n += 4;
   }
   if (phase != 1) {
     H(kStageScan, true);

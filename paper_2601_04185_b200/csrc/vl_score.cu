@@ -101,6 +101,14 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive,
     cfg.gridDim = dim3(score_grid(wk, num_sms * occ, 0, nactive), 1, 1);
     cfg.dynamicSmemBytes = kCoarseSmem;
     cudaLaunchKernelEx(&cfg, ckern, wk, tau2);
+    if (wk.prune) {
+      // the survivors of pruned tiles (a few per query; no tasks in rounds
+      // without a best pose): 8 CTAs of 4 warps per SM, one task per CTA at a time
+      cfg.gridDim = dim3(8 * num_sms, 1, 1);
+      cfg.dynamicSmemBytes = 0;
+      cudaLaunchKernelEx(&cfg, k_score_tail<kScoreThreads>, wk, tau2);
+      return 2;
+    }
   }
   return 1;
 }

@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   float4* rec = reinterpret_cast<float4*>(score_dyn);                                   // [3 * SPI * SCH / 2]
   float (*red)[SPI > 1 ? NT * HT : 1] = reinterpret_cast<float (*)[SPI > 1 ? NT * HT : 1]>(
       score_dyn + sizeof(float4) * (3 * SPI * SCH / 2));                                // [SPI][NT * HT]
-  __shared__ int s_it, s_last;
+  __shared__ int s_it, s_last, s_nsurv, s_base;
+  __shared__ int s_surv[NT * HT];  // a tile's surviving hypotheses (pruned rounds)
   const int nitems = wk.item_count[0];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // dynamic work cursor: items differ in cost (partial tiles), and a static
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     const int NS = S.nsplit;
     const int NG = (NS + kGroupSplits - 1) / kGroupSplits;
     if (threadIdx.x == 0) {
-      const int tile_items = SPI == 1 ? NS : NG;
+      const int tile_items = SPI == 1 ? NS : S.gA;  // coarse: groups [0, gA) (gA < NG in pruned rounds)
       s_last = atomicAdd(wk.tile_cnt + (int64_t)item.q * wk.TCAP + item.tile, 1) == tile_items - 1;
     }
     __syncthreads();
@@ -179,6 +180,18 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
       __threadfence();
       const int h1 = min(nh, tile0 + NT * HT);
       float* costq = wk.cost32 + (int64_t)item.q * wk.HCAP;
+      // pruned round: the tile holds the prefix over groups [0, gA) of every
+      // hypothesis; one whose prefix is >= the best cost can never be accepted
+      // by the ordered scan (`cost < best`, posest.py:258: the remaining
+      // groups only add non-negative terms and fp32 addition is monotone), so
+      // the prefix stands as its cost; the others are listed for k_score_tail
+      const int gend = SPI == 1 ? NG : S.gA;
+      const bool pruning = SPI > 1 && gend < NG;
+      const double best = S.best_cost;
+      if (pruning) {
+        if (threadIdx.x == 0) s_nsurv = 0;
+        __syncthreads();
+      }
       for (int h = tile0 + threadIdx.x; h < h1; h += NT) {
         // the partials of 4 groups (fine: 16 splits) / 8 groups (coarse) are
         // loaded before they are added, in the canonical order, so the
@@ -207,18 +220,106 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
             }
           }
         } else {
-          for (int g0 = 0; g0 < NG; g0 += 8) {
+          for (int g0 = 0; g0 < gend; g0 += 8) {
             float v[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = g0 + k < NG ? __ldcg(outq + (int64_t)(g0 + k) * wk.HCAP + h) : 0.f;
+            for (int k = 0; k < 8; ++k) v[k] = g0 + k < gend ? __ldcg(outq + (int64_t)(g0 + k) * wk.HCAP + h) : 0.f;
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-              if (g0 + k < NG) c += v[k];
+              if (g0 + k < gend) c += v[k];
           }
         }
         costq[h] = c;
+        if (pruning && !((double)c >= best)) s_surv[atomicAdd(&s_nsurv, 1)] = h;
+      }
+      if (pruning) {
+        // append the tile's survivors to the query's list; the query's last
+        // tile to close turns the list into tail tasks of up to 32 hypotheses
+        QState* Sq = wk.qs + item.q;
+        __syncthreads();
+        const int ns_ = s_nsurv;
+        if (threadIdx.x == 0) s_base = ns_ ? atomicAdd(&Sq->nsurv, ns_) : 0;
+        __syncthreads();
+        int* sv = wk.surv + (int64_t)item.q * wk.HCAP;
+        for (int i = threadIdx.x; i < ns_; i += NT) sv[s_base + i] = s_surv[i];
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const long long rest = (long long)nsub - min((long long)nsub, (long long)gend * kGroupSplits * SCH);
+          atomicAdd(wk.prune_ctr, (unsigned long long)((h1 - tile0 - ns_) * rest));
+          atomicAdd(wk.prune_ctr + 1, (unsigned long long)(ns_ * rest));
+          const int ntile = (nh + NT * HT - 1) / (NT * HT);
+          if (atomicAdd(&Sq->tiles_closed, 1) == ntile - 1) {
+            __threadfence();
+            const int nq = atomicAdd(&Sq->nsurv, 0), ntask = (nq + 31) / 32;
+            const int base = ntask ? atomicAdd(wk.item_count + 3, ntask) : 0;
+            for (int k = 0; k < ntask; ++k)
+              if (base + k < wk.tail_cap) wk.tail[base + k] = TailTask{item.q, 32 * k, min(32, nq - 32 * k), 0};
+          }
+        }
       }
     }
+  }
+}
+
+// Scoring tail of a pruned round: one CTA per task (up to 32 surviving
+// hypotheses of one tile), lane = hypothesis, warp w = split w of the current
+// split group.  The group's 512 records are staged in shared memory (one
+// cooperative load, broadcast reads), every warp forms its split sum with the
+// same EVAL2 sequence as k_score2_t, and warp 0 continues each hypothesis'
+// canonical sum from the prefix the tile left in cost32 with the group sums
+// ((p0 + p1) + p2) + p3 over groups [gA, NG) — so the cost bits equal a full
+// scoring.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_score_tail(Work wk, float tau2) {
+  pdl_enter();
+  static_assert(NT / 32 == kGroupSplits, "one warp per split of a group");
+  constexpr int GP = kGroupSplits * kScoreChunk / 2;  // record pairs per group
+  __shared__ __align__(16) float4 rec[3 * GP];
+  __shared__ float red[kGroupSplits][32];
+  const int ntask = min((int64_t)wk.item_count[3], wk.tail_cap);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = blockIdx.x; t < ntask; t += gridDim.x) {
+    const TailTask tk = wk.tail[t];
+    const QState& S = wk.qs[tk.q];
+    const bool on = lane < tk.cnt;
+    const int h = wk.surv[(int64_t)tk.q * wk.HCAP + tk.base + (on ? lane : 0)];
+    const float* Pq = wk.P32 + (int64_t)tk.q * 12 * wk.HCAP;
+    float P[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) P[c] = Pq[(int64_t)c * wk.HCAP + h];
+    float* cp = wk.cost32 + (int64_t)tk.q * wk.HCAP + h;
+    float c = w == 0 ? *cp : 0.f;
+    const int NS = S.nsplit, pn = (S.nsub + 1) >> 1, NG = (NS + kGroupSplits - 1) / kGroupSplits;
+    const float4* src = wk.sub32 + 3 * (S.sub_off >> 1);
+    for (int g = S.gA; g < NG; ++g) {
+      const int p0 = g * GP, np = min(GP, pn - p0);
+      __syncthreads();  // the previous group's records and split sums are consumed
+      for (int k = threadIdx.x; k < 3 * np; k += NT) rec[k] = src[3 * p0 + k];
+      __syncthreads();
+      const int sp = g * kGroupSplits + w;
+      if (sp < NS) {
+        float2 acc = make_float2(0.f, 0.f);
+        const int pe = min((w + 1) * (kScoreChunk / 2), np);
+#pragma unroll 4
+        for (int p = w * (kScoreChunk / 2); p < pe; ++p) {
+          const float4 r0 = rec[3 * p], r1 = rec[3 * p + 1], r2 = rec[3 * p + 2];
+          const float2 X2 = make_float2(r0.x, r0.y), Y2 = make_float2(r0.z, r0.w);
+          const float2 Z2 = make_float2(r1.x, r1.y), A2 = make_float2(r1.z, r1.w);
+          const float2 B2 = make_float2(r2.x, r2.y), W2 = make_float2(r2.z, r2.w);
+          VL_SCORE_EVAL2(P, acc);
+        }
+        red[w][lane] = acc.x + acc.y;
+      }
+      __syncthreads();
+      if (w == 0) {
+        float gs = red[0][lane];
+        for (int k = 1; k < kGroupSplits; ++k)
+          if (g * kGroupSplits + k < NS) gs += red[k][lane];  // ((p0 + p1) + p2) + p3
+        c += gs;
+      }
+    }
+    if (w == 0 && on) *cp = c;
   }
 }
 
