@@ -65,15 +65,19 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive,
   cudaGetDevice(&dev);
   constexpr size_t kFineSmem = score_smem_bytes<kScoreThreads, kScoreHypPerThreadFine, 1, kScoreChunk>();
   constexpr size_t kCoarseSmem = score_smem_bytes<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk>();
-  auto fkern = k_score2_t<kScoreThreads, kScoreHypPerThreadFine, 1, kScoreChunk, kFineMinBlocks, 2>;
-  auto ckern = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks,
-                          VL_SCORE_UNR>;
+  auto fkern = k_score2_t<kScoreThreads, kScoreHypPerThreadFine, 1, kScoreChunk, kFineMinBlocks, 2, false>;
+  auto ckern_full = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks,
+                               VL_SCORE_UNR, false>;
+  auto ckern_prune = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks,
+                                VL_SCORE_UNR, true>;
+  auto ckern = wk.prune ? ckern_prune : ckern_full;
   {
     std::lock_guard<std::mutex> g(mu);
     bool& a = attr_dev[dev < kMaxDevices ? dev : 0];
     if (!a) {
       cudaFuncSetAttribute(fkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFineSmem);
-      cudaFuncSetAttribute(ckern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoarseSmem);
+      cudaFuncSetAttribute(ckern_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoarseSmem);
+      cudaFuncSetAttribute(ckern_prune, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoarseSmem);
       a = true;
     }
   }

@@ -70,7 +70,111 @@ constexpr size_t score_smem_bytes() {
   return sizeof(float4) * (3 * SPI * SCH / 2) + sizeof(float) * SPI * (SPI > 1 ? NT * HT : 1);
 }
 
-template <int NT, int HT, int SPI, int SCH, int MINB, int UNR>
+// The closing item of a (query, tile): canonical sums of the tile's
+// hypotheses from the partial slots (and, in pruned rounds, the survivor list
+// for k_score_tail).  PRUNE = false is the kernel instance of runs without
+// pruning, so the pruning code's registers stay out of it (-2 % scoring time,
+// 161 vs 168 registers); the pruning instance calls it out of line (-1 %).
+template <int NT, int HT, int SPI, int SCH, bool PRUNE>
+__device__ __forceinline__ void score_close_tile(const Work& wk, const ScoreItem& item, const float* outq, int tile0,
+                                               float* red_area, int* sh) {
+  const QState& S = wk.qs[item.q];
+  const int nh = S.nh, nsub = S.nsub;
+  const int NS = S.nsplit;
+  const int NG = (NS + kGroupSplits - 1) / kGroupSplits;
+  __threadfence();
+  const int h1 = min(nh, tile0 + NT * HT);
+  float* costq = wk.cost32 + (int64_t)item.q * wk.HCAP;
+  // pruned round: the tile holds the prefix over groups [0, gA) of every
+  // hypothesis; one whose prefix is >= the best cost can never be accepted
+  // by the ordered scan (`cost < best`, posest.py:258: the remaining
+  // groups only add non-negative terms and fp32 addition is monotone), so
+  // the prefix stands as its cost; the others are listed for k_score_tail
+  const int gend = SPI == 1 ? NG : S.gA;
+  const bool pruning = PRUNE && SPI > 1 && gend < NG;
+  const double best = S.best_cost;
+  // a tile's surviving hypotheses (pruned rounds), in the split-sum area
+  // (coarse items: SPI * NT * HT floats >= NT * HT), free once the ticket is taken
+  int* s_surv = reinterpret_cast<int*>(red_area);
+  if (pruning) {
+    if (threadIdx.x == 0) sh[0] = 0;
+    __syncthreads();
+  }
+  for (int h = tile0 + threadIdx.x; h < h1; h += NT) {
+    // the partials of 4 groups (fine: 16 splits) / 8 groups (coarse) are
+    // loaded before they are added, in the canonical order, so the
+    // closing item waits for a few L2 round trips instead of one per group
+    float c = 0.f;
+    if (SPI == 1) {
+      for (int g0 = 0; g0 < NG; g0 += 4) {
+        float v[4][kGroupSplits];
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg)
+#pragma unroll
+          for (int k = 0; k < kGroupSplits; ++k) {
+            const int sp = (g0 + gg) * kGroupSplits + k;
+            v[gg][k] = sp < NS ? __ldcg(outq + (int64_t)sp * wk.HCAP + h) : 0.f;
+          }
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg) {
+          const int g = g0 + gg;
+          if (g < NG) {
+            float gs = v[gg][0];
+#pragma unroll
+            for (int k = 1; k < kGroupSplits; ++k)
+              if (g * kGroupSplits + k < NS) gs += v[gg][k];
+            c += gs;
+          }
+        }
+      }
+    } else {
+      for (int g0 = 0; g0 < gend; g0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = g0 + k < gend ? __ldcg(outq + (int64_t)(g0 + k) * wk.HCAP + h) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (g0 + k < gend) c += v[k];
+      }
+    }
+    costq[h] = c;
+    if (pruning && !((double)c >= best)) s_surv[atomicAdd(&sh[0], 1)] = h;
+  }
+  if (pruning) {
+    // append the tile's survivors to the query's list; the query's last
+    // tile to close turns the list into tail tasks of up to 32 hypotheses
+    QState* Sq = wk.qs + item.q;
+    __syncthreads();
+    const int ns_ = sh[0];
+    if (threadIdx.x == 0) sh[1] = ns_ ? atomicAdd(&Sq->nsurv, ns_) : 0;
+    __syncthreads();
+    int* sv = wk.surv + (int64_t)item.q * wk.HCAP;
+    for (int i = threadIdx.x; i < ns_; i += NT) sv[sh[1] + i] = s_surv[i];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long rest = (long long)nsub - min((long long)nsub, (long long)gend * kGroupSplits * SCH);
+      atomicAdd(wk.prune_ctr, (unsigned long long)((h1 - tile0 - ns_) * rest));
+      atomicAdd(wk.prune_ctr + 1, (unsigned long long)(ns_ * rest));
+      const int ntile = (nh + NT * HT - 1) / (NT * HT);
+      if (atomicAdd(&Sq->tiles_closed, 1) == ntile - 1) {
+        __threadfence();
+        const int nq = atomicAdd(&Sq->nsurv, 0), ntask = (nq + 31) / 32;
+        const int base = ntask ? atomicAdd(wk.item_count + 3, ntask) : 0;
+        for (int k = 0; k < ntask; ++k)
+          if (base + k < wk.tail_cap) wk.tail[base + k] = TailTask{item.q, 32 * k, min(32, nq - 32 * k), 0};
+      }
+    }
+  }
+}
+
+template <int NT, int HT, int SPI, int SCH>
+__device__ __noinline__ void score_close_tile_pruning(const Work& wk, const ScoreItem& item, const float* outq,
+                                                      int tile0, float* red_area, int* sh) {
+  score_close_tile<NT, HT, SPI, SCH, true>(wk, item, outq, tile0, red_area, sh);
+}
+
+template <int NT, int HT, int SPI, int SCH, int MINB, int UNR, bool PRUNE>
 __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   pdl_enter();
   static_assert(SCH % 2 == 0, "splits hold whole record pairs");
@@ -83,8 +187,7 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
   float4* rec = reinterpret_cast<float4*>(score_dyn);                                   // [3 * SPI * SCH / 2]
   float (*red)[SPI > 1 ? NT * HT : 1] = reinterpret_cast<float (*)[SPI > 1 ? NT * HT : 1]>(
       score_dyn + sizeof(float4) * (3 * SPI * SCH / 2));                                // [SPI][NT * HT]
-  __shared__ int s_it, s_last, s_nsurv, s_base;
-  __shared__ int s_surv[NT * HT];  // a tile's surviving hypotheses (pruned rounds)
+  __shared__ int s_it, s_last, s_sh[2];
   const int nitems = wk.item_count[0];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // dynamic work cursor: items differ in cost (partial tiles), and a static
@@ -177,87 +280,8 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     }
     __syncthreads();
     if (s_last) {
-      __threadfence();
-      const int h1 = min(nh, tile0 + NT * HT);
-      float* costq = wk.cost32 + (int64_t)item.q * wk.HCAP;
-      // pruned round: the tile holds the prefix over groups [0, gA) of every
-      // hypothesis; one whose prefix is >= the best cost can never be accepted
-      // by the ordered scan (`cost < best`, posest.py:258: the remaining
-      // groups only add non-negative terms and fp32 addition is monotone), so
-      // the prefix stands as its cost; the others are listed for k_score_tail
-      const int gend = SPI == 1 ? NG : S.gA;
-      const bool pruning = SPI > 1 && gend < NG;
-      const double best = S.best_cost;
-      if (pruning) {
-        if (threadIdx.x == 0) s_nsurv = 0;
-        __syncthreads();
-      }
-      for (int h = tile0 + threadIdx.x; h < h1; h += NT) {
-        // the partials of 4 groups (fine: 16 splits) / 8 groups (coarse) are
-        // loaded before they are added, in the canonical order, so the
-        // closing item waits for a few L2 round trips instead of one per group
-        float c = 0.f;
-        if (SPI == 1) {
-          for (int g0 = 0; g0 < NG; g0 += 4) {
-            float v[4][kGroupSplits];
-#pragma unroll
-            for (int gg = 0; gg < 4; ++gg)
-#pragma unroll
-              for (int k = 0; k < kGroupSplits; ++k) {
-                const int sp = (g0 + gg) * kGroupSplits + k;
-                v[gg][k] = sp < NS ? __ldcg(outq + (int64_t)sp * wk.HCAP + h) : 0.f;
-              }
-#pragma unroll
-            for (int gg = 0; gg < 4; ++gg) {
-              const int g = g0 + gg;
-              if (g < NG) {
-                float gs = v[gg][0];
-#pragma unroll
-                for (int k = 1; k < kGroupSplits; ++k)
-                  if (g * kGroupSplits + k < NS) gs += v[gg][k];
-                c += gs;
-              }
-            }
-          }
-        } else {
-          for (int g0 = 0; g0 < gend; g0 += 8) {
-            float v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = g0 + k < gend ? __ldcg(outq + (int64_t)(g0 + k) * wk.HCAP + h) : 0.f;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (g0 + k < gend) c += v[k];
-          }
-        }
-        costq[h] = c;
-        if (pruning && !((double)c >= best)) s_surv[atomicAdd(&s_nsurv, 1)] = h;
-      }
-      if (pruning) {
-        // append the tile's survivors to the query's list; the query's last
-        // tile to close turns the list into tail tasks of up to 32 hypotheses
-        QState* Sq = wk.qs + item.q;
-        __syncthreads();
-        const int ns_ = s_nsurv;
-        if (threadIdx.x == 0) s_base = ns_ ? atomicAdd(&Sq->nsurv, ns_) : 0;
-        __syncthreads();
-        int* sv = wk.surv + (int64_t)item.q * wk.HCAP;
-        for (int i = threadIdx.x; i < ns_; i += NT) sv[s_base + i] = s_surv[i];
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          const long long rest = (long long)nsub - min((long long)nsub, (long long)gend * kGroupSplits * SCH);
-          atomicAdd(wk.prune_ctr, (unsigned long long)((h1 - tile0 - ns_) * rest));
-          atomicAdd(wk.prune_ctr + 1, (unsigned long long)(ns_ * rest));
-          const int ntile = (nh + NT * HT - 1) / (NT * HT);
-          if (atomicAdd(&Sq->tiles_closed, 1) == ntile - 1) {
-            __threadfence();
-            const int nq = atomicAdd(&Sq->nsurv, 0), ntask = (nq + 31) / 32;
-            const int base = ntask ? atomicAdd(wk.item_count + 3, ntask) : 0;
-            for (int k = 0; k < ntask; ++k)
-              if (base + k < wk.tail_cap) wk.tail[base + k] = TailTask{item.q, 32 * k, min(32, nq - 32 * k), 0};
-          }
-        }
-      }
+      if constexpr (PRUNE) score_close_tile_pruning<NT, HT, SPI, SCH>(wk, item, outq, tile0, &red[0][0], s_sh);
+      else score_close_tile<NT, HT, SPI, SCH, false>(wk, item, outq, tile0, &red[0][0], s_sh);
     }
   }
 }

@@ -45,7 +45,7 @@ double run_variant(Bench& b, const char* name, std::vector<float>& ref, int reps
   int dev = 0, sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int occ = 0;
-  auto kern = k_score2_t<NT, HT, SPI, 128, MINB, UNR>;
+  auto kern = k_score2_t<NT, HT, SPI, 128, MINB, UNR, false>;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0));
   const int grid = sms * occ * grid_mult;
   const float tau2 = 144.f;
