@@ -54,12 +54,13 @@ struct __align__(16) QState {
   int best_cnt_valid, pad_;
   // exact scoring pruning (vl_score.cuh): prune_ok = every fp32 subset weight
   // is >= 0 (MSAC partial sums then only grow), cost_typ = mean fp32 cost of
-  // the last fully scored round, gA = split groups scored for EVERY hypothesis
-  // this round (the rest only for hypotheses whose prefix is below best_cost)
+  // the last fully scored round, sA = splits scored for EVERY hypothesis this
+  // round (the rest only for hypotheses whose prefix is below best_cost)
   float cost_typ;
-  int gA, prune_ok;
+  int sA, prune_ok;
   int nsurv, tiles_closed;  // this round's surviving hypotheses / closed scoring tiles (reset by k_compact)
-  int pad2_[3];
+  float prune_m;            // prefix margin (x best / typical cost), raised when many hypotheses survive
+  int pad2_[2];
 };
 
 struct ScoreItem {
@@ -67,7 +68,7 @@ struct ScoreItem {
 };
 
 // Scoring tail task (pruned rounds): up to 32 surviving hypotheses of one
-// query, listed at surv[q][base .. base + cnt), finished over groups [gA, NG).
+// query, listed at surv[q][base .. base + cnt), finished over splits [sA, NS).
 struct TailTask {
   int q, base, cnt, pad;
 };

@@ -24,6 +24,15 @@
 
 namespace vl {
 
+// Initial phase-A prefix margin of exact scoring pruning: sA / NS = margin x
+// best cost / typical hypothesis cost.  C3 step: 1.08 -> 53.3 ms, 1.05 ->
+// 52.6, 1.03 -> 52.3, 1.00 -> 52.1, 0.97 -> 72.1 (most hypotheses survive the
+// prefix and go to the tail); k_scan raises a query's margin by 10 % after a
+// round in which more than a quarter of its hypotheses survived.
+#ifndef VL_PRUNE_MARGIN
+#define VL_PRUNE_MARGIN 1.03f
+#endif
+
 // ------------------------------------------------------------------ prep
 // The per-query states come straight from the mapped pinned staging buffer
 // (kernel loads over PCIe, not a copy-engine transfer, so a chunk never waits
@@ -76,8 +85,9 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
   w_ok = __syncthreads_and(w_ok);
   if (threadIdx.x == 0) {
     S.prune_ok = w_ok;
-    S.gA = 0;
+    S.sA = 0;
     S.cost_typ = 0.f;
+    S.prune_m = VL_PRUNE_MARGIN;
   }
 }
 
@@ -482,18 +492,18 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
   const int tile_h = fine ? kScoreTileHypsFine : kScoreTileHyps;
   const int spi = fine ? 1 : kScoreItemSplits;
   const int ntile = (nh + tile_h - 1) / tile_h;
-  int ngroups = (S.nsplit + spi - 1) / spi;
   // exact pruning (coarse rounds, a best pose known, non-negative weights):
-  // score the first gA split groups of every hypothesis, where gA / NG is the
-  // best cost over the typical hypothesis cost of the last fully scored round
+  // score the first sA splits of every hypothesis, where sA / NS is the best
+  // cost over the typical hypothesis cost of the last fully scored round
   // (plus 8 %): a typical hypothesis' prefix then already exceeds the best
-  // cost, and only the others are finished (k_score_tail)
-  int gA = ngroups;
+  // cost, and only the others are finished (k_score_tail).  The last phase-A
+  // item of a tile may cover only the first sA mod 4 splits of its group.
+  int sA = S.nsplit;
   if (wk.prune && !fine && S.prune_ok && S.has_best && S.cost_typ > 0.f) {
-    const double f = S.best_cost / (double)S.cost_typ * 1.08;
-    if (f < 1.0) gA = max(1, min(ngroups, (int)ceil(f * ngroups)));
+    const double f = S.best_cost / (double)S.cost_typ * (double)S.prune_m;
+    if (f < 1.0) sA = max(1, min(S.nsplit, (int)ceil(f * S.nsplit)));
   }
-  ngroups = gA;
+  const int ngroups = (sA + spi - 1) / spi;
   // hypothesis-split mode: tile (q, t) belongs to rank (q*TCAP + t) mod size;
   // the other ranks leave its costs at zero for the SUM all-reduce
   const int size = wk.split_size;
@@ -506,7 +516,7 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
       if ((h / tile_h) % size != t0) wk.cost32[(int64_t)q * wk.HCAP + h] = 0.f;
   if (threadIdx.x == 0) {
     S.nh = nh;
-    S.gA = gA;
+    S.sA = sA;
     S.nsurv = 0;
     S.tiles_closed = 0;
     S.hyps += nh;
@@ -519,7 +529,7 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
     it.q = q;
     it.tile = t0 + (i / ngroups) * size;
     it.split = (i % ngroups) * spi;
-    it.nsplit = min(spi, S.nsplit - it.split);
+    it.nsplit = min(spi, sA - it.split);
     const int64_t pos = (int64_t)s_item0 + i;
     if (pos < wk.item_cap) wk.items[pos] = it;
   }
@@ -604,8 +614,9 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   __syncthreads();
   // typical hypothesis cost (mean fp32 cost) of a fully scored round: sizes
   // the next rounds' pruning prefix (k_compact); pruned rounds keep it
-  float cost_typ = S.cost_typ;
-  if (wk.prune && nh > 0 && S.gA * kGroupSplits >= S.nsplit) {
+  float cost_typ = S.cost_typ, prune_m = S.prune_m;
+  if (S.sA < S.nsplit && S.nsurv * 4 > nh) prune_m *= 1.1f;  // pruned round, many survivors
+  if (wk.prune && nh > 0 && S.sA >= S.nsplit) {
     double acc[1] = {0.0};
     for (int h = threadIdx.x; h < nh; h += kScanThreads) acc[0] += (double)costs[h];
     block_sum<kScanThreads, 1>(acc, sm.scratch, sm.red);
@@ -695,6 +706,7 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     S.best_sub_cnt = best_cnt;
     S.best_cnt_valid = has_best ? 1 : 0;
     S.cost_typ = cost_typ;
+    S.prune_m = prune_m;
   }
   // the last cluster to finish compacts the active list for the next round
   // (was a separate one-CTA kernel per round: ~8.6 us of launch + drain per

@@ -85,13 +85,15 @@ __device__ __forceinline__ void score_close_tile(const Work& wk, const ScoreItem
   __threadfence();
   const int h1 = min(nh, tile0 + NT * HT);
   float* costq = wk.cost32 + (int64_t)item.q * wk.HCAP;
-  // pruned round: the tile holds the prefix over groups [0, gA) of every
-  // hypothesis; one whose prefix is >= the best cost can never be accepted
-  // by the ordered scan (`cost < best`, posest.py:258: the remaining
-  // groups only add non-negative terms and fp32 addition is monotone), so
-  // the prefix stands as its cost; the others are listed for k_score_tail
-  const int gend = SPI == 1 ? NG : S.gA;
-  const bool pruning = PRUNE && SPI > 1 && gend < NG;
+  // pruned round: the tile holds the group sums of splits [0, sA) (the last
+  // group possibly partial: the left fold of its first sA mod 4 splits);
+  // their running sum is a lower bound of the final fp32 cost (every later
+  // term and split sum is >= 0, fp32 addition is monotone and the group sum
+  // is a left fold).  A hypothesis whose bound is >= the best cost can never
+  // be accepted by the ordered scan (`cost < best`, posest.py:258), so the
+  // bound stands as its cost; the others are listed for k_score_tail
+  const int gend = SPI == 1 ? NG : (S.sA + kGroupSplits - 1) / kGroupSplits;
+  const bool pruning = PRUNE && SPI > 1 && S.sA < NS;
   const double best = S.best_cost;
   // a tile's surviving hypotheses (pruned rounds), in the split-sum area
   // (coarse items: SPI * NT * HT floats >= NT * HT), free once the ticket is taken
@@ -153,7 +155,7 @@ __device__ __forceinline__ void score_close_tile(const Work& wk, const ScoreItem
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-      const long long rest = (long long)nsub - min((long long)nsub, (long long)gend * kGroupSplits * SCH);
+      const long long rest = (long long)nsub - min((long long)nsub, (long long)S.sA * SCH);
       atomicAdd(wk.prune_ctr, (unsigned long long)((h1 - tile0 - ns_) * rest));
       atomicAdd(wk.prune_ctr + 1, (unsigned long long)(ns_ * rest));
       const int ntile = (nh + NT * HT - 1) / (NT * HT);
@@ -275,7 +277,8 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     const int NS = S.nsplit;
     const int NG = (NS + kGroupSplits - 1) / kGroupSplits;
     if (threadIdx.x == 0) {
-      const int tile_items = SPI == 1 ? NS : S.gA;  // coarse: groups [0, gA) (gA < NG in pruned rounds)
+      // coarse: the groups of splits [0, sA) (sA < NS in pruned rounds)
+      const int tile_items = SPI == 1 ? NS : (S.sA + kGroupSplits - 1) / kGroupSplits;
       s_last = atomicAdd(wk.tile_cnt + (int64_t)item.q * wk.TCAP + item.tile, 1) == tile_items - 1;
     }
     __syncthreads();
@@ -287,12 +290,14 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
 }
 
 // Scoring tail of a pruned round: one CTA per task (up to 32 surviving
-// hypotheses of one tile), lane = hypothesis, warp w = split w of the current
-// split group.  The group's 512 records are staged in shared memory (one
+// hypotheses of one query), lane = hypothesis, warp w = split w of the
+// current split group.  Each survivor's canonical sum is rebuilt from the
+// tile's group slots in the canonical order (full groups of [0, sA), then
+// the left fold of the partial group, continued), and completed over the
+// remaining splits: a group's 512 records are staged in shared memory (one
 // cooperative load, broadcast reads), every warp forms its split sum with the
-// same EVAL2 sequence as k_score2_t, and warp 0 continues each hypothesis'
-// canonical sum from the prefix the tile left in cost32 with the group sums
-// ((p0 + p1) + p2) + p3 over groups [gA, NG) — so the cost bits equal a full
+// same EVAL2 sequence as k_score2_t, and warp 0 folds the group sums
+// ((p0 + p1) + p2) + p3 into the running sum — so the cost bits equal a full
 // scoring.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_score_tail(Work wk, float tau2) {
@@ -312,21 +317,27 @@ __global__ void __launch_bounds__(NT) k_score_tail(Work wk, float tau2) {
     float P[12];
 #pragma unroll
     for (int c = 0; c < 12; ++c) P[c] = Pq[(int64_t)c * wk.HCAP + h];
-    float* cp = wk.cost32 + (int64_t)tk.q * wk.HCAP + h;
-    float c = w == 0 ? *cp : 0.f;
     const int NS = S.nsplit, pn = (S.nsub + 1) >> 1, NG = (NS + kGroupSplits - 1) / kGroupSplits;
+    const int gfull = S.sA / kGroupSplits, k0 = S.sA % kGroupSplits;
+    const float* slot = wk.partial + (int64_t)tk.q * wk.NSPLIT * wk.HCAP + h;  // group g at slot[g * HCAP]
+    float c = 0.f, carry = 0.f;
+    if (w == 0) {
+      for (int g = 0; g < gfull; ++g) c += __ldcg(slot + (int64_t)g * wk.HCAP);
+      if (k0) carry = __ldcg(slot + (int64_t)gfull * wk.HCAP);
+    }
     const float4* src = wk.sub32 + 3 * (S.sub_off >> 1);
-    for (int g = S.gA; g < NG; ++g) {
-      const int p0 = g * GP, np = min(GP, pn - p0);
+    for (int g = gfull; g < NG; ++g) {
+      const int kf = g == gfull ? k0 : 0;  // first split of the group still to score
+      const int p0 = g * GP + kf * (kScoreChunk / 2), np = min(GP, pn - g * GP) - kf * (kScoreChunk / 2);
       __syncthreads();  // the previous group's records and split sums are consumed
       for (int k = threadIdx.x; k < 3 * np; k += NT) rec[k] = src[3 * p0 + k];
       __syncthreads();
       const int sp = g * kGroupSplits + w;
-      if (sp < NS) {
+      if (w >= kf && sp < NS) {
         float2 acc = make_float2(0.f, 0.f);
-        const int pe = min((w + 1) * (kScoreChunk / 2), np);
+        const int pb = (w - kf) * (kScoreChunk / 2), pe = min(pb + kScoreChunk / 2, np);
 #pragma unroll 4
-        for (int p = w * (kScoreChunk / 2); p < pe; ++p) {
+        for (int p = pb; p < pe; ++p) {
           const float4 r0 = rec[3 * p], r1 = rec[3 * p + 1], r2 = rec[3 * p + 2];
           const float2 X2 = make_float2(r0.x, r0.y), Y2 = make_float2(r0.z, r0.w);
           const float2 Z2 = make_float2(r1.x, r1.y), A2 = make_float2(r1.z, r1.w);
@@ -337,13 +348,13 @@ __global__ void __launch_bounds__(NT) k_score_tail(Work wk, float tau2) {
       }
       __syncthreads();
       if (w == 0) {
-        float gs = red[0][lane];
-        for (int k = 1; k < kGroupSplits; ++k)
+        float gs = kf ? carry : red[0][lane];
+        for (int k = kf ? kf : 1; k < kGroupSplits; ++k)
           if (g * kGroupSplits + k < NS) gs += red[k][lane];  // ((p0 + p1) + p2) + p3
         c += gs;
       }
     }
-    if (w == 0 && on) *cp = c;
+    if (w == 0 && on) wk.cost32[(int64_t)tk.q * wk.HCAP + h] = c;
   }
 }
 
