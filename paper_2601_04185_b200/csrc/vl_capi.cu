@@ -786,6 +786,7 @@ int vl_score_hypotheses(vl_ctx* c, const double* R, const double* t, int32_t H, 
   int rc;
   if ((rc = ensure(c, c->qs, sizeof(QState))) || (rc = ensure(c, c->items, ntile * S.nsplit * sizeof(ScoreItem))) ||
       (rc = ensure(c, c->item_count, 4 * sizeof(int))) || (rc = ensure(c, c->P32, 12 * HCAP * sizeof(float))) ||
+      (rc = ensure(c, c->hsrc, HCAP * sizeof(int))) ||
       (rc = ensure(c, c->partial, (size_t)S.nsplit * HCAP * sizeof(float))) ||
       (rc = ensure(c, c->cost32, HCAP * sizeof(float))) || (rc = ensure(c, c->tile_cnt, ntile * sizeof(int))) ||
       (rc = ensure(c, c->sub_pk, nsub_pad * 3 * sizeof(double2))) ||
@@ -797,6 +798,7 @@ int vl_score_hypotheses(vl_ctx* c, const double* R, const double* t, int32_t H, 
   wk.items = (ScoreItem*)c->items.p;
   wk.item_count = (int*)c->item_count.p;
   wk.P32 = (float*)c->P32.p;
+  wk.hsrc = (int*)c->hsrc.p;
   wk.partial = (float*)c->partial.p;
   wk.cost32 = (float*)c->cost32.p;
   wk.tile_cnt = (int*)c->tile_cnt.p;

@@ -231,6 +231,24 @@ struct CandRec {
   int lane, pad;
 };
 
+// fp32 scoring row of one hypothesis: diag(fx, fy, 1) [R | t] (R row-major,
+// t in sl[9..11]), folded in fp64 and rounded once, stored SoA with column
+// stride cs (k_score reads entry c of hypothesis h at P[c * cs + h]).
+__device__ __forceinline__ void store_p32(float* P, int64_t cs, double fx, double fy, const double* sl, int es = 1) {
+  P[0 * cs] = (float)(fx * sl[0 * es]);
+  P[1 * cs] = (float)(fx * sl[1 * es]);
+  P[2 * cs] = (float)(fx * sl[2 * es]);
+  P[3 * cs] = (float)(fx * sl[9 * es]);
+  P[4 * cs] = (float)(fy * sl[3 * es]);
+  P[5 * cs] = (float)(fy * sl[4 * es]);
+  P[6 * cs] = (float)(fy * sl[5 * es]);
+  P[7 * cs] = (float)(fy * sl[10 * es]);
+  P[8 * cs] = (float)sl[6 * es];
+  P[9 * cs] = (float)sl[7 * es];
+  P[10 * cs] = (float)sl[8 * es];
+  P[11 * cs] = (float)sl[11 * es];
+}
+
 #ifndef VL_P3P_ROOT_MINB
 #define VL_P3P_ROOT_MINB 5  // measured: 5 resident CTAs (96 regs) beat 4 (112 regs)
 #endif
@@ -337,6 +355,8 @@ __global__ void __launch_bounds__(kP3PThreads, VL_P3P_POLISH_MINB) k_p3p_polish(
       }
       if (dup) continue;
       for (int i = 0; i < 12; ++i) slot[32 * (12 * kept + i)] = rr[i];
+      // the fp32 scoring row, at P32 column kept * B + s of the query
+      store_p32(wk.P32 + (int64_t)q * 12 * wk.HCAP + (int64_t)kept * wk.B + s, wk.HCAP, S.in.fx, S.in.fy, rr);
       ++kept;
     }
     __syncwarp();
@@ -411,24 +431,6 @@ int launch_p3p_batch(const double* f, const double* P, int B, double* slots, int
   return 2;
 }
 
-// fp32 scoring row of one hypothesis: diag(fx, fy, 1) [R | t] (R row-major,
-// t in sl[9..11]), folded in fp64 and rounded once, stored SoA with column
-// stride cs (k_score reads entry c of hypothesis h at P[c * cs + h]).
-__device__ __forceinline__ void store_p32(float* P, int64_t cs, double fx, double fy, const double* sl, int es = 1) {
-  P[0 * cs] = (float)(fx * sl[0 * es]);
-  P[1 * cs] = (float)(fx * sl[1 * es]);
-  P[2 * cs] = (float)(fx * sl[2 * es]);
-  P[3 * cs] = (float)(fx * sl[9 * es]);
-  P[4 * cs] = (float)(fy * sl[3 * es]);
-  P[5 * cs] = (float)(fy * sl[4 * es]);
-  P[6 * cs] = (float)(fy * sl[5 * es]);
-  P[7 * cs] = (float)(fy * sl[10 * es]);
-  P[8 * cs] = (float)sl[6 * es];
-  P[9 * cs] = (float)sl[7 * es];
-  P[10 * cs] = (float)sl[8 * es];
-  P[11 * cs] = (float)sl[11 * es];
-}
-
 // Standalone scoring (vl_score_hypotheses): rows of caller-given hypotheses
 // for query 0 of a one-query workspace, plus that round's score items.
 __global__ void k_hyp_rows(Work wk, const double* R, const double* t, int H, int fine) {
@@ -438,6 +440,7 @@ __global__ void k_hyp_rows(Work wk, const double* R, const double* t, int H, int
     for (int i = 0; i < 9; ++i) sl[i] = R[9 * (int64_t)h + i];
     for (int i = 0; i < 3; ++i) sl[9 + i] = t[3 * (int64_t)h + i];
     store_p32(wk.P32 + h, wk.HCAP, S.in.fx, S.in.fy, sl);
+    wk.hsrc[h] = h;  // P32 column of hypothesis h
   }
   const int tile_h = fine ? kScoreTileHypsFine : kScoreTileHyps;
   const int spi = fine ? 1 : kScoreItemSplits;
@@ -472,18 +475,15 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
   const int q = wk.active_list[blockIdx.x];
   QState& S = wk.qs[q];
   const int bn = S.batch_n;
-  const double fx = S.in.fx, fy = S.in.fy;
   int running = 0;
   for (int base = 0; base < bn; base += NT) {
     const int s = base + threadIdx.x;
     const int c = s < bn ? wk.slot_cnt[(int64_t)q * wk.B + s] : 0;
     int total;
     const int ex = block_excl_scan<NT>(c, warp_tot, total);
-    for (int k = 0; k < c; ++k) {
-      const int h = running + ex + k;
-      wk.hsrc[(int64_t)q * wk.HCAP + h] = s * 4 + k;
-      store_p32(wk.P32 + (int64_t)q * 12 * wk.HCAP + h, wk.HCAP, fx, fy, slot_ptr(wk, q, s, k), 32);
-    }
+    // hypothesis h -> its solution slot and P32 column k * B + s (the fp32
+    // rows were written there by k_p3p_polish)
+    for (int k = 0; k < c; ++k) wk.hsrc[(int64_t)q * wk.HCAP + running + ex + k] = k * wk.B + s;
     running += total;
   }
   const int nh = running;
@@ -653,8 +653,8 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     best_cost = (double)costs[found];
     has_best = 1;
     if (threadIdx.x == 0) {
-      const int src = wk.hsrc[(int64_t)q * wk.HCAP + found];
-      const double* sp = slot_ptr(wk, q, src >> 2, src & 3);
+      const int src = wk.hsrc[(int64_t)q * wk.HCAP + found];  // k * B + s
+      const double* sp = slot_ptr(wk, q, src % wk.B, src / wk.B);
       double sl[12];
 #pragma unroll
       for (int i = 0; i < 12; ++i) sl[i] = sp[32 * i];

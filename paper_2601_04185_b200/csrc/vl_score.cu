@@ -31,9 +31,6 @@
 namespace vl {
 
 // coarse: 768-hypothesis tiles x 512 correspondences (big batches)
-#ifndef VL_SCORE_MINB
-#define VL_SCORE_MINB 3
-#endif
 #ifndef VL_SCORE_UNR
 #define VL_SCORE_UNR 2
 #endif

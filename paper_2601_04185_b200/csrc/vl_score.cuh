@@ -4,6 +4,11 @@
 
 namespace vl {
 
+// resident CTAs per SM of the coarse scorer (vl_score.cu)
+#ifndef VL_SCORE_MINB
+#define VL_SCORE_MINB 3
+#endif
+
 // ---------------------------------------------------------------- f32x2 path
 // Blackwell packed FP32 (FFMA2 / FMUL2): one instruction evaluates the same
 // step for TWO CORRESPONDENCES of one hypothesis.  Records are stored in
@@ -176,8 +181,21 @@ __device__ __noinline__ void score_close_tile_pruning(const Work& wk, const Scor
   score_close_tile<NT, HT, SPI, SCH, true>(wk, item, outq, tile0, red_area, sh);
 }
 
+// Register cap of the scorer: 160 fits 3 CTAs of 128 threads per SM (the
+// MINB of __launch_bounds__, which would allow 168).  C3 step at 168 / 160 /
+// 152: 93.9 / 93.3 / 94.0 ms (the instance without pruning code then uses
+// 154 registers, no spills).  0 = __launch_bounds__(NT, MINB) alone.
+#ifndef VL_SCORE_MAXNREG
+#define VL_SCORE_MAXNREG 160
+#endif
+#if VL_SCORE_MAXNREG > 0
+// (the fine instance keeps its occupancy bound: 65536 / (NT x MINB) rounded down to 8)
+#define VL_SCORE_BOUNDS(NT, MINB) __maxnreg__((MINB) == VL_SCORE_MINB ? VL_SCORE_MAXNREG : 65536 / ((NT) * (MINB)) / 8 * 8)
+#else
+#define VL_SCORE_BOUNDS(NT, MINB) __launch_bounds__(NT, MINB)
+#endif
 template <int NT, int HT, int SPI, int SCH, int MINB, int UNR, bool PRUNE>
-__global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
+__global__ void VL_SCORE_BOUNDS(NT, MINB) k_score2_t(Work wk, float tau2) {
   pdl_enter();
   static_assert(SCH % 2 == 0, "splits hold whole record pairs");
   constexpr int NW = NT / 32;
@@ -224,12 +242,15 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     float P[HT][12];
     // hypotheses hid0 .. hid0 + HT - 1 of this thread (thread-contiguous)
     const int hid0 = tile0 + hs * WHYP + lane * HT;
+    // hypothesis h's fp32 row sits at P32 column hsrc[h] (k_p3p_polish wrote
+    // it at its solution slot; k_compact only orders the hypotheses)
     const float* Pq = wk.P32 + (int64_t)item.q * 12 * wk.HCAP;
+    const int* hq = wk.hsrc + (int64_t)item.q * wk.HCAP;
 #pragma unroll
     for (int j = 0; j < HT; ++j) {
-      const int h = hid0 + j < nh ? hid0 + j : 0;
+      const int col = __ldg(hq + (hid0 + j < nh ? hid0 + j : 0));
 #pragma unroll
-      for (int c = 0; c < 12; ++c) P[j][c] = Pq[(int64_t)c * wk.HCAP + h];
+      for (int c = 0; c < 12; ++c) P[j][c] = Pq[(int64_t)c * wk.HCAP + col];
     }
     __syncthreads();
     for (int s = grp; s < ns && grp < G; s += G) {
@@ -275,7 +296,6 @@ __global__ void __launch_bounds__(NT, MINB) k_score2_t(Work wk, float tau2) {
     __threadfence();
     __syncthreads();
     const int NS = S.nsplit;
-    const int NG = (NS + kGroupSplits - 1) / kGroupSplits;
     if (threadIdx.x == 0) {
       // coarse: the groups of splits [0, sA) (sA < NS in pruned rounds)
       const int tile_items = SPI == 1 ? NS : (S.sA + kGroupSplits - 1) / kGroupSplits;
@@ -314,9 +334,10 @@ __global__ void __launch_bounds__(NT) k_score_tail(Work wk, float tau2) {
     const bool on = lane < tk.cnt;
     const int h = wk.surv[(int64_t)tk.q * wk.HCAP + tk.base + (on ? lane : 0)];
     const float* Pq = wk.P32 + (int64_t)tk.q * 12 * wk.HCAP;
+    const int col = wk.hsrc[(int64_t)tk.q * wk.HCAP + h];
     float P[12];
 #pragma unroll
-    for (int c = 0; c < 12; ++c) P[c] = Pq[(int64_t)c * wk.HCAP + h];
+    for (int c = 0; c < 12; ++c) P[c] = Pq[(int64_t)c * wk.HCAP + col];
     const int NS = S.nsplit, pn = (S.nsub + 1) >> 1, NG = (NS + kGroupSplits - 1) / kGroupSplits;
     const int gfull = S.sA / kGroupSplits, k0 = S.sA % kGroupSplits;
     const float* slot = wk.partial + (int64_t)tk.q * wk.NSPLIT * wk.HCAP + h;  // group g at slot[g * HCAP]
