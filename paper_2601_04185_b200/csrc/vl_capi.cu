@@ -483,7 +483,8 @@ static int round_loop_lookahead(vl_ctx* c, const Work& wk, const Inputs& in, con
   volatile int* h_count = (volatile int*)((char*)c->h_pinned + c->h_pinned_cap - 16);
   int nlaunch = Qn;
   int64_t r = 0;
-  c->launches += launch_round(wk, in, p, nlaunch, c->num_sms, st, nullptr, nullptr, 0);
+  // the first round splits (head / rest) for the queries that have no best pose yet
+  c->launches += launch_round(wk, in, p, nlaunch, c->num_sms, st, nullptr, nullptr, 0, 1);
   VL_CUDA(c, cudaEventRecord(c->round_ev[0], st));
   while (true) {
     c->launches += launch_round(wk, in, p, nlaunch, c->num_sms, st, nullptr, nullptr, 0);
@@ -520,7 +521,7 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
     int guard = 0;
     if (c->prof) {  // per-stage event brackets: one round in flight at a time
       while (nactive > 0) {
-        c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c, 0);
+        c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c, 0, guard == 0);
         if ((rc = check_launch(c))) return rc;
         if ((rc = read_active(c, wk, st, &nactive))) return rc;
         if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
@@ -563,6 +564,7 @@ static int staged_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, 
   int admitted = 0, nactive = 0, guard = 0;
   while (true) {
     // admit every stage whose copy has landed (block on the next one only when idle)
+    const int admitted0 = admitted;
     while (admitted < nstage) {
       cudaEvent_t ev = evs[admitted];
       if (nactive > 0) {
@@ -584,7 +586,8 @@ static int staged_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, 
       if ((rc = round_loop_lookahead(c, wk, in, p, nactive, max_rounds, st))) return rc;
       break;
     }
-    c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c, 0);
+    // (a round right after an admission splits for the new queries)
+    c->launches += launch_round(wk, in, p, nactive, c->num_sms, st, prof_hook, c, 0, admitted > admitted0);
     if ((rc = check_launch(c))) return rc;
     if ((rc = read_active(c, wk, st, &nactive))) return rc;
     if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
@@ -779,6 +782,8 @@ int vl_score_hypotheses(vl_ctx* c, const double* R, const double* t, int32_t H, 
   S.nsplit = (int)((n + kScoreChunk - 1) / kScoreChunk);
   S.in = Intr{intr.fx, intr.fy, intr.cx, intr.cy};
   S.nh = H;
+  S.h_lo = 0;
+  S.h_hi = H;
   // tile shape: the one the estimator picks for a lone query (fine), or forced
   const int fine = shape == 2 ? 0 : 1;
   const int64_t HCAP = H, ntile = (H + kScoreTileHypsFine - 1) / kScoreTileHypsFine;

@@ -60,7 +60,7 @@ struct __align__(16) QState {
   int sA, prune_ok;
   int nsurv, tiles_closed;  // this round's surviving hypotheses / closed scoring tiles (reset by k_compact)
   float prune_m;            // prefix margin (x best / typical cost), raised when many hypotheses survive
-  int pad2_[2];
+  int h_lo, h_hi;           // hypotheses [h_lo, h_hi) scored / scanned in this launch phase (head / rest / full)
 };
 
 struct ScoreItem {
@@ -164,9 +164,12 @@ int launch_prep(const Work& wk, const Inputs& in, int q0, int nq, int list_pos, 
 // profiling stages (vl_profile_read order)
 enum { kStagePrep = 0, kStageSample, kStageP3P, kStageCompact, kStageScore, kStageScan, kStageActive,
        kStageFinal, kStageLift, kNumStages };
-// phase 0: whole round; 1: sample .. score; 2: scan + active (stepwise driver)
+// phase 0: whole round; 1: sample .. score; 2: scan + active (stepwise driver).
+// split (phase 0, pruning on, coarse rounds): queries without a best pose
+// first score and scan their first kHeadHyps hypotheses, so the rest of the
+// round is already pruned against that best (vl_ransac.cu, k_compact)
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
-                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg, int phase);
+                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg, int phase, int split = 0);
 int launch_final(const Work& wk, const Inputs& in, const Outputs& out, const RansacParams& p, int Q,
                  int q_base, cudaStream_t st);
 

@@ -466,32 +466,51 @@ int launch_hyp_rows(const Work& wk, const double* R, const double* t, int H, int
   return 1;
 }
 
+// mode 0 (full round): order the hypotheses, items for all of them.  Split
+// rounds: mode 1 (head) orders them and emits items only for the first
+// kHeadHyps of queries without a best pose; mode 2 (rest) emits the items of
+// the remaining hypotheses (all of them for queries that had a best pose),
+// pruned against the best the head scan found.
+#ifndef VL_HEAD_HYPS
+#define VL_HEAD_HYPS 384
+#endif
+constexpr int kHeadHyps = VL_HEAD_HYPS;
+
 template <int NT>
-__global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
+__global__ void __launch_bounds__(NT) k_compact(Work wk, int fine, int mode) {
   pdl_enter();
   __shared__ int warp_tot[32];
   __shared__ int s_item0;
   if ((int)blockIdx.x >= *wk.active_count) return;
   const int q = wk.active_list[blockIdx.x];
   QState& S = wk.qs[q];
-  const int bn = S.batch_n;
-  int running = 0;
-  for (int base = 0; base < bn; base += NT) {
-    const int s = base + threadIdx.x;
-    const int c = s < bn ? wk.slot_cnt[(int64_t)q * wk.B + s] : 0;
-    int total;
-    const int ex = block_excl_scan<NT>(c, warp_tot, total);
-    // hypothesis h -> its solution slot and P32 column k * B + s (the fp32
-    // rows were written there by k_p3p_polish)
-    for (int k = 0; k < c; ++k) wk.hsrc[(int64_t)q * wk.HCAP + running + ex + k] = k * wk.B + s;
-    running += total;
+  int nh;
+  if (mode != 2) {
+    const int bn = S.batch_n;
+    int running = 0;
+    for (int base = 0; base < bn; base += NT) {
+      const int s = base + threadIdx.x;
+      const int c = s < bn ? wk.slot_cnt[(int64_t)q * wk.B + s] : 0;
+      int total;
+      const int ex = block_excl_scan<NT>(c, warp_tot, total);
+      // hypothesis h -> its solution slot and P32 column k * B + s (the fp32
+      // rows were written there by k_p3p_polish)
+      for (int k = 0; k < c; ++k) wk.hsrc[(int64_t)q * wk.HCAP + running + ex + k] = k * wk.B + s;
+      running += total;
+    }
+    nh = running;
+  } else {
+    nh = S.nh;
   }
-  const int nh = running;
+  int lo = 0, hi = nh;
+  if (mode == 1) hi = S.has_best ? 0 : min(nh, kHeadHyps);
+  else if (mode == 2) lo = S.h_hi;
   // score work items: coarse (768-hypothesis tiles x 4 splits) for big batches,
-  // fine (256 x 1) when the batch is too small to fill the GPU otherwise
+  // fine (256 x 1) when the batch is too small to fill the GPU otherwise;
+  // tiles count from h_lo
   const int tile_h = fine ? kScoreTileHypsFine : kScoreTileHyps;
   const int spi = fine ? 1 : kScoreItemSplits;
-  const int ntile = (nh + tile_h - 1) / tile_h;
+  const int ntile = (hi - lo + tile_h - 1) / tile_h;
   // exact pruning (coarse rounds, a best pose known, non-negative weights):
   // score the first sA splits of every hypothesis, where sA / NS is the best
   // cost over the typical hypothesis cost of the last fully scored round
@@ -499,7 +518,7 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
   // cost, and only the others are finished (k_score_tail).  The last phase-A
   // item of a tile may cover only the first sA mod 4 splits of its group.
   int sA = S.nsplit;
-  if (wk.prune && !fine && S.prune_ok && S.has_best && S.cost_typ > 0.f) {
+  if (mode != 1 && wk.prune && !fine && S.prune_ok && S.has_best && S.cost_typ > 0.f) {
     const double f = S.best_cost / (double)S.cost_typ * (double)S.prune_m;
     if (f < 1.0) sA = max(1, min(S.nsplit, (int)ceil(f * S.nsplit)));
   }
@@ -515,12 +534,16 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine) {
     for (int h = threadIdx.x; h < nh; h += NT)
       if ((h / tile_h) % size != t0) wk.cost32[(int64_t)q * wk.HCAP + h] = 0.f;
   if (threadIdx.x == 0) {
-    S.nh = nh;
+    if (mode != 2) {
+      S.nh = nh;
+      S.hyps += nh;
+      S.evals += (int64_t)nh * S.nsub;
+    }
+    S.h_lo = lo;
+    S.h_hi = hi;
     S.sA = sA;
     S.nsurv = 0;
     S.tiles_closed = 0;
-    S.hyps += nh;
-    S.evals += (int64_t)nh * S.nsub;
     s_item0 = nitems > 0 ? atomicAdd(wk.item_count, nitems) : 0;
   }
   __syncthreads();
@@ -587,7 +610,10 @@ __device__ void compact_active(Work wk, int nactive) {
 // costs_smem: the round's fp32 costs are copied to shared memory (HCAP floats
 // after the staging ring) unless a huge batch_size would not fit, in which
 // case the scan reads them from L2.
-__global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, RansacParams p, int costs_smem) {
+// mode (k_compact's): 0 full round, 1 head of a split round (hypotheses
+// [h_lo, h_hi) only; no stop rule, the active list stays), 2 rest of it.
+__global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, RansacParams p, int costs_smem,
+                                                                  int mode) {
   pdl_enter();
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   double2* ring = reinterpret_cast<double2*>(dyn_smem);  // kStageBytes (TMA staging ring)
@@ -602,25 +628,25 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   if ((int)(blockIdx.x / cl_size()) >= nlist) return;  // whole cluster
   const int q = wk.active_list[blockIdx.x / cl_size()];
   QState& S = wk.qs[q];
-  const int nh = S.nh;
+  const int hlo = S.h_lo, nh = S.h_hi;  // this phase's hypotheses [hlo, nh)
   // final fp32 costs (canonical order, reduced by the scorer's tile tickets)
   const float* cq = wk.cost32 + (int64_t)q * wk.HCAP;
   const float* costs = cq;
   if (costs_smem) {
     float* cs = reinterpret_cast<float*>(dyn_smem + kStageBytes);  // [HCAP]
-    for (int h = threadIdx.x; h < nh; h += kScanThreads) cs[h] = __ldcg(cq + h);
+    for (int h = hlo + threadIdx.x; h < nh; h += kScanThreads) cs[h] = __ldcg(cq + h);
     costs = cs;
   }
   __syncthreads();
-  // typical hypothesis cost (mean fp32 cost) of a fully scored round: sizes
-  // the next rounds' pruning prefix (k_compact); pruned rounds keep it
+  // typical hypothesis cost (mean fp32 cost) of fully scored hypotheses: sizes
+  // the next pruning prefix (k_compact); pruned phases keep it
   float cost_typ = S.cost_typ, prune_m = S.prune_m;
-  if (S.sA < S.nsplit && S.nsurv * 4 > nh) prune_m *= 1.1f;  // pruned round, many survivors
-  if (wk.prune && nh > 0 && S.sA >= S.nsplit) {
+  if (S.sA < S.nsplit && S.nsurv * 4 > nh - hlo) prune_m *= 1.1f;  // pruned, many survivors
+  if (wk.prune && nh > hlo && S.sA >= S.nsplit) {
     double acc[1] = {0.0};
-    for (int h = threadIdx.x; h < nh; h += kScanThreads) acc[0] += (double)costs[h];
+    for (int h = hlo + threadIdx.x; h < nh; h += kScanThreads) acc[0] += (double)costs[h];
     block_sum<kScanThreads, 1>(acc, sm.scratch, sm.red);
-    const double m = sm.red[0] / nh;
+    const double m = sm.red[0] / (nh - hlo);
     cost_typ = m < 3.0e38 ? (float)m : 0.f;
     __syncthreads();
   }
@@ -632,7 +658,7 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   int64_t lo_calls = 0;
   int64_t best_cnt = S.best_cnt_valid ? S.best_sub_cnt : -1;  // -1: not known for `best`
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int h0 = 0;
+  int h0 = hlo;
   while (h0 < nh) {
     int found = INT_MAX;
     for (int base = h0; base < nh; base += kScanThreads) {
@@ -681,7 +707,7 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     __syncthreads();
   }
   int active = 1;
-  if (has_best) {
+  if (mode != 1 && has_best) {
     // the stop rule's subset inlier count (posest.py:269-273): computed once
     // per best pose — an unchanged best (most rounds after the first) or a
     // best just set by an accepted LO (its msac pass above) reuses the count,
@@ -702,9 +728,9 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     S.has_best = has_best;
     S.best = best;
     S.lo_calls += lo_calls;
-    S.active = active;
+    if (mode != 1) S.active = active;  // (head phase: the round goes on)
     S.best_sub_cnt = best_cnt;
-    S.best_cnt_valid = has_best ? 1 : 0;
+    S.best_cnt_valid = best_cnt >= 0 ? 1 : 0;
     S.cost_typ = cost_typ;
     S.prune_m = prune_m;
   }
@@ -719,7 +745,11 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     __syncthreads();
     if (s_last) {
       __threadfence();
-      compact_active<kScanThreads>(wk, nlist);
+      if (mode != 1) {
+        compact_active<kScanThreads>(wk, nlist);
+      } else if (threadIdx.x == 0) {  // head phase: only the work counters restart
+        wk.item_count[0] = wk.item_count[1] = wk.item_count[2] = wk.item_count[3] = 0;
+      }
     }
   }
 }
@@ -857,47 +887,40 @@ int launch_split_apply_argmin(const Work& wk, int nactive, const long long* keys
 // One round, kernel by kernel; `hook(stage, begin)` lets the caller bracket
 // each launch with CUDA events (profiling) without touching the kernels.
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
-                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg, int phase) {
+                 cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg, int phase, int split) {
   auto H = [&](int stage, bool begin) {
     if (hook) hook(hook_arg, stage, begin);
   };
   int n = 0;
   const int fine = round_is_fine(wk, nactive, num_sms) ? 1 : 0;
   const bool pdl = use_pdl(nactive) && !hook;  // (profiling brackets every launch with events)
-  if (phase != 2) {
-    H(kStageSample, true);
-    if (nactive * 4 <= num_sms) launch_k(k_sample<1024>, dim3(nactive), 1024, st, pdl, wk, p);
-    else launch_k(k_sample<256>, dim3(nactive), 256, st, pdl, wk, p);
-    H(kStageSample, false);
-    H(kStageP3P, true);
-    dim3 gr(nactive, (wk.B + kP3PRootThreads - 1) / kP3PRootThreads);
-    launch_k(k_p3p_roots, gr, kP3PRootThreads, st, pdl, wk, in);
-    dim3 gp(nactive, (wk.B + kP3PThreads - 1) / kP3PThreads);
-    launch_k(k_p3p_polish, gp, kP3PThreads, st, pdl, wk);
-    H(kStageP3P, false);
+  // split round (pruning on, coarse items, phase 0): head then rest (k_compact)
+  const bool two = split && phase == 0 && wk.prune && !fine && kHeadHyps > 0;
+  auto compact = [&](int mode) {
     H(kStageCompact, true);
-    {
-      // threads per CTA (A/B knob VISLOC_COMPACT_NT: 256 / 512 / 1024); C3:
-      // 256 -> 1.39 ms/step, 512 -> 1.63, 1024 -> 1.47 (spills at the 64-register
-      // cap); a few queries (C4) take one 1024-thread pass: 2.3 vs 2.8 ms at 256
-      static int cnt = -1;
-      if (cnt < 0) {
-        const char* e = getenv("VISLOC_COMPACT_NT");
-        cnt = e ? atoi(e) : 256;
-      }
-      // up to 2 queries per SM (C5: 256, C4: 1): one 1024-thread pass per query
-      // (C5 compact 0.096 -> 0.037 ms); big batches (C3: 1000) at 256 threads
-      if (nactive <= 2 * num_sms) launch_k(k_compact<1024>, dim3(nactive), 1024, st, pdl, wk, fine);
-      else if (cnt == 256) launch_k(k_compact<256>, dim3(nactive), 256, st, pdl, wk, fine);
-      else if (cnt == 512) launch_k(k_compact<512>, dim3(nactive), 512, st, pdl, wk, fine);
-      else launch_k(k_compact<1024>, dim3(nactive), 1024, st, pdl, wk, fine);
+    // threads per CTA (A/B knob VISLOC_COMPACT_NT: 256 / 512 / 1024); C3:
+    // 256 -> 1.39 ms/step, 512 -> 1.63, 1024 -> 1.47 (spills at the 64-register
+    // cap); a few queries (C4) take one 1024-thread pass: 2.3 vs 2.8 ms at 256
+    static int cnt = -1;
+    if (cnt < 0) {
+      const char* e = getenv("VISLOC_COMPACT_NT");
+      cnt = e ? atoi(e) : 256;
     }
+    // up to 2 queries per SM (C5: 256, C4: 1): one 1024-thread pass per query
+    // (C5 compact 0.096 -> 0.037 ms); big batches (C3: 1000) at 256 threads
+    if (nactive <= 2 * num_sms) launch_k(k_compact<1024>, dim3(nactive), 1024, st, pdl, wk, fine, mode);
+    else if (cnt == 256) launch_k(k_compact<256>, dim3(nactive), 256, st, pdl, wk, fine, mode);
+    else if (cnt == 512) launch_k(k_compact<512>, dim3(nactive), 512, st, pdl, wk, fine, mode);
+    else launch_k(k_compact<1024>, dim3(nactive), 1024, st, pdl, wk, fine, mode);
     H(kStageCompact, false);
+    n += 1;
+  };
+  auto score = [&]() {
     H(kStageScore, true);
-    n += 4 + launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, nactive, st, pdl);  // (+ pruning tail)
+    n += launch_score(wk, (float)(p.tau * p.tau), num_sms, fine, nactive, st, pdl);  // (+ pruning tail)
     H(kStageScore, false);
-  }
-  if (phase != 1) {
+  };
+  auto scan = [&](int mode) {
     H(kStageScan, true);
     // function attributes are per device: set once for each device used
     // (host threads driving separate contexts may get here together)
@@ -927,10 +950,34 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     // 1000-query C3 scan stays one CTA per query: clusters measured slower)
     if (cs == 1 && nactive <= VL_LO_MINB * num_sms) cs = 2;
     if (const char* e = getenv("VISLOC_SCAN_CS")) cs = atoi(e);  // tuning knob
-    launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, pdl, wk, p, costs_smem);  // + active-list compaction
+    // (+ active-list compaction, except after a head phase)
+    launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, pdl, wk, p, costs_smem, mode);
     H(kStageScan, false);
     n += 1;
+  };
+  if (phase != 2) {
+    H(kStageSample, true);
+    if (nactive * 4 <= num_sms) launch_k(k_sample<1024>, dim3(nactive), 1024, st, pdl, wk, p);
+    else launch_k(k_sample<256>, dim3(nactive), 256, st, pdl, wk, p);
+    H(kStageSample, false);
+    H(kStageP3P, true);
+    dim3 gr(nactive, (wk.B + kP3PRootThreads - 1) / kP3PRootThreads);
+    launch_k(k_p3p_roots, gr, kP3PRootThreads, st, pdl, wk, in);
+    dim3 gp(nactive, (wk.B + kP3PThreads - 1) / kP3PThreads);
+    launch_k(k_p3p_polish, gp, kP3PThreads, st, pdl, wk);
+    H(kStageP3P, false);
+    n += 3;
+    if (two) {
+      compact(1);
+      score();
+      scan(1);
+      compact(2);
+    } else {
+      compact(0);
+    }
+    score();
   }
+  if (phase != 1) scan(two ? 2 : 0);
   return n;
 }
 

@@ -84,7 +84,7 @@ template <int NT, int HT, int SPI, int SCH, bool PRUNE>
 __device__ __forceinline__ void score_close_tile(const Work& wk, const ScoreItem& item, const float* outq, int tile0,
                                                float* red_area, int* sh) {
   const QState& S = wk.qs[item.q];
-  const int nh = S.nh, nsub = S.nsub;
+  const int nh = S.h_hi, nsub = S.nsub;
   const int NS = S.nsplit;
   const int NG = (NS + kGroupSplits - 1) / kGroupSplits;
   __threadfence();
@@ -163,7 +163,7 @@ __device__ __forceinline__ void score_close_tile(const Work& wk, const ScoreItem
       const long long rest = (long long)nsub - min((long long)nsub, (long long)S.sA * SCH);
       atomicAdd(wk.prune_ctr, (unsigned long long)((h1 - tile0 - ns_) * rest));
       atomicAdd(wk.prune_ctr + 1, (unsigned long long)(ns_ * rest));
-      const int ntile = (nh + NT * HT - 1) / (NT * HT);
+      const int ntile = (nh - S.h_lo + NT * HT - 1) / (NT * HT);
       if (atomicAdd(&Sq->tiles_closed, 1) == ntile - 1) {
         __threadfence();
         const int nq = atomicAdd(&Sq->nsurv, 0), ntask = (nq + 31) / 32;
@@ -219,8 +219,8 @@ __global__ void VL_SCORE_BOUNDS(NT, MINB) k_score2_t(Work wk, float tau2) {
     if (it >= nitems) break;
     const ScoreItem item = wk.items[it];
     const QState& S = wk.qs[item.q];
-    const int nh = S.nh, nsub = S.nsub;
-    const int tile0 = item.tile * (NT * HT);
+    const int nh = S.h_hi, nsub = S.nsub;  // this phase's hypotheses end at h_hi; tiles count from h_lo
+    const int tile0 = S.h_lo + item.tile * (NT * HT);
     const int ns = item.nsplit;
     float* outq = wk.partial + (int64_t)item.q * wk.NSPLIT * wk.HCAP;
     // partial slot layout: fine items (SPI == 1) write one slot per split;

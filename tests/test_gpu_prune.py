@@ -125,3 +125,41 @@ def test_pruned_batch_vs_oracle(vl):
         check_pose(on["q"][qi], on["t"][qi], ref.q, ref.t)
         check_mask(on["flags"][qi * n:(qi + 1) * n].astype(bool), ref.inlier_flags, on["q"][qi], on["t"][qi],
                    px, X, (700.0, 700.0, 350.0, 350.0), 12.0, q_ref=ref.q, t_ref=ref.t)
+
+
+def test_pruning_staged_host_api_identical(vl):
+    """The staged host pipeline (queries admitted stage by stage, each admission
+    followed by a split head / rest round) gives the same results with pruning
+    on and off, and the same as the device-resident call."""
+    from paper_2601_04185_b200 import _lib
+    from paper_2601_04185_b200.posest import ransac_pnp_host
+    Q, n = 48, 30_000
+    qs = _batch(Q, n, 0.7, 9900)
+    seeds = [12_000 + qi for qi in range(Q)]
+    cfg = vl.RansacConfig(max_iterations=3_000, miss_probability=1e-4)
+    offsets = np.arange(Q + 1, dtype=np.int64) * n
+    intr = [vl.CameraIntrinsics(700.0, 700.0, 350.0, 350.0, 700, 700)] * Q
+    px, X, w = (np.concatenate([x[k] for x in qs]) for k in range(3))
+    ctx = _lib.context()
+    outs = []
+    try:
+        for prune in (True, False):
+            ctx.set_pruning(prune)
+            ctx.scoring_counters(reset=True)
+            res, _, _ = ransac_pnp_host(px, X, w, offsets, intr, seeds, cfg, stage_ends=[8, 24, 48])
+            outs.append((res, ctx.scoring_counters(reset=True)))
+    finally:
+        ctx.set_pruning(True)
+    (on, (skipped, _)), (off, (skipped0, _)) = outs
+    # stages are admitted as their copies land (timing-dependent round
+    # compositions, hence LO cluster shapes): decisions exact, poses to ~1e-15
+    for k in ("flags", "count", "iterations", "converged", "stats"):
+        assert np.array_equal(on[k], off[k]), k
+    for k in ("q", "t", "score"):
+        assert np.allclose(on[k], off[k], rtol=1e-12, atol=1e-12), k
+    assert skipped > 0 and skipped0 == 0
+    dev, _ = _run(vl, qs, cfg, seeds, True)
+    for k in ("iterations", "converged"):
+        assert np.array_equal(on[k], dev[k]), k
+    for k in ("q", "t", "score"):  # (other round compositions: LO cluster shapes differ, ~1e-15)
+        assert np.allclose(on[k], dev[k], rtol=1e-12, atol=1e-12), k
