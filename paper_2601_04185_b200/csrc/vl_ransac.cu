@@ -471,8 +471,12 @@ int launch_hyp_rows(const Work& wk, const double* R, const double* t, int H, int
 // kHeadHyps of queries without a best pose; mode 2 (rest) emits the items of
 // the remaining hypotheses (all of them for queries that had a best pose),
 // pruned against the best the head scan found.
+// head size (A/B, ms per step C3a / C3 pruned / C5): 192: 11.10 / 48.74 /
+// 6.93, 256: 11.68 / 49.28 / 7.14, 384: 11.29 / 48.74 / 7.12, 576: 12.65 /
+// 50.23 / 7.41.  (P(no all-inlier sample among the head's ~128 samples) at
+// 30 % inliers: 3 %; a weak head best only weakens the pruning, never the result)
 #ifndef VL_HEAD_HYPS
-#define VL_HEAD_HYPS 384
+#define VL_HEAD_HYPS 192
 #endif
 constexpr int kHeadHyps = VL_HEAD_HYPS;
 
