@@ -23,7 +23,7 @@ struct vl_ctx {
   int num_sms = 148;
   std::string err;
   int64_t launches = 0;
-  DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, p3p_geo, p3p_cand, p3p_nc, P32, hsrc, items, item_count,
+  DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, p3p_geo, p3p_cand, p3p_nc, P32, P32s, hsrc, items, item_count,
       partial, cost32, tile_cnt, sub_pk, sub32, comp_pk;
   DevBuf surv, tail, prune_ctr;  // exact scoring pruning (vl_score.cuh)
   int prune = -1;                // -1: VISLOC_PRUNE (default on), else vl_set_scoring_pruning
@@ -212,7 +212,7 @@ int vl_destroy(vl_ctx* c) {
   if (!c) return VL_OK;
   cudaSetDevice(c->device);
   DevBuf* bufs[] = {&c->qs,      &c->active, &c->next_active, &c->active_count, &c->samples, &c->slots,
-                    &c->slot_cnt, &c->p3p_geo, &c->p3p_cand, &c->p3p_nc, &c->P32,   &c->hsrc,        &c->items,        &c->item_count,
+                    &c->slot_cnt, &c->p3p_geo, &c->p3p_cand, &c->p3p_nc, &c->P32, &c->P32s, &c->hsrc,        &c->items,        &c->item_count,
                     &c->partial, &c->cost32, &c->tile_cnt, &c->sub_pk, &c->sub32, &c->comp_pk,
                     &c->surv, &c->tail, &c->prune_ctr,
                     &c->scratch, &c->lift_meta, &c->lift_blk_count,
@@ -293,6 +293,7 @@ int vl_reserve(vl_ctx* c, int32_t max_queries, int64_t max_n_per_query, int32_t 
   rc |= ensure(c, c->p3p_cand, Qc * B32 * 3 * kMaxCandSlots * sizeof(double));
   rc |= ensure(c, c->p3p_nc, Qc * B * sizeof(int));
   rc |= ensure(c, c->P32, Qc * 12 * H * sizeof(float));
+  rc |= ensure(c, c->P32s, Qc * 12 * H * sizeof(float));
   rc |= ensure(c, c->hsrc, Qc * H * sizeof(int));
   rc |= ensure(c, c->partial, Qc * ns * H * sizeof(float));
   rc |= ensure(c, c->cost32, Qc * H * sizeof(float));
@@ -385,6 +386,7 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
         (rc = ensure(c, c->p3p_cand, Qn * ((B + 31) / 32 * 32) * 3 * kMaxCandSlots * sizeof(double))) ||
         (rc = ensure(c, c->p3p_nc, Qn * B * sizeof(int))) ||
         (rc = ensure(c, c->P32, Qn * 12 * HCAP * sizeof(float))) ||
+        (rc = ensure(c, c->P32s, Qn * 12 * HCAP * sizeof(float))) ||
         (rc = ensure(c, c->hsrc, Qn * HCAP * sizeof(int))) ||
         (rc = ensure(c, c->items, item_cap * sizeof(ScoreItem))) ||
         (rc = ensure(c, c->item_count, 4 * sizeof(int))) ||
@@ -416,6 +418,7 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
     wk.p3p_cand = (double*)c->p3p_cand.p;
     wk.p3p_nc = (int*)c->p3p_nc.p;
     wk.P32 = (float*)c->P32.p;
+    wk.P32s = (float*)c->P32s.p;
     wk.hsrc = (int*)c->hsrc.p;
     wk.items = (ScoreItem*)c->items.p;
     wk.item_count = (int*)c->item_count.p;

@@ -30,6 +30,14 @@ constexpr int kScoreTileHypsFine = kScoreThreads * kScoreHypPerThreadFine;  // 2
 // so the cost bits do not depend on the tile shape, item size or grid
 constexpr int kScoreChunk = 128;
 
+// fp32 scoring rows: 0 = the scorer reads them at their solution slot
+// through hsrc; 1 = k_compact copies them into hypothesis order first (A/B,
+// ms per step C3 / C3 pruned: 93.3 / 48.5 vs 93.1 / 49.6: the copy costs
+// 0.9 ms of compaction per step and saves ~1 ms of full scoring rounds only)
+#ifndef VL_P32_COPY
+#define VL_P32_COPY 0
+#endif
+
 // Per-query device state of the batched estimator.
 struct __align__(16) QState {
   GenState gen;        // initial generator state
@@ -101,7 +109,8 @@ struct Work {
   double* p3p_geo;       // [Qc][ceil(B/32)][kGeoDoubles][32] per-sample geometry
   double* p3p_cand;      // [Qc][ceil(B/32)][8 * 3][32] distance-triple candidates
   int* p3p_nc;           // [Qc][B] candidate counts
-  float* P32;            // [Qc][12][HCAP]
+  float* P32;            // [Qc][12][HCAP] fp32 scoring rows in hypothesis order (k_compact)
+  float* P32s;           // [Qc][12][4][B]  the same rows at their solution slot, column k * B + s (k_p3p_polish)
   int* hsrc;             // [Qc][HCAP]
   ScoreItem* items;      // [item_cap]
   int* item_count;       // [0] items appended this round, [1] scoring work cursor, [2] k_scan completion ticket,

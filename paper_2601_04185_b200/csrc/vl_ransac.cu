@@ -355,8 +355,8 @@ __global__ void __launch_bounds__(kP3PThreads, VL_P3P_POLISH_MINB) k_p3p_polish(
       }
       if (dup) continue;
       for (int i = 0; i < 12; ++i) slot[32 * (12 * kept + i)] = rr[i];
-      // the fp32 scoring row, at P32 column kept * B + s of the query
-      store_p32(wk.P32 + (int64_t)q * 12 * wk.HCAP + (int64_t)kept * wk.B + s, wk.HCAP, S.in.fx, S.in.fy, rr);
+      // the fp32 scoring row, at slot column kept * B + s of the query
+      store_p32(wk.P32s + (int64_t)q * 12 * wk.HCAP + (int64_t)kept * wk.B + s, wk.HCAP, S.in.fx, S.in.fy, rr);
       ++kept;
     }
     __syncwarp();
@@ -440,7 +440,6 @@ __global__ void k_hyp_rows(Work wk, const double* R, const double* t, int H, int
     for (int i = 0; i < 9; ++i) sl[i] = R[9 * (int64_t)h + i];
     for (int i = 0; i < 3; ++i) sl[9 + i] = t[3 * (int64_t)h + i];
     store_p32(wk.P32 + h, wk.HCAP, S.in.fx, S.in.fy, sl);
-    wk.hsrc[h] = h;  // P32 column of hypothesis h
   }
   const int tile_h = fine ? kScoreTileHypsFine : kScoreTileHyps;
   const int spi = fine ? 1 : kScoreItemSplits;
@@ -497,12 +496,24 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine, int mode) {
       const int c = s < bn ? wk.slot_cnt[(int64_t)q * wk.B + s] : 0;
       int total;
       const int ex = block_excl_scan<NT>(c, warp_tot, total);
-      // hypothesis h -> its solution slot and P32 column k * B + s (the fp32
-      // rows were written there by k_p3p_polish)
+      // hypothesis h -> its solution slot k * B + s
       for (int k = 0; k < c; ++k) wk.hsrc[(int64_t)q * wk.HCAP + running + ex + k] = k * wk.B + s;
       running += total;
     }
     nh = running;
+#if VL_P32_COPY
+    __syncthreads();
+    // the fp32 rows (written by k_p3p_polish at the slot columns) in
+    // hypothesis order: the scorer then reads them with no indirection
+    const int* hq = wk.hsrc + (int64_t)q * wk.HCAP;
+    const float* src = wk.P32s + (int64_t)q * 12 * wk.HCAP;
+    float* dst = wk.P32 + (int64_t)q * 12 * wk.HCAP;
+    for (int h = threadIdx.x; h < nh; h += NT) {
+      const int col = hq[h];
+#pragma unroll
+      for (int e = 0; e < 12; ++e) dst[(int64_t)e * wk.HCAP + h] = src[(int64_t)e * wk.HCAP + col];
+    }
+#endif
   } else {
     nh = S.nh;
   }

@@ -181,12 +181,12 @@ __device__ __noinline__ void score_close_tile_pruning(const Work& wk, const Scor
   score_close_tile<NT, HT, SPI, SCH, true>(wk, item, outq, tile0, red_area, sh);
 }
 
-// Register cap of the scorer: 160 fits 3 CTAs of 128 threads per SM (the
-// MINB of __launch_bounds__, which would allow 168).  C3 step at 168 / 160 /
-// 152: 93.9 / 93.3 / 94.0 ms (the instance without pruning code then uses
-// 154 registers, no spills).  0 = __launch_bounds__(NT, MINB) alone.
+// Register cap of the scorer via __maxnreg__ (A/B knob; 0 =
+// __launch_bounds__(NT, MINB) alone, 159 registers with the hsrc row reads):
+// C3 / C3 pruned ms per step 93.3 / 48.5 uncapped, 93.5 / 48.7 at 160 (154
+// registers), 94.0 at 152.
 #ifndef VL_SCORE_MAXNREG
-#define VL_SCORE_MAXNREG 160
+#define VL_SCORE_MAXNREG 0
 #endif
 #if VL_SCORE_MAXNREG > 0
 // (the fine instance keeps its occupancy bound: 65536 / (NT x MINB) rounded down to 8)
@@ -242,16 +242,25 @@ __global__ void VL_SCORE_BOUNDS(NT, MINB) k_score2_t(Work wk, float tau2) {
     float P[HT][12];
     // hypotheses hid0 .. hid0 + HT - 1 of this thread (thread-contiguous)
     const int hid0 = tile0 + hs * WHYP + lane * HT;
-    // hypothesis h's fp32 row sits at P32 column hsrc[h] (k_p3p_polish wrote
-    // it at its solution slot; k_compact only orders the hypotheses)
+#if VL_P32_COPY
     const float* Pq = wk.P32 + (int64_t)item.q * 12 * wk.HCAP;
+#pragma unroll
+    for (int j = 0; j < HT; ++j) {
+      const int h = hid0 + j < nh ? hid0 + j : 0;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) P[j][c] = Pq[(int64_t)c * wk.HCAP + h];
+    }
+#else
+    // hypothesis h's row at its solution slot column hsrc[h] (k_p3p_polish)
+    const float* Pq = (wk.P32s ? wk.P32s : wk.P32) + (int64_t)item.q * 12 * wk.HCAP;
     const int* hq = wk.hsrc + (int64_t)item.q * wk.HCAP;
 #pragma unroll
     for (int j = 0; j < HT; ++j) {
-      const int col = __ldg(hq + (hid0 + j < nh ? hid0 + j : 0));
+      const int col = wk.P32s ? __ldg(hq + (hid0 + j < nh ? hid0 + j : 0)) : (hid0 + j < nh ? hid0 + j : 0);
 #pragma unroll
       for (int c = 0; c < 12; ++c) P[j][c] = Pq[(int64_t)c * wk.HCAP + col];
     }
+#endif
     __syncthreads();
     for (int s = grp; s < ns && grp < G; s += G) {
       float2 acc[HT];
@@ -333,8 +342,13 @@ __global__ void __launch_bounds__(NT) k_score_tail(Work wk, float tau2) {
     const QState& S = wk.qs[tk.q];
     const bool on = lane < tk.cnt;
     const int h = wk.surv[(int64_t)tk.q * wk.HCAP + tk.base + (on ? lane : 0)];
+#if VL_P32_COPY
     const float* Pq = wk.P32 + (int64_t)tk.q * 12 * wk.HCAP;
+    const int col = h;
+#else
+    const float* Pq = wk.P32s + (int64_t)tk.q * 12 * wk.HCAP;
     const int col = wk.hsrc[(int64_t)tk.q * wk.HCAP + h];
+#endif
     float P[12];
 #pragma unroll
     for (int c = 0; c < 12; ++c) P[c] = Pq[(int64_t)c * wk.HCAP + col];
