@@ -1,8 +1,8 @@
 """Parity of the benchmarked workloads themselves against the CPU oracle (tools only).
 
-    python tools/bench_parity.py [N] [c3|c3a|c5|all]
+    python tools/bench_parity.py [N] [c3|c3p|c3a|c5|all]
 
-Runs the GPU estimator on the bench's full batch — C3 / C3a: the 1000
+Runs the GPU estimator on the bench's full batch — C3 / C3p (pruned) / C3a: the 1000
 generator-A queries of `bench.py` with its seeds; C5: the 256 lifted queries
 (8-bit depth, IMLC-style f32 fields) through `LiftPlan` exactly as the bench
 times them — and compares the first N queries of that batch with the
@@ -98,6 +98,8 @@ def run_a(name, N):
     from paper_2601_04185_b200.posest import RansacConfig, ransac_pnp_device
     wl = WORKLOADS[name]
     Q, n = wl["queries"], wl["n"]
+    from paper_2601_04185_b200 import _lib
+    _lib.context().set_pruning(bool(wl.get("prune", True)))  # as bench.py runs the workload
     with mp.get_context("spawn").Pool(len(os.sched_getaffinity(0))) as pool:
         ref_async = pool.map_async(_oracle_a, [(qi, wl) for qi in range(N)], chunksize=1)
         qs = [query_a(qi, n, wl["outlier"], wl["sigma"], 3000) for qi in range(Q)]
@@ -139,7 +141,7 @@ def run_c5(N):
 def main():
     N = int(sys.argv[1]) if len(sys.argv) > 1 else 32
     which = sys.argv[2] if len(sys.argv) > 2 else "all"
-    for name in (["c3", "c3a", "c5"] if which == "all" else [which]):
+    for name in (["c3", "c3p", "c3a", "c5"] if which == "all" else [which]):
         st = run_c5(N) if name == "c5" else run_a(name, N)
         print(json.dumps(st), flush=True)
 
