@@ -26,6 +26,7 @@ struct vl_ctx {
   DevBuf qs, active, next_active, active_count, samples, slots, slot_cnt, p3p_geo, p3p_cand, p3p_nc, P32, P32s, hsrc, items, item_count,
       partial, cost32, tile_cnt, sub_pk, sub32, comp_pk;
   DevBuf surv, tail, prune_ctr;  // exact scoring pruning (vl_score.cuh)
+  DevBuf jump;                   // per-query PCG64 jump tables
   int prune = -1;                // -1: VISLOC_PRUNE (default on), else vl_set_scoring_pruning
   DevBuf scratch;  // small standalone-call scratch
   DevBuf lift_meta, lift_blk_count, lift_blk_off, lift_seg_off;  // vl_lift
@@ -214,7 +215,7 @@ int vl_destroy(vl_ctx* c) {
   DevBuf* bufs[] = {&c->qs,      &c->active, &c->next_active, &c->active_count, &c->samples, &c->slots,
                     &c->slot_cnt, &c->p3p_geo, &c->p3p_cand, &c->p3p_nc, &c->P32, &c->P32s, &c->hsrc,        &c->items,        &c->item_count,
                     &c->partial, &c->cost32, &c->tile_cnt, &c->sub_pk, &c->sub32, &c->comp_pk,
-                    &c->surv, &c->tail, &c->prune_ctr,
+                    &c->surv, &c->tail, &c->prune_ctr, &c->jump,
                     &c->scratch, &c->lift_meta, &c->lift_blk_count,
                     &c->lift_blk_off, &c->lift_seg_off, &c->tri_meta};
   for (DevBuf* b : bufs)
@@ -397,6 +398,7 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
         (rc = ensure(c, c->sub32, (nsub_tot / 2) * 3 * sizeof(float4))) ||
         (rc = ensure(c, c->comp_pk, ncomp * 3 * sizeof(double2))) ||
         (rc = ensure(c, c->surv, (size_t)Qn * HCAP * sizeof(int))) ||
+        (rc = ensure(c, c->jump, (size_t)Qn * 2 * kJumpBits * sizeof(u128))) ||
         (rc = ensure(c, c->tail, (size_t)Qn * (HCAP / 32 + ntile) * sizeof(TailTask))) ||
         (rc = ensure_ctr(c)))
       return rc;
@@ -436,6 +438,7 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
     wk.split_rank = 0;
     wk.split_size = 1;
     wk.prune = prune_enabled(c);
+    wk.jump = (u128*)c->jump.p;
     wk.surv = (int*)c->surv.p;
     wk.tail = (TailTask*)c->tail.p;
     wk.tail_cap = (int64_t)Qn * (HCAP / 32 + ntile);

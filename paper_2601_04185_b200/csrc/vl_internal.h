@@ -41,6 +41,11 @@ constexpr int kScoreChunk = 128;
 // Per-query device state of the batched estimator.
 struct __align__(16) QState {
   GenState gen;        // initial generator state
+  // sampler cache: the PCG64 state advanced m_cache steps from gen.state (the
+  // base of the last speculation window; m_cache = ~0: none), so the next
+  // round's base is a short table jump instead of an O(log n) advance
+  u128 st_cache;
+  uint64_t m_cache;
   int64_t off;         // first row in px/X/w (absolute)
   int64_t coff;        // first row in the chunk-relative compaction buffer
   int64_t sub_off;     // first row in the scoring-subset arrays
@@ -125,6 +130,7 @@ struct Work {
   int64_t item_cap;
   int split_rank, split_size;  // hypothesis-split mode: scoring tiles dealt round-robin
   int* host_count;       // mapped pinned mirror of *active_count (nullable)
+  u128* jump;            // [Qc][2][kJumpBits] per-query PCG64 jump tables (k_prep; nullable)
   // exact scoring pruning (coarse rounds with a best pose; 0 = every
   // hypothesis scored on the whole subset, as the reference does)
   int prune;

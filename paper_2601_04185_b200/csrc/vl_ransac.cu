@@ -84,6 +84,9 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
   }
   w_ok = __syncthreads_and(w_ok);
   if (threadIdx.x == 0) {
+    if (wk.jump) pcg_jump_table(S.gen.inc, wk.jump + (int64_t)q * 2 * kJumpBits,
+                                wk.jump + (int64_t)q * 2 * kJumpBits + kJumpBits);
+    S.m_cache = ~0ull;
     S.prune_ok = w_ok;
     S.sA = 0;
     S.cost_typ = 0.f;
@@ -106,21 +109,38 @@ int launch_prep(const Work& wk, const Inputs& in, int q0, int nq, int list_pos, 
 // O(log n) pcg_advance); each thread then jumps only its own offset within
 // the batch through the block's 2^k jump table (a few affine compositions
 // instead of a full O(log n) advance per thread).
+// With a per-query jump table `tab` (k_prep) and the cached base of the
+// previous round (`cache_st` advanced `*cache_m` steps), the base of the
+// first window is a short table jump (one batch of draws ahead) instead of an
+// O(log n) advance from the seed state; both give the same state.
 template <int NT>
-__device__ void sample_batch(const GenState& g, uint64_t& pos, int64_t n, int bn, int* out) {
+__device__ void sample_batch(const GenState& g, uint64_t& pos, int64_t n, int bn, int* out,
+                             const u128* tab = nullptr, u128* cache_st = nullptr, uint64_t* cache_m = nullptr) {
   __shared__ int s_first;
   __shared__ unsigned long long s_pos;
   __shared__ u128 s_tmul[kJumpBits], s_tplus[kJumpBits], s_base;
   __shared__ unsigned long long s_m0;
   const int D = draws_per_sample(n);
-  if (threadIdx.x == 0) pcg_jump_table(g.inc, s_tmul, s_tplus);
+  if (tab) {
+    if (threadIdx.x < kJumpBits) {
+      s_tmul[threadIdx.x] = tab[threadIdx.x];
+      s_tplus[threadIdx.x] = tab[kJumpBits + threadIdx.x];
+    }
+    __syncthreads();
+  } else if (threadIdx.x == 0) {
+    pcg_jump_table(g.inc, s_tmul, s_tplus);
+  }
   int i0 = 0;
   while (i0 < bn) {
     if (threadIdx.x == 0) {
       s_first = INT_MAX;
       const uint64_t q0 = pos >= (uint64_t)g.has0 ? pos - g.has0 : 0;  // first non-buffered word
       s_m0 = q0 >> 1;
-      s_base = pcg_advance(g.state, g.inc, s_m0 + 1);
+      const uint64_t want = s_m0 + 1, have = cache_m ? *cache_m : ~0ull;
+      if (have != ~0ull && want >= have && want - have < (1ull << kJumpBits))
+        s_base = pcg_advance_tab(*cache_st, want - have, s_tmul, s_tplus);
+      else
+        s_base = pcg_advance(g.state, g.inc, want);
     }
     __syncthreads();
     // the speculative window spans at most NT samples at a time: offsets < 2^kJumpBits words
@@ -163,6 +183,10 @@ __device__ void sample_batch(const GenState& g, uint64_t& pos, int64_t n, int bn
     i0 = r + 1;
     __syncthreads();
   }
+  if (cache_m && threadIdx.x == 0) {  // the last window's base
+    *cache_st = s_base;
+    *cache_m = s_m0 + 1;
+  }
 }
 
 // NT threads per query: 256 for big batches, 1024 when few queries are active
@@ -179,7 +203,8 @@ __global__ void __launch_bounds__(NT) k_sample(Work wk, RansacParams p) {
   const int64_t rem = p.max_iterations - S.iters;
   const int bn = (int)(rem < p.batch_size ? rem : p.batch_size);
   uint64_t pos = S.rng_pos;
-  sample_batch<NT>(S.gen, pos, S.n, bn, wk.samples + (int64_t)q * wk.B * 3);
+  sample_batch<NT>(S.gen, pos, S.n, bn, wk.samples + (int64_t)q * wk.B * 3,
+                   wk.jump ? wk.jump + (int64_t)q * 2 * kJumpBits : nullptr, &S.st_cache, &S.m_cache);
   if (threadIdx.x == 0) {
     S.rng_pos = pos;
     S.batch_n = bn;
