@@ -163,3 +163,26 @@ def test_pruning_staged_host_api_identical(vl):
         assert np.array_equal(on[k], dev[k]), k
     for k in ("q", "t", "score"):  # (other round compositions: LO cluster shapes differ, ~1e-15)
         assert np.allclose(on[k], dev[k], rtol=1e-12, atol=1e-12), k
+
+
+def test_pruning_mixed_batch_identical(vl):
+    """A coarse batch mixing query sizes — single-split subsets (n = 50, nothing to
+    prune), a degenerate query whose points are all identical (no P3P solution,
+    no hypotheses in any round), odd sizes — gives identical outputs with pruning
+    on and off."""
+    sizes = [50, 20_000, 77, 9_999, 30_000, 120, 20_000, 15_001] * 5
+    qs = []
+    for qi, n in enumerate(sizes):
+        rng = np.random.default_rng(4400 + qi)
+        _, R, t = random_pose(rng, 0.2, 0.2)
+        px, X, w, _ = matches_a(n, 0.6, 1.0, seed=4400 + 7919 * qi + 1, R=R, t=t)
+        if qi == 9:  # degenerate: every correspondence the same
+            px, X = np.repeat(px[:1], n, 0), np.repeat(X[:1], n, 0)
+        qs.append((px, X, w))
+    seeds = [900 + qi for qi in range(len(qs))]
+    cfg = vl.RansacConfig(max_iterations=4_000, miss_probability=1e-300)
+    on, (skipped, _) = _run(vl, qs, cfg, seeds, True)
+    off, _ = _run(vl, qs, cfg, seeds, False)
+    _same(on, off)
+    assert skipped > 0
+    assert int(on["stats"][9, 1]) == 0 and not on["converged"][9]  # no hypotheses at all
