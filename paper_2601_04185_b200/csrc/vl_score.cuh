@@ -80,6 +80,9 @@ constexpr size_t score_smem_bytes() {
 // for k_score_tail).  PRUNE = false is the kernel instance of runs without
 // pruning, so the pruning code's registers stay out of it (-2 % scoring time,
 // 161 vs 168 registers); the pruning instance calls it out of line (-1 %).
+#ifndef VL_CLOSE_FINE_G
+#define VL_CLOSE_FINE_G 8  // fine closer: split groups loaded per batch (A/B, C4 ms: 4 8.79, 8 8.72, 20 9.17)
+#endif
 template <int NT, int HT, int SPI, int SCH, bool PRUNE>
 __device__ __forceinline__ void score_close_tile(const Work& wk, const ScoreItem& item, const float* outq, int tile0,
                                                float* red_area, int* sh) {
@@ -113,17 +116,17 @@ __device__ __forceinline__ void score_close_tile(const Work& wk, const ScoreItem
     // closing item waits for a few L2 round trips instead of one per group
     float c = 0.f;
     if (SPI == 1) {
-      for (int g0 = 0; g0 < NG; g0 += 4) {
-        float v[4][kGroupSplits];
+      for (int g0 = 0; g0 < NG; g0 += VL_CLOSE_FINE_G) {
+        float v[VL_CLOSE_FINE_G][kGroupSplits];
 #pragma unroll
-        for (int gg = 0; gg < 4; ++gg)
+        for (int gg = 0; gg < VL_CLOSE_FINE_G; ++gg)
 #pragma unroll
           for (int k = 0; k < kGroupSplits; ++k) {
             const int sp = (g0 + gg) * kGroupSplits + k;
             v[gg][k] = sp < NS ? __ldcg(outq + (int64_t)sp * wk.HCAP + h) : 0.f;
           }
 #pragma unroll
-        for (int gg = 0; gg < 4; ++gg) {
+        for (int gg = 0; gg < VL_CLOSE_FINE_G; ++gg) {
           const int g = g0 + gg;
           if (g < NG) {
             float gs = v[gg][0];
