@@ -437,6 +437,9 @@ static int setup_chunk(vl_ctx* c, const vl_ransac_args* a, int64_t q0, int Qn, c
     wk.item_cap = item_cap;
     wk.split_rank = 0;
     wk.split_size = 1;
+    wk.par = 0;
+    wk.next_list = wk.active_list;
+    wk.next_count = wk.active_count;
     wk.prune = prune_enabled(c);
     wk.jump = (u128*)c->jump.p;
     wk.surv = (int*)c->surv.p;

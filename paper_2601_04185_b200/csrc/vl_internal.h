@@ -52,9 +52,15 @@ struct __align__(16) QState {
   int n, nsub, stride, nsplit;
   Intr in;
   // dynamic
-  uint64_t rng_pos;    // uint32 words consumed so far
-  int64_t iters;       // minimal samples drawn
-  int batch_n;         // samples in the current round
+  uint64_t rng_pos;    // uint32 words consumed so far (the sampler's own chain)
+  int64_t iters;       // minimal samples drawn in the rounds scanned so far (committed by k_scan)
+  int64_t spec_iters;  // samples drawn by the sampler so far (may run one round ahead, see below)
+  // per round parity (Work::par): samples of that round and the sample count
+  // after it.  The pipelined loop (small batches) samples and solves round
+  // r+1 on a side stream while round r is scored and scanned, so the
+  // sampler's outputs are double-buffered and k_scan commits `iters`.
+  int64_t iters_p[2];
+  int bn_p[2];
   int active;
   int has_best;
   int nh;              // hypotheses in the current round
@@ -129,6 +135,9 @@ struct Work {
   int B, HCAP, NSPLIT, TCAP;
   int64_t item_cap;
   int split_rank, split_size;  // hypothesis-split mode: scoring tiles dealt round-robin
+  int par;               // round parity: selects bn_p / iters_p (0 unless pipelined)
+  int* next_list;        // k_scan's compaction target (== active_list: in place)
+  int* next_count;       // (== active_count)
   int* host_count;       // mapped pinned mirror of *active_count (nullable)
   u128* jump;            // [Qc][2][kJumpBits] per-query PCG64 jump tables (k_prep; nullable)
   // exact scoring pruning (coarse rounds with a best pose; 0 = every

@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(256) k_prep(Work wk, Inputs in, const QState* 
     if (wk.jump) pcg_jump_table(S.gen.inc, wk.jump + (int64_t)q * 2 * kJumpBits,
                                 wk.jump + (int64_t)q * 2 * kJumpBits + kJumpBits);
     S.m_cache = ~0ull;
+    S.spec_iters = S.iters;
     S.prune_ok = w_ok;
     S.sA = 0;
     S.cost_typ = 0.f;
@@ -200,16 +201,16 @@ __global__ void __launch_bounds__(NT) k_sample(Work wk, RansacParams p) {
   if ((int)blockIdx.x >= *wk.active_count) return;
   const int q = wk.active_list[blockIdx.x];
   QState& S = wk.qs[q];
-  const int64_t rem = p.max_iterations - S.iters;
+  const int64_t rem = p.max_iterations - S.spec_iters;
   const int bn = (int)(rem < p.batch_size ? rem : p.batch_size);
   uint64_t pos = S.rng_pos;
   sample_batch<NT>(S.gen, pos, S.n, bn, wk.samples + (int64_t)q * wk.B * 3,
                    wk.jump ? wk.jump + (int64_t)q * 2 * kJumpBits : nullptr, &S.st_cache, &S.m_cache);
   if (threadIdx.x == 0) {
     S.rng_pos = pos;
-    S.batch_n = bn;
-    S.iters += bn;
-    S.rounds += 1;
+    S.bn_p[wk.par] = bn;
+    S.spec_iters += bn;
+    S.iters_p[wk.par] = S.spec_iters;
   }
 }
 
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kP3PRootThreads, VL_P3P_ROOT_MINB) k_p3p_roots
   const int q = wk.active_list[blockIdx.x];
   const QState& S = wk.qs[q];
   const int s = blockIdx.y * kP3PRootThreads + threadIdx.x;
-  if (s >= S.batch_n) return;
+  if (s >= S.bn_p[wk.par]) return;
   const int64_t si = (int64_t)q * wk.B + s;
   const int* smp = wk.samples + si * 3;
   double f[9], P[9];
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(kP3PThreads, VL_P3P_POLISH_MINB) k_p3p_polish(
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int s = blockIdx.y * kP3PThreads + threadIdx.x;
   const int64_t si = (int64_t)q * wk.B + s;
-  const bool live = s < S.batch_n;
+  const bool live = s < S.bn_p[wk.par];
   const int nc = live ? wk.p3p_nc[si] : 0;
   // warp exclusive scan of candidate counts
   int incl = nc;
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine, int mode) {
   QState& S = wk.qs[q];
   int nh;
   if (mode != 2) {
-    const int bn = S.batch_n;
+    const int bn = S.bn_p[wk.par];
     int running = 0;
     for (int base = 0; base < bn; base += NT) {
       const int s = base + threadIdx.x;
@@ -633,12 +634,13 @@ __device__ void compact_active(Work wk, int nactive) {
     const int a = (q >= 0 && __ldcg(&wk.qs[q].active)) ? 1 : 0;
     int total;
     const int ex = block_excl_scan<NT>(a, warp_tot, total);
-    if (a) wk.active_list[running + ex] = q;  // in place: write index <= read index
+    // (in place when next_list == active_list: write index <= read index)
+    if (a) wk.next_list[running + ex] = q;
     running += total;
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    *wk.active_count = running;
+    *wk.next_count = running;
     if (wk.host_count) *(volatile int*)wk.host_count = running;  // mapped pinned: read after the stream sync
     wk.item_count[0] = 0;  // items appended next round
     wk.item_count[1] = 0;  // scoring work cursor
@@ -747,6 +749,7 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     __syncthreads();
   }
   int active = 1;
+  const int64_t iters_r = S.iters_p[wk.par];  // samples drawn up to this round
   if (mode != 1 && has_best) {
     // the stop rule's subset inlier count (posest.py:269-273): computed once
     // per best pose — an unchanged best (most rounds after the first) or a
@@ -758,9 +761,9 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
       best_cnt = (int64_t)sm.red[1];
     }
     const int64_t need = required_iters_dev((double)best_cnt / (double)S.nsub, p.eta, p.max_iterations);
-    if (S.iters >= need) active = 0;
+    if (iters_r >= need) active = 0;
   }
-  if (S.iters >= p.max_iterations) active = 0;
+  if (iters_r >= p.max_iterations) active = 0;
   __syncthreads();
   if (cl_size() > 1) cl_sync();  // every CTA of the cluster has read S
   if (threadIdx.x == 0 && cl_rank() == 0) {
@@ -768,7 +771,11 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
     S.has_best = has_best;
     S.best = best;
     S.lo_calls += lo_calls;
-    if (mode != 1) S.active = active;  // (head phase: the round goes on)
+    if (mode != 1) {  // (head phase: the round goes on)
+      S.active = active;
+      S.iters = iters_r;  // the round is scanned: its samples count
+      S.rounds += 1;
+    }
     S.best_sub_cnt = best_cnt;
     S.best_cnt_valid = best_cnt >= 0 ? 1 : 0;
     S.cost_typ = cost_typ;
