@@ -27,6 +27,11 @@ struct vl_ctx {
       partial, cost32, tile_cnt, sub_pk, sub32, comp_pk;
   DevBuf surv, tail, prune_ctr;  // exact scoring pruning (vl_score.cuh)
   DevBuf jump;                   // per-query PCG64 jump tables
+  // pipelined round loop (small batches): the parity-1 copies of the round
+  // buffers, the second active list, the side stream and its events
+  DevBuf samples2, slots2, slot_cnt2, p3p_geo2, p3p_cand2, p3p_nc2, P32s2, active2, active_count2;
+  cudaStream_t side = nullptr;
+  cudaEvent_t pev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int prune = -1;                // -1: VISLOC_PRUNE (default on), else vl_set_scoring_pruning
   DevBuf scratch;  // small standalone-call scratch
   DevBuf lift_meta, lift_blk_count, lift_blk_off, lift_seg_off;  // vl_lift
@@ -216,6 +221,8 @@ int vl_destroy(vl_ctx* c) {
                     &c->slot_cnt, &c->p3p_geo, &c->p3p_cand, &c->p3p_nc, &c->P32, &c->P32s, &c->hsrc,        &c->items,        &c->item_count,
                     &c->partial, &c->cost32, &c->tile_cnt, &c->sub_pk, &c->sub32, &c->comp_pk,
                     &c->surv, &c->tail, &c->prune_ctr, &c->jump,
+                    &c->samples2, &c->slots2, &c->slot_cnt2, &c->p3p_geo2, &c->p3p_cand2, &c->p3p_nc2,
+                    &c->P32s2, &c->active2, &c->active_count2,
                     &c->scratch, &c->lift_meta, &c->lift_blk_count,
                     &c->lift_blk_off, &c->lift_seg_off, &c->tri_meta};
   for (DevBuf* b : bufs)
@@ -223,6 +230,9 @@ int vl_destroy(vl_ctx* c) {
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->round_ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->pev)
+    if (e) cudaEventDestroy(e);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   delete c;
   return VL_OK;
@@ -509,6 +519,103 @@ static int round_loop_lookahead(vl_ctx* c, const Work& wk, const Inputs& in, con
   return VL_OK;
 }
 
+// Pipelined round loop for small batches (fine scoring rounds: the GPU is
+// far from full): the side stream samples and solves P3P for round r+1 while
+// the caller's stream scores and scans round r.  The sampler's outputs are
+// double-buffered by round parity (Work::par), round r+1's side chain reads
+// round r's active list (a superset: a query that stops after round r wastes
+// one speculative batch, never its results — k_scan commits the iteration
+// count), and k_scan compacts into the other list.  Same kernels, same
+// arithmetic, identical results to round_loop_lookahead.
+static bool pipeline_enabled() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("VISLOC_PIPE");
+    mode = e ? (atoi(e) != 0) : 1;
+  }
+  return mode != 0;
+}
+
+static int round_loop_pipelined(vl_ctx* c, const Work& wk, const Inputs& in, const RansacParams& p, int Qn,
+                                int64_t max_rounds, cudaStream_t st) {
+  const int64_t B = wk.B, B32 = (B + 31) / 32 * 32, HCAP = wk.HCAP;
+  int rc;
+  if ((rc = ensure(c, c->samples2, Qn * B * 3 * sizeof(int))) ||
+      (rc = ensure(c, c->slots2, Qn * B32 * 48 * sizeof(double))) ||
+      (rc = ensure(c, c->slot_cnt2, Qn * B * sizeof(int))) ||
+      (rc = ensure(c, c->p3p_geo2, Qn * B32 * kGeoDoubles * sizeof(double))) ||
+      (rc = ensure(c, c->p3p_cand2, Qn * B32 * 3 * kMaxCandSlots * sizeof(double))) ||
+      (rc = ensure(c, c->p3p_nc2, Qn * B * sizeof(int))) ||
+      (rc = ensure(c, c->P32s2, Qn * 12 * HCAP * sizeof(float))) ||
+      (rc = ensure(c, c->active2, Qn * sizeof(int))) || (rc = ensure(c, c->active_count2, 2 * sizeof(int))))
+    return rc;
+  if (!c->side) VL_CUDA(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  if (!c->pev[0])
+    for (auto& e : c->pev) VL_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (!c->round_ev[0])
+    for (auto& e : c->round_ev) VL_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // main view of round r: W[r & 1] (its buffers, its list, compaction into the other list)
+  Work W[2] = {wk, wk};
+  W[1].par = 1;
+  W[1].samples = (int*)c->samples2.p;
+  W[1].slots = (double*)c->slots2.p;
+  W[1].slot_cnt = (int*)c->slot_cnt2.p;
+  W[1].p3p_geo = (double*)c->p3p_geo2.p;
+  W[1].p3p_cand = (double*)c->p3p_cand2.p;
+  W[1].p3p_nc = (int*)c->p3p_nc2.p;
+  W[1].P32s = (float*)c->P32s2.p;
+  W[1].active_list = (int*)c->active2.p;
+  W[1].active_count = (int*)c->active_count2.p;
+  W[0].next_list = W[1].active_list;
+  W[0].next_count = W[1].active_count;
+  W[1].next_list = W[0].active_list;
+  W[1].next_count = W[0].active_count;
+  // side view of round r: W[r & 1]'s buffers, the list of round r - 1 (round 0: the admitted list)
+  auto side_view = [&](int64_t r) {
+    Work v = W[r & 1];
+    if (r > 0) {
+      v.active_list = W[(r - 1) & 1].active_list;
+      v.active_count = W[(r - 1) & 1].active_count;
+    }
+    return v;
+  };
+  cudaEvent_t ev_start = c->pev[0], ev_p[2] = {c->pev[1], c->pev[2]}, ev_c[2] = {c->pev[3], c->pev[4]};
+  cudaEvent_t ev_end = c->pev[5];
+  volatile int* h_count = (volatile int*)((char*)c->h_pinned + c->h_pinned_cap - 16);
+  VL_CUDA(c, cudaEventRecord(ev_start, st));  // the admitted queries (k_prep)
+  VL_CUDA(c, cudaStreamWaitEvent(c->side, ev_start, 0));
+  c->launches += launch_round(side_view(0), in, p, Qn, c->num_sms, c->side, nullptr, nullptr, 3);
+  VL_CUDA(c, cudaEventRecord(ev_p[0], c->side));
+  int nlaunch = Qn;
+  // queue round r: compaction (after its side chain), round r+1's side chain
+  // (after the compaction: it overwrites round r-1's buffers), scores + scan
+  auto queue = [&](int64_t r) -> int {
+    VL_CUDA(c, cudaStreamWaitEvent(st, ev_p[r & 1], 0));
+    c->launches += launch_round(W[r & 1], in, p, nlaunch, c->num_sms, st, nullptr, nullptr, 4);
+    VL_CUDA(c, cudaEventRecord(ev_c[r & 1], st));
+    VL_CUDA(c, cudaStreamWaitEvent(c->side, ev_c[r & 1], 0));
+    c->launches += launch_round(side_view(r + 1), in, p, nlaunch, c->num_sms, c->side, nullptr, nullptr, 3);
+    VL_CUDA(c, cudaEventRecord(ev_p[(r + 1) & 1], c->side));
+    c->launches += launch_round(W[r & 1], in, p, nlaunch, c->num_sms, st, nullptr, nullptr, 5);
+    VL_CUDA(c, cudaEventRecord(c->round_ev[r & 1], st));
+    return check_launch(c);
+  };
+  int64_t r = 0;
+  if ((rc = queue(0))) return rc;
+  while (true) {
+    if ((rc = queue(r + 1))) return rc;  // one round ahead, with the last count read (a superset)
+    VL_CUDA(c, cudaEventSynchronize(c->round_ev[r & 1]));
+    const int n = *h_count;
+    if (n == 0) break;
+    nlaunch = n;
+    if (++r > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
+  }
+  // the side stream's queued speculative work ends before anything reuses its buffers
+  VL_CUDA(c, cudaEventRecord(ev_end, c->side));
+  VL_CUDA(c, cudaStreamWaitEvent(st, ev_end, 0));
+  return VL_OK;
+}
+
 int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, void* stream) {
   if (!c || !a || !o) return fail(c, VL_ERR_INVALID, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
@@ -535,6 +642,8 @@ int vl_ransac_pnp(vl_ctx* c, const vl_ransac_args* a, const vl_ransac_out* o, vo
         if ((rc = read_active(c, wk, st, &nactive))) return rc;
         if (++guard > max_rounds) return fail(c, VL_ERR_CUDA, "round loop did not terminate");
       }
+    } else if (pipeline_enabled() && round_is_fine(wk, Qn, c->num_sms)) {
+      if ((rc = round_loop_pipelined(c, wk, in, p, Qn, max_rounds, st))) return rc;
     } else if ((rc = round_loop_lookahead(c, wk, in, p, Qn, max_rounds, st))) {
       return rc;
     }

@@ -188,7 +188,10 @@ int launch_prep(const Work& wk, const Inputs& in, int q0, int nq, int list_pos, 
 // profiling stages (vl_profile_read order)
 enum { kStagePrep = 0, kStageSample, kStageP3P, kStageCompact, kStageScore, kStageScan, kStageActive,
        kStageFinal, kStageLift, kNumStages };
-// phase 0: whole round; 1: sample .. score; 2: scan + active (stepwise driver).
+// fine scoring items (256-hypothesis tiles x 1 split) for a round of nactive queries
+bool round_is_fine(const Work& wk, int nactive, int num_sms);
+// phase 0: whole round; 1: sample .. score; 2: scan + active (stepwise driver);
+// pipelined loop: 3 sampling + P3P, 4 compaction, 5 scores + scan.
 // split (phase 0, pruning on, coarse rounds): queries without a best pose
 // first score and scan their first kHeadHyps hypotheses, so the rest of the
 // round is already pruned against that best (vl_ransac.cu, k_compact)

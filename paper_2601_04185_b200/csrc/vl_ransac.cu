@@ -861,7 +861,7 @@ static bool use_pdl(int) {
 }
 
 // coarse scoring items unless the whole batch would not fill ~3 waves of SMs
-static bool round_is_fine(const Work& wk, int nactive, int num_sms) {
+bool round_is_fine(const Work& wk, int nactive, int num_sms) {
   const int coarse_items = nactive * 2 * ((wk.NSPLIT + kScoreItemSplits - 1) / kScoreItemSplits);
   return coarse_items < 3 * num_sms;
 }
@@ -1002,7 +1002,13 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     H(kStageScan, false);
     n += 1;
   };
-  if (phase != 2) {
+  // phase 0: all; 1: up to the scores; 2: the scan; pipelined loop: 3: the
+  // side chain (sampling + P3P), 4: the compaction, 5: scores + scan
+  const bool side = phase == 0 || phase == 1 || phase == 3;
+  const bool comp = phase == 0 || phase == 1 || phase == 4;
+  const bool scr = phase == 0 || phase == 1 || phase == 5;
+  const bool scn = phase == 0 || phase == 2 || phase == 5;
+  if (side) {
     H(kStageSample, true);
     if (nactive * 4 <= num_sms) launch_k(k_sample<1024>, dim3(nactive), 1024, st, pdl, wk, p);
     else launch_k(k_sample<256>, dim3(nactive), 256, st, pdl, wk, p);
@@ -1014,17 +1020,17 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     launch_k(k_p3p_polish, gp, kP3PThreads, st, pdl, wk);
     H(kStageP3P, false);
     n += 3;
-    if (two) {
-      compact(1);
-      score();
-      scan(1);
-      compact(2);
-    } else {
-      compact(0);
-    }
-    score();
   }
-  if (phase != 1) scan(two ? 2 : 0);
+  if (two) {
+    compact(1);
+    score();
+    scan(1);
+    compact(2);
+  } else if (comp) {
+    compact(0);
+  }
+  if (scr) score();
+  if (scn) scan(two ? 2 : 0);
   return n;
 }
 
