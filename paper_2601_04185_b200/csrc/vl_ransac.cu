@@ -655,7 +655,7 @@ __device__ void compact_active(Work wk, int nactive) {
 // mode (k_compact's): 0 full round, 1 head of a split round (hypotheses
 // [h_lo, h_hi) only; no stop rule, the active list stays), 2 rest of it.
 __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, RansacParams p, int costs_smem,
-                                                                  int mode) {
+                                                                  int mode, int fine) {
   pdl_enter();
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   double2* ring = reinterpret_cast<double2*>(dyn_smem);  // kStageBytes (TMA staging ring)
@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   // the next pruning prefix (k_compact); pruned phases keep it
   float cost_typ = S.cost_typ, prune_m = S.prune_m;
   if (S.sA < S.nsplit && S.nsurv * 4 > nh - hlo) prune_m *= 1.1f;  // pruned, many survivors
-  if (wk.prune && nh > hlo && S.sA >= S.nsplit) {
+  if (wk.prune && !fine && nh > hlo && S.sA >= S.nsplit) {  // (fine rounds never prune)
     double acc[1] = {0.0};
     for (int h = hlo + threadIdx.x; h < nh; h += kScanThreads) acc[0] += (double)costs[h];
     block_sum<kScanThreads, 1>(acc, sm.scratch, sm.red);
@@ -702,21 +702,21 @@ __global__ void __launch_bounds__(kScanThreads, VL_LO_MINB) k_scan(Work wk, Rans
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int h0 = hlo;
   while (h0 < nh) {
-    int found = INT_MAX;
-    for (int base = h0; base < nh; base += kScanThreads) {
-      const int i = base + threadIdx.x;
-      const bool pred = i < nh && (double)costs[i] < best_cost;
-      const unsigned bal = __ballot_sync(0xffffffffu, pred);
-      if (lane == 0) sm.ibuf[wid] = bal ? base + wid * 32 + __ffs(bal) - 1 : INT_MAX;
-      __syncthreads();
-      int f = INT_MAX;
-      for (int w = 0; w < kScanThreads / 32; ++w) f = min(f, sm.ibuf[w]);
-      __syncthreads();
-      if (f != INT_MAX) {
-        found = f;
+    // the first h >= h0 with cost < best: every thread stops at its own first
+    // hit (strided), one block minimum (a round without an LO: one reduction
+    // instead of one per 256 hypotheses)
+    int f = INT_MAX;
+    for (int i = h0 + threadIdx.x; i < nh; i += kScanThreads)
+      if ((double)costs[i] < best_cost) {
+        f = i;
         break;
       }
-    }
+    f = (int)__reduce_min_sync(0xffffffffu, (unsigned)f);
+    if (lane == 0) sm.ibuf[wid] = f;
+    __syncthreads();
+    int found = INT_MAX;
+    for (int w = 0; w < kScanThreads / 32; ++w) found = min(found, sm.ibuf[w]);
+    __syncthreads();
     if (found == INT_MAX) break;
     best_cost = (double)costs[found];
     has_best = 1;
@@ -998,7 +998,7 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     if (cs == 1 && nactive <= VL_LO_MINB * num_sms) cs = 2;
     if (const char* e = getenv("VISLOC_SCAN_CS")) cs = atoi(e);  // tuning knob
     // (+ active-list compaction, except after a head phase)
-    launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, pdl, wk, p, costs_smem, mode);
+    launch_clustered(k_scan, nactive, kScanThreads, smem, cs, st, pdl, wk, p, costs_smem, mode, fine);
     H(kStageScan, false);
     n += 1;
   };
