@@ -94,7 +94,17 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive,
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fkern, kScoreThreads, kFineSmem) !=
                          cudaSuccess || occ < 1))
       occ = kFineMinBlocks;
-    cfg.gridDim = dim3(score_grid(wk, num_sms * occ, 1, nactive), 1, 1);
+    // CTAs per SM of the fine grid: a single query's round (a few hundred
+    // items) runs faster on 2 CTAs per SM than on all 6 (C4 5.82 -> 5.57 ms,
+    // C2 1.22 -> 1.21; A/B knob VISLOC_SCORE_FINE_CTAS, 0 = occupancy)
+    static int fine_ctas = -1;
+    if (fine_ctas < 0) {
+      const char* e = getenv("VISLOC_SCORE_FINE_CTAS");
+      fine_ctas = e ? atoi(e) : -2;
+    }
+    const int want = fine_ctas == -2 ? (nactive == 1 ? 2 : 0) : fine_ctas;
+    const int per_sm = want > 0 ? std::min(want, occ) : occ;
+    cfg.gridDim = dim3(score_grid(wk, num_sms * per_sm, 1, nactive), 1, 1);
     cfg.dynamicSmemBytes = kFineSmem;
     cudaLaunchKernelEx(&cfg, fkern, wk, tau2);
   } else {
