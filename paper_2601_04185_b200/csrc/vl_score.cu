@@ -97,8 +97,8 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive,
     // CTAs per SM of the fine grid: a single query's round (a few hundred
     // items) runs faster on 2 CTAs per SM than on all 6 (C4 5.82 -> 5.57 ms,
     // C2 1.22 -> 1.21; A/B knob VISLOC_SCORE_FINE_CTAS, 0 = occupancy)
-    static int fine_ctas = -1;
-    if (fine_ctas < 0) {
+    static int fine_ctas = -3;  // -3: not read yet; -2: automatic
+    if (fine_ctas == -3) {
       const char* e = getenv("VISLOC_SCORE_FINE_CTAS");
       fine_ctas = e ? atoi(e) : -2;
     }
