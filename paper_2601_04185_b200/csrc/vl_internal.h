@@ -188,6 +188,8 @@ int launch_prep(const Work& wk, const Inputs& in, int q0, int nq, int list_pos, 
 // profiling stages (vl_profile_read order)
 enum { kStagePrep = 0, kStageSample, kStageP3P, kStageCompact, kStageScore, kStageScan, kStageActive,
        kStageFinal, kStageLift, kNumStages };
+// VISLOC_CARVEOUT A/B knob (vl_ransac.cu)
+int carveout_mode();
 // fine scoring items (256-hypothesis tiles x 1 split) for a round of nactive queries
 bool round_is_fine(const Work& wk, int nactive, int num_sms);
 // phase 0: whole round; 1: sample .. score; 2: scan + active (stepwise driver);

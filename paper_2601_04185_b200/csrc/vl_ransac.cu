@@ -933,8 +933,40 @@ int launch_split_apply_argmin(const Work& wk, int nactive, const long long* keys
 
 // One round, kernel by kernel; `hook(stage, begin)` lets the caller bracket
 // each launch with CUDA events (profiling) without touching the kernels.
+// A/B knob VISLOC_CARVEOUT=1: every round kernel prefers the maximum shared
+// memory carve-out, so consecutive (PDL-overlapped) kernels never need an
+// L1 / shared-memory reconfiguration between them.
+int carveout_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("VISLOC_CARVEOUT");
+    mode = e ? atoi(e) : 0;
+  }
+  return mode;
+}
+
+static void set_round_carveouts() {
+  static bool done[kMaxDevices] = {false};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (done[dev < kMaxDevices ? dev : 0]) return;
+  done[dev < kMaxDevices ? dev : 0] = true;
+  const int v = cudaSharedmemCarveoutMaxShared;
+  cudaFuncSetAttribute(k_sample<256>, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+  cudaFuncSetAttribute(k_sample<1024>, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+  cudaFuncSetAttribute(k_p3p_roots, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+  cudaFuncSetAttribute(k_p3p_polish, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+  cudaFuncSetAttribute(k_compact<256>, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+  cudaFuncSetAttribute(k_compact<512>, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+  cudaFuncSetAttribute(k_compact<1024>, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+  cudaFuncSetAttribute(k_scan, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+}
+
 int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int nactive, int num_sms,
                  cudaStream_t st, void (*hook)(void*, int, bool), void* hook_arg, int phase, int split) {
+  if (carveout_mode()) set_round_carveouts();
   auto H = [&](int stage, bool begin) {
     if (hook) hook(hook_arg, stage, begin);
   };

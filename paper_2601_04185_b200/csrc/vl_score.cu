@@ -78,6 +78,13 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive,
       cudaFuncSetAttribute(fkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFineSmem);
       cudaFuncSetAttribute(ckern_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoarseSmem);
       cudaFuncSetAttribute(ckern_prune, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoarseSmem);
+      if (carveout_mode()) {  // (see set_round_carveouts, vl_ransac.cu)
+        const int v = cudaSharedmemCarveoutMaxShared;
+        cudaFuncSetAttribute(fkern, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+        cudaFuncSetAttribute(ckern_full, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+        cudaFuncSetAttribute(ckern_prune, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+        cudaFuncSetAttribute(k_score_tail<kScoreThreads>, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+      }
       a = true;
     }
   }
