@@ -549,8 +549,9 @@ __global__ void __launch_bounds__(NT) k_compact(Work wk, int fine, int mode) {
   // score work items: coarse (768-hypothesis tiles x 4 splits) for big batches,
   // fine (256 x 1) when the batch is too small to fill the GPU otherwise;
   // tiles count from h_lo
+  // (fine == 2, "medium": a single query's round, 256-hypothesis tiles x 4-split items)
   const int tile_h = fine ? kScoreTileHypsFine : kScoreTileHyps;
-  const int spi = fine ? 1 : kScoreItemSplits;
+  const int spi = fine == 1 ? 1 : kScoreItemSplits;
   const int ntile = (hi - lo + tile_h - 1) / tile_h;
   // exact pruning (coarse rounds, a best pose known, non-negative weights):
   // score the first sA splits of every hypothesis, where sA / NS is the best
@@ -971,7 +972,14 @@ int launch_round(const Work& wk, const Inputs& in, const RansacParams& p, int na
     if (hook) hook(hook_arg, stage, begin);
   };
   int n = 0;
-  const int fine = round_is_fine(wk, nactive, num_sms) ? 1 : 0;
+  // scoring items: coarse (0), fine (1), or medium (2: 256-hypothesis tiles x
+  // 4 splits, a single query's round — fewer, longer items; A/B VISLOC_MEDIUM=1: C4 6.55 vs 5.58 ms, off)
+  static int medium = -1;
+  if (medium < 0) {
+    const char* e = getenv("VISLOC_MEDIUM");
+    medium = e ? atoi(e) : 0;
+  }
+  const int fine = round_is_fine(wk, nactive, num_sms) ? (medium && nactive == 1 ? 2 : 1) : 0;
   const bool pdl = use_pdl(nactive) && !hook;  // (profiling brackets every launch with events)
   // split round (pruning on, coarse items, phase 0): head then rest (k_compact)
   const bool two = split && phase == 0 && wk.prune && !fine && kHeadHyps > 0;

@@ -50,7 +50,7 @@ static int score_grid(const Work& wk, int persistent, int fine, int nactive) {
     const char* e = getenv("VISLOC_SCORE_GRID");
     mode = (e && e[0] == 'i') ? 1 : 0;
   }
-  const int tile = fine ? kScoreTileHypsFine : kScoreTileHyps, spi = fine ? 1 : kScoreItemSplits;
+  const int tile = fine ? kScoreTileHypsFine : kScoreTileHyps, spi = fine == 1 ? 1 : kScoreItemSplits;
   const int64_t ub = (int64_t)nactive * ((wk.HCAP + tile - 1) / tile) * ((wk.NSPLIT + spi - 1) / spi);
   if (!mode) return (int)std::max<int64_t>(1, std::min<int64_t>(persistent, ub));
   return (int)std::min<int64_t>(ub, 1 << 30);
@@ -66,6 +66,10 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive,
   constexpr size_t kFineSmem = score_smem_bytes<kScoreThreads, kScoreHypPerThreadFine, 1, kScoreChunk>();
   constexpr size_t kCoarseSmem = score_smem_bytes<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk>();
   auto fkern = k_score2_t<kScoreThreads, kScoreHypPerThreadFine, 1, kScoreChunk, kFineMinBlocks, 2, false>;
+  auto mkern = k_score2_t<kScoreThreads, kScoreHypPerThreadFine, kScoreItemSplits, kScoreChunk, kFineMinBlocks, 2,
+                          false>;
+  constexpr size_t kMediumSmem = score_smem_bytes<kScoreThreads, kScoreHypPerThreadFine, kScoreItemSplits,
+                                                  kScoreChunk>();
   auto ckern_full = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks,
                                VL_SCORE_UNR, false>;
   auto ckern_prune = k_score2_t<kScoreThreads, kScoreHypPerThread, kScoreItemSplits, kScoreChunk, kCoarseMinBlocks,
@@ -76,6 +80,7 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive,
     bool& a = attr_dev[dev < kMaxDevices ? dev : 0];
     if (!a) {
       cudaFuncSetAttribute(fkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFineSmem);
+      cudaFuncSetAttribute(mkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMediumSmem);
       cudaFuncSetAttribute(ckern_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoarseSmem);
       cudaFuncSetAttribute(ckern_prune, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoarseSmem);
       if (carveout_mode()) {  // (see set_round_carveouts, vl_ransac.cu)
@@ -96,7 +101,12 @@ int launch_score(const Work& wk, float tau2, int num_sms, int fine, int nactive,
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (fine) {
+  if (fine == 2) {
+    // medium items of a single query: one CTA per item (item upper bound)
+    cfg.gridDim = dim3(score_grid(wk, num_sms * kFineMinBlocks, 2, nactive), 1, 1);
+    cfg.dynamicSmemBytes = kMediumSmem;
+    cudaLaunchKernelEx(&cfg, mkern, wk, tau2);
+  } else if (fine) {
     static int occ = 0;
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fkern, kScoreThreads, kFineSmem) !=
                          cudaSuccess || occ < 1))
