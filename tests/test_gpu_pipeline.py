@@ -57,6 +57,8 @@ def _run(spec, pipe, tmp_path):
     dict(queries=[[3000, 0.5], [800, 0.8], [20_000, 0.6], [500, 0.9], [5000, 0.3]],
          iters=30_000, eta=1e-4, batch=1000),                                    # adaptive, ragged stops
     dict(queries=[[1500, 0.7], [1501, 0.85]], iters=2_500, eta=1e-300, batch=999),  # partial last batch
+    dict(queries=[[3, 0.0], [4, 0.0], [7, 0.3]], iters=1_000, eta=1e-4, batch=250),     # minimal sets
+    dict(queries=[[60_000, 0.8], [2_000, 0.5]], iters=7_777, eta=1e-2, batch=250),     # stride-6 subset, many rounds
 ])
 def test_pipelined_loop_identical(spec, tmp_path):
     import torch
