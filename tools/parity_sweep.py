@@ -4,15 +4,16 @@ The oracle runs on every host core (one process per problem); each problem
 draws its size, inlier ratio, noise, outlier weights, ground-truth pose,
 seed and RansacConfig (iterations, eta, batch size, tau, subset size) from
 one generator.  Prints the summary counts that DESIGN.md quotes.  GPU only:
-    python tools/parity_sweep.py [N] [seed] [batch|lowinlier]
+    python tools/parity_sweep.py [N] [seed] [batch|lowinlier|lowsingle]
 With "batch" every problem shares one RansacConfig (own seed, n <= 20001)
 and the GPU side is ONE ransac_pnp_batch call, so batches of more than 74
 problems run k_final one CTA per query (TMA-streamed full-set passes).
 "lowinlier" is the BASELINE C4 regime (posest.py:257-276, the LO-heavy
 ordered first-better scan): eps in {3, 5, 8} %, n in {2k, 5k, 10k}, 100k
 maximum samples, half the problems with the fixed-iteration eta = 1e-300 and
-half with the adaptive default eta = 1e-4, each half one ransac_pnp_batch.
-Every mode also compares the LO-call counts.
+half with the adaptive default eta = 1e-4, each half one ransac_pnp_batch;
+"lowsingle" runs the same problems one ransac_pnp call each (the pipelined
+single-query round loop).  Every mode also compares the LO-call counts.
 """
 import json
 import multiprocessing as mp
@@ -62,7 +63,7 @@ def main():
     mode = sys.argv[3] if len(sys.argv) > 3 else "single"
     batched = mode in ("batch", "lowinlier")
     probs = [draw(k, seed0) for k in range(N)]
-    if mode == "lowinlier":
+    if mode in ("lowinlier", "lowsingle"):
         for k, p in enumerate(probs):
             r = np.random.default_rng([seed0, k, 2])
             p["n"] = int(r.choice([2000, 5000, 10_000]))
