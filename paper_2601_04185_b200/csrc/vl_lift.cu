@@ -16,6 +16,7 @@
 // from IMLC records (12 B/cell, matchio.py:9-20) — in HBM or in mapped pinned
 // host memory.
 #include <climits>
+#include <cstdlib>
 #include <cuda_fp16.h>
 #include "vl_common.cuh"
 #include "vl_lift.h"
@@ -288,6 +289,14 @@ struct CellWalk {
       ++row;
     }
   }
+  // grids at least 32 cells wide wrap at most once per step: no loop
+  __device__ __forceinline__ void next_wide(int gw) {
+    cell += 32;
+    col += 32;
+    const bool wrap = col >= gw;
+    col -= wrap ? gw : 0;
+    row += wrap ? 1 : 0;
+  }
 };
 
 // KIND = kGateOnly: mode 1 (gate only, no depth)
@@ -436,8 +445,89 @@ __device__ __forceinline__ int count_run(const SegP& S, const DepP& D, T thr, in
   return cnt;
 }
 
+// Count of a warp's run from the block's staged IMLC records (f32), in
+// groups of kCountGroup cells: first every cell of the group is gated and
+// validated and its depth-tap index formed (shared memory and ALU only),
+// then the group's tap loads are issued back to back with no branch in
+// between (a cell that failed the gate reads tap 0 and is not counted), so a
+// lane has kCountGroup (db -> query) or 4 x kCountGroup (query -> db) loads
+// in flight instead of one dependent load per cell (count_run: ncu r02s,
+// long_scoreboard the top stall, 2.5 TB/s).  Same decisions as count_run.
+constexpr int kCountGroup = 4;
+
+__device__ __forceinline__ int content_flags_f(float c, float tx, float ty) {
+  int f = 0;
+  if (!(c >= 0.f && c <= 1.f)) f |= kFieldBadConf;  // false for NaN and +-inf: isfinite implied
+  if (c > 0.f && !(isfinite(tx) && isfinite(ty))) f |= kFieldBadTarget;
+  return f;
+}
+
+template <int DIR, int KIND>
+__device__ __forceinline__ int count_run_staged(const SegP& S, const DepP& D, float thr, int cw, int lane,
+                                                int& flags, const float* srec, int c0, const Dir0Tab tab) {
+  int cnt = 0;
+  CellWalk cwk(cw + lane, S.gw);
+  const bool wide = S.gw >= 32;
+#pragma unroll 1
+  for (int g = 0; g < kLiftPerThread; g += kCountGroup) {
+    if (cw + g * 32 >= S.cells) break;  // uniform across the warp
+    int idx[kCountGroup];
+    bool kp[kCountGroup];
+#pragma unroll
+    for (int j = 0; j < kCountGroup; ++j, wide ? cwk.next_wide(S.gw) : cwk.next(S.gw)) {
+      kp[j] = false;
+      idx[j] = 0;
+      if (cwk.cell < S.cells) {
+        const float* r = srec + 3 * (cwk.cell - c0);
+        const float c = r[2], tx = r[0], ty = r[1];
+        flags |= content_flags_f(c, tx, ty);
+        bool keep = gate<float>(c, thr);
+        if (KIND != kGateOnly) {
+          if (DIR == 0) {
+            if (tab.on) {
+              idx[j] = tab.iy[cwk.row - tab.row0] * D.w + tab.ix[cwk.col];
+            } else {
+              double sx, sy;
+              source_px(S, cwk.row, cwk.col, sx, sy);
+              idx[j] = direct_idx(D, sx, sy);
+            }
+          } else {
+            const Bilin b = bilin(D, dmul((double)tx, D.sxd), dmul((double)ty, D.syd));
+            keep = keep && b.inside;
+            idx[j] = b.i00;
+          }
+        }
+        kp[j] = keep;
+        if (!keep) idx[j] = 0;
+      }
+    }
+    if (KIND == kGateOnly) {
+#pragma unroll
+      for (int j = 0; j < kCountGroup; ++j) cnt += kp[j] ? 1 : 0;
+    } else if (DIR == 0) {
+      bool ok[kCountGroup];
+#pragma unroll
+      for (int j = 0; j < kCountGroup; ++j) ok[j] = tap_ok<KIND>(D, idx[j]);
+#pragma unroll
+      for (int j = 0; j < kCountGroup; ++j) cnt += (kp[j] && ok[j]) ? 1 : 0;
+    } else {
+      bool ok[kCountGroup][4];
+#pragma unroll
+      for (int j = 0; j < kCountGroup; ++j) {
+        ok[j][0] = tap_ok<KIND>(D, idx[j]);
+        ok[j][1] = tap_ok<KIND>(D, idx[j] + 1);
+        ok[j][2] = tap_ok<KIND>(D, idx[j] + D.w);
+        ok[j][3] = tap_ok<KIND>(D, idx[j] + D.w + 1);
+      }
+#pragma unroll
+      for (int j = 0; j < kCountGroup; ++j) cnt += (kp[j] && ok[j][0] && ok[j][1] && ok[j][2] && ok[j][3]) ? 1 : 0;
+    }
+  }
+  return cnt;
+}
+
 template <typename T>
-__global__ void __launch_bounds__(kLiftThreads, VL_LIFT_CMINB) k_lift_count(LiftArgs a, int mode) {
+__global__ void __launch_bounds__(kLiftThreads, VL_LIFT_CMINB) k_lift_count(LiftArgs a, int mode, int grouped) {
   const int64_t b = blockIdx.x;
   const int s = __ldg(a.seg_of_blk + b);  // host-built tile -> segment table (no per-thread binary search)
   const SegP S = load_seg(a.segs + s);
@@ -462,8 +552,21 @@ __global__ void __launch_bounds__(kLiftThreads, VL_LIFT_CMINB) k_lift_count(Lift
   Dir0Tab notab = tab;
   notab.on = false;
   int cnt = 0, flags = 0;
-  if (cw < S.cells) {
-#define VL_LIFT_COUNT(K)                                                                         \
+  if (cw < S.cells && srec && grouped) {
+    // staged IMLC records are f32 (T = float for them)
+#define VL_LIFT_COUNT2(K)                                                                                   \
+  cnt = S.direction == 0 ? count_run_staged<0, K>(S, D, (float)thr, cw, lane, flags, srec, c0, tab)         \
+                         : count_run_staged<1, K>(S, D, (float)thr, cw, lane, flags, srec, c0, notab);
+    switch (kind) {
+      case kDepthF32: VL_LIFT_COUNT2(kDepthF32) break;
+      case kDepthF16: VL_LIFT_COUNT2(kDepthF16) break;
+      case kDepthCode8: VL_LIFT_COUNT2(kDepthCode8) break;
+      case kDepthCode16: VL_LIFT_COUNT2(kDepthCode16) break;
+      default: cnt = count_run_staged<0, kGateOnly>(S, D, (float)thr, cw, lane, flags, srec, c0, notab); break;
+    }
+#undef VL_LIFT_COUNT2
+  } else if (cw < S.cells) {
+#define VL_LIFT_COUNT(K)                                                                       \
   cnt = S.direction == 0 ? count_run<T, 0, K>(S, D, thr, cw, lane, flags, srec, c0, tab)         \
                          : count_run<T, 1, K>(S, D, thr, cw, lane, flags, srec, c0, notab);
     switch (kind) {
@@ -719,8 +822,13 @@ __global__ void __launch_bounds__(kLiftThreads, VL_LIFT_WMINB) k_lift_write(Lift
 
 int launch_lift(const LiftArgs& a, int field_f64, int mode, cudaStream_t st) {
   if (a.nblk <= 0) return 0;
-  if (field_f64) k_lift_count<double><<<(unsigned)a.nblk, kLiftThreads, 0, st>>>(a, mode);
-  else k_lift_count<float><<<(unsigned)a.nblk, kLiftThreads, 0, st>>>(a, mode);
+  // VISLOC_LIFT_GROUPED=0: the per-cell count loop (A/B switch, read once)
+  static const int grouped = [] {
+    const char* e = getenv("VISLOC_LIFT_GROUPED");
+    return e ? atoi(e) : 1;
+  }();
+  if (field_f64) k_lift_count<double><<<(unsigned)a.nblk, kLiftThreads, 0, st>>>(a, mode, grouped);
+  else k_lift_count<float><<<(unsigned)a.nblk, kLiftThreads, 0, st>>>(a, mode, grouped);
   k_lift_scan<<<(unsigned)((a.nblk + kScanChunk - 1) / kScanChunk), kScanChunk, 0, st>>>(a);
   return 2;
 }

@@ -104,21 +104,23 @@ def test_lift_paths_vs_oracle(vl, gw, gh, kind):
     _check(vl.lift_arrays(job, e, dobj, THR), ref)  # planar f32 fields
 
 
-@pytest.mark.parametrize("gw,gh", [(117, 117), (600, 7), (3, 5)])
-def test_lift_imlc_aligned_and_unaligned_records(vl, gw, gh):
-    """IMLC records 16-B aligned (bulk-copy staging) and at a 4-B offset (per-cell loads)."""
+@pytest.mark.parametrize("gw,gh", [(117, 117), (600, 7), (20, 300), (3, 5)])
+@pytest.mark.parametrize("kind", ["u8", "f32", "f16", "u16"])
+def test_lift_imlc_aligned_and_unaligned_records(vl, gw, gh, kind):
+    """IMLC records 16-B aligned (bulk-copy staging: the grouped count loop)
+    and at a 4-B offset (per-cell loads), every depth kind."""
     import torch
     from paper_2601_04185_b200 import _lib
     from paper_2601_04185_b200.localizer import _depth_record, _call_lift, FieldPair, QueryJob
     from paper_2601_04185_b200.matchio import FieldArena, field_bytes
-    intr, pose, depth, valid, f1, f2 = _scene(gw, gh, "u8", seed=gw + gh)
+    intr, pose, depth, valid, f1, f2 = _scene(gw, gh, kind, seed=gw + gh)
 
     class Entry:
         pass
 
     e = Entry()
     e.id, e.pose, e.intrinsics = "db", pose, intr
-    dobj, vals, ok = _depth_obj(vl, "u8", depth, valid, intr)
+    dobj, vals, ok = _depth_obj(vl, kind, depth, valid, intr)
     ref = _oracle(intr, pose, vals, ok, f1, f2)
     fq = vl.CorrespondenceField("q", "db", f2[0], f2[1], 4.0, 4.0)
     fd = vl.CorrespondenceField("db", "q", f1[0], f1[1], 4.0, 4.0)
@@ -153,3 +155,47 @@ def test_lift_imlc_aligned_and_unaligned_records(vl, gw, gh):
     _call_lift(table, 2, deps, 1, False, THR, 0, px, X, w, ent, cap, offs, flags, [fd, fq])
     n = int(offs[-1])
     _check((px[:n], X[:n], w[:n]), ref)
+
+
+def test_lift_grouped_loops_equal_per_cell_loops(tmp_path):
+    """The grouped count loop over staged IMLC records (default) and the
+    per-cell loop (VISLOC_LIFT_GROUPED=0, read once per process) give the same
+    matches bit for bit on a C5-shaped lift (u8 and f16 depth, both
+    directions, 117 x 117 fields)."""
+    import os
+    import subprocess
+    import sys
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import sys, numpy as np\n"
+        f"sys.path[:0] = [{root!r}, {os.path.join(root, 'tests')!r}]\n"
+        "from synth_inputs import lifted_scene\n"
+        "import paper_2601_04185_b200.localizer as L\n"
+        "from paper_2601_04185_b200.matchio import FieldArena, field_bytes\n"
+        "from paper_2601_04185_b200.localizer import FieldPair\n"
+        "out = {}\n"
+        "for kind in ('u8', 'f16'):\n"
+        "    vmap, jobs, dc = lifted_scene(3, 2, 117, seed=5, depth_kind=kind, fields='f32')\n"
+        "    for qi, job in enumerate(jobs):\n"
+        "        for e in vmap.entries:\n"
+        "            fp = job.fields[e.id]\n"
+        "            ar = FieldArena([field_bytes(fp.query_to_db), field_bytes(fp.db_to_query)])\n"
+        "            job.fields[e.id] = FieldPair(ar[0], ar[1])\n"
+        "            d = e.qdepth if kind == 'u8' else dc[e.id]\n"
+        "            px, X, w = (a.cpu().numpy() if hasattr(a, 'cpu') else np.asarray(a) for a in L.lift_arrays(job, e, d, 0.05))\n"
+        "            for nm, a in (('px', px), ('X', X), ('w', w)):\n"
+        "                out[f'{kind}_{qi}_{e.id}_{nm}'] = a\n"
+        "np.savez(sys.argv[1], **out)\n")
+    res = {}
+    for v in ("0", "1"):
+        f = tmp_path / f"lift_{v}.npz"
+        env = dict(os.environ, VISLOC_LIFT_GROUPED=v)
+        subprocess.run([sys.executable, "-c", script, str(f)], check=True, env=env, cwd=root)
+        res[v] = np.load(f)
+    assert len(res["0"].files) == len(res["1"].files) > 0
+    for k in res["0"].files:
+        assert np.array_equal(res["0"][k], res["1"][k]), k
+    assert sum(res["0"][k].shape[0] for k in res["0"].files if k.endswith("_w")) > 10000
