@@ -322,8 +322,8 @@ struct Dir0Tab {
 // All threads call it; the caller's next __syncthreads publishes the tables.
 // Returns false (tables unused) when the segment does not qualify.
 __device__ __forceinline__ bool fill_dir0_tab(const SegP& S, const DepP& D, int c0, bool with_n, int* ix, int* iy,
-                                              double* xn, double* yn, Dir0Tab& tab, int span = kLiftBlockCells) {
-  const int row0 = c0 / S.gw, row1 = (min(S.cells, c0 + span) - 1) / S.gw;
+                                              double* xn, double* yn, Dir0Tab& tab) {
+  const int row0 = c0 / S.gw, row1 = (min(S.cells, c0 + kLiftBlockCells) - 1) / S.gw;
   tab.on = false;
   if (S.direction != 0 || S.gw > kTabCols || row1 - row0 + 1 > kTabRows) return false;
   for (int col = threadIdx.x; col < S.gw; col += blockDim.x) {
@@ -366,26 +366,18 @@ __device__ __forceinline__ void lift_point_n(const double* R, const double* t, d
 // block barrier on both paths.
 __device__ __forceinline__ unsigned lift_smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-// `uses`: how many bulk copies this CTA has already completed on `bar`
-// (block-uniform; the barrier is initialised on the first and phase `uses`
-// is waited on — a CTA counting several blocks reuses it); incremented when
-// the copy path is taken.
-__device__ __forceinline__ const float* stage_records(const SegP& S, int c0, float* srec, uint64_t* bar,
-                                                      int* uses = nullptr) {
+__device__ __forceinline__ const float* stage_records(const SegP& S, int c0, float* srec, uint64_t* bar) {
   if (S.layout != kLayoutImlc || (reinterpret_cast<uintptr_t>(S.targets) & 15) || c0 >= S.cells) {
     __syncthreads();  // block-uniform: callers rely on this barrier either way
     return nullptr;
   }
-  const int phase = uses ? (*uses)++ : 0;
   const int ncell = min(kLiftBlockCells, S.cells - c0);
   const float* src = (const float*)S.targets + 3 * (int64_t)c0;
   const unsigned bytes = (unsigned)ncell * 12u, bulk = bytes & ~15u;
   const unsigned b = lift_smem_u32(bar);
   if (threadIdx.x == 0) {
-    if (phase == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bulk) : "memory");
     if (bulk)
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -396,8 +388,8 @@ __device__ __forceinline__ const float* stage_records(const SegP& S, int c0, flo
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "LIFT_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra LIFT_WAIT_%=;\n}" ::"r"(b), "r"(phase & 1)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra LIFT_WAIT_%=;\n}" ::"r"(b)
       : "memory");
   return srec;
 }
@@ -534,100 +526,76 @@ __device__ __forceinline__ int count_run_staged(const SegP& S, const DepP& D, fl
   return cnt;
 }
 
-// A CTA counts `nb` consecutive 2048-cell blocks (nb = kCountBlocks with the
-// grouped loop, else 1): the segment / depth parameters and the db->query
-// tables are loaded once for the CTA's blocks of one segment (tables over
-// their joint row span) and the records bulk copy reuses one mbarrier, so
-// the per-warp setup (~210 of ~930 warp instructions per block, ncu r02z)
-// is paid once per nb blocks.  Counts, warp counts and flags per block are
-// the one-block kernel's.
-constexpr int kCountBlocks = 2;
-
-template <typename T, int NB, int MINB>
-__global__ void __launch_bounds__(kLiftThreads, MINB) k_lift_count(LiftArgs a, int mode, int grouped) {
+template <typename T>
+__global__ void __launch_bounds__(kLiftThreads, VL_LIFT_CMINB) k_lift_count(LiftArgs a, int mode, int grouped) {
+  const int64_t b = blockIdx.x;
+  const int s = __ldg(a.seg_of_blk + b);  // host-built tile -> segment table (no per-thread binary search)
+  const SegP S = load_seg(a.segs + s);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c0 = (int)(b - a.seg_blk0[s]) * kLiftBlockCells;
+  const int cw = c0 + wid * kLiftWarpCells;
   const T thr = (T)a.threshold;
   __shared__ __align__(16) float srec_buf[3 * kLiftBlockCells];
   __shared__ __align__(8) uint64_t sbar;
   __shared__ int s_ix[kTabCols], s_iy[kTabRows];
-  __shared__ int wsum[kLiftWarps];
-  __shared__ int wflag[kLiftWarps];
-  constexpr int nb = NB;
-  const int64_t bfirst = (int64_t)blockIdx.x * nb;
-  int s = -1, uses = 0, kind = kGateOnly;
-  SegP S;
   DepP D{};
+  int kind = kGateOnly;
   Dir0Tab tab;
   tab.on = false;
-  for (int k = 0; k < nb; ++k) {
-    const int64_t b = bfirst + k;
-    if (b >= a.nblk) break;  // block-uniform
-    const int sb = __ldg(a.seg_of_blk + b);  // host-built tile -> segment table (no per-thread binary search)
-    if (k > 0) __syncthreads();  // the previous block is done with srec, the tables and wsum
-    const int c0 = (int)(b - a.seg_blk0[sb]) * kLiftBlockCells;
-    if (sb != s) {
-      s = sb;
-      S = load_seg(a.segs + s);
-      tab.on = false;
-      if (mode == 0) {
-        const LiftDepth* gd = a.depths + S.depth;
-        D = load_dep(gd);
-        kind = __ldg(&gd->kind);
-        // the tables cover this CTA's remaining blocks of the segment
-        int span = kLiftBlockCells;
-        for (int j = k + 1; j < nb && bfirst + j < a.nblk && __ldg(a.seg_of_blk + bfirst + j) == s; ++j)
-          span += kLiftBlockCells;
-        fill_dir0_tab(S, D, c0, false, s_ix, s_iy, nullptr, nullptr, tab, span);
-      }
-    }
-    const int cw = c0 + wid * kLiftWarpCells;
-    const float* srec = stage_records(S, c0, srec_buf, &sbar, &uses);  // its barrier also publishes the tables
-    Dir0Tab notab = tab;
-    notab.on = false;
-    int cnt = 0, flags = 0;
-    if (cw < S.cells && srec && grouped) {
-      // staged IMLC records are f32 (T = float for them)
+  if (mode == 0) {
+    const LiftDepth* gd = a.depths + S.depth;
+    D = load_dep(gd);
+    kind = __ldg(&gd->kind);
+    fill_dir0_tab(S, D, c0, false, s_ix, s_iy, nullptr, nullptr, tab);
+  }
+  const float* srec = stage_records(S, c0, srec_buf, &sbar);  // its barrier also publishes the tables
+  Dir0Tab notab = tab;
+  notab.on = false;
+  int cnt = 0, flags = 0;
+  if (cw < S.cells && srec && grouped) {
+    // staged IMLC records are f32 (T = float for them)
 #define VL_LIFT_COUNT2(K)                                                                                   \
   cnt = S.direction == 0 ? count_run_staged<0, K>(S, D, (float)thr, cw, lane, flags, srec, c0, tab)         \
                          : count_run_staged<1, K>(S, D, (float)thr, cw, lane, flags, srec, c0, notab);
-      switch (kind) {
-        case kDepthF32: VL_LIFT_COUNT2(kDepthF32) break;
-        case kDepthF16: VL_LIFT_COUNT2(kDepthF16) break;
-        case kDepthCode8: VL_LIFT_COUNT2(kDepthCode8) break;
-        case kDepthCode16: VL_LIFT_COUNT2(kDepthCode16) break;
-        default: cnt = count_run_staged<0, kGateOnly>(S, D, (float)thr, cw, lane, flags, srec, c0, notab); break;
-      }
+    switch (kind) {
+      case kDepthF32: VL_LIFT_COUNT2(kDepthF32) break;
+      case kDepthF16: VL_LIFT_COUNT2(kDepthF16) break;
+      case kDepthCode8: VL_LIFT_COUNT2(kDepthCode8) break;
+      case kDepthCode16: VL_LIFT_COUNT2(kDepthCode16) break;
+      default: cnt = count_run_staged<0, kGateOnly>(S, D, (float)thr, cw, lane, flags, srec, c0, notab); break;
+    }
 #undef VL_LIFT_COUNT2
-    } else if (cw < S.cells) {
+  } else if (cw < S.cells) {
 #define VL_LIFT_COUNT(K)                                                                       \
   cnt = S.direction == 0 ? count_run<T, 0, K>(S, D, thr, cw, lane, flags, srec, c0, tab)         \
                          : count_run<T, 1, K>(S, D, thr, cw, lane, flags, srec, c0, notab);
-      switch (kind) {
-        case kDepthF32: VL_LIFT_COUNT(kDepthF32) break;
-        case kDepthF16: VL_LIFT_COUNT(kDepthF16) break;
-        case kDepthCode8: VL_LIFT_COUNT(kDepthCode8) break;
-        case kDepthCode16: VL_LIFT_COUNT(kDepthCode16) break;
-        default: cnt = count_run<T, 0, kGateOnly>(S, D, thr, cw, lane, flags, srec, c0, notab); break;
-      }
+    switch (kind) {
+      case kDepthF32: VL_LIFT_COUNT(kDepthF32) break;
+      case kDepthF16: VL_LIFT_COUNT(kDepthF16) break;
+      case kDepthCode8: VL_LIFT_COUNT(kDepthCode8) break;
+      case kDepthCode16: VL_LIFT_COUNT(kDepthCode16) break;
+      default: cnt = count_run<T, 0, kGateOnly>(S, D, thr, cw, lane, flags, srec, c0, notab); break;
+    }
 #undef VL_LIFT_COUNT
+  }
+  __shared__ int wsum[kLiftWarps];
+  __shared__ int wflag[kLiftWarps];
+  cnt = warp_sum(cnt);
+  flags = __reduce_or_sync(0xffffffffu, (unsigned)flags);
+  if (lane == 0) {
+    wsum[wid] = cnt;
+    wflag[wid] = flags;
+    a.warp_count[b * kLiftWarps + wid] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0, f = 0;
+    for (int w = 0; w < kLiftWarps; ++w) {
+      t += wsum[w];
+      f |= wflag[w];
     }
-    cnt = warp_sum(cnt);
-    flags = __reduce_or_sync(0xffffffffu, (unsigned)flags);
-    if (lane == 0) {
-      wsum[wid] = cnt;
-      wflag[wid] = flags;
-      a.warp_count[b * kLiftWarps + wid] = cnt;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0, f = 0;
-      for (int w = 0; w < kLiftWarps; ++w) {
-        t += wsum[w];
-        f |= wflag[w];
-      }
-      a.blk_count[b] = t;
-      if (f && a.seg_flags) atomicOr(a.seg_flags + s, f);
-    }
+    a.blk_count[b] = t;
+    if (f && a.seg_flags) atomicOr(a.seg_flags + s, f);
   }
 }
 
@@ -859,18 +827,8 @@ int launch_lift(const LiftArgs& a, int field_f64, int mode, cudaStream_t st) {
     const char* e = getenv("VISLOC_LIFT_GROUPED");
     return e ? atoi(e) : 1;
   }();
-  // bit 1: kCountBlocks blocks per CTA (grouped only); bits 2 / 3: 5 / 4 resident CTAs
-  const int nb = (grouped & 1) && (grouped & 2) ? kCountBlocks : 1;
-  const unsigned grid = (unsigned)((a.nblk + nb - 1) / nb);
-  const int g = grouped & 1;
-#define VL_COUNT_LAUNCH(NB, M)                                                                   \
-  (field_f64 ? k_lift_count<double, NB, M><<<grid, kLiftThreads, 0, st>>>(a, mode, g)            \
-             : k_lift_count<float, NB, M><<<grid, kLiftThreads, 0, st>>>(a, mode, g))
-  if (nb == 1) VL_COUNT_LAUNCH(1, VL_LIFT_CMINB);
-  else if (grouped & 4) VL_COUNT_LAUNCH(kCountBlocks, 5);
-  else if (grouped & 8) VL_COUNT_LAUNCH(kCountBlocks, 4);
-  else VL_COUNT_LAUNCH(kCountBlocks, VL_LIFT_CMINB);
-#undef VL_COUNT_LAUNCH
+  if (field_f64) k_lift_count<double><<<(unsigned)a.nblk, kLiftThreads, 0, st>>>(a, mode, grouped);
+  else k_lift_count<float><<<(unsigned)a.nblk, kLiftThreads, 0, st>>>(a, mode, grouped);
   k_lift_scan<<<(unsigned)((a.nblk + kScanChunk - 1) / kScanChunk), kScanChunk, 0, st>>>(a);
   return 2;
 }
